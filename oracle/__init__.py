@@ -1,0 +1,142 @@
+"""CPU oracle for exact triangle counting -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and the ``cpu_baseline`` /
+``--impl reference`` legs of ``bench.py`` may import this package.  The
+product package ``paper_1804_06926_b200`` never imports it and shares no
+code with it.
+
+The arithmetic lives in ``oracle/tc_oracle.c`` (plain C, OpenMP over source
+vertices only); this module is argument marshalling over ctypes plus the
+build step.  Every function cites the PAPER.md passage it follows in the C
+file's comments.
+
+Parity status: every function here is pinned by ``tests/test_oracle_pins.py``
+(paper worked example, closed forms, brute force, trace(A^3)/6, Kronecker
+products); none is "parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "tc_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+_u64p = ctypes.POINTER(ctypes.c_uint64)
+_u32p = ctypes.POINTER(ctypes.c_uint32)
+
+
+def build(force: bool = False) -> str:
+    """Compile tc_oracle.c into liboracle.so (gcc, -O2, OpenMP)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-std=c11", "-Wall",
+               "-o", _LIB, _SRC]
+        subprocess.run(cmd, check=True)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB)
+        lib.oracle_clean.restype = ctypes.c_int64
+        lib.oracle_clean.argtypes = [ctypes.c_uint64, _u64p, _u32p, _u64p, _u32p]
+        lib.oracle_orient.restype = ctypes.c_int64
+        lib.oracle_orient.argtypes = [ctypes.c_uint64, _u64p, _u32p, _u64p, _u32p]
+        lib.oracle_forward.restype = ctypes.c_uint64
+        lib.oracle_forward.argtypes = [ctypes.c_uint64, _u64p, _u32p, ctypes.c_void_p]
+        lib.oracle_count.restype = ctypes.c_int
+        lib.oracle_count.argtypes = [ctypes.c_uint64, _u64p, _u32p, _u64p,
+                                     ctypes.c_void_p, ctypes.c_void_p]
+        lib.oracle_vertex_triangles.restype = ctypes.c_uint64
+        lib.oracle_vertex_triangles.argtypes = [ctypes.c_uint64, _u64p, _u32p, ctypes.c_uint64]
+        lib.oracle_num_threads.restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+def _csr(rowptr, col):
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.uint64)
+    col = np.ascontiguousarray(col, dtype=np.uint32)
+    if col.size == 0:
+        col = np.zeros(1, dtype=np.uint32)          # never read; keeps a valid pointer
+    return rowptr, col
+
+
+def _p64(a):
+    return a.ctypes.data_as(_u64p)
+
+
+def _p32(a):
+    return a.ctypes.data_as(_u32p)
+
+
+def clean(n: int, rowptr, col):
+    """Step 1: simple undirected graph as symmetric sorted CSR."""
+    lib = _load()
+    rowptr, col = _csr(rowptr, col)
+    out_row = np.zeros(n + 1, dtype=np.uint64)
+    out_col = np.zeros(max(1, 2 * int(rowptr[n])), dtype=np.uint32)
+    r = lib.oracle_clean(n, _p64(rowptr), _p32(col), _p64(out_row), _p32(out_col))
+    if r < 0:
+        raise ValueError(f"oracle_clean failed ({r}): arc id >= n or out of memory")
+    return out_row, out_col[:r].copy()
+
+
+def orient(n: int, clean_rowptr, clean_col):
+    """Step 2 (Alg. 2 Form_Filtered_Edge_List): N+ lists by (deg, id)."""
+    lib = _load()
+    clean_rowptr, clean_col = _csr(clean_rowptr, clean_col)
+    off = np.zeros(n + 1, dtype=np.uint64)
+    colp = np.zeros(max(1, int(clean_rowptr[n]) // 2 + 1), dtype=np.uint32)
+    m = lib.oracle_orient(n, _p64(clean_rowptr), _p32(clean_col), _p64(off), _p32(colp))
+    return off, colp[:m].copy()
+
+
+def forward(n: int, off_plus, col_plus, per_vertex: bool = False):
+    """Steps 3+4 on an oriented CSR; returns T or (T, t)."""
+    lib = _load()
+    off_plus, col_plus = _csr(off_plus, col_plus)
+    pv = np.zeros(max(n, 1), dtype=np.uint64) if per_vertex else None
+    T = lib.oracle_forward(n, _p64(off_plus), _p32(col_plus),
+                           pv.ctypes.data if pv is not None else None)
+    return (int(T), pv[:n]) if per_vertex else int(T)
+
+
+def count(n: int, rowptr, col, per_vertex: bool = False, with_stats: bool = False):
+    """Whole oracle: T (and t(v), stats) of the simple graph the arcs define."""
+    lib = _load()
+    rowptr, col = _csr(rowptr, col)
+    if int(rowptr[0]) != 0 or len(rowptr) != n + 1:
+        raise ValueError("rowptr must have n+1 entries starting at 0")
+    total = np.zeros(1, dtype=np.uint64)
+    pv = np.zeros(max(n, 1), dtype=np.uint64) if per_vertex else None
+    st = np.zeros(8, dtype=np.uint64)
+    r = lib.oracle_count(n, _p64(rowptr), _p32(col), _p64(total),
+                         pv.ctypes.data if pv is not None else None, st.ctypes.data)
+    if r != 0:
+        raise ValueError(f"oracle_count failed ({r})")
+    out = [int(total[0])]
+    if per_vertex:
+        out.append(pv[:n])
+    if with_stats:
+        out.append(dict(m=int(st[0]), W=int(st[1]), SSD=int(st[2]), sum_dminus_dplus=int(st[3]),
+                        max_dplus=int(st[4]), max_deg=int(st[5]), wedges=int(st[6])))
+    return out[0] if len(out) == 1 else tuple(out)
+
+
+def vertex_triangles(n: int, clean_rowptr, clean_col, v: int) -> int:
+    """t(v) by definition (edges among N(v)) on a clean symmetric sorted CSR."""
+    lib = _load()
+    clean_rowptr, clean_col = _csr(clean_rowptr, clean_col)
+    return int(lib.oracle_vertex_triangles(n, _p64(clean_rowptr), _p32(clean_col), v))
+
+
+def num_threads() -> int:
+    return int(_load().oracle_num_threads())

@@ -1,0 +1,255 @@
+/*
+ * oracle/tc_oracle.c -- CPU oracle for exact triangle counting.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * The product path (paper_1804_06926_b200/) never imports, links or calls it,
+ * and this file shares no source, header, table or helper with the CUDA path.
+ *
+ * Plain, slow, obviously-correct C.  Integer arithmetic only (there is no
+ * floating point anywhere on the path: PAPER.md never rounds).
+ * Citations: "P:n" = /root/reference/PAPER.md line n.
+ *
+ * What it computes (the plain definition):
+ *   T(G) = |{ {a,b,c} : {a,b},{b,c},{a,c} in E }|,
+ *   E    = { {u,v} : u != v and (u,v) or (v,u) is an input arc },
+ *   t(v) = number of those triangles that contain v.
+ *
+ * How (the paper's own CPU baseline, Schank-Wagner "forward", P:577-579,
+ * P:301-306 §3.2; Alg. 2 P:333-366 in its step order):
+ *   1. clean      -- arcs read as undirected, self-loops dropped, duplicates
+ *                    collapsed (Table 1 caption P:604-606; DESIGN reading R1).
+ *   2. orient     -- "Form_Filtered_Edge_List" (Alg. 2): keep each
+ *                    undirected edge once, from lower to higher (degree, id)
+ *                    rank (DESIGN reading R2: direction per north_star,
+ *                    tie-break by smaller id exactly as P:521-522).
+ *   3. intersect  -- "Compute_Intersection": for every kept edge
+ *                    (u,v) the matches w of N+(u) and N+(v) ("Let the
+ *                    intersections between the neighbor lists of u and v be
+ *                    (w_1..w_N) ... the number of triangles formed with e is N",
+ *                    P:315-321), by a plain two-pointer merge of sorted lists.
+ *   4. reduce     -- "Count = Reduce(IntersectList)", uint64.
+ *
+ * Per-vertex counts: each match w of edge (u,v) is the triangle {u,v,w}; it
+ * adds one to t(u), t(v) and t(w) (clustering-coefficient use).
+ *
+ * oracle_vertex_triangles() is the per-vertex DEFINITION written out
+ * (t(v) = number of edges among N(v)) for sampled checks at full size.
+ *
+ * Error behaviour: functions return a negative int on bad input (an arc id
+ * >= n) or allocation failure; nothing is ever partially trusted.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+static int cmp_u64(const void *a, const void *b) {
+    uint64_t x = *(const uint64_t *)a, y = *(const uint64_t *)b;
+    return (x > y) - (x < y);
+}
+
+static int cmp_u32(const void *a, const void *b) {
+    uint32_t x = *(const uint32_t *)a, y = *(const uint32_t *)b;
+    return (x > y) - (x < y);
+}
+
+/*
+ * Step 1: clean.  Input: any CSR of n vertices (arcs u -> col[k] for
+ * rowptr[u] <= k < rowptr[u+1]).  Output: the simple undirected graph as a
+ * symmetric CSR with each row sorted ascending: out_rowptr[n+1],
+ * out_col[capacity 2*rowptr[n]].  Returns the number of stored arcs (= 2m),
+ * or -1 if an arc points outside [0,n), -2 on allocation failure.
+ */
+int64_t oracle_clean(uint64_t n, const uint64_t *rowptr, const uint32_t *col,
+                     uint64_t *out_rowptr, uint32_t *out_col) {
+    uint64_t M = rowptr[n];
+    uint64_t *pairs = (uint64_t *)malloc((M ? M : 1) * sizeof(uint64_t));
+    if (!pairs) return -2;
+    uint64_t k = 0;
+    for (uint64_t u = 0; u < n; u++) {
+        for (uint64_t e = rowptr[u]; e < rowptr[u + 1]; e++) {
+            uint64_t v = col[e];
+            if (v >= n) { free(pairs); return -1; }
+            if (v == u) continue;                     /* self-loop dropped */
+            uint64_t a = u < v ? u : v, b = u < v ? v : u;
+            pairs[k++] = (a << 32) | b;               /* undirected edge {a,b} */
+        }
+    }
+    qsort(pairs, k, sizeof(uint64_t), cmp_u64);
+    uint64_t m = 0;                                   /* duplicates collapsed */
+    for (uint64_t i = 0; i < k; i++)
+        if (m == 0 || pairs[i] != pairs[m - 1]) pairs[m++] = pairs[i];
+
+    uint64_t *deg = (uint64_t *)calloc(n + 1, sizeof(uint64_t));
+    if (!deg) { free(pairs); return -2; }
+    for (uint64_t i = 0; i < m; i++) {
+        deg[pairs[i] >> 32]++;
+        deg[pairs[i] & 0xffffffffu]++;
+    }
+    out_rowptr[0] = 0;
+    for (uint64_t v = 0; v < n; v++) out_rowptr[v + 1] = out_rowptr[v] + deg[v];
+    for (uint64_t v = 0; v < n; v++) deg[v] = out_rowptr[v];   /* reuse as cursor */
+    for (uint64_t i = 0; i < m; i++) {
+        uint32_t a = (uint32_t)(pairs[i] >> 32), b = (uint32_t)(pairs[i] & 0xffffffffu);
+        out_col[deg[a]++] = b;
+        out_col[deg[b]++] = a;
+    }
+    for (uint64_t v = 0; v < n; v++)
+        qsort(out_col + out_rowptr[v], out_rowptr[v + 1] - out_rowptr[v],
+              sizeof(uint32_t), cmp_u32);
+    free(deg);
+    free(pairs);
+    return (int64_t)(2 * m);
+}
+
+/* rank(u) < rank(v) with rank = (d, id) compared lexicographically. */
+static int rank_less(const uint64_t *rowptr, uint64_t u, uint64_t v) {
+    uint64_t du = rowptr[u + 1] - rowptr[u], dv = rowptr[v + 1] - rowptr[v];
+    return du < dv || (du == dv && u < v);
+}
+
+/*
+ * Step 2: orient ("Form_Filtered_Edge_List", Alg. 2; filter rule
+ * P:520-523).  Input: a clean symmetric CSR with sorted rows (oracle_clean's
+ * output).  Output: N+(u) = { v in N(u) : rank(u) < rank(v) } in
+ * off_plus[n+1] / col_plus[capacity rowptr[n]/2], each row ascending because
+ * N(u) is.  Returns m (the number of kept edges).
+ */
+int64_t oracle_orient(uint64_t n, const uint64_t *rowptr, const uint32_t *col,
+                      uint64_t *off_plus, uint32_t *col_plus) {
+    uint64_t k = 0;
+    off_plus[0] = 0;
+    for (uint64_t u = 0; u < n; u++) {
+        for (uint64_t e = rowptr[u]; e < rowptr[u + 1]; e++)
+            if (rank_less(rowptr, u, col[e])) col_plus[k++] = col[e];
+        off_plus[u + 1] = k;
+    }
+    return (int64_t)k;
+}
+
+/*
+ * Steps 3+4: for each kept edge (u,v), merge N+(u) and N+(v); every common
+ * element w is one triangle {u,v,w}; Count = sum.
+ * per_vertex (nullable, n entries, zeroed here) receives t(v).
+ */
+uint64_t oracle_forward(uint64_t n, const uint64_t *off_plus, const uint32_t *col_plus,
+                        uint64_t *per_vertex) {
+    if (per_vertex) memset(per_vertex, 0, n * sizeof(uint64_t));
+    uint64_t T = 0;
+    int64_t nn = (int64_t)n;
+#pragma omp parallel for schedule(dynamic, 64) reduction(+ : T)
+    for (int64_t uu = 0; uu < nn; uu++) {
+        uint64_t u = (uint64_t)uu;
+        for (uint64_t e = off_plus[u]; e < off_plus[u + 1]; e++) {
+            uint64_t v = col_plus[e];
+            uint64_t i = off_plus[u], iend = off_plus[u + 1];
+            uint64_t j = off_plus[v], jend = off_plus[v + 1];
+            while (i < iend && j < jend) {
+                uint32_t a = col_plus[i], b = col_plus[j];
+                if (a < b) {
+                    i++;
+                } else if (a > b) {
+                    j++;
+                } else {                               /* w = a is in both lists */
+                    T++;
+                    if (per_vertex) {
+#pragma omp atomic
+                        per_vertex[u]++;
+#pragma omp atomic
+                        per_vertex[v]++;
+#pragma omp atomic
+                        per_vertex[a]++;
+                    }
+                    i++;
+                    j++;
+                }
+            }
+        }
+    }
+    return T;
+}
+
+/*
+ * Whole oracle: clean -> orient -> intersect -> reduce.
+ * stats (nullable, 8 entries): [0] m (undirected edges), [1] W =
+ * sum over kept edges of d+(u)+d+(v) (merge work), [2] SSD = sum d(v)^2
+ * (Fig. ssd), [3] sum_v d-(v)*d+(v), [4] max d+, [5] max d,
+ * [6] wedges = sum C(d(v),2), [7] unused (0).
+ * Returns 0 and writes *total, or a negative error from oracle_clean.
+ */
+int oracle_count(uint64_t n, const uint64_t *rowptr, const uint32_t *col,
+                 uint64_t *total, uint64_t *per_vertex, uint64_t *stats) {
+    uint64_t M = rowptr[n];
+    uint64_t *crow = (uint64_t *)malloc((n + 1) * sizeof(uint64_t));
+    uint32_t *ccol = (uint32_t *)malloc((M ? 2 * M : 1) * sizeof(uint32_t));
+    uint64_t *orow = (uint64_t *)malloc((n + 1) * sizeof(uint64_t));
+    uint32_t *ocol = (uint32_t *)malloc((M ? M : 1) * sizeof(uint32_t));
+    if (!crow || !ccol || !orow || !ocol) {
+        free(crow); free(ccol); free(orow); free(ocol);
+        return -2;
+    }
+    int64_t arcs = oracle_clean(n, rowptr, col, crow, ccol);
+    if (arcs < 0) {
+        free(crow); free(ccol); free(orow); free(ocol);
+        return (int)arcs;
+    }
+    int64_t m = oracle_orient(n, crow, ccol, orow, ocol);
+    *total = oracle_forward(n, orow, ocol, per_vertex);
+    if (stats) {
+        memset(stats, 0, 8 * sizeof(uint64_t));
+        stats[0] = (uint64_t)m;
+        for (uint64_t u = 0; u < n; u++) {
+            uint64_t dp = orow[u + 1] - orow[u];
+            uint64_t d = crow[u + 1] - crow[u];
+            for (uint64_t e = orow[u]; e < orow[u + 1]; e++) {
+                uint64_t v = ocol[e];
+                stats[1] += dp + (orow[v + 1] - orow[v]);
+            }
+            stats[2] += d * d;
+            stats[3] += (d - dp) * dp;
+            if (dp > stats[4]) stats[4] = dp;
+            if (d > stats[5]) stats[5] = d;
+            stats[6] += d * (d ? d - 1 : 0) / 2;
+        }
+    }
+    free(crow); free(ccol); free(orow); free(ocol);
+    return 0;
+}
+
+static int contains(const uint32_t *list, uint64_t len, uint32_t x) {
+    return bsearch(&x, list, len, sizeof(uint32_t), cmp_u32) != NULL;
+}
+
+/*
+ * Per-vertex definition for sampled checks: t(v) = number of edges {x,y}
+ * with x,y in N(v), i.e. (1/2) sum_{x in N(v)} |N(v) cap N(x)|.  Input is a
+ * clean symmetric CSR with sorted rows.  Each |N(v) cap N(x)| scans the
+ * shorter list and looks each element up in the longer one (bsearch).
+ */
+uint64_t oracle_vertex_triangles(uint64_t n, const uint64_t *rowptr, const uint32_t *col,
+                                 uint64_t v) {
+    (void)n;
+    const uint32_t *Nv = col + rowptr[v];
+    uint64_t dv = rowptr[v + 1] - rowptr[v];
+    uint64_t twice = 0;
+    for (uint64_t i = 0; i < dv; i++) {
+        uint32_t x = Nv[i];
+        const uint32_t *Nx = col + rowptr[x];
+        uint64_t dx = rowptr[x + 1] - rowptr[x];
+        const uint32_t *s = dx < dv ? Nx : Nv, *l = dx < dv ? Nv : Nx;
+        uint64_t ls = dx < dv ? dx : dv, ll = dx < dv ? dv : dx;
+        for (uint64_t k = 0; k < ls; k++) twice += (uint64_t)contains(l, ll, s[k]);
+    }
+    return twice / 2;
+}
+
+int oracle_num_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
