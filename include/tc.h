@@ -1,0 +1,174 @@
+/*
+ * tc.h -- C ABI of libtc_b200.so, the B200 (sm_100a) exact triangle counter.
+ *
+ * The operation (§3.2, Alg. 2 "TC using edge-based set
+ * intersection"; §4.2): for the simple undirected graph G that the
+ * input arcs define, return
+ *
+ *     T(G) = |{ {a,b,c} : {a,b}, {b,c}, {a,c} are edges of G }|
+ *
+ * computed as in Alg. 2: orient every edge from lower to higher (degree, id)
+ * rank and compact (Form_Filtered_Edge_List, filter rule P:520-523,
+ * induced subgraph P:523-525), intersect N+(u) and N+(v) for every kept edge
+ * (Compute_Intersection; "the number of triangles formed with e is
+ * N") and reduce (Count = Reduce(IntersectList)).  Optional
+ * per-vertex counts t(v) (number of triangles through v) serve clustering
+ * coefficients and transitivity.
+ *
+ * Every step runs in hand-written sm_100a kernels; there is no CPU fallback.
+ * All results are exact integers (uint64): the path has no floating point.
+ *
+ * INPUT LAYOUT (CSR, "Graph" of SPEC.md S:31-41):
+ *   n            number of vertices, ids in [0, n), n < 2^32.
+ *   m            number of arcs = row_offsets[n].  Each arc is read as an
+ *                undirected edge.
+ *   row_offsets  uint64[n+1], row_offsets[0] = 0, non-decreasing,
+ *                row_offsets[n] = m.
+ *   col_indices  uint32[m]; arc k in row u is u -> col_indices[k].
+ *   Unless TC_CLEAN is given, self-loops are dropped, duplicate and
+ *   antiparallel arcs collapse to one edge, and one-directional arcs are
+ *   symmetrised (Table 1 caption P:604-606).  Isolated vertices are allowed.
+ *
+ * POINTERS: by default all array pointers are DEVICE pointers on the current
+ * CUDA device; with TC_HOST_PTRS they are HOST pointers (pinned memory gives
+ * the fastest copies) and the library copies them in and results out.
+ * Inputs are borrowed, read-only, and must stay valid for the call.
+ *
+ * OWNERSHIP: the library allocates its own workspace with cudaMallocAsync on
+ * the call's stream and frees it before returning.  Outputs are
+ * caller-allocated.  tc_count / tc_count_ex / tc_orient are synchronous (they
+ * return once results are on their destination); tc_count_shard is
+ * stream-ordered (its device result is ready when the stream reaches it).
+ *
+ * ERRORS: every entry point validates its arguments (null pointers, n >= 2^32,
+ * unknown flag bits, m >= 2^32 when cleaning) and returns TC_EINVAL before
+ * touching the device.  With TC_VALIDATE the graph itself is checked on the
+ * device (offsets, ids, and for TC_CLEAN: no self-loops, symmetry, and with
+ * TC_SORTED strictly increasing rows) and a violation returns TC_EGRAPH.
+ * Without TC_VALIDATE a malformed graph, or a false TC_CLEAN / TC_SORTED
+ * claim, is undefined behaviour.  CUDA failures return TC_ECUDA, allocation
+ * failures TC_ENOMEM.  tc_last_error() gives a thread-local message.
+ *
+ * THREAD SAFETY: calls on different streams or devices are independent; the
+ * only global state is the thread-local error string.
+ */
+#ifndef TC_B200_H
+#define TC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TC_ERROR UINT64_MAX /* tc_count's failure value (unreachable as a count) */
+
+enum {
+    TC_CLEAN = 1u << 0,      /* input is already simple and symmetric: no self-loops, no
+                                duplicate arcs, (u,v) present iff (v,u).  Skips step a1.    */
+    TC_SORTED = 1u << 1,     /* with TC_CLEAN: every row ascending; skips the segmented sort */
+    TC_PER_VERTEX = 1u << 2, /* fill per_vertex[n] with t(v)                                  */
+    TC_HOST_PTRS = 1u << 3,  /* all arrays are host pointers                                   */
+    TC_VALIDATE = 1u << 4,   /* check the graph on the device; TC_EGRAPH on violation          */
+    TC_ALL_FLAGS = 0x1fu
+};
+
+typedef enum {
+    TC_OK = 0,
+    TC_EINVAL = 1, /* bad argument                          */
+    TC_EGRAPH = 2, /* malformed graph (under TC_VALIDATE)   */
+    TC_ENOMEM = 3, /* device allocation failed              */
+    TC_ECUDA = 4   /* CUDA launch / runtime failure          */
+} tc_status;
+
+/* Intersection variants (§4.2.2 P:527-542 "dynamic grouping"; third kernel P:704-708). */
+enum {
+    TC_VARIANT_AUTO = -1,
+    TC_VARIANT_SHORT = 0,  /* one thread per edge, two-pointer merge ("TwoSmall")      */
+    TC_VARIANT_MERGE = 1,  /* one warp per edge, merge-path split ("TwoLarge"/balanced path,
+                              P:534-539)                                                      */
+    TC_VARIANT_SEARCH = 2, /* short list binary-searched in the long one           */
+    TC_VARIANT_HASH = 3    /* CTA per source: N+(u) staged in a shared-memory hash, every
+                              N+(v), v in N+(u), streamed and probed (north_star hub kernel)  */
+};
+
+typedef struct {
+    uint32_t short_max;         /* edge -> SHORT bin if max(d+u, d+v) <= short_max            */
+    uint32_t skew_ratio;        /* edge -> SEARCH bin if max >= skew_ratio * min                */
+    uint32_t hub_min_dplus;     /* sources with d+(u) >= this -> HASH kernel (all their edges) */
+    int32_t force_variant;      /* TC_VARIANT_AUTO, or route EVERY edge to one variant          */
+    void *stream;               /* cudaStream_t to run on; NULL = legacy default stream         */
+    uint32_t segsort_block_max; /* rows longer than this use the global segmented-sort path     */
+    uint32_t reserved[9];       /* must be zero                                                 */
+} tc_options;
+
+typedef struct {
+    /* phase times (ms, CUDA events on the call's stream); 0 when the phase did not run */
+    double ms_clean;     /* a1: keys, radix sort, unique                                   */
+    double ms_orient;    /* a2+a3: degrees, rank filter, compaction into N+ CSR            */
+    double ms_sort;      /* a4: segmented sort (TC_CLEAN without TC_SORTED)                */
+    double ms_bin;       /* a5: work estimation + binning                                  */
+    double ms_intersect; /* a6+a7: intersection kernels and the per-block reduction        */
+    double ms_total;     /* whole call, including host<->device copies with TC_HOST_PTRS   */
+    uint64_t m_undirected;    /* simple undirected edges = |E+|                             */
+    uint64_t work_W;          /* sum over E+ of d+(u) + d+(v)   (merge work)                */
+    uint64_t work_probe;      /* sum over E+ of d+(v)            (hash-probe work)          */
+    uint64_t bytes_alg;       /* 4*W + 16*m: algorithmic bytes of the intersection (B_alg)  */
+    uint64_t bin_edges[4];    /* edges routed to SHORT, MERGE, SEARCH, HASH                 */
+    uint64_t skipped_edges;   /* edges that cannot close a triangle (d+(u) < 2 or d+(v) = 0) */
+    uint64_t hub_sources;     /* sources handled by the HASH kernel                         */
+    uint64_t max_dplus;       /* max out-degree after orientation                           */
+    uint64_t kernel_launches; /* kernels this call launched                                 */
+    uint64_t h2d_bytes;       /* bytes copied host->device (TC_HOST_PTRS)                   */
+    uint64_t d2h_bytes;       /* bytes copied device->host                                   */
+} tc_stats;
+
+/* Fill *opt with the defaults (auto variant selection, default stream). */
+void tc_default_options(tc_options *opt);
+
+/* Triangle count, or TC_ERROR (reason in tc_last_error()).  Default options. */
+uint64_t tc_count(uint64_t n, uint64_t m, const uint64_t *row_offsets,
+                  const uint32_t *col_indices, uint32_t flags);
+
+/* Full form.  total: host uint64 (always host).  per_vertex: n entries on the
+ * pointer side given by TC_HOST_PTRS, required iff TC_PER_VERTEX.  opt and
+ * stats are host structs and may be NULL. */
+tc_status tc_count_ex(uint64_t n, uint64_t m, const uint64_t *row_offsets,
+                      const uint32_t *col_indices, uint32_t flags, const tc_options *opt,
+                      uint64_t *total, uint64_t *per_vertex, tc_stats *stats);
+
+/* Multi-GPU shard: every rank passes the SAME graph; the library
+ * runs the (replicated) preprocessing, splits source vertices into `world`
+ * contiguous-in-order groups of equal estimated work sum_{v in N+(u)} (d+u+d+v)
+ * (prefix sum over sources, no communication), and counts only triangles whose
+ * lowest-rank vertex falls in rank `rank`'s group.  partial_dev (device, 1
+ * entry) is OVERWRITTEN with this rank's partial count; per_vertex_partial
+ * (device, n entries, nullable unless TC_PER_VERTEX) is overwritten with this
+ * rank's per-vertex contributions.  Summing over ranks (one allreduce) gives
+ * exactly tc_count's results.  TC_HOST_PTRS is not allowed here.  Returns
+ * once the work is enqueued on opt->stream (stream-ordered). */
+tc_status tc_count_shard(uint64_t n, uint64_t m, const uint64_t *row_offsets,
+                         const uint32_t *col_indices, uint32_t flags, const tc_options *opt,
+                         int rank, int world, uint64_t *partial_dev,
+                         uint64_t *per_vertex_partial, tc_stats *stats);
+
+/* Steps a1-a4 only ("Form_Filtered_Edge_List", Alg. 2): writes the
+ * oriented, compacted CSR N+ (off_plus: n+1 entries; col_plus: capacity m
+ * entries, first m_plus used; each row ascending) and *m_plus (host).
+ * Pointer side per TC_HOST_PTRS.  Used by the parity tests of those steps. */
+tc_status tc_orient(uint64_t n, uint64_t m, const uint64_t *row_offsets,
+                    const uint32_t *col_indices, uint32_t flags, const tc_options *opt,
+                    uint64_t *off_plus, uint32_t *col_plus, uint64_t *m_plus);
+
+/* Thread-local message describing the last failure on this thread ("" if none). */
+const char *tc_last_error(void);
+
+/* Library version string. */
+const char *tc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TC_B200_H */

@@ -1,0 +1,229 @@
+"""B200 (sm_100a) exact triangle counting -- Python binding of libtc_b200.so.
+
+Argument marshalling only: every step of the path (clean, orient, sort, bin,
+intersect, reduce) runs in the CUDA kernels behind the C ABI declared in
+``include/tc.h``.  There is no CPU fallback: if the extension is missing or no
+CUDA device is present, the calls raise.
+
+PyTorch supplies device memory and the current stream; numpy arrays / CPU
+tensors are passed as host pointers (TC_HOST_PTRS) and copied by the library.
+Paper: Wang, Wang, Yang, Owens, "A Comparative Study on Exact Triangle Counting
+Algorithms on the GPU" (arxiv 1804.06926), Alg. 2.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+__all__ = ["count", "count_ex", "count_shard", "orient", "stats_dict", "library_path",
+           "TC_CLEAN", "TC_SORTED", "TC_PER_VERTEX", "TC_HOST_PTRS", "TC_VALIDATE",
+           "VARIANT_AUTO", "VARIANT_SHORT", "VARIANT_MERGE", "VARIANT_SEARCH", "VARIANT_HASH",
+           "TCError"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libtc_b200.so")
+
+TC_CLEAN, TC_SORTED, TC_PER_VERTEX, TC_HOST_PTRS, TC_VALIDATE = 1, 2, 4, 8, 16
+VARIANT_AUTO, VARIANT_SHORT, VARIANT_MERGE, VARIANT_SEARCH, VARIANT_HASH = -1, 0, 1, 2, 3
+_STATUS = {0: "TC_OK", 1: "TC_EINVAL", 2: "TC_EGRAPH", 3: "TC_ENOMEM", 4: "TC_ECUDA"}
+TC_ERROR = (1 << 64) - 1
+
+
+class TCError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Options(ctypes.Structure):
+    _fields_ = [("short_max", ctypes.c_uint32), ("skew_ratio", ctypes.c_uint32),
+                ("hub_min_dplus", ctypes.c_uint32), ("force_variant", ctypes.c_int32),
+                ("stream", ctypes.c_void_p), ("segsort_block_max", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint32 * 9)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("ms_clean", ctypes.c_double), ("ms_orient", ctypes.c_double),
+                ("ms_sort", ctypes.c_double), ("ms_bin", ctypes.c_double),
+                ("ms_intersect", ctypes.c_double), ("ms_total", ctypes.c_double),
+                ("m_undirected", ctypes.c_uint64), ("work_W", ctypes.c_uint64),
+                ("work_probe", ctypes.c_uint64), ("bytes_alg", ctypes.c_uint64),
+                ("bin_edges", ctypes.c_uint64 * 4), ("skipped_edges", ctypes.c_uint64),
+                ("hub_sources", ctypes.c_uint64), ("max_dplus", ctypes.c_uint64),
+                ("kernel_launches", ctypes.c_uint64), ("h2d_bytes", ctypes.c_uint64),
+                ("d2h_bytes", ctypes.c_uint64)]
+
+
+_lib = None
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise RuntimeError(f"{_LIB_PATH} is missing: run `python __graft_entry__.py` / "
+                           "paper_1804_06926_b200/_build.py first (there is no CPU fallback)")
+    lib = ctypes.CDLL(_LIB_PATH)
+    u64, u32, vp = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p
+    lib.tc_default_options.argtypes = [ctypes.POINTER(Options)]
+    lib.tc_default_options.restype = None
+    lib.tc_count.argtypes = [u64, u64, vp, vp, u32]
+    lib.tc_count.restype = u64
+    lib.tc_count_ex.argtypes = [u64, u64, vp, vp, u32, ctypes.POINTER(Options), vp, vp,
+                                ctypes.POINTER(Stats)]
+    lib.tc_count_ex.restype = ctypes.c_int
+    lib.tc_count_shard.argtypes = [u64, u64, vp, vp, u32, ctypes.POINTER(Options), ctypes.c_int,
+                                   ctypes.c_int, vp, vp, ctypes.POINTER(Stats)]
+    lib.tc_count_shard.restype = ctypes.c_int
+    lib.tc_orient.argtypes = [u64, u64, vp, vp, u32, ctypes.POINTER(Options), vp, vp, vp]
+    lib.tc_orient.restype = ctypes.c_int
+    lib.tc_last_error.argtypes = []
+    lib.tc_last_error.restype = ctypes.c_char_p
+    lib.tc_version.argtypes = []
+    lib.tc_version.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def _check(status: int):
+    if status != 0:
+        raise TCError(status, _load().tc_last_error().decode())
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def _arrays(rowptr, col):
+    """-> (n, M, rowptr_ptr, col_ptr, on_device, keepalive)."""
+    if _is_torch(rowptr):
+        import torch
+        assert rowptr.dtype in (torch.int64, torch.uint64) and col.dtype in (torch.int32, torch.uint32)
+        rowptr = rowptr.contiguous()
+        col = col.contiguous()
+        on_dev = rowptr.is_cuda
+        if on_dev != col.is_cuda:
+            raise ValueError("rowptr and col must be on the same side")
+        n = rowptr.numel() - 1
+        M = col.numel()
+        return n, M, rowptr.data_ptr(), (col.data_ptr() if M else None), on_dev, (rowptr, col)
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.uint64)
+    col = np.ascontiguousarray(col, dtype=np.uint32)
+    n = rowptr.size - 1
+    return n, col.size, rowptr.ctypes.data, (col.ctypes.data if col.size else None), False, (rowptr, col)
+
+
+def _options(stream=None, force_variant=None, short_max=None, skew_ratio=None, hub_min_dplus=None,
+             segsort_block_max=None, on_device=True):
+    o = Options()
+    _load().tc_default_options(ctypes.byref(o))
+    if stream is None and on_device:
+        import torch
+        stream = torch.cuda.current_stream().cuda_stream
+    o.stream = stream or None
+    if force_variant is not None:
+        o.force_variant = force_variant
+    if short_max is not None:
+        o.short_max = short_max
+    if skew_ratio is not None:
+        o.skew_ratio = skew_ratio
+    if hub_min_dplus is not None:
+        o.hub_min_dplus = hub_min_dplus
+    if segsort_block_max is not None:
+        o.segsort_block_max = segsort_block_max
+    return o
+
+
+def stats_dict(s: Stats) -> dict:
+    d = {f: getattr(s, f) for f, _ in Stats._fields_}
+    d["bin_edges"] = list(s.bin_edges)
+    return d
+
+
+def count_ex(rowptr, col, *, clean=False, sorted_rows=False, per_vertex=False, validate=False,
+             stream=None, with_stats=False, **opts):
+    """Triangle count of the graph (rowptr, col) [+ per-vertex counts, stats].
+
+    torch CUDA tensors -> device pointers on the current stream; numpy arrays or
+    CPU tensors -> TC_HOST_PTRS (the library copies in and out).
+    """
+    lib = _load()
+    n, M, rp, cp, on_dev, keep = _arrays(rowptr, col)
+    flags = (TC_CLEAN if clean else 0) | (TC_SORTED if sorted_rows else 0) | \
+            (TC_PER_VERTEX if per_vertex else 0) | (TC_VALIDATE if validate else 0) | \
+            (0 if on_dev else TC_HOST_PTRS)
+    o = _options(stream=stream, on_device=on_dev, **opts)
+    total = ctypes.c_uint64(0)
+    pv = None
+    pv_ptr = None
+    if per_vertex:
+        if on_dev:
+            import torch
+            pv = torch.empty(max(n, 1), dtype=torch.int64, device=keep[0].device)
+            pv_ptr = pv.data_ptr()
+        else:
+            pv = np.zeros(max(n, 1), dtype=np.uint64)
+            pv_ptr = pv.ctypes.data
+    st = Stats()
+    _check(lib.tc_count_ex(n, M, rp, cp, flags, ctypes.byref(o), ctypes.addressof(total), pv_ptr,
+                           ctypes.byref(st) if with_stats else None))
+    out = [int(total.value)]
+    if per_vertex:
+        out.append(pv[:n])
+    if with_stats:
+        out.append(stats_dict(st))
+    return out[0] if len(out) == 1 else tuple(out)
+
+
+def count(rowptr, col, **kw):
+    """Convenience: total triangle count (see count_ex for keywords)."""
+    return count_ex(rowptr, col, **kw)
+
+
+def count_shard(rowptr, col, rank: int, world: int, partial, *, clean=False, sorted_rows=False,
+                per_vertex_partial=None, stream=None, with_stats=False, **opts):
+    """Enqueue this rank's share; `partial` is a 1-element int64 CUDA tensor (overwritten)."""
+    lib = _load()
+    n, M, rp, cp, on_dev, keep = _arrays(rowptr, col)
+    if not on_dev:
+        raise ValueError("count_shard takes CUDA tensors")
+    flags = (TC_CLEAN if clean else 0) | (TC_SORTED if sorted_rows else 0) | \
+            (TC_PER_VERTEX if per_vertex_partial is not None else 0)
+    o = _options(stream=stream, **opts)
+    st = Stats()
+    _check(lib.tc_count_shard(n, M, rp, cp, flags, ctypes.byref(o), rank, world, partial.data_ptr(),
+                              per_vertex_partial.data_ptr() if per_vertex_partial is not None else None,
+                              ctypes.byref(st) if with_stats else None))
+    return stats_dict(st) if with_stats else None
+
+
+def orient(rowptr, col, *, clean=False, sorted_rows=False, stream=None, **opts):
+    """Steps a1-a4 only: the oriented compacted CSR (off+, col+) on the input's side."""
+    lib = _load()
+    n, M, rp, cp, on_dev, keep = _arrays(rowptr, col)
+    flags = (TC_CLEAN if clean else 0) | (TC_SORTED if sorted_rows else 0) | (0 if on_dev else TC_HOST_PTRS)
+    o = _options(stream=stream, on_device=on_dev, **opts)
+    mp = ctypes.c_uint64(0)
+    if on_dev:
+        import torch
+        off = torch.empty(n + 1, dtype=torch.int64, device=keep[0].device)
+        colp = torch.empty(max(M, 1), dtype=torch.int32, device=keep[0].device)
+        _check(lib.tc_orient(n, M, rp, cp, flags, ctypes.byref(o), off.data_ptr(), colp.data_ptr(),
+                             ctypes.addressof(mp)))
+    else:
+        off = np.zeros(n + 1, dtype=np.uint64)
+        colp = np.zeros(max(M, 1), dtype=np.uint32)
+        _check(lib.tc_orient(n, M, rp, cp, flags, ctypes.byref(o), off.ctypes.data, colp.ctypes.data,
+                             ctypes.addressof(mp)))
+    return off, colp[:mp.value]
+
+
+def version() -> str:
+    return _load().tc_version().decode()

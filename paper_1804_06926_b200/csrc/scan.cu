@@ -1,0 +1,78 @@
+// scan.cu -- device-wide exclusive scan (reduce-then-scan) and the block-level
+// scan / tile row-search helpers every tile kernel uses.
+#include "tc_internal.cuh"
+#include "block_scan.cuh"
+
+namespace tc {
+
+// ------------------------------------------------------------------ global scan
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+template <class T>
+__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const T *__restrict__ in,
+                                                              uint64_t count,
+                                                              uint64_t *__restrict__ partial) {
+    __shared__ uint64_t s_scratch[kScanThreads / 32];
+    uint64_t base = (uint64_t)blockIdx.x * kScanTile;
+    uint64_t sum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; k++) {
+        uint64_t i = base + (uint64_t)k * kScanThreads + threadIdx.x;
+        if (i < count) sum += (uint64_t)in[i];
+    }
+    sum = block_sum_u64(sum, s_scratch);
+    if (threadIdx.x == 0) partial[blockIdx.x] = sum;
+}
+
+template <class T>
+__global__ void __launch_bounds__(kScanThreads) k_scan_apply(const T *__restrict__ in,
+                                                             uint64_t count,
+                                                             const uint64_t *__restrict__ offsets,
+                                                             uint64_t *__restrict__ out) {
+    __shared__ uint64_t s_scan[kScanThreads / 32];
+    uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanItems;
+    uint64_t v[kScanItems];
+    uint64_t run = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; k++) {
+        uint64_t i = base + k;
+        uint64_t x = i < count ? (uint64_t)in[i] : 0;
+        v[k] = run;
+        run += x;
+    }
+    uint64_t prefix = block_exclusive_scan<SumOp64>(run, s_scan) + offsets[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < kScanItems; k++) {
+        uint64_t i = base + k;
+        if (i <= count) out[i] = v[k] + prefix;   // out[count] = total
+    }
+}
+
+template <class T>
+static void scan_impl(Ctx &ctx, const T *in, uint64_t *out, uint64_t count) {
+    // tiles cover [0, count] inclusive so the total lands in out[count]
+    uint64_t items = count + 1;
+    uint64_t tiles = (items + kScanTile - 1) / kScanTile;
+    uint64_t *partial = ctx.alloc<uint64_t>(tiles);
+    uint64_t *offsets = ctx.alloc<uint64_t>(tiles + 1);
+    k_scan_reduce<T><<<(unsigned)tiles, kScanThreads, 0, ctx.stream>>>(in, count, partial);
+    TC_LAUNCHED(ctx);
+    if (tiles == 1) {
+        TC_CUDA(cudaMemsetAsync(offsets, 0, sizeof(uint64_t), ctx.stream));
+    } else {
+        scan_impl<uint64_t>(ctx, partial, offsets, tiles);
+    }
+    k_scan_apply<T><<<(unsigned)tiles, kScanThreads, 0, ctx.stream>>>(in, count, offsets, out);
+    TC_LAUNCHED(ctx);
+}
+
+void scan_exclusive(Ctx &ctx, const uint32_t *in, uint64_t *out, uint64_t count) {
+    scan_impl<uint32_t>(ctx, in, out, count);
+}
+void scan_exclusive(Ctx &ctx, const uint64_t *in, uint64_t *out, uint64_t count) {
+    scan_impl<uint64_t>(ctx, in, out, count);
+}
+
+}  // namespace tc

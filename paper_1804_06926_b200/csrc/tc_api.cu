@@ -1,0 +1,348 @@
+// tc_api.cu -- the C ABI (include/tc.h): argument checks, workspace, stream,
+// host<->device staging, and the phase sequence of Alg. 2:
+//   Form_Filtered_Edge_List (a1-a4) -> Partition (a5) -> intersections (a6)
+//   -> Reduce (a7, fused).  The whole sequence is stream-ordered: no host
+//   synchronisation until the 8-byte count is read back.
+#include <cstdio>
+#include <cstring>
+
+#include "tc_internal.cuh"
+
+namespace tc {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+static int device_sms(int dev) {
+    static int cache[64] = {0};
+    if (dev < 0 || dev >= 64) return 148;
+    if (!cache[dev]) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+            v = 148;
+        cache[dev] = v;
+    }
+    return cache[dev];
+}
+
+static void keep_pool_warm(int dev) {
+    static bool done[64] = {false};
+    if (dev < 0 || dev >= 64 || done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[dev] = true;
+}
+
+// 32 uint64 of pinned host memory per thread for asynchronous stat read-back.
+static uint64_t *pinned_scratch() {
+    static thread_local uint64_t *p = nullptr;
+    if (!p) TC_CUDA(cudaMallocHost((void **)&p, 32 * sizeof(uint64_t)));
+    return p;
+}
+
+enum Mode { kCount, kShard, kOrientOnly };
+
+struct Call {
+    uint64_t n, M;
+    const uint64_t *rowptr;
+    const uint32_t *col;
+    uint32_t flags;
+    tc_options opt;
+    int rank = 0, world = 1;
+    Mode mode = kCount;
+    // outputs
+    uint64_t *total_host = nullptr;   // kCount
+    uint64_t *partial_dev = nullptr;  // kShard
+    uint64_t *per_vertex = nullptr;
+    tc_stats *stats = nullptr;
+    uint64_t *off_plus = nullptr;     // kOrientOnly
+    uint32_t *col_plus = nullptr;
+    uint64_t *m_plus = nullptr;
+};
+
+static tc_status check_args(const Call &c) {
+    if (c.flags & ~(uint32_t)TC_ALL_FLAGS) return set_error("unknown flag bits"), TC_EINVAL;
+    if (c.n >= (1ull << 32)) return set_error("n must be < 2^32"), TC_EINVAL;
+    if (!c.rowptr) return set_error("row_offsets is NULL"), TC_EINVAL;
+    if (c.M > 0 && !c.col) return set_error("col_indices is NULL with m > 0"), TC_EINVAL;
+    if (c.mode == kCount && !c.total_host) return set_error("total is NULL"), TC_EINVAL;
+    if (c.mode == kShard) {
+        if (!c.partial_dev) return set_error("partial_dev is NULL"), TC_EINVAL;
+        if (c.world < 1 || c.rank < 0 || c.rank >= c.world)
+            return set_error("need 0 <= rank < world"), TC_EINVAL;
+        if (c.flags & TC_HOST_PTRS) return set_error("tc_count_shard takes device pointers"), TC_EINVAL;
+    }
+    if (c.mode == kOrientOnly && (!c.off_plus || (!c.col_plus && c.M > 0) || !c.m_plus))
+        return set_error("tc_orient output pointer is NULL"), TC_EINVAL;
+    if ((c.flags & TC_PER_VERTEX) && c.mode != kOrientOnly && !c.per_vertex)
+        return set_error("TC_PER_VERTEX needs per_vertex"), TC_EINVAL;
+    if ((c.flags & TC_SORTED) && !(c.flags & TC_CLEAN))
+        return set_error("TC_SORTED is only meaningful with TC_CLEAN"), TC_EINVAL;
+    if (c.opt.force_variant < -1 || c.opt.force_variant > 3)
+        return set_error("force_variant out of range"), TC_EINVAL;
+    for (uint32_t r : c.opt.reserved)
+        if (r) return set_error("tc_options.reserved must be zero"), TC_EINVAL;
+    return TC_OK;
+}
+
+static void run(Call &c) {
+    Ctx ctx;
+    TC_CUDA(cudaGetDevice(&ctx.device));
+    ctx.stream = (cudaStream_t)c.opt.stream;
+    ctx.num_sms = device_sms(ctx.device);
+    keep_pool_warm(ctx.device);
+    const bool host = c.flags & TC_HOST_PTRS;
+    const bool pv = (c.flags & TC_PER_VERTEX) && c.mode != kOrientOnly;
+    tc_stats st;
+    memset(&st, 0, sizeof(st));
+    Timer *tm = nullptr;
+    cudaEvent_t t_begin = nullptr, t_end = nullptr;
+    if (c.stats) {
+        tm = new Timer(ctx.stream);
+        cudaEventCreate(&t_begin);
+        cudaEventCreate(&t_end);
+        cudaEventRecord(t_begin, ctx.stream);
+    }
+    struct Cleanup {
+        Timer *&tm;
+        cudaEvent_t &a, &b;
+        ~Cleanup() {
+            delete tm;
+            if (a) cudaEventDestroy(a);
+            if (b) cudaEventDestroy(b);
+        }
+    } cleanup{tm, t_begin, t_end};
+
+    // ---- inputs on the device
+    const uint64_t *rowptr = c.rowptr;
+    const uint32_t *col = c.col;
+    if (host) {
+        uint64_t *d_row = ctx.alloc<uint64_t>(c.n + 1);
+        TC_CUDA(cudaMemcpyAsync(d_row, c.rowptr, (c.n + 1) * sizeof(uint64_t),
+                                cudaMemcpyHostToDevice, ctx.stream));
+        st.h2d_bytes += (c.n + 1) * sizeof(uint64_t);
+        rowptr = d_row;
+        if (c.M) {
+            uint32_t *d_col = ctx.alloc<uint32_t>(c.M);
+            TC_CUDA(cudaMemcpyAsync(d_col, c.col, c.M * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                    ctx.stream));
+            st.h2d_bytes += c.M * sizeof(uint32_t);
+            col = d_col;
+        }
+    }
+    if (c.flags & TC_VALIDATE) {
+        std::string msg = validate_graph(ctx, c.n, c.M, rowptr, col, c.flags & TC_CLEAN,
+                                         c.flags & TC_SORTED);
+        if (!msg.empty()) throw Error{TC_EGRAPH, msg};
+    }
+
+    uint64_t *pv_dev = nullptr;
+    if (pv) {
+        pv_dev = host ? ctx.alloc<uint64_t>(c.n) : c.per_vertex;
+        if (c.n) TC_CUDA(cudaMemsetAsync(pv_dev, 0, c.n * sizeof(uint64_t), ctx.stream));
+    }
+    uint64_t *total_dev = c.mode == kShard ? c.partial_dev : ctx.alloc<uint64_t>(1);
+    TC_CUDA(cudaMemsetAsync(total_dev, 0, sizeof(uint64_t), ctx.stream));
+    uint64_t *pin = pinned_scratch();
+    if (c.stats) memset(pin, 0, 32 * sizeof(uint64_t));
+
+    if (c.n > 0 && c.M > 0) {
+        Oriented g;
+        if (c.flags & TC_CLEAN)
+            orient_clean(ctx, c.n, c.M, rowptr, col, c.flags & TC_SORTED, c.opt.segsort_block_max,
+                         g, tm);
+        else
+            orient_dirty(ctx, c.n, c.M, rowptr, col, g, tm);
+
+        if (c.mode == kOrientOnly) {
+            cudaMemcpyKind kind = host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+            uint64_t m = 0;
+            TC_CUDA(cudaMemcpyAsync(&m, g.m_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx.stream));
+            TC_CUDA(cudaStreamSynchronize(ctx.stream));
+            TC_CUDA(cudaMemcpyAsync(c.off_plus, g.off, (c.n + 1) * sizeof(uint64_t), kind, ctx.stream));
+            if (m) TC_CUDA(cudaMemcpyAsync(c.col_plus, g.col, m * sizeof(uint32_t), kind, ctx.stream));
+            TC_CUDA(cudaStreamSynchronize(ctx.stream));
+            *c.m_plus = m;
+            return;
+        }
+
+        if (tm) tm->begin(kBin);
+        BinParams bp;
+        bp.short_max = c.opt.short_max;
+        bp.skew_ratio = c.opt.skew_ratio;
+        bp.hub_min = c.opt.hub_min_dplus;
+        bp.force = c.opt.force_variant;
+        bp.rank = c.rank;
+        bp.world = c.world;
+        bp.work_prefix = nullptr;
+        bp.work_chunk = 0;
+        if (c.world > 1) {
+            uint64_t *prefix = ctx.alloc<uint64_t>(c.n + 1);
+            work_prefix(ctx, g, prefix);
+            bp.work_prefix = prefix;
+        }
+        Bins bins;
+        bin_edges(ctx, g, bp, bins);
+        if (tm) tm->end(kBin);
+
+        if (tm) tm->begin(kIntersect);
+        intersect_all(ctx, g, bins, total_dev, pv_dev);
+        if (tm) tm->end(kIntersect);
+        if (c.stats) {  // async into pinned memory; read after the final sync
+            TC_CUDA(cudaMemcpyAsync(pin, bins.count, 16 * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                                    ctx.stream));
+            TC_CUDA(cudaMemcpyAsync(pin + 16, g.m_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                                    ctx.stream));
+        }
+    } else if (c.mode == kOrientOnly) {
+        cudaMemcpyKind kind = host ? cudaMemcpyHostToHost : cudaMemcpyHostToDevice;
+        std::vector<uint64_t> zeros(c.n + 1, 0);
+        TC_CUDA(cudaMemcpyAsync(c.off_plus, zeros.data(), (c.n + 1) * sizeof(uint64_t), kind,
+                                ctx.stream));
+        TC_CUDA(cudaStreamSynchronize(ctx.stream));
+        *c.m_plus = 0;
+        return;
+    }
+
+    if (c.mode == kCount) {
+        TC_CUDA(cudaMemcpyAsync(pin + 20, total_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                                ctx.stream));
+        st.d2h_bytes += sizeof(uint64_t);
+        if (pv && host && c.n) {
+            TC_CUDA(cudaMemcpyAsync(c.per_vertex, pv_dev, c.n * sizeof(uint64_t),
+                                    cudaMemcpyDeviceToHost, ctx.stream));
+            st.d2h_bytes += c.n * sizeof(uint64_t);
+        }
+    }
+    if (c.stats) cudaEventRecord(t_end, ctx.stream);
+    ctx.release();
+    if (c.mode != kShard || c.stats) TC_CUDA(cudaStreamSynchronize(ctx.stream));
+    TC_CUDA(cudaGetLastError());
+    if (c.mode == kCount) *c.total_host = pin[20];
+
+    if (c.stats) {
+        st.ms_clean = tm->ms(kClean);
+        st.ms_orient = tm->ms(kOrient);
+        st.ms_sort = tm->ms(kSort);
+        st.ms_bin = tm->ms(kBin);
+        st.ms_intersect = tm->ms(kIntersect);
+        float t = 0.f;
+        cudaEventElapsedTime(&t, t_begin, t_end);
+        st.ms_total = t;
+        st.m_undirected = pin[16];
+        st.work_W = pin[4];
+        st.work_probe = pin[5];
+        st.bytes_alg = 4 * st.work_W + 16 * st.m_undirected;
+        st.bin_edges[0] = pin[0];
+        st.bin_edges[1] = pin[1];
+        st.bin_edges[2] = pin[2];
+        st.bin_edges[3] = pin[8];
+        st.skipped_edges = pin[6];
+        st.hub_sources = pin[3];
+        st.max_dplus = pin[7];
+        st.kernel_launches = ctx.launches;
+        *c.stats = st;
+    }
+}
+
+static tc_status guarded(Call &c) {
+    tc_status s = check_args(c);
+    if (s != TC_OK) return s;
+    try {
+        run(c);
+    } catch (const Error &e) {
+        set_error(e.msg);
+        return e.status;
+    } catch (const std::bad_alloc &) {
+        set_error("host allocation failed");
+        return TC_ENOMEM;
+    }
+    set_error("");
+    return TC_OK;
+}
+
+static tc_options resolve(const tc_options *opt) {
+    tc_options o;
+    tc_default_options(&o);
+    if (opt) {
+        o = *opt;
+        if (!o.short_max) o.short_max = 32;
+        if (!o.skew_ratio) o.skew_ratio = 16;
+        if (!o.hub_min_dplus) o.hub_min_dplus = 128;
+    }
+    return o;
+}
+
+}  // namespace tc
+
+using namespace tc;
+
+extern "C" {
+
+void tc_default_options(tc_options *opt) {
+    if (!opt) return;
+    memset(opt, 0, sizeof(*opt));
+    opt->short_max = 32;
+    opt->skew_ratio = 16;
+    opt->hub_min_dplus = 128;
+    opt->force_variant = TC_VARIANT_AUTO;
+    opt->stream = nullptr;
+    opt->segsort_block_max = 8192;
+}
+
+tc_status tc_count_ex(uint64_t n, uint64_t m, const uint64_t *row_offsets,
+                      const uint32_t *col_indices, uint32_t flags, const tc_options *opt,
+                      uint64_t *total, uint64_t *per_vertex, tc_stats *stats) {
+    Call c{n, m, row_offsets, col_indices, flags, resolve(opt)};
+    c.mode = kCount;
+    c.total_host = total;
+    c.per_vertex = per_vertex;
+    c.stats = stats;
+    return guarded(c);
+}
+
+uint64_t tc_count(uint64_t n, uint64_t m, const uint64_t *row_offsets,
+                  const uint32_t *col_indices, uint32_t flags) {
+    uint64_t total = 0;
+    if (flags & TC_PER_VERTEX) {
+        set_error("tc_count has no per-vertex output; use tc_count_ex");
+        return TC_ERROR;
+    }
+    tc_status s = tc_count_ex(n, m, row_offsets, col_indices, flags, nullptr, &total, nullptr, nullptr);
+    return s == TC_OK ? total : TC_ERROR;
+}
+
+tc_status tc_count_shard(uint64_t n, uint64_t m, const uint64_t *row_offsets,
+                         const uint32_t *col_indices, uint32_t flags, const tc_options *opt,
+                         int rank, int world, uint64_t *partial_dev,
+                         uint64_t *per_vertex_partial, tc_stats *stats) {
+    Call c{n, m, row_offsets, col_indices, flags, resolve(opt)};
+    c.mode = kShard;
+    c.rank = rank;
+    c.world = world;
+    c.partial_dev = partial_dev;
+    c.per_vertex = per_vertex_partial;
+    c.stats = stats;
+    return guarded(c);
+}
+
+tc_status tc_orient(uint64_t n, uint64_t m, const uint64_t *row_offsets,
+                    const uint32_t *col_indices, uint32_t flags, const tc_options *opt,
+                    uint64_t *off_plus, uint32_t *col_plus, uint64_t *m_plus) {
+    Call c{n, m, row_offsets, col_indices, flags, resolve(opt)};
+    c.mode = kOrientOnly;
+    c.off_plus = off_plus;
+    c.col_plus = col_plus;
+    c.m_plus = m_plus;
+    return guarded(c);
+}
+
+const char *tc_last_error(void) { return g_last_error.c_str(); }
+
+const char *tc_version(void) { return "tc_b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

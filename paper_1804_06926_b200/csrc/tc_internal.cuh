@@ -1,0 +1,248 @@
+// tc_internal.cuh -- shared device helpers and host-side declarations of the
+// B200 triangle-counting pipeline.  Product code only: nothing here is shared
+// with oracle/ (which is independent test infrastructure).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/tc.h"
+#include "block_scan.cuh"
+
+namespace tc {
+
+constexpr uint32_t kEmpty = 0xffffffffu;
+
+// ------------------------------------------------------------------ errors
+struct Error {
+    tc_status status;
+    std::string msg;
+};
+
+void set_error(const std::string &msg);
+
+#define TC_CUDA(call)                                                                  \
+    do {                                                                               \
+        cudaError_t e_ = (call);                                                       \
+        if (e_ != cudaSuccess)                                                         \
+            throw ::tc::Error{e_ == cudaErrorMemoryAllocation ? TC_ENOMEM : TC_ECUDA, \
+                              std::string(#call) + ": " + cudaGetErrorString(e_)};    \
+    } while (0)
+
+#define TC_LAUNCHED(ctx)                                                                   \
+    do {                                                                                   \
+        cudaError_t e_ = cudaGetLastError();                                               \
+        if (e_ != cudaSuccess)                                                             \
+            throw ::tc::Error{TC_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)}; \
+        (ctx).launches++;                                                                  \
+    } while (0)
+
+// ------------------------------------------------------------------ context
+// Stream-ordered workspace: every allocation is cudaMallocAsync on the call's
+// stream and freed (stream-ordered) when the context is destroyed.
+struct Ctx {
+    cudaStream_t stream = nullptr;
+    int device = 0;
+    int num_sms = 148;
+    uint64_t launches = 0;
+    std::vector<void *> allocs;
+
+    template <class T>
+    T *alloc(uint64_t count) {
+        void *p = nullptr;
+        size_t bytes = (size_t)(count ? count : 1) * sizeof(T);
+        cudaError_t e = cudaMallocAsync(&p, bytes, stream);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            throw Error{TC_ENOMEM, "cudaMallocAsync(" + std::to_string(bytes) + " B) failed: " +
+                                       cudaGetErrorString(e)};
+        }
+        allocs.push_back(p);
+        return (T *)p;
+    }
+    void release() {
+        for (void *p : allocs) cudaFreeAsync(p, stream);
+        allocs.clear();
+    }
+    ~Ctx() { release(); }
+    // Grid for a persistent (grid-stride) kernel: `per_sm` resident CTAs per SM.
+    int persistent_grid(int per_sm) const { return num_sms * per_sm; }
+};
+
+// ------------------------------------------------------------------ device helpers
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Block-wide sum of a per-thread uint64; result valid in thread 0.  `scratch`
+// must hold blockDim.x/32 entries.
+__device__ __forceinline__ uint64_t block_sum_u64(uint64_t v, uint64_t *scratch) {
+    v = warp_sum_u64(v);
+    int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) scratch[warp] = v;
+    __syncthreads();
+    uint64_t total = 0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) total += scratch[w];
+    __syncthreads();
+    return total;
+}
+
+// Largest u in [0, n) with rowptr[u] <= x  (rowptr non-decreasing, rowptr[0] = 0).
+__device__ __forceinline__ uint64_t row_of(const uint64_t *__restrict__ rowptr, uint64_t n,
+                                           uint64_t x) {
+    uint64_t lo = 0, hi = n;  // answer in [lo, hi)
+    while (hi - lo > 1) {
+        uint64_t mid = (lo + hi) >> 1;
+        if (rowptr[mid] <= x) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// First u in [0, n] with rowptr[u] >= x.
+__device__ __forceinline__ uint64_t lower_bound_u64(const uint64_t *__restrict__ a, uint64_t len,
+                                                    uint64_t x) {
+    uint64_t lo = 0, hi = len;
+    while (lo < hi) {
+        uint64_t mid = (lo + hi) >> 1;
+        if (a[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// ------------------------------------------------------------------ tiles
+// A "tile" is a contiguous range of kTileItems arcs (or oriented edges) handled
+// by one CTA of kTileThreads threads, each owning kItemsPerThread consecutive
+// items (blocked arrangement, so block scans preserve index order).
+constexpr int kTileThreads = 256;
+constexpr int kItemsPerThread = 8;
+constexpr int kTileItems = kTileThreads * kItemsPerThread;
+
+// Fill s_row[0..len) with the CSR row of items tile_start .. tile_start+len-1
+// (load-balanced row search: rows whose start falls inside the tile mark their
+// first item, then an inclusive max-scan propagates row ids).  Must be called
+// by all threads of the block.  s_scan: kTileThreads/32 uint32 scratch.
+__device__ __forceinline__ void tile_rows(const uint64_t *__restrict__ rowptr, uint64_t n, uint64_t tile_start,
+                          uint32_t len, uint32_t *s_row, uint32_t *s_scan) {
+    __shared__ uint64_t s_bounds[2];
+    for (int i = threadIdx.x; i < kTileItems; i += blockDim.x) s_row[i] = 0;
+    if (threadIdx.x == 0) {
+        s_bounds[0] = lower_bound_u64(rowptr, n + 1, tile_start + 1);
+        s_bounds[1] = lower_bound_u64(rowptr, n + 1, tile_start + len);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(&s_row[0], (uint32_t)row_of(rowptr, n, tile_start));
+    uint64_t ulo = s_bounds[0], uhi = s_bounds[1];
+    for (uint64_t u = ulo + threadIdx.x; u < uhi; u += blockDim.x)
+        atomicMax(&s_row[rowptr[u] - tile_start], (uint32_t)u);
+    __syncthreads();
+    // inclusive max-scan over the tile (blocked: thread t owns items [8t, 8t+8))
+    uint32_t v[kItemsPerThread];
+    uint32_t run = 0;
+#pragma unroll
+    for (int k = 0; k < kItemsPerThread; k++) {
+        run = max(run, s_row[threadIdx.x * kItemsPerThread + k]);
+        v[k] = run;
+    }
+    uint32_t prefix = block_exclusive_scan<MaxOp>(run, s_scan);
+#pragma unroll
+    for (int k = 0; k < kItemsPerThread; k++)
+        s_row[threadIdx.x * kItemsPerThread + k] = max(v[k], prefix);
+    __syncthreads();
+}
+
+
+// ------------------------------------------------------------------ host primitives
+// Exclusive scan: out[i] = sum_{j<i} in[j] for i in [0, count], out[count] = total.
+void scan_exclusive(Ctx &ctx, const uint32_t *in, uint64_t *out, uint64_t count);
+void scan_exclusive(Ctx &ctx, const uint64_t *in, uint64_t *out, uint64_t count);
+
+// Stable LSD radix sort on bits [0, bits) of the keys.  `count_dev`, if non-null,
+// is a device counter that caps the number of valid items (<= capacity).
+// Returns true if the sorted result ended in the *_alt buffers.
+bool radix_sort(Ctx &ctx, uint64_t *keys, uint64_t *keys_alt, uint64_t capacity,
+                const uint64_t *count_dev, int bits);
+bool radix_sort_pairs(Ctx &ctx, uint32_t *keys, uint32_t *keys_alt, uint32_t *vals,
+                      uint32_t *vals_alt, uint64_t capacity, const uint64_t *count_dev, int bits);
+
+// ------------------------------------------------------------------ pipeline stages
+struct Oriented {
+    uint64_t n = 0;
+    uint64_t *off = nullptr;    // off+[n+1]
+    uint32_t *col = nullptr;    // col+[m]
+    uint32_t *dplus = nullptr;  // d+[n]
+    uint64_t *m_dev = nullptr;  // device scalar m
+    uint64_t m_cap = 0;         // capacity bound for m (host-known)
+};
+
+// Phase timer: CUDA events on the call's stream, read after the final sync.
+enum Phase { kClean = 0, kOrient, kSort, kBin, kIntersect, kNumPhases };
+struct Timer {
+    cudaEvent_t ev[kNumPhases][2] = {};
+    bool used[kNumPhases] = {};
+    cudaStream_t stream = nullptr;
+    explicit Timer(cudaStream_t s) : stream(s) {
+        for (auto &p : ev) {
+            cudaEventCreate(&p[0]);
+            cudaEventCreate(&p[1]);
+        }
+    }
+    ~Timer() {
+        for (auto &p : ev) {
+            cudaEventDestroy(p[0]);
+            cudaEventDestroy(p[1]);
+        }
+    }
+    void begin(Phase p) { cudaEventRecord(ev[p][0], stream); used[p] = true; }
+    void end(Phase p) { cudaEventRecord(ev[p][1], stream); }
+    double ms(Phase p) const {
+        float t = 0.f;
+        if (!used[p] || cudaEventElapsedTime(&t, ev[p][0], ev[p][1]) != cudaSuccess) return 0.0;
+        return (double)t;
+    }
+};
+
+// a1 (dirty input) + a2 + a3 (+ a4 by construction): raw CSR -> oriented CSR.
+void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
+                  Oriented &out, Timer *tm);
+// a2 + a3 for clean symmetric input, then a4 (segmented sort) unless sorted.
+void orient_clean(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
+                  bool sorted, uint32_t segsort_block_max, Oriented &out, Timer *tm);
+// a4: sort each row of (off, col) ascending.
+void segmented_sort(Ctx &ctx, uint64_t n, const uint64_t *off, uint32_t *col, uint64_t m_cap,
+                    uint32_t block_max);
+
+struct Bins {
+    uint2 *edges[3] = {nullptr, nullptr, nullptr};  // SHORT, MERGE, SEARCH: (u, v) pairs
+    uint64_t *count = nullptr;                       // device: [0..2] bin sizes, [3] hubs,
+                                                     // [4] W, [5] probe work, [6] skipped,
+                                                     // [7] max d+, [8] hash-bin edges
+    uint32_t *hubs = nullptr;                        // HASH sources
+    uint64_t cap = 0;
+};
+
+struct BinParams {
+    uint32_t short_max, skew_ratio, hub_min;
+    int force;
+    int rank, world;
+    const uint64_t *work_prefix;  // exclusive prefix of per-source work (world > 1)
+    uint64_t work_chunk;          // ceil(W_total / world)
+};
+
+void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins);
+void work_prefix(Ctx &ctx, const Oriented &g, uint64_t *prefix /* n+1 */);
+
+// a6 + a7: all intersection kernels; adds into total_dev (and per_vertex if non-null).
+void intersect_all(Ctx &ctx, const Oriented &g, const Bins &bins, uint64_t *total_dev,
+                   uint64_t *per_vertex);
+
+// Validation (TC_VALIDATE); returns a TC_EGRAPH message or "".
+std::string validate_graph(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr,
+                           const uint32_t *col, bool clean, bool sorted);
+
+}  // namespace tc

@@ -1,0 +1,258 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element.
+
+All counts are integers: the bar is bit-exact equality of T, of every t(v),
+and of the oriented CSR (off+, col+) produced by steps a1-a4.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import graphgen as G
+import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # collected on CPU boxes, skipped there
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1804_06926_b200 as tc  # noqa: E402
+
+DEV = torch.device("cuda:0")
+VARIANTS = [None, tc.VARIANT_SHORT, tc.VARIANT_MERGE, tc.VARIANT_SEARCH, tc.VARIANT_HASH]
+
+
+def on_dev(rowptr, col):
+    return (torch.from_numpy(np.ascontiguousarray(rowptr, np.uint64).view(np.int64)).to(DEV),
+            torch.from_numpy(np.ascontiguousarray(col, np.uint32).view(np.int32)).to(DEV))
+
+
+def gpu_count(rowptr, col, **kw):
+    rp, cl = on_dev(rowptr, col)
+    out = tc.count_ex(rp, cl, **kw)
+    torch.cuda.synchronize()
+    return out
+
+
+def pv_np(t):
+    return t.cpu().numpy().view(np.uint64)
+
+
+def check_graph(g, variants=VARIANTS, per_vertex=True, **kw):
+    T, t = O.count(g.n, g.rowptr, g.col, per_vertex=True)
+    for v in variants:
+        if per_vertex:
+            got, pv = gpu_count(g.rowptr, g.col, per_vertex=True, force_variant=v, **kw)
+            assert got == T, (g.name, v, got, T)
+            assert (pv_np(pv) == t).all(), (g.name, v)
+        else:
+            assert gpu_count(g.rowptr, g.col, force_variant=v, **kw) == T, (g.name, v)
+    return T
+
+
+# ------------------------------------------------------------------ fixtures / closed forms
+def test_fixtures(golden):
+    assert check_graph(G.fig_mm()) == golden("fig_mm.txt")["T"][0][0] == 3
+    assert check_graph(G.karate()) == golden("karate.txt")["T"][0][0] == 45
+    assert check_graph(G.complete(20)) == 1140
+    assert check_graph(G.wheel(10)) == 9
+
+
+def test_degenerate():
+    assert gpu_count(np.zeros(1, np.uint64), np.zeros(0, np.uint32)) == 0            # n = 0
+    T, pv = gpu_count(np.zeros(6, np.uint64), np.zeros(0, np.uint32), per_vertex=True)
+    assert T == 0 and (pv_np(pv) == 0).all()                                         # m = 0
+    for g in [G.from_edges(2, [(0, 1)]), G.from_edges(3, [(0, 1), (1, 2), (2, 0)]),
+              G.from_edges(4, [(0, 0), (1, 1), (2, 2)]), G.path(50), G.star(300),
+              G.from_edges(10, [(3, 4), (4, 5), (5, 3), (3, 4), (4, 3)])]:
+        check_graph(g)
+
+
+@pytest.mark.parametrize("n", [3, 4, 5, 33, 64, 65, 200, 700])
+def test_complete(n):
+    assert check_graph(G.complete(n), per_vertex=n <= 200) == math.comb(n, 3)
+
+
+def test_closed_forms_mix():
+    assert check_graph(G.complete_multipartite([5, 6, 7])) == 210
+    assert check_graph(G.friendship(40)) == 40
+    assert check_graph(G.windmill(30, 8)) == 30 * 56
+    assert check_graph(G.random_bipartite(60, 70, 0.3, 1)) == 0
+    assert check_graph(G.random_tree(5000, 3)) == 0
+    assert check_graph(G.triangulated_grid(123, 77)) == 2 * 122 * 76
+
+
+# ------------------------------------------------------------------ random graphs
+@pytest.mark.parametrize("seed", range(24))
+def test_gnp_dirty(seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(4, 600))
+    p = [0.005, 0.02, 0.1, 0.3][seed % 4]
+    check_graph(G.dirty(G.gnp(n, p, seed), seed))
+
+
+@pytest.mark.parametrize("scale", [8, 10, 12, 14])
+def test_rmat_all_variants(scale):
+    check_graph(G.rmat(scale, 16, seed=scale))
+
+
+@pytest.mark.parametrize("kw", [dict(short_max=1), dict(short_max=1 << 31), dict(skew_ratio=1),
+                                dict(skew_ratio=1 << 31), dict(hub_min_dplus=2),
+                                dict(hub_min_dplus=1 << 31), dict(short_max=4, skew_ratio=2, hub_min_dplus=8)])
+def test_threshold_invariance(kw):
+    """The count is invariant under any bin thresholds."""
+    check_graph(G.rmat(13, 16, seed=77), variants=[None], **kw)
+
+
+def test_generators_small():
+    check_graph(G.chung_lu(20000, 150000, seed=3))
+    check_graph(G.clique_union(5000, 4000, seed=4))
+    check_graph(G.road_mesh(200, 150, seed=5))
+    check_graph(G.kron(G.karate(), G.karate()))
+
+
+# ------------------------------------------------------------------ clean-input paths, orientation
+def clean_csr(g):
+    return O.clean(g.n, g.rowptr, g.col)
+
+
+def shuffled_rows(n, row, col, seed):
+    rng = np.random.default_rng(seed)
+    col = col.copy()
+    for u in range(n):
+        a, b = int(row[u]), int(row[u + 1])
+        col[a:b] = rng.permutation(col[a:b])
+    return col
+
+
+@pytest.mark.parametrize("name", ["rmat12", "karate", "K300", "gnp"])
+def test_orientation_parity(name):
+    g = {"rmat12": lambda: G.rmat(12, 16, seed=3), "karate": G.karate,
+         "K300": lambda: G.complete(300), "gnp": lambda: G.gnp(500, 0.05, 2)}[name]()
+    row, col = clean_csr(g)
+    want_off, want_col = O.orient(g.n, row, col)
+    cases = [dict(rowptr=g.rowptr, col=g.col),                                   # a1 path
+             dict(rowptr=row, col=col, clean=True, sorted_rows=True),             # sorted clean
+             dict(rowptr=row, col=shuffled_rows(g.n, row, col, 1), clean=True),   # a4 segsort
+             dict(rowptr=row, col=shuffled_rows(g.n, row, col, 2), clean=True, segsort_block_max=32)]
+    for c in cases:
+        rp, cl = on_dev(c.pop("rowptr"), c.pop("col"))
+        off, colp = tc.orient(rp, cl, **c)
+        torch.cuda.synchronize()
+        assert (off.cpu().numpy().view(np.uint64) == want_off).all(), (name, c)
+        assert (colp.cpu().numpy().view(np.uint32) == want_col).all(), (name, c)
+
+
+@pytest.mark.parametrize("scale", [10, 13])
+def test_clean_input_counts(scale):
+    g = G.rmat(scale, 16, seed=scale + 5)
+    T, t = O.count(g.n, g.rowptr, g.col, per_vertex=True)
+    row, col = clean_csr(g)
+    for kw in [dict(clean=True, sorted_rows=True), dict(clean=True),
+               dict(clean=True, segsort_block_max=32)]:
+        c = shuffled_rows(g.n, row, col, scale) if not kw.get("sorted_rows") else col
+        for v in VARIANTS:
+            got, pv = gpu_count(row, c, per_vertex=True, force_variant=v, **kw)
+            assert got == T and (pv_np(pv) == t).all(), (kw, v)
+
+
+def test_host_pointer_path():
+    g = G.rmat(12, 16, seed=9)
+    T, t = O.count(g.n, g.rowptr, g.col, per_vertex=True)
+    got, pv, st = tc.count_ex(g.rowptr, g.col, per_vertex=True, with_stats=True)
+    assert got == T and (pv == t).all()
+    assert st["h2d_bytes"] == g.rowptr.nbytes + g.col.nbytes
+    assert st["d2h_bytes"] == 8 + 8 * g.n
+
+
+def test_stats_consistent():
+    g = G.rmat(12, 16, seed=4)
+    T, st_o = O.count(g.n, g.rowptr, g.col, with_stats=True)
+    got, st = gpu_count(g.rowptr, g.col, with_stats=True)
+    assert got == T
+    assert st["m_undirected"] == st_o["m"] and st["work_W"] == st_o["W"]
+    assert st["max_dplus"] == st_o["max_dplus"]
+    assert st["bytes_alg"] == 4 * st_o["W"] + 16 * st_o["m"]
+    assert sum(st["bin_edges"]) + st["skipped_edges"] == st_o["m"]
+    assert st["kernel_launches"] > 0
+
+
+# ------------------------------------------------------------------ multi-GPU partition (on one GPU)
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_shards_sum_to_total(world):
+    g = G.rmat(12, 16, seed=21)
+    T, t = O.count(g.n, g.rowptr, g.col, per_vertex=True)
+    rp, cl = on_dev(g.rowptr, g.col)
+    tot, pv_sum, parts = 0, torch.zeros(g.n, dtype=torch.int64, device=DEV), []
+    for r in range(world):
+        partial = torch.zeros(1, dtype=torch.int64, device=DEV)
+        pv = torch.zeros(g.n, dtype=torch.int64, device=DEV)
+        tc.count_shard(rp, cl, r, world, partial, per_vertex_partial=pv)
+        torch.cuda.synchronize()
+        parts.append(int(partial.item()))
+        pv_sum += pv
+    assert sum(parts) == T and (pv_np(pv_sum) == t).all()
+    assert sum(1 for p in parts if p > 0) >= min(world, 2)      # work really is split
+
+
+# ------------------------------------------------------------------ errors
+def test_validate_rejects_bad_graphs():
+    bad = [(np.array([0, 1, 2], np.uint64), np.array([1, 5], np.uint32)),     # id >= n
+           (np.array([0, 2, 1], np.uint64), np.array([1, 0], np.uint32))]     # non-monotone
+    for rp, cl in bad:
+        with pytest.raises(tc.TCError) as e:
+            gpu_count(rp, cl, validate=True)
+        assert e.value.status == 2
+    row, col = clean_csr(G.karate())
+    with pytest.raises(tc.TCError):   # TC_CLEAN claim on asymmetric input
+        gpu_count(np.array([0, 1, 1], np.uint64), np.array([1], np.uint32), clean=True,
+                  sorted_rows=True, validate=True)
+    assert gpu_count(row, col, clean=True, sorted_rows=True, validate=True) == 45
+
+
+# ------------------------------------------------------------------ full-size configurations
+def test_config_chung_lu_full():
+    g = G.chung_lu()
+    T = O.count(g.n, g.rowptr, g.col)
+    assert gpu_count(g.rowptr, g.col) == T
+
+
+def test_config_road_full():
+    g = G.road_mesh()
+    T, t = O.count(g.n, g.rowptr, g.col, per_vertex=True)
+    got, pv = gpu_count(g.rowptr, g.col, per_vertex=True)
+    assert got == T and (pv_np(pv) == t).all()
+
+
+def test_config_clique_union_full():
+    g = G.clique_union()
+    T = O.count(g.n, g.rowptr, g.col)
+    assert gpu_count(g.rowptr, g.col) == T
+
+
+def test_config_rmat21_full():
+    """BASELINE configs[1]: R-MAT s21 ef16, the bench workload, in the bench's launch config."""
+    g = G.rmat(21, 16)
+    T = O.count(g.n, g.rowptr, g.col)
+    got, pv = gpu_count(g.rowptr, g.col, per_vertex=True)
+    assert got == T
+    assert gpu_count(g.rowptr, g.col) == T
+    # sampled per-vertex counts by definition (edges among N(v))
+    row, col = clean_csr(g)
+    pvh = pv_np(pv)
+    rng = np.random.default_rng(0)
+    deg = np.diff(row)
+    sample = np.concatenate([rng.integers(0, g.n, 300), np.argsort(deg)[-20:]])
+    for v in sample:
+        assert int(pvh[v]) == O.vertex_triangles(g.n, row, col, int(v)), v
+    assert int(pvh.sum()) == 3 * T
+
+
+def test_large_closed_forms():
+    g = G.complete(3000)                       # T = C(3000,3) > 2^32: uint64 totals
+    assert gpu_count(g.rowptr, g.col) == math.comb(3000, 3)
+    g = G.kron_power(G.karate(), 3)
+    assert gpu_count(g.rowptr, g.col) == 3_280_500
+    g = G.triangulated_grid(1000, 1000)
+    assert gpu_count(g.rowptr, g.col) == 2 * 999 * 999
