@@ -41,7 +41,7 @@
  * stream-ordered (its device result is ready when the stream reaches it).
  *
  * ERRORS: every entry point validates its arguments (null pointers, n >= 2^32,
- * unknown flag bits, m >= 2^32 when cleaning) and returns TC_EINVAL before
+ * unknown flag bits, bad options) and returns TC_EINVAL before
  * touching the device.  With TC_VALIDATE the graph itself is checked on the
  * device (offsets, ids, and for TC_CLEAN: no self-loops, symmetry, and with
  * TC_SORTED strictly increasing rows) and a violation returns TC_EGRAPH.
@@ -89,14 +89,15 @@ enum {
     TC_VARIANT_MERGE = 1,  /* one warp per edge, merge-path split ("TwoLarge"/balanced path,
                               P:534-539)                                                      */
     TC_VARIANT_SEARCH = 2, /* short list binary-searched in the long one           */
-    TC_VARIANT_HASH = 3    /* CTA per source: N+(u) staged in a shared-memory hash, every
-                              N+(v), v in N+(u), streamed and probed (north_star hub kernel)  */
+    TC_VARIANT_HASH = 3    /* the shorter of N+(u), N+(v) probed into a shared-memory hash of
+                              the longer; edges grouped by the longer list's vertex (owner):
+                              a warp per small owner, a CTA per hub owner (north_star)        */
 };
 
 typedef struct {
-    uint32_t short_max;         /* edge -> SHORT bin if max(d+u, d+v) <= short_max            */
-    uint32_t skew_ratio;        /* edge -> SEARCH bin if max >= skew_ratio * min                */
-    uint32_t hub_min_dplus;     /* sources with d+(u) >= this -> HASH kernel (all their edges) */
+    uint32_t short_max;         /* AUTO: edge -> SHORT if max(d+u, d+v) <= short_max           */
+    uint32_t skew_ratio;        /* AUTO: edge -> SEARCH if max >= skew_ratio * min (0 = never)  */
+    uint32_t hub_min_dplus;     /* HASH owners with d+ >= this get a whole CTA (capped at 129)  */
     int32_t force_variant;      /* TC_VARIANT_AUTO, or route EVERY edge to one variant          */
     void *stream;               /* cudaStream_t to run on; NULL = legacy default stream         */
     uint32_t segsort_block_max; /* rows longer than this use the global segmented-sort path     */
@@ -113,11 +114,11 @@ typedef struct {
     double ms_total;     /* whole call, including host<->device copies with TC_HOST_PTRS   */
     uint64_t m_undirected;    /* simple undirected edges = |E+|                             */
     uint64_t work_W;          /* sum over E+ of d+(u) + d+(v)   (merge work)                */
-    uint64_t work_probe;      /* sum over E+ of d+(v)            (hash-probe work)          */
+    uint64_t work_probe;      /* sum over E+ of min(d+u, d+v)    (hash-probe work)          */
     uint64_t bytes_alg;       /* 4*W + 16*m: algorithmic bytes of the intersection (B_alg)  */
     uint64_t bin_edges[4];    /* edges routed to SHORT, MERGE, SEARCH, HASH                 */
     uint64_t skipped_edges;   /* edges that cannot close a triangle (d+(u) < 2 or d+(v) = 0) */
-    uint64_t hub_sources;     /* sources handled by the HASH kernel                         */
+    uint64_t hub_sources;     /* HASH owners handled by a whole CTA (d+ >= hub_min_dplus)   */
     uint64_t max_dplus;       /* max out-degree after orientation                           */
     uint64_t kernel_launches; /* kernels this call launched                                 */
     uint64_t h2d_bytes;       /* bytes copied host->device (TC_HOST_PTRS)                   */

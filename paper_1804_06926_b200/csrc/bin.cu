@@ -1,11 +1,17 @@
 // bin.cu -- a5: work estimation and binning (§4.2.2 P:527-542 "dynamic
 // grouping ... divide the edge lists into groups"; third kernel P:704-708).
 // Per oriented edge (u,v): a = min(d+u, d+v), b = max.  Edges that cannot close
-// a triangle (d+(u) < 2 or d+(v) = 0) are skipped.  Sources with
-// d+(u) >= hub_min go whole to the HASH kernel; other edges go to
-// SHORT (b <= short_max), SEARCH (b >= skew_ratio * a) or MERGE.
+// a triangle (d+(u) < 2 or d+(v) = 0) are skipped.  AUTO policy:
+//   b <= short_max            -> SHORT   (thread per edge)
+//   skew_ratio && b >= r * a  -> SEARCH  (binary search of the short list)
+//   otherwise                 -> HASH    (shorter list probed into a shared-memory
+//                                         hash of the longer one, grouped by owner)
+// force_variant routes every edge to one variant instead.
+// HASH edges are regrouped into an owner CSR (counting sort by owner with
+// atomics; order inside a group is irrelevant to the count).  Owners with
+// d+ >= hub_min (or too long for a warp table) go to the CTA kernel.
 // Multi-GPU: sources are split into `world` groups by an exclusive
-// prefix of per-source work w(u) = sum_{v in N+(u)} (d+u + d+v); a rank keeps
+// prefix of per-source work w(u) = sum_{v in N+(u)} (1 + min(d+u, d+v)); a rank keeps
 // only its group's edges.  The split needs no communication.
 #include "block_scan.cuh"
 #include "tc_internal.cuh"
@@ -35,7 +41,8 @@ __global__ void __launch_bounds__(kTileThreads)
     k_bin(const uint64_t *__restrict__ off, const uint32_t *__restrict__ col,
           const uint32_t *__restrict__ dplus, uint64_t n, const uint64_t *__restrict__ m_dev,
           BinParams p, uint2 *__restrict__ b_short, uint2 *__restrict__ b_merge,
-          uint2 *__restrict__ b_search, uint64_t *__restrict__ counts) {
+          uint2 *__restrict__ b_search, uint2 *__restrict__ b_hash, uint32_t *__restrict__ pcnt,
+          uint64_t *__restrict__ counts) {
     __shared__ uint32_t s_row[kTileItems];
     __shared__ uint32_t s_scan[kTileThreads / 32];
     __shared__ uint64_t s_red[kTileThreads / 32];
@@ -46,7 +53,7 @@ __global__ void __launch_bounds__(kTileThreads)
     tile_rows(off, n, t0, len, s_row, s_scan);
     uint64_t chunk = 0;
     if (p.world > 1) chunk = (p.work_prefix[n] + p.world - 1) / p.world;
-    uint64_t W = 0, probe = 0, skipped = 0, hashed = 0;
+    uint64_t W = 0, probe = 0, skipped = 0;
     // striped over the tile so each warp handles 32 consecutive edges per round
     for (uint32_t base = 0; base < kTileItems; base += kTileThreads) {
         uint32_t i = base + threadIdx.x;
@@ -58,68 +65,122 @@ __global__ void __launch_bounds__(kTileThreads)
             du = dplus[u];
             dv = dplus[v];
             W += du + dv;
-            probe += dv;
+            probe += min(du, dv);
         }
         int bin = -1;
+        uint2 item = make_uint2(u, v);
         if (valid && owner_of(p.work_prefix, chunk, u, p.world) == p.rank) {
+            uint32_t a = min(du, dv), b = max(du, dv);
             if (du < 2 || dv == 0) {
                 skipped++;
-            } else if (p.force == TC_VARIANT_HASH || (p.force < 0 && du >= p.hub_min)) {
-                hashed++;
             } else if (p.force >= 0) {
                 bin = p.force;
+            } else if (b <= p.short_max) {
+                bin = TC_VARIANT_SHORT;
+            } else if (p.skew_ratio && (uint64_t)b >= (uint64_t)p.skew_ratio * a) {
+                bin = TC_VARIANT_SEARCH;
             } else {
-                uint32_t a = min(du, dv), b = max(du, dv);
-                if (b <= p.short_max) bin = 0;
-                else if ((uint64_t)b >= (uint64_t)p.skew_ratio * a) bin = 2;
-                else bin = 1;
+                bin = TC_VARIANT_HASH;
+            }
+            if (bin == TC_VARIANT_HASH) {
+                if (dv > du) item = make_uint2(v, u);   // owner = longer list (ties: source)
+                atomicAdd(&pcnt[item.x], 1u);
             }
         }
-        uint2 item = make_uint2(u, v);
-        warp_append(bin == 0, &counts[0], b_short, item);
-        warp_append(bin == 1, &counts[1], b_merge, item);
-        warp_append(bin == 2, &counts[2], b_search, item);
+        warp_append(bin == TC_VARIANT_SHORT, &counts[0], b_short, item);
+        warp_append(bin == TC_VARIANT_MERGE, &counts[1], b_merge, item);
+        warp_append(bin == TC_VARIANT_SEARCH, &counts[2], b_search, item);
+        warp_append(bin == TC_VARIANT_HASH, &counts[3], b_hash, item);
     }
     W = block_sum_u64(W, s_red);
     probe = block_sum_u64(probe, s_red);
     skipped = block_sum_u64(skipped, s_red);
-    hashed = block_sum_u64(hashed, s_red);
     if (threadIdx.x == 0) {
         atomicAdd((unsigned long long *)&counts[4], (unsigned long long)W);
         atomicAdd((unsigned long long *)&counts[5], (unsigned long long)probe);
         atomicAdd((unsigned long long *)&counts[6], (unsigned long long)skipped);
-        atomicAdd((unsigned long long *)&counts[8], (unsigned long long)hashed);
     }
 }
 
-__global__ void k_hubs(const uint32_t *__restrict__ dplus, uint64_t n, BinParams p,
-                       uint32_t *__restrict__ hubs, uint64_t *__restrict__ counts) {
-    uint64_t chunk = 0;
-    if (p.world > 1) chunk = (p.work_prefix[n] + p.world - 1) / p.world;
+// Scatter HASH pairs into the owner CSR (poff = exclusive scan of pcnt).
+__global__ void k_group(const uint2 *__restrict__ b_hash, const uint64_t *__restrict__ counts,
+                        const uint64_t *__restrict__ poff, uint32_t *__restrict__ cursor,
+                        uint32_t *__restrict__ plist) {
+    uint64_t ne = counts[3];
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ne;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint2 e = b_hash[i];
+        plist[poff[e.x] + atomicAdd(&cursor[e.x], 1u)] = e.y;
+    }
+}
+
+// Owner lists (warp owners / CTA owners) and max d+.
+__global__ void k_owners(const uint32_t *__restrict__ dplus, const uint32_t *__restrict__ pcnt,
+                         uint64_t n, uint32_t cta_min, uint32_t *__restrict__ owners_warp,
+                         uint32_t *__restrict__ owners_cta, uint64_t *__restrict__ counts) {
     uint32_t local_max = 0;
     uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    uint64_t end = (n + 31) & ~31ull;  // keep whole warps in the loop for warp_append
+    uint64_t end = (n + 31) & ~31ull;  // whole warps stay in the loop (warp-aggregated appends)
+    int lane = threadIdx.x & 31;
     for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < end; u += stride) {
-        bool take = false;
+        bool w = false, c = false;
         if (u < n) {
             uint32_t du = dplus[u];
             local_max = max(local_max, du);
-            uint32_t thr = p.force == TC_VARIANT_HASH ? 2u : p.hub_min;
-            take = (p.force < 0 || p.force == TC_VARIANT_HASH) && du >= thr &&
-                   owner_of(p.work_prefix, chunk, (uint32_t)u, p.world) == p.rank;
+            if (pcnt[u]) {
+                c = du >= cta_min;
+                w = !c;
+            }
         }
-        uint32_t mask = __ballot_sync(0xffffffffu, take);
-        if (mask) {
-            int lane = threadIdx.x & 31, leader = __ffs(mask) - 1;
-            uint64_t base = 0;
-            if (lane == leader)
-                base = atomicAdd((unsigned long long *)&counts[3], (unsigned long long)__popc(mask));
-            base = __shfl_sync(0xffffffffu, base, leader);
-            if (take) hubs[base + __popc(mask & ((1u << lane) - 1u))] = (uint32_t)u;
-        }
+        uint32_t mw = __ballot_sync(0xffffffffu, w), mc = __ballot_sync(0xffffffffu, c);
+        uint64_t bw = 0, bc = 0;
+        if (lane == 0 && mw) bw = atomicAdd((unsigned long long *)&counts[8], (unsigned long long)__popc(mw));
+        if (lane == 0 && mc) bc = atomicAdd((unsigned long long *)&counts[9], (unsigned long long)__popc(mc));
+        bw = __shfl_sync(0xffffffffu, bw, 0);
+        bc = __shfl_sync(0xffffffffu, bc, 0);
+        uint32_t lt = (1u << lane) - 1u;
+        if (w) owners_warp[bw + __popc(mw & lt)] = (uint32_t)u;
+        if (c) owners_cta[bc + __popc(mc & lt)] = (uint32_t)u;
     }
     local_max = __reduce_max_sync(0xffffffffu, local_max);
-    if ((threadIdx.x & 31) == 0) atomicMax((unsigned long long *)&counts[7], (unsigned long long)local_max);
+    if (lane == 0) atomicMax((unsigned long long *)&counts[7], (unsigned long long)local_max);
+}
+
+// Tasks: owner i of `owners` (i < *ocount) gets ceil(pcnt / L) tasks.
+__global__ void k_task_count(const uint32_t *__restrict__ owners, const uint64_t *__restrict__ ocount,
+                             const uint32_t *__restrict__ pcnt, uint64_t n, uint32_t L,
+                             uint32_t *__restrict__ tcnt) {
+    uint64_t no = *ocount;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        tcnt[i] = i < no ? (pcnt[owners[i]] + L - 1) / L : 0u;
+}
+
+__global__ void k_task_expand(const uint32_t *__restrict__ owners, const uint64_t *__restrict__ ocount,
+                              const uint32_t *__restrict__ tcnt, const uint64_t *__restrict__ toff,
+                              uint2 *__restrict__ tasks) {
+    uint64_t no = *ocount;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < no;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t x = owners[i], c = tcnt[i];
+        uint64_t o = toff[i];
+        for (uint32_t k = 0; k < c; k++) tasks[o + k] = make_uint2(x, k);
+    }
+}
+
+static void make_tasks(Ctx &ctx, uint64_t n, uint64_t cap, const uint32_t *owners,
+                       const uint64_t *ocount, const uint32_t *pcnt, uint32_t L, uint2 *&tasks,
+                       uint64_t *&ntasks) {
+    uint32_t *tcnt = ctx.alloc<uint32_t>(n);
+    uint64_t *toff = ctx.alloc<uint64_t>(n + 1);
+    int grid = ctx.persistent_grid(4);
+    k_task_count<<<grid, 256, 0, ctx.stream>>>(owners, ocount, pcnt, n, L, tcnt);
+    TC_LAUNCHED(ctx);
+    scan_exclusive(ctx, tcnt, toff, n);
+    tasks = ctx.alloc<uint2>(cap / L + n + 1);
+    k_task_expand<<<grid, 256, 0, ctx.stream>>>(owners, ocount, tcnt, toff, tasks);
+    TC_LAUNCHED(ctx);
+    ntasks = toff + n;
 }
 
 void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
@@ -127,26 +188,47 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
     bins.cap = cap;
     bins.count = ctx.alloc<uint64_t>(16);
     TC_CUDA(cudaMemsetAsync(bins.count, 0, 16 * sizeof(uint64_t), ctx.stream));
-    for (int k = 0; k < 3; k++) bins.edges[k] = ctx.alloc<uint2>(cap);
-    bins.hubs = ctx.alloc<uint32_t>(g.n);
+    for (int k = 0; k < 4; k++) bins.edges[k] = ctx.alloc<uint2>(cap);
+    bins.pcnt = ctx.alloc<uint32_t>(g.n + 1);
+    uint32_t *cursor = ctx.alloc<uint32_t>(g.n + 1);
+    TC_CUDA(cudaMemsetAsync(bins.pcnt, 0, (g.n + 1) * sizeof(uint32_t), ctx.stream));
+    TC_CUDA(cudaMemsetAsync(cursor, 0, (g.n + 1) * sizeof(uint32_t), ctx.stream));
     uint32_t tiles = (uint32_t)((cap + kTileItems - 1) / kTileItems);
     if (tiles) {
         k_bin<<<tiles, kTileThreads, 0, ctx.stream>>>(g.off, g.col, g.dplus, g.n, g.m_dev, p,
                                                       bins.edges[0], bins.edges[1], bins.edges[2],
-                                                      bins.count);
+                                                      bins.edges[3], bins.pcnt, bins.count);
         TC_LAUNCHED(ctx);
     }
-    k_hubs<<<ctx.persistent_grid(4), 256, 0, ctx.stream>>>(g.dplus, g.n, p, bins.hubs, bins.count);
+    bins.poff = ctx.alloc<uint64_t>(g.n + 1);
+    scan_exclusive(ctx, bins.pcnt, bins.poff, g.n);
+    bins.plist = ctx.alloc<uint32_t>(cap);
+    k_group<<<ctx.persistent_grid(8), 256, 0, ctx.stream>>>(bins.edges[3], bins.count, bins.poff,
+                                                            cursor, bins.plist);
     TC_LAUNCHED(ctx);
+    bins.owners_warp = ctx.alloc<uint32_t>(g.n);
+    bins.owners_cta = ctx.alloc<uint32_t>(g.n);
+    uint32_t cta_min = p.hub_min < kWarpTableSlots / 4 + 1 ? p.hub_min : kWarpTableSlots / 4 + 1;
+    k_owners<<<ctx.persistent_grid(4), 256, 0, ctx.stream>>>(g.dplus, bins.pcnt, g.n, cta_min,
+                                                             bins.owners_warp, bins.owners_cta,
+                                                             bins.count);
+    TC_LAUNCHED(ctx);
+    make_tasks(ctx, g.n, cap, bins.owners_warp, bins.count + 8, bins.pcnt, kWarpTaskLists,
+               bins.tasks_warp, bins.ntasks_warp);
+    make_tasks(ctx, g.n, cap, bins.owners_cta, bins.count + 9, bins.pcnt, kCtaTaskLists,
+               bins.tasks_cta, bins.ntasks_cta);
 }
 
-// per-source work w(u) = sum_{v in N+(u)} (d+u + d+v), then exclusive prefix.
+// Per-source work estimate w(u) = sum_{v in N+(u)} (1 + min(d+u, d+v)) -- the
+// probe count of the HASH kernel plus one per edge -- then exclusive prefix.
 __global__ void k_work(const uint64_t *__restrict__ off, const uint32_t *__restrict__ col,
                        const uint32_t *__restrict__ dplus, uint64_t n, uint64_t *__restrict__ work) {
     for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
          u += (uint64_t)gridDim.x * blockDim.x) {
-        uint64_t b = off[u], e = off[u + 1], du = e - b, w = du * du;
-        for (uint64_t k = b; k < e; k++) w += dplus[col[k]];
+        uint64_t b = off[u], e = off[u + 1];
+        uint32_t du = (uint32_t)(e - b);
+        uint64_t w = 0;
+        for (uint64_t k = b; k < e; k++) w += 1 + min(du, dplus[col[k]]);
         work[u] = w;
     }
 }

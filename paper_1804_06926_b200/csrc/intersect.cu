@@ -12,8 +12,10 @@
 //   SEARCH lanes own elements of the shorter list and binary-search the longer
 //          one ("scan each node in the smaller list and search the larger list",
 //          P:706-707)
-//   HASH   one CTA per hub source u: N+(u) staged in a shared-memory open-
-//          addressing hash, every w in N+(v), v in N+(u), probed (north_star).
+//   HASH   per edge, the SHORTER list probed into a shared-memory hash of the
+//          longer one; edges grouped by the longer list's vertex ("owner"), one
+//          warp per small owner, one CTA per hub owner (north_star hub kernel).
+//          Cost: min(d+u, d+v) probes per edge instead of d+u + d+v merge steps.
 // Per-vertex mode (TC_PER_VERTEX): each match w of (u,v) adds 1 to t(u), t(v),
 // t(w).
 #include "block_scan.cuh"
@@ -168,114 +170,305 @@ __global__ void __launch_bounds__(kIxThreads)
 }
 
 // ------------------------------------------------------------------ HASH
-constexpr uint32_t kHashSlots = 4096;  // shared-memory table capacity (power of two)
-constexpr uint32_t kHashChunk = 2048;  // N+(u) elements per table build (load factor <= 1/2)
-constexpr uint32_t kVChunk = 1024;     // neighbour descriptors staged per round
+// Owner x's list N+(x) (the longer one of each of its edges) lives in a
+// shared-memory hash table (load factor <= 1/2, multiplicative hash, buckets of
+// 4 slots read with one 16-byte shared load, linear probing over buckets).
+// For each probe vertex y of x every element w of N+(y) is looked up; a hit is
+// the triangle {x, y, w}.
+// A task = (owner, up to L probe lists).  The task's list descriptors go to
+// shared memory (exclusive prefix of lengths, start - prefix, id), the items of
+// all its lists are flattened, and each warp takes an equal contiguous item
+// range.  In each 32-item window lane t finds its list from a bitmap of the list
+// starts inside the window (reduce-or + popc): no per-item search.
+constexpr uint32_t kHashSlots = 8192;  // CTA table capacity (power of two), 32 KB
+constexpr uint32_t kHashChunk = 2048;  // owner elements per table build (load factor <= 1/4)
+constexpr int kUnroll = 2;             // independent 32-quad windows per probe step
+constexpr int kHashWarps = kIxThreads / 32;
+
+// Explicit shared-memory accesses on 32-bit shared addresses (keeps the hot
+// loop free of generic-address conversions).
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
 
 __device__ __forceinline__ uint32_t hash_slot(uint32_t x, int bits) {
     return (x * 0x9E3779B1u) >> (32 - bits);
 }
 
+// Table of 2^bits slots (>= 4 * len: load factor <= 1/4) = 2^(bits-2) buckets of 4.
+__device__ __forceinline__ int table_bits(uint32_t len) {
+    int bits = 5;
+    while ((1u << bits) < 4 * len) bits++;
+    return bits;
+}
+
+// Build: `nthreads` cooperating threads (index `tid`) insert keys[0..len).  A key
+// goes to the first free slot of its home bucket or of the following buckets;
+// within a bucket slots fill in order, so a bucket with an EMPTY slot ends every
+// probe sequence that reaches it.
+__device__ __forceinline__ void table_insert(uint32_t *tab, int bits, const uint32_t *__restrict__ keys,
+                                             uint32_t len, uint32_t tid, uint32_t nthreads) {
+    uint32_t bmask = (1u << (bits - 2)) - 1u;
+    for (uint32_t k = tid; k < len; k += nthreads) {
+        uint32_t x = keys[k], b = hash_slot(x, bits - 2);
+        while (true) {
+            uint32_t *slot = tab + 4 * b;
+            if (atomicCAS(slot + 0, kEmpty, x) == kEmpty) break;
+            if (atomicCAS(slot + 1, kEmpty, x) == kEmpty) break;
+            if (atomicCAS(slot + 2, kEmpty, x) == kEmpty) break;
+            if (atomicCAS(slot + 3, kEmpty, x) == kEmpty) break;
+            b = (b + 1) & bmask;
+        }
+    }
+}
+
+// Rare slow path: w's home bucket was full and did not hold it.
+__device__ __noinline__ uint32_t table_contains_slow(uint32_t tab, uint32_t bmask, uint32_t b,
+                                                     uint32_t w) {
+    while (true) {
+        b = (b + 1) & bmask;
+        uint4 q = lds128(tab + 16 * b);
+        if (q.x == w || q.y == w || q.z == w || q.w == w) return 1u;
+        if (q.w == kEmpty) return 0u;
+    }
+}
+
+// 1 if w is in the table at shared address `tab`.
+__device__ __forceinline__ uint32_t table_contains(uint32_t tab, int bits, uint32_t w) {
+    uint32_t b = hash_slot(w, bits - 2);
+    uint4 q = lds128(tab + 16 * b);
+    bool hit = q.x == w || q.y == w || q.z == w || q.w == w;
+    if (hit || q.w == kEmpty) return hit;  // slots fill in order: a free last slot ends the search
+    return table_contains_slow(tab, (1u << (bits - 2)) - 1u, b, w);
+}
+
+// Keep a shared-memory base address in a register (stops the compiler from
+// re-deriving it from SR_CgaCtaId at every use).
+__device__ __forceinline__ uint32_t opaque(uint32_t v) {
+    asm volatile("mov.b32 %0, %0;" : "+r"(v));
+    return v;
+}
+
+// Probe-list descriptors in shared memory, in QUAD space: list i covers the
+// aligned 16-byte quads [qlo_i, qhi_i) of col+ that overlap its element range
+// [lo_i, hi_i).  s_pre[i] = exclusive prefix of quad counts (s_pre[nl] = total),
+// s_qb[i] = qlo_i - s_pre[i] (mod 2^32), s_rng[i] = (lo_i, hi_i).  All offsets
+// fit in 32 bits (the host routes graphs with >= 2^32 oriented edges away).
+struct QuadDesc {
+    uint32_t *pre, *qb, *vid;
+    uint2 *rng;
+};
+
+__device__ __forceinline__ void put_desc(const QuadDesc &d, uint32_t i, uint32_t lo, uint32_t hi,
+                                         uint32_t pre, uint32_t y, bool pv) {
+    d.pre[i] = pre;
+    d.qb[i] = (lo >> 2) - pre;
+    d.rng[i] = make_uint2(lo, hi);
+    if (pv) d.vid[i] = y;
+}
+
+__device__ __forceinline__ uint32_t quad_count(uint32_t lo, uint32_t hi) {
+    return ((hi + 3) >> 2) - (lo >> 2);
+}
+
+// The calling warp probes quads [ib, ie) of the flattened quad space: one aligned
+// uint4 load and four probes per lane per window.  In each 32-quad window lane t
+// finds its list from a bitmap of the list starts inside the window (reduce-or +
+// popc): no per-item search.  Returns the number of hits.
+template <bool PV>
+__device__ __forceinline__ uint64_t probe_quads(uint32_t tab, int bits, uint32_t absent,
+                                                const QuadDesc &d, uint32_t nl, uint32_t ib,
+                                                uint32_t ie,
+                                                const uint32_t *__restrict__ col,
+                                                uint64_t *__restrict__ pv) {
+    const int lane = threadIdx.x & 31;
+    uint32_t hits = 0;
+    if (ib >= ie) return 0;
+    uint32_t lo = 0, hi = nl;  // i0 = the list containing quad ib
+    while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (d.pre[mid] <= ib) lo = mid; else hi = mid;
+    }
+    uint32_t i0 = lo;
+    const uint32_t le_mask = (2u << lane) - 1u;
+    const uint4 *col4 = reinterpret_cast<const uint4 *>(col);
+    for (uint32_t wb = ib; wb < ie; wb += 32 * kUnroll) {
+        uint4 q[kUnroll];
+        uint2 r[kUnroll];
+        uint32_t e0[kUnroll], ly[kUnroll];
+#pragma unroll
+        for (int k = 0; k < kUnroll; k++) {
+            uint32_t wk = wb + 32 * k;
+            uint32_t j = i0 + 1 + lane;           // candidate list starts after list i0
+            uint32_t s = (j < nl ? d.pre[j] : 0xffffffffu) - wk;
+            uint32_t starts = __reduce_or_sync(0xffffffffu, s < 32 ? (1u << s) : 0u);
+            uint32_t li = i0 + __popc(starts & le_mask);
+            uint32_t t = wk + lane;
+            uint32_t qi = d.qb[li] + t;
+            r[k] = t < ie ? d.rng[li] : make_uint2(0u, 0u);
+            e0[k] = qi << 2;
+            ly[k] = PV ? d.vid[li] : 0u;
+            q[k] = t < ie ? __ldg(col4 + qi) : make_uint4(0u, 0u, 0u, 0u);
+            i0 = __shfl_sync(0xffffffffu, li, 31);  // list holding quad wk + 31
+        }
+#pragma unroll
+        for (int k = 0; k < kUnroll; k++) {
+            uint32_t e[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                // elements outside the list probe `absent` (the owner: never in its own N+)
+                uint32_t idx = e0[k] + c;
+                uint32_t key = (idx >= r[k].x && idx < r[k].y) ? e[c] : absent;
+                uint32_t h = table_contains(tab, bits, key);
+                hits += h;
+                if (PV && h) {
+                    atomicAdd((unsigned long long *)&pv[e[c]], 1ull);
+                    atomicAdd((unsigned long long *)&pv[ly[k]], 1ull);
+                }
+            }
+        }
+    }
+    return hits;
+}
+
+// Warp tasks: owners with d+(x) <= kWarpTableSlots/4 (table in the warp's smem slice).
 template <bool PV>
 __global__ void __launch_bounds__(kIxThreads)
-    k_hash(const uint32_t *__restrict__ hubs, const uint64_t *__restrict__ count,
-           const uint64_t *__restrict__ off, const uint32_t *__restrict__ col,
-           uint64_t *__restrict__ total, uint64_t *__restrict__ pv) {
-    __shared__ uint32_t s_table[kHashSlots];
-    __shared__ uint64_t s_vstart[kVChunk];
-    __shared__ uint32_t s_vid[kVChunk];
-    __shared__ uint32_t s_vpre[kVChunk + 1];
-    __shared__ uint32_t s_scan[kIxThreads / 32];
-    __shared__ unsigned long long s_uhits;
-    uint64_t nh = count[3];
+    k_hash_warp(const uint2 *__restrict__ tasks, const uint64_t *__restrict__ ntasks,
+                const uint64_t *__restrict__ off, const uint32_t *__restrict__ col,
+                const uint64_t *__restrict__ poff, const uint32_t *__restrict__ plist,
+                uint64_t *__restrict__ total, uint64_t *__restrict__ pv) {
+    constexpr uint32_t L = kWarpTaskLists;
+    __shared__ __align__(16) uint32_t s_tab[kHashWarps][kWarpTableSlots];
+    __shared__ uint32_t s_qb[kHashWarps][L];
+    __shared__ uint2 s_rng[kHashWarps][L];
+    __shared__ uint32_t s_pre[kHashWarps][L + 1];
+    __shared__ uint32_t s_vid[kHashWarps][PV ? L : 1];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const QuadDesc d{s_pre[wib], s_qb[wib], s_vid[wib], s_rng[wib]};
+    uint64_t nt = *ntasks;
+    uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    uint32_t *tab = s_tab[wib];
     uint64_t acc = 0;
-    for (uint64_t h = blockIdx.x; h < nh; h += gridDim.x) {
-        uint32_t u = hubs[h];
-        uint64_t ub = off[u];
-        uint32_t du = (uint32_t)(off[u + 1] - ub);
-        if (PV && threadIdx.x == 0) s_uhits = 0;
-        for (uint32_t c0 = 0; c0 < du; c0 += kHashChunk) {
-            uint32_t clen = min(kHashChunk, du - c0);
-            int bits = 6;
-            while ((1u << bits) < 2 * clen) bits++;
-            uint32_t tsize = 1u << bits;
-            for (uint32_t s = threadIdx.x; s < tsize; s += blockDim.x) s_table[s] = kEmpty;
-            __syncthreads();
-            for (uint32_t k = threadIdx.x; k < clen; k += blockDim.x) {
-                uint32_t x = col[ub + c0 + k], slot = hash_slot(x, bits);
-                while (atomicCAS(&s_table[slot], kEmpty, x) != kEmpty) slot = (slot + 1) & (tsize - 1);
-            }
-            __syncthreads();
-            for (uint32_t v0 = 0; v0 < du; v0 += kVChunk) {
-                uint32_t vlen = min(kVChunk, du - v0);
-                // stage descriptors of N+(v) for v = N+(u)[v0 .. v0+vlen) and scan lengths
-                uint32_t lens[kVChunk / kIxThreads], run = 0;
+    for (uint64_t i = gw; i < nt; i += nw) {
+        uint2 task = tasks[i];
+        uint32_t x = task.x;
+        uint64_t xb = off[x];
+        uint32_t dx = (uint32_t)(off[x + 1] - xb);
+        uint64_t p0 = poff[x] + (uint64_t)task.y * L;
+        uint32_t nl = (uint32_t)(min(poff[x + 1], p0 + L) - p0);
+        uint32_t run = 0;  // descriptors: lists lane, lane + 32 (prefix in list order)
 #pragma unroll
-                for (int q = 0; q < (int)(kVChunk / kIxThreads); q++) {
-                    uint32_t i = threadIdx.x * (kVChunk / kIxThreads) + q;
-                    uint32_t l = 0;
-                    if (i < vlen) {
-                        uint32_t v = col[ub + v0 + i];
-                        uint64_t s = off[v];
-                        l = (uint32_t)(off[v + 1] - s);
-                        s_vstart[i] = s;
-                        s_vid[i] = v;
-                    }
-                    lens[q] = run;
-                    run += l;
-                }
-                uint32_t items;
-                uint32_t pre = block_exclusive_scan<SumOp>(run, s_scan, &items);
-#pragma unroll
-                for (int q = 0; q < (int)(kVChunk / kIxThreads); q++) {
-                    uint32_t i = threadIdx.x * (kVChunk / kIxThreads) + q;
-                    if (i < vlen) s_vpre[i] = pre + lens[q];
-                }
-                if (threadIdx.x == 0) s_vpre[vlen] = items;
-                __syncthreads();
-                for (uint32_t t = threadIdx.x; t < items; t += blockDim.x) {
-                    // list index: largest i with s_vpre[i] <= t
-                    uint32_t lo = 0, hi = vlen;
-                    while (hi - lo > 1) {
-                        uint32_t mid = (lo + hi) >> 1;
-                        if (s_vpre[mid] <= t) lo = mid; else hi = mid;
-                    }
-                    uint32_t w = col[s_vstart[lo] + (t - s_vpre[lo])];
-                    uint32_t slot = hash_slot(w, bits);
-                    while (true) {
-                        uint32_t y = s_table[slot];
-                        if (y == w) {
-                            acc++;
-                            if (PV) {
-                                atomicAdd((unsigned long long *)&pv[w], 1ull);
-                                atomicAdd((unsigned long long *)&pv[s_vid[lo]], 1ull);
-                                atomicAdd(&s_uhits, 1ull);
-                            }
-                            break;
-                        }
-                        if (y == kEmpty) break;
-                        slot = (slot + 1) & (tsize - 1);
-                    }
-                }
-                __syncthreads();
+        for (uint32_t h = 0; h < L; h += 32) {
+            uint32_t li = h + lane, nq = 0, y = 0, lo = 0, hi = 0;
+            if (li < nl) {
+                y = plist[p0 + li];
+                lo = (uint32_t)off[y];
+                hi = (uint32_t)off[y + 1];
+                nq = quad_count(lo, hi);
             }
+            uint32_t inc = warp_inclusive_scan<SumOp>(nq);
+            if (li < nl) put_desc(d, li, lo, hi, run + inc - nq, y, PV);
+            run += __shfl_sync(0xffffffffu, inc, 31);
         }
+        if (lane == 0) d.pre[nl] = run;
+        int bits = table_bits(dx);
+        for (uint32_t s = lane; s < (1u << bits); s += 32) tab[s] = kEmpty;
+        __syncwarp();
+        table_insert(tab, bits, col + xb, dx, lane, 32);
+        __syncwarp();
+        uint64_t h = probe_quads<PV>(opaque(smem_addr(tab)), bits, x, d, nl, 0, run, col, pv);
         if (PV) {
-            __syncthreads();
-            if (threadIdx.x == 0 && s_uhits) atomicAdd((unsigned long long *)&pv[u], s_uhits);
-            __syncthreads();
+            uint64_t hw = warp_sum_u64(h);
+            if (lane == 0 && hw) atomicAdd((unsigned long long *)&pv[x], (unsigned long long)hw);
         }
+        acc += h;
+        __syncwarp();
     }
     flush_count(acc, total);
 }
 
-// ------------------------------------------------------------------ launch all
+// CTA tasks: large owners ("hubs"); the task's items are split evenly over the warps.
+template <bool PV>
+__global__ void __launch_bounds__(kIxThreads)
+    k_hash_cta(const uint2 *__restrict__ tasks, const uint64_t *__restrict__ ntasks,
+               const uint64_t *__restrict__ off, const uint32_t *__restrict__ col,
+               const uint64_t *__restrict__ poff, const uint32_t *__restrict__ plist,
+               uint64_t *__restrict__ total, uint64_t *__restrict__ pv) {
+    constexpr uint32_t L = kCtaTaskLists;
+    static_assert(L <= kIxThreads, "one descriptor per thread");
+    __shared__ __align__(16) uint32_t s_tab[kHashSlots];
+    __shared__ uint32_t s_qb[L];
+    __shared__ uint2 s_rng[L];
+    __shared__ uint32_t s_pre[L + 1];
+    __shared__ uint32_t s_vid[PV ? L : 1];
+    __shared__ uint32_t s_scan[kHashWarps];
+    const int wib = threadIdx.x >> 5;
+    const QuadDesc d{s_pre, s_qb, s_vid, s_rng};
+    uint64_t nt = *ntasks;
+    uint64_t acc = 0;
+    for (uint64_t i = blockIdx.x; i < nt; i += gridDim.x) {
+        uint2 task = tasks[i];
+        uint32_t x = task.x;
+        uint64_t xb = off[x];
+        uint32_t dx = (uint32_t)(off[x + 1] - xb);
+        uint64_t p0 = poff[x] + (uint64_t)task.y * L;
+        uint32_t nl = (uint32_t)(min(poff[x + 1], p0 + L) - p0);
+        uint32_t nq = 0, y = 0, lo = 0, hi = 0;
+        if (threadIdx.x < nl) {
+            y = plist[p0 + threadIdx.x];
+            lo = (uint32_t)off[y];
+            hi = (uint32_t)off[y + 1];
+            nq = quad_count(lo, hi);
+        }
+        uint32_t items;
+        uint32_t pre = block_exclusive_scan<SumOp>(nq, s_scan, &items);
+        if (threadIdx.x < nl) put_desc(d, threadIdx.x, lo, hi, pre, y, PV);
+        if (threadIdx.x == 0) d.pre[nl] = items;
+        uint32_t ib = (uint32_t)(((uint64_t)items * wib) / kHashWarps);
+        uint32_t ie = (uint32_t)(((uint64_t)items * (wib + 1)) / kHashWarps);
+        uint64_t h = 0;
+        for (uint32_t c0 = 0; c0 < dx; c0 += kHashChunk) {
+            uint32_t clen = min(kHashChunk, dx - c0);
+            int bits = table_bits(clen);
+            for (uint32_t s = threadIdx.x; s < (1u << bits); s += blockDim.x) s_tab[s] = kEmpty;
+            __syncthreads();
+            table_insert(s_tab, bits, col + xb + c0, clen, threadIdx.x, blockDim.x);
+            __syncthreads();
+            h += probe_quads<PV>(opaque(smem_addr(s_tab)), bits, x, d, nl, ib, ie, col, pv);
+            __syncthreads();
+        }
+        if (PV) {
+            uint64_t hw = warp_sum_u64(h);
+            if ((threadIdx.x & 31) == 0 && hw)
+                atomicAdd((unsigned long long *)&pv[x], (unsigned long long)hw);
+        }
+        acc += h;
+    }
+    flush_count(acc, total);
+}
+
 template <bool PV>
 static void launch_all(Ctx &ctx, const Oriented &g, const Bins &bins, uint64_t *total,
                        uint64_t *pv) {
     int grid = ctx.persistent_grid(8);
-    k_hash<PV><<<ctx.persistent_grid(4), kIxThreads, 0, ctx.stream>>>(bins.hubs, bins.count, g.off,
-                                                                       g.col, total, pv);
+    k_hash_cta<PV><<<ctx.persistent_grid(8), kIxThreads, 0, ctx.stream>>>(
+        bins.tasks_cta, bins.ntasks_cta, g.off, g.col, bins.poff, bins.plist, total, pv);
+    TC_LAUNCHED(ctx);
+    k_hash_warp<PV><<<grid, kIxThreads, 0, ctx.stream>>>(bins.tasks_warp, bins.ntasks_warp, g.off,
+                                                          g.col, bins.poff, bins.plist, total, pv);
     TC_LAUNCHED(ctx);
     k_merge<PV><<<grid, kIxThreads, 0, ctx.stream>>>(bins.edges[1], bins.count + 1, g.off, g.col,
                                                      total, pv);

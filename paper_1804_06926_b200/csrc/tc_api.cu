@@ -185,6 +185,9 @@ static void run(Call &c) {
             work_prefix(ctx, g, prefix);
             bp.work_prefix = prefix;
         }
+        // The HASH kernels index col+ with 32-bit offsets; beyond that size route to MERGE.
+        if (g.m_cap >= (1ull << 32) && (bp.force < 0 || bp.force == TC_VARIANT_HASH))
+            bp.force = TC_VARIANT_MERGE;
         Bins bins;
         bin_edges(ctx, g, bp, bins);
         if (tm) tm->end(kBin);
@@ -240,9 +243,9 @@ static void run(Call &c) {
         st.bin_edges[0] = pin[0];
         st.bin_edges[1] = pin[1];
         st.bin_edges[2] = pin[2];
-        st.bin_edges[3] = pin[8];
+        st.bin_edges[3] = pin[3];
         st.skipped_edges = pin[6];
-        st.hub_sources = pin[3];
+        st.hub_sources = pin[9];
         st.max_dplus = pin[7];
         st.kernel_launches = ctx.launches;
         *c.stats = st;
@@ -268,12 +271,7 @@ static tc_status guarded(Call &c) {
 static tc_options resolve(const tc_options *opt) {
     tc_options o;
     tc_default_options(&o);
-    if (opt) {
-        o = *opt;
-        if (!o.short_max) o.short_max = 32;
-        if (!o.skew_ratio) o.skew_ratio = 16;
-        if (!o.hub_min_dplus) o.hub_min_dplus = 128;
-    }
+    if (opt) o = *opt;  // taken as given: 0 disables the SHORT / SEARCH bins
     return o;
 }
 
@@ -286,9 +284,12 @@ extern "C" {
 void tc_default_options(tc_options *opt) {
     if (!opt) return;
     memset(opt, 0, sizeof(*opt));
-    opt->short_max = 32;
-    opt->skew_ratio = 16;
-    opt->hub_min_dplus = 128;
+    // AUTO defaults, measured on R-MAT s21: the HASH
+    // variant (cost min(d+u, d+v) per edge) beats SHORT / SEARCH / MERGE on every
+    // bin, so those bins are off unless enabled here or forced.
+    opt->short_max = 0;
+    opt->skew_ratio = 0;
+    opt->hub_min_dplus = 64;
     opt->force_variant = TC_VARIANT_AUTO;
     opt->stream = nullptr;
     opt->segsort_block_max = 8192;

@@ -217,14 +217,29 @@ void orient_clean(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, cons
 void segmented_sort(Ctx &ctx, uint64_t n, const uint64_t *off, uint32_t *col, uint64_t m_cap,
                     uint32_t block_max);
 
+// Edge bins (a5).  SHORT / MERGE / SEARCH hold (u, v) pairs.  HASH edges are
+// regrouped by "owner" = the endpoint with the LONGER list N+ (ties: the source):
+// the owner's N+ is staged in a shared-memory hash and the other endpoint's
+// (shorter) list is probed, so an edge costs min(d+u, d+v) probes.
 struct Bins {
-    uint2 *edges[3] = {nullptr, nullptr, nullptr};  // SHORT, MERGE, SEARCH: (u, v) pairs
-    uint64_t *count = nullptr;                       // device: [0..2] bin sizes, [3] hubs,
-                                                     // [4] W, [5] probe work, [6] skipped,
-                                                     // [7] max d+, [8] hash-bin edges
-    uint32_t *hubs = nullptr;                        // HASH sources
+    uint2 *edges[4] = {nullptr, nullptr, nullptr, nullptr};  // SHORT, MERGE, SEARCH, HASH(owner, probe)
+    uint64_t *count = nullptr;  // device: [0..3] bin sizes, [4] W, [5] sum min(d+u,d+v),
+                                // [6] skipped, [7] max d+, [8] warp owners, [9] CTA owners
+    uint32_t *pcnt = nullptr;   // per owner: number of probe lists (n)
+    uint64_t *poff = nullptr;   // owner CSR offsets (n+1)
+    uint32_t *plist = nullptr;  // probe vertices grouped by owner
+    uint32_t *owners_warp = nullptr;  // owners with d+ < hub_min: tables of one warp
+    uint32_t *owners_cta = nullptr;   // larger owners ("hubs"): tables of one CTA
+    // Tasks = (owner, k): the k-th block of kWarpTaskLists / kCtaTaskLists probe
+    // lists of an owner, so no warp / CTA is stuck with a hub's whole group.
+    uint2 *tasks_warp = nullptr, *tasks_cta = nullptr;
+    uint64_t *ntasks_warp = nullptr, *ntasks_cta = nullptr;  // device counters
     uint64_t cap = 0;
 };
+
+constexpr uint32_t kWarpTableSlots = 512;   // per-warp hash table (owner d+ <= 128, load <= 1/4)
+constexpr uint32_t kWarpTaskLists = 64;     // probe lists per warp task
+constexpr uint32_t kCtaTaskLists = 256;     // probe lists per CTA task
 
 struct BinParams {
     uint32_t short_max, skew_ratio, hub_min;
