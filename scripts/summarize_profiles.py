@@ -16,7 +16,8 @@ ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Met
 per = []
 for r in rows[start:]:
     v = float(r[vi].replace(",", ""))
-    v *= {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}[r[ui]]
+    v *= {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0,
+          "second": 1e3, "s": 1e3}[r[ui]]
     per.append((r[ki].split("(")[0].replace("void ", ""), v))
 agg = {}
 for k, v in per:
