@@ -1,0 +1,77 @@
+"""World-size-2 CPU (gloo) test of the multi-GPU driver's host logic (dist.py):
+process-group plumbing, the int64 allreduce of partial counts, and the per-vertex
+allreduce.  The per-rank shard here is a CPU stand-in -- the oracle counting one
+connected component of a disjoint union per rank -- because no GPU is present; the CUDA
+partition itself is covered by tests/test_gpu_parity.py::test_shards_sum_to_total."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _parts():
+    import graphgen as G
+    return [G.karate(), G.rmat(9, 16, seed=3)]
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import graphgen as G
+        import oracle as O
+        from paper_1804_06926_b200.dist import count_distributed
+
+        parts = _parts()
+        g = G.disjoint_union(*parts)
+        offsets = np.cumsum([0] + [p.n for p in parts])
+
+        def shard_fn(rowptr, col, r, w, partial, per_vertex_partial=None, **kw):
+            assert (r, w) == (rank, world)
+            p = parts[r]
+            T, t = O.count(p.n, p.rowptr, p.col, per_vertex=True)
+            partial.fill_(T)
+            if per_vertex_partial is not None:
+                per_vertex_partial.zero_()
+                per_vertex_partial[offsets[r]:offsets[r + 1]] = torch.from_numpy(t.astype(np.int64))
+
+        rp = torch.from_numpy(g.rowptr.view(np.int64))
+        cl = torch.from_numpy(g.col.view(np.int32))
+        T = count_distributed(rp, cl, shard_fn=shard_fn)
+        T2, pv = count_distributed(rp, cl, shard_fn=shard_fn, per_vertex=True)
+        q.put((rank, T, T2, pv.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_allreduce_wiring_world2():
+    import graphgen as G
+    import oracle as O
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = G.disjoint_union(*_parts())
+    T, t = O.count(g.n, g.rowptr, g.col, per_vertex=True)
+    for rank, T1, T2, pv in res:
+        assert T1 == T and T2 == T
+        assert (pv.astype(np.uint64) == t).all()
