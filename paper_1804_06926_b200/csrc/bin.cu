@@ -114,33 +114,34 @@ __global__ void k_group(const uint2 *__restrict__ b_hash, const uint64_t *__rest
     }
 }
 
-// Owner lists (warp owners / CTA owners) and max d+.
+// Owner lists and max d+: warp owners (d+ < cta_min), CTA bitmap owners (rank span
+// n-1-x <= kCtaBitmapBits) and CTA hash owners (the rest).
 __global__ void k_owners(const uint32_t *__restrict__ dplus, const uint32_t *__restrict__ pcnt,
                          uint64_t n, uint32_t cta_min, uint32_t *__restrict__ owners_warp,
-                         uint32_t *__restrict__ owners_cta, uint64_t *__restrict__ counts) {
+                         uint32_t *__restrict__ owners_cta, uint32_t *__restrict__ owners_bitmap,
+                         uint64_t *__restrict__ counts) {
     uint32_t local_max = 0;
     uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     uint64_t end = (n + 31) & ~31ull;  // whole warps stay in the loop (warp-aggregated appends)
     int lane = threadIdx.x & 31;
+    uint32_t lt = (1u << lane) - 1u;
     for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < end; u += stride) {
-        bool w = false, c = false;
+        int kind = -1;
         if (u < n) {
             uint32_t du = dplus[u];
             local_max = max(local_max, du);
-            if (pcnt[u]) {
-                c = du >= cta_min;
-                w = !c;
-            }
+            if (pcnt[u]) kind = du < cta_min ? 0 : (n - 1 - u <= kCtaBitmapBits ? 2 : 1);
         }
-        uint32_t mw = __ballot_sync(0xffffffffu, w), mc = __ballot_sync(0xffffffffu, c);
-        uint64_t bw = 0, bc = 0;
-        if (lane == 0 && mw) bw = atomicAdd((unsigned long long *)&counts[8], (unsigned long long)__popc(mw));
-        if (lane == 0 && mc) bc = atomicAdd((unsigned long long *)&counts[9], (unsigned long long)__popc(mc));
-        bw = __shfl_sync(0xffffffffu, bw, 0);
-        bc = __shfl_sync(0xffffffffu, bc, 0);
-        uint32_t lt = (1u << lane) - 1u;
-        if (w) owners_warp[bw + __popc(mw & lt)] = (uint32_t)u;
-        if (c) owners_cta[bc + __popc(mc & lt)] = (uint32_t)u;
+        uint32_t *dst[3] = {owners_warp, owners_cta, owners_bitmap};
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+            uint32_t mk = __ballot_sync(0xffffffffu, kind == k);
+            uint64_t base = 0;
+            if (lane == 0 && mk)
+                base = atomicAdd((unsigned long long *)&counts[8 + k], (unsigned long long)__popc(mk));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (kind == k) dst[k][base + __popc(mk & lt)] = (uint32_t)u;
+        }
     }
     local_max = __reduce_max_sync(0xffffffffu, local_max);
     if (lane == 0) atomicMax((unsigned long long *)&counts[7], (unsigned long long)local_max);
@@ -208,15 +209,18 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
     TC_LAUNCHED(ctx);
     bins.owners_warp = ctx.alloc<uint32_t>(g.n);
     bins.owners_cta = ctx.alloc<uint32_t>(g.n);
+    bins.owners_bitmap = ctx.alloc<uint32_t>(g.n);
     uint32_t cta_min = p.hub_min < kWarpTableSlots / 4 + 1 ? p.hub_min : kWarpTableSlots / 4 + 1;
     k_owners<<<ctx.persistent_grid(4), 256, 0, ctx.stream>>>(g.dplus, bins.pcnt, g.n, cta_min,
                                                              bins.owners_warp, bins.owners_cta,
-                                                             bins.count);
+                                                             bins.owners_bitmap, bins.count);
     TC_LAUNCHED(ctx);
     make_tasks(ctx, g.n, cap, bins.owners_warp, bins.count + 8, bins.pcnt, kWarpTaskLists,
                bins.tasks_warp, bins.ntasks_warp);
     make_tasks(ctx, g.n, cap, bins.owners_cta, bins.count + 9, bins.pcnt, kCtaTaskLists,
                bins.tasks_cta, bins.ntasks_cta);
+    make_tasks(ctx, g.n, cap, bins.owners_bitmap, bins.count + 10, bins.pcnt, kCtaTaskLists,
+               bins.tasks_bitmap, bins.ntasks_bitmap);
 }
 
 // Per-source work estimate w(u) = sum_{v in N+(u)} (1 + min(d+u, d+v)) -- the

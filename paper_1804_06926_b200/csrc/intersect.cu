@@ -260,6 +260,21 @@ __device__ __forceinline__ uint32_t opaque(uint32_t v) {
     return v;
 }
 
+// Membership tests used by probe_quads.
+struct HashProbe {  // bucket hash of the owner's N+ (any id range)
+    uint32_t tab;
+    int bits;
+    __device__ __forceinline__ uint32_t operator()(uint32_t w) const { return table_contains(tab, bits, w); }
+};
+struct BitProbe {   // bitmap over the rank-id range [base, base + span) of the owner's N+
+    uint32_t bm, base, span;
+    __device__ __forceinline__ uint32_t operator()(uint32_t w) const {
+        uint32_t o = w - base;
+        uint32_t word = lds32(bm + 4 * (min(o, span - 1) >> 5));  // clamped: no branch
+        return (uint32_t)(o < span) & (word >> (o & 31));
+    }
+};
+
 // Probe-list descriptors in shared memory, in QUAD space: list i covers the
 // aligned 16-byte quads [qlo_i, qhi_i) of col+ that overlap its element range
 // [lo_i, hi_i).  s_pre[i] = exclusive prefix of quad counts (s_pre[nl] = total),
@@ -286,8 +301,8 @@ __device__ __forceinline__ uint32_t quad_count(uint32_t lo, uint32_t hi) {
 // uint4 load and four probes per lane per window.  In each 32-quad window lane t
 // finds its list from a bitmap of the list starts inside the window (reduce-or +
 // popc): no per-item search.  Returns the number of hits.
-template <bool PV>
-__device__ __forceinline__ uint64_t probe_quads(uint32_t tab, int bits, uint32_t absent,
+template <bool PV, class Probe>
+__device__ __forceinline__ uint64_t probe_quads(const Probe &contains, uint32_t absent,
                                                 const QuadDesc &d, uint32_t nl, uint32_t ib,
                                                 uint32_t ie,
                                                 const uint32_t *__restrict__ col,
@@ -330,7 +345,7 @@ __device__ __forceinline__ uint64_t probe_quads(uint32_t tab, int bits, uint32_t
                 // elements outside the list probe `absent` (the owner: never in its own N+)
                 uint32_t idx = e0[k] + c;
                 uint32_t key = (idx >= r[k].x && idx < r[k].y) ? e[c] : absent;
-                uint32_t h = table_contains(tab, bits, key);
+                uint32_t h = contains(key);
                 hits += h;
                 if (PV && h) {
                     atomicAdd((unsigned long long *)&pv[e[c]], 1ull);
@@ -389,7 +404,7 @@ __global__ void __launch_bounds__(kIxThreads)
         __syncwarp();
         table_insert(tab, bits, col + xb, dx, lane, 32);
         __syncwarp();
-        uint64_t h = probe_quads<PV>(opaque(smem_addr(tab)), bits, x, d, nl, 0, run, col, pv);
+        uint64_t h = probe_quads<PV>(HashProbe{opaque(smem_addr(tab)), bits}, x, d, nl, 0, run, col, pv);
         if (PV) {
             uint64_t hw = warp_sum_u64(h);
             if (lane == 0 && hw) atomicAdd((unsigned long long *)&pv[x], (unsigned long long)hw);
@@ -401,15 +416,19 @@ __global__ void __launch_bounds__(kIxThreads)
 }
 
 // CTA tasks: large owners ("hubs"); the task's items are split evenly over the warps.
-template <bool PV>
+// kBitmap: the owner's N+ (rank ids in (x, n)) is a bitmap over [x+1, n) -- one
+// 32-bit shared load per probe; otherwise the bucket hash (chunked if d+ > 2048).
+constexpr uint32_t kSmemWords = kHashSlots;            // 32 KB of table / bitmap per CTA
+static_assert(kCtaBitmapBits == kSmemWords * 32, "bitmap owners are classified in bin.cu");
+template <bool PV, bool kBitmap>
 __global__ void __launch_bounds__(kIxThreads)
     k_hash_cta(const uint2 *__restrict__ tasks, const uint64_t *__restrict__ ntasks,
                const uint64_t *__restrict__ off, const uint32_t *__restrict__ col,
-               const uint64_t *__restrict__ poff, const uint32_t *__restrict__ plist,
+               const uint64_t *__restrict__ poff, const uint32_t *__restrict__ plist, uint32_t n,
                uint64_t *__restrict__ total, uint64_t *__restrict__ pv) {
     constexpr uint32_t L = kCtaTaskLists;
     static_assert(L <= kIxThreads, "one descriptor per thread");
-    __shared__ __align__(16) uint32_t s_tab[kHashSlots];
+    __shared__ __align__(16) uint32_t s_tab[kSmemWords];
     __shared__ uint32_t s_qb[L];
     __shared__ uint2 s_rng[L];
     __shared__ uint32_t s_pre[L + 1];
@@ -417,6 +436,7 @@ __global__ void __launch_bounds__(kIxThreads)
     __shared__ uint32_t s_scan[kHashWarps];
     const int wib = threadIdx.x >> 5;
     const QuadDesc d{s_pre, s_qb, s_vid, s_rng};
+    const uint32_t tab = opaque(smem_addr(s_tab));
     uint64_t nt = *ntasks;
     uint64_t acc = 0;
     for (uint64_t i = blockIdx.x; i < nt; i += gridDim.x) {
@@ -440,15 +460,28 @@ __global__ void __launch_bounds__(kIxThreads)
         uint32_t ib = (uint32_t)(((uint64_t)items * wib) / kHashWarps);
         uint32_t ie = (uint32_t)(((uint64_t)items * (wib + 1)) / kHashWarps);
         uint64_t h = 0;
-        for (uint32_t c0 = 0; c0 < dx; c0 += kHashChunk) {
-            uint32_t clen = min(kHashChunk, dx - c0);
-            int bits = table_bits(clen);
-            for (uint32_t s = threadIdx.x; s < (1u << bits); s += blockDim.x) s_tab[s] = kEmpty;
+        if (kBitmap) {
+            const uint32_t base = x + 1, span = n - 1 - x;   // N+(x) lies in (x, n)
+            for (uint32_t w = threadIdx.x; w < (span + 31) / 32; w += blockDim.x) s_tab[w] = 0u;
             __syncthreads();
-            table_insert(s_tab, bits, col + xb + c0, clen, threadIdx.x, blockDim.x);
+            for (uint32_t k = threadIdx.x; k < dx; k += blockDim.x) {
+                uint32_t o = col[xb + k] - base;
+                atomicOr(&s_tab[o >> 5], 1u << (o & 31));
+            }
             __syncthreads();
-            h += probe_quads<PV>(opaque(smem_addr(s_tab)), bits, x, d, nl, ib, ie, col, pv);
+            h = probe_quads<PV>(BitProbe{tab, base, span}, x, d, nl, ib, ie, col, pv);
             __syncthreads();
+        } else {
+            for (uint32_t c0 = 0; c0 < dx; c0 += kHashChunk) {
+                uint32_t clen = min(kHashChunk, dx - c0);
+                int bits = table_bits(clen);
+                for (uint32_t s = threadIdx.x; s < (1u << bits); s += blockDim.x) s_tab[s] = kEmpty;
+                __syncthreads();
+                table_insert(s_tab, bits, col + xb + c0, clen, threadIdx.x, blockDim.x);
+                __syncthreads();
+                h += probe_quads<PV>(HashProbe{tab, bits}, x, d, nl, ib, ie, col, pv);
+                __syncthreads();
+            }
         }
         if (PV) {
             uint64_t hw = warp_sum_u64(h);
@@ -464,8 +497,12 @@ template <bool PV>
 static void launch_all(Ctx &ctx, const Oriented &g, const Bins &bins, uint64_t *total,
                        uint64_t *pv) {
     int grid = ctx.persistent_grid(8);
-    k_hash_cta<PV><<<ctx.persistent_grid(8), kIxThreads, 0, ctx.stream>>>(
-        bins.tasks_cta, bins.ntasks_cta, g.off, g.col, bins.poff, bins.plist, total, pv);
+    uint32_t n = (uint32_t)g.n;
+    k_hash_cta<PV, true><<<ctx.persistent_grid(6), kIxThreads, 0, ctx.stream>>>(
+        bins.tasks_bitmap, bins.ntasks_bitmap, g.off, g.col, bins.poff, bins.plist, n, total, pv);
+    TC_LAUNCHED(ctx);
+    k_hash_cta<PV, false><<<ctx.persistent_grid(6), kIxThreads, 0, ctx.stream>>>(
+        bins.tasks_cta, bins.ntasks_cta, g.off, g.col, bins.poff, bins.plist, n, total, pv);
     TC_LAUNCHED(ctx);
     k_hash_warp<PV><<<grid, kIxThreads, 0, ctx.stream>>>(bins.tasks_warp, bins.ntasks_warp, g.off,
                                                           g.col, bins.poff, bins.plist, total, pv);

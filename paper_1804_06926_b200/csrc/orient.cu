@@ -1,4 +1,4 @@
-// orient.cu -- steps a1-a3 of the hot path:
+// orient.cu -- steps a1-a4 of the hot path:
 //   a1 clean: arcs -> 64-bit undirected keys (min << b | max), radix sort,
 //      unique (Table 1 caption P:604-606: "treated as undirected ... de-duplicate");
 //   a2 degree d(v) of the cleaned graph;
@@ -6,11 +6,13 @@
 //      P:336-343; Advance + Filter + segmented reduction, §4.2.1):
 //      keep (u,v) iff rank(u) < rank(v), rank = (d, id), ties by smaller id
 //      (P:521-522); direction low -> high rank (DESIGN reading R2).
-// Dirty input: the unique pair list is sorted by (a, b); a STABLE radix sort of
-// the oriented pairs by source then yields every N+(u) ascending (the a4 sort
-// is subsumed: N+(x) = [a < x in increasing order] ++ [b > x in increasing order]).
-// Clean input: the compaction is stable, so rows stay sorted iff the input rows
-// were; otherwise a4 (segmented_sort) runs.
+// Vertices are RELABELLED by rank: a stable radix sort of (d, id) gives
+// order[i] = the vertex of rank position i and newid[order[i]] = i, so
+// rank(u) < rank(v) <=> newid[u] < newid[v].  The oriented CSR is built in the
+// new id space (sources by a stable radix sort of the oriented pairs), so a
+// hub's N+ lies in the short id range above it (bitmap staging in a6) and the
+// hot lists are contiguous at the end of col+.  Rows are put in ascending order
+// (a4, segmented sort) only when a merge/search variant needs them.
 #include "block_scan.cuh"
 #include "tc_internal.cuh"
 
@@ -100,23 +102,76 @@ __global__ void k_deg_pairs(const uint64_t *__restrict__ E, const uint64_t *__re
 }
 
 __global__ void k_orient_pairs(const uint64_t *__restrict__ E, const uint64_t *__restrict__ m_dev,
-                               int b, const uint32_t *__restrict__ deg, uint32_t *__restrict__ okey,
+                               int b, const uint32_t *__restrict__ newid, uint32_t *__restrict__ okey,
                                uint32_t *__restrict__ oval, uint32_t *__restrict__ dplus) {
     uint64_t m = *m_dev, mask = (1ull << b) - 1;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
          i += (uint64_t)gridDim.x * blockDim.x) {
         uint64_t k = E[i];
-        uint32_t a = (uint32_t)(k >> b), c = (uint32_t)(k & mask);
-        bool fwd = rank_less(deg, a, c);
-        uint32_t s = fwd ? a : c, d = fwd ? c : a;
+        uint32_t a = newid[k >> b], c = newid[k & mask];
+        uint32_t s = min(a, c), d = max(a, c);   // low -> high rank
         okey[i] = s;
         oval[i] = d;
         atomicAdd(&dplus[s], 1u);
     }
 }
 
+// ------------------------------------------------------------------ rank relabelling
+__global__ void k_iota(uint32_t *__restrict__ a, uint64_t n) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        a[i] = (uint32_t)i;
+}
+
+__global__ void k_newid(const uint32_t *__restrict__ order, uint64_t n, uint32_t *__restrict__ newid) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        newid[order[i]] = (uint32_t)i;
+}
+
+// order[i] = vertex with the i-th smallest (d, id); newid = inverse.  `deg` is clobbered.
+static void rank_permutation(Ctx &ctx, uint64_t n, uint32_t *deg, Oriented &out) {
+    int b = id_bits(n);
+    int grid = ctx.persistent_grid(8);
+    uint32_t *ids = ctx.alloc<uint32_t>(n), *ids2 = ctx.alloc<uint32_t>(n);
+    uint32_t *deg2 = ctx.alloc<uint32_t>(n);
+    k_iota<<<grid, 256, 0, ctx.stream>>>(ids, n);
+    TC_LAUNCHED(ctx);
+    // stable sort by degree (< n <= 2^b); ids enter ascending, so ties stay ordered by id
+    bool alt = radix_sort_pairs(ctx, deg, deg2, ids, ids2, n, nullptr, b);
+    out.order = alt ? ids2 : ids;
+    out.newid = ctx.alloc<uint32_t>(n);
+    k_newid<<<grid, 256, 0, ctx.stream>>>(out.order, n, out.newid);
+    TC_LAUNCHED(ctx);
+}
+
+// Oriented pairs (okey = source, oval = target, new ids; m_dev of them) -> CSR by a
+// stable radix sort on the source; dplus already counted.
+static void pairs_to_csr(Ctx &ctx, uint64_t n, uint64_t cap, uint32_t *okey, uint32_t *oval,
+                         uint32_t *dplus, uint64_t *m_dev, bool need_sorted,
+                         uint32_t segsort_block_max, Oriented &out, Timer *tm) {
+    int b = id_bits(n);
+    uint32_t *okey2 = ctx.alloc<uint32_t>(cap), *oval2 = ctx.alloc<uint32_t>(cap);
+    bool alt = radix_sort_pairs(ctx, okey, okey2, oval, oval2, cap, m_dev, b);
+    uint64_t *off = ctx.alloc<uint64_t>(n + 1);
+    scan_exclusive(ctx, dplus, off, n);
+    out.n = n;
+    out.off = off;
+    out.col = alt ? oval2 : oval;
+    out.dplus = dplus;
+    out.m_dev = m_dev;
+    out.m_cap = cap;
+    out.rows_sorted = need_sorted;
+    if (tm) tm->end(kOrient);
+    if (need_sorted) {
+        if (tm) tm->begin(kSort);
+        segmented_sort(ctx, n, off, out.col, cap, segsort_block_max);
+        if (tm) tm->end(kSort);
+    }
+}
+
 void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
-                  Oriented &out, Timer *tm) {
+                  bool need_sorted, uint32_t segsort_block_max, Oriented &out, Timer *tm) {
     int b = id_bits(n);
     uint32_t tiles = (uint32_t)((M + kTileItems - 1) / kTileItems);
     if (tm) tm->begin(kClean);
@@ -144,20 +199,11 @@ void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, cons
     int grid = ctx.persistent_grid(8);
     k_deg_pairs<<<grid, 256, 0, ctx.stream>>>(E, m_dev, b, deg);
     TC_LAUNCHED(ctx);
+    rank_permutation(ctx, n, deg, out);
     uint32_t *okey = ctx.alloc<uint32_t>(M), *oval = ctx.alloc<uint32_t>(M);
-    uint32_t *okey2 = ctx.alloc<uint32_t>(M), *oval2 = ctx.alloc<uint32_t>(M);
-    k_orient_pairs<<<grid, 256, 0, ctx.stream>>>(E, m_dev, b, deg, okey, oval, dplus);
+    k_orient_pairs<<<grid, 256, 0, ctx.stream>>>(E, m_dev, b, out.newid, okey, oval, dplus);
     TC_LAUNCHED(ctx);
-    bool alt2 = radix_sort_pairs(ctx, okey, okey2, oval, oval2, M, m_dev, b);
-    uint64_t *off = ctx.alloc<uint64_t>(n + 1);
-    scan_exclusive(ctx, dplus, off, n);
-    if (tm) tm->end(kOrient);
-    out.n = n;
-    out.off = off;
-    out.col = alt2 ? oval2 : oval;
-    out.dplus = dplus;
-    out.m_dev = m_dev;
-    out.m_cap = M;
+    pairs_to_csr(ctx, n, M, okey, oval, dplus, m_dev, need_sorted, segsort_block_max, out, tm);
 }
 
 // ------------------------------------------------------------------ clean input
@@ -186,14 +232,13 @@ __global__ void __launch_bounds__(kTileThreads)
 }
 
 __global__ void __launch_bounds__(kTileThreads)
-    k_orient_scatter(const uint64_t *__restrict__ rowptr, const uint32_t *__restrict__ col,
-                     uint64_t n, uint64_t M, const uint32_t *__restrict__ deg,
-                     const uint64_t *__restrict__ offs, uint32_t *__restrict__ col_plus,
-                     uint64_t *__restrict__ off_plus) {
+    k_orient_emit(const uint64_t *__restrict__ rowptr, const uint32_t *__restrict__ col,
+                  uint64_t n, uint64_t M, const uint32_t *__restrict__ deg,
+                  const uint32_t *__restrict__ newid, const uint64_t *__restrict__ offs,
+                  uint32_t *__restrict__ okey, uint32_t *__restrict__ oval,
+                  uint32_t *__restrict__ dplus) {
     __shared__ uint32_t s_row[kTileItems];
-    __shared__ uint32_t s_excl[kTileItems];
     __shared__ uint32_t s_scan[kTileThreads / 32];
-    __shared__ uint64_t s_bounds[2];
     uint64_t t0 = (uint64_t)blockIdx.x * kTileItems;
     uint32_t len = (uint32_t)min((uint64_t)kTileItems, M - t0);
     tile_rows(rowptr, n, t0, len, s_row, s_scan);
@@ -207,73 +252,98 @@ __global__ void __launch_bounds__(kTileThreads)
         c += f[k];
     }
     uint32_t pos = block_exclusive_scan<SumOp>(c, s_scan);
-    uint64_t base = offs[blockIdx.x];
+    uint64_t base = offs[blockIdx.x] + pos;
 #pragma unroll
     for (int k = 0; k < kItemsPerThread; k++) {
-        s_excl[i0 + k] = pos;
-        if (f[k]) col_plus[base + pos] = v[k];
-        pos += f[k];
+        if (f[k]) {
+            uint32_t s = newid[s_row[i0 + k]];
+            okey[base] = s;
+            oval[base] = newid[v[k]];
+            atomicAdd(&dplus[s], 1u);
+            base++;
+        }
     }
-    if (threadIdx.x == 0) {
-        s_bounds[0] = lower_bound_u64(rowptr, n + 1, t0);
-        s_bounds[1] = lower_bound_u64(rowptr, n + 1, t0 + len);
-    }
-    __syncthreads();
-    for (uint64_t u = s_bounds[0] + threadIdx.x; u < s_bounds[1]; u += kTileThreads)
-        off_plus[u] = base + s_excl[rowptr[u] - t0];
-}
-
-// Rows starting at M (trailing empty rows, and u = n) get off+ = m.
-__global__ void k_orient_tail(const uint64_t *__restrict__ rowptr, uint64_t n, uint64_t M,
-                              const uint64_t *__restrict__ m_dev, uint64_t *__restrict__ off_plus) {
-    uint64_t m = *m_dev;
-    for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u <= n;
-         u += (uint64_t)gridDim.x * blockDim.x)
-        if (rowptr[u] >= M) off_plus[u] = m;
-}
-
-__global__ void k_dplus(const uint64_t *__restrict__ off, uint64_t n, uint32_t *__restrict__ dplus) {
-    for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
-         u += (uint64_t)gridDim.x * blockDim.x)
-        dplus[u] = (uint32_t)(off[u + 1] - off[u]);
 }
 
 void orient_clean(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
-                  bool sorted, uint32_t segsort_block_max, Oriented &out, Timer *tm) {
+                  bool need_sorted, uint32_t segsort_block_max, Oriented &out, Timer *tm) {
     uint32_t tiles = (uint32_t)((M + kTileItems - 1) / kTileItems);
     int grid = ctx.persistent_grid(8);
     if (tm) tm->begin(kOrient);
-    uint32_t *deg = ctx.alloc<uint32_t>(n);
+    uint32_t *deg = ctx.alloc<uint32_t>(n), *deg_keys = ctx.alloc<uint32_t>(n);
     k_deg_rowptr<<<grid, 256, 0, ctx.stream>>>(rowptr, n, deg);
     TC_LAUNCHED(ctx);
+    TC_CUDA(cudaMemcpyAsync(deg_keys, deg, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, ctx.stream));
+    rank_permutation(ctx, n, deg_keys, out);
     uint32_t *counts = ctx.alloc<uint32_t>(tiles);
     uint64_t *offs = ctx.alloc<uint64_t>(tiles + 1);
     k_orient_count<<<tiles, kTileThreads, 0, ctx.stream>>>(rowptr, col, n, M, deg, counts);
     TC_LAUNCHED(ctx);
     scan_exclusive(ctx, counts, offs, tiles);
-    uint64_t m_cap = M / 2 + 1;
-    uint32_t *col_plus = ctx.alloc<uint32_t>(m_cap);
-    uint64_t *off_plus = ctx.alloc<uint64_t>(n + 1);
-    k_orient_scatter<<<tiles, kTileThreads, 0, ctx.stream>>>(rowptr, col, n, M, deg, offs,
-                                                             col_plus, off_plus);
-    TC_LAUNCHED(ctx);
-    k_orient_tail<<<grid, 256, 0, ctx.stream>>>(rowptr, n, M, offs + tiles, off_plus);
-    TC_LAUNCHED(ctx);
+    uint64_t cap = M / 2 + 1;
+    uint32_t *okey = ctx.alloc<uint32_t>(cap), *oval = ctx.alloc<uint32_t>(cap);
     uint32_t *dplus = ctx.alloc<uint32_t>(n + 1);
-    k_dplus<<<grid, 256, 0, ctx.stream>>>(off_plus, n, dplus);
+    TC_CUDA(cudaMemsetAsync(dplus, 0, (n + 1) * sizeof(uint32_t), ctx.stream));
+    k_orient_emit<<<tiles, kTileThreads, 0, ctx.stream>>>(rowptr, col, n, M, deg, out.newid, offs,
+                                                          okey, oval, dplus);
     TC_LAUNCHED(ctx);
-    if (tm) tm->end(kOrient);
-    if (!sorted) {
-        if (tm) tm->begin(kSort);
-        segmented_sort(ctx, n, off_plus, col_plus, m_cap, segsort_block_max);
-        if (tm) tm->end(kSort);
+    pairs_to_csr(ctx, n, cap, okey, oval, dplus, offs + tiles, need_sorted, segsort_block_max, out,
+                 tm);
+}
+
+// ------------------------------------------------------------------ back to original ids
+__global__ void __launch_bounds__(kTileThreads)
+    k_pairs_original(const uint64_t *__restrict__ off, const uint32_t *__restrict__ colp, uint64_t n,
+                     const uint64_t *__restrict__ m_dev, const uint32_t *__restrict__ order,
+                     uint32_t *__restrict__ src, uint32_t *__restrict__ dst,
+                     uint32_t *__restrict__ dcount) {
+    __shared__ uint32_t s_row[kTileItems];
+    __shared__ uint32_t s_scan[kTileThreads / 32];
+    uint64_t m = *m_dev;
+    uint64_t t0 = (uint64_t)blockIdx.x * kTileItems;
+    if (t0 >= m) return;
+    uint32_t len = (uint32_t)min((uint64_t)kTileItems, m - t0);
+    tile_rows(off, n, t0, len, s_row, s_scan);
+    for (uint32_t i = threadIdx.x; i < len; i += kTileThreads) {
+        uint32_t a = order[s_row[i]], c = order[colp[t0 + i]];
+        src[t0 + i] = a;
+        dst[t0 + i] = c;
+        atomicAdd(&dcount[a], 1u);
     }
-    out.n = n;
-    out.off = off_plus;
-    out.col = col_plus;
-    out.dplus = dplus;
-    out.m_dev = offs + tiles;
-    out.m_cap = m_cap;
+}
+
+void to_original(Ctx &ctx, const Oriented &g, uint64_t *off_out, uint32_t *col_out) {
+    uint64_t cap = g.m_cap, n = g.n;
+    int b = id_bits(n);
+    uint32_t *src = ctx.alloc<uint32_t>(cap), *dst = ctx.alloc<uint32_t>(cap);
+    uint32_t *src2 = ctx.alloc<uint32_t>(cap), *dst2 = ctx.alloc<uint32_t>(cap);
+    uint32_t *cnt = ctx.alloc<uint32_t>(n + 1);
+    TC_CUDA(cudaMemsetAsync(cnt, 0, (n + 1) * sizeof(uint32_t), ctx.stream));
+    uint32_t tiles = (uint32_t)((cap + kTileItems - 1) / kTileItems);
+    k_pairs_original<<<tiles, kTileThreads, 0, ctx.stream>>>(g.off, g.col, n, g.m_dev, g.order, src,
+                                                             dst, cnt);
+    TC_LAUNCHED(ctx);
+    // rows ascending: stable sort by target, then stable sort by source
+    bool a1 = radix_sort_pairs(ctx, dst, dst2, src, src2, cap, g.m_dev, b);
+    uint32_t *d1 = a1 ? dst2 : dst, *s1 = a1 ? src2 : src;
+    uint32_t *d2 = a1 ? dst : dst2, *s2 = a1 ? src : src2;
+    bool a2 = radix_sort_pairs(ctx, s1, s2, d1, d2, cap, g.m_dev, b);
+    uint32_t *col_sorted = a2 ? d2 : d1;
+    scan_exclusive(ctx, cnt, off_out, n);
+    TC_CUDA(cudaMemcpyAsync(col_out, col_sorted, cap * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
+                            ctx.stream));
+}
+
+__global__ void k_pv_original(const uint64_t *__restrict__ pv_new, const uint32_t *__restrict__ newid,
+                              uint64_t n, uint64_t *__restrict__ pv_out) {
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * blockDim.x)
+        pv_out[v] = pv_new[newid[v]];
+}
+
+void per_vertex_to_original(Ctx &ctx, const Oriented &g, const uint64_t *pv_new, uint64_t *pv_out) {
+    k_pv_original<<<ctx.persistent_grid(8), 256, 0, ctx.stream>>>(pv_new, g.newid, g.n, pv_out);
+    TC_LAUNCHED(ctx);
 }
 
 }  // namespace tc

@@ -140,31 +140,42 @@ static void run(Call &c) {
         if (!msg.empty()) throw Error{TC_EGRAPH, msg};
     }
 
-    uint64_t *pv_dev = nullptr;
+    uint64_t *pv_dev = nullptr, *pv_new = nullptr;  // output side / rank-id side
     if (pv) {
         pv_dev = host ? ctx.alloc<uint64_t>(c.n) : c.per_vertex;
+        pv_new = ctx.alloc<uint64_t>(c.n);
         if (c.n) TC_CUDA(cudaMemsetAsync(pv_dev, 0, c.n * sizeof(uint64_t), ctx.stream));
+        if (c.n) TC_CUDA(cudaMemsetAsync(pv_new, 0, c.n * sizeof(uint64_t), ctx.stream));
     }
     uint64_t *total_dev = c.mode == kShard ? c.partial_dev : ctx.alloc<uint64_t>(1);
     TC_CUDA(cudaMemsetAsync(total_dev, 0, sizeof(uint64_t), ctx.stream));
     uint64_t *pin = pinned_scratch();
     if (c.stats) memset(pin, 0, 32 * sizeof(uint64_t));
 
+    // Rows of N+ must be ascending only for the merge / search / two-pointer variants.
+    const int fv = c.opt.force_variant;
+    const bool need_sorted = fv == TC_VARIANT_SHORT || fv == TC_VARIANT_MERGE ||
+                             fv == TC_VARIANT_SEARCH ||
+                             (fv < 0 && (c.opt.short_max > 0 || c.opt.skew_ratio > 0)) ||
+                             c.M >= (1ull << 32);   // HASH needs 32-bit offsets (R8)
+
     if (c.n > 0 && c.M > 0) {
         Oriented g;
         if (c.flags & TC_CLEAN)
-            orient_clean(ctx, c.n, c.M, rowptr, col, c.flags & TC_SORTED, c.opt.segsort_block_max,
-                         g, tm);
+            orient_clean(ctx, c.n, c.M, rowptr, col, need_sorted, c.opt.segsort_block_max, g, tm);
         else
-            orient_dirty(ctx, c.n, c.M, rowptr, col, g, tm);
+            orient_dirty(ctx, c.n, c.M, rowptr, col, need_sorted, c.opt.segsort_block_max, g, tm);
 
-        if (c.mode == kOrientOnly) {
+        if (c.mode == kOrientOnly) {  // N+ in the caller's ids, rows ascending
+            uint64_t *off_o = ctx.alloc<uint64_t>(c.n + 1);
+            uint32_t *col_o = ctx.alloc<uint32_t>(g.m_cap);
+            to_original(ctx, g, off_o, col_o);
             cudaMemcpyKind kind = host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
             uint64_t m = 0;
             TC_CUDA(cudaMemcpyAsync(&m, g.m_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx.stream));
             TC_CUDA(cudaStreamSynchronize(ctx.stream));
-            TC_CUDA(cudaMemcpyAsync(c.off_plus, g.off, (c.n + 1) * sizeof(uint64_t), kind, ctx.stream));
-            if (m) TC_CUDA(cudaMemcpyAsync(c.col_plus, g.col, m * sizeof(uint32_t), kind, ctx.stream));
+            TC_CUDA(cudaMemcpyAsync(c.off_plus, off_o, (c.n + 1) * sizeof(uint64_t), kind, ctx.stream));
+            if (m) TC_CUDA(cudaMemcpyAsync(c.col_plus, col_o, m * sizeof(uint32_t), kind, ctx.stream));
             TC_CUDA(cudaStreamSynchronize(ctx.stream));
             *c.m_plus = m;
             return;
@@ -193,8 +204,9 @@ static void run(Call &c) {
         if (tm) tm->end(kBin);
 
         if (tm) tm->begin(kIntersect);
-        intersect_all(ctx, g, bins, total_dev, pv_dev);
+        intersect_all(ctx, g, bins, total_dev, pv_new);
         if (tm) tm->end(kIntersect);
+        if (pv) per_vertex_to_original(ctx, g, pv_new, pv_dev);
         if (c.stats) {  // async into pinned memory; read after the final sync
             TC_CUDA(cudaMemcpyAsync(pin, bins.count, 16 * sizeof(uint64_t), cudaMemcpyDeviceToHost,
                                     ctx.stream));
@@ -245,7 +257,7 @@ static void run(Call &c) {
         st.bin_edges[2] = pin[2];
         st.bin_edges[3] = pin[3];
         st.skipped_edges = pin[6];
-        st.hub_sources = pin[9];
+        st.hub_sources = pin[9] + pin[10];
         st.max_dplus = pin[7];
         st.kernel_launches = ctx.launches;
         *c.stats = st;

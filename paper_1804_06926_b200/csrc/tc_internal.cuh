@@ -171,13 +171,18 @@ bool radix_sort_pairs(Ctx &ctx, uint32_t *keys, uint32_t *keys_alt, uint32_t *va
                       uint32_t *vals_alt, uint64_t capacity, const uint64_t *count_dev, int bits);
 
 // ------------------------------------------------------------------ pipeline stages
+// Oriented CSR in RANK-RELABELLED ids: vertex v of the input is newid[v] here,
+// order[i] is the input vertex of new id i, and newid[u] < newid[v] <=> rank(u) < rank(v).
 struct Oriented {
     uint64_t n = 0;
-    uint64_t *off = nullptr;    // off+[n+1]
-    uint32_t *col = nullptr;    // col+[m]
-    uint32_t *dplus = nullptr;  // d+[n]
-    uint64_t *m_dev = nullptr;  // device scalar m
-    uint64_t m_cap = 0;         // capacity bound for m (host-known)
+    uint64_t *off = nullptr;     // off+[n+1]   (indexed by new id)
+    uint32_t *col = nullptr;     // col+[m]     (new ids; ascending per row iff rows_sorted)
+    uint32_t *dplus = nullptr;   // d+[n]       (indexed by new id)
+    uint32_t *order = nullptr;   // new id -> input id
+    uint32_t *newid = nullptr;   // input id -> new id
+    uint64_t *m_dev = nullptr;   // device scalar m
+    uint64_t m_cap = 0;          // capacity bound for m (host-known)
+    bool rows_sorted = false;
 };
 
 // Phase timer: CUDA events on the call's stream, read after the final sync.
@@ -207,12 +212,16 @@ struct Timer {
     }
 };
 
-// a1 (dirty input) + a2 + a3 (+ a4 by construction): raw CSR -> oriented CSR.
+// a1 (dirty input) + a2 + a3: raw CSR -> oriented relabelled CSR (+ a4 if need_sorted).
 void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
-                  Oriented &out, Timer *tm);
-// a2 + a3 for clean symmetric input, then a4 (segmented sort) unless sorted.
+                  bool need_sorted, uint32_t segsort_block_max, Oriented &out, Timer *tm);
+// a2 + a3 for clean symmetric input (+ a4 if need_sorted).
 void orient_clean(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
-                  bool sorted, uint32_t segsort_block_max, Oriented &out, Timer *tm);
+                  bool need_sorted, uint32_t segsort_block_max, Oriented &out, Timer *tm);
+// The oriented CSR in INPUT ids with ascending rows (tc_orient output).
+void to_original(Ctx &ctx, const Oriented &g, uint64_t *off_out, uint32_t *col_out);
+// pv_out[v] = pv_new[newid[v]].
+void per_vertex_to_original(Ctx &ctx, const Oriented &g, const uint64_t *pv_new, uint64_t *pv_out);
 // a4: sort each row of (off, col) ascending.
 void segmented_sort(Ctx &ctx, uint64_t n, const uint64_t *off, uint32_t *col, uint64_t m_cap,
                     uint32_t block_max);
@@ -224,7 +233,8 @@ void segmented_sort(Ctx &ctx, uint64_t n, const uint64_t *off, uint32_t *col, ui
 struct Bins {
     uint2 *edges[4] = {nullptr, nullptr, nullptr, nullptr};  // SHORT, MERGE, SEARCH, HASH(owner, probe)
     uint64_t *count = nullptr;  // device: [0..3] bin sizes, [4] W, [5] sum min(d+u,d+v),
-                                // [6] skipped, [7] max d+, [8] warp owners, [9] CTA owners
+                                // [6] skipped, [7] max d+, [8] warp owners, [9] CTA hash
+                                // owners, [10] CTA bitmap owners
     uint32_t *pcnt = nullptr;   // per owner: number of probe lists (n)
     uint64_t *poff = nullptr;   // owner CSR offsets (n+1)
     uint32_t *plist = nullptr;  // probe vertices grouped by owner
@@ -232,14 +242,16 @@ struct Bins {
     uint32_t *owners_cta = nullptr;   // larger owners ("hubs"): tables of one CTA
     // Tasks = (owner, k): the k-th block of kWarpTaskLists / kCtaTaskLists probe
     // lists of an owner, so no warp / CTA is stuck with a hub's whole group.
-    uint2 *tasks_warp = nullptr, *tasks_cta = nullptr;
-    uint64_t *ntasks_warp = nullptr, *ntasks_cta = nullptr;  // device counters
+    uint2 *tasks_warp = nullptr, *tasks_cta = nullptr, *tasks_bitmap = nullptr;
+    uint64_t *ntasks_warp = nullptr, *ntasks_cta = nullptr, *ntasks_bitmap = nullptr;  // device
+    uint32_t *owners_bitmap = nullptr;  // hubs whose rank span (x, n) fits a smem bitmap
     uint64_t cap = 0;
 };
 
 constexpr uint32_t kWarpTableSlots = 512;   // per-warp hash table (owner d+ <= 128, load <= 1/4)
 constexpr uint32_t kWarpTaskLists = 64;     // probe lists per warp task
 constexpr uint32_t kCtaTaskLists = 256;     // probe lists per CTA task
+constexpr uint32_t kCtaBitmapBits = 8192 * 32;  // rank span of a CTA bitmap (32 KB)
 
 struct BinParams {
     uint32_t short_max, skew_ratio, hub_min;
