@@ -1,30 +1,27 @@
 // bin.cu -- a5: work estimation and binning (§4.2.2 P:527-542 "dynamic
 // grouping ... divide the edge lists into groups"; third kernel P:704-708).
-// Per oriented edge (u,v): a = min(d+u, d+v), b = max.  Edges that cannot close
-// a triangle (d+(u) < 2 or d+(v) = 0) are skipped.  AUTO policy:
-//   b <= short_max            -> SHORT   (thread per edge)
-//   skew_ratio && b >= r * a  -> SEARCH  (binary search of the short list)
-//   otherwise                 -> HASH    (shorter list probed into a shared-memory
-//                                         hash of the longer one, grouped by owner)
-// force_variant routes every edge to one variant instead.
-// HASH edges are regrouped into an owner CSR (counting sort by owner with
-// atomics; order inside a group is irrelevant to the count).  Owners with
-// d+ >= hub_min (or too long for a warp table) go to the CTA kernel.
+//
+// Oriented edge (u,v) in rank ids (u < v, rows ascending).  A triangle {u,v,w}
+// counted on it needs w in N+(u) and w > v, so only suf = |N+(u) after v| elements
+// of N+(u) matter (they sit right after the edge in col+).  Edges with suf = 0 or
+// d+(v) = 0 are skipped.  AUTO policy (edge_bin): SHORT if max(d+u, d+v) <=
+// short_max, SEARCH if skew_ratio and max >= skew_ratio * min, else HASH.
+//
+// HASH owners.  An edge costs min(suf, d+v) probes.  If suf <= d+(v) (96% of R-MAT
+// edges) its owner is v and it probes the suffix of N+(u) after v into a table of
+// N+(v): these entries of v are exactly its in-list (the transposed CSR built in
+// a3), so no grouping pass is needed -- k_inpos locates each in-edge in its source
+// row (binary search) and writes its probe range.  Otherwise the owner is u and it
+// probes N+(v) into a table of N+(u): such out-part entries are compacted in CSR
+// order (so grouped by u) by a tile scan.  Owner x's entries = in-list ++ out-part.
+//
 // Multi-GPU: sources are split into `world` groups by an exclusive
 // prefix of per-source work w(u) = sum_{v in N+(u)} (1 + min(d+u, d+v)); a rank keeps
-// only its group's edges.  The split needs no communication.
+// only the edges whose source is in its group.  The split needs no communication.
 #include "block_scan.cuh"
 #include "tc_internal.cuh"
 
 namespace tc {
-
-// Rank owning source u: floor(prefix[u] / ceil(W/world)), clamped.
-__device__ __forceinline__ int owner_of(const uint64_t *__restrict__ prefix, uint64_t chunk,
-                                        uint32_t u, int world) {
-    if (world <= 1 || chunk == 0) return 0;
-    uint64_t r = prefix[u] / chunk;
-    return r >= (uint64_t)world ? world - 1 : (int)r;
-}
 
 __device__ __forceinline__ void warp_append(bool take, uint64_t *counter, uint2 *out, uint2 item) {
     uint32_t mask = __ballot_sync(0xffffffffu, take);
@@ -37,12 +34,48 @@ __device__ __forceinline__ void warp_append(bool take, uint64_t *counter, uint2 
     if (take) out[base + __popc(mask & ((1u << lane) - 1u))] = item;
 }
 
+// SHORT / MERGE / SEARCH bins (edge-centric); only launched when a policy uses them.
 __global__ void __launch_bounds__(kTileThreads)
-    k_bin(const uint64_t *__restrict__ off, const uint32_t *__restrict__ col,
-          const uint32_t *__restrict__ dplus, uint64_t n, const uint64_t *__restrict__ m_dev,
-          BinParams p, uint2 *__restrict__ b_short, uint2 *__restrict__ b_merge,
-          uint2 *__restrict__ b_search, uint2 *__restrict__ b_hash, uint32_t *__restrict__ pcnt,
-          uint64_t *__restrict__ counts) {
+    k_bin(HashParams hp, const uint64_t *__restrict__ m_dev, uint2 *__restrict__ b_short,
+          uint2 *__restrict__ b_merge, uint2 *__restrict__ b_search, uint64_t *__restrict__ counts) {
+    __shared__ uint32_t s_row[kTileItems];
+    __shared__ uint32_t s_scan[kTileThreads / 32];
+    uint64_t m = *m_dev;
+    uint64_t t0 = (uint64_t)blockIdx.x * kTileItems;
+    if (t0 >= m) return;
+    uint32_t len = (uint32_t)min((uint64_t)kTileItems, m - t0);
+    tile_rows(hp.off, hp.n, t0, len, s_row, s_scan);
+    const uint64_t chunk = work_chunk(hp);
+    for (uint32_t base = 0; base < kTileItems; base += kTileThreads) {
+        uint32_t i = base + threadIdx.x;
+        int bin = -1;
+        uint2 item = make_uint2(0, 0);
+        if (i < len) {
+            uint64_t e = t0 + i;
+            uint32_t u = s_row[i], v = hp.col[e];
+            uint64_t uend = hp.off[u + 1];
+            uint32_t du = (uint32_t)(uend - hp.off[u]), dv = hp.dplus[v];
+            uint32_t suf = (uint32_t)(uend - e - 1);
+            if (rank_owner(hp, chunk, u) == hp.rank) bin = edge_bin(hp, du, dv, suf);
+            item = make_uint2(u, v);
+        }
+        warp_append(bin == TC_VARIANT_SHORT, &counts[0], b_short, item);
+        warp_append(bin == TC_VARIANT_MERGE, &counts[1], b_merge, item);
+        warp_append(bin == TC_VARIANT_SEARCH, &counts[2], b_search, item);
+    }
+}
+
+// For every in-edge p = (u -> x): locate x in row u (binary search in the ascending
+// row: position e), then
+//   - x owns the edge (suf = |N+(u) after x| <= d+(x)): urange[p] = [e+1, end of row u),
+//     an in-part entry of x;
+//   - u owns it (suf > d+(x), ~4% of R-MAT edges): orng[e] = [off[x], off[x] + d+(x)),
+//     an out-part entry of u (compacted in CSR order by k_ocompact);
+// the other slot gets an empty range.  Not-HASH / skipped / other-rank edges: both
+// empty.  Also accumulates the work statistics.
+__global__ void __launch_bounds__(kTileThreads)
+    k_inpos(HashParams hp, const uint64_t *__restrict__ m_dev, uint2 *__restrict__ urange,
+            uint2 *__restrict__ orng, uint64_t *__restrict__ counts) {
     __shared__ uint32_t s_row[kTileItems];
     __shared__ uint32_t s_scan[kTileThreads / 32];
     __shared__ uint64_t s_red[kTileThreads / 32];
@@ -50,74 +83,110 @@ __global__ void __launch_bounds__(kTileThreads)
     uint64_t t0 = (uint64_t)blockIdx.x * kTileItems;
     if (t0 >= m) return;
     uint32_t len = (uint32_t)min((uint64_t)kTileItems, m - t0);
-    tile_rows(off, n, t0, len, s_row, s_scan);
-    uint64_t chunk = 0;
-    if (p.world > 1) chunk = (p.work_prefix[n] + p.world - 1) / p.world;
-    uint64_t W = 0, probe = 0, skipped = 0;
-    // striped over the tile so each warp handles 32 consecutive edges per round
-    for (uint32_t base = 0; base < kTileItems; base += kTileThreads) {
-        uint32_t i = base + threadIdx.x;
-        bool valid = i < len;
-        uint32_t u = 0, v = 0, du = 0, dv = 0;
-        if (valid) {
-            u = s_row[i];
-            v = col[t0 + i];
-            du = dplus[u];
-            dv = dplus[v];
-            W += du + dv;
-            probe += min(du, dv);
+    tile_rows(hp.in_off, hp.n, t0, len, s_row, s_scan);
+    const uint64_t chunk = work_chunk(hp);
+    uint64_t W = 0, probe = 0, skipped = 0, hashed = 0;
+    for (uint32_t i = threadIdx.x; i < len; i += kTileThreads) {
+        uint64_t p = t0 + i;
+        uint32_t x = s_row[i], u = hp.in_src[p];
+        uint64_t ub = hp.off[u], ue = hp.off[u + 1];
+        uint64_t lo = ub, hi = ue;   // lower_bound of x in col+[ub, ue)
+        while (lo < hi) {
+            uint64_t mid = (lo + hi) >> 1;
+            if (hp.col[mid] < x) lo = mid + 1; else hi = mid;
         }
-        int bin = -1;
-        uint2 item = make_uint2(u, v);
-        if (valid && owner_of(p.work_prefix, chunk, u, p.world) == p.rank) {
-            uint32_t a = min(du, dv), b = max(du, dv);
-            if (du < 2 || dv == 0) {
-                skipped++;
-            } else if (p.force >= 0) {
-                bin = p.force;
-            } else if (b <= p.short_max) {
-                bin = TC_VARIANT_SHORT;
-            } else if (p.skew_ratio && (uint64_t)b >= (uint64_t)p.skew_ratio * a) {
-                bin = TC_VARIANT_SEARCH;
+        uint32_t du = (uint32_t)(ue - ub), dv = hp.dplus[x], suf = (uint32_t)(ue - lo - 1);
+        W += du + dv;
+        probe += min(suf, dv);
+        int bin = edge_bin(hp, du, dv, suf);
+        skipped += bin < 0;
+        uint2 ri = make_uint2(0, 0), ro = make_uint2(0, 0);
+        if (bin == TC_VARIANT_HASH && rank_owner(hp, chunk, u) == hp.rank) {
+            hashed++;
+            if (suf <= dv) {
+                ri = make_uint2((uint32_t)(lo + 1), (uint32_t)ue);
             } else {
-                bin = TC_VARIANT_HASH;
-            }
-            if (bin == TC_VARIANT_HASH) {
-                if (dv > du) item = make_uint2(v, u);   // owner = longer list (ties: source)
-                atomicAdd(&pcnt[item.x], 1u);
+                uint64_t xb = hp.off[x];
+                ro = make_uint2((uint32_t)xb, (uint32_t)(xb + dv));
             }
         }
-        warp_append(bin == TC_VARIANT_SHORT, &counts[0], b_short, item);
-        warp_append(bin == TC_VARIANT_MERGE, &counts[1], b_merge, item);
-        warp_append(bin == TC_VARIANT_SEARCH, &counts[2], b_search, item);
-        warp_append(bin == TC_VARIANT_HASH, &counts[3], b_hash, item);
+        urange[p] = ri;
+        orng[lo] = ro;
     }
     W = block_sum_u64(W, s_red);
     probe = block_sum_u64(probe, s_red);
     skipped = block_sum_u64(skipped, s_red);
+    hashed = block_sum_u64(hashed, s_red);
     if (threadIdx.x == 0) {
+        atomicAdd((unsigned long long *)&counts[3], (unsigned long long)hashed);
         atomicAdd((unsigned long long *)&counts[4], (unsigned long long)W);
         atomicAdd((unsigned long long *)&counts[5], (unsigned long long)probe);
         atomicAdd((unsigned long long *)&counts[6], (unsigned long long)skipped);
     }
 }
 
-// Scatter HASH pairs into the owner CSR (poff = exclusive scan of pcnt).
-__global__ void k_group(const uint2 *__restrict__ b_hash, const uint64_t *__restrict__ counts,
-                        const uint64_t *__restrict__ poff, uint32_t *__restrict__ cursor,
-                        uint32_t *__restrict__ plist) {
-    uint64_t ne = counts[3];
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ne;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        uint2 e = b_hash[i];
-        plist[poff[e.x] + atomicAdd(&cursor[e.x], 1u)] = e.y;
+// Compaction of the out-part entries (CSR order => grouped by the owning source).
+__global__ void __launch_bounds__(kTileThreads)
+    k_ocount(const uint2 *__restrict__ orng, const uint64_t *__restrict__ m_dev,
+             uint32_t *__restrict__ tcount) {
+    __shared__ uint64_t s_red[kTileThreads / 32];
+    uint64_t m = *m_dev, t0 = (uint64_t)blockIdx.x * kTileItems, c = 0;
+    for (uint32_t i = threadIdx.x; i < kTileItems; i += kTileThreads)
+        if (t0 + i < m) {
+            uint2 r = orng[t0 + i];
+            c += r.y > r.x;
+        }
+    c = block_sum_u64(c, s_red);
+    if (threadIdx.x == 0) tcount[blockIdx.x] = (uint32_t)c;
+}
+
+__global__ void __launch_bounds__(kTileThreads)
+    k_ocompact(const uint2 *__restrict__ orng, const uint32_t *__restrict__ col,
+               const uint64_t *__restrict__ m_dev, const uint64_t *__restrict__ toff,
+               uint2 *__restrict__ orange, uint32_t *__restrict__ ovid, uint32_t *__restrict__ before) {
+    __shared__ uint32_t s_scan[kTileThreads / 32];
+    uint64_t m = *m_dev, t0 = (uint64_t)blockIdx.x * kTileItems;
+    if (t0 >= m) return;
+    uint32_t len = (uint32_t)min((uint64_t)kTileItems, m - t0);
+    uint32_t i0 = threadIdx.x * kItemsPerThread, c = 0;
+    uint2 r[kItemsPerThread];
+#pragma unroll
+    for (int k = 0; k < kItemsPerThread; k++) {
+        r[k] = i0 + k < len ? orng[t0 + i0 + k] : make_uint2(0, 0);
+        c += r[k].y > r[k].x;
+    }
+    uint32_t pos = block_exclusive_scan<SumOp>(c, s_scan);
+    uint64_t base = toff[blockIdx.x] + pos;
+#pragma unroll
+    for (int k = 0; k < kItemsPerThread; k++) {
+        uint32_t i = i0 + k;
+        if (i < len) before[t0 + i] = (uint32_t)base;
+        if (r[k].y > r[k].x) {
+            orange[base] = r[k];
+            ovid[base] = col[t0 + i];
+            base++;
+        }
     }
 }
 
-// Owner lists and max d+: warp owners (d+ < cta_min), CTA bitmap owners (rank span
-// n-1-x <= kCtaBitmapBits) and CTA hash owners (the rest).
-__global__ void k_owners(const uint32_t *__restrict__ dplus, const uint32_t *__restrict__ pcnt,
-                         uint64_t n, uint32_t cta_min, uint32_t *__restrict__ owners_warp,
+// ooff[x] = out-part entries before x's row (gather; empty rows are fine).
+__global__ void k_ooff(const uint64_t *__restrict__ off, uint64_t n, const uint64_t *__restrict__ m_dev,
+                       const uint32_t *__restrict__ before, const uint64_t *__restrict__ total,
+                       uint64_t *__restrict__ ooff) {
+    uint64_t m = *m_dev, t = *total;
+    for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x <= n;
+         x += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t s = off[x];
+        ooff[x] = s < m ? before[s] : t;
+    }
+}
+
+// Owner lists and max d+.  pcnt[x] = probe entries of owner x = its in-degree (empty
+// entries included) + its compacted out-part entries; warp owners (d+ < cta_min), CTA
+// bitmap owners (rank span n-1-x <= kCtaBitmapBits) and CTA hash owners (the rest).
+__global__ void k_owners(const uint32_t *__restrict__ dplus, const uint64_t *__restrict__ in_off,
+                         const uint64_t *__restrict__ ooff, uint64_t n, uint32_t cta_min,
+                         uint32_t *__restrict__ pcnt, uint32_t *__restrict__ owners_warp,
                          uint32_t *__restrict__ owners_cta, uint32_t *__restrict__ owners_bitmap,
                          uint64_t *__restrict__ counts) {
     uint32_t local_max = 0;
@@ -130,7 +199,10 @@ __global__ void k_owners(const uint32_t *__restrict__ dplus, const uint32_t *__r
         if (u < n) {
             uint32_t du = dplus[u];
             local_max = max(local_max, du);
-            if (pcnt[u]) kind = du < cta_min ? 0 : (n - 1 - u <= kCtaBitmapBits ? 2 : 1);
+            uint32_t c = 0;
+            if (du) c = (uint32_t)(in_off[u + 1] - in_off[u] + ooff[u + 1] - ooff[u]);
+            pcnt[u] = c;
+            if (c) kind = du < cta_min ? 0 : (n - 1 - u <= kCtaBitmapBits ? 2 : 1);
         }
         uint32_t *dst[3] = {owners_warp, owners_cta, owners_bitmap};
 #pragma unroll
@@ -178,53 +250,87 @@ static void make_tasks(Ctx &ctx, uint64_t n, uint64_t cap, const uint32_t *owner
     k_task_count<<<grid, 256, 0, ctx.stream>>>(owners, ocount, pcnt, n, L, tcnt);
     TC_LAUNCHED(ctx);
     scan_exclusive(ctx, tcnt, toff, n);
-    tasks = ctx.alloc<uint2>(cap / L + n + 1);
+    tasks = ctx.alloc<uint2>((2 * cap) / L + n + 1);
     k_task_expand<<<grid, 256, 0, ctx.stream>>>(owners, ocount, tcnt, toff, tasks);
     TC_LAUNCHED(ctx);
     ntasks = toff + n;
 }
 
 void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
-    uint64_t cap = g.m_cap;
+    uint64_t cap = g.m_cap, n = g.n;
     bins.cap = cap;
     bins.count = ctx.alloc<uint64_t>(16);
     TC_CUDA(cudaMemsetAsync(bins.count, 0, 16 * sizeof(uint64_t), ctx.stream));
-    for (int k = 0; k < 4; k++) bins.edges[k] = ctx.alloc<uint2>(cap);
-    bins.pcnt = ctx.alloc<uint32_t>(g.n + 1);
-    uint32_t *cursor = ctx.alloc<uint32_t>(g.n + 1);
-    TC_CUDA(cudaMemsetAsync(bins.pcnt, 0, (g.n + 1) * sizeof(uint32_t), ctx.stream));
-    TC_CUDA(cudaMemsetAsync(cursor, 0, (g.n + 1) * sizeof(uint32_t), ctx.stream));
+    HashParams &hp = bins.hp;
+    hp.off = g.off;
+    hp.col = g.col;
+    hp.dplus = g.dplus;
+    hp.in_off = g.in_off;
+    hp.in_src = g.in_src;
+    hp.n = (uint32_t)n;
+    hp.short_max = p.short_max;
+    hp.skew_ratio = p.skew_ratio;
+    hp.force = p.force;
+    hp.rank = p.rank;
+    hp.world = p.world;
+    hp.work_prefix = p.work_prefix;
     uint32_t tiles = (uint32_t)((cap + kTileItems - 1) / kTileItems);
-    if (tiles) {
-        k_bin<<<tiles, kTileThreads, 0, ctx.stream>>>(g.off, g.col, g.dplus, g.n, g.m_dev, p,
-                                                      bins.edges[0], bins.edges[1], bins.edges[2],
-                                                      bins.edges[3], bins.pcnt, bins.count);
+
+    // edge bins for the merge / search / two-pointer variants (only if a policy uses them)
+    const bool edge_bins = p.force == TC_VARIANT_SHORT || p.force == TC_VARIANT_MERGE ||
+                           p.force == TC_VARIANT_SEARCH ||
+                           (p.force < 0 && (p.short_max > 0 || p.skew_ratio > 0));
+    for (int k = 0; k < 3; k++) bins.edges[k] = ctx.alloc<uint2>(edge_bins ? cap : 1);
+    if (edge_bins && tiles) {
+        k_bin<<<tiles, kTileThreads, 0, ctx.stream>>>(hp, g.m_dev, bins.edges[0], bins.edges[1],
+                                                      bins.edges[2], bins.count);
         TC_LAUNCHED(ctx);
     }
-    bins.poff = ctx.alloc<uint64_t>(g.n + 1);
-    scan_exclusive(ctx, bins.pcnt, bins.poff, g.n);
-    bins.plist = ctx.alloc<uint32_t>(cap);
-    k_group<<<ctx.persistent_grid(8), 256, 0, ctx.stream>>>(bins.edges[3], bins.count, bins.poff,
-                                                            cursor, bins.plist);
+
+    // HASH: in-part ranges (in-list order), out-part entries (compacted, CSR order),
+    // statistics, owners, tasks
+    uint2 *urange = ctx.alloc<uint2>(cap), *orng = ctx.alloc<uint2>(cap);
+    uint2 *orange = ctx.alloc<uint2>(cap);
+    uint32_t *ovid = ctx.alloc<uint32_t>(cap), *before = ctx.alloc<uint32_t>(cap);
+    uint32_t *tcount = ctx.alloc<uint32_t>(tiles + 1);
+    uint64_t *toff = ctx.alloc<uint64_t>(tiles + 1), *ooff = ctx.alloc<uint64_t>(n + 1);
+    if (tiles) {
+        k_inpos<<<tiles, kTileThreads, 0, ctx.stream>>>(hp, g.m_dev, urange, orng, bins.count);
+        TC_LAUNCHED(ctx);
+        k_ocount<<<tiles, kTileThreads, 0, ctx.stream>>>(orng, g.m_dev, tcount);
+        TC_LAUNCHED(ctx);
+    }
+    scan_exclusive(ctx, tcount, toff, tiles);
+    if (tiles) {
+        k_ocompact<<<tiles, kTileThreads, 0, ctx.stream>>>(orng, g.col, g.m_dev, toff, orange, ovid,
+                                                           before);
+        TC_LAUNCHED(ctx);
+    }
+    k_ooff<<<ctx.persistent_grid(4), 256, 0, ctx.stream>>>(g.off, n, g.m_dev, before, toff + tiles,
+                                                           ooff);
     TC_LAUNCHED(ctx);
-    bins.owners_warp = ctx.alloc<uint32_t>(g.n);
-    bins.owners_cta = ctx.alloc<uint32_t>(g.n);
-    bins.owners_bitmap = ctx.alloc<uint32_t>(g.n);
+    hp.urange = urange;
+    hp.orange = orange;
+    hp.ovid = ovid;
+    hp.ooff = ooff;
+    bins.pcnt = ctx.alloc<uint32_t>(n + 1);
+    bins.owners_warp = ctx.alloc<uint32_t>(n);
+    bins.owners_cta = ctx.alloc<uint32_t>(n);
+    bins.owners_bitmap = ctx.alloc<uint32_t>(n);
     uint32_t cta_min = p.hub_min < kWarpTableSlots / 4 + 1 ? p.hub_min : kWarpTableSlots / 4 + 1;
-    k_owners<<<ctx.persistent_grid(4), 256, 0, ctx.stream>>>(g.dplus, bins.pcnt, g.n, cta_min,
-                                                             bins.owners_warp, bins.owners_cta,
-                                                             bins.owners_bitmap, bins.count);
+    k_owners<<<ctx.persistent_grid(4), 256, 0, ctx.stream>>>(
+        g.dplus, g.in_off, ooff, n, cta_min, bins.pcnt, bins.owners_warp, bins.owners_cta,
+        bins.owners_bitmap, bins.count);
     TC_LAUNCHED(ctx);
-    make_tasks(ctx, g.n, cap, bins.owners_warp, bins.count + 8, bins.pcnt, kWarpTaskLists,
+    make_tasks(ctx, n, cap, bins.owners_warp, bins.count + 8, bins.pcnt, kWarpTaskLists,
                bins.tasks_warp, bins.ntasks_warp);
-    make_tasks(ctx, g.n, cap, bins.owners_cta, bins.count + 9, bins.pcnt, kCtaTaskLists,
+    make_tasks(ctx, n, cap, bins.owners_cta, bins.count + 9, bins.pcnt, kCtaTaskLists,
                bins.tasks_cta, bins.ntasks_cta);
-    make_tasks(ctx, g.n, cap, bins.owners_bitmap, bins.count + 10, bins.pcnt, kCtaTaskLists,
+    make_tasks(ctx, n, cap, bins.owners_bitmap, bins.count + 10, bins.pcnt, kCtaTaskLists,
                bins.tasks_bitmap, bins.ntasks_bitmap);
 }
 
-// Per-source work estimate w(u) = sum_{v in N+(u)} (1 + min(d+u, d+v)) -- the
-// probe count of the HASH kernel plus one per edge -- then exclusive prefix.
+// Per-source work estimate w(u) = sum_{v in N+(u)} (1 + min(d+u, d+v)), then exclusive prefix.
 __global__ void k_work(const uint64_t *__restrict__ off, const uint32_t *__restrict__ col,
                        const uint32_t *__restrict__ dplus, uint64_t n, uint64_t *__restrict__ work) {
     for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;

@@ -12,10 +12,12 @@
 //   SEARCH lanes own elements of the shorter list and binary-search the longer
 //          one ("scan each node in the smaller list and search the larger list",
 //          P:706-707)
-//   HASH   per edge, the SHORTER list probed into a shared-memory hash of the
-//          longer one; edges grouped by the longer list's vertex ("owner"), one
-//          warp per small owner, one CTA per hub owner (north_star hub kernel).
-//          Cost: min(d+u, d+v) probes per edge instead of d+u + d+v merge steps.
+//   HASH   per edge (u,v), u < v in rank ids, the shorter of (N+(u) after v) and
+//          N+(v) is probed into a shared-memory table (bucket hash, or a bitmap
+//          over the rank range for hubs) of the other endpoint's N+ ("owner");
+//          one warp per small owner task, one CTA per hub task (north_star hub
+//          kernel).  Cost: min(|N+(u) > v|, d+v) probes per edge instead of
+//          d+u + d+v merge steps.
 // Per-vertex mode (TC_PER_VERTEX): each match w of (u,v) adds 1 to t(u), t(v),
 // t(w).
 #include "block_scan.cuh"
@@ -357,12 +359,31 @@ __device__ __forceinline__ uint64_t probe_quads(const Probe &contains, uint32_t 
     return hits;
 }
 
+// Probe entry j of HASH owner x (bin.cu header): j < indeg -> the j-th in-edge
+// (u -> x) of x's in-list, range = N+(u) after x (empty if x does not own it), y = u;
+// else the (j - indeg)-th compacted out-part entry of x: range = N+(v), y = v.
+__device__ __forceinline__ void hash_desc(const HashParams &hp, uint64_t inb, uint32_t indeg,
+                                          uint64_t ob, uint32_t ocnt, uint32_t j, uint32_t &lo,
+                                          uint32_t &hi, uint32_t &y) {
+    lo = hi = y = 0;
+    uint2 r;
+    if (j < indeg) {
+        r = hp.urange[inb + j];
+        y = hp.in_src[inb + j];
+    } else if (j - indeg < ocnt) {
+        r = hp.orange[ob + (j - indeg)];
+        y = hp.ovid[ob + (j - indeg)];
+    } else {
+        return;
+    }
+    lo = r.x;
+    hi = r.y;
+}
+
 // Warp tasks: owners with d+(x) <= kWarpTableSlots/4 (table in the warp's smem slice).
 template <bool PV>
 __global__ void __launch_bounds__(kIxThreads)
-    k_hash_warp(const uint2 *__restrict__ tasks, const uint64_t *__restrict__ ntasks,
-                const uint64_t *__restrict__ off, const uint32_t *__restrict__ col,
-                const uint64_t *__restrict__ poff, const uint32_t *__restrict__ plist,
+    k_hash_warp(const uint2 *__restrict__ tasks, const uint64_t *__restrict__ ntasks, HashParams hp,
                 uint64_t *__restrict__ total, uint64_t *__restrict__ pv) {
     constexpr uint32_t L = kWarpTaskLists;
     __shared__ __align__(16) uint32_t s_tab[kHashWarps][kWarpTableSlots];
@@ -376,27 +397,29 @@ __global__ void __launch_bounds__(kIxThreads)
     uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     uint32_t *tab = s_tab[wib];
+    const uint32_t *col = hp.col;
     uint64_t acc = 0;
     for (uint64_t i = gw; i < nt; i += nw) {
         uint2 task = tasks[i];
         uint32_t x = task.x;
-        uint64_t xb = off[x];
-        uint32_t dx = (uint32_t)(off[x + 1] - xb);
-        uint64_t p0 = poff[x] + (uint64_t)task.y * L;
-        uint32_t nl = (uint32_t)(min(poff[x + 1], p0 + L) - p0);
-        uint32_t run = 0;  // descriptors: lists lane, lane + 32 (prefix in list order)
+        uint64_t xb = hp.off[x];
+        uint32_t dx = (uint32_t)(hp.off[x + 1] - xb);
+        uint64_t inb = hp.in_off[x], ob = hp.ooff[x];
+        uint32_t indeg = (uint32_t)(hp.in_off[x + 1] - inb), ocnt = (uint32_t)(hp.ooff[x + 1] - ob);
+        uint32_t j0 = task.y * L;
+        // descriptors of entries j0 + lane, j0 + 32 + lane; non-empty ones compacted in
+        // order (the list-start bitmap of probe_quads needs distinct starts)
+        uint32_t run = 0, nl = 0;
 #pragma unroll
         for (uint32_t h = 0; h < L; h += 32) {
-            uint32_t li = h + lane, nq = 0, y = 0, lo = 0, hi = 0;
-            if (li < nl) {
-                y = plist[p0 + li];
-                lo = (uint32_t)off[y];
-                hi = (uint32_t)off[y + 1];
-                nq = quad_count(lo, hi);
-            }
+            uint32_t lo = 0, hi = 0, y = 0;
+            hash_desc(hp, inb, indeg, ob, ocnt, j0 + h + lane, lo, hi, y);
+            uint32_t nq = quad_count(lo, hi);
             uint32_t inc = warp_inclusive_scan<SumOp>(nq);
-            if (li < nl) put_desc(d, li, lo, hi, run + inc - nq, y, PV);
+            uint32_t keep = __ballot_sync(0xffffffffu, nq != 0);
+            if (nq) put_desc(d, nl + __popc(keep & ((1u << lane) - 1u)), lo, hi, run + inc - nq, y, PV);
             run += __shfl_sync(0xffffffffu, inc, 31);
+            nl += __popc(keep);
         }
         if (lane == 0) d.pre[nl] = run;
         int bits = table_bits(dx);
@@ -404,7 +427,8 @@ __global__ void __launch_bounds__(kIxThreads)
         __syncwarp();
         table_insert(tab, bits, col + xb, dx, lane, 32);
         __syncwarp();
-        uint64_t h = probe_quads<PV>(HashProbe{opaque(smem_addr(tab)), bits}, x, d, nl, 0, run, col, pv);
+        uint64_t h = probe_quads<PV>(HashProbe{opaque(smem_addr(tab)), bits}, x, d, nl, 0, run,
+                                     col, pv);
         if (PV) {
             uint64_t hw = warp_sum_u64(h);
             if (lane == 0 && hw) atomicAdd((unsigned long long *)&pv[x], (unsigned long long)hw);
@@ -422,40 +446,38 @@ constexpr uint32_t kSmemWords = kHashSlots;            // 32 KB of table / bitma
 static_assert(kCtaBitmapBits == kSmemWords * 32, "bitmap owners are classified in bin.cu");
 template <bool PV, bool kBitmap>
 __global__ void __launch_bounds__(kIxThreads)
-    k_hash_cta(const uint2 *__restrict__ tasks, const uint64_t *__restrict__ ntasks,
-               const uint64_t *__restrict__ off, const uint32_t *__restrict__ col,
-               const uint64_t *__restrict__ poff, const uint32_t *__restrict__ plist, uint32_t n,
+    k_hash_cta(const uint2 *__restrict__ tasks, const uint64_t *__restrict__ ntasks, HashParams hp,
                uint64_t *__restrict__ total, uint64_t *__restrict__ pv) {
     constexpr uint32_t L = kCtaTaskLists;
-    static_assert(L <= kIxThreads, "one descriptor per thread");
+    static_assert(L == kIxThreads, "one descriptor per thread");
     __shared__ __align__(16) uint32_t s_tab[kSmemWords];
     __shared__ uint32_t s_qb[L];
     __shared__ uint2 s_rng[L];
     __shared__ uint32_t s_pre[L + 1];
     __shared__ uint32_t s_vid[PV ? L : 1];
-    __shared__ uint32_t s_scan[kHashWarps];
+    __shared__ uint64_t s_scan[kHashWarps];
     const int wib = threadIdx.x >> 5;
     const QuadDesc d{s_pre, s_qb, s_vid, s_rng};
     const uint32_t tab = opaque(smem_addr(s_tab));
+    const uint32_t *col = hp.col;
+    const uint32_t n = hp.n;
     uint64_t nt = *ntasks;
     uint64_t acc = 0;
     for (uint64_t i = blockIdx.x; i < nt; i += gridDim.x) {
         uint2 task = tasks[i];
         uint32_t x = task.x;
-        uint64_t xb = off[x];
-        uint32_t dx = (uint32_t)(off[x + 1] - xb);
-        uint64_t p0 = poff[x] + (uint64_t)task.y * L;
-        uint32_t nl = (uint32_t)(min(poff[x + 1], p0 + L) - p0);
-        uint32_t nq = 0, y = 0, lo = 0, hi = 0;
-        if (threadIdx.x < nl) {
-            y = plist[p0 + threadIdx.x];
-            lo = (uint32_t)off[y];
-            hi = (uint32_t)off[y + 1];
-            nq = quad_count(lo, hi);
-        }
-        uint32_t items;
-        uint32_t pre = block_exclusive_scan<SumOp>(nq, s_scan, &items);
-        if (threadIdx.x < nl) put_desc(d, threadIdx.x, lo, hi, pre, y, PV);
+        uint64_t xb = hp.off[x];
+        uint32_t dx = (uint32_t)(hp.off[x + 1] - xb);
+        uint64_t inb = hp.in_off[x], ob = hp.ooff[x];
+        uint32_t indeg = (uint32_t)(hp.in_off[x + 1] - inb), ocnt = (uint32_t)(hp.ooff[x + 1] - ob);
+        uint32_t lo, hi, y;
+        hash_desc(hp, inb, indeg, ob, ocnt, task.y * L + threadIdx.x, lo, hi, y);
+        uint32_t nq = quad_count(lo, hi);
+        // one 64-bit scan: high word = compacted index of non-empty entries, low = quads
+        uint64_t tot;
+        uint64_t pre = block_exclusive_scan<SumOp64>(((uint64_t)(nq != 0) << 32) | nq, s_scan, &tot);
+        const uint32_t items = (uint32_t)tot, nl = (uint32_t)(tot >> 32);
+        if (nq) put_desc(d, (uint32_t)(pre >> 32), lo, hi, (uint32_t)pre, y, PV);
         if (threadIdx.x == 0) d.pre[nl] = items;
         uint32_t ib = (uint32_t)(((uint64_t)items * wib) / kHashWarps);
         uint32_t ie = (uint32_t)(((uint64_t)items * (wib + 1)) / kHashWarps);
@@ -497,15 +519,14 @@ template <bool PV>
 static void launch_all(Ctx &ctx, const Oriented &g, const Bins &bins, uint64_t *total,
                        uint64_t *pv) {
     int grid = ctx.persistent_grid(8);
-    uint32_t n = (uint32_t)g.n;
     k_hash_cta<PV, true><<<ctx.persistent_grid(6), kIxThreads, 0, ctx.stream>>>(
-        bins.tasks_bitmap, bins.ntasks_bitmap, g.off, g.col, bins.poff, bins.plist, n, total, pv);
+        bins.tasks_bitmap, bins.ntasks_bitmap, bins.hp, total, pv);
     TC_LAUNCHED(ctx);
     k_hash_cta<PV, false><<<ctx.persistent_grid(6), kIxThreads, 0, ctx.stream>>>(
-        bins.tasks_cta, bins.ntasks_cta, g.off, g.col, bins.poff, bins.plist, n, total, pv);
+        bins.tasks_cta, bins.ntasks_cta, bins.hp, total, pv);
     TC_LAUNCHED(ctx);
-    k_hash_warp<PV><<<grid, kIxThreads, 0, ctx.stream>>>(bins.tasks_warp, bins.ntasks_warp, g.off,
-                                                          g.col, bins.poff, bins.plist, total, pv);
+    k_hash_warp<PV><<<grid, kIxThreads, 0, ctx.stream>>>(bins.tasks_warp, bins.ntasks_warp, bins.hp,
+                                                          total, pv);
     TC_LAUNCHED(ctx);
     k_merge<PV><<<grid, kIxThreads, 0, ctx.stream>>>(bins.edges[1], bins.count + 1, g.off, g.col,
                                                      total, pv);

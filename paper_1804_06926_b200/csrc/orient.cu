@@ -129,45 +129,65 @@ __global__ void k_newid(const uint32_t *__restrict__ order, uint64_t n, uint32_t
         newid[order[i]] = (uint32_t)i;
 }
 
-// order[i] = vertex with the i-th smallest (d, id); newid = inverse.  `deg` is clobbered.
-static void rank_permutation(Ctx &ctx, uint64_t n, uint32_t *deg, Oriented &out) {
+// order[i] = vertex with the i-th smallest (d, id); newid = inverse.  `deg` is kept.
+static void rank_permutation(Ctx &ctx, uint64_t n, const uint32_t *deg, Oriented &out) {
     int b = id_bits(n);
     int grid = ctx.persistent_grid(8);
-    uint32_t *ids = ctx.alloc<uint32_t>(n), *ids2 = ctx.alloc<uint32_t>(n);
-    uint32_t *deg2 = ctx.alloc<uint32_t>(n);
+    uint32_t *ids = ctx.alloc<uint32_t>(n);
+    uint32_t *kA = ctx.alloc<uint32_t>(n), *kB = ctx.alloc<uint32_t>(n);
+    uint32_t *vA = ctx.alloc<uint32_t>(n), *vB = ctx.alloc<uint32_t>(n);
     k_iota<<<grid, 256, 0, ctx.stream>>>(ids, n);
     TC_LAUNCHED(ctx);
     // stable sort by degree (< n <= 2^b); ids enter ascending, so ties stay ordered by id
-    bool alt = radix_sort_pairs(ctx, deg, deg2, ids, ids2, n, nullptr, b);
-    out.order = alt ? ids2 : ids;
+    uint32_t *rk, *rv;
+    radix_sort_pairs_from(ctx, deg, ids, kA, kB, vA, vB, n, nullptr, b, &rk, &rv);
+    out.order = rv;
     out.newid = ctx.alloc<uint32_t>(n);
     k_newid<<<grid, 256, 0, ctx.stream>>>(out.order, n, out.newid);
     TC_LAUNCHED(ctx);
 }
 
-// Oriented pairs (okey = source, oval = target, new ids; m_dev of them) -> CSR by a
-// stable radix sort on the source; dplus already counted.
+// d-(x) = d(x) - d+(x), in rank ids.
+__global__ void k_dminus(const uint32_t *__restrict__ deg, const uint32_t *__restrict__ newid,
+                         const uint32_t *__restrict__ dplus, uint64_t n, uint32_t *__restrict__ dminus) {
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t x = newid[v];
+        dminus[x] = deg[v] - dplus[x];
+    }
+}
+
+// Oriented pairs (okey = source, oval = target, new ids; m_dev of them) -> CSR with
+// ascending rows (a4) by an LSD radix sort on (source, target): a stable pass set
+// over the target, then one over the source.  The intermediate after the first
+// set -- sources grouped by target, ascending -- is kept as the transposed CSR
+// (in-lists N-(x)), which the HASH owners use.  dplus / dminus already counted.
 static void pairs_to_csr(Ctx &ctx, uint64_t n, uint64_t cap, uint32_t *okey, uint32_t *oval,
-                         uint32_t *dplus, uint64_t *m_dev, bool need_sorted,
-                         uint32_t segsort_block_max, Oriented &out, Timer *tm) {
+                         uint32_t *dplus, uint32_t *dminus, uint64_t *m_dev, Oriented &out,
+                         Timer *tm) {
     int b = id_bits(n);
     uint32_t *okey2 = ctx.alloc<uint32_t>(cap), *oval2 = ctx.alloc<uint32_t>(cap);
-    bool alt = radix_sort_pairs(ctx, okey, okey2, oval, oval2, cap, m_dev, b);
-    uint64_t *off = ctx.alloc<uint64_t>(n + 1);
+    // 1) by target (keys = oval, values = okey): T1 = (targets, sources) = transposed CSR
+    bool a1 = radix_sort_pairs(ctx, oval, oval2, okey, okey2, cap, m_dev, b);
+    uint32_t *t_tgt = a1 ? oval2 : oval, *t_src = a1 ? okey2 : okey;
+    uint32_t *f_key = a1 ? oval : oval2, *f_val = a1 ? okey : okey2;   // free pair
+    // 2) stable by source, reading T1 without modifying it
+    uint32_t *g_key = ctx.alloc<uint32_t>(cap), *g_val = ctx.alloc<uint32_t>(cap);
+    uint32_t *rk, *rv;
+    radix_sort_pairs_from(ctx, t_src, t_tgt, f_key, g_key, f_val, g_val, cap, m_dev, b, &rk, &rv);
+    uint64_t *off = ctx.alloc<uint64_t>(n + 1), *in_off = ctx.alloc<uint64_t>(n + 1);
     scan_exclusive(ctx, dplus, off, n);
+    scan_exclusive(ctx, dminus, in_off, n);
     out.n = n;
     out.off = off;
-    out.col = alt ? oval2 : oval;
+    out.col = rv;
     out.dplus = dplus;
+    out.in_off = in_off;
+    out.in_src = t_src;
     out.m_dev = m_dev;
     out.m_cap = cap;
-    out.rows_sorted = need_sorted;
+    out.rows_sorted = true;
     if (tm) tm->end(kOrient);
-    if (need_sorted) {
-        if (tm) tm->begin(kSort);
-        segmented_sort(ctx, n, off, out.col, cap, segsort_block_max);
-        if (tm) tm->end(kSort);
-    }
 }
 
 void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
@@ -193,9 +213,10 @@ void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, cons
 
     if (tm) tm->begin(kOrient);
     uint32_t *deg = ctx.alloc<uint32_t>(n);
-    uint32_t *dplus = ctx.alloc<uint32_t>(n + 1);
+    uint32_t *dplus = ctx.alloc<uint32_t>(n + 1), *dminus = ctx.alloc<uint32_t>(n + 1);
     TC_CUDA(cudaMemsetAsync(deg, 0, n * sizeof(uint32_t), ctx.stream));
     TC_CUDA(cudaMemsetAsync(dplus, 0, (n + 1) * sizeof(uint32_t), ctx.stream));
+    TC_CUDA(cudaMemsetAsync(dminus, 0, (n + 1) * sizeof(uint32_t), ctx.stream));
     int grid = ctx.persistent_grid(8);
     k_deg_pairs<<<grid, 256, 0, ctx.stream>>>(E, m_dev, b, deg);
     TC_LAUNCHED(ctx);
@@ -203,7 +224,11 @@ void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, cons
     uint32_t *okey = ctx.alloc<uint32_t>(M), *oval = ctx.alloc<uint32_t>(M);
     k_orient_pairs<<<grid, 256, 0, ctx.stream>>>(E, m_dev, b, out.newid, okey, oval, dplus);
     TC_LAUNCHED(ctx);
-    pairs_to_csr(ctx, n, M, okey, oval, dplus, m_dev, need_sorted, segsort_block_max, out, tm);
+    k_dminus<<<grid, 256, 0, ctx.stream>>>(deg, out.newid, dplus, n, dminus);
+    TC_LAUNCHED(ctx);
+    (void)need_sorted;
+    (void)segsort_block_max;
+    pairs_to_csr(ctx, n, M, okey, oval, dplus, dminus, m_dev, out, tm);
 }
 
 // ------------------------------------------------------------------ clean input
@@ -256,9 +281,9 @@ __global__ void __launch_bounds__(kTileThreads)
 #pragma unroll
     for (int k = 0; k < kItemsPerThread; k++) {
         if (f[k]) {
-            uint32_t s = newid[s_row[i0 + k]];
+            uint32_t s = newid[s_row[i0 + k]], t = newid[v[k]];
             okey[base] = s;
-            oval[base] = newid[v[k]];
+            oval[base] = t;
             atomicAdd(&dplus[s], 1u);
             base++;
         }
@@ -270,11 +295,10 @@ void orient_clean(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, cons
     uint32_t tiles = (uint32_t)((M + kTileItems - 1) / kTileItems);
     int grid = ctx.persistent_grid(8);
     if (tm) tm->begin(kOrient);
-    uint32_t *deg = ctx.alloc<uint32_t>(n), *deg_keys = ctx.alloc<uint32_t>(n);
+    uint32_t *deg = ctx.alloc<uint32_t>(n);
     k_deg_rowptr<<<grid, 256, 0, ctx.stream>>>(rowptr, n, deg);
     TC_LAUNCHED(ctx);
-    TC_CUDA(cudaMemcpyAsync(deg_keys, deg, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, ctx.stream));
-    rank_permutation(ctx, n, deg_keys, out);
+    rank_permutation(ctx, n, deg, out);
     uint32_t *counts = ctx.alloc<uint32_t>(tiles);
     uint64_t *offs = ctx.alloc<uint64_t>(tiles + 1);
     k_orient_count<<<tiles, kTileThreads, 0, ctx.stream>>>(rowptr, col, n, M, deg, counts);
@@ -282,13 +306,17 @@ void orient_clean(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, cons
     scan_exclusive(ctx, counts, offs, tiles);
     uint64_t cap = M / 2 + 1;
     uint32_t *okey = ctx.alloc<uint32_t>(cap), *oval = ctx.alloc<uint32_t>(cap);
-    uint32_t *dplus = ctx.alloc<uint32_t>(n + 1);
+    uint32_t *dplus = ctx.alloc<uint32_t>(n + 1), *dminus = ctx.alloc<uint32_t>(n + 1);
     TC_CUDA(cudaMemsetAsync(dplus, 0, (n + 1) * sizeof(uint32_t), ctx.stream));
+    TC_CUDA(cudaMemsetAsync(dminus, 0, (n + 1) * sizeof(uint32_t), ctx.stream));
     k_orient_emit<<<tiles, kTileThreads, 0, ctx.stream>>>(rowptr, col, n, M, deg, out.newid, offs,
                                                           okey, oval, dplus);
     TC_LAUNCHED(ctx);
-    pairs_to_csr(ctx, n, cap, okey, oval, dplus, offs + tiles, need_sorted, segsort_block_max, out,
-                 tm);
+    k_dminus<<<grid, 256, 0, ctx.stream>>>(deg, out.newid, dplus, n, dminus);
+    TC_LAUNCHED(ctx);
+    (void)need_sorted;
+    (void)segsort_block_max;
+    pairs_to_csr(ctx, n, cap, okey, oval, dplus, dminus, offs + tiles, out, tm);
 }
 
 // ------------------------------------------------------------------ back to original ids

@@ -1,17 +1,30 @@
-// radix.cu -- hand-written stable LSD radix sort (8-bit digits) for 64-bit keys
-// and for 32-bit key / 32-bit value pairs.  Per pass: a per-tile digit
-// histogram, a device-wide exclusive scan of the digit-major histogram, and a
-// stable scatter that ranks equal digits inside each warp with __match_any_sync.
+// radix.cu -- hand-written stable LSD radix sort (8-bit digits), onesweep style:
+//   1. one histogram kernel reads the keys once and counts the digits of EVERY
+//      pass (shared-memory histograms, one global atomic per digit per block);
+//   2. a tiny kernel turns them into per-pass exclusive digit offsets;
+//   3. per pass ONE kernel: each CTA takes the next tile (atomic ticket, so a
+//      tile only ever waits on tiles that already started), ranks its keys
+//      stably inside the tile (__match_any_sync per warp round), publishes its
+//      per-digit counts, and obtains the exclusive prefix of earlier tiles by
+//      DECOUPLED LOOK-BACK over their published (aggregate | inclusive) words.
+//      The tile is then reordered by digit in shared memory and written out as
+//      coalesced runs (global position = digit offset + look-back prefix + rank).
+// Keys are read once and written once per pass.
 #include "tc_internal.cuh"
 
 namespace tc {
 
-constexpr int kRadixThreads = 256;
-constexpr int kRadixWarps = kRadixThreads / 32;
-constexpr int kRadixRounds = 16;                         // 32-item rounds per warp
-constexpr int kRadixWarpItems = 32 * kRadixRounds;       // 512
-constexpr int kRadixTile = kRadixWarps * kRadixWarpItems;  // 4096
+constexpr int kRsThreads = 256;
+constexpr int kRsWarps = kRsThreads / 32;
+constexpr int kRsRounds = 8;                           // 32-item rounds per warp
+constexpr int kRsWarpItems = 32 * kRsRounds;           // 256
+constexpr int kRsTile = kRsWarps * kRsWarpItems;       // 2048 items per tile
 constexpr int kDigits = 256;
+constexpr int kMaxPasses = 8;
+
+constexpr uint64_t kFlagAgg = 1ull << 62;   // status word: tile aggregate published
+constexpr uint64_t kFlagPre = 2ull << 62;   // status word: inclusive prefix published
+constexpr uint64_t kCountMask = (1ull << 62) - 1;
 
 __device__ __forceinline__ uint64_t valid_count(uint64_t cap, const uint64_t *count_dev) {
     if (!count_dev) return cap;
@@ -19,122 +32,265 @@ __device__ __forceinline__ uint64_t valid_count(uint64_t cap, const uint64_t *co
     return c < cap ? c : cap;
 }
 
+// Status words carry their own payload (flag | count in one 64-bit word), so
+// relaxed gpu-scope single-copy-atomic accesses suffice: no acquire/release
+// (which would invalidate L1 on every spin iteration).
+__device__ __forceinline__ void st_relaxed(uint64_t *p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// All-pass digit histogram: hist[pass * 256 + digit].
 template <class K>
-__global__ void __launch_bounds__(kRadixThreads)
-    k_radix_hist(const K *__restrict__ keys, uint64_t cap, const uint64_t *__restrict__ count_dev,
-                 int shift, uint32_t *__restrict__ hist, uint32_t tiles) {
-    __shared__ uint32_t h[kDigits];
+__global__ void __launch_bounds__(kRsThreads)
+    k_rs_hist(const K *__restrict__ keys, uint64_t cap, const uint64_t *__restrict__ count_dev,
+              int passes, uint32_t *__restrict__ hist) {
+    __shared__ uint32_t h[kMaxPasses][kDigits];
     uint64_t n = valid_count(cap, count_dev);
-    h[threadIdx.x] = 0;
+    for (int i = threadIdx.x; i < kMaxPasses * kDigits; i += kRsThreads) (&h[0][0])[i] = 0;
     __syncthreads();
-    uint64_t base = (uint64_t)blockIdx.x * kRadixTile;
-    if (base < n) {
-        for (int k = 0; k < kRadixTile / kRadixThreads; k++) {
-            uint64_t i = base + (uint64_t)k * kRadixThreads + threadIdx.x;
-            if (i < n) atomicAdd(&h[(uint32_t)(keys[i] >> shift) & 0xffu], 1u);
-        }
+    for (uint64_t i = (uint64_t)blockIdx.x * kRsThreads + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * kRsThreads) {
+        K k = keys[i];
+        for (int p = 0; p < passes; p++) atomicAdd(&h[p][(uint32_t)(k >> (8 * p)) & 0xffu], 1u);
     }
     __syncthreads();
-    hist[(uint64_t)threadIdx.x * tiles + blockIdx.x] = h[threadIdx.x];
+    for (int i = threadIdx.x; i < passes * kDigits; i += kRsThreads) {
+        uint32_t v = (&h[0][0])[i];
+        if (v) atomicAdd(&hist[i], v);
+    }
+}
+
+// Exclusive scan of each pass's 256 digit counts (one warp per pass).
+__global__ void k_rs_digit_offsets(const uint32_t *__restrict__ hist, int passes,
+                                   uint64_t *__restrict__ offs) {
+    int p = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (p >= passes) return;
+    uint64_t run = 0;
+    for (int c = 0; c < kDigits; c += 32) {
+        uint64_t v = hist[p * kDigits + c + lane], inc = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            uint64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        offs[p * kDigits + c + lane] = run + inc - v;
+        run += __shfl_sync(0xffffffffu, inc, 31);
+    }
 }
 
 template <class K, bool kVals>
-__global__ void __launch_bounds__(kRadixThreads)
-    k_radix_scatter(const K *__restrict__ keys, const uint32_t *__restrict__ vals,
-                    K *__restrict__ keys_out, uint32_t *__restrict__ vals_out, uint64_t cap,
-                    const uint64_t *__restrict__ count_dev, int shift,
-                    const uint64_t *__restrict__ offsets, uint32_t tiles) {
-    __shared__ uint32_t s_wc[kRadixWarps][kDigits];
-    __shared__ uint64_t s_base[kDigits];
-    uint64_t n = valid_count(cap, count_dev);
-    uint64_t tile_base = (uint64_t)blockIdx.x * kRadixTile;
-    if (tile_base >= n) return;
-    int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int i = threadIdx.x; i < kRadixWarps * kDigits; i += kRadixThreads)
-        (&s_wc[0][0])[i] = 0;
-    __syncthreads();
+struct RsSmem {
+    K keys[kRsTile];
+    uint32_t vals[kVals ? kRsTile : 1];
+    uint32_t wc[kRsWarps][kDigits];   // per-warp digit counters -> per-warp exclusive offsets
+    uint32_t dstart[kDigits];         // tile-local digit start
+    uint64_t gbase[kDigits];          // global start of this tile's run of each digit
+    uint32_t scan[kRsWarps];
+    uint32_t tile;
+};
 
-    uint64_t wbase = tile_base + (uint64_t)warp * kRadixWarpItems;
-    K key[kRadixRounds];
-    uint32_t val[kRadixRounds];
-    uint32_t rank[kRadixRounds];
-    uint32_t lt = (1u << lane) - 1u;
-#pragma unroll
-    for (int j = 0; j < kRadixRounds; j++) {
-        uint64_t idx = wbase + (uint64_t)j * 32 + lane;
-        bool valid = idx < n;
-        key[j] = valid ? keys[idx] : (K)0;
-        if (kVals) val[j] = valid ? vals[idx] : 0u;
-        uint32_t d = (uint32_t)(key[j] >> shift) & 0xffu;
-        uint32_t active = __ballot_sync(0xffffffffu, valid);
-        uint32_t old = 0, peers = 0;
-        if (valid) {
-            peers = __match_any_sync(active, d);
-            old = s_wc[warp][d];
-        }
-        __syncwarp();
-        if (valid && (peers & lt) == 0) s_wc[warp][d] = old + __popc(peers);
-        __syncwarp();
-        rank[j] = old + __popc(peers & lt);
-    }
+template <class K, bool kVals>
+__global__ void __launch_bounds__(kRsThreads, 4)
+    k_rs_pass(const K *__restrict__ keys, const uint32_t *__restrict__ vals, K *__restrict__ keys_out,
+              uint32_t *__restrict__ vals_out, uint64_t cap, const uint64_t *__restrict__ count_dev,
+              int shift, const uint64_t *__restrict__ digit_off, uint32_t *__restrict__ ticket,
+              uint64_t *__restrict__ status) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    RsSmem<K, kVals> &S = *reinterpret_cast<RsSmem<K, kVals> *>(smem_raw);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t n = valid_count(cap, count_dev);
+    if (threadIdx.x == 0) S.tile = atomicAdd(ticket, 1u);
+    for (int i = threadIdx.x; i < kRsWarps * kDigits; i += kRsThreads) (&S.wc[0][0])[i] = 0;
     __syncthreads();
-    {
-        uint32_t d = threadIdx.x;  // kRadixThreads == kDigits
-        uint32_t run = 0;
+    const uint32_t tile = S.tile;
+    const uint64_t tile_base = (uint64_t)tile * kRsTile;
+    if (tile_base >= n) return;  // empty tail tiles: nobody waits on them
+    const uint32_t tile_n = (uint32_t)min((uint64_t)kRsTile, n - tile_base);
+
+    // ---- load (warp-blocked, coalesced rounds) and rank stably inside the tile
+    const uint32_t wlocal = (uint32_t)warp * kRsWarpItems;
+    const K *kp = keys + tile_base + wlocal + lane;
+    const uint32_t *vp = kVals ? vals + tile_base + wlocal + lane : nullptr;
+    K key[kRsRounds];
+    uint32_t val[kRsRounds], rank[kRsRounds];
+    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t *wc = S.wc[warp];
+    if (tile_n == kRsTile) {  // full tile: no bounds checks, straight-line ranking
 #pragma unroll
-        for (int w = 0; w < kRadixWarps; w++) {
-            uint32_t c = s_wc[w][d];
-            s_wc[w][d] = run;
-            run += c;
+        for (int j = 0; j < kRsRounds; j++) {
+            key[j] = kp[32 * j];
+            if (kVals) val[j] = vp[32 * j];
         }
-        s_base[d] = offsets[(uint64_t)d * tiles + blockIdx.x];
-    }
-    __syncthreads();
 #pragma unroll
-    for (int j = 0; j < kRadixRounds; j++) {
-        uint64_t idx = wbase + (uint64_t)j * 32 + lane;
-        if (idx < n) {
+        for (int j = 0; j < kRsRounds; j++) {
             uint32_t d = (uint32_t)(key[j] >> shift) & 0xffu;
-            uint64_t pos = s_base[d] + s_wc[warp][d] + rank[j];
-            keys_out[pos] = key[j];
-            if (kVals) vals_out[pos] = val[j];
+            uint32_t peers = __match_any_sync(0xffffffffu, d);
+            uint32_t old = wc[d];
+            __syncwarp();
+            if ((peers & lt) == 0) wc[d] = old + __popc(peers);
+            __syncwarp();
+            rank[j] = old + __popc(peers & lt);
         }
+    } else {
+#pragma unroll
+        for (int j = 0; j < kRsRounds; j++) {
+            bool ok = wlocal + 32 * j + lane < tile_n;
+            key[j] = ok ? kp[32 * j] : (K)0;
+            if (kVals) val[j] = ok ? vp[32 * j] : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < kRsRounds; j++) {
+            bool ok = wlocal + 32 * j + lane < tile_n;
+            uint32_t d = (uint32_t)(key[j] >> shift) & 0xffu;
+            uint32_t active = __ballot_sync(0xffffffffu, ok);
+            uint32_t old = 0, peers = 0;
+            if (ok) {
+                peers = __match_any_sync(active, d);
+                old = wc[d];
+            }
+            __syncwarp();
+            if (ok && (peers & lt) == 0) wc[d] = old + __popc(peers);
+            __syncwarp();
+            rank[j] = old + __popc(peers & lt);
+        }
+    }
+    __syncthreads();
+
+    // ---- per digit: warp-exclusive offsets, tile count, publish aggregate, look back
+    const uint32_t d = threadIdx.x;  // kRsThreads == kDigits
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int w = 0; w < kRsWarps; w++) {
+        uint32_t c = S.wc[w][d];
+        S.wc[w][d] = cnt;
+        cnt += c;
+    }
+    uint64_t *my = status + (uint64_t)tile * kDigits + d;
+    if (tile == 0) {
+        st_relaxed(my, kFlagPre | cnt);
+    } else {
+        st_relaxed(my, kFlagAgg | cnt);
+    }
+    uint32_t dstart = block_exclusive_scan<SumOp>(cnt, S.scan);  // ends with __syncthreads
+    uint64_t excl = 0;
+    if (tile > 0) {
+        // look back in batches of kLb predecessors (loads in flight together); a
+        // missing tile index (< 0) reads as an inclusive prefix of 0
+        constexpr int kLb = 8;
+        for (int64_t t = (int64_t)tile - 1;; t -= kLb) {
+            uint64_t sw[kLb];
+#pragma unroll
+            for (int k = 0; k < kLb; k++)
+                sw[k] = t - k >= 0 ? ld_relaxed(status + (uint64_t)(t - k) * kDigits + d) : kFlagPre;
+            bool done = false;
+#pragma unroll
+            for (int k = 0; k < kLb; k++) {
+                if (done) break;
+                while ((sw[k] & ~kCountMask) == 0)
+                    sw[k] = ld_relaxed(status + (uint64_t)(t - k) * kDigits + d);
+                excl += sw[k] & kCountMask;
+                done = (sw[k] & kFlagPre) != 0;
+            }
+            if (done) break;
+        }
+        st_relaxed(my, kFlagPre | (excl + cnt));
+    }
+    S.dstart[d] = dstart;
+    S.gbase[d] = digit_off[d] + excl;
+    __syncthreads();
+
+    // ---- reorder by digit in shared memory, then coalesced write-out
+#pragma unroll
+    for (int j = 0; j < kRsRounds; j++) {
+        uint32_t local = wlocal + 32 * j + lane;
+        if (local < tile_n) {
+            uint32_t dg = (uint32_t)(key[j] >> shift) & 0xffu;
+            uint32_t pos = S.dstart[dg] + S.wc[warp][dg] + rank[j];
+            S.keys[pos] = key[j];
+            if (kVals) S.vals[pos] = val[j];
+        }
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (uint32_t i = threadIdx.x; i < tile_n; i += kRsThreads) {
+        K k = S.keys[i];
+        uint32_t dg = (uint32_t)(k >> shift) & 0xffu;
+        uint64_t g = S.gbase[dg] + (i - S.dstart[dg]);
+        keys_out[g] = k;
+        if (kVals) vals_out[g] = S.vals[i];
     }
 }
 
+// Passes read (kin0, vin0) first, then ping-pong between (A) and (B); the inputs
+// are never written.  Returns the buffers holding the sorted result.
 template <class K, bool kVals>
-static bool radix_impl(Ctx &ctx, K *keys, K *keys_alt, uint32_t *vals, uint32_t *vals_alt,
-                       uint64_t capacity, const uint64_t *count_dev, int bits) {
-    if (capacity == 0 || bits <= 0) return false;
-    uint32_t tiles = (uint32_t)((capacity + kRadixTile - 1) / kRadixTile);
-    uint32_t *hist = ctx.alloc<uint32_t>((uint64_t)kDigits * tiles);
-    uint64_t *offsets = ctx.alloc<uint64_t>((uint64_t)kDigits * tiles + 1);
-    bool alt = false;
-    for (int shift = 0; shift < bits; shift += 8) {
-        K *kin = alt ? keys_alt : keys, *kout = alt ? keys : keys_alt;
-        uint32_t *vin = alt ? vals_alt : vals, *vout = alt ? vals : vals_alt;
-        k_radix_hist<K><<<tiles, kRadixThreads, 0, ctx.stream>>>(kin, capacity, count_dev, shift,
-                                                                 hist, tiles);
+static void radix_impl(Ctx &ctx, const K *kin0, const uint32_t *vin0, K *kA, K *kB, uint32_t *vA,
+                       uint32_t *vB, uint64_t capacity, const uint64_t *count_dev, int bits,
+                       K **kres, uint32_t **vres) {
+    *kres = const_cast<K *>(kin0);
+    *vres = const_cast<uint32_t *>(vin0);
+    if (capacity == 0 || bits <= 0) return;
+    const int passes = (bits + 7) / 8;
+    const uint32_t tiles = (uint32_t)((capacity + kRsTile - 1) / kRsTile);
+    uint32_t *hist = ctx.alloc<uint32_t>((uint64_t)passes * kDigits);
+    uint64_t *doff = ctx.alloc<uint64_t>((uint64_t)passes * kDigits);
+    uint32_t *tickets = ctx.alloc<uint32_t>(passes);
+    uint64_t *status = ctx.alloc<uint64_t>((uint64_t)tiles * kDigits);   // reused per pass
+    TC_CUDA(cudaMemsetAsync(hist, 0, (size_t)passes * kDigits * sizeof(uint32_t), ctx.stream));
+    TC_CUDA(cudaMemsetAsync(tickets, 0, passes * sizeof(uint32_t), ctx.stream));
+    k_rs_hist<K><<<ctx.persistent_grid(4), kRsThreads, 0, ctx.stream>>>(kin0, capacity, count_dev,
+                                                                        passes, hist);
+    TC_LAUNCHED(ctx);
+    k_rs_digit_offsets<<<1, 32 * kMaxPasses, 0, ctx.stream>>>(hist, passes, doff);
+    TC_LAUNCHED(ctx);
+    const size_t smem = sizeof(RsSmem<K, kVals>);
+    TC_CUDA(cudaFuncSetAttribute(k_rs_pass<K, kVals>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    const K *kin = kin0;
+    const uint32_t *vin = vin0;
+    for (int p = 0; p < passes; p++) {
+        K *kout = (p & 1) ? kB : kA;
+        uint32_t *vout = (p & 1) ? vB : vA;
+        TC_CUDA(cudaMemsetAsync(status, 0, (size_t)tiles * kDigits * sizeof(uint64_t), ctx.stream));
+        k_rs_pass<K, kVals><<<tiles, kRsThreads, smem, ctx.stream>>>(
+            kin, vin, kout, vout, capacity, count_dev, 8 * p, doff + (uint64_t)p * kDigits,
+            tickets + p, status);
         TC_LAUNCHED(ctx);
-        scan_exclusive(ctx, hist, offsets, (uint64_t)kDigits * tiles);
-        k_radix_scatter<K, kVals><<<tiles, kRadixThreads, 0, ctx.stream>>>(
-            kin, vin, kout, vout, capacity, count_dev, shift, offsets, tiles);
-        TC_LAUNCHED(ctx);
-        alt = !alt;
+        kin = kout;
+        vin = vout;
     }
-    return alt;
+    *kres = const_cast<K *>(kin);
+    *vres = const_cast<uint32_t *>(vin);
 }
 
 bool radix_sort(Ctx &ctx, uint64_t *keys, uint64_t *keys_alt, uint64_t capacity,
                 const uint64_t *count_dev, int bits) {
-    return radix_impl<uint64_t, false>(ctx, keys, keys_alt, nullptr, nullptr, capacity, count_dev,
-                                       bits);
+    // (keys -> alt -> keys ...): first pass reads `keys`, then alt/keys alternate
+    uint64_t *kr;
+    uint32_t *vr;
+    radix_impl<uint64_t, false>(ctx, keys, nullptr, keys_alt, keys, nullptr, nullptr, capacity,
+                                count_dev, bits, &kr, &vr);
+    return kr == keys_alt;
 }
 
 bool radix_sort_pairs(Ctx &ctx, uint32_t *keys, uint32_t *keys_alt, uint32_t *vals,
                       uint32_t *vals_alt, uint64_t capacity, const uint64_t *count_dev, int bits) {
-    return radix_impl<uint32_t, true>(ctx, keys, keys_alt, vals, vals_alt, capacity, count_dev,
-                                      bits);
+    uint32_t *kr, *vr;
+    radix_impl<uint32_t, true>(ctx, keys, vals, keys_alt, keys, vals_alt, vals, capacity, count_dev,
+                               bits, &kr, &vr);
+    return kr == keys_alt;
+}
+
+void radix_sort_pairs_from(Ctx &ctx, const uint32_t *keys_in, const uint32_t *vals_in,
+                           uint32_t *kA, uint32_t *kB, uint32_t *vA, uint32_t *vB,
+                           uint64_t capacity, const uint64_t *count_dev, int bits,
+                           uint32_t **keys_out, uint32_t **vals_out) {
+    radix_impl<uint32_t, true>(ctx, keys_in, vals_in, kA, kB, vA, vB, capacity, count_dev, bits,
+                               keys_out, vals_out);
 }
 
 }  // namespace tc

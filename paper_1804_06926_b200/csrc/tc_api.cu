@@ -152,12 +152,9 @@ static void run(Call &c) {
     uint64_t *pin = pinned_scratch();
     if (c.stats) memset(pin, 0, 32 * sizeof(uint64_t));
 
-    // Rows of N+ must be ascending only for the merge / search / two-pointer variants.
-    const int fv = c.opt.force_variant;
-    const bool need_sorted = fv == TC_VARIANT_SHORT || fv == TC_VARIANT_MERGE ||
-                             fv == TC_VARIANT_SEARCH ||
-                             (fv < 0 && (c.opt.short_max > 0 || c.opt.skew_ratio > 0)) ||
-                             c.M >= (1ull << 32);   // HASH needs 32-bit offsets (R8)
+    // Rows of N+ are always put in ascending order: the merge / search variants need
+    // it, and the HASH ranges probe only the part of N+(a) after b.
+    const bool need_sorted = true;
 
     if (c.n > 0 && c.M > 0) {
         Oriented g;

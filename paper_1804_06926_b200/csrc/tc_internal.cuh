@@ -169,6 +169,12 @@ bool radix_sort(Ctx &ctx, uint64_t *keys, uint64_t *keys_alt, uint64_t capacity,
                 const uint64_t *count_dev, int bits);
 bool radix_sort_pairs(Ctx &ctx, uint32_t *keys, uint32_t *keys_alt, uint32_t *vals,
                       uint32_t *vals_alt, uint64_t capacity, const uint64_t *count_dev, int bits);
+// Same, reading (keys_in, vals_in) without modifying them; passes ping-pong between
+// A and B; *keys_out / *vals_out receive the buffers holding the result.
+void radix_sort_pairs_from(Ctx &ctx, const uint32_t *keys_in, const uint32_t *vals_in,
+                           uint32_t *kA, uint32_t *kB, uint32_t *vA, uint32_t *vB,
+                           uint64_t capacity, const uint64_t *count_dev, int bits,
+                           uint32_t **keys_out, uint32_t **vals_out);
 
 // ------------------------------------------------------------------ pipeline stages
 // Oriented CSR in RANK-RELABELLED ids: vertex v of the input is newid[v] here,
@@ -178,6 +184,8 @@ struct Oriented {
     uint64_t *off = nullptr;     // off+[n+1]   (indexed by new id)
     uint32_t *col = nullptr;     // col+[m]     (new ids; ascending per row iff rows_sorted)
     uint32_t *dplus = nullptr;   // d+[n]       (indexed by new id)
+    uint64_t *in_off = nullptr;  // transposed CSR: in-lists N-(x), sources ascending
+    uint32_t *in_src = nullptr;
     uint32_t *order = nullptr;   // new id -> input id
     uint32_t *newid = nullptr;   // input id -> new id
     uint64_t *m_dev = nullptr;   // device scalar m
@@ -226,31 +234,66 @@ void per_vertex_to_original(Ctx &ctx, const Oriented &g, const uint64_t *pv_new,
 void segmented_sort(Ctx &ctx, uint64_t n, const uint64_t *off, uint32_t *col, uint64_t m_cap,
                     uint32_t block_max);
 
+// HASH-variant context passed by value to the binning and intersection kernels.
+struct HashParams {
+    const uint64_t *off = nullptr;     // oriented CSR (rank ids, rows ascending)
+    const uint32_t *col = nullptr;
+    const uint32_t *dplus = nullptr;
+    const uint64_t *in_off = nullptr;  // transposed CSR: in-lists
+    const uint32_t *in_src = nullptr;
+    const uint2 *urange = nullptr;     // in-edge p: probe range [lo, hi) of col+ (empty if none)
+    const uint64_t *ooff = nullptr;    // compacted out-part entries of each owner:
+    const uint2 *orange = nullptr;     //   probe ranges [lo, hi) of col+
+    const uint32_t *ovid = nullptr;    //   the edge's target (per-vertex credit)
+    const uint64_t *work_prefix = nullptr;  // multi-GPU source split (world > 1)
+    uint32_t n = 0, short_max = 0, skew_ratio = 0;
+    int force = -1, rank = 0, world = 1;
+};
+
+// ceil(total work / world) for the multi-GPU source split (0 when world == 1).
+__device__ __forceinline__ uint64_t work_chunk(const HashParams &hp) {
+    return hp.world > 1 ? (hp.work_prefix[hp.n] + hp.world - 1) / hp.world : 0;
+}
+// Rank owning source u: floor(prefix[u] / chunk), clamped.
+__device__ __forceinline__ int rank_owner(const HashParams &hp, uint64_t chunk, uint32_t u) {
+    if (hp.world <= 1 || chunk == 0) return 0;
+    uint64_t r = hp.work_prefix[u] / chunk;
+    return r >= (uint64_t)hp.world ? hp.world - 1 : (int)r;
+}
+// Variant of oriented edge (u,v): -1 = cannot close a triangle (suf = |N+(u) after
+// v| = 0, or d+(v) = 0); else the forced variant, or the AUTO policy.
+__device__ __forceinline__ int edge_bin(const HashParams &hp, uint32_t du, uint32_t dv, uint32_t suf) {
+    if (suf == 0 || dv == 0) return -1;
+    if (hp.force >= 0) return hp.force;
+    uint32_t a = du < dv ? du : dv, b = du < dv ? dv : du;
+    if (b <= hp.short_max) return TC_VARIANT_SHORT;
+    if (hp.skew_ratio && (uint64_t)b >= (uint64_t)hp.skew_ratio * a) return TC_VARIANT_SEARCH;
+    return TC_VARIANT_HASH;
+}
+
 // Edge bins (a5).  SHORT / MERGE / SEARCH hold (u, v) pairs.  HASH edges are
-// regrouped by "owner" = the endpoint with the LONGER list N+ (ties: the source):
-// the owner's N+ is staged in a shared-memory hash and the other endpoint's
-// (shorter) list is probed, so an edge costs min(d+u, d+v) probes.
+// handled per owner (bin.cu header): owner x's probe entries are its in-list
+// followed, if it owns out-part edges, by its own row.
 struct Bins {
-    uint2 *edges[4] = {nullptr, nullptr, nullptr, nullptr};  // SHORT, MERGE, SEARCH, HASH(owner, probe)
-    uint64_t *count = nullptr;  // device: [0..3] bin sizes, [4] W, [5] sum min(d+u,d+v),
-                                // [6] skipped, [7] max d+, [8] warp owners, [9] CTA hash
-                                // owners, [10] CTA bitmap owners
-    uint32_t *pcnt = nullptr;   // per owner: number of probe lists (n)
-    uint64_t *poff = nullptr;   // owner CSR offsets (n+1)
-    uint32_t *plist = nullptr;  // probe vertices grouped by owner
-    uint32_t *owners_warp = nullptr;  // owners with d+ < hub_min: tables of one warp
-    uint32_t *owners_cta = nullptr;   // larger owners ("hubs"): tables of one CTA
+    uint2 *edges[3] = {nullptr, nullptr, nullptr};  // SHORT, MERGE, SEARCH: (u, v) pairs
+    uint64_t *count = nullptr;  // device: [0..3] SHORT/MERGE/SEARCH/HASH edges, [4] W,
+                                // [5] sum min(|N+(u) after v|, d+(v)), [6] skipped, [7] max d+,
+                                // [8] warp owners, [9] CTA hash owners, [10] CTA bitmap owners
+    uint32_t *pcnt = nullptr;   // per owner: probe entries
+    uint32_t *owners_warp = nullptr;   // owners with d+ < hub_min: tables of one warp
+    uint32_t *owners_cta = nullptr;    // larger owners ("hubs"): tables of one CTA
+    uint32_t *owners_bitmap = nullptr; // hubs whose rank span (x, n) fits a smem bitmap
     // Tasks = (owner, k): the k-th block of kWarpTaskLists / kCtaTaskLists probe
-    // lists of an owner, so no warp / CTA is stuck with a hub's whole group.
+    // entries of an owner, so no warp / CTA is stuck with a hub's whole group.
     uint2 *tasks_warp = nullptr, *tasks_cta = nullptr, *tasks_bitmap = nullptr;
     uint64_t *ntasks_warp = nullptr, *ntasks_cta = nullptr, *ntasks_bitmap = nullptr;  // device
-    uint32_t *owners_bitmap = nullptr;  // hubs whose rank span (x, n) fits a smem bitmap
+    HashParams hp;
     uint64_t cap = 0;
 };
 
 constexpr uint32_t kWarpTableSlots = 512;   // per-warp hash table (owner d+ <= 128, load <= 1/4)
-constexpr uint32_t kWarpTaskLists = 64;     // probe lists per warp task
-constexpr uint32_t kCtaTaskLists = 256;     // probe lists per CTA task
+constexpr uint32_t kWarpTaskLists = 64;     // probe entries per warp task
+constexpr uint32_t kCtaTaskLists = 256;     // probe entries per CTA task
 constexpr uint32_t kCtaBitmapBits = 8192 * 32;  // rank span of a CTA bitmap (32 KB)
 
 struct BinParams {
@@ -258,7 +301,7 @@ struct BinParams {
     int force;
     int rank, world;
     const uint64_t *work_prefix;  // exclusive prefix of per-source work (world > 1)
-    uint64_t work_chunk;          // ceil(W_total / world)
+    uint64_t work_chunk;          // unused (computed on the device)
 };
 
 void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins);
