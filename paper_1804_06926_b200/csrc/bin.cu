@@ -10,8 +10,8 @@
 // HASH owners.  An edge costs min(suf, d+v) probes.  If suf <= d+(v) (96% of R-MAT
 // edges) its owner is v and it probes the suffix of N+(u) after v into a table of
 // N+(v): these entries of v are exactly its in-list (the transposed CSR built in
-// a3), so no grouping pass is needed -- k_inpos locates each in-edge in its source
-// row (binary search) and writes its probe range.  Otherwise the owner is u and it
+// a3), so no grouping pass is needed -- k_edges writes each edge's probe range to
+// its in-list slot (known from the a3 sort).  Otherwise the owner is u and it
 // probes N+(v) into a table of N+(u): such out-part entries are compacted in CSR
 // order (so grouped by u) by a tile scan.  Owner x's entries = in-list ++ out-part.
 //
@@ -65,8 +65,8 @@ __global__ void __launch_bounds__(kTileThreads)
     }
 }
 
-// For every in-edge p = (u -> x): locate x in row u (binary search in the ascending
-// row: position e), then
+// For every CSR edge e = (u -> x) (row u, rows ascending), with p = pidx[e] its slot
+// in x's in-list:
 //   - x owns the edge (suf = |N+(u) after x| <= d+(x)): urange[p] = [e+1, end of row u),
 //     an in-part entry of x;
 //   - u owns it (suf > d+(x), ~4% of R-MAT edges): orng[e] = [off[x], off[x] + d+(x)),
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(kTileThreads)
 // the other slot gets an empty range.  Not-HASH / skipped / other-rank edges: both
 // empty.  Also accumulates the work statistics.
 __global__ void __launch_bounds__(kTileThreads)
-    k_inpos(HashParams hp, const uint64_t *__restrict__ m_dev, uint2 *__restrict__ urange,
+    k_edges(HashParams hp, const uint64_t *__restrict__ m_dev, uint2 *__restrict__ urange,
             uint2 *__restrict__ orng, uint64_t *__restrict__ counts) {
     __shared__ uint32_t s_row[kTileItems];
     __shared__ uint32_t s_scan[kTileThreads / 32];
@@ -83,19 +83,14 @@ __global__ void __launch_bounds__(kTileThreads)
     uint64_t t0 = (uint64_t)blockIdx.x * kTileItems;
     if (t0 >= m) return;
     uint32_t len = (uint32_t)min((uint64_t)kTileItems, m - t0);
-    tile_rows(hp.in_off, hp.n, t0, len, s_row, s_scan);
+    tile_rows(hp.off, hp.n, t0, len, s_row, s_scan);
     const uint64_t chunk = work_chunk(hp);
     uint64_t W = 0, probe = 0, skipped = 0, hashed = 0;
     for (uint32_t i = threadIdx.x; i < len; i += kTileThreads) {
-        uint64_t p = t0 + i;
-        uint32_t x = s_row[i], u = hp.in_src[p];
-        uint64_t ub = hp.off[u], ue = hp.off[u + 1];
-        uint64_t lo = ub, hi = ue;   // lower_bound of x in col+[ub, ue)
-        while (lo < hi) {
-            uint64_t mid = (lo + hi) >> 1;
-            if (hp.col[mid] < x) lo = mid + 1; else hi = mid;
-        }
-        uint32_t du = (uint32_t)(ue - ub), dv = hp.dplus[x], suf = (uint32_t)(ue - lo - 1);
+        uint64_t e = t0 + i;
+        uint32_t u = s_row[i], x = hp.col[e];
+        uint64_t ue = hp.off[u + 1];
+        uint32_t du = (uint32_t)(ue - hp.off[u]), dv = hp.dplus[x], suf = (uint32_t)(ue - e - 1);
         W += du + dv;
         probe += min(suf, dv);
         int bin = edge_bin(hp, du, dv, suf);
@@ -104,14 +99,14 @@ __global__ void __launch_bounds__(kTileThreads)
         if (bin == TC_VARIANT_HASH && rank_owner(hp, chunk, u) == hp.rank) {
             hashed++;
             if (suf <= dv) {
-                ri = make_uint2((uint32_t)(lo + 1), (uint32_t)ue);
+                ri = make_uint2((uint32_t)(e + 1), (uint32_t)ue);
             } else {
                 uint64_t xb = hp.off[x];
                 ro = make_uint2((uint32_t)xb, (uint32_t)(xb + dv));
             }
         }
-        urange[p] = ri;
-        orng[lo] = ro;
+        urange[hp.pidx[e]] = ri;
+        orng[e] = ro;
     }
     W = block_sum_u64(W, s_red);
     probe = block_sum_u64(probe, s_red);
@@ -267,6 +262,7 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
     hp.dplus = g.dplus;
     hp.in_off = g.in_off;
     hp.in_src = g.in_src;
+    hp.pidx = g.pidx;
     hp.n = (uint32_t)n;
     hp.short_max = p.short_max;
     hp.skew_ratio = p.skew_ratio;
@@ -295,7 +291,7 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
     uint32_t *tcount = ctx.alloc<uint32_t>(tiles + 1);
     uint64_t *toff = ctx.alloc<uint64_t>(tiles + 1), *ooff = ctx.alloc<uint64_t>(n + 1);
     if (tiles) {
-        k_inpos<<<tiles, kTileThreads, 0, ctx.stream>>>(hp, g.m_dev, urange, orng, bins.count);
+        k_edges<<<tiles, kTileThreads, 0, ctx.stream>>>(hp, g.m_dev, urange, orng, bins.count);
         TC_LAUNCHED(ctx);
         k_ocount<<<tiles, kTileThreads, 0, ctx.stream>>>(orng, g.m_dev, tcount);
         TC_LAUNCHED(ctx);

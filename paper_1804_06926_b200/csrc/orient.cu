@@ -159,31 +159,48 @@ __global__ void k_dminus(const uint32_t *__restrict__ deg, const uint32_t *__res
 
 // Oriented pairs (okey = source, oval = target, new ids; m_dev of them) -> CSR with
 // ascending rows (a4) by an LSD radix sort on (source, target): a stable pass set
-// over the target, then one over the source.  The intermediate after the first
-// set -- sources grouped by target, ascending -- is kept as the transposed CSR
-// (in-lists N-(x)), which the HASH owners use.  dplus / dminus already counted.
+// over the target gives the transposed CSR T (in-lists N-(x), sources ascending),
+// then a stable pass set over the source of T's index p.  So pidx[e] = the in-list
+// slot of CSR edge e, col+[e] = T's target at pidx[e], and no edge ever has to be
+// searched for.  dplus / dminus already counted.
+__global__ void k_gather_col(const uint32_t *__restrict__ pidx, const uint32_t *__restrict__ t_tgt,
+                             const uint64_t *__restrict__ m_dev, uint32_t *__restrict__ col) {
+    uint64_t m = *m_dev;
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+         e += (uint64_t)gridDim.x * blockDim.x)
+        col[e] = t_tgt[pidx[e]];
+}
+
 static void pairs_to_csr(Ctx &ctx, uint64_t n, uint64_t cap, uint32_t *okey, uint32_t *oval,
                          uint32_t *dplus, uint32_t *dminus, uint64_t *m_dev, Oriented &out,
                          Timer *tm) {
     int b = id_bits(n);
+    int grid = ctx.persistent_grid(8);
     uint32_t *okey2 = ctx.alloc<uint32_t>(cap), *oval2 = ctx.alloc<uint32_t>(cap);
-    // 1) by target (keys = oval, values = okey): T1 = (targets, sources) = transposed CSR
+    // 1) by target (keys = oval, values = okey): T = (targets, sources) = transposed CSR
     bool a1 = radix_sort_pairs(ctx, oval, oval2, okey, okey2, cap, m_dev, b);
     uint32_t *t_tgt = a1 ? oval2 : oval, *t_src = a1 ? okey2 : okey;
     uint32_t *f_key = a1 ? oval : oval2, *f_val = a1 ? okey : okey2;   // free pair
-    // 2) stable by source, reading T1 without modifying it
+    // 2) stable by source of T's index p (values = p), reading T without modifying it
+    uint32_t *iota = ctx.alloc<uint32_t>(cap);
+    k_iota<<<grid, 256, 0, ctx.stream>>>(iota, cap);
+    TC_LAUNCHED(ctx);
     uint32_t *g_key = ctx.alloc<uint32_t>(cap), *g_val = ctx.alloc<uint32_t>(cap);
     uint32_t *rk, *rv;
-    radix_sort_pairs_from(ctx, t_src, t_tgt, f_key, g_key, f_val, g_val, cap, m_dev, b, &rk, &rv);
+    radix_sort_pairs_from(ctx, t_src, iota, f_key, g_key, f_val, g_val, cap, m_dev, b, &rk, &rv);
+    uint32_t *col = (rk == f_key) ? g_key : f_key;   // a free buffer of cap entries
+    k_gather_col<<<grid, 256, 0, ctx.stream>>>(rv, t_tgt, m_dev, col);
+    TC_LAUNCHED(ctx);
     uint64_t *off = ctx.alloc<uint64_t>(n + 1), *in_off = ctx.alloc<uint64_t>(n + 1);
     scan_exclusive(ctx, dplus, off, n);
     scan_exclusive(ctx, dminus, in_off, n);
     out.n = n;
     out.off = off;
-    out.col = rv;
+    out.col = col;
     out.dplus = dplus;
     out.in_off = in_off;
     out.in_src = t_src;
+    out.pidx = rv;
     out.m_dev = m_dev;
     out.m_cap = cap;
     out.rows_sorted = true;

@@ -186,6 +186,7 @@ struct Oriented {
     uint32_t *dplus = nullptr;   // d+[n]       (indexed by new id)
     uint64_t *in_off = nullptr;  // transposed CSR: in-lists N-(x), sources ascending
     uint32_t *in_src = nullptr;
+    uint32_t *pidx = nullptr;    // CSR edge e -> its slot in the transposed CSR
     uint32_t *order = nullptr;   // new id -> input id
     uint32_t *newid = nullptr;   // input id -> new id
     uint64_t *m_dev = nullptr;   // device scalar m
@@ -241,6 +242,7 @@ struct HashParams {
     const uint32_t *dplus = nullptr;
     const uint64_t *in_off = nullptr;  // transposed CSR: in-lists
     const uint32_t *in_src = nullptr;
+    const uint32_t *pidx = nullptr;    // CSR edge e -> its in-list slot
     const uint2 *urange = nullptr;     // in-edge p: probe range [lo, hi) of col+ (empty if none)
     const uint64_t *ooff = nullptr;    // compacted out-part entries of each owner:
     const uint2 *orange = nullptr;     //   probe ranges [lo, hi) of col+
