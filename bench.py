@@ -249,7 +249,9 @@ def main():
 
     peak, peak_kind = load_peaks()
     b_alg = st["bytes_alg"]
-    achieved = b_alg / (ix_ms * 1e-3) / 1e9 / world  # GB/s per GPU
+    b_hash = st["bytes_hash"]
+    achieved = b_hash / (ix_ms * 1e-3) / 1e9 / world  # GB/s per GPU
+    achieved_alg = b_alg / (ix_ms * 1e-3) / 1e9 / world
     line = {
         "metric": METRIC, "value": m / (ms * 1e-3), "unit": "edges/s", "n_gpus": world,
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
@@ -264,12 +266,16 @@ def main():
                       for k in ("ms_clean", "ms_orient", "ms_sort", "ms_bin", "ms_intersect", "ms_total")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None,
-                     "kernel": "a6+a7 intersection phase (k_hash_cta + k_hash_warp [+ empty SHORT/"
-                               "MERGE/SEARCH launches]), CUDA events on the launch stream",
-                     "bytes_model": "B_alg = 4W + 16m (SURVEY.md 8(d))", "bytes_alg": b_alg,
-                     "work_W": st["work_W"], "work_probe_sum_min": st["work_probe"],
-                     "kernel_ms": ix_ms, "bin_ms": bin_ms, "peak_kind": peak_kind,
-                     "frac_incl_binning": b_alg / ((ix_ms + bin_ms) * 1e-3) / 1e9 / world / peak},
+                     "kernel": "a6+a7 intersection phase (k_hash_cta bitmap + hash, k_hash_warp "
+                               "[+ empty SHORT/MERGE/SEARCH launches]), CUDA events on the launch stream",
+                     "bytes_model": "B_hash = 4*sum min(|N+(u)>v|, d+v) + 8*HASH edges + 4*table loads "
+                                    "(bytes the implemented a6 must read; DESIGN.md sec. 5)",
+                     "bytes_hash": b_hash, "kernel_ms": ix_ms, "bin_ms": bin_ms, "peak_kind": peak_kind,
+                     "survey_B_alg": {"bytes": b_alg, "model": "4W + 16m (SURVEY.md 8(d), merge-based)",
+                                      "achieved": achieved_alg, "frac": achieved_alg / peak,
+                                      "frac_incl_binning": b_alg / ((ix_ms + bin_ms) * 1e-3) / 1e9 / world / peak},
+                     "work_W": st["work_W"], "work_probe": st["work_probe"],
+                     "table_loads": st["table_loads"]},
         "gpu_launches": launches,
         "e2e": e2e,
         "clocks": clocks,

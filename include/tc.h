@@ -114,7 +114,7 @@ typedef struct {
     double ms_total;     /* whole call, including host<->device copies with TC_HOST_PTRS   */
     uint64_t m_undirected;    /* simple undirected edges = |E+|                             */
     uint64_t work_W;          /* sum over E+ of d+(u) + d+(v)   (merge work)                */
-    uint64_t work_probe;      /* sum over E+ of min(d+u, d+v)    (hash-probe work)          */
+    uint64_t work_probe;      /* sum over E+ of min(|N+(u) after v|, d+v) (HASH probe work)  */
     uint64_t bytes_alg;       /* 4*W + 16*m: algorithmic bytes of the intersection (B_alg)  */
     uint64_t bin_edges[4];    /* edges routed to SHORT, MERGE, SEARCH, HASH                 */
     uint64_t skipped_edges;   /* edges that cannot close a triangle (d+(u) < 2 or d+(v) = 0) */
@@ -123,6 +123,9 @@ typedef struct {
     uint64_t kernel_launches; /* kernels this call launched                                 */
     uint64_t h2d_bytes;       /* bytes copied host->device (TC_HOST_PTRS)                   */
     uint64_t d2h_bytes;       /* bytes copied device->host                                   */
+    uint64_t table_loads;     /* HASH: sum over owner tasks of d+(owner) (table builds)      */
+    uint64_t bytes_hash;      /* HASH algorithmic bytes: 4*work_probe + 8*HASH edges +
+                                 4*table_loads (the method's own a6 byte model)           */
 } tc_stats;
 
 /* Fill *opt with the defaults (auto variant selection, default stream). */

@@ -53,7 +53,8 @@ class Stats(ctypes.Structure):
                 ("bin_edges", ctypes.c_uint64 * 4), ("skipped_edges", ctypes.c_uint64),
                 ("hub_sources", ctypes.c_uint64), ("max_dplus", ctypes.c_uint64),
                 ("kernel_launches", ctypes.c_uint64), ("h2d_bytes", ctypes.c_uint64),
-                ("d2h_bytes", ctypes.c_uint64)]
+                ("d2h_bytes", ctypes.c_uint64), ("table_loads", ctypes.c_uint64),
+                ("bytes_hash", ctypes.c_uint64)]
 
 
 _lib = None

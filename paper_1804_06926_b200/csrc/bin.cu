@@ -215,13 +215,24 @@ __global__ void k_owners(const uint32_t *__restrict__ dplus, const uint64_t *__r
 }
 
 // Tasks: owner i of `owners` (i < *ocount) gets ceil(pcnt / L) tasks.
+// Also accumulates the table-build loads sum over tasks of d+(owner) into *tloads.
 __global__ void k_task_count(const uint32_t *__restrict__ owners, const uint64_t *__restrict__ ocount,
-                             const uint32_t *__restrict__ pcnt, uint64_t n, uint32_t L,
-                             uint32_t *__restrict__ tcnt) {
-    uint64_t no = *ocount;
+                             const uint32_t *__restrict__ pcnt, const uint32_t *__restrict__ dplus,
+                             uint64_t n, uint32_t L, uint32_t *__restrict__ tcnt,
+                             uint64_t *__restrict__ tloads) {
+    uint64_t no = *ocount, loads = 0;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x)
-        tcnt[i] = i < no ? (pcnt[owners[i]] + L - 1) / L : 0u;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t t = 0;
+        if (i < no) {
+            uint32_t x = owners[i];
+            t = (pcnt[x] + L - 1) / L;
+            loads += (uint64_t)t * dplus[x];
+        }
+        tcnt[i] = t;
+    }
+    loads = warp_sum_u64(loads);
+    if ((threadIdx.x & 31) == 0 && loads) atomicAdd((unsigned long long *)tloads, (unsigned long long)loads);
 }
 
 __global__ void k_task_expand(const uint32_t *__restrict__ owners, const uint64_t *__restrict__ ocount,
@@ -237,12 +248,12 @@ __global__ void k_task_expand(const uint32_t *__restrict__ owners, const uint64_
 }
 
 static void make_tasks(Ctx &ctx, uint64_t n, uint64_t cap, const uint32_t *owners,
-                       const uint64_t *ocount, const uint32_t *pcnt, uint32_t L, uint2 *&tasks,
-                       uint64_t *&ntasks) {
+                       const uint64_t *ocount, const uint32_t *pcnt, const uint32_t *dplus,
+                       uint32_t L, uint64_t *tloads, uint2 *&tasks, uint64_t *&ntasks) {
     uint32_t *tcnt = ctx.alloc<uint32_t>(n);
     uint64_t *toff = ctx.alloc<uint64_t>(n + 1);
     int grid = ctx.persistent_grid(4);
-    k_task_count<<<grid, 256, 0, ctx.stream>>>(owners, ocount, pcnt, n, L, tcnt);
+    k_task_count<<<grid, 256, 0, ctx.stream>>>(owners, ocount, pcnt, dplus, n, L, tcnt, tloads);
     TC_LAUNCHED(ctx);
     scan_exclusive(ctx, tcnt, toff, n);
     tasks = ctx.alloc<uint2>((2 * cap) / L + n + 1);
@@ -318,12 +329,12 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
         g.dplus, g.in_off, ooff, n, cta_min, bins.pcnt, bins.owners_warp, bins.owners_cta,
         bins.owners_bitmap, bins.count);
     TC_LAUNCHED(ctx);
-    make_tasks(ctx, n, cap, bins.owners_warp, bins.count + 8, bins.pcnt, kWarpTaskLists,
-               bins.tasks_warp, bins.ntasks_warp);
-    make_tasks(ctx, n, cap, bins.owners_cta, bins.count + 9, bins.pcnt, kCtaTaskLists,
-               bins.tasks_cta, bins.ntasks_cta);
-    make_tasks(ctx, n, cap, bins.owners_bitmap, bins.count + 10, bins.pcnt, kCtaTaskLists,
-               bins.tasks_bitmap, bins.ntasks_bitmap);
+    make_tasks(ctx, n, cap, bins.owners_warp, bins.count + 8, bins.pcnt, g.dplus, kWarpTaskLists,
+               bins.count + 11, bins.tasks_warp, bins.ntasks_warp);
+    make_tasks(ctx, n, cap, bins.owners_cta, bins.count + 9, bins.pcnt, g.dplus, kCtaTaskLists,
+               bins.count + 11, bins.tasks_cta, bins.ntasks_cta);
+    make_tasks(ctx, n, cap, bins.owners_bitmap, bins.count + 10, bins.pcnt, g.dplus, kCtaTaskLists,
+               bins.count + 11, bins.tasks_bitmap, bins.ntasks_bitmap);
 }
 
 // Per-source work estimate w(u) = sum_{v in N+(u)} (1 + min(d+u, d+v)), then exclusive prefix.

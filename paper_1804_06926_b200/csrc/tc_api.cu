@@ -256,6 +256,10 @@ static void run(Call &c) {
         st.skipped_edges = pin[6];
         st.hub_sources = pin[9] + pin[10];
         st.max_dplus = pin[7];
+        st.table_loads = pin[11];
+        // bytes the HASH method reads in a6: probed elements + one 8-byte range per probe
+        // entry (<= 2 per edge, 1 for ~96%) + the owners' lists for the table builds
+        st.bytes_hash = 4 * st.work_probe + 8 * st.bin_edges[3] + 4 * st.table_loads;
         st.kernel_launches = ctx.launches;
         *c.stats = st;
     }

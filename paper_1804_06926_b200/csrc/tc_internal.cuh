@@ -280,7 +280,8 @@ struct Bins {
     uint2 *edges[3] = {nullptr, nullptr, nullptr};  // SHORT, MERGE, SEARCH: (u, v) pairs
     uint64_t *count = nullptr;  // device: [0..3] SHORT/MERGE/SEARCH/HASH edges, [4] W,
                                 // [5] sum min(|N+(u) after v|, d+(v)), [6] skipped, [7] max d+,
-                                // [8] warp owners, [9] CTA hash owners, [10] CTA bitmap owners
+                                // [8] warp owners, [9] CTA hash owners, [10] CTA bitmap owners,
+                                // [11] table-build loads (sum over tasks of d+(owner))
     uint32_t *pcnt = nullptr;   // per owner: probe entries
     uint32_t *owners_warp = nullptr;   // owners with d+ < hub_min: tables of one warp
     uint32_t *owners_cta = nullptr;    // larger owners ("hubs"): tables of one CTA

@@ -44,7 +44,7 @@ def test_struct_layout(lib):
     assert ctypes.sizeof(tc.Options) == 64
     assert o.short_max == 0 and o.skew_ratio == 0 and o.hub_min_dplus == 64
     assert o.force_variant == -1 and o.segsort_block_max == 8192
-    assert ctypes.sizeof(tc.Stats) == 6 * 8 + 14 * 8
+    assert ctypes.sizeof(tc.Stats) == 6 * 8 + 16 * 8
 
 
 def test_argument_errors_before_device(lib):
