@@ -178,7 +178,8 @@ __global__ void k_ooff(const uint64_t *__restrict__ off, uint64_t n, const uint6
 
 // Owner lists and max d+.  pcnt[x] = probe entries of owner x = its in-degree (empty
 // entries included) + its compacted out-part entries; warp owners (d+ < cta_min), CTA
-// bitmap owners (rank span n-1-x <= kCtaBitmapBits) and CTA hash owners (the rest).
+// bitmap owners (rank span n-1-x plus a spare zero word fits kCtaBitmapBits) and CTA
+// hash owners (the rest).
 __global__ void k_owners(const uint32_t *__restrict__ dplus, const uint64_t *__restrict__ in_off,
                          const uint64_t *__restrict__ ooff, uint64_t n, uint32_t cta_min,
                          uint32_t *__restrict__ pcnt, uint32_t *__restrict__ owners_warp,
@@ -197,7 +198,7 @@ __global__ void k_owners(const uint32_t *__restrict__ dplus, const uint64_t *__r
             uint32_t c = 0;
             if (du) c = (uint32_t)(in_off[u + 1] - in_off[u] + ooff[u + 1] - ooff[u]);
             pcnt[u] = c;
-            if (c) kind = du < cta_min ? 0 : (n - 1 - u <= kCtaBitmapBits ? 2 : 1);
+            if (c) kind = du < cta_min ? 0 : (n - 1 - u + 32 <= kCtaBitmapBits ? 2 : 1);
         }
         uint32_t *dst[3] = {owners_warp, owners_cta, owners_bitmap};
 #pragma unroll

@@ -182,8 +182,8 @@ __global__ void __launch_bounds__(kIxThreads)
 // all its lists are flattened, and each warp takes an equal contiguous item
 // range.  In each 32-item window lane t finds its list from a bitmap of the list
 // starts inside the window (reduce-or + popc): no per-item search.
-constexpr uint32_t kHashSlots = 8192;  // CTA table capacity (power of two), 32 KB
-constexpr uint32_t kHashChunk = 2048;  // owner elements per table build (load factor <= 1/4)
+constexpr uint32_t kHashSlots = 4096;  // CTA table capacity (power of two), 16 KB
+constexpr uint32_t kHashChunk = 1024;  // owner elements per table build (load factor <= 1/4)
 constexpr int kUnroll = 2;             // independent 32-quad windows per probe step
 constexpr int kHashWarps = kIxThreads / 32;
 
@@ -263,17 +263,22 @@ __device__ __forceinline__ uint32_t opaque(uint32_t v) {
 }
 
 // Membership tests used by probe_quads.
+// Membership tests used by probe_quads: key(e, valid) maps a loaded element (or a
+// masked slot outside the probe range) to a probe key; test(key) answers 0/1.
 struct HashProbe {  // bucket hash of the owner's N+ (any id range)
-    uint32_t tab;
+    uint32_t tab, absent;  // absent = the owner itself: never in its own N+
     int bits;
-    __device__ __forceinline__ uint32_t operator()(uint32_t w) const { return table_contains(tab, bits, w); }
+    __device__ __forceinline__ uint32_t key(uint32_t e, bool valid) const { return valid ? e : absent; }
+    __device__ __forceinline__ uint32_t test(uint32_t k) const { return table_contains(tab, bits, k); }
 };
 struct BitProbe {   // bitmap over the rank-id range [base, base + span) of the owner's N+
-    uint32_t bm, base, span;
-    __device__ __forceinline__ uint32_t operator()(uint32_t w) const {
-        uint32_t o = w - base;
-        uint32_t word = lds32(bm + 4 * (min(o, span - 1) >> 5));  // clamped: no branch
-        return (uint32_t)(o < span) & (word >> (o & 31));
+    // Every element probed for owner x lies in (x, n) (it is in N+(u) after x, or in
+    // N+(v) for v > x), so its bit index is in range with no clamp; masked slots use
+    // index `zero`, a bit of the spare all-zero word after the bitmap.
+    uint32_t bm, base, zero;
+    __device__ __forceinline__ uint32_t key(uint32_t e, bool valid) const { return valid ? e - base : zero; }
+    __device__ __forceinline__ uint32_t test(uint32_t o) const {
+        return (lds32(bm + 4 * (o >> 5)) >> (o & 31)) & 1u;
     }
 };
 
@@ -304,7 +309,7 @@ __device__ __forceinline__ uint32_t quad_count(uint32_t lo, uint32_t hi) {
 // finds its list from a bitmap of the list starts inside the window (reduce-or +
 // popc): no per-item search.  Returns the number of hits.
 template <bool PV, class Probe>
-__device__ __forceinline__ uint64_t probe_quads(const Probe &contains, uint32_t absent,
+__device__ __forceinline__ uint64_t probe_quads(const Probe &contains,
                                                 const QuadDesc &d, uint32_t nl, uint32_t ib,
                                                 uint32_t ie,
                                                 const uint32_t *__restrict__ col,
@@ -342,12 +347,11 @@ __device__ __forceinline__ uint64_t probe_quads(const Probe &contains, uint32_t 
 #pragma unroll
         for (int k = 0; k < kUnroll; k++) {
             uint32_t e[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
+            const uint32_t rel = e0[k] - r[k].x, len = r[k].y - r[k].x;  // mod 2^32
 #pragma unroll
             for (int c = 0; c < 4; c++) {
-                // elements outside the list probe `absent` (the owner: never in its own N+)
-                uint32_t idx = e0[k] + c;
-                uint32_t key = (idx >= r[k].x && idx < r[k].y) ? e[c] : absent;
-                uint32_t h = contains(key);
+                // element idx = e0 + c is in [lo, hi) iff (idx - lo) mod 2^32 < hi - lo
+                uint32_t h = contains.test(contains.key(e[c], rel + c < len));
                 hits += h;
                 if (PV && h) {
                     atomicAdd((unsigned long long *)&pv[e[c]], 1ull);
@@ -427,7 +431,7 @@ __global__ void __launch_bounds__(kIxThreads)
         __syncwarp();
         table_insert(tab, bits, col + xb, dx, lane, 32);
         __syncwarp();
-        uint64_t h = probe_quads<PV>(HashProbe{opaque(smem_addr(tab)), bits}, x, d, nl, 0, run,
+        uint64_t h = probe_quads<PV>(HashProbe{opaque(smem_addr(tab)), x, bits}, d, nl, 0, run,
                                      col, pv);
         if (PV) {
             uint64_t hw = warp_sum_u64(h);
@@ -442,7 +446,7 @@ __global__ void __launch_bounds__(kIxThreads)
 // CTA tasks: large owners ("hubs"); the task's items are split evenly over the warps.
 // kBitmap: the owner's N+ (rank ids in (x, n)) is a bitmap over [x+1, n) -- one
 // 32-bit shared load per probe; otherwise the bucket hash (chunked if d+ > 2048).
-constexpr uint32_t kSmemWords = kHashSlots;            // 32 KB of table / bitmap per CTA
+constexpr uint32_t kSmemWords = kHashSlots;            // 16 KB of table / bitmap per CTA
 static_assert(kCtaBitmapBits == kSmemWords * 32, "bitmap owners are classified in bin.cu");
 template <bool PV, bool kBitmap>
 __global__ void __launch_bounds__(kIxThreads)
@@ -483,15 +487,16 @@ __global__ void __launch_bounds__(kIxThreads)
         uint32_t ie = (uint32_t)(((uint64_t)items * (wib + 1)) / kHashWarps);
         uint64_t h = 0;
         if (kBitmap) {
-            const uint32_t base = x + 1, span = n - 1 - x;   // N+(x) lies in (x, n)
-            for (uint32_t w = threadIdx.x; w < (span + 31) / 32; w += blockDim.x) s_tab[w] = 0u;
+            // N+(x) lies in (x, n): bits [0, span) for ids x+1 .. n-1, then one zero word
+            const uint32_t base = x + 1, span = n - 1 - x, words = span / 32 + 1;
+            for (uint32_t w = threadIdx.x; w < words; w += blockDim.x) s_tab[w] = 0u;
             __syncthreads();
             for (uint32_t k = threadIdx.x; k < dx; k += blockDim.x) {
                 uint32_t o = col[xb + k] - base;
                 atomicOr(&s_tab[o >> 5], 1u << (o & 31));
             }
             __syncthreads();
-            h = probe_quads<PV>(BitProbe{tab, base, span}, x, d, nl, ib, ie, col, pv);
+            h = probe_quads<PV>(BitProbe{tab, base, (words - 1) * 32 + 31}, d, nl, ib, ie, col, pv);
             __syncthreads();
         } else {
             for (uint32_t c0 = 0; c0 < dx; c0 += kHashChunk) {
@@ -501,7 +506,7 @@ __global__ void __launch_bounds__(kIxThreads)
                 __syncthreads();
                 table_insert(s_tab, bits, col + xb + c0, clen, threadIdx.x, blockDim.x);
                 __syncthreads();
-                h += probe_quads<PV>(HashProbe{tab, bits}, x, d, nl, ib, ie, col, pv);
+                h += probe_quads<PV>(HashProbe{tab, x, bits}, d, nl, ib, ie, col, pv);
                 __syncthreads();
             }
         }
@@ -519,10 +524,10 @@ template <bool PV>
 static void launch_all(Ctx &ctx, const Oriented &g, const Bins &bins, uint64_t *total,
                        uint64_t *pv) {
     int grid = ctx.persistent_grid(8);
-    k_hash_cta<PV, true><<<ctx.persistent_grid(6), kIxThreads, 0, ctx.stream>>>(
+    k_hash_cta<PV, true><<<ctx.persistent_grid(8), kIxThreads, 0, ctx.stream>>>(
         bins.tasks_bitmap, bins.ntasks_bitmap, bins.hp, total, pv);
     TC_LAUNCHED(ctx);
-    k_hash_cta<PV, false><<<ctx.persistent_grid(6), kIxThreads, 0, ctx.stream>>>(
+    k_hash_cta<PV, false><<<ctx.persistent_grid(8), kIxThreads, 0, ctx.stream>>>(
         bins.tasks_cta, bins.ntasks_cta, bins.hp, total, pv);
     TC_LAUNCHED(ctx);
     k_hash_warp<PV><<<grid, kIxThreads, 0, ctx.stream>>>(bins.tasks_warp, bins.ntasks_warp, bins.hp,

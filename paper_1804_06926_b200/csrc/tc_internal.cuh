@@ -297,7 +297,7 @@ struct Bins {
 constexpr uint32_t kWarpTableSlots = 512;   // per-warp hash table (owner d+ <= 128, load <= 1/4)
 constexpr uint32_t kWarpTaskLists = 64;     // probe entries per warp task
 constexpr uint32_t kCtaTaskLists = 256;     // probe entries per CTA task
-constexpr uint32_t kCtaBitmapBits = 8192 * 32;  // rank span of a CTA bitmap (32 KB)
+constexpr uint32_t kCtaBitmapBits = 4096 * 32;  // rank span of a CTA bitmap (16 KB)
 
 struct BinParams {
     uint32_t short_max, skew_ratio, hub_min;
