@@ -292,16 +292,20 @@ struct QuadDesc {
     uint2 *rng;
 };
 
+// Probe slots are aligned groups of kSlot elements of col+ (kSlot / 4 128-bit loads).
+constexpr int kSlotShift = 3;
+constexpr int kSlot = 1 << kSlotShift;
+
 __device__ __forceinline__ void put_desc(const QuadDesc &d, uint32_t i, uint32_t lo, uint32_t hi,
                                          uint32_t pre, uint32_t y, bool pv) {
     d.pre[i] = pre;
-    d.qb[i] = (lo >> 2) - pre;
+    d.qb[i] = (lo >> kSlotShift) - pre;
     d.rng[i] = make_uint2(lo, hi);
     if (pv) d.vid[i] = y;
 }
 
 __device__ __forceinline__ uint32_t quad_count(uint32_t lo, uint32_t hi) {
-    return ((hi + 3) >> 2) - (lo >> 2);
+    return ((hi + kSlot - 1) >> kSlotShift) - (lo >> kSlotShift);
 }
 
 // The calling warp probes quads [ib, ie) of the flattened quad space: one aligned
@@ -326,7 +330,7 @@ __device__ __forceinline__ uint64_t probe_quads(const Probe &contains,
     const uint32_t le_mask = (2u << lane) - 1u;
     const uint4 *col4 = reinterpret_cast<const uint4 *>(col);
     for (uint32_t wb = ib; wb < ie; wb += 32 * kUnroll) {
-        uint4 q[kUnroll];
+        uint4 q[kUnroll][kSlot / 4];
         uint2 r[kUnroll];
         uint32_t e0[kUnroll], ly[kUnroll];
 #pragma unroll
@@ -339,23 +343,29 @@ __device__ __forceinline__ uint64_t probe_quads(const Probe &contains,
             uint32_t t = wk + lane;
             uint32_t qi = d.qb[li] + t;
             r[k] = t < ie ? d.rng[li] : make_uint2(0u, 0u);
-            e0[k] = qi << 2;
+            e0[k] = qi << kSlotShift;
             ly[k] = PV ? d.vid[li] : 0u;
-            q[k] = t < ie ? __ldg(col4 + qi) : make_uint4(0u, 0u, 0u, 0u);
-            i0 = __shfl_sync(0xffffffffu, li, 31);  // list holding quad wk + 31
+#pragma unroll
+            for (int v = 0; v < kSlot / 4; v++)
+                q[k][v] = t < ie ? __ldg(col4 + (uint64_t)qi * (kSlot / 4) + v)
+                                 : make_uint4(0u, 0u, 0u, 0u);
+            i0 = __shfl_sync(0xffffffffu, li, 31);  // list holding slot wk + 31
         }
 #pragma unroll
         for (int k = 0; k < kUnroll; k++) {
-            uint32_t e[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
             const uint32_t rel = e0[k] - r[k].x, len = r[k].y - r[k].x;  // mod 2^32
 #pragma unroll
-            for (int c = 0; c < 4; c++) {
-                // element idx = e0 + c is in [lo, hi) iff (idx - lo) mod 2^32 < hi - lo
-                uint32_t h = contains.test(contains.key(e[c], rel + c < len));
-                hits += h;
-                if (PV && h) {
-                    atomicAdd((unsigned long long *)&pv[e[c]], 1ull);
-                    atomicAdd((unsigned long long *)&pv[ly[k]], 1ull);
+            for (int v = 0; v < kSlot / 4; v++) {
+                uint32_t e[4] = {q[k][v].x, q[k][v].y, q[k][v].z, q[k][v].w};
+#pragma unroll
+                for (int c = 0; c < 4; c++) {
+                    // element idx = e0 + 4v + c is in [lo, hi) iff (idx - lo) mod 2^32 < hi - lo
+                    uint32_t h = contains.test(contains.key(e[c], rel + (4 * v + c) < len));
+                    hits += h;
+                    if (PV && h) {
+                        atomicAdd((unsigned long long *)&pv[e[c]], 1ull);
+                        atomicAdd((unsigned long long *)&pv[ly[k]], 1ull);
+                    }
                 }
             }
         }
