@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(kIxThreads)
 constexpr uint32_t kSmemWords = kHashSlots;            // 16 KB of table / bitmap per CTA
 static_assert(kCtaBitmapBits == kSmemWords * 32, "bitmap owners are classified in bin.cu");
 template <bool PV, bool kBitmap>
-__global__ void __launch_bounds__(kIxThreads)
+__global__ void __launch_bounds__(kIxThreads, 5)
     k_hash_cta(const uint2 *__restrict__ tasks, const uint64_t *__restrict__ ntasks, HashParams hp,
                uint64_t *__restrict__ total, uint64_t *__restrict__ pv) {
     constexpr uint32_t L = kCtaTaskLists;
