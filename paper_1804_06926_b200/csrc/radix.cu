@@ -14,11 +14,11 @@
 
 namespace tc {
 
-constexpr int kRsThreads = 256;
+constexpr int kRsThreads = 512;
 constexpr int kRsWarps = kRsThreads / 32;
 constexpr int kRsRounds = 8;                           // 32-item rounds per warp
 constexpr int kRsWarpItems = 32 * kRsRounds;           // 256
-constexpr int kRsTile = kRsWarps * kRsWarpItems;       // 2048 items per tile
+constexpr int kRsTile = kRsWarps * kRsWarpItems;       // 4096 items per tile
 constexpr int kDigits = 256;
 constexpr int kMaxPasses = 8;
 
@@ -94,7 +94,7 @@ struct RsSmem {
 };
 
 template <class K, bool kVals>
-__global__ void __launch_bounds__(kRsThreads, 4)
+__global__ void __launch_bounds__(kRsThreads, 2)
     k_rs_pass(const K *__restrict__ keys, const uint32_t *__restrict__ vals, K *__restrict__ keys_out,
               uint32_t *__restrict__ vals_out, uint64_t cap, const uint64_t *__restrict__ count_dev,
               int shift, const uint64_t *__restrict__ digit_off, uint32_t *__restrict__ ticket,
@@ -160,47 +160,50 @@ __global__ void __launch_bounds__(kRsThreads, 4)
     }
     __syncthreads();
 
-    // ---- per digit: warp-exclusive offsets, tile count, publish aggregate, look back
-    const uint32_t d = threadIdx.x;  // kRsThreads == kDigits
+    // ---- per digit (threads 0..255): warp-exclusive offsets, tile count, publish the
+    // aggregate, look back
+    static_assert(kRsThreads >= kDigits, "one thread per digit");
+    const uint32_t d = threadIdx.x;
+    const bool is_digit = d < kDigits;
     uint32_t cnt = 0;
-#pragma unroll
-    for (int w = 0; w < kRsWarps; w++) {
-        uint32_t c = S.wc[w][d];
-        S.wc[w][d] = cnt;
-        cnt += c;
-    }
     uint64_t *my = status + (uint64_t)tile * kDigits + d;
-    if (tile == 0) {
-        st_relaxed(my, kFlagPre | cnt);
-    } else {
-        st_relaxed(my, kFlagAgg | cnt);
+    if (is_digit) {
+#pragma unroll
+        for (int w = 0; w < kRsWarps; w++) {
+            uint32_t c = S.wc[w][d];
+            S.wc[w][d] = cnt;
+            cnt += c;
+        }
+        st_relaxed(my, (tile == 0 ? kFlagPre : kFlagAgg) | cnt);
     }
     uint32_t dstart = block_exclusive_scan<SumOp>(cnt, S.scan);  // ends with __syncthreads
-    uint64_t excl = 0;
-    if (tile > 0) {
-        // look back in batches of kLb predecessors (loads in flight together); a
-        // missing tile index (< 0) reads as an inclusive prefix of 0
-        constexpr int kLb = 8;
-        for (int64_t t = (int64_t)tile - 1;; t -= kLb) {
-            uint64_t sw[kLb];
+    if (is_digit) {
+        uint64_t excl = 0;
+        if (tile > 0) {
+            // look back in batches of kLb predecessors (loads in flight together); a
+            // missing tile index (< 0) reads as an inclusive prefix of 0
+            constexpr int kLb = 8;
+            for (int64_t t = (int64_t)tile - 1;; t -= kLb) {
+                uint64_t sw[kLb];
 #pragma unroll
-            for (int k = 0; k < kLb; k++)
-                sw[k] = t - k >= 0 ? ld_relaxed(status + (uint64_t)(t - k) * kDigits + d) : kFlagPre;
-            bool done = false;
+                for (int k = 0; k < kLb; k++)
+                    sw[k] = t - k >= 0 ? ld_relaxed(status + (uint64_t)(t - k) * kDigits + d) : kFlagPre;
+                bool done = false;
 #pragma unroll
-            for (int k = 0; k < kLb; k++) {
+                for (int k = 0; k < kLb; k++) {
+                    if (done) break;
+                    while ((sw[k] & ~kCountMask) == 0)
+                        sw[k] = ld_relaxed(status + (uint64_t)(t - k) * kDigits + d);
+                    excl += sw[k] & kCountMask;
+                    done = (sw[k] & kFlagPre) != 0;
+                }
                 if (done) break;
-                while ((sw[k] & ~kCountMask) == 0)
-                    sw[k] = ld_relaxed(status + (uint64_t)(t - k) * kDigits + d);
-                excl += sw[k] & kCountMask;
-                done = (sw[k] & kFlagPre) != 0;
             }
-            if (done) break;
+            st_relaxed(my, kFlagPre | (excl + cnt));
         }
-        st_relaxed(my, kFlagPre | (excl + cnt));
+        S.dstart[d] = dstart;
+        S.gbase[d] = digit_off[d] + excl;
     }
-    S.dstart[d] = dstart;
-    S.gbase[d] = digit_off[d] + excl;
     __syncthreads();
 
     // ---- reorder by digit in shared memory, then coalesced write-out
