@@ -340,15 +340,17 @@ __device__ __forceinline__ uint64_t probe_quads(const Probe &contains,
             uint32_t s = (j < nl ? d.pre[j] : 0xffffffffu) - wk;
             uint32_t starts = __reduce_or_sync(0xffffffffu, s < 32 ? (1u << s) : 0u);
             uint32_t li = i0 + __popc(starts & le_mask);
-            uint32_t t = wk + lane;
-            uint32_t qi = d.qb[li] + t;
-            r[k] = t < ie ? d.rng[li] : make_uint2(0u, 0u);
+            const uint32_t t = wk + lane;
+            const bool live = t < ie;
+            // lanes past ie load slot 0 of col+ (always allocated, >= 256 bytes) and are
+            // masked by an empty range
+            uint32_t qi = live ? d.qb[li] + t : 0u;
+            r[k] = d.rng[li];
+            if (!live) r[k].y = r[k].x;
             e0[k] = qi << kSlotShift;
             ly[k] = PV ? d.vid[li] : 0u;
 #pragma unroll
-            for (int v = 0; v < kSlot / 4; v++)
-                q[k][v] = t < ie ? __ldg(col4 + (uint64_t)qi * (kSlot / 4) + v)
-                                 : make_uint4(0u, 0u, 0u, 0u);
+            for (int v = 0; v < kSlot / 4; v++) q[k][v] = __ldg(col4 + (uint64_t)qi * (kSlot / 4) + v);
             i0 = __shfl_sync(0xffffffffu, li, 31);  // list holding slot wk + 31
         }
 #pragma unroll
