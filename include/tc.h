@@ -67,7 +67,7 @@ extern "C" {
 enum {
     TC_CLEAN = 1u << 0,      /* input is already simple and symmetric: no self-loops, no
                                 duplicate arcs, (u,v) present iff (v,u).  Skips step a1.    */
-    TC_SORTED = 1u << 1,     /* with TC_CLEAN: every row ascending; skips the segmented sort */
+    TC_SORTED = 1u << 1,     /* with TC_CLEAN: every row ascending (checked by TC_VALIDATE)   */
     TC_PER_VERTEX = 1u << 2, /* fill per_vertex[n] with t(v)                                  */
     TC_HOST_PTRS = 1u << 3,  /* all arrays are host pointers                                   */
     TC_VALIDATE = 1u << 4,   /* check the graph on the device; TC_EGRAPH on violation          */
@@ -100,7 +100,8 @@ typedef struct {
     uint32_t hub_min_dplus;     /* HASH owners with d+ >= this get a whole CTA (capped at 129)  */
     int32_t force_variant;      /* TC_VARIANT_AUTO, or route EVERY edge to one variant          */
     void *stream;               /* cudaStream_t to run on; NULL = legacy default stream         */
-    uint32_t segsort_block_max; /* rows longer than this use the global segmented-sort path     */
+    uint32_t segsort_block_max; /* ignored (kept for layout stability): rows are sorted by the
+                                   two-key radix sort of a3/a4 on every path                 */
     uint32_t reserved[9];       /* must be zero                                                 */
 } tc_options;
 
@@ -108,7 +109,7 @@ typedef struct {
     /* phase times (ms, CUDA events on the call's stream); 0 when the phase did not run */
     double ms_clean;     /* a1: keys, radix sort, unique                                   */
     double ms_orient;    /* a2+a3: degrees, rank filter, compaction into N+ CSR            */
-    double ms_sort;      /* a4: segmented sort (TC_CLEAN without TC_SORTED)                */
+    double ms_sort;      /* a4: reported inside ms_orient (the two-key sort); always 0     */
     double ms_bin;       /* a5: work estimation + binning                                  */
     double ms_intersect; /* a6+a7: intersection kernels and the per-block reduction        */
     double ms_total;     /* whole call, including host<->device copies with TC_HOST_PTRS   */

@@ -231,9 +231,6 @@ void orient_clean(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, cons
 void to_original(Ctx &ctx, const Oriented &g, uint64_t *off_out, uint32_t *col_out);
 // pv_out[v] = pv_new[newid[v]].
 void per_vertex_to_original(Ctx &ctx, const Oriented &g, const uint64_t *pv_new, uint64_t *pv_out);
-// a4: sort each row of (off, col) ascending.
-void segmented_sort(Ctx &ctx, uint64_t n, const uint64_t *off, uint32_t *col, uint64_t m_cap,
-                    uint32_t block_max);
 
 // HASH-variant context passed by value to the binning and intersection kernels.
 struct HashParams {

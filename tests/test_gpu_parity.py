@@ -256,3 +256,27 @@ def test_large_closed_forms():
     assert gpu_count(g.rowptr, g.col) == 3_280_500
     g = G.triangulated_grid(1000, 1000)
     assert gpu_count(g.rowptr, g.col) == 2 * 999 * 999
+
+
+def test_kronecker_exact_pins():
+    """Closed forms at scale (no oracle): T(B (x) C) = 6 T(B) T(C), t = 2 t_B t_C."""
+    k3 = G.kron_power(G.karate(), 3)
+    g = G.kron(k3, G.fig_mm())                               # n = 275,128, m = 37,964,160
+    got, pv = gpu_count(g.rowptr, g.col, per_vertex=True)
+    assert got == 6 * 3_280_500 * 3 == 59_049_000
+    # per-vertex closed form: t(u1, u2) = 2 t_{k3}(u1) t_{fig}(u2), with t_{k3} from the
+    # closed form again (karate^3 = karate (x) karate^2)
+    tk = np.array([18, 12, 11, 10, 2, 3, 3, 6, 5, 0, 2, 0, 1, 6, 1, 1, 1, 1, 1, 1, 1, 1, 1, 4,
+                   1, 1, 1, 1, 1, 4, 3, 3, 13, 15], dtype=np.uint64)      # karate (golden)
+    tk2 = 2 * np.outer(tk, tk).reshape(-1)
+    tk3 = 2 * np.outer(tk, tk2).reshape(-1)
+    tfig = np.array([2, 1, 0, 1, 2, 3, 0], dtype=np.uint64)
+    assert (pv_np(pv) == 2 * np.outer(tk3, tfig).reshape(-1)).all()
+
+
+def test_karate_fourth_power():
+    """karate^(x)4: n = 1,336,336, m = 296,120,448, T = 6^3 * 45^4 = 885,735,000 (s24-sized)."""
+    g = G.kron_power(G.karate(), 4)
+    got, st = gpu_count(g.rowptr, g.col, with_stats=True)
+    assert st["m_undirected"] == 2 ** 3 * 78 ** 4 == 296_120_448
+    assert got == 6 ** 3 * 45 ** 4 == 885_735_000
