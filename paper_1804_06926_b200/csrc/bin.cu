@@ -34,37 +34,6 @@ __device__ __forceinline__ void warp_append(bool take, uint64_t *counter, uint2 
     if (take) out[base + __popc(mask & ((1u << lane) - 1u))] = item;
 }
 
-// SHORT / MERGE / SEARCH bins (edge-centric); only launched when a policy uses them.
-__global__ void __launch_bounds__(kTileThreads)
-    k_bin(HashParams hp, const uint64_t *__restrict__ m_dev, uint2 *__restrict__ b_short,
-          uint2 *__restrict__ b_merge, uint2 *__restrict__ b_search, uint64_t *__restrict__ counts) {
-    __shared__ uint32_t s_row[kTileItems];
-    __shared__ uint32_t s_scan[kTileThreads / 32];
-    uint64_t m = *m_dev;
-    uint64_t t0 = (uint64_t)blockIdx.x * kTileItems;
-    if (t0 >= m) return;
-    uint32_t len = (uint32_t)min((uint64_t)kTileItems, m - t0);
-    tile_rows(hp.off, hp.n, t0, len, s_row, s_scan);
-    const uint64_t chunk = work_chunk(hp);
-    for (uint32_t base = 0; base < kTileItems; base += kTileThreads) {
-        uint32_t i = base + threadIdx.x;
-        int bin = -1;
-        uint2 item = make_uint2(0, 0);
-        if (i < len) {
-            uint64_t e = t0 + i;
-            uint32_t u = s_row[i], v = hp.col[e];
-            uint64_t uend = hp.off[u + 1];
-            uint32_t du = (uint32_t)(uend - hp.off[u]), dv = hp.dplus[v];
-            uint32_t suf = (uint32_t)(uend - e - 1);
-            if (rank_owner(hp, chunk, u) == hp.rank) bin = edge_bin(hp, du, dv, suf);
-            item = make_uint2(u, v);
-        }
-        warp_append(bin == TC_VARIANT_SHORT, &counts[0], b_short, item);
-        warp_append(bin == TC_VARIANT_MERGE, &counts[1], b_merge, item);
-        warp_append(bin == TC_VARIANT_SEARCH, &counts[2], b_search, item);
-    }
-}
-
 // For every CSR edge e = (u -> x) (row u, rows ascending), with p = pidx[e] its slot
 // in x's in-list:
 //   - x owns the edge (suf = |N+(u) after x| <= d+(x)): urange[p] = [e+1, end of row u),
@@ -72,10 +41,13 @@ __global__ void __launch_bounds__(kTileThreads)
 //   - u owns it (suf > d+(x), ~4% of R-MAT edges): orng[e] = [off[x], off[x] + d+(x)),
 //     an out-part entry of u (compacted in CSR order by k_ocompact);
 // the other slot gets an empty range.  Not-HASH / skipped / other-rank edges: both
-// empty.  Also accumulates the work statistics.
+// empty.  SHORT / MERGE / SEARCH edges are appended to their bins.  Also accumulates
+// the work statistics.
 __global__ void __launch_bounds__(kTileThreads)
     k_edges(HashParams hp, const uint64_t *__restrict__ m_dev, uint2 *__restrict__ urange,
-            uint2 *__restrict__ orng, uint64_t *__restrict__ counts) {
+            uint2 *__restrict__ orng, uint32_t *__restrict__ has_in, uint2 *__restrict__ b_short,
+            uint2 *__restrict__ b_merge, uint2 *__restrict__ b_search,
+            uint64_t *__restrict__ counts) {
     __shared__ uint32_t s_row[kTileItems];
     __shared__ uint32_t s_scan[kTileThreads / 32];
     __shared__ uint64_t s_red[kTileThreads / 32];
@@ -86,27 +58,39 @@ __global__ void __launch_bounds__(kTileThreads)
     tile_rows(hp.off, hp.n, t0, len, s_row, s_scan);
     const uint64_t chunk = work_chunk(hp);
     uint64_t W = 0, probe = 0, skipped = 0, hashed = 0;
-    for (uint32_t i = threadIdx.x; i < len; i += kTileThreads) {
-        uint64_t e = t0 + i;
-        uint32_t u = s_row[i], x = hp.col[e];
-        uint64_t ue = hp.off[u + 1];
-        uint32_t du = (uint32_t)(ue - hp.off[u]), dv = hp.dplus[x], suf = (uint32_t)(ue - e - 1);
-        W += du + dv;
-        probe += min(suf, dv);
-        int bin = edge_bin(hp, du, dv, suf);
-        skipped += bin < 0;
-        uint2 ri = make_uint2(0, 0), ro = make_uint2(0, 0);
-        if (bin == TC_VARIANT_HASH && rank_owner(hp, chunk, u) == hp.rank) {
-            hashed++;
-            if (suf <= dv) {
-                ri = make_uint2((uint32_t)(e + 1), (uint32_t)ue);
-            } else {
-                uint64_t xb = hp.off[x];
-                ro = make_uint2((uint32_t)xb, (uint32_t)(xb + dv));
+    // striped: each warp handles 32 consecutive edges per round (warp-aggregated appends)
+    for (uint32_t base = 0; base < kTileItems; base += kTileThreads) {
+        uint32_t i = base + threadIdx.x;
+        int bin = -1;
+        uint2 item = make_uint2(0, 0);
+        if (i < len) {
+            uint64_t e = t0 + i;
+            uint32_t u = s_row[i], x = hp.col[e];
+            uint64_t ue = hp.off[u + 1];
+            uint32_t du = (uint32_t)(ue - hp.off[u]), dv = hp.dplus[x], suf = (uint32_t)(ue - e - 1);
+            W += du + dv;
+            probe += min(suf, dv);
+            bin = edge_bin(hp, du, dv, suf);
+            skipped += bin < 0;
+            if (bin >= 0 && rank_owner(hp, chunk, u) != hp.rank) bin = -1;
+            item = make_uint2(u, x);
+            uint2 ri = make_uint2(0, 0), ro = make_uint2(0, 0);
+            if (bin == TC_VARIANT_HASH) {
+                hashed++;
+                if (suf <= dv) {
+                    ri = make_uint2((uint32_t)(e + 1), (uint32_t)ue);
+                    has_in[x] = 1u;   // x owns an in-part entry (benign racing stores)
+                } else {
+                    uint64_t xb = hp.off[x];
+                    ro = make_uint2((uint32_t)xb, (uint32_t)(xb + dv));
+                }
             }
+            urange[hp.pidx[e]] = ri;
+            orng[e] = ro;
         }
-        urange[hp.pidx[e]] = ri;
-        orng[e] = ro;
+        warp_append(bin == TC_VARIANT_SHORT, &counts[0], b_short, item);
+        warp_append(bin == TC_VARIANT_MERGE, &counts[1], b_merge, item);
+        warp_append(bin == TC_VARIANT_SEARCH, &counts[2], b_search, item);
     }
     W = block_sum_u64(W, s_red);
     probe = block_sum_u64(probe, s_red);
@@ -177,11 +161,12 @@ __global__ void k_ooff(const uint64_t *__restrict__ off, uint64_t n, const uint6
 }
 
 // Owner lists and max d+.  pcnt[x] = probe entries of owner x = its in-degree (empty
-// entries included) + its compacted out-part entries; warp owners (d+ < cta_min), CTA
+// entries included; 0 if none of them is x's) + its compacted out-part entries; warp owners (d+ < cta_min), CTA
 // bitmap owners (rank span n-1-x plus a spare zero word fits kCtaBitmapBits) and CTA
 // hash owners (the rest).
 __global__ void k_owners(const uint32_t *__restrict__ dplus, const uint64_t *__restrict__ in_off,
-                         const uint64_t *__restrict__ ooff, uint64_t n, uint32_t cta_min,
+                         const uint32_t *__restrict__ has_in, const uint64_t *__restrict__ ooff,
+                         uint64_t n, uint32_t cta_min,
                          uint32_t *__restrict__ pcnt, uint32_t *__restrict__ owners_warp,
                          uint32_t *__restrict__ owners_cta, uint32_t *__restrict__ owners_bitmap,
                          uint64_t *__restrict__ counts) {
@@ -196,7 +181,8 @@ __global__ void k_owners(const uint32_t *__restrict__ dplus, const uint64_t *__r
             uint32_t du = dplus[u];
             local_max = max(local_max, du);
             uint32_t c = 0;
-            if (du) c = (uint32_t)(in_off[u + 1] - in_off[u] + ooff[u + 1] - ooff[u]);
+            if (du) c = (has_in[u] ? (uint32_t)(in_off[u + 1] - in_off[u]) : 0u) +
+                        (uint32_t)(ooff[u + 1] - ooff[u]);
             pcnt[u] = c;
             if (c) kind = du < cta_min ? 0 : (n - 1 - u + 32 <= kCtaBitmapBits ? 2 : 1);
         }
@@ -284,16 +270,11 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
     hp.work_prefix = p.work_prefix;
     uint32_t tiles = (uint32_t)((cap + kTileItems - 1) / kTileItems);
 
-    // edge bins for the merge / search / two-pointer variants (only if a policy uses them)
+    // edge bins for the merge / search / two-pointer variants (filled by k_edges)
     const bool edge_bins = p.force == TC_VARIANT_SHORT || p.force == TC_VARIANT_MERGE ||
                            p.force == TC_VARIANT_SEARCH ||
                            (p.force < 0 && (p.short_max > 0 || p.skew_ratio > 0));
     for (int k = 0; k < 3; k++) bins.edges[k] = ctx.alloc<uint2>(edge_bins ? cap : 1);
-    if (edge_bins && tiles) {
-        k_bin<<<tiles, kTileThreads, 0, ctx.stream>>>(hp, g.m_dev, bins.edges[0], bins.edges[1],
-                                                      bins.edges[2], bins.count);
-        TC_LAUNCHED(ctx);
-    }
 
     // HASH: in-part ranges (in-list order), out-part entries (compacted, CSR order),
     // statistics, owners, tasks
@@ -302,8 +283,12 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
     uint32_t *ovid = ctx.alloc<uint32_t>(cap), *before = ctx.alloc<uint32_t>(cap);
     uint32_t *tcount = ctx.alloc<uint32_t>(tiles + 1);
     uint64_t *toff = ctx.alloc<uint64_t>(tiles + 1), *ooff = ctx.alloc<uint64_t>(n + 1);
+    uint32_t *has_in = ctx.alloc<uint32_t>(n + 1);
+    TC_CUDA(cudaMemsetAsync(has_in, 0, (n + 1) * sizeof(uint32_t), ctx.stream));
     if (tiles) {
-        k_edges<<<tiles, kTileThreads, 0, ctx.stream>>>(hp, g.m_dev, urange, orng, bins.count);
+        k_edges<<<tiles, kTileThreads, 0, ctx.stream>>>(hp, g.m_dev, urange, orng, has_in,
+                                                        bins.edges[0], bins.edges[1], bins.edges[2],
+                                                        bins.count);
         TC_LAUNCHED(ctx);
         k_ocount<<<tiles, kTileThreads, 0, ctx.stream>>>(orng, g.m_dev, tcount);
         TC_LAUNCHED(ctx);
@@ -318,6 +303,7 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
                                                            ooff);
     TC_LAUNCHED(ctx);
     hp.urange = urange;
+    hp.has_in = has_in;
     hp.orange = orange;
     hp.ovid = ovid;
     hp.ooff = ooff;
@@ -327,7 +313,7 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
     bins.owners_bitmap = ctx.alloc<uint32_t>(n);
     uint32_t cta_min = p.hub_min < kWarpTableSlots / 4 + 1 ? p.hub_min : kWarpTableSlots / 4 + 1;
     k_owners<<<ctx.persistent_grid(4), 256, 0, ctx.stream>>>(
-        g.dplus, g.in_off, ooff, n, cta_min, bins.pcnt, bins.owners_warp, bins.owners_cta,
+        g.dplus, g.in_off, has_in, ooff, n, cta_min, bins.pcnt, bins.owners_warp, bins.owners_cta,
         bins.owners_bitmap, bins.count);
     TC_LAUNCHED(ctx);
     make_tasks(ctx, n, cap, bins.owners_warp, bins.count + 8, bins.pcnt, g.dplus, kWarpTaskLists,

@@ -421,7 +421,8 @@ __global__ void __launch_bounds__(kIxThreads)
         uint64_t xb = hp.off[x];
         uint32_t dx = (uint32_t)(hp.off[x + 1] - xb);
         uint64_t inb = hp.in_off[x], ob = hp.ooff[x];
-        uint32_t indeg = (uint32_t)(hp.in_off[x + 1] - inb), ocnt = (uint32_t)(hp.ooff[x + 1] - ob);
+        uint32_t indeg = hp.has_in[x] ? (uint32_t)(hp.in_off[x + 1] - inb) : 0u;
+        uint32_t ocnt = (uint32_t)(hp.ooff[x + 1] - ob);
         uint32_t j0 = task.y * L;
         // descriptors of entries j0 + lane, j0 + 32 + lane; non-empty ones compacted in
         // order (the list-start bitmap of probe_quads needs distinct starts)
@@ -485,7 +486,8 @@ __global__ void __launch_bounds__(kIxThreads, 5)
         uint64_t xb = hp.off[x];
         uint32_t dx = (uint32_t)(hp.off[x + 1] - xb);
         uint64_t inb = hp.in_off[x], ob = hp.ooff[x];
-        uint32_t indeg = (uint32_t)(hp.in_off[x + 1] - inb), ocnt = (uint32_t)(hp.ooff[x + 1] - ob);
+        uint32_t indeg = hp.has_in[x] ? (uint32_t)(hp.in_off[x + 1] - inb) : 0u;
+        uint32_t ocnt = (uint32_t)(hp.ooff[x + 1] - ob);
         uint32_t lo, hi, y;
         hash_desc(hp, inb, indeg, ob, ocnt, task.y * L + threadIdx.x, lo, hi, y);
         uint32_t nq = quad_count(lo, hi);

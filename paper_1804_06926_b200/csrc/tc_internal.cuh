@@ -240,6 +240,8 @@ struct HashParams {
     const uint64_t *in_off = nullptr;  // transposed CSR: in-lists
     const uint32_t *in_src = nullptr;
     const uint32_t *pidx = nullptr;    // CSR edge e -> its in-list slot
+    const uint32_t *has_in = nullptr;  // x: 1 if some in-part entry of x is this rank's HASH
+                                       // work (else x's probe entries skip its in-list)
     const uint2 *urange = nullptr;     // in-edge p: probe range [lo, hi) of col+ (empty if none)
     const uint64_t *ooff = nullptr;    // compacted out-part entries of each owner:
     const uint2 *orange = nullptr;     //   probe ranges [lo, hi) of col+

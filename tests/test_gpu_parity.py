@@ -196,6 +196,27 @@ def test_shards_sum_to_total(world):
     assert sum(1 for p in parts if p > 0) >= min(world, 2)      # work really is split
 
 
+@pytest.mark.parametrize("short_max", [0, 8, 32, 128])
+@pytest.mark.parametrize("world", [1, 3])
+@pytest.mark.parametrize("gname", ["rmat", "chung_lu"])
+def test_shards_with_short_bin(gname, world, short_max):
+    """Owners whose in-part entries all left HASH (SHORT bin or another rank's sources)
+    keep only their out-part probe entries (regression: entry indexing must skip the
+    in-list consistently in the task builder and the kernels)."""
+    g = G.rmat(12, 8, seed=5) if gname == "rmat" else G.chung_lu(20000, 200000, seed=6)
+    T, t = O.count(g.n, g.rowptr, g.col, per_vertex=True)
+    rp, cl = on_dev(g.rowptr, g.col)
+    tot, pv_sum = 0, torch.zeros(g.n, dtype=torch.int64, device=DEV)
+    for r in range(world):
+        partial = torch.zeros(1, dtype=torch.int64, device=DEV)
+        pv = torch.zeros(g.n, dtype=torch.int64, device=DEV)
+        tc.count_shard(rp, cl, r, world, partial, per_vertex_partial=pv, short_max=short_max)
+        torch.cuda.synchronize()
+        tot += int(partial.item())
+        pv_sum += pv
+    assert tot == T and (pv_np(pv_sum) == t).all()
+
+
 # ------------------------------------------------------------------ errors
 def test_validate_rejects_bad_graphs():
     bad = [(np.array([0, 1, 2], np.uint64), np.array([1, 5], np.uint32)),     # id >= n
