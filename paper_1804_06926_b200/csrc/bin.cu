@@ -36,7 +36,8 @@ __device__ __forceinline__ void warp_append(bool take, uint64_t *counter, uint2 
 
 // For every CSR edge e = (u -> x) (row u, rows ascending), with p = pidx[e] its slot
 // in x's in-list:
-//   - x owns the edge (suf = |N+(u) after x| <= d+(x)): urange[p] = [e+1, end of row u),
+//   - x owns the edge (suf = |N+(u) after x| <= d+(x)): ulo[p] = e+1 (probe range
+//     [e+1, off[u+1]), the end re-read by the kernel from u = in_src[p]),
 //     an in-part entry of x;
 //   - u owns it (suf > d+(x), ~4% of R-MAT edges): orng[e] = [off[x], off[x] + d+(x)),
 //     an out-part entry of u (compacted in CSR order by k_ocompact);
@@ -44,8 +45,8 @@ __device__ __forceinline__ void warp_append(bool take, uint64_t *counter, uint2 
 // empty.  SHORT / MERGE / SEARCH edges are appended to their bins.  Also accumulates
 // the work statistics.
 __global__ void __launch_bounds__(kTileThreads)
-    k_edges(HashParams hp, const uint64_t *__restrict__ m_dev, uint2 *__restrict__ urange,
-            uint2 *__restrict__ orng, uint32_t *__restrict__ has_in, uint2 *__restrict__ b_short,
+    k_edges(HashParams hp, const uint64_t *__restrict__ m_dev, uint32_t *__restrict__ ulo,
+            uint2 *__restrict__ orng, uint2 *__restrict__ b_short,
             uint2 *__restrict__ b_merge, uint2 *__restrict__ b_search,
             uint64_t *__restrict__ counts) {
     __shared__ uint32_t s_row[kTileItems];
@@ -58,39 +59,61 @@ __global__ void __launch_bounds__(kTileThreads)
     tile_rows(hp.off, hp.n, t0, len, s_row, s_scan);
     const uint64_t chunk = work_chunk(hp);
     uint64_t W = 0, probe = 0, skipped = 0, hashed = 0;
-    // striped: each warp handles 32 consecutive edges per round (warp-aggregated appends)
-    for (uint32_t base = 0; base < kTileItems; base += kTileThreads) {
-        uint32_t i = base + threadIdx.x;
-        int bin = -1;
-        uint2 item = make_uint2(0, 0);
-        if (i < len) {
-            uint64_t e = t0 + i;
-            uint32_t u = s_row[i], x = hp.col[e];
-            uint64_t ue = hp.off[u + 1];
-            uint32_t du = (uint32_t)(ue - hp.off[u]), dv = hp.dplus[x], suf = (uint32_t)(ue - e - 1);
-            W += du + dv;
-            probe += min(suf, dv);
-            bin = edge_bin(hp, du, dv, suf);
-            skipped += bin < 0;
-            if (bin >= 0 && rank_owner(hp, chunk, u) != hp.rank) bin = -1;
-            item = make_uint2(u, x);
-            uint2 ri = make_uint2(0, 0), ro = make_uint2(0, 0);
-            if (bin == TC_VARIANT_HASH) {
-                hashed++;
-                if (suf <= dv) {
-                    ri = make_uint2((uint32_t)(e + 1), (uint32_t)ue);
-                    has_in[x] = 1u;   // x owns an in-part entry (benign racing stores)
-                } else {
-                    uint64_t xb = hp.off[x];
-                    ro = make_uint2((uint32_t)xb, (uint32_t)(xb + dv));
-                }
-            }
-            urange[hp.pidx[e]] = ri;
-            orng[e] = ro;
+    // striped: each warp handles 32 consecutive edges per round (warp-aggregated
+    // appends); the loads of kBatch rounds are issued before any is used
+    constexpr int kRounds = kTileItems / kTileThreads, kBatch = 4;
+#pragma unroll 1
+    for (int r0 = 0; r0 < kRounds; r0 += kBatch) {
+        uint32_t us[kBatch], xs[kBatch], ps[kBatch], dvs[kBatch];
+        uint64_t ubs[kBatch], ues[kBatch];
+#pragma unroll
+        for (int j = 0; j < kBatch; j++) {
+            uint32_t i = (r0 + j) * kTileThreads + threadIdx.x;
+            bool ok = i < len;
+            us[j] = ok ? s_row[i] : 0u;
+            xs[j] = ok ? hp.col[t0 + i] : 0u;
+            ps[j] = ok ? hp.pidx[t0 + i] : 0u;
         }
-        warp_append(bin == TC_VARIANT_SHORT, &counts[0], b_short, item);
-        warp_append(bin == TC_VARIANT_MERGE, &counts[1], b_merge, item);
-        warp_append(bin == TC_VARIANT_SEARCH, &counts[2], b_search, item);
+#pragma unroll
+        for (int j = 0; j < kBatch; j++) {
+            dvs[j] = hp.dplus[xs[j]];
+            ubs[j] = hp.off[us[j]];
+            ues[j] = hp.off[us[j] + 1];
+        }
+#pragma unroll
+        for (int j = 0; j < kBatch; j++) {
+            uint32_t i = (r0 + j) * kTileThreads + threadIdx.x;
+            int bin = -1;
+            uint2 item = make_uint2(0, 0);
+            if (i < len) {
+                uint64_t e = t0 + i;
+                uint32_t u = us[j], x = xs[j], dv = dvs[j];
+                uint64_t ue = ues[j];
+                uint32_t du = (uint32_t)(ue - ubs[j]), suf = (uint32_t)(ue - e - 1);
+                W += du + dv;
+                probe += min(suf, dv);
+                bin = edge_bin(hp, du, dv, suf);
+                skipped += bin < 0;
+                if (bin >= 0 && rank_owner(hp, chunk, u) != hp.rank) bin = -1;
+                item = make_uint2(u, x);
+                uint32_t ri = 0;
+                uint2 ro = make_uint2(0, 0);
+                if (bin == TC_VARIANT_HASH) {
+                    hashed++;
+                    if (suf <= dv) {
+                        ri = (uint32_t)(e + 1);
+                    } else {
+                        uint64_t xb = hp.off[x];
+                        ro = make_uint2((uint32_t)xb, (uint32_t)(xb + dv));
+                    }
+                }
+                ulo[ps[j]] = ri;
+                orng[e] = ro;
+            }
+            warp_append(bin == TC_VARIANT_SHORT, &counts[0], b_short, item);
+            warp_append(bin == TC_VARIANT_MERGE, &counts[1], b_merge, item);
+            warp_append(bin == TC_VARIANT_SEARCH, &counts[2], b_search, item);
+        }
     }
     W = block_sum_u64(W, s_red);
     probe = block_sum_u64(probe, s_red);
@@ -165,7 +188,8 @@ __global__ void k_ooff(const uint64_t *__restrict__ off, uint64_t n, const uint6
 // bitmap owners (rank span n-1-x plus a spare zero word fits kCtaBitmapBits) and CTA
 // hash owners (the rest).
 __global__ void k_owners(const uint32_t *__restrict__ dplus, const uint64_t *__restrict__ in_off,
-                         const uint32_t *__restrict__ has_in, const uint64_t *__restrict__ ooff,
+                         const uint32_t *__restrict__ ulo, uint32_t *__restrict__ has_in,
+                         const uint64_t *__restrict__ ooff,
                          uint64_t n, uint32_t cta_min,
                          uint32_t *__restrict__ pcnt, uint32_t *__restrict__ owners_warp,
                          uint32_t *__restrict__ owners_cta, uint32_t *__restrict__ owners_bitmap,
@@ -180,9 +204,18 @@ __global__ void k_owners(const uint32_t *__restrict__ dplus, const uint64_t *__r
         if (u < n) {
             uint32_t du = dplus[u];
             local_max = max(local_max, du);
-            uint32_t c = 0;
-            if (du) c = (has_in[u] ? (uint32_t)(in_off[u + 1] - in_off[u]) : 0u) +
-                        (uint32_t)(ooff[u + 1] - ooff[u]);
+            uint32_t c = 0, hin = 0;
+            if (du) {
+                // does some in-entry of u carry this rank's HASH work?  (first hit exits)
+                uint64_t ib = in_off[u], ie = in_off[u + 1];
+                for (uint64_t p = ib; p < ie; p++)
+                    if (ulo[p]) {
+                        hin = 1;
+                        break;
+                    }
+                c = (hin ? (uint32_t)(ie - ib) : 0u) + (uint32_t)(ooff[u + 1] - ooff[u]);
+            }
+            has_in[u] = hin;
             pcnt[u] = c;
             if (c) kind = du < cta_min ? 0 : (n - 1 - u + 32 <= kCtaBitmapBits ? 2 : 1);
         }
@@ -278,15 +311,15 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
 
     // HASH: in-part ranges (in-list order), out-part entries (compacted, CSR order),
     // statistics, owners, tasks
-    uint2 *urange = ctx.alloc<uint2>(cap), *orng = ctx.alloc<uint2>(cap);
+    uint32_t *ulo = ctx.alloc<uint32_t>(cap);
+    uint2 *orng = ctx.alloc<uint2>(cap);
     uint2 *orange = ctx.alloc<uint2>(cap);
     uint32_t *ovid = ctx.alloc<uint32_t>(cap), *before = ctx.alloc<uint32_t>(cap);
     uint32_t *tcount = ctx.alloc<uint32_t>(tiles + 1);
     uint64_t *toff = ctx.alloc<uint64_t>(tiles + 1), *ooff = ctx.alloc<uint64_t>(n + 1);
     uint32_t *has_in = ctx.alloc<uint32_t>(n + 1);
-    TC_CUDA(cudaMemsetAsync(has_in, 0, (n + 1) * sizeof(uint32_t), ctx.stream));
     if (tiles) {
-        k_edges<<<tiles, kTileThreads, 0, ctx.stream>>>(hp, g.m_dev, urange, orng, has_in,
+        k_edges<<<tiles, kTileThreads, 0, ctx.stream>>>(hp, g.m_dev, ulo, orng,
                                                         bins.edges[0], bins.edges[1], bins.edges[2],
                                                         bins.count);
         TC_LAUNCHED(ctx);
@@ -302,7 +335,7 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
     k_ooff<<<ctx.persistent_grid(4), 256, 0, ctx.stream>>>(g.off, n, g.m_dev, before, toff + tiles,
                                                            ooff);
     TC_LAUNCHED(ctx);
-    hp.urange = urange;
+    hp.ulo = ulo;
     hp.has_in = has_in;
     hp.orange = orange;
     hp.ovid = ovid;
@@ -313,7 +346,7 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
     bins.owners_bitmap = ctx.alloc<uint32_t>(n);
     uint32_t cta_min = p.hub_min < kWarpTableSlots / 4 + 1 ? p.hub_min : kWarpTableSlots / 4 + 1;
     k_owners<<<ctx.persistent_grid(4), 256, 0, ctx.stream>>>(
-        g.dplus, g.in_off, has_in, ooff, n, cta_min, bins.pcnt, bins.owners_warp, bins.owners_cta,
+        g.dplus, g.in_off, ulo, has_in, ooff, n, cta_min, bins.pcnt, bins.owners_warp, bins.owners_cta,
         bins.owners_bitmap, bins.count);
     TC_LAUNCHED(ctx);
     make_tasks(ctx, n, cap, bins.owners_warp, bins.count + 8, bins.pcnt, g.dplus, kWarpTaskLists,

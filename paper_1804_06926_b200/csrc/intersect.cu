@@ -382,18 +382,16 @@ __device__ __forceinline__ void hash_desc(const HashParams &hp, uint64_t inb, ui
                                           uint64_t ob, uint32_t ocnt, uint32_t j, uint32_t &lo,
                                           uint32_t &hi, uint32_t &y) {
     lo = hi = y = 0;
-    uint2 r;
     if (j < indeg) {
-        r = hp.urange[inb + j];
+        lo = hp.ulo[inb + j];
         y = hp.in_src[inb + j];
+        if (lo) hi = (uint32_t)hp.off[y + 1];
     } else if (j - indeg < ocnt) {
-        r = hp.orange[ob + (j - indeg)];
+        uint2 r = hp.orange[ob + (j - indeg)];
         y = hp.ovid[ob + (j - indeg)];
-    } else {
-        return;
+        lo = r.x;
+        hi = r.y;
     }
-    lo = r.x;
-    hi = r.y;
 }
 
 // Warp tasks: owners with d+(x) <= kWarpTableSlots/4 (table in the warp's smem slice).

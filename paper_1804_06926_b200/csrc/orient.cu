@@ -90,14 +90,30 @@ __global__ void __launch_bounds__(kTileThreads)
 }
 
 // ------------------------------------------------------------------ a2/a3 from pairs
+// E is sorted by (min, max): consecutive keys share their min, so the min side is
+// counted per run of equal mins inside a warp (one atomic per run); the max side
+// (distinct within a run) takes one atomic per key.
 __global__ void k_deg_pairs(const uint64_t *__restrict__ E, const uint64_t *__restrict__ m_dev,
                             int b, uint32_t *__restrict__ deg) {
     uint64_t m = *m_dev, mask = (1ull << b) - 1;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        uint64_t k = E[i];
-        atomicAdd(&deg[k >> b], 1u);
-        atomicAdd(&deg[k & mask], 1u);
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x; i0 < m; i0 += stride) {
+        uint64_t i = i0 + threadIdx.x;
+        bool ok = i < m;
+        uint64_t k = ok ? E[i] : 0;
+        uint32_t a = (uint32_t)(k >> b);
+        uint32_t prev = __shfl_up_sync(0xffffffffu, a, 1);
+        uint32_t valid = __ballot_sync(0xffffffffu, ok);   // a prefix of the warp
+        uint32_t heads = __ballot_sync(0xffffffffu, ok && (lane == 0 || prev != a));
+        if (ok) {
+            if ((heads >> lane) & 1u) {
+                uint32_t above = heads & ~((2u << lane) - 1u);
+                uint32_t end = above ? (uint32_t)(__ffs(above) - 1) : (uint32_t)__popc(valid);
+                atomicAdd(&deg[a], end - lane);
+            }
+            atomicAdd(&deg[k & mask], 1u);
+        }
     }
 }
 
@@ -105,14 +121,22 @@ __global__ void k_orient_pairs(const uint64_t *__restrict__ E, const uint64_t *_
                                int b, const uint32_t *__restrict__ newid, uint32_t *__restrict__ okey,
                                uint32_t *__restrict__ oval, uint32_t *__restrict__ dplus) {
     uint64_t m = *m_dev, mask = (1ull << b) - 1;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        uint64_t k = E[i];
-        uint32_t a = newid[k >> b], c = newid[k & mask];
-        uint32_t s = min(a, c), d = max(a, c);   // low -> high rank
-        okey[i] = s;
-        oval[i] = d;
-        atomicAdd(&dplus[s], 1u);
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x; i0 < m; i0 += stride) {
+        uint64_t i = i0 + threadIdx.x;
+        bool ok = i < m;
+        uint32_t s = 0xffffffffu;
+        if (ok) {
+            uint64_t k = E[i];
+            uint32_t a = newid[k >> b], c = newid[k & mask];
+            s = min(a, c);   // low -> high rank
+            okey[i] = s;
+            oval[i] = max(a, c);
+        }
+        // runs of one min often keep the same (low-rank) source: aggregate per warp
+        uint32_t peers = __match_any_sync(0xffffffffu, s);
+        if (ok && (peers & ((1u << lane) - 1u)) == 0) atomicAdd(&dplus[s], (uint32_t)__popc(peers));
     }
 }
 

@@ -93,28 +93,6 @@ __device__ __forceinline__ uint64_t block_sum_u64(uint64_t v, uint64_t *scratch)
     return total;
 }
 
-// Largest u in [0, n) with rowptr[u] <= x  (rowptr non-decreasing, rowptr[0] = 0).
-__device__ __forceinline__ uint64_t row_of(const uint64_t *__restrict__ rowptr, uint64_t n,
-                                           uint64_t x) {
-    uint64_t lo = 0, hi = n;  // answer in [lo, hi)
-    while (hi - lo > 1) {
-        uint64_t mid = (lo + hi) >> 1;
-        if (rowptr[mid] <= x) lo = mid; else hi = mid;
-    }
-    return lo;
-}
-
-// First u in [0, n] with rowptr[u] >= x.
-__device__ __forceinline__ uint64_t lower_bound_u64(const uint64_t *__restrict__ a, uint64_t len,
-                                                    uint64_t x) {
-    uint64_t lo = 0, hi = len;
-    while (lo < hi) {
-        uint64_t mid = (lo + hi) >> 1;
-        if (a[mid] < x) lo = mid + 1; else hi = mid;
-    }
-    return lo;
-}
-
 // ------------------------------------------------------------------ tiles
 // A "tile" is a contiguous range of kTileItems arcs (or oriented edges) handled
 // by one CTA of kTileThreads threads, each owning kItemsPerThread consecutive
@@ -127,17 +105,44 @@ constexpr int kTileItems = kTileThreads * kItemsPerThread;
 // (load-balanced row search: rows whose start falls inside the tile mark their
 // first item, then an inclusive max-scan propagates row ids).  Must be called
 // by all threads of the block.  s_scan: kTileThreads/32 uint32 scratch.
+// First i in [0, len] with a[i] >= x (a non-decreasing), found by one warp with a
+// 33-ary search (each round 32 lanes probe 32 split points: ~log33(len) dependent
+// L2 round trips instead of log2(len)).  Every lane returns the answer.
+__device__ __forceinline__ uint64_t warp_lower_bound(const uint64_t *__restrict__ a, uint64_t len,
+                                                     uint64_t x) {
+    const uint32_t lane = threadIdx.x & 31;
+    uint64_t lo = 0, hi = len;  // answer in [lo, hi]; a[lo-1] < x, a[hi] >= x (or hi = len)
+    while (hi - lo > 32) {
+        uint64_t idx = lo + (hi - lo) * (lane + 1) / 33;   // strictly inside [lo, hi)
+        uint32_t ge = __ballot_sync(0xffffffffu, a[idx] >= x);
+        int f = __ffs(ge) - 1;                               // first probe with a >= x
+        uint64_t below = __shfl_sync(0xffffffffu, idx, f > 0 ? f - 1 : 0);
+        uint64_t at = __shfl_sync(0xffffffffu, idx, f >= 0 ? f : 31);
+        if (f < 0) lo = at + 1;
+        else {
+            hi = at;
+            if (f > 0) lo = below + 1;
+        }
+    }
+    uint64_t i = lo + lane;
+    uint32_t ge = __ballot_sync(0xffffffffu, i < hi && a[i] >= x);
+    return ge ? lo + (uint64_t)(__ffs(ge) - 1) : hi;
+}
+
 __device__ __forceinline__ void tile_rows(const uint64_t *__restrict__ rowptr, uint64_t n, uint64_t tile_start,
                           uint32_t len, uint32_t *s_row, uint32_t *s_scan) {
     __shared__ uint64_t s_bounds[2];
     for (int i = threadIdx.x; i < kTileItems; i += blockDim.x) s_row[i] = 0;
-    if (threadIdx.x == 0) {
-        s_bounds[0] = lower_bound_u64(rowptr, n + 1, tile_start + 1);
-        s_bounds[1] = lower_bound_u64(rowptr, n + 1, tile_start + len);
+    // warp 0: first row starting after tile_start (its predecessor holds item
+    // tile_start); warp 1: first row starting at or after the tile's last item
+    if (threadIdx.x < 64) {
+        uint64_t b = warp_lower_bound(rowptr, n + 1, threadIdx.x < 32 ? tile_start + 1 : tile_start + len);
+        if ((threadIdx.x & 31) == 0) s_bounds[threadIdx.x >> 5] = b;
     }
     __syncthreads();
-    if (threadIdx.x == 0) atomicMax(&s_row[0], (uint32_t)row_of(rowptr, n, tile_start));
     uint64_t ulo = s_bounds[0], uhi = s_bounds[1];
+    // row of item tile_start = last u with rowptr[u] <= tile_start = ulo - 1 (ulo >= 1)
+    if (threadIdx.x == 0) atomicMax(&s_row[0], (uint32_t)(ulo - 1));
     for (uint64_t u = ulo + threadIdx.x; u < uhi; u += blockDim.x)
         atomicMax(&s_row[rowptr[u] - tile_start], (uint32_t)u);
     __syncthreads();
@@ -242,7 +247,8 @@ struct HashParams {
     const uint32_t *pidx = nullptr;    // CSR edge e -> its in-list slot
     const uint32_t *has_in = nullptr;  // x: 1 if some in-part entry of x is this rank's HASH
                                        // work (else x's probe entries skip its in-list)
-    const uint2 *urange = nullptr;     // in-edge p: probe range [lo, hi) of col+ (empty if none)
+    const uint32_t *ulo = nullptr;     // in-edge p = (u,x): e+1 (probe range [e+1, off[u+1]) of
+                                       // col+), 0 if not this rank's in-part HASH work
     const uint64_t *ooff = nullptr;    // compacted out-part entries of each owner:
     const uint2 *orange = nullptr;     //   probe ranges [lo, hi) of col+
     const uint32_t *ovid = nullptr;    //   the edge's target (per-vertex credit)
