@@ -4,7 +4,7 @@
 //   2. a tiny kernel turns them into per-pass exclusive digit offsets;
 //   3. per pass ONE kernel: each CTA takes the next tile (atomic ticket, so a
 //      tile only ever waits on tiles that already started), ranks its keys
-//      stably inside the tile (__match_any_sync per warp round), publishes its
+//      stably inside the tile (ballot-built digit peer masks per warp round), publishes its
 //      per-digit counts, and obtains the exclusive prefix of earlier tiles by
 //      DECOUPLED LOOK-BACK over their published (aggregate | inclusive) words.
 //      The tile is then reordered by digit in shared memory and written out as
@@ -82,6 +82,18 @@ __global__ void k_rs_digit_offsets(const uint32_t *__restrict__ hist, int passes
     }
 }
 
+// Lanes of `active` holding the same 8-bit digit d as this lane: 8 ballots, measured
+// a little faster than __match_any_sync on sm_100a.
+__device__ __forceinline__ uint32_t digit_peers(uint32_t active, uint32_t d) {
+    uint32_t peers = active;
+#pragma unroll
+    for (int b = 0; b < 8; b++) {
+        uint32_t m = __ballot_sync(active, (d >> b) & 1u);
+        peers &= ((d >> b) & 1u) ? m : ~m;
+    }
+    return peers;
+}
+
 template <class K, bool kVals>
 struct RsSmem {
     K keys[kRsTile];
@@ -128,7 +140,7 @@ __global__ void __launch_bounds__(kRsThreads, 2)
 #pragma unroll
         for (int j = 0; j < kRsRounds; j++) {
             uint32_t d = (uint32_t)(key[j] >> shift) & 0xffu;
-            uint32_t peers = __match_any_sync(0xffffffffu, d);
+            uint32_t peers = digit_peers(0xffffffffu, d);
             uint32_t old = wc[d];
             __syncwarp();
             if ((peers & lt) == 0) wc[d] = old + __popc(peers);
@@ -149,7 +161,7 @@ __global__ void __launch_bounds__(kRsThreads, 2)
             uint32_t active = __ballot_sync(0xffffffffu, ok);
             uint32_t old = 0, peers = 0;
             if (ok) {
-                peers = __match_any_sync(active, d);
+                peers = digit_peers(active, d);
                 old = wc[d];
             }
             __syncwarp();
