@@ -184,7 +184,16 @@ __global__ void __launch_bounds__(kIxThreads)
 // starts inside the window (reduce-or + popc): no per-item search.
 constexpr uint32_t kHashSlots = 4096;  // CTA table capacity (power of two), 16 KB
 constexpr uint32_t kHashChunk = 1024;  // owner elements per table build (load factor <= 1/4)
-constexpr int kUnroll = 2;             // independent 32-quad windows per probe step
+#ifndef TC_HASH_UNROLL
+#define TC_HASH_UNROLL 1
+#endif
+#ifndef TC_HASH_WARP_MINBLOCKS
+#define TC_HASH_WARP_MINBLOCKS 1
+#endif
+#ifndef TC_HASH_CTA_MINBLOCKS
+#define TC_HASH_CTA_MINBLOCKS 8
+#endif
+constexpr int kUnroll = TC_HASH_UNROLL;  // independent 32-slot windows per probe step
 constexpr int kHashWarps = kIxThreads / 32;
 
 // Explicit shared-memory accesses on 32-bit shared addresses (keeps the hot
@@ -268,17 +277,42 @@ __device__ __forceinline__ uint32_t opaque(uint32_t v) {
 struct HashProbe {  // bucket hash of the owner's N+ (any id range)
     uint32_t tab, absent;  // absent = the owner itself: never in its own N+
     int bits;
-    __device__ __forceinline__ uint32_t key(uint32_t e, bool valid) const { return valid ? e : absent; }
-    __device__ __forceinline__ uint32_t test(uint32_t k) const { return table_contains(tab, bits, k); }
+    // hits among the kSlot elements e[] of one slot; element c is in the list iff
+    // rel + c < len (mod 2^32)
+    template <int N>
+    __device__ __forceinline__ uint32_t count_slot(const uint32_t (&e)[N], uint32_t rel,
+                                                   uint32_t len) const {
+        uint32_t h = 0;
+#pragma unroll
+        for (int c = 0; c < N; c++) h += table_contains(tab, bits, rel + c < len ? e[c] : absent);
+        return h;
+    }
 };
 struct BitProbe {   // bitmap over the rank-id range [base, base + span) of the owner's N+
-    // Every element probed for owner x lies in (x, n) (it is in N+(u) after x, or in
-    // N+(v) for v > x), so its bit index is in range with no clamp; masked slots use
-    // index `zero`, a bit of the spare all-zero word after the bitmap.
+    // Any element e of col+ maps to bit min(e - base, zero) (mod 2^32): ids below base
+    // wrap high and land on `zero`, a bit of the spare all-zero word after the bitmap,
+    // so no load leaves the bitmap; elements outside the slot's list range are then
+    // removed by a per-slot mask instead of a per-element select.
     uint32_t bm, base, zero;
-    __device__ __forceinline__ uint32_t key(uint32_t e, bool valid) const { return valid ? e - base : zero; }
-    __device__ __forceinline__ uint32_t test(uint32_t o) const {
-        return (lds32(bm + 4 * (o >> 5)) >> (o & 31)) & 1u;
+    template <int N>
+    __device__ __forceinline__ uint32_t count_slot(const uint32_t (&e)[N], uint32_t rel,
+                                                   uint32_t len) const {
+        static_assert(N <= 32, "slot hit vector is one word");
+        uint32_t hv = 0;
+#pragma unroll
+        for (int c = 0; c < N; c++) {
+            uint32_t o = min(e[c] - base, zero);
+            uint32_t w = lds32(bm + 4 * (o >> 5));
+            // rotate bit (o & 31) of w to position c, collect it in hv
+            hv |= __funnelshift_r(w, w, o - c) & (1u << c);
+        }
+        // valid elements: c in [a, b).  rel < len: the slot starts inside the list,
+        // a = 0, b = min(N, hi - e0); else it starts before lo (a = min(N, lo - e0),
+        // b = min(N, hi - e0)) or at/after hi (a = N: none); len == 0 (masked lane): none
+        uint32_t a = rel < len ? 0u : min((uint32_t)N, 0u - rel);
+        uint32_t b = min((uint32_t)N, len - rel);
+        uint32_t m = len ? ((1u << b) - 1u) & ~((1u << a) - 1u) : 0u;
+        return __popc(hv & m);
     }
 };
 
@@ -356,15 +390,23 @@ __device__ __forceinline__ uint64_t probe_quads(const Probe &contains,
 #pragma unroll
         for (int k = 0; k < kUnroll; k++) {
             const uint32_t rel = e0[k] - r[k].x, len = r[k].y - r[k].x;  // mod 2^32
+            uint32_t e[kSlot];
 #pragma unroll
             for (int v = 0; v < kSlot / 4; v++) {
-                uint32_t e[4] = {q[k][v].x, q[k][v].y, q[k][v].z, q[k][v].w};
+                e[4 * v + 0] = q[k][v].x;
+                e[4 * v + 1] = q[k][v].y;
+                e[4 * v + 2] = q[k][v].z;
+                e[4 * v + 3] = q[k][v].w;
+            }
+            if (!PV) {
+                hits += contains.count_slot(e, rel, len);
+            } else {
 #pragma unroll
-                for (int c = 0; c < 4; c++) {
-                    // element idx = e0 + 4v + c is in [lo, hi) iff (idx - lo) mod 2^32 < hi - lo
-                    uint32_t h = contains.test(contains.key(e[c], rel + (4 * v + c) < len));
+                for (int c = 0; c < kSlot; c++) {
+                    uint32_t ec[1] = {e[c]};
+                    uint32_t h = contains.count_slot(ec, rel + c, len);
                     hits += h;
-                    if (PV && h) {
+                    if (h) {
                         atomicAdd((unsigned long long *)&pv[e[c]], 1ull);
                         atomicAdd((unsigned long long *)&pv[ly[k]], 1ull);
                     }
@@ -396,7 +438,7 @@ __device__ __forceinline__ void hash_desc(const HashParams &hp, uint64_t inb, ui
 
 // Warp tasks: owners with d+(x) <= kWarpTableSlots/4 (table in the warp's smem slice).
 template <bool PV>
-__global__ void __launch_bounds__(kIxThreads)
+__global__ void __launch_bounds__(kIxThreads, TC_HASH_WARP_MINBLOCKS)
     k_hash_warp(const uint2 *__restrict__ tasks, const uint64_t *__restrict__ ntasks, HashParams hp,
                 uint64_t *__restrict__ total, uint64_t *__restrict__ pv) {
     constexpr uint32_t L = kWarpTaskLists;
@@ -460,7 +502,7 @@ __global__ void __launch_bounds__(kIxThreads)
 constexpr uint32_t kSmemWords = kHashSlots;            // 16 KB of table / bitmap per CTA
 static_assert(kCtaBitmapBits == kSmemWords * 32, "bitmap owners are classified in bin.cu");
 template <bool PV, bool kBitmap>
-__global__ void __launch_bounds__(kIxThreads, 5)
+__global__ void __launch_bounds__(kIxThreads, TC_HASH_CTA_MINBLOCKS)
     k_hash_cta(const uint2 *__restrict__ tasks, const uint64_t *__restrict__ ntasks, HashParams hp,
                uint64_t *__restrict__ total, uint64_t *__restrict__ pv) {
     constexpr uint32_t L = kCtaTaskLists;
