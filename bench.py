@@ -289,6 +289,25 @@ def main():
                 line["roofline"]["traffic_source"] = tr["source"]
         except (OSError, ValueError):
             pass
+    if world == 1:
+        # NEXT-1: clustering coefficients + transitivity on the same
+        # workload through tc_clustering (count with t(v), then the c(v) kernel)
+        cev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(3)]
+        tc.clustering(rp, cl)
+        for a, b in cev:
+            flush.fill_(1)
+            a.record(stream)
+            _, summ = tc.clustering(rp, cl)
+            b.record(stream)
+        torch.cuda.synchronize()
+        cms = sum(a.elapsed_time(b) for a, b in cev) / len(cev)
+        assert summ["triangles"] == T_total
+        line["next_rows"] = {"NEXT-1 clustering": {
+            "ms_per_call": cms, "edges_per_s": m / (cms * 1e-3), "overhead_vs_count_ms": cms - ms,
+            "transitivity": summ["transitivity"], "avg_clustering": summ["avg_clustering"],
+            "wedges": summ["wedges"],
+            "call": "tc_clustering (device pointers): count with per-vertex t(v) + local c(v) for all n"}}
     if world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline(g, m)
         assert cb.pop("T") == T_total, "oracle and CUDA path disagree"

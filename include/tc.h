@@ -166,6 +166,31 @@ tc_status tc_orient(uint64_t n, uint64_t m, const uint64_t *row_offsets,
                     const uint32_t *col_indices, uint32_t flags, const tc_options *opt,
                     uint64_t *off_plus, uint32_t *col_plus, uint64_t *m_plus);
 
+/* NEXT-1: "with little modification ... clustering coefficient
+ * and transitivity".  With t(v) the per-vertex triangle count
+ * and d(v) the degree of the cleaned graph (reading R14):
+ *   local_cc[v]    = 2 t(v) / (d(v) (d(v) - 1)), 0 when d(v) < 2       (double, n entries)
+ *   wedges         = sum_v d(v) (d(v) - 1) / 2   (connected triples, exact uint64)
+ *   transitivity   = 3 T / wedges, 0 when wedges = 0
+ *   avg_clustering = (1/n) sum_v local_cc[v] over all n vertices (isolated ones give 0)
+ * Each local_cc[v] and the transitivity are ONE correctly rounded fp64 division of
+ * exact integers; avg_clustering is an fp64 sum (deterministic order for a given
+ * device, not the oracle's order).  Flags: TC_CLEAN, TC_SORTED, TC_HOST_PTRS,
+ * TC_VALIDATE (TC_PER_VERTEX is implied).  local_cc and per_vertex (uint64 t(v))
+ * are optional outputs (NULL = not wanted) on the TC_HOST_PTRS side; summary and
+ * stats are host structs (nullable).  Synchronous. */
+typedef struct {
+    uint64_t triangles;     /* T */
+    uint64_t wedges;        /* sum_v C(d(v), 2) */
+    double transitivity;    /* 3T / wedges */
+    double avg_clustering;  /* mean of local_cc over all n vertices */
+} tc_clustering_summary;
+
+tc_status tc_clustering(uint64_t n, uint64_t m, const uint64_t *row_offsets,
+                        const uint32_t *col_indices, uint32_t flags, const tc_options *opt,
+                        double *local_cc, uint64_t *per_vertex, tc_clustering_summary *summary,
+                        tc_stats *stats);
+
 /* Thread-local message describing the last failure on this thread ("" if none). */
 const char *tc_last_error(void);
 

@@ -57,6 +57,10 @@ def _load():
         lib.oracle_vertex_triangles.restype = ctypes.c_uint64
         lib.oracle_vertex_triangles.argtypes = [ctypes.c_uint64, _u64p, _u32p, ctypes.c_uint64]
         lib.oracle_num_threads.restype = ctypes.c_int
+        lib.oracle_clustering.restype = None
+        lib.oracle_clustering.argtypes = [ctypes.c_uint64, _u64p, _u64p, ctypes.c_uint64,
+                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                          ctypes.c_void_p]
         _lib = lib
     return _lib
 
@@ -136,6 +140,24 @@ def vertex_triangles(n: int, clean_rowptr, clean_col, v: int) -> int:
     lib = _load()
     clean_rowptr, clean_col = _csr(clean_rowptr, clean_col)
     return int(lib.oracle_vertex_triangles(n, _p64(clean_rowptr), _p32(clean_col), v))
+
+
+def clustering(n: int, rowptr, col):
+    """NEXT-1: (local cc[n], summary dict) of the simple graph the
+    arcs define -- clean, per-vertex counts, then the definitions in tc_oracle.c."""
+    lib = _load()
+    crow, ccol = clean(n, rowptr, col)
+    T, t = count(n, rowptr, col, per_vertex=True)
+    t = np.ascontiguousarray(t, dtype=np.uint64)
+    cc = np.zeros(max(n, 1), dtype=np.float64)
+    w = np.zeros(1, dtype=np.uint64)
+    s = np.zeros(1, dtype=np.float64)
+    tr = np.zeros(1, dtype=np.float64)
+    lib.oracle_clustering(n, _p64(crow), _p64(t) if n else None, T, cc.ctypes.data, w.ctypes.data,
+                          s.ctypes.data, tr.ctypes.data)
+    summary = dict(triangles=T, wedges=int(w[0]), transitivity=float(tr[0]),
+                   avg_clustering=float(s[0]) / n if n else 0.0)
+    return cc[:n], summary
 
 
 def num_threads() -> int:

@@ -246,6 +246,35 @@ uint64_t oracle_vertex_triangles(uint64_t n, const uint64_t *rowptr, const uint3
     return twice / 2;
 }
 
+/*
+ * NEXT-1 ("clustering coefficient and
+ * transitivity"), conventions of SURVEY §8(c) reading 9 / DESIGN.md R14, written
+ * out by definition on the CLEAN symmetric CSR (d(v) = row length) and the
+ * per-vertex counts t(v):
+ *   cc[v]   = 2 t(v) / (d(v) (d(v) - 1)), 0 when d(v) < 2;
+ *   *wedges = sum_v d(v) (d(v) - 1) / 2 (connected triples);
+ *   *sum    = sum_v cc[v], added in vertex order;
+ *   *trans  = 3 T / *wedges, 0 when there is no wedge.
+ */
+void oracle_clustering(uint64_t n, const uint64_t *rowptr, const uint64_t *t, uint64_t T,
+                       double *cc, uint64_t *wedges, double *sum, double *trans) {
+    uint64_t w = 0;
+    double s = 0.0;
+    for (uint64_t v = 0; v < n; v++) {
+        uint64_t d = rowptr[v + 1] - rowptr[v];
+        double c = 0.0;
+        if (d >= 2) {
+            c = (2.0 * (double)t[v]) / (double)(d * (d - 1));
+            w += d * (d - 1) / 2;
+        }
+        cc[v] = c;
+        s += c;
+    }
+    *wedges = w;
+    *sum = s;
+    *trans = w ? (3.0 * (double)T) / (double)w : 0.0;
+}
+
 int oracle_num_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

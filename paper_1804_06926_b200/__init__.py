@@ -17,7 +17,7 @@ import os
 
 import numpy as np
 
-__all__ = ["count", "count_ex", "count_shard", "orient", "stats_dict", "library_path",
+__all__ = ["count", "count_ex", "count_shard", "orient", "clustering", "stats_dict", "library_path",
            "TC_CLEAN", "TC_SORTED", "TC_PER_VERTEX", "TC_HOST_PTRS", "TC_VALIDATE",
            "VARIANT_AUTO", "VARIANT_SHORT", "VARIANT_MERGE", "VARIANT_SEARCH", "VARIANT_HASH",
            "TCError"]
@@ -57,6 +57,11 @@ class Stats(ctypes.Structure):
                 ("bytes_hash", ctypes.c_uint64)]
 
 
+class ClusteringSummary(ctypes.Structure):
+    _fields_ = [("triangles", ctypes.c_uint64), ("wedges", ctypes.c_uint64),
+                ("transitivity", ctypes.c_double), ("avg_clustering", ctypes.c_double)]
+
+
 _lib = None
 
 
@@ -85,6 +90,9 @@ def _load():
     lib.tc_count_shard.restype = ctypes.c_int
     lib.tc_orient.argtypes = [u64, u64, vp, vp, u32, ctypes.POINTER(Options), vp, vp, vp]
     lib.tc_orient.restype = ctypes.c_int
+    lib.tc_clustering.argtypes = [u64, u64, vp, vp, u32, ctypes.POINTER(Options), vp, vp,
+                                  ctypes.POINTER(ClusteringSummary), ctypes.POINTER(Stats)]
+    lib.tc_clustering.restype = ctypes.c_int
     lib.tc_last_error.argtypes = []
     lib.tc_last_error.restype = ctypes.c_char_p
     lib.tc_version.argtypes = []
@@ -224,6 +232,47 @@ def orient(rowptr, col, *, clean=False, sorted_rows=False, stream=None, **opts):
         _check(lib.tc_orient(n, M, rp, cp, flags, ctypes.byref(o), off.ctypes.data, colp.ctypes.data,
                              ctypes.addressof(mp)))
     return off, colp[:mp.value]
+
+
+def clustering(rowptr, col, *, clean=False, sorted_rows=False, validate=False, per_vertex=False,
+               local=True, stream=None, with_stats=False, **opts):
+    """NEXT-1: (local clustering coefficients or None, summary dict[, t(v)][, stats]).
+
+    local_cc[v] = 2t(v)/(d(v)(d(v)-1)) (0 if d(v) < 2); summary = triangles, wedges,
+    transitivity = 3T/wedges, avg_clustering over all n vertices (include/tc.h).
+    Outputs live on the input's side (CUDA tensors or numpy arrays).
+    """
+    lib = _load()
+    n, M, rp, cp, on_dev, keep = _arrays(rowptr, col)
+    flags = (TC_CLEAN if clean else 0) | (TC_SORTED if sorted_rows else 0) | \
+            (TC_VALIDATE if validate else 0) | (0 if on_dev else TC_HOST_PTRS)
+    o = _options(stream=stream, on_device=on_dev, **opts)
+    cc = pv = None
+    if on_dev:
+        import torch
+        dev = keep[0].device
+        if local:
+            cc = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+        if per_vertex:
+            pv = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+        ptr = lambda a: a.data_ptr() if a is not None else None  # noqa: E731
+    else:
+        if local:
+            cc = np.zeros(max(n, 1), dtype=np.float64)
+        if per_vertex:
+            pv = np.zeros(max(n, 1), dtype=np.uint64)
+        ptr = lambda a: a.ctypes.data if a is not None else None  # noqa: E731
+    summ = ClusteringSummary()
+    st = Stats()
+    _check(lib.tc_clustering(n, M, rp, cp, flags, ctypes.byref(o), ptr(cc), ptr(pv), ctypes.byref(summ),
+                             ctypes.byref(st) if with_stats else None))
+    out = [cc[:n] if cc is not None else None,
+           {f: getattr(summ, f) for f, _ in ClusteringSummary._fields_}]
+    if per_vertex:
+        out.append(pv[:n])
+    if with_stats:
+        out.append(stats_dict(st))
+    return tuple(out)
 
 
 def version() -> str:

@@ -255,6 +255,19 @@ __device__ __noinline__ uint32_t table_contains_slow(uint32_t tab, uint32_t bmas
     }
 }
 
+// Slot index of w, which is known to be in the table (per-vertex credits).
+__device__ __forceinline__ uint32_t table_find(uint32_t tab, int bits, uint32_t w) {
+    uint32_t bmask = (1u << (bits - 2)) - 1u, b = hash_slot(w, bits - 2);
+    while (true) {
+        uint4 q = lds128(tab + 16 * b);
+        if (q.x == w) return 4 * b;
+        if (q.y == w) return 4 * b + 1;
+        if (q.z == w) return 4 * b + 2;
+        if (q.w == w) return 4 * b + 3;
+        b = (b + 1) & bmask;
+    }
+}
+
 // 1 if w is in the table at shared address `tab`.
 __device__ __forceinline__ uint32_t table_contains(uint32_t tab, int bits, uint32_t w) {
     uint32_t b = hash_slot(w, bits - 2);
@@ -277,15 +290,26 @@ __device__ __forceinline__ uint32_t opaque(uint32_t v) {
 struct HashProbe {  // bucket hash of the owner's N+ (any id range)
     uint32_t tab, absent;  // absent = the owner itself: never in its own N+
     int bits;
-    // hits among the kSlot elements e[] of one slot; element c is in the list iff
-    // rel + c < len (mod 2^32)
+    // per-vertex mode: hit counters per table slot (cnt != nullptr), else global atomics
+    uint32_t *cnt = nullptr;
+    // bit c set iff element c of the slot is in the list (rel + c < len, mod 2^32)
+    // and in the table
     template <int N>
-    __device__ __forceinline__ uint32_t count_slot(const uint32_t (&e)[N], uint32_t rel,
-                                                   uint32_t len) const {
+    __device__ __forceinline__ uint32_t hit_mask(const uint32_t (&e)[N], uint32_t rel,
+                                                 uint32_t len) const {
         uint32_t h = 0;
 #pragma unroll
-        for (int c = 0; c < N; c++) h += table_contains(tab, bits, rel + c < len ? e[c] : absent);
+        for (int c = 0; c < N; c++)
+            h |= table_contains(tab, bits, rel + c < len ? e[c] : absent) << c;
         return h;
+    }
+    // per-vertex credit of a hit's third vertex w
+    __device__ __forceinline__ void credit(uint32_t w, uint64_t *pv) const {
+        if (!cnt) {
+            atomicAdd((unsigned long long *)&pv[w], 1ull);
+            return;
+        }
+        atomicAdd(&cnt[table_find(tab, bits, w)], 1u);
     }
 };
 struct BitProbe {   // bitmap over the rank-id range [base, base + span) of the owner's N+
@@ -294,9 +318,13 @@ struct BitProbe {   // bitmap over the rank-id range [base, base + span) of the 
     // so no load leaves the bitmap; elements outside the slot's list range are then
     // removed by a per-slot mask instead of a per-element select.
     uint32_t bm, base, zero;
+    // per-vertex mode: hits of w are counted in shared memory at w's rank among the
+    // owner's set bits (wpre = per-word prefix popcounts) when cnt != nullptr
+    uint32_t *cnt = nullptr;
+    const uint16_t *wpre = nullptr;
     template <int N>
-    __device__ __forceinline__ uint32_t count_slot(const uint32_t (&e)[N], uint32_t rel,
-                                                   uint32_t len) const {
+    __device__ __forceinline__ uint32_t hit_mask(const uint32_t (&e)[N], uint32_t rel,
+                                                 uint32_t len) const {
         static_assert(N <= 32, "slot hit vector is one word");
         uint32_t hv = 0;
 #pragma unroll
@@ -312,7 +340,16 @@ struct BitProbe {   // bitmap over the rank-id range [base, base + span) of the 
         uint32_t a = rel < len ? 0u : min((uint32_t)N, 0u - rel);
         uint32_t b = min((uint32_t)N, len - rel);
         uint32_t m = len ? ((1u << b) - 1u) & ~((1u << a) - 1u) : 0u;
-        return __popc(hv & m);
+        return hv & m;
+    }
+    __device__ __forceinline__ void credit(uint32_t w, uint64_t *pv) const {
+        if (!cnt) {
+            atomicAdd((unsigned long long *)&pv[w], 1ull);
+            return;
+        }
+        uint32_t o = w - base, word = lds32(bm + 4 * (o >> 5));
+        uint32_t idx = wpre[o >> 5] + __popc(word & ((1u << (o & 31)) - 1u));
+        atomicAdd(&cnt[idx], 1u);
     }
 };
 
@@ -398,19 +435,13 @@ __device__ __forceinline__ uint64_t probe_quads(const Probe &contains,
                 e[4 * v + 2] = q[k][v].z;
                 e[4 * v + 3] = q[k][v].w;
             }
-            if (!PV) {
-                hits += contains.count_slot(e, rel, len);
-            } else {
+            const uint32_t hm = contains.hit_mask(e, rel, len);
+            hits += __popc(hm);
+            if (PV && hm) {
 #pragma unroll
-                for (int c = 0; c < kSlot; c++) {
-                    uint32_t ec[1] = {e[c]};
-                    uint32_t h = contains.count_slot(ec, rel + c, len);
-                    hits += h;
-                    if (h) {
-                        atomicAdd((unsigned long long *)&pv[e[c]], 1ull);
-                        atomicAdd((unsigned long long *)&pv[ly[k]], 1ull);
-                    }
-                }
+                for (int c = 0; c < kSlot; c++)
+                    if ((hm >> c) & 1u) contains.credit(e[c], pv);
+                atomicAdd((unsigned long long *)&pv[ly[k]], (unsigned long long)__popc(hm));
             }
         }
     }
@@ -447,6 +478,7 @@ __global__ void __launch_bounds__(kIxThreads, TC_HASH_WARP_MINBLOCKS)
     __shared__ uint2 s_rng[kHashWarps][L];
     __shared__ uint32_t s_pre[kHashWarps][L + 1];
     __shared__ uint32_t s_vid[kHashWarps][PV ? L : 1];
+    __shared__ uint32_t s_cnt[PV ? kHashWarps : 1][PV ? kWarpTableSlots : 1];  // per-vertex hits per slot
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const QuadDesc d{s_pre[wib], s_qb[wib], s_vid[wib], s_rng[wib]};
     uint64_t nt = *ntasks;
@@ -480,13 +512,20 @@ __global__ void __launch_bounds__(kIxThreads, TC_HASH_WARP_MINBLOCKS)
         }
         if (lane == 0) d.pre[nl] = run;
         int bits = table_bits(dx);
-        for (uint32_t s = lane; s < (1u << bits); s += 32) tab[s] = kEmpty;
+        for (uint32_t s = lane; s < (1u << bits); s += 32) {
+            tab[s] = kEmpty;
+            if (PV) s_cnt[wib][s] = 0u;
+        }
         __syncwarp();
         table_insert(tab, bits, col + xb, dx, lane, 32);
         __syncwarp();
-        uint64_t h = probe_quads<PV>(HashProbe{opaque(smem_addr(tab)), x, bits}, d, nl, 0, run,
-                                     col, pv);
+        HashProbe hpb{opaque(smem_addr(tab)), x, bits};
+        if (PV) hpb.cnt = s_cnt[wib];
+        uint64_t h = probe_quads<PV>(hpb, d, nl, 0, run, col, pv);
         if (PV) {
+            __syncwarp();
+            for (uint32_t s = lane; s < (1u << bits); s += 32)
+                if (s_cnt[wib][s]) atomicAdd((unsigned long long *)&pv[tab[s]], (unsigned long long)s_cnt[wib][s]);
             uint64_t hw = warp_sum_u64(h);
             if (lane == 0 && hw) atomicAdd((unsigned long long *)&pv[x], (unsigned long long)hw);
         }
@@ -500,9 +539,10 @@ __global__ void __launch_bounds__(kIxThreads, TC_HASH_WARP_MINBLOCKS)
 // kBitmap: the owner's N+ (rank ids in (x, n)) is a bitmap over [x+1, n) -- one
 // 32-bit shared load per probe; otherwise the bucket hash (chunked if d+ > 2048).
 constexpr uint32_t kSmemWords = kHashSlots;            // 16 KB of table / bitmap per CTA
+constexpr uint32_t kPvCounters = 4096;                 // per-vertex: smem hit counters (16 KB)
 static_assert(kCtaBitmapBits == kSmemWords * 32, "bitmap owners are classified in bin.cu");
 template <bool PV, bool kBitmap>
-__global__ void __launch_bounds__(kIxThreads, TC_HASH_CTA_MINBLOCKS)
+__global__ void __launch_bounds__(kIxThreads, PV ? 4 : TC_HASH_CTA_MINBLOCKS)
     k_hash_cta(const uint2 *__restrict__ tasks, const uint64_t *__restrict__ ntasks, HashParams hp,
                uint64_t *__restrict__ total, uint64_t *__restrict__ pv) {
     constexpr uint32_t L = kCtaTaskLists;
@@ -513,6 +553,12 @@ __global__ void __launch_bounds__(kIxThreads, TC_HASH_CTA_MINBLOCKS)
     __shared__ uint32_t s_pre[L + 1];
     __shared__ uint32_t s_vid[PV ? L : 1];
     __shared__ uint64_t s_scan[kHashWarps];
+    // per-vertex bitmap owners: hit counters per element of N+(x) (owners with
+    // d+ <= kPvCounters; others credit w with global atomics) + word prefix popcounts
+    constexpr bool kCnt = PV;   // bitmap: counter per set bit; hash: counter per slot
+    static_assert(kPvCounters == kHashSlots, "hash owners count hits per table slot");
+    __shared__ uint32_t s_cnt[kCnt ? kPvCounters : 1];
+    __shared__ uint16_t s_wpre[kCnt && kBitmap ? kSmemWords + 1 : 1];
     const int wib = threadIdx.x >> 5;
     const QuadDesc d{s_pre, s_qb, s_vid, s_rng};
     const uint32_t tab = opaque(smem_addr(s_tab));
@@ -550,18 +596,51 @@ __global__ void __launch_bounds__(kIxThreads, TC_HASH_CTA_MINBLOCKS)
                 atomicOr(&s_tab[o >> 5], 1u << (o & 31));
             }
             __syncthreads();
-            h = probe_quads<PV>(BitProbe{tab, base, (words - 1) * 32 + 31}, d, nl, ib, ie, col, pv);
+            BitProbe bp{tab, base, (words - 1) * 32 + 31};
+            const bool use_cnt = kCnt && kBitmap && dx <= kPvCounters;
+            if (use_cnt) {
+                // exclusive prefix popcount per bitmap word (blocked: thread t owns a run)
+                const uint32_t per = (words + kIxThreads - 1) / kIxThreads;
+                const uint32_t w0 = min(words, threadIdx.x * per), w1 = min(words, w0 + per);
+                uint32_t c = 0;
+                for (uint32_t w = w0; w < w1; w++) c += __popc(s_tab[w]);
+                uint32_t run = (uint32_t)block_exclusive_scan<SumOp64>((uint64_t)c, s_scan);
+                for (uint32_t w = w0; w < w1; w++) {
+                    s_wpre[w] = (uint16_t)run;
+                    run += __popc(s_tab[w]);
+                }
+                for (uint32_t k = threadIdx.x; k < dx; k += blockDim.x) s_cnt[k] = 0u;
+                __syncthreads();
+                bp.cnt = s_cnt;
+                bp.wpre = s_wpre;
+            }
+            h = probe_quads<PV>(bp, d, nl, ib, ie, col, pv);
             __syncthreads();
+            if (use_cnt) {   // the k-th set bit is the k-th element of the sorted N+(x)
+                for (uint32_t k = threadIdx.x; k < dx; k += blockDim.x)
+                    if (s_cnt[k]) atomicAdd((unsigned long long *)&pv[col[xb + k]], (unsigned long long)s_cnt[k]);
+                __syncthreads();
+            }
         } else {
             for (uint32_t c0 = 0; c0 < dx; c0 += kHashChunk) {
                 uint32_t clen = min(kHashChunk, dx - c0);
                 int bits = table_bits(clen);
-                for (uint32_t s = threadIdx.x; s < (1u << bits); s += blockDim.x) s_tab[s] = kEmpty;
+                for (uint32_t s = threadIdx.x; s < (1u << bits); s += blockDim.x) {
+                    s_tab[s] = kEmpty;
+                    if (kCnt) s_cnt[s] = 0u;
+                }
                 __syncthreads();
                 table_insert(s_tab, bits, col + xb + c0, clen, threadIdx.x, blockDim.x);
                 __syncthreads();
-                h += probe_quads<PV>(HashProbe{tab, x, bits}, d, nl, ib, ie, col, pv);
+                HashProbe hpb{tab, x, bits};
+                if (kCnt) hpb.cnt = s_cnt;
+                h += probe_quads<PV>(hpb, d, nl, ib, ie, col, pv);
                 __syncthreads();
+                if (kCnt) {
+                    for (uint32_t s = threadIdx.x; s < (1u << bits); s += blockDim.x)
+                        if (s_cnt[s]) atomicAdd((unsigned long long *)&pv[s_tab[s]], (unsigned long long)s_cnt[s]);
+                    __syncthreads();
+                }
             }
         }
         if (PV) {

@@ -14,9 +14,18 @@
 
 namespace tc {
 
-constexpr int kRsThreads = 512;
+#ifndef TC_RS_THREADS
+#define TC_RS_THREADS 512
+#endif
+#ifndef TC_RS_ROUNDS
+#define TC_RS_ROUNDS 8
+#endif
+#ifndef TC_RS_MINBLOCKS
+#define TC_RS_MINBLOCKS 2
+#endif
+constexpr int kRsThreads = TC_RS_THREADS;
 constexpr int kRsWarps = kRsThreads / 32;
-constexpr int kRsRounds = 8;                           // 32-item rounds per warp
+constexpr int kRsRounds = TC_RS_ROUNDS;                // 32-item rounds per warp
 constexpr int kRsWarpItems = 32 * kRsRounds;           // 256
 constexpr int kRsTile = kRsWarps * kRsWarpItems;       // 4096 items per tile
 constexpr int kDigits = 256;
@@ -106,7 +115,7 @@ struct RsSmem {
 };
 
 template <class K, bool kVals>
-__global__ void __launch_bounds__(kRsThreads, 2)
+__global__ void __launch_bounds__(kRsThreads, TC_RS_MINBLOCKS)
     k_rs_pass(const K *__restrict__ keys, const uint32_t *__restrict__ vals, K *__restrict__ keys_out,
               uint32_t *__restrict__ vals_out, uint64_t cap, const uint64_t *__restrict__ count_dev,
               int shift, const uint64_t *__restrict__ digit_off, uint32_t *__restrict__ ticket,

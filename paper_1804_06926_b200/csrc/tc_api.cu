@@ -44,7 +44,7 @@ static uint64_t *pinned_scratch() {
     return p;
 }
 
-enum Mode { kCount, kShard, kOrientOnly };
+enum Mode { kCount, kShard, kOrientOnly, kClustering };
 
 struct Call {
     uint64_t n, M;
@@ -62,6 +62,8 @@ struct Call {
     uint64_t *off_plus = nullptr;     // kOrientOnly
     uint32_t *col_plus = nullptr;
     uint64_t *m_plus = nullptr;
+    double *cc = nullptr;             // kClustering (nullable)
+    tc_clustering_summary *csum = nullptr;
 };
 
 static tc_status check_args(const Call &c) {
@@ -70,6 +72,8 @@ static tc_status check_args(const Call &c) {
     if (!c.rowptr) return set_error("row_offsets is NULL"), TC_EINVAL;
     if (c.M > 0 && !c.col) return set_error("col_indices is NULL with m > 0"), TC_EINVAL;
     if (c.mode == kCount && !c.total_host) return set_error("total is NULL"), TC_EINVAL;
+    if (c.mode == kClustering && (c.flags & TC_PER_VERTEX))
+        return set_error("tc_clustering: TC_PER_VERTEX is implied (pass per_vertex or NULL)"), TC_EINVAL;
     if (c.mode == kShard) {
         if (!c.partial_dev) return set_error("partial_dev is NULL"), TC_EINVAL;
         if (c.world < 1 || c.rank < 0 || c.rank >= c.world)
@@ -96,7 +100,8 @@ static void run(Call &c) {
     ctx.num_sms = device_sms(ctx.device);
     keep_pool_warm(ctx.device);
     const bool host = c.flags & TC_HOST_PTRS;
-    const bool pv = (c.flags & TC_PER_VERTEX) && c.mode != kOrientOnly;
+    const bool pv = ((c.flags & TC_PER_VERTEX) && c.mode != kOrientOnly) || c.mode == kClustering;
+    const bool pv_out = pv && c.per_vertex;   // t(v) wanted by the caller
     tc_stats st;
     memset(&st, 0, sizeof(st));
     Timer *tm = nullptr;
@@ -142,10 +147,22 @@ static void run(Call &c) {
 
     uint64_t *pv_dev = nullptr, *pv_new = nullptr;  // output side / rank-id side
     if (pv) {
-        pv_dev = host ? ctx.alloc<uint64_t>(c.n) : c.per_vertex;
         pv_new = ctx.alloc<uint64_t>(c.n);
-        if (c.n) TC_CUDA(cudaMemsetAsync(pv_dev, 0, c.n * sizeof(uint64_t), ctx.stream));
         if (c.n) TC_CUDA(cudaMemsetAsync(pv_new, 0, c.n * sizeof(uint64_t), ctx.stream));
+    }
+    if (pv_out) {
+        pv_dev = host ? ctx.alloc<uint64_t>(c.n) : c.per_vertex;
+        if (c.n) TC_CUDA(cudaMemsetAsync(pv_dev, 0, c.n * sizeof(uint64_t), ctx.stream));
+    }
+    double *cc_dev = nullptr;                       // kClustering: local coefficients
+    uint64_t *cc_out = nullptr;                     // {wedges, bits of sum c}
+    if (c.mode == kClustering) {
+        if (c.cc) {
+            cc_dev = host ? ctx.alloc<double>(c.n) : c.cc;
+            if (c.n) TC_CUDA(cudaMemsetAsync(cc_dev, 0, c.n * sizeof(double), ctx.stream));
+        }
+        cc_out = ctx.alloc<uint64_t>(2);
+        TC_CUDA(cudaMemsetAsync(cc_out, 0, 2 * sizeof(uint64_t), ctx.stream));
     }
     uint64_t *total_dev = c.mode == kShard ? c.partial_dev : ctx.alloc<uint64_t>(1);
     TC_CUDA(cudaMemsetAsync(total_dev, 0, sizeof(uint64_t), ctx.stream));
@@ -203,7 +220,8 @@ static void run(Call &c) {
         if (tm) tm->begin(kIntersect);
         intersect_all(ctx, g, bins, total_dev, pv_new);
         if (tm) tm->end(kIntersect);
-        if (pv) per_vertex_to_original(ctx, g, pv_new, pv_dev);
+        if (pv_out) per_vertex_to_original(ctx, g, pv_new, pv_dev);
+        if (c.mode == kClustering) clustering(ctx, g, pv_new, cc_dev, cc_out);
         if (c.stats) {  // async into pinned memory; read after the final sync
             TC_CUDA(cudaMemcpyAsync(pin, bins.count, 16 * sizeof(uint64_t), cudaMemcpyDeviceToHost,
                                     ctx.stream));
@@ -220,11 +238,21 @@ static void run(Call &c) {
         return;
     }
 
-    if (c.mode == kCount) {
+    if (c.mode == kCount || c.mode == kClustering) {
         TC_CUDA(cudaMemcpyAsync(pin + 20, total_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost,
                                 ctx.stream));
         st.d2h_bytes += sizeof(uint64_t);
-        if (pv && host && c.n) {
+        if (cc_out) {
+            TC_CUDA(cudaMemcpyAsync(pin + 21, cc_out, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                                    ctx.stream));
+            st.d2h_bytes += 2 * sizeof(uint64_t);
+        }
+        if (cc_dev && host && c.n) {
+            TC_CUDA(cudaMemcpyAsync(c.cc, cc_dev, c.n * sizeof(double), cudaMemcpyDeviceToHost,
+                                    ctx.stream));
+            st.d2h_bytes += c.n * sizeof(double);
+        }
+        if (pv_out && host && c.n) {
             TC_CUDA(cudaMemcpyAsync(c.per_vertex, pv_dev, c.n * sizeof(uint64_t),
                                     cudaMemcpyDeviceToHost, ctx.stream));
             st.d2h_bytes += c.n * sizeof(uint64_t);
@@ -235,6 +263,16 @@ static void run(Call &c) {
     if (c.mode != kShard || c.stats) TC_CUDA(cudaStreamSynchronize(ctx.stream));
     TC_CUDA(cudaGetLastError());
     if (c.mode == kCount) *c.total_host = pin[20];
+    if (c.mode == kClustering && c.csum) {
+        tc_clustering_summary &r = *c.csum;
+        r.triangles = pin[20];
+        r.wedges = pin[21];
+        double sum;
+        memcpy(&sum, &pin[22], sizeof(sum));
+        // 3T and the wedge count are exact integers below 2^53: one rounded division
+        r.transitivity = r.wedges ? (3.0 * (double)r.triangles) / (double)r.wedges : 0.0;
+        r.avg_clustering = c.n ? sum / (double)c.n : 0.0;
+    }
 
     if (c.stats) {
         st.ms_clean = tm->ms(kClean);
@@ -352,6 +390,19 @@ tc_status tc_orient(uint64_t n, uint64_t m, const uint64_t *row_offsets,
     c.off_plus = off_plus;
     c.col_plus = col_plus;
     c.m_plus = m_plus;
+    return guarded(c);
+}
+
+tc_status tc_clustering(uint64_t n, uint64_t m, const uint64_t *row_offsets,
+                        const uint32_t *col_indices, uint32_t flags, const tc_options *opt,
+                        double *local_cc, uint64_t *per_vertex, tc_clustering_summary *summary,
+                        tc_stats *stats) {
+    Call c{n, m, row_offsets, col_indices, flags, resolve(opt)};
+    c.mode = kClustering;
+    c.cc = local_cc;
+    c.per_vertex = per_vertex;
+    c.csum = summary;
+    c.stats = stats;
     return guarded(c);
 }
 

@@ -237,6 +237,10 @@ void to_original(Ctx &ctx, const Oriented &g, uint64_t *off_out, uint32_t *col_o
 // pv_out[v] = pv_new[newid[v]].
 void per_vertex_to_original(Ctx &ctx, const Oriented &g, const uint64_t *pv_new, uint64_t *pv_out);
 
+// NEXT-1: local clustering coefficients (input ids, nullable) from t (rank ids);
+// out2 (device) = {sum_v C(d(v),2), bits of sum_v c(v)}.
+void clustering(Ctx &ctx, const Oriented &g, const uint64_t *t_new, double *cc, uint64_t *out2);
+
 // HASH-variant context passed by value to the binning and intersection kernels.
 struct HashParams {
     const uint64_t *off = nullptr;     // oriented CSR (rank ids, rows ascending)

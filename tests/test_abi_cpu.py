@@ -28,7 +28,7 @@ def declared_functions():
 def test_exports_every_declared_symbol(lib):
     names = declared_functions()
     assert set(names) >= {"tc_count", "tc_count_ex", "tc_count_shard", "tc_orient",
-                          "tc_last_error", "tc_default_options", "tc_version"}
+                          "tc_clustering", "tc_last_error", "tc_default_options", "tc_version"}
     for name in names:
         assert hasattr(lib, name), name
 
@@ -45,6 +45,17 @@ def test_struct_layout(lib):
     assert o.short_max == 32 and o.skew_ratio == 0 and o.hub_min_dplus == 64
     assert o.force_variant == -1 and o.segsort_block_max == 8192
     assert ctypes.sizeof(tc.Stats) == 6 * 8 + 16 * 8
+    assert ctypes.sizeof(tc.ClusteringSummary) == 32
+
+
+def test_clustering_argument_errors(lib):
+    rp = np.zeros(2, np.uint64)
+    EINVAL = 1
+    # TC_PER_VERTEX is implied by tc_clustering and rejected as a flag
+    assert lib.tc_clustering(1, 0, rp.ctypes.data, None, tc.TC_PER_VERTEX | tc.TC_HOST_PTRS, None,
+                             None, None, None, None) == EINVAL
+    assert b"implied" in lib.tc_last_error()
+    assert lib.tc_clustering(1, 0, None, None, tc.TC_HOST_PTRS, None, None, None, None, None) == EINVAL
 
 
 def test_argument_errors_before_device(lib):

@@ -301,3 +301,66 @@ def test_karate_fourth_power():
     got, st = gpu_count(g.rowptr, g.col, with_stats=True)
     assert st["m_undirected"] == 2 ** 3 * 78 ** 4 == 296_120_448
     assert got == 6 ** 3 * 45 ** 4 == 885_735_000
+
+
+# ------------------------------------------------------------------ NEXT-1: clustering
+# Bar (R14): every local c(v), the wedge count, T and the transitivity are
+# bit-exact (each c(v) and 3T/wedges is one correctly rounded fp64 division of exact
+# integers on both sides); the average is an fp64 sum in a different order, so it is
+# compared within the recursive-summation bound n * 2^-53 * sum_v c(v) (c(v) >= 0).
+def check_clustering(g, **kw):
+    cc_o, s_o = O.clustering(g.n, g.rowptr, g.col)
+    rp, cl = on_dev(g.rowptr, g.col)
+    cc, s, t = tc.clustering(rp, cl, per_vertex=True, **kw)
+    torch.cuda.synchronize()
+    _, t_o = O.count(g.n, g.rowptr, g.col, per_vertex=True)
+    assert (cc.cpu().numpy() == cc_o).all(), g.name
+    assert (pv_np(t) == t_o).all(), g.name
+    assert s["triangles"] == s_o["triangles"] and s["wedges"] == s_o["wedges"], g.name
+    assert s["transitivity"] == s_o["transitivity"], g.name
+    bound = max(g.n, 1) * 2.0 ** -53 * s_o["avg_clustering"] * max(g.n, 1)
+    assert abs(s["avg_clustering"] * g.n - s_o["avg_clustering"] * g.n) <= bound + 1e-300, g.name
+    return cc, s
+
+
+def test_clustering_fixtures():
+    cc, s = check_clustering(G.karate())
+    assert s["triangles"] == 45 and s["wedges"] == 528 and s["transitivity"] == 135 / 528
+    assert round(s["avg_clustering"], 5) == 0.57064
+    cc, s = check_clustering(G.complete(40))
+    assert (cc.cpu().numpy() == 1.0).all() and s["transitivity"] == 1.0
+    for g in (G.wheel(9), G.friendship(7), G.complete_multipartite([2, 3, 4]), G.star(12),
+              G.random_tree(300, seed=2), G.fig_mm()):
+        check_clustering(g)
+
+
+@pytest.mark.parametrize("gname", ["rmat12", "rmat16_dirty", "chung_lu_small", "clique_small", "road_small"])
+def test_clustering_generators(gname):
+    g = {"rmat12": lambda: G.rmat(12, 16, seed=4),
+         "rmat16_dirty": lambda: G.dirty(G.rmat(16, 8, seed=9), seed=1),
+         "chung_lu_small": lambda: G.chung_lu(20000, 200000, seed=6),
+         "clique_small": lambda: G.clique_union(5000, 8000, seed=3),
+         "road_small": lambda: G.road_mesh(200, 200, seed=2)}[gname]()
+    check_clustering(g)
+
+
+def test_clustering_host_clean_and_variants():
+    g = G.rmat(13, 16, seed=8)
+    cc_o, s_o = O.clustering(g.n, g.rowptr, g.col)
+    cc, s = tc.clustering(g.rowptr, g.col)                       # host pointers
+    assert (cc == cc_o).all() and s["wedges"] == s_o["wedges"]
+    crow, ccol = O.clean(g.n, g.rowptr, g.col)                   # TC_CLEAN input
+    rp, cl = on_dev(crow, ccol)
+    for v in VARIANTS:
+        cc, s = tc.clustering(rp, cl, clean=True, force_variant=v)
+        torch.cuda.synchronize()
+        assert (cc.cpu().numpy() == cc_o).all() and s["transitivity"] == s_o["transitivity"], v
+    e = G.from_edges(5, np.zeros((0, 2), np.int64))              # no edges: all zero
+    cc, s = tc.clustering(e.rowptr, e.col)
+    assert (cc == 0).all() and s == dict(triangles=0, wedges=0, transitivity=0.0, avg_clustering=0.0)
+
+
+def test_clustering_rmat21_full():
+    """Bench workload (R-MAT s21 ef16, raw arcs): every c(v) bit-exact."""
+    g = G.rmat(21, 16)
+    check_clustering(g)

@@ -346,3 +346,89 @@ def test_empty_and_degenerate():
 def test_bad_input_rejected():
     with pytest.raises(ValueError):
         O.count(2, np.array([0, 1, 1], np.uint64), np.array([5], np.uint32))
+
+
+# ------------------------------------------------------------------ NEXT-1: clustering
+# Conventions (SURVEY §8(c) reading 9, R14): c(v) = 2t(v)/(d(v)(d(v)-1)),
+# 0 for d(v) < 2; transitivity = 3T / sum_v C(d(v),2); average over all n vertices.
+def test_clustering_karate_published():
+    """Karate: transitivity 0.25568 and average clustering 0.57064 (SURVEY §8(c)
+    reading 9, measured with networkx); T = 45 and 528 wedges give 135/528 exactly."""
+    g = G.karate()
+    cc, s = O.clustering(g.n, g.rowptr, g.col)
+    assert s["triangles"] == 45 and s["wedges"] == 528
+    assert s["transitivity"] == 135 / 528
+    assert round(s["transitivity"], 5) == 0.25568
+    assert round(s["avg_clustering"], 5) == 0.57064
+    assert cc[0] == 0.15          # vertex 0: d = 16, t = 18 -> 36 / 240
+    assert cc[11] == 0.0          # vertex 11: d = 1 -> 0 by convention
+
+
+@pytest.mark.parametrize("n", [3, 4, 7, 20])
+def test_clustering_complete(n):
+    g = G.complete(n)
+    cc, s = O.clustering(g.n, g.rowptr, g.col)
+    assert (cc == 1.0).all() and s["transitivity"] == 1.0 and s["avg_clustering"] == 1.0
+    assert s["wedges"] == n * math.comb(n - 1, 2)
+
+
+@pytest.mark.parametrize("n", [5, 6, 9, 30])
+def test_clustering_wheel(n):
+    """Wheel with n vertices (hub 0 + rim cycle of n-1, n >= 5): hub c = 2/(n-2),
+    rim c = 2/3; transitivity 3(n-1) / (C(n-1,2) + 3(n-1))."""
+    g = G.wheel(n)
+    cc, s = O.clustering(g.n, g.rowptr, g.col)
+    hub = int(np.argmax(np.diff(g_clean_rowptr(g))))
+    assert cc[hub] == 2.0 / (n - 2)
+    assert all(cc[v] == 2.0 / 3.0 for v in range(n) if v != hub)
+    assert s["wedges"] == math.comb(n - 1, 2) + 3 * (n - 1)
+    assert s["transitivity"] == 3.0 * (n - 1) / (math.comb(n - 1, 2) + 3 * (n - 1))
+
+
+def g_clean_rowptr(g):
+    return O.clean(g.n, g.rowptr, g.col)[0]
+
+
+@pytest.mark.parametrize("k", [1, 2, 5, 12])
+def test_clustering_friendship(k):
+    """F_k: centre d = 2k, t = k -> 1/(2k-1); every other vertex d = 2, t = 1 -> 1."""
+    g = G.friendship(k)
+    cc, s = O.clustering(g.n, g.rowptr, g.col)
+    deg = np.diff(g_clean_rowptr(g))
+    centre = int(np.argmax(deg))
+    assert cc[centre] == 1.0 / (2 * k - 1) if k > 1 else cc[centre] == 1.0
+    assert all(cc[v] == 1.0 for v in range(g.n) if v != centre)
+
+
+def test_clustering_multipartite_and_zero_cases():
+    """K_{a,b,c}: a vertex of part A has d = b+c, t = bc; trees and stars are 0;
+    isolated vertices count 0 in the average."""
+    a, b, c = 2, 3, 4
+    g = G.complete_multipartite([a, b, c])
+    cc, s = O.clustering(g.n, g.rowptr, g.col)
+    want = {a: 2 * b * c / ((b + c) * (b + c - 1)), b: 2 * a * c / ((a + c) * (a + c - 1)),
+            c: 2 * a * b / ((a + b) * (a + b - 1))}
+    sizes = [a] * a + [b] * b + [c] * c
+    assert all(cc[v] == want[sizes[v]] for v in range(g.n))
+    wedges = a * math.comb(b + c, 2) + b * math.comb(a + c, 2) + c * math.comb(a + b, 2)
+    assert s["wedges"] == wedges and s["transitivity"] == 3 * a * b * c / wedges
+    for h in (G.star(9), G.random_tree(50, seed=3), G.path(7)):
+        cc, s = O.clustering(h.n, h.rowptr, h.col)
+        assert (cc == 0).all() and s["transitivity"] == 0.0 and s["avg_clustering"] == 0.0
+    k4 = G.complete(4)
+    iso = G.from_edges(10, np.stack(k4.arc_list(), 1))     # K4 + 6 isolated vertices
+    cc, s = O.clustering(iso.n, iso.rowptr, iso.col)
+    assert s["avg_clustering"] == 4 / 10 and (cc[4:] == 0).all()
+
+
+def test_clustering_matches_dense_definition():
+    """A different route: d = row sums of A, t = diag(A^3)/2 on small random graphs."""
+    for seed in range(4):
+        g = G.gnp(60, 0.15, seed=seed)
+        A = dense(g)
+        d = A.sum(1)
+        t = np.diag(A @ A @ A) // 2
+        cc, s = O.clustering(g.n, g.rowptr, g.col)
+        want = np.where(d >= 2, 2.0 * t / np.maximum(d * (d - 1), 1), 0.0)
+        assert (cc == want).all()
+        assert s["wedges"] == int((d * (d - 1) // 2).sum())
