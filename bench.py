@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--edge-factor", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-next", action="store_true", help="skip the NEXT-row measurements")
     return ap.parse_args()
 
 
@@ -289,7 +290,7 @@ def main():
                 line["roofline"]["traffic_source"] = tr["source"]
         except (OSError, ValueError):
             pass
-    if world == 1:
+    if world == 1 and not args.no_next:
         # NEXT-1: clustering coefficients + transitivity on the same
         # workload through tc_clustering (count with t(v), then the c(v) kernel)
         cev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
