@@ -57,6 +57,14 @@ def _load():
         lib.oracle_vertex_triangles.restype = ctypes.c_uint64
         lib.oracle_vertex_triangles.argtypes = [ctypes.c_uint64, _u64p, _u32p, ctypes.c_uint64]
         lib.oracle_num_threads.restype = ctypes.c_int
+        lib.oracle_prune.restype = ctypes.c_int64
+        lib.oracle_prune.argtypes = [ctypes.c_uint64, _u64p, _u32p, ctypes.c_uint32, _u64p, _u32p,
+                                     ctypes.c_void_p]
+        lib.oracle_edge_support.restype = None
+        lib.oracle_edge_support.argtypes = [ctypes.c_uint64, _u64p, _u32p, _u64p, _u32p, _u32p]
+        lib.oracle_enumerate.restype = ctypes.c_uint64
+        lib.oracle_enumerate.argtypes = [ctypes.c_uint64, _u64p, _u32p, ctypes.c_void_p,
+                                         ctypes.c_uint64]
         lib.oracle_clustering.restype = None
         lib.oracle_clustering.argtypes = [ctypes.c_uint64, _u64p, _u64p, ctypes.c_uint64,
                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
@@ -158,6 +166,45 @@ def clustering(n: int, rowptr, col):
     summary = dict(triangles=T, wedges=int(w[0]), transitivity=float(tr[0]),
                    avg_clustering=float(s[0]) / n if n else 0.0)
     return cc[:n], summary
+
+
+def prune(n: int, clean_rowptr, clean_col, rounds: int = 0):
+    """NEXT-2: delete edges with an endpoint of degree < 2, `rounds`
+    times (0 = until nothing changes: the 2-core).  -> (rowptr, col, rounds executed)."""
+    lib = _load()
+    clean_rowptr, clean_col = _csr(clean_rowptr, clean_col)
+    out_row = np.zeros(n + 1, dtype=np.uint64)
+    out_col = np.zeros(max(1, int(clean_rowptr[n])), dtype=np.uint32)
+    done = np.zeros(1, dtype=np.uint32)
+    r = lib.oracle_prune(n, _p64(clean_rowptr), _p32(clean_col), rounds, _p64(out_row),
+                         _p32(out_col), done.ctypes.data)
+    if r < 0:
+        raise MemoryError("oracle_prune: allocation failed")
+    return out_row, out_col[:r].copy(), int(done[0])
+
+
+def edge_support(n: int, clean_rowptr, clean_col, off_plus, col_plus):
+    """NEXT-3: sup[e] = |N(u) cap N(v)| for every entry e = (u, col_plus[e]) of an
+    oriented CSR, by merging the full rows of the clean symmetric CSR."""
+    lib = _load()
+    clean_rowptr, clean_col = _csr(clean_rowptr, clean_col)
+    m = int(off_plus[n]) if n else 0
+    off_plus, col_plus = _csr(off_plus, col_plus)
+    sup = np.zeros(max(m, 1), dtype=np.uint32)
+    lib.oracle_edge_support(n, _p64(clean_rowptr), _p32(clean_col), _p64(off_plus), _p32(col_plus),
+                            _p32(sup))
+    return sup[:m]
+
+
+def enumerate_triangles(n: int, clean_rowptr, clean_col):
+    """NEXT-3: all triangles as a (T, 3) uint32 array of (a<b<c), lexicographic."""
+    lib = _load()
+    clean_rowptr, clean_col = _csr(clean_rowptr, clean_col)
+    T = int(lib.oracle_enumerate(n, _p64(clean_rowptr), _p32(clean_col), None, 0))
+    out = np.zeros(max(3 * T, 3), dtype=np.uint32)
+    T2 = int(lib.oracle_enumerate(n, _p64(clean_rowptr), _p32(clean_col), out.ctypes.data, T))
+    assert T2 == T
+    return out[:3 * T].reshape(T, 3)
 
 
 def num_threads() -> int:

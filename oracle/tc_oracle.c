@@ -282,3 +282,124 @@ int oracle_num_threads(void) {
     return 1;
 #endif
 }
+
+/*
+ * NEXT-2: leaf pruning before orientation.  The paper's
+ * filtering stage removes vertices that cannot be in any triangle: "nodes with
+ * degree less than two cannot be matched [to] any query vertex, since every node
+ * in a triangle has a degree of two", prunes the non-candidate
+ * edges and "reconstruct[s] the graph ... update[s] node degree and neighbor list
+ * information.  So we can run the above two steps for a few iterations in order
+ * to prune out more edges".  One ROUND, written out:
+ *   1. d(v) = degree of v in the current graph;
+ *   2. delete every edge {u,v} with d(u) < 2 or d(v) < 2.
+ * rounds > 0: exactly that many rounds.  rounds = 0: repeat until a round deletes
+ * nothing (the result is then the edge set of the 2-core; reading R15).
+ * Input: clean symmetric CSR with sorted rows (oracle_clean's output); output in
+ * the same format (out_col capacity rowptr[n]).  Returns the number of stored
+ * arcs (2m'), *done = rounds executed (in fixed-point mode including the final
+ * round that deleted nothing), or -2 on allocation failure.
+ */
+int64_t oracle_prune(uint64_t n, const uint64_t *rowptr, const uint32_t *col, uint32_t rounds,
+                     uint64_t *out_rowptr, uint32_t *out_col, uint32_t *done) {
+    uint64_t M = rowptr[n];
+    uint64_t *deg = (uint64_t *)malloc((n + 1) * sizeof(uint64_t));
+    uint64_t *tmp_row = (uint64_t *)malloc((n + 1) * sizeof(uint64_t));
+    uint32_t *tmp_col = (uint32_t *)malloc((M ? M : 1) * sizeof(uint32_t));
+    if (!deg || !tmp_row || !tmp_col) {
+        free(deg); free(tmp_row); free(tmp_col);
+        return -2;
+    }
+    /* current graph := input */
+    memcpy(out_rowptr, rowptr, (n + 1) * sizeof(uint64_t));
+    if (M) memcpy(out_col, col, M * sizeof(uint32_t));
+    uint32_t r = 0;
+    for (;;) {
+        if (rounds && r == rounds) break;
+        /* 1. degrees of the current graph */
+        for (uint64_t v = 0; v < n; v++) deg[v] = out_rowptr[v + 1] - out_rowptr[v];
+        /* 2. keep arc (u,v) iff d(u) >= 2 and d(v) >= 2 (rows stay sorted) */
+        uint64_t k = 0, deleted = 0;
+        tmp_row[0] = 0;
+        for (uint64_t u = 0; u < n; u++) {
+            for (uint64_t e = out_rowptr[u]; e < out_rowptr[u + 1]; e++) {
+                uint32_t v = out_col[e];
+                if (deg[u] >= 2 && deg[v] >= 2) tmp_col[k++] = v;
+                else deleted++;
+            }
+            tmp_row[u + 1] = k;
+        }
+        memcpy(out_rowptr, tmp_row, (n + 1) * sizeof(uint64_t));
+        if (k) memcpy(out_col, tmp_col, k * sizeof(uint32_t));
+        r++;
+        if (!rounds && deleted == 0) break;
+    }
+    if (done) *done = r;
+    free(deg); free(tmp_row); free(tmp_col);
+    return (int64_t)out_rowptr[n];
+}
+
+/*
+ * NEXT-3: edge support, the k-truss prerequisite ("enumerating
+ * triangles is useful as a subroutine in solving k-truss"; "the three ...
+ * algorithms we examine ... will also enumerate triangles").  By
+ * definition sup({u,v}) = number of triangles containing the edge {u,v}
+ * = |N(u) cap N(v)| in the simple graph.  For every entry e of an oriented CSR
+ * (off_plus, col_plus; edge (u, col_plus[e])) this writes sup[e], computed as a
+ * two-pointer merge of the FULL sorted rows N(u), N(v) of the clean symmetric
+ * CSR (crow, ccol).
+ */
+void oracle_edge_support(uint64_t n, const uint64_t *crow, const uint32_t *ccol,
+                         const uint64_t *off_plus, const uint32_t *col_plus, uint32_t *sup) {
+    for (uint64_t u = 0; u < n; u++) {
+        for (uint64_t e = off_plus[u]; e < off_plus[u + 1]; e++) {
+            uint64_t v = col_plus[e];
+            uint64_t i = crow[u], iend = crow[u + 1], j = crow[v], jend = crow[v + 1];
+            uint32_t c = 0;
+            while (i < iend && j < jend) {
+                if (ccol[i] < ccol[j]) i++;
+                else if (ccol[i] > ccol[j]) j++;
+                else { c++; i++; j++; }
+            }
+            sup[e] = c;
+        }
+    }
+}
+
+/*
+ * NEXT-3: triangle enumeration ("we can get the listings of all the triangles for
+ * free").  Every triangle {a,b,c} exactly once as the triple (a,b,c)
+ * with a < b < c (input ids), in lexicographic order: for each a, each b in N(a)
+ * with b > a, each c in N(a) cap N(b) with c > b.  Input: clean symmetric CSR with
+ * sorted rows.  Writes at most `cap` triples (3 uint32 each) to out (nullable
+ * when cap = 0) and returns the total number of triangles.
+ */
+uint64_t oracle_enumerate(uint64_t n, const uint64_t *crow, const uint32_t *ccol, uint32_t *out,
+                          uint64_t cap) {
+    uint64_t k = 0;
+    for (uint64_t a = 0; a < n; a++) {
+        for (uint64_t e = crow[a]; e < crow[a + 1]; e++) {
+            uint64_t b = ccol[e];
+            if (b <= a) continue;
+            uint64_t i = crow[a], iend = crow[a + 1], j = crow[b], jend = crow[b + 1];
+            while (i < iend && j < jend) {
+                if (ccol[i] < ccol[j]) i++;
+                else if (ccol[i] > ccol[j]) j++;
+                else {
+                    uint64_t c = ccol[i];
+                    if (c > b) {
+                        if (k < cap) {
+                            out[3 * k + 0] = (uint32_t)a;
+                            out[3 * k + 1] = (uint32_t)b;
+                            out[3 * k + 2] = (uint32_t)c;
+                        }
+                        k++;
+                    }
+                    i++;
+                    j++;
+                }
+            }
+        }
+    }
+    return k;
+}
