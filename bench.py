@@ -152,6 +152,59 @@ def reference_arm(args, g, rank, world):
             "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+def _timed(torch, flush, stream, fn, reps=3):
+    """Mean CUDA-event ms of fn() over reps calls (L2 flushed before each), last result."""
+    fn()
+    tot, out = 0.0, None
+    for _ in range(reps):
+        flush.fill_(3)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        out = fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        tot += a.elapsed_time(b)
+    return tot / reps, out
+
+
+def next_rows_23(tc, torch, np, graphgen, rp, cl, flush, stream, m, T, count_ms):
+    """NEXT-2 / NEXT-3 timed through their C-ABI calls, device pointers."""
+    rows = {}
+    # NEXT-3 edge support on the bench workload
+    sms, (off, colp, sup) = _timed(torch, flush, stream, lambda: tc.edge_support(rp, cl))
+    assert int(sup.to(torch.int64).sum().item()) == 3 * T
+    rows["NEXT-3 edge support"] = {
+        "ms_per_call": sms, "edges_per_s": m / (sms * 1e-3), "overhead_vs_count_ms": sms - count_ms,
+        "max_support": int(sup.max().item()),
+        "call": "tc_edge_support: count crediting all three edges of every triangle + the "
+                "oriented CSR and supports mapped back to input ids"}
+    del off, colp, sup
+    # NEXT-3 enumeration: output-bound (12 B per triangle)
+    tri = torch.empty((T, 3), dtype=torch.int32, device=rp.device)
+    ems, (Te, _) = _timed(torch, flush, stream, lambda: tc.enumerate_triangles(rp, cl, out=tri))
+    assert Te == T
+    rows["NEXT-3 enumeration"] = {
+        "ms_per_call": ems, "triangles_per_s": T / (ems * 1e-3), "output_bytes": 12 * T,
+        "output_GB_per_s": 12 * T / (ems * 1e-3) / 1e9,
+        "call": "tc_enumerate into a preallocated device buffer of T triples (capacity = T)"}
+    del tri
+    # NEXT-2 leaf pruning where it matters: the road mesh (BASELINE configs[3])
+    g = graphgen.road_mesh()
+    rrp = torch.from_numpy(g.rowptr.view(np.int64)).to(rp.device)
+    rcl = torch.from_numpy(g.col.view(np.int32)).to(rp.device)
+    bms, (Tb, sb) = _timed(torch, flush, stream, lambda: tc.count_ex(rrp, rcl, with_stats=True))
+    out = {"workload": g.name, "count_ms_unpruned": bms, "m": sb["m_undirected"]}
+    for r in (1, 2, 0):
+        pms, (Tp, sp) = _timed(torch, flush, stream,
+                               lambda: tc.count_ex(rrp, rcl, prune=True, prune_rounds=r, with_stats=True))
+        assert Tp == Tb
+        out[f"rounds={r or 'fixed-point'}"] = {
+            "ms_per_call": pms, "prune_ms": sp["ms_prune"], "pruned_edges": sp["pruned_edges"],
+            "rounds_run": sp["prune_rounds"], "edges_per_s": sb["m_undirected"] / (pms * 1e-3)}
+    rows["NEXT-2 leaf pruning (road mesh)"] = out
+    return rows
+
+
 # ------------------------------------------------------------------ native arm
 def main():
     args = parse()
@@ -309,6 +362,8 @@ def main():
             "transitivity": summ["transitivity"], "avg_clustering": summ["avg_clustering"],
             "wedges": summ["wedges"],
             "call": "tc_clustering (device pointers): count with per-vertex t(v) + local c(v) for all n"}}
+        line["next_rows"].update(next_rows_23(tc, torch, np, graphgen, rp, cl, flush, stream, m,
+                                              T_total, ms))
     if world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline(g, m)
         assert cb.pop("T") == T_total, "oracle and CUDA path disagree"

@@ -71,7 +71,16 @@ enum {
     TC_PER_VERTEX = 1u << 2, /* fill per_vertex[n] with t(v)                                  */
     TC_HOST_PTRS = 1u << 3,  /* all arrays are host pointers                                   */
     TC_VALIDATE = 1u << 4,   /* check the graph on the device; TC_EGRAPH on violation          */
-    TC_ALL_FLAGS = 0x1fu
+    TC_PRUNE = 1u << 5,      /* NEXT-2 leaf pruning before orientation ("nodes with degree less
+                                than two cannot be matched"; repeated "for a few
+                                iterations"): each round deletes every edge with an
+                                endpoint of degree < 2 in the current graph; rounds =
+                                tc_options.prune_rounds, 0 = until a round deletes nothing
+                                (the 2-core).  T and t(v) are unchanged (every vertex of a
+                                triangle keeps degree >= 2); ranks use the PRUNED degrees, so
+                                tc_orient returns the oriented pruned graph.  Not allowed with
+                                tc_clustering (c(v) needs the unpruned degrees).             */
+    TC_ALL_FLAGS = 0x3fu
 };
 
 typedef enum {
@@ -102,7 +111,9 @@ typedef struct {
     void *stream;               /* cudaStream_t to run on; NULL = legacy default stream         */
     uint32_t segsort_block_max; /* ignored (kept for layout stability): rows are sorted by the
                                    two-key radix sort of a3/a4 on every path                 */
-    uint32_t reserved[9];       /* must be zero                                                 */
+    uint32_t prune_rounds;      /* TC_PRUNE: rounds to run; 0 = to the fixed point (one 8-byte
+                                   device->host read per round)                               */
+    uint32_t reserved[8];       /* must be zero                                                 */
 } tc_options;
 
 typedef struct {
@@ -127,6 +138,10 @@ typedef struct {
     uint64_t table_loads;     /* HASH: sum over owner tasks of d+(owner) (table builds)      */
     uint64_t bytes_hash;      /* HASH algorithmic bytes: 4*work_probe + 8*HASH edges +
                                  4*table_loads (the method's own a6 byte model)           */
+    double ms_prune;          /* TC_PRUNE: the pruning rounds (inside ms_orient)             */
+    uint64_t pruned_edges;    /* TC_PRUNE: undirected edges deleted                          */
+    uint64_t prune_rounds;    /* TC_PRUNE: rounds executed (fixed-point mode: including the
+                                 final round that deleted nothing)                         */
 } tc_stats;
 
 /* Fill *opt with the defaults (auto variant selection, default stream). */
@@ -190,6 +205,34 @@ tc_status tc_clustering(uint64_t n, uint64_t m, const uint64_t *row_offsets,
                         const uint32_t *col_indices, uint32_t flags, const tc_options *opt,
                         double *local_cc, uint64_t *per_vertex, tc_clustering_summary *summary,
                         tc_stats *stats);
+
+/* NEXT-3: edge support, the k-truss input ("enumerating triangles is
+ * useful as a subroutine in solving k-truss").  sup({u,v}) = number of triangles
+ * containing the edge = |N(u) cap N(v)|.  Every triangle found by the a6 kernels credits
+ * its three edges (its base edge, and the two edges through the match w, located by
+ * their col+ slot / the owner's table position).  Output: the oriented CSR exactly as
+ * tc_orient returns it (input ids, each undirected edge once, rows ascending; off_plus
+ * n+1 entries, col_plus capacity m entries, *m_plus edges used) and support[e] for each
+ * of its entries (capacity m, uint32).  Pointer side per TC_HOST_PTRS (m_plus: host).
+ * Flags: TC_CLEAN, TC_SORTED, TC_HOST_PTRS, TC_VALIDATE, TC_PRUNE (pruned edges have
+ * support 0 and are not listed).  sum_e support[e] = 3T.  Synchronous. */
+tc_status tc_edge_support(uint64_t n, uint64_t m, const uint64_t *row_offsets,
+                          const uint32_t *col_indices, uint32_t flags, const tc_options *opt,
+                          uint64_t *off_plus, uint32_t *col_plus, uint32_t *support,
+                          uint64_t *m_plus, tc_stats *stats);
+
+/* NEXT-3: triangle enumeration ("we can get the listings of all the triangles for
+ * free").  Writes each triangle {a,b,c} once as three uint32 input ids
+ * a < b < c into triangles[3k .. 3k+2], for min(T, capacity) triangles, in an
+ * UNSPECIFIED order (slots are reserved by atomic counters; the set is deterministic
+ * when capacity >= T), and sets *total (host) = T.  If T > capacity an unspecified
+ * subset of `capacity` triangles is written: call again with capacity >= *total.
+ * capacity = 0 (triangles may be NULL) only counts.  triangles is on the TC_HOST_PTRS
+ * side (host mode stages min(T, capacity) triples in device memory).  Flags: TC_CLEAN,
+ * TC_SORTED, TC_HOST_PTRS, TC_VALIDATE, TC_PRUNE.  Synchronous. */
+tc_status tc_enumerate(uint64_t n, uint64_t m, const uint64_t *row_offsets,
+                       const uint32_t *col_indices, uint32_t flags, const tc_options *opt,
+                       uint32_t *triangles, uint64_t capacity, uint64_t *total, tc_stats *stats);
 
 /* Thread-local message describing the last failure on this thread ("" if none). */
 const char *tc_last_error(void);

@@ -17,15 +17,16 @@ import os
 
 import numpy as np
 
-__all__ = ["count", "count_ex", "count_shard", "orient", "clustering", "stats_dict", "library_path",
-           "TC_CLEAN", "TC_SORTED", "TC_PER_VERTEX", "TC_HOST_PTRS", "TC_VALIDATE",
+__all__ = ["count", "count_ex", "count_shard", "orient", "clustering", "edge_support",
+           "enumerate_triangles", "stats_dict", "library_path",
+           "TC_CLEAN", "TC_SORTED", "TC_PER_VERTEX", "TC_HOST_PTRS", "TC_VALIDATE", "TC_PRUNE",
            "VARIANT_AUTO", "VARIANT_SHORT", "VARIANT_MERGE", "VARIANT_SEARCH", "VARIANT_HASH",
            "TCError"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libtc_b200.so")
 
-TC_CLEAN, TC_SORTED, TC_PER_VERTEX, TC_HOST_PTRS, TC_VALIDATE = 1, 2, 4, 8, 16
+TC_CLEAN, TC_SORTED, TC_PER_VERTEX, TC_HOST_PTRS, TC_VALIDATE, TC_PRUNE = 1, 2, 4, 8, 16, 32
 VARIANT_AUTO, VARIANT_SHORT, VARIANT_MERGE, VARIANT_SEARCH, VARIANT_HASH = -1, 0, 1, 2, 3
 _STATUS = {0: "TC_OK", 1: "TC_EINVAL", 2: "TC_EGRAPH", 3: "TC_ENOMEM", 4: "TC_ECUDA"}
 TC_ERROR = (1 << 64) - 1
@@ -41,7 +42,7 @@ class Options(ctypes.Structure):
     _fields_ = [("short_max", ctypes.c_uint32), ("skew_ratio", ctypes.c_uint32),
                 ("hub_min_dplus", ctypes.c_uint32), ("force_variant", ctypes.c_int32),
                 ("stream", ctypes.c_void_p), ("segsort_block_max", ctypes.c_uint32),
-                ("reserved", ctypes.c_uint32 * 9)]
+                ("prune_rounds", ctypes.c_uint32), ("reserved", ctypes.c_uint32 * 8)]
 
 
 class Stats(ctypes.Structure):
@@ -54,7 +55,8 @@ class Stats(ctypes.Structure):
                 ("hub_sources", ctypes.c_uint64), ("max_dplus", ctypes.c_uint64),
                 ("kernel_launches", ctypes.c_uint64), ("h2d_bytes", ctypes.c_uint64),
                 ("d2h_bytes", ctypes.c_uint64), ("table_loads", ctypes.c_uint64),
-                ("bytes_hash", ctypes.c_uint64)]
+                ("bytes_hash", ctypes.c_uint64), ("ms_prune", ctypes.c_double),
+                ("pruned_edges", ctypes.c_uint64), ("prune_rounds", ctypes.c_uint64)]
 
 
 class ClusteringSummary(ctypes.Structure):
@@ -93,6 +95,12 @@ def _load():
     lib.tc_clustering.argtypes = [u64, u64, vp, vp, u32, ctypes.POINTER(Options), vp, vp,
                                   ctypes.POINTER(ClusteringSummary), ctypes.POINTER(Stats)]
     lib.tc_clustering.restype = ctypes.c_int
+    lib.tc_edge_support.argtypes = [u64, u64, vp, vp, u32, ctypes.POINTER(Options), vp, vp, vp, vp,
+                                    ctypes.POINTER(Stats)]
+    lib.tc_edge_support.restype = ctypes.c_int
+    lib.tc_enumerate.argtypes = [u64, u64, vp, vp, u32, ctypes.POINTER(Options), vp, u64, vp,
+                                 ctypes.POINTER(Stats)]
+    lib.tc_enumerate.restype = ctypes.c_int
     lib.tc_last_error.argtypes = []
     lib.tc_last_error.restype = ctypes.c_char_p
     lib.tc_version.argtypes = []
@@ -130,7 +138,7 @@ def _arrays(rowptr, col):
 
 
 def _options(stream=None, force_variant=None, short_max=None, skew_ratio=None, hub_min_dplus=None,
-             segsort_block_max=None, on_device=True):
+             segsort_block_max=None, prune_rounds=None, on_device=True):
     o = Options()
     _load().tc_default_options(ctypes.byref(o))
     if stream is None and on_device:
@@ -147,6 +155,8 @@ def _options(stream=None, force_variant=None, short_max=None, skew_ratio=None, h
         o.hub_min_dplus = hub_min_dplus
     if segsort_block_max is not None:
         o.segsort_block_max = segsort_block_max
+    if prune_rounds is not None:
+        o.prune_rounds = prune_rounds
     return o
 
 
@@ -157,7 +167,7 @@ def stats_dict(s: Stats) -> dict:
 
 
 def count_ex(rowptr, col, *, clean=False, sorted_rows=False, per_vertex=False, validate=False,
-             stream=None, with_stats=False, **opts):
+             prune=False, stream=None, with_stats=False, **opts):
     """Triangle count of the graph (rowptr, col) [+ per-vertex counts, stats].
 
     torch CUDA tensors -> device pointers on the current stream; numpy arrays or
@@ -167,7 +177,7 @@ def count_ex(rowptr, col, *, clean=False, sorted_rows=False, per_vertex=False, v
     n, M, rp, cp, on_dev, keep = _arrays(rowptr, col)
     flags = (TC_CLEAN if clean else 0) | (TC_SORTED if sorted_rows else 0) | \
             (TC_PER_VERTEX if per_vertex else 0) | (TC_VALIDATE if validate else 0) | \
-            (0 if on_dev else TC_HOST_PTRS)
+            (TC_PRUNE if prune else 0) | (0 if on_dev else TC_HOST_PTRS)
     o = _options(stream=stream, on_device=on_dev, **opts)
     total = ctypes.c_uint64(0)
     pv = None
@@ -197,14 +207,14 @@ def count(rowptr, col, **kw):
 
 
 def count_shard(rowptr, col, rank: int, world: int, partial, *, clean=False, sorted_rows=False,
-                per_vertex_partial=None, stream=None, with_stats=False, **opts):
+                per_vertex_partial=None, prune=False, stream=None, with_stats=False, **opts):
     """Enqueue this rank's share; `partial` is a 1-element int64 CUDA tensor (overwritten)."""
     lib = _load()
     n, M, rp, cp, on_dev, keep = _arrays(rowptr, col)
     if not on_dev:
         raise ValueError("count_shard takes CUDA tensors")
     flags = (TC_CLEAN if clean else 0) | (TC_SORTED if sorted_rows else 0) | \
-            (TC_PER_VERTEX if per_vertex_partial is not None else 0)
+            (TC_PER_VERTEX if per_vertex_partial is not None else 0) | (TC_PRUNE if prune else 0)
     o = _options(stream=stream, **opts)
     st = Stats()
     _check(lib.tc_count_shard(n, M, rp, cp, flags, ctypes.byref(o), rank, world, partial.data_ptr(),
@@ -213,11 +223,13 @@ def count_shard(rowptr, col, rank: int, world: int, partial, *, clean=False, sor
     return stats_dict(st) if with_stats else None
 
 
-def orient(rowptr, col, *, clean=False, sorted_rows=False, stream=None, **opts):
-    """Steps a1-a4 only: the oriented compacted CSR (off+, col+) on the input's side."""
+def orient(rowptr, col, *, clean=False, sorted_rows=False, prune=False, stream=None, **opts):
+    """Steps a1-a4 only: the oriented compacted CSR (off+, col+) on the input's side
+    (with prune=True: of the leaf-pruned graph, NEXT-2)."""
     lib = _load()
     n, M, rp, cp, on_dev, keep = _arrays(rowptr, col)
-    flags = (TC_CLEAN if clean else 0) | (TC_SORTED if sorted_rows else 0) | (0 if on_dev else TC_HOST_PTRS)
+    flags = (TC_CLEAN if clean else 0) | (TC_SORTED if sorted_rows else 0) | \
+            (TC_PRUNE if prune else 0) | (0 if on_dev else TC_HOST_PTRS)
     o = _options(stream=stream, on_device=on_dev, **opts)
     mp = ctypes.c_uint64(0)
     if on_dev:
@@ -235,7 +247,7 @@ def orient(rowptr, col, *, clean=False, sorted_rows=False, stream=None, **opts):
 
 
 def clustering(rowptr, col, *, clean=False, sorted_rows=False, validate=False, per_vertex=False,
-               local=True, stream=None, with_stats=False, **opts):
+               local=True, prune=False, stream=None, with_stats=False, **opts):
     """NEXT-1: (local clustering coefficients or None, summary dict[, t(v)][, stats]).
 
     local_cc[v] = 2t(v)/(d(v)(d(v)-1)) (0 if d(v) < 2); summary = triangles, wedges,
@@ -245,7 +257,8 @@ def clustering(rowptr, col, *, clean=False, sorted_rows=False, validate=False, p
     lib = _load()
     n, M, rp, cp, on_dev, keep = _arrays(rowptr, col)
     flags = (TC_CLEAN if clean else 0) | (TC_SORTED if sorted_rows else 0) | \
-            (TC_VALIDATE if validate else 0) | (0 if on_dev else TC_HOST_PTRS)
+            (TC_VALIDATE if validate else 0) | (TC_PRUNE if prune else 0) | \
+            (0 if on_dev else TC_HOST_PTRS)
     o = _options(stream=stream, on_device=on_dev, **opts)
     cc = pv = None
     if on_dev:
@@ -273,6 +286,73 @@ def clustering(rowptr, col, *, clean=False, sorted_rows=False, validate=False, p
     if with_stats:
         out.append(stats_dict(st))
     return tuple(out)
+
+
+def edge_support(rowptr, col, *, clean=False, sorted_rows=False, validate=False, prune=False,
+                 stream=None, with_stats=False, **opts):
+    """NEXT-3: (off+, col+, support) -- the oriented CSR exactly as orient() returns it (input
+    ids, each undirected edge once, rows ascending) and the number of triangles through each
+    of its edges (uint32), on the input's side [+ stats]."""
+    lib = _load()
+    n, M, rp, cp, on_dev, keep = _arrays(rowptr, col)
+    flags = (TC_CLEAN if clean else 0) | (TC_SORTED if sorted_rows else 0) | \
+            (TC_VALIDATE if validate else 0) | (TC_PRUNE if prune else 0) | \
+            (0 if on_dev else TC_HOST_PTRS)
+    o = _options(stream=stream, on_device=on_dev, **opts)
+    mp = ctypes.c_uint64(0)
+    st = Stats()
+    if on_dev:
+        import torch
+        dev = keep[0].device
+        off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        colp = torch.empty(max(M, 1), dtype=torch.int32, device=dev)
+        sup = torch.empty(max(M, 1), dtype=torch.int32, device=dev)
+        ptrs = (off.data_ptr(), colp.data_ptr(), sup.data_ptr())
+    else:
+        off = np.zeros(n + 1, dtype=np.uint64)
+        colp = np.zeros(max(M, 1), dtype=np.uint32)
+        sup = np.zeros(max(M, 1), dtype=np.uint32)
+        ptrs = (off.ctypes.data, colp.ctypes.data, sup.ctypes.data)
+    _check(lib.tc_edge_support(n, M, rp, cp, flags, ctypes.byref(o), *ptrs, ctypes.addressof(mp),
+                               ctypes.byref(st) if with_stats else None))
+    out = (off, colp[:mp.value], sup[:mp.value])
+    return out + (stats_dict(st),) if with_stats else out
+
+
+def enumerate_triangles(rowptr, col, *, capacity=None, out=None, clean=False, sorted_rows=False,
+                        validate=False, prune=False, stream=None, with_stats=False, **opts):
+    """NEXT-3: (T, triangles) -- triangles is a (min(T, capacity), 3) array of ascending input
+    ids (int32 CUDA tensor / uint32 numpy array on the input's side), unspecified row order.
+    capacity=None sizes the output exactly (one counting call first); `out` = a preallocated
+    contiguous (capacity, 3) 32-bit array on the input's side (capacity = len(out))."""
+    lib = _load()
+    n, M, rp, cp, on_dev, keep = _arrays(rowptr, col)
+    flags = (TC_CLEAN if clean else 0) | (TC_SORTED if sorted_rows else 0) | \
+            (TC_VALIDATE if validate else 0) | (TC_PRUNE if prune else 0) | \
+            (0 if on_dev else TC_HOST_PTRS)
+    o = _options(stream=stream, on_device=on_dev, **opts)
+    total = ctypes.c_uint64(0)
+    st = Stats()
+    if out is not None:
+        capacity = len(out)
+    if capacity is None:
+        _check(lib.tc_enumerate(n, M, rp, cp, flags, ctypes.byref(o), None, 0,
+                                ctypes.addressof(total), None))
+        capacity = total.value
+    if out is not None:
+        tri = out
+        tp = out.data_ptr() if on_dev else out.ctypes.data
+    elif on_dev:
+        import torch
+        tri = torch.empty((max(capacity, 1), 3), dtype=torch.int32, device=keep[0].device)
+        tp = tri.data_ptr()
+    else:
+        tri = np.zeros((max(capacity, 1), 3), dtype=np.uint32)
+        tp = tri.ctypes.data
+    _check(lib.tc_enumerate(n, M, rp, cp, flags, ctypes.byref(o), tp, capacity,
+                            ctypes.addressof(total), ctypes.byref(st) if with_stats else None))
+    out = (int(total.value), tri[:min(total.value, capacity)])
+    return out + (stats_dict(st),) if with_stats else out
 
 
 def version() -> str:

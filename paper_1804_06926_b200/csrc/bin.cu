@@ -145,7 +145,8 @@ __global__ void __launch_bounds__(kTileThreads)
 __global__ void __launch_bounds__(kTileThreads)
     k_ocompact(const uint2 *__restrict__ orng, const uint32_t *__restrict__ col,
                const uint64_t *__restrict__ m_dev, const uint64_t *__restrict__ toff,
-               uint2 *__restrict__ orange, uint32_t *__restrict__ ovid, uint32_t *__restrict__ before) {
+               uint2 *__restrict__ orange, uint32_t *__restrict__ ovid, uint32_t *__restrict__ before,
+               bool edge_ids) {
     __shared__ uint32_t s_scan[kTileThreads / 32];
     uint64_t m = *m_dev, t0 = (uint64_t)blockIdx.x * kTileItems;
     if (t0 >= m) return;
@@ -165,7 +166,7 @@ __global__ void __launch_bounds__(kTileThreads)
         if (i < len) before[t0 + i] = (uint32_t)base;
         if (r[k].y > r[k].x) {
             orange[base] = r[k];
-            ovid[base] = col[t0 + i];
+            ovid[base] = edge_ids ? (uint32_t)(t0 + i) : col[t0 + i];
             base++;
         }
     }
@@ -329,7 +330,7 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
     scan_exclusive(ctx, tcount, toff, tiles);
     if (tiles) {
         k_ocompact<<<tiles, kTileThreads, 0, ctx.stream>>>(orng, g.col, g.m_dev, toff, orange, ovid,
-                                                           before);
+                                                           before, p.edge_ids);
         TC_LAUNCHED(ctx);
     }
     k_ooff<<<ctx.persistent_grid(4), 256, 0, ctx.stream>>>(g.off, n, g.m_dev, before, toff + tiles,

@@ -18,8 +18,15 @@
 //          one warp per small owner task, one CTA per hub task (north_star hub
 //          kernel).  Cost: min(|N+(u) > v|, d+v) probes per edge instead of
 //          d+u + d+v merge steps.
-// Per-vertex mode (TC_PER_VERTEX): each match w of (u,v) adds 1 to t(u), t(v),
-// t(w).
+// Credit modes (template parameter CM, Credit in tc_internal.cuh): every match w of
+// an oriented edge (u,v) is the triangle {u,v,w}, and besides the count it can
+//   kCmVertex  add 1 to t(u), t(v), t(w)  (TC_PER_VERTEX);
+//   kCmEdge    add 1 to the support of its three edges (u,v), (u,w), (v,w), each an
+//              entry of col+ (NEXT-3 edge support, the k-truss input);
+//   kCmList    write the triangle as three ascending input ids (NEXT-3 enumeration,
+//              "the listings of all the triangles for free").
+// In the HASH kernels the owner-side credit (t(w), or the support of (owner, w)) is
+// counted in shared memory per owner element and flushed once per task.
 #include "block_scan.cuh"
 #include "tc_internal.cuh"
 
@@ -33,46 +40,95 @@ __device__ __forceinline__ void flush_count(uint64_t acc, uint64_t *total) {
     if (threadIdx.x == 0 && t) atomicAdd((unsigned long long *)total, (unsigned long long)t);
 }
 
-template <bool PV>
-__device__ __forceinline__ void credit_edge(uint64_t *pv, uint32_t u, uint32_t v, uint32_t c) {
-    if (PV && c) {
-        atomicAdd((unsigned long long *)&pv[u], (unsigned long long)c);
-        atomicAdd((unsigned long long *)&pv[v], (unsigned long long)c);
+template <int CM>
+__device__ __forceinline__ void credit_edge(const Credit &cr, uint32_t u, uint32_t v, uint32_t c) {
+    if (CM == kCmVertex && c) {
+        atomicAdd((unsigned long long *)&cr.pv[u], (unsigned long long)c);
+        atomicAdd((unsigned long long *)&cr.pv[v], (unsigned long long)c);
     }
 }
 
+// Index of w in the ascending list a[0, len) (w must be present): edge-support credit.
+__device__ __forceinline__ uint32_t list_pos(const uint32_t *__restrict__ a, uint32_t len, uint32_t w) {
+    uint32_t lo = 0, hi = len;
+    while (lo < hi) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (a[mid] < w) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// CSR index of oriented edge (u, v) (v in N+(u)).
+__device__ __forceinline__ uint64_t edge_index(const uint64_t *__restrict__ off,
+                                               const uint32_t *__restrict__ col, uint32_t u, uint32_t v) {
+    uint64_t b = off[u];
+    return b + list_pos(col + b, (uint32_t)(off[u + 1] - b), v);
+}
+
+// kCmList: triangle {a, b, c} (rank ids) -> slot s as ascending input ids (if s < cap).
+__device__ __forceinline__ void put_triangle(const Credit &cr, uint64_t s, uint32_t a, uint32_t b,
+                                             uint32_t c) {
+    if (s >= cr.cap) return;
+    uint32_t x = cr.order[a], y = cr.order[b], z = cr.order[c];
+    uint32_t lo = min(x, min(y, z)), hi = max(x, max(y, z));
+    uint32_t* t = cr.tri + 3 * s;
+    t[0] = lo;
+    t[1] = x ^ y ^ z ^ lo ^ hi;
+    t[2] = hi;
+}
+
 // ------------------------------------------------------------------ SHORT
-template <bool PV>
+// Two-pointer merge of col+[i, ie) and col+[j, je); hit(i, j, w) per common w.
+template <class Hit>
+__device__ __forceinline__ uint32_t merge_short(const uint32_t *__restrict__ col, uint64_t i, uint64_t ie,
+                                                uint64_t j, uint64_t je, Hit hit) {
+    uint32_t c = 0;
+    if (i < ie && j < je) {
+        uint32_t a = col[i], b = col[j];
+        while (true) {
+            if (a < b) {
+                if (++i == ie) break;
+                a = col[i];
+            } else if (a > b) {
+                if (++j == je) break;
+                b = col[j];
+            } else {
+                c++;
+                hit(i, j, a);
+                if (++i == ie || ++j == je) break;
+                a = col[i];
+                b = col[j];
+            }
+        }
+    }
+    return c;
+}
+
+template <int CM>
 __global__ void __launch_bounds__(kIxThreads)
     k_short(const uint2 *__restrict__ edges, const uint64_t *__restrict__ count,
             const uint64_t *__restrict__ off, const uint32_t *__restrict__ col,
-            uint64_t *__restrict__ total, uint64_t *__restrict__ pv) {
+            uint64_t *__restrict__ total, Credit cr) {
     uint64_t ne = *count;
     uint64_t acc = 0;
     for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne;
          e += (uint64_t)gridDim.x * blockDim.x) {
         uint2 uv = edges[e];
         uint64_t i = off[uv.x], ie = off[uv.x + 1], j = off[uv.y], je = off[uv.y + 1];
-        uint32_t c = 0;
-        if (i < ie && j < je) {
-            uint32_t a = col[i], b = col[j];
-            while (true) {
-                if (a < b) {
-                    if (++i == ie) break;
-                    a = col[i];
-                } else if (a > b) {
-                    if (++j == je) break;
-                    b = col[j];
-                } else {
-                    c++;
-                    if (PV) atomicAdd((unsigned long long *)&pv[a], 1ull);
-                    if (++i == ie || ++j == je) break;
-                    a = col[i];
-                    b = col[j];
-                }
+        uint32_t c = merge_short(col, i, ie, j, je, [&](uint64_t pi, uint64_t pj, uint32_t w) {
+            if (CM == kCmVertex) atomicAdd((unsigned long long *)&cr.pv[w], 1ull);
+            if (CM == kCmEdge) {
+                atomicAdd(&cr.sup[pi], 1u);
+                atomicAdd(&cr.sup[pj], 1u);
             }
+        });
+        credit_edge<CM>(cr, uv.x, uv.y, c);
+        if (CM == kCmEdge && c) atomicAdd(&cr.sup[edge_index(off, col, uv.x, uv.y)], c);
+        if (CM == kCmList && c) {  // reserve c slots, then merge again to write them
+            uint64_t s = atomicAdd((unsigned long long *)cr.cursor, (unsigned long long)c);
+            merge_short(col, i, ie, j, je,
+                        [&](uint64_t, uint64_t, uint32_t w) { put_triangle(cr, s++, uv.x, uv.y, w); });
         }
-        credit_edge<PV>(pv, uv.x, uv.y, c);
         acc += c;
     }
     flush_count(acc, total);
@@ -83,11 +139,11 @@ __global__ void __launch_bounds__(kIxThreads)
 // Lane l walks diagonals [k0, k1); a match is counted when A[i] is taken and
 // B[j] == A[i] (B[j] is then the first element of B >= A[i]), so every common
 // element is counted exactly once across lanes.
-template <bool PV>
+template <int CM>
 __global__ void __launch_bounds__(kIxThreads)
     k_merge(const uint2 *__restrict__ edges, const uint64_t *__restrict__ count,
             const uint64_t *__restrict__ off, const uint32_t *__restrict__ col,
-            uint64_t *__restrict__ total, uint64_t *__restrict__ pv) {
+            uint64_t *__restrict__ total, Credit cr) {
     uint64_t ne = *count;
     int lane = threadIdx.x & 31;
     uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -108,21 +164,37 @@ __global__ void __launch_bounds__(kIxThreads)
             uint32_t mid = (lo + hi) >> 1;
             if (A[mid] > B[k0 - mid - 1]) hi = mid; else lo = mid + 1;
         }
-        uint32_t i = lo, j = k0 - lo, c = 0;
-        for (uint32_t k = k0; k < k1; k++) {
-            if (j >= nb || (i < na && A[i] <= B[j])) {
-                if (j < nb && A[i] == B[j]) {
-                    c++;
-                    if (PV) atomicAdd((unsigned long long *)&pv[A[i]], 1ull);
+        auto walk = [&](auto hit) {
+            uint32_t i = lo, j = k0 - lo, c = 0;
+            for (uint32_t k = k0; k < k1; k++) {
+                if (j >= nb || (i < na && A[i] <= B[j])) {
+                    if (j < nb && A[i] == B[j]) {
+                        c++;
+                        hit(i, j, A[i]);
+                    }
+                    i++;
+                } else {
+                    j++;
                 }
-                i++;
-            } else {
-                j++;
             }
-        }
-        if (PV) {
+            return c;
+        };
+        const uint64_t ab = off[uv.x], bb = off[uv.y];
+        uint32_t c = walk([&](uint32_t i, uint32_t j, uint32_t w) {
+            if (CM == kCmVertex) atomicAdd((unsigned long long *)&cr.pv[w], 1ull);
+            if (CM == kCmEdge) {
+                atomicAdd(&cr.sup[ab + i], 1u);
+                atomicAdd(&cr.sup[bb + j], 1u);
+            }
+        });
+        if (CM == kCmVertex || CM == kCmEdge) {
             uint32_t ce = __reduce_add_sync(0xffffffffu, c);
-            if (lane == 0) credit_edge<PV>(pv, uv.x, uv.y, ce);
+            if (lane == 0) credit_edge<CM>(cr, uv.x, uv.y, ce);
+            if (CM == kCmEdge && lane == 0 && ce) atomicAdd(&cr.sup[edge_index(off, col, uv.x, uv.y)], ce);
+        }
+        if (CM == kCmList && c) {
+            uint64_t s = atomicAdd((unsigned long long *)cr.cursor, (unsigned long long)c);
+            walk([&](uint32_t, uint32_t, uint32_t w) { put_triangle(cr, s++, uv.x, uv.y, w); });
         }
         acc += c;
     }
@@ -130,11 +202,11 @@ __global__ void __launch_bounds__(kIxThreads)
 }
 
 // ------------------------------------------------------------------ SEARCH
-template <bool PV>
+template <int CM>
 __global__ void __launch_bounds__(kIxThreads)
     k_search(const uint2 *__restrict__ edges, const uint64_t *__restrict__ count,
              const uint64_t *__restrict__ off, const uint32_t *__restrict__ col,
-             uint64_t *__restrict__ total, uint64_t *__restrict__ pv) {
+             uint64_t *__restrict__ total, Credit cr) {
     uint64_t ne = *count;
     int lane = threadIdx.x & 31;
     uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -150,21 +222,36 @@ __global__ void __launch_bounds__(kIxThreads)
             const uint32_t *t = A; A = B; B = t;
             uint32_t tn = na; na = nb; nb = tn;
         }
-        uint32_t c = 0;
-        for (uint32_t k = lane; k < na; k += 32) {
-            uint32_t x = A[k], lo = 0, hi = nb;
-            while (lo < hi) {
-                uint32_t mid = (lo + hi) >> 1;
-                if (B[mid] < x) lo = mid + 1; else hi = mid;
+        auto scan = [&](auto hit) {
+            uint32_t c = 0;
+            for (uint32_t k = lane; k < na; k += 32) {
+                uint32_t x = A[k], lo = 0, hi = nb;
+                while (lo < hi) {
+                    uint32_t mid = (lo + hi) >> 1;
+                    if (B[mid] < x) lo = mid + 1; else hi = mid;
+                }
+                if (lo < nb && B[lo] == x) {
+                    c++;
+                    hit(k, lo, x);
+                }
             }
-            if (lo < nb && B[lo] == x) {
-                c++;
-                if (PV) atomicAdd((unsigned long long *)&pv[x], 1ull);
+            return c;
+        };
+        uint32_t c = scan([&](uint32_t k, uint32_t l, uint32_t w) {
+            if (CM == kCmVertex) atomicAdd((unsigned long long *)&cr.pv[w], 1ull);
+            if (CM == kCmEdge) {
+                atomicAdd(&cr.sup[A - col + k], 1u);
+                atomicAdd(&cr.sup[B - col + l], 1u);
             }
-        }
-        if (PV) {
+        });
+        if (CM == kCmVertex || CM == kCmEdge) {
             uint32_t ce = __reduce_add_sync(0xffffffffu, c);
-            if (lane == 0) credit_edge<PV>(pv, uv.x, uv.y, ce);
+            if (lane == 0) credit_edge<CM>(cr, uv.x, uv.y, ce);
+            if (CM == kCmEdge && lane == 0 && ce) atomicAdd(&cr.sup[edge_index(off, col, uv.x, uv.y)], ce);
+        }
+        if (CM == kCmList && c) {
+            uint64_t s = atomicAdd((unsigned long long *)cr.cursor, (unsigned long long)c);
+            scan([&](uint32_t, uint32_t, uint32_t w) { put_triangle(cr, s++, uv.x, uv.y, w); });
         }
         acc += c;
     }
@@ -290,8 +377,11 @@ __device__ __forceinline__ uint32_t opaque(uint32_t v) {
 struct HashProbe {  // bucket hash of the owner's N+ (any id range)
     uint32_t tab, absent;  // absent = the owner itself: never in its own N+
     int bits;
-    // per-vertex mode: hit counters per table slot (cnt != nullptr), else global atomics
+    // per-vertex / edge mode: hit counters per table slot (cnt != nullptr), else global atomics
     uint32_t *cnt = nullptr;
+    const uint32_t *xl = nullptr;  // edge mode without counters: the owner's N+ (col+ at xb)
+    uint32_t xlen = 0;
+    uint64_t xb = 0;
     // bit c set iff element c of the slot is in the list (rel + c < len, mod 2^32)
     // and in the table
     template <int N>
@@ -303,10 +393,12 @@ struct HashProbe {  // bucket hash of the owner's N+ (any id range)
             h |= table_contains(tab, bits, rel + c < len ? e[c] : absent) << c;
         return h;
     }
-    // per-vertex credit of a hit's third vertex w
-    __device__ __forceinline__ void credit(uint32_t w, uint64_t *pv) const {
+    // owner-side credit of a hit w: t(w) (vertex mode) or sup(owner, w) (edge mode)
+    template <int CM>
+    __device__ __forceinline__ void credit(uint32_t w, const Credit &cr) const {
         if (!cnt) {
-            atomicAdd((unsigned long long *)&pv[w], 1ull);
+            if (CM == kCmVertex) atomicAdd((unsigned long long *)&cr.pv[w], 1ull);
+            if (CM == kCmEdge) atomicAdd(&cr.sup[xb + list_pos(xl, xlen, w)], 1u);
             return;
         }
         atomicAdd(&cnt[table_find(tab, bits, w)], 1u);
@@ -322,6 +414,9 @@ struct BitProbe {   // bitmap over the rank-id range [base, base + span) of the 
     // owner's set bits (wpre = per-word prefix popcounts) when cnt != nullptr
     uint32_t *cnt = nullptr;
     const uint16_t *wpre = nullptr;
+    const uint32_t *xl = nullptr;  // edge mode without counters: the owner's N+ (col+ at xb)
+    uint32_t xlen = 0;
+    uint64_t xb = 0;
     template <int N>
     __device__ __forceinline__ uint32_t hit_mask(const uint32_t (&e)[N], uint32_t rel,
                                                  uint32_t len) const {
@@ -342,9 +437,11 @@ struct BitProbe {   // bitmap over the rank-id range [base, base + span) of the 
         uint32_t m = len ? ((1u << b) - 1u) & ~((1u << a) - 1u) : 0u;
         return hv & m;
     }
-    __device__ __forceinline__ void credit(uint32_t w, uint64_t *pv) const {
+    template <int CM>
+    __device__ __forceinline__ void credit(uint32_t w, const Credit &cr) const {
         if (!cnt) {
-            atomicAdd((unsigned long long *)&pv[w], 1ull);
+            if (CM == kCmVertex) atomicAdd((unsigned long long *)&cr.pv[w], 1ull);
+            if (CM == kCmEdge) atomicAdd(&cr.sup[xb + list_pos(xl, xlen, w)], 1u);
             return;
         }
         uint32_t o = w - base, word = lds32(bm + 4 * (o >> 5));
@@ -383,12 +480,13 @@ __device__ __forceinline__ uint32_t quad_count(uint32_t lo, uint32_t hi) {
 // uint4 load and four probes per lane per window.  In each 32-quad window lane t
 // finds its list from a bitmap of the list starts inside the window (reduce-or +
 // popc): no per-item search.  Returns the number of hits.
-template <bool PV, class Probe>
+template <int CM, class Probe>
 __device__ __forceinline__ uint64_t probe_quads(const Probe &contains,
                                                 const QuadDesc &d, uint32_t nl, uint32_t ib,
                                                 uint32_t ie,
                                                 const uint32_t *__restrict__ col,
-                                                uint64_t *__restrict__ pv) {
+                                                uint32_t owner, const Credit &cr) {
+    constexpr bool kVid = CM != kCmNone;
     const int lane = threadIdx.x & 31;
     uint32_t hits = 0;
     if (ib >= ie) return 0;
@@ -419,7 +517,7 @@ __device__ __forceinline__ uint64_t probe_quads(const Probe &contains,
             r[k] = d.rng[li];
             if (!live) r[k].y = r[k].x;
             e0[k] = qi << kSlotShift;
-            ly[k] = PV ? d.vid[li] : 0u;
+            ly[k] = kVid ? d.vid[li] : 0u;
 #pragma unroll
             for (int v = 0; v < kSlot / 4; v++) q[k][v] = __ldg(col4 + (uint64_t)qi * (kSlot / 4) + v);
             i0 = __shfl_sync(0xffffffffu, li, 31);  // list holding slot wk + 31
@@ -437,11 +535,32 @@ __device__ __forceinline__ uint64_t probe_quads(const Probe &contains,
             }
             const uint32_t hm = contains.hit_mask(e, rel, len);
             hits += __popc(hm);
-            if (PV && hm) {
+            if (CM == kCmVertex && hm) {
 #pragma unroll
                 for (int c = 0; c < kSlot; c++)
-                    if ((hm >> c) & 1u) contains.credit(e[c], pv);
-                atomicAdd((unsigned long long *)&pv[ly[k]], (unsigned long long)__popc(hm));
+                    if ((hm >> c) & 1u) contains.template credit<CM>(e[c], cr);
+                atomicAdd((unsigned long long *)&cr.pv[ly[k]], (unsigned long long)__popc(hm));
+            }
+            if (CM == kCmEdge && hm) {   // (list vertex, w) at its col+ slot; base edge ly
+#pragma unroll
+                for (int c = 0; c < kSlot; c++)
+                    if ((hm >> c) & 1u) {
+                        contains.template credit<CM>(e[c], cr);
+                        atomicAdd(&cr.sup[e0[k] + c], 1u);
+                    }
+                atomicAdd(&cr.sup[ly[k]], (uint32_t)__popc(hm));
+            }
+            if (CM == kCmList) {         // warp-aggregated reservation of the output slots
+                const uint32_t nh = __popc(hm);
+                const uint32_t incl = warp_inclusive_scan<SumOp>(nh);
+                const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+                uint64_t sb = 0;
+                if (lane == 0 && tot)
+                    sb = atomicAdd((unsigned long long *)cr.cursor, (unsigned long long)tot);
+                uint64_t slot = __shfl_sync(0xffffffffu, sb, 0) + incl - nh;
+#pragma unroll
+                for (int c = 0; c < kSlot; c++)
+                    if ((hm >> c) & 1u) put_triangle(cr, slot++, ly[k], owner, e[c]);
             }
         }
     }
@@ -451,14 +570,18 @@ __device__ __forceinline__ uint64_t probe_quads(const Probe &contains,
 // Probe entry j of HASH owner x (bin.cu header): j < indeg -> the j-th in-edge
 // (u -> x) of x's in-list, range = N+(u) after x (empty if x does not own it), y = u;
 // else the (j - indeg)-th compacted out-part entry of x: range = N+(v), y = v.
+// Edge mode: y = the CSR index of the entry's own edge instead (in-part: lo - 1;
+// out-part: ovid holds edge indices, bin_edges' edge_ids).
+template <int CM>
 __device__ __forceinline__ void hash_desc(const HashParams &hp, uint64_t inb, uint32_t indeg,
                                           uint64_t ob, uint32_t ocnt, uint32_t j, uint32_t &lo,
                                           uint32_t &hi, uint32_t &y) {
     lo = hi = y = 0;
     if (j < indeg) {
         lo = hp.ulo[inb + j];
-        y = hp.in_src[inb + j];
-        if (lo) hi = (uint32_t)hp.off[y + 1];
+        uint32_t u = hp.in_src[inb + j];
+        if (lo) hi = (uint32_t)hp.off[u + 1];
+        y = CM == kCmEdge ? lo - 1 : u;
     } else if (j - indeg < ocnt) {
         uint2 r = hp.orange[ob + (j - indeg)];
         y = hp.ovid[ob + (j - indeg)];
@@ -468,17 +591,19 @@ __device__ __forceinline__ void hash_desc(const HashParams &hp, uint64_t inb, ui
 }
 
 // Warp tasks: owners with d+(x) <= kWarpTableSlots/4 (table in the warp's smem slice).
-template <bool PV>
+template <int CM>
 __global__ void __launch_bounds__(kIxThreads, TC_HASH_WARP_MINBLOCKS)
     k_hash_warp(const uint2 *__restrict__ tasks, const uint64_t *__restrict__ ntasks, HashParams hp,
-                uint64_t *__restrict__ total, uint64_t *__restrict__ pv) {
+                uint64_t *__restrict__ total, Credit cr) {
     constexpr uint32_t L = kWarpTaskLists;
+    constexpr bool PV = CM != kCmNone;                        // descriptors carry vid
+    constexpr bool kCnt = CM == kCmVertex || CM == kCmEdge;   // owner-side hit counters
     __shared__ __align__(16) uint32_t s_tab[kHashWarps][kWarpTableSlots];
     __shared__ uint32_t s_qb[kHashWarps][L];
     __shared__ uint2 s_rng[kHashWarps][L];
     __shared__ uint32_t s_pre[kHashWarps][L + 1];
     __shared__ uint32_t s_vid[kHashWarps][PV ? L : 1];
-    __shared__ uint32_t s_cnt[PV ? kHashWarps : 1][PV ? kWarpTableSlots : 1];  // per-vertex hits per slot
+    __shared__ uint32_t s_cnt[kCnt ? kHashWarps : 1][kCnt ? kWarpTableSlots : 1];  // owner hits per slot
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const QuadDesc d{s_pre[wib], s_qb[wib], s_vid[wib], s_rng[wib]};
     uint64_t nt = *ntasks;
@@ -502,7 +627,7 @@ __global__ void __launch_bounds__(kIxThreads, TC_HASH_WARP_MINBLOCKS)
 #pragma unroll
         for (uint32_t h = 0; h < L; h += 32) {
             uint32_t lo = 0, hi = 0, y = 0;
-            hash_desc(hp, inb, indeg, ob, ocnt, j0 + h + lane, lo, hi, y);
+            hash_desc<CM>(hp, inb, indeg, ob, ocnt, j0 + h + lane, lo, hi, y);
             uint32_t nq = quad_count(lo, hi);
             uint32_t inc = warp_inclusive_scan<SumOp>(nq);
             uint32_t keep = __ballot_sync(0xffffffffu, nq != 0);
@@ -514,20 +639,26 @@ __global__ void __launch_bounds__(kIxThreads, TC_HASH_WARP_MINBLOCKS)
         int bits = table_bits(dx);
         for (uint32_t s = lane; s < (1u << bits); s += 32) {
             tab[s] = kEmpty;
-            if (PV) s_cnt[wib][s] = 0u;
+            if (kCnt) s_cnt[wib][s] = 0u;
         }
         __syncwarp();
         table_insert(tab, bits, col + xb, dx, lane, 32);
         __syncwarp();
         HashProbe hpb{opaque(smem_addr(tab)), x, bits};
-        if (PV) hpb.cnt = s_cnt[wib];
-        uint64_t h = probe_quads<PV>(hpb, d, nl, 0, run, col, pv);
-        if (PV) {
+        if (kCnt) hpb.cnt = s_cnt[wib];
+        uint64_t h = probe_quads<CM>(hpb, d, nl, 0, run, col, x, cr);
+        if (kCnt) {
             __syncwarp();
-            for (uint32_t s = lane; s < (1u << bits); s += 32)
-                if (s_cnt[wib][s]) atomicAdd((unsigned long long *)&pv[tab[s]], (unsigned long long)s_cnt[wib][s]);
+            for (uint32_t s = lane; s < (1u << bits); s += 32) {
+                uint32_t c = s_cnt[wib][s];
+                if (!c) continue;
+                if (CM == kCmVertex) atomicAdd((unsigned long long *)&cr.pv[tab[s]], (unsigned long long)c);
+                if (CM == kCmEdge) atomicAdd(&cr.sup[xb + list_pos(col + xb, dx, tab[s])], c);
+            }
+        }
+        if (CM == kCmVertex) {
             uint64_t hw = warp_sum_u64(h);
-            if (lane == 0 && hw) atomicAdd((unsigned long long *)&pv[x], (unsigned long long)hw);
+            if (lane == 0 && hw) atomicAdd((unsigned long long *)&cr.pv[x], (unsigned long long)hw);
         }
         acc += h;
         __syncwarp();
@@ -541,11 +672,12 @@ __global__ void __launch_bounds__(kIxThreads, TC_HASH_WARP_MINBLOCKS)
 constexpr uint32_t kSmemWords = kHashSlots;            // 16 KB of table / bitmap per CTA
 constexpr uint32_t kPvCounters = 4096;                 // per-vertex: smem hit counters (16 KB)
 static_assert(kCtaBitmapBits == kSmemWords * 32, "bitmap owners are classified in bin.cu");
-template <bool PV, bool kBitmap>
-__global__ void __launch_bounds__(kIxThreads, PV ? 4 : TC_HASH_CTA_MINBLOCKS)
+template <int CM, bool kBitmap>
+__global__ void __launch_bounds__(kIxThreads, CM != kCmNone ? 4 : TC_HASH_CTA_MINBLOCKS)
     k_hash_cta(const uint2 *__restrict__ tasks, const uint64_t *__restrict__ ntasks, HashParams hp,
-               uint64_t *__restrict__ total, uint64_t *__restrict__ pv) {
+               uint64_t *__restrict__ total, Credit cr) {
     constexpr uint32_t L = kCtaTaskLists;
+    constexpr bool PV = CM != kCmNone;   // descriptors carry vid
     static_assert(L == kIxThreads, "one descriptor per thread");
     __shared__ __align__(16) uint32_t s_tab[kSmemWords];
     __shared__ uint32_t s_qb[L];
@@ -555,7 +687,7 @@ __global__ void __launch_bounds__(kIxThreads, PV ? 4 : TC_HASH_CTA_MINBLOCKS)
     __shared__ uint64_t s_scan[kHashWarps];
     // per-vertex bitmap owners: hit counters per element of N+(x) (owners with
     // d+ <= kPvCounters; others credit w with global atomics) + word prefix popcounts
-    constexpr bool kCnt = PV;   // bitmap: counter per set bit; hash: counter per slot
+    constexpr bool kCnt = CM == kCmVertex || CM == kCmEdge;  // bitmap: per set bit; hash: per slot
     static_assert(kPvCounters == kHashSlots, "hash owners count hits per table slot");
     __shared__ uint32_t s_cnt[kCnt ? kPvCounters : 1];
     __shared__ uint16_t s_wpre[kCnt && kBitmap ? kSmemWords + 1 : 1];
@@ -575,7 +707,7 @@ __global__ void __launch_bounds__(kIxThreads, PV ? 4 : TC_HASH_CTA_MINBLOCKS)
         uint32_t indeg = hp.has_in[x] ? (uint32_t)(hp.in_off[x + 1] - inb) : 0u;
         uint32_t ocnt = (uint32_t)(hp.ooff[x + 1] - ob);
         uint32_t lo, hi, y;
-        hash_desc(hp, inb, indeg, ob, ocnt, task.y * L + threadIdx.x, lo, hi, y);
+        hash_desc<CM>(hp, inb, indeg, ob, ocnt, task.y * L + threadIdx.x, lo, hi, y);
         uint32_t nq = quad_count(lo, hi);
         // one 64-bit scan: high word = compacted index of non-empty entries, low = quads
         uint64_t tot;
@@ -597,6 +729,9 @@ __global__ void __launch_bounds__(kIxThreads, PV ? 4 : TC_HASH_CTA_MINBLOCKS)
             }
             __syncthreads();
             BitProbe bp{tab, base, (words - 1) * 32 + 31};
+            bp.xl = col + xb;
+            bp.xlen = dx;
+            bp.xb = xb;
             const bool use_cnt = kCnt && kBitmap && dx <= kPvCounters;
             if (use_cnt) {
                 // exclusive prefix popcount per bitmap word (blocked: thread t owns a run)
@@ -614,11 +749,15 @@ __global__ void __launch_bounds__(kIxThreads, PV ? 4 : TC_HASH_CTA_MINBLOCKS)
                 bp.cnt = s_cnt;
                 bp.wpre = s_wpre;
             }
-            h = probe_quads<PV>(bp, d, nl, ib, ie, col, pv);
+            h = probe_quads<CM>(bp, d, nl, ib, ie, col, x, cr);
             __syncthreads();
             if (use_cnt) {   // the k-th set bit is the k-th element of the sorted N+(x)
-                for (uint32_t k = threadIdx.x; k < dx; k += blockDim.x)
-                    if (s_cnt[k]) atomicAdd((unsigned long long *)&pv[col[xb + k]], (unsigned long long)s_cnt[k]);
+                for (uint32_t k = threadIdx.x; k < dx; k += blockDim.x) {
+                    uint32_t c = s_cnt[k];
+                    if (!c) continue;
+                    if (CM == kCmVertex) atomicAdd((unsigned long long *)&cr.pv[col[xb + k]], (unsigned long long)c);
+                    if (CM == kCmEdge) atomicAdd(&cr.sup[xb + k], c);
+                }
                 __syncthreads();
             }
         } else {
@@ -634,53 +773,63 @@ __global__ void __launch_bounds__(kIxThreads, PV ? 4 : TC_HASH_CTA_MINBLOCKS)
                 __syncthreads();
                 HashProbe hpb{tab, x, bits};
                 if (kCnt) hpb.cnt = s_cnt;
-                h += probe_quads<PV>(hpb, d, nl, ib, ie, col, pv);
+                h += probe_quads<CM>(hpb, d, nl, ib, ie, col, x, cr);
                 __syncthreads();
                 if (kCnt) {
-                    for (uint32_t s = threadIdx.x; s < (1u << bits); s += blockDim.x)
-                        if (s_cnt[s]) atomicAdd((unsigned long long *)&pv[s_tab[s]], (unsigned long long)s_cnt[s]);
+                    for (uint32_t s = threadIdx.x; s < (1u << bits); s += blockDim.x) {
+                        uint32_t c = s_cnt[s];
+                        if (!c) continue;
+                        if (CM == kCmVertex)
+                            atomicAdd((unsigned long long *)&cr.pv[s_tab[s]], (unsigned long long)c);
+                        if (CM == kCmEdge)   // the chunk is col+[xb + c0, + clen), ascending
+                            atomicAdd(&cr.sup[xb + c0 + list_pos(col + xb + c0, clen, s_tab[s])], c);
+                    }
                     __syncthreads();
                 }
             }
         }
-        if (PV) {
+        if (CM == kCmVertex) {
             uint64_t hw = warp_sum_u64(h);
             if ((threadIdx.x & 31) == 0 && hw)
-                atomicAdd((unsigned long long *)&pv[x], (unsigned long long)hw);
+                atomicAdd((unsigned long long *)&cr.pv[x], (unsigned long long)hw);
         }
         acc += h;
     }
     flush_count(acc, total);
 }
 
-template <bool PV>
+template <int CM>
 static void launch_all(Ctx &ctx, const Oriented &g, const Bins &bins, uint64_t *total,
-                       uint64_t *pv) {
+                       const Credit &cr) {
     int grid = ctx.persistent_grid(8);
-    k_hash_cta<PV, true><<<ctx.persistent_grid(8), kIxThreads, 0, ctx.stream>>>(
-        bins.tasks_bitmap, bins.ntasks_bitmap, bins.hp, total, pv);
+    k_hash_cta<CM, true><<<ctx.persistent_grid(8), kIxThreads, 0, ctx.stream>>>(
+        bins.tasks_bitmap, bins.ntasks_bitmap, bins.hp, total, cr);
     TC_LAUNCHED(ctx);
-    k_hash_cta<PV, false><<<ctx.persistent_grid(8), kIxThreads, 0, ctx.stream>>>(
-        bins.tasks_cta, bins.ntasks_cta, bins.hp, total, pv);
+    k_hash_cta<CM, false><<<ctx.persistent_grid(8), kIxThreads, 0, ctx.stream>>>(
+        bins.tasks_cta, bins.ntasks_cta, bins.hp, total, cr);
     TC_LAUNCHED(ctx);
-    k_hash_warp<PV><<<grid, kIxThreads, 0, ctx.stream>>>(bins.tasks_warp, bins.ntasks_warp, bins.hp,
-                                                          total, pv);
+    k_hash_warp<CM><<<grid, kIxThreads, 0, ctx.stream>>>(bins.tasks_warp, bins.ntasks_warp, bins.hp,
+                                                          total, cr);
     TC_LAUNCHED(ctx);
-    k_merge<PV><<<grid, kIxThreads, 0, ctx.stream>>>(bins.edges[1], bins.count + 1, g.off, g.col,
-                                                     total, pv);
+    k_merge<CM><<<grid, kIxThreads, 0, ctx.stream>>>(bins.edges[1], bins.count + 1, g.off, g.col,
+                                                     total, cr);
     TC_LAUNCHED(ctx);
-    k_search<PV><<<grid, kIxThreads, 0, ctx.stream>>>(bins.edges[2], bins.count + 2, g.off, g.col,
-                                                      total, pv);
+    k_search<CM><<<grid, kIxThreads, 0, ctx.stream>>>(bins.edges[2], bins.count + 2, g.off, g.col,
+                                                      total, cr);
     TC_LAUNCHED(ctx);
-    k_short<PV><<<grid, kIxThreads, 0, ctx.stream>>>(bins.edges[0], bins.count + 0, g.off, g.col,
-                                                     total, pv);
+    k_short<CM><<<grid, kIxThreads, 0, ctx.stream>>>(bins.edges[0], bins.count + 0, g.off, g.col,
+                                                     total, cr);
     TC_LAUNCHED(ctx);
 }
 
 void intersect_all(Ctx &ctx, const Oriented &g, const Bins &bins, uint64_t *total_dev,
-                   uint64_t *per_vertex) {
-    if (per_vertex) launch_all<true>(ctx, g, bins, total_dev, per_vertex);
-    else launch_all<false>(ctx, g, bins, total_dev, nullptr);
+                   const Credit &cr) {
+    switch (cr.mode) {
+        case kCmVertex: launch_all<kCmVertex>(ctx, g, bins, total_dev, cr); break;
+        case kCmEdge: launch_all<kCmEdge>(ctx, g, bins, total_dev, cr); break;
+        case kCmList: launch_all<kCmList>(ctx, g, bins, total_dev, cr); break;
+        default: launch_all<kCmNone>(ctx, g, bins, total_dev, cr); break;
+    }
 }
 
 }  // namespace tc

@@ -18,10 +18,12 @@
 
 namespace tc {
 
+// Also the TC_PRUNE survival test: a pruned-away vertex has degree 0 (prune.cu), and
+// without pruning every arc's endpoints have degree >= 1.
 __device__ __forceinline__ bool rank_less(const uint32_t *__restrict__ deg, uint32_t u,
                                           uint32_t v) {
     uint32_t du = deg[u], dv = deg[v];
-    return du < dv || (du == dv && u < v);
+    return du != 0 && (du < dv || (du == dv && u < v));
 }
 
 static int id_bits(uint64_t n) {
@@ -232,7 +234,8 @@ static void pairs_to_csr(Ctx &ctx, uint64_t n, uint64_t cap, uint32_t *okey, uin
 }
 
 void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
-                  bool need_sorted, uint32_t segsort_block_max, Oriented &out, Timer *tm) {
+                  bool need_sorted, uint32_t segsort_block_max, Oriented &out, Timer *tm,
+                  PruneInfo &prune) {
     int b = id_bits(n);
     uint32_t tiles = (uint32_t)((M + kTileItems - 1) / kTileItems);
     if (tm) tm->begin(kClean);
@@ -261,6 +264,11 @@ void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, cons
     int grid = ctx.persistent_grid(8);
     k_deg_pairs<<<grid, 256, 0, ctx.stream>>>(E, m_dev, b, deg);
     TC_LAUNCHED(ctx);
+    if (prune.enabled) {
+        if (tm) tm->begin(kPrune);
+        prune_pairs(ctx, n, b, prune.rounds_wanted, E, m_dev, deg, M, prune);
+        if (tm) tm->end(kPrune);
+    }
     rank_permutation(ctx, n, deg, out);
     uint32_t *okey = ctx.alloc<uint32_t>(M), *oval = ctx.alloc<uint32_t>(M);
     k_orient_pairs<<<grid, 256, 0, ctx.stream>>>(E, m_dev, b, out.newid, okey, oval, dplus);
@@ -332,13 +340,20 @@ __global__ void __launch_bounds__(kTileThreads)
 }
 
 void orient_clean(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
-                  bool need_sorted, uint32_t segsort_block_max, Oriented &out, Timer *tm) {
+                  bool need_sorted, uint32_t segsort_block_max, Oriented &out, Timer *tm,
+                  PruneInfo &prune) {
     uint32_t tiles = (uint32_t)((M + kTileItems - 1) / kTileItems);
     int grid = ctx.persistent_grid(8);
     if (tm) tm->begin(kOrient);
     uint32_t *deg = ctx.alloc<uint32_t>(n);
     k_deg_rowptr<<<grid, 256, 0, ctx.stream>>>(rowptr, n, deg);
     TC_LAUNCHED(ctx);
+    if (prune.enabled) {
+        if (tm) tm->begin(kPrune);
+        prune.m_before_host = M / 2;
+        prune_csr(ctx, n, M, rowptr, col, prune.rounds_wanted, deg, prune);
+        if (tm) tm->end(kPrune);
+    }
     rank_permutation(ctx, n, deg, out);
     uint32_t *counts = ctx.alloc<uint32_t>(tiles);
     uint64_t *offs = ctx.alloc<uint64_t>(tiles + 1);
@@ -365,7 +380,7 @@ __global__ void __launch_bounds__(kTileThreads)
     k_pairs_original(const uint64_t *__restrict__ off, const uint32_t *__restrict__ colp, uint64_t n,
                      const uint64_t *__restrict__ m_dev, const uint32_t *__restrict__ order,
                      uint32_t *__restrict__ src, uint32_t *__restrict__ dst,
-                     uint32_t *__restrict__ dcount) {
+                     uint32_t *__restrict__ idx, uint32_t *__restrict__ dcount) {
     __shared__ uint32_t s_row[kTileItems];
     __shared__ uint32_t s_scan[kTileThreads / 32];
     uint64_t m = *m_dev;
@@ -377,30 +392,51 @@ __global__ void __launch_bounds__(kTileThreads)
         uint32_t a = order[s_row[i]], c = order[colp[t0 + i]];
         src[t0 + i] = a;
         dst[t0 + i] = c;
+        idx[t0 + i] = (uint32_t)(t0 + i);
         atomicAdd(&dcount[a], 1u);
     }
 }
 
-void to_original(Ctx &ctx, const Oriented &g, uint64_t *off_out, uint32_t *col_out) {
+// out[k] = in[perm[k]] for k < *m_dev.
+__global__ void k_permute(const uint32_t *__restrict__ in, const uint32_t *__restrict__ perm,
+                          const uint64_t *__restrict__ m_dev, uint32_t *__restrict__ out) {
+    uint64_t m = *m_dev;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m;
+         k += (uint64_t)gridDim.x * blockDim.x)
+        out[k] = in[perm[k]];
+}
+
+void to_original(Ctx &ctx, const Oriented &g, uint64_t *off_out, uint32_t *col_out,
+                 const uint32_t *pay_in, uint32_t *pay_out) {
     uint64_t cap = g.m_cap, n = g.n;
     int b = id_bits(n);
+    int grid = ctx.persistent_grid(8);
     uint32_t *src = ctx.alloc<uint32_t>(cap), *dst = ctx.alloc<uint32_t>(cap);
-    uint32_t *src2 = ctx.alloc<uint32_t>(cap), *dst2 = ctx.alloc<uint32_t>(cap);
+    uint32_t *kA = ctx.alloc<uint32_t>(cap), *kB = ctx.alloc<uint32_t>(cap);
+    uint32_t *kC = ctx.alloc<uint32_t>(cap);
+    uint32_t *vA = ctx.alloc<uint32_t>(cap), *vB = ctx.alloc<uint32_t>(cap);
+    uint32_t *vC = ctx.alloc<uint32_t>(cap), *vD = ctx.alloc<uint32_t>(cap);
     uint32_t *cnt = ctx.alloc<uint32_t>(n + 1);
     TC_CUDA(cudaMemsetAsync(cnt, 0, (n + 1) * sizeof(uint32_t), ctx.stream));
     uint32_t tiles = (uint32_t)((cap + kTileItems - 1) / kTileItems);
     k_pairs_original<<<tiles, kTileThreads, 0, ctx.stream>>>(g.off, g.col, n, g.m_dev, g.order, src,
-                                                             dst, cnt);
+                                                             dst, vA, cnt);
     TC_LAUNCHED(ctx);
-    // rows ascending: stable sort by target, then stable sort by source
-    bool a1 = radix_sort_pairs(ctx, dst, dst2, src, src2, cap, g.m_dev, b);
-    uint32_t *d1 = a1 ? dst2 : dst, *s1 = a1 ? src2 : src;
-    uint32_t *d2 = a1 ? dst : dst2, *s2 = a1 ? src : src2;
-    bool a2 = radix_sort_pairs(ctx, s1, s2, d1, d2, cap, g.m_dev, b);
-    uint32_t *col_sorted = a2 ? d2 : d1;
+    // rows ascending: the edge index (vA) sorted stably by target, then by source
+    uint32_t *k1, *p1, *k2, *p2;
+    radix_sort_pairs_from(ctx, dst, vA, kA, kB, vB, vC, cap, g.m_dev, b, &k1, &p1);
+    uint32_t *s1 = (k1 == kA) ? kB : kA;
+    k_permute<<<grid, 256, 0, ctx.stream>>>(src, p1, g.m_dev, s1);
+    TC_LAUNCHED(ctx);
+    radix_sort_pairs_from(ctx, s1, p1, k1, kC, vA, vD, cap, g.m_dev, b, &k2, &p2);
+    (void)k2;
     scan_exclusive(ctx, cnt, off_out, n);
-    TC_CUDA(cudaMemcpyAsync(col_out, col_sorted, cap * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
-                            ctx.stream));
+    k_permute<<<grid, 256, 0, ctx.stream>>>(dst, p2, g.m_dev, col_out);
+    TC_LAUNCHED(ctx);
+    if (pay_in) {
+        k_permute<<<grid, 256, 0, ctx.stream>>>(pay_in, p2, g.m_dev, pay_out);
+        TC_LAUNCHED(ctx);
+    }
 }
 
 __global__ void k_pv_original(const uint64_t *__restrict__ pv_new, const uint32_t *__restrict__ newid,

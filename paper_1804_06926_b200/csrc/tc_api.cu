@@ -44,7 +44,7 @@ static uint64_t *pinned_scratch() {
     return p;
 }
 
-enum Mode { kCount, kShard, kOrientOnly, kClustering };
+enum Mode { kCount, kShard, kOrientOnly, kClustering, kSupport, kEnumerate };
 
 struct Call {
     uint64_t n, M;
@@ -64,6 +64,9 @@ struct Call {
     uint64_t *m_plus = nullptr;
     double *cc = nullptr;             // kClustering (nullable)
     tc_clustering_summary *csum = nullptr;
+    uint32_t *support = nullptr;      // kSupport (with off_plus / col_plus / m_plus)
+    uint32_t *triangles = nullptr;    // kEnumerate: capacity triples
+    uint64_t capacity = 0;
 };
 
 static tc_status check_args(const Call &c) {
@@ -74,14 +77,25 @@ static tc_status check_args(const Call &c) {
     if (c.mode == kCount && !c.total_host) return set_error("total is NULL"), TC_EINVAL;
     if (c.mode == kClustering && (c.flags & TC_PER_VERTEX))
         return set_error("tc_clustering: TC_PER_VERTEX is implied (pass per_vertex or NULL)"), TC_EINVAL;
+    if (c.mode == kClustering && (c.flags & TC_PRUNE))
+        return set_error("tc_clustering: TC_PRUNE would change the degrees d(v) of c(v)"), TC_EINVAL;
     if (c.mode == kShard) {
         if (!c.partial_dev) return set_error("partial_dev is NULL"), TC_EINVAL;
         if (c.world < 1 || c.rank < 0 || c.rank >= c.world)
             return set_error("need 0 <= rank < world"), TC_EINVAL;
         if (c.flags & TC_HOST_PTRS) return set_error("tc_count_shard takes device pointers"), TC_EINVAL;
     }
-    if (c.mode == kOrientOnly && (!c.off_plus || (!c.col_plus && c.M > 0) || !c.m_plus))
-        return set_error("tc_orient output pointer is NULL"), TC_EINVAL;
+    if ((c.mode == kOrientOnly || c.mode == kSupport) &&
+        (!c.off_plus || (!c.col_plus && c.M > 0) || !c.m_plus))
+        return set_error("tc_orient / tc_edge_support output pointer is NULL"), TC_EINVAL;
+    if (c.mode == kSupport && !c.support && c.M > 0)
+        return set_error("tc_edge_support: support is NULL"), TC_EINVAL;
+    if (c.mode == kEnumerate && (!c.total_host || (c.capacity && !c.triangles)))
+        return set_error("tc_enumerate: total is NULL, or triangles is NULL with capacity > 0"),
+               TC_EINVAL;
+    if ((c.mode == kSupport || c.mode == kEnumerate) && (c.flags & TC_PER_VERTEX))
+        return set_error("TC_PER_VERTEX is not an option of tc_edge_support / tc_enumerate"),
+               TC_EINVAL;
     if ((c.flags & TC_PER_VERTEX) && c.mode != kOrientOnly && !c.per_vertex)
         return set_error("TC_PER_VERTEX needs per_vertex"), TC_EINVAL;
     if ((c.flags & TC_SORTED) && !(c.flags & TC_CLEAN))
@@ -173,14 +187,25 @@ static void run(Call &c) {
     // it, and the HASH ranges probe only the part of N+(a) after b.
     const bool need_sorted = true;
 
+    PruneInfo prune;
+    prune.enabled = c.flags & TC_PRUNE;
+    prune.rounds_wanted = c.opt.prune_rounds;
     if (c.n > 0 && c.M > 0) {
         Oriented g;
         if (c.flags & TC_CLEAN)
-            orient_clean(ctx, c.n, c.M, rowptr, col, need_sorted, c.opt.segsort_block_max, g, tm);
+            orient_clean(ctx, c.n, c.M, rowptr, col, need_sorted, c.opt.segsort_block_max, g, tm,
+                         prune);
         else
-            orient_dirty(ctx, c.n, c.M, rowptr, col, need_sorted, c.opt.segsort_block_max, g, tm);
+            orient_dirty(ctx, c.n, c.M, rowptr, col, need_sorted, c.opt.segsort_block_max, g, tm,
+                         prune);
+        if (c.stats && prune.m_before)
+            TC_CUDA(cudaMemcpyAsync(pin + 24, prune.m_before, sizeof(uint64_t),
+                                    cudaMemcpyDeviceToHost, ctx.stream));
+        if (c.stats && prune.enabled)
+            TC_CUDA(cudaMemcpyAsync(pin + 25, g.m_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                                    ctx.stream));
 
-        if (c.mode == kOrientOnly) {  // N+ in the caller's ids, rows ascending
+        if (c.mode == kOrientOnly) {  // N+ in the caller's ids, rows ascending (tc_orient)
             uint64_t *off_o = ctx.alloc<uint64_t>(c.n + 1);
             uint32_t *col_o = ctx.alloc<uint32_t>(g.m_cap);
             to_original(ctx, g, off_o, col_o);
@@ -197,6 +222,7 @@ static void run(Call &c) {
 
         if (tm) tm->begin(kBin);
         BinParams bp;
+        bp.edge_ids = c.mode == kSupport;
         bp.short_max = c.opt.short_max;
         bp.skew_ratio = c.opt.skew_ratio;
         bp.hub_min = c.opt.hub_min_dplus;
@@ -217,9 +243,53 @@ static void run(Call &c) {
         bin_edges(ctx, g, bp, bins);
         if (tm) tm->end(kBin);
 
+        Credit cr;
+        uint32_t *sup = nullptr;
+        if (pv) {
+            cr.mode = kCmVertex;
+            cr.pv = pv_new;
+        } else if (c.mode == kSupport) {
+            sup = ctx.alloc<uint32_t>(g.m_cap);
+            TC_CUDA(cudaMemsetAsync(sup, 0, g.m_cap * sizeof(uint32_t), ctx.stream));
+            cr.mode = kCmEdge;
+            cr.sup = sup;
+        } else if (c.mode == kEnumerate) {
+            cr.mode = kCmList;
+            cr.cap = c.capacity;
+            cr.tri = (host && c.capacity) ? ctx.alloc<uint32_t>(3 * c.capacity) : c.triangles;
+            cr.cursor = ctx.alloc<uint64_t>(1);
+            cr.order = g.order;
+            TC_CUDA(cudaMemsetAsync(cr.cursor, 0, sizeof(uint64_t), ctx.stream));
+        }
         if (tm) tm->begin(kIntersect);
-        intersect_all(ctx, g, bins, total_dev, pv_new);
+        intersect_all(ctx, g, bins, total_dev, cr);
         if (tm) tm->end(kIntersect);
+        if (c.mode == kSupport) {   // N+ in the caller's ids with each edge's support
+            uint64_t *off_o = ctx.alloc<uint64_t>(c.n + 1);
+            uint32_t *col_o = ctx.alloc<uint32_t>(g.m_cap), *sup_o = ctx.alloc<uint32_t>(g.m_cap);
+            to_original(ctx, g, off_o, col_o, sup, sup_o);
+            cudaMemcpyKind kind = host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+            uint64_t m = 0;
+            TC_CUDA(cudaMemcpyAsync(&m, g.m_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx.stream));
+            TC_CUDA(cudaStreamSynchronize(ctx.stream));
+            TC_CUDA(cudaMemcpyAsync(c.off_plus, off_o, (c.n + 1) * sizeof(uint64_t), kind, ctx.stream));
+            if (m) {
+                TC_CUDA(cudaMemcpyAsync(c.col_plus, col_o, m * sizeof(uint32_t), kind, ctx.stream));
+                TC_CUDA(cudaMemcpyAsync(c.support, sup_o, m * sizeof(uint32_t), kind, ctx.stream));
+            }
+            if (host) st.d2h_bytes += (c.n + 1) * sizeof(uint64_t) + 2 * m * sizeof(uint32_t);
+            *c.m_plus = m;
+        }
+        if (c.mode == kEnumerate && host && c.capacity) {  // min(T, capacity) triples back
+            uint64_t T = 0;
+            TC_CUDA(cudaMemcpyAsync(&T, total_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx.stream));
+            TC_CUDA(cudaStreamSynchronize(ctx.stream));
+            uint64_t k = T < c.capacity ? T : c.capacity;
+            if (k)
+                TC_CUDA(cudaMemcpyAsync(c.triangles, cr.tri, 3 * k * sizeof(uint32_t),
+                                        cudaMemcpyDeviceToHost, ctx.stream));
+            st.d2h_bytes += 3 * k * sizeof(uint32_t);
+        }
         if (pv_out) per_vertex_to_original(ctx, g, pv_new, pv_dev);
         if (c.mode == kClustering) clustering(ctx, g, pv_new, cc_dev, cc_out);
         if (c.stats) {  // async into pinned memory; read after the final sync
@@ -228,7 +298,7 @@ static void run(Call &c) {
             TC_CUDA(cudaMemcpyAsync(pin + 16, g.m_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost,
                                     ctx.stream));
         }
-    } else if (c.mode == kOrientOnly) {
+    } else if (c.mode == kOrientOnly || c.mode == kSupport) {
         cudaMemcpyKind kind = host ? cudaMemcpyHostToHost : cudaMemcpyHostToDevice;
         std::vector<uint64_t> zeros(c.n + 1, 0);
         TC_CUDA(cudaMemcpyAsync(c.off_plus, zeros.data(), (c.n + 1) * sizeof(uint64_t), kind,
@@ -238,7 +308,7 @@ static void run(Call &c) {
         return;
     }
 
-    if (c.mode == kCount || c.mode == kClustering) {
+    if (c.mode == kCount || c.mode == kClustering || c.mode == kEnumerate || c.mode == kSupport) {
         TC_CUDA(cudaMemcpyAsync(pin + 20, total_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost,
                                 ctx.stream));
         st.d2h_bytes += sizeof(uint64_t);
@@ -262,7 +332,7 @@ static void run(Call &c) {
     ctx.release();
     if (c.mode != kShard || c.stats) TC_CUDA(cudaStreamSynchronize(ctx.stream));
     TC_CUDA(cudaGetLastError());
-    if (c.mode == kCount) *c.total_host = pin[20];
+    if (c.mode == kCount || c.mode == kEnumerate) *c.total_host = pin[20];
     if (c.mode == kClustering && c.csum) {
         tc_clustering_summary &r = *c.csum;
         r.triangles = pin[20];
@@ -299,6 +369,12 @@ static void run(Call &c) {
         // entry (<= 2 per edge, 1 for ~96%) + the owners' lists for the table builds
         st.bytes_hash = 4 * st.work_probe + 8 * st.bin_edges[3] + 4 * st.table_loads;
         st.kernel_launches = ctx.launches;
+        if (prune.enabled && c.n > 0 && c.M > 0) {
+            st.ms_prune = tm->ms(kPrune);
+            uint64_t before = prune.m_before ? pin[24] : prune.m_before_host;
+            st.pruned_edges = before - pin[25];
+            st.prune_rounds = prune.rounds;
+        }
         *c.stats = st;
     }
 }
@@ -402,6 +478,32 @@ tc_status tc_clustering(uint64_t n, uint64_t m, const uint64_t *row_offsets,
     c.cc = local_cc;
     c.per_vertex = per_vertex;
     c.csum = summary;
+    c.stats = stats;
+    return guarded(c);
+}
+
+tc_status tc_edge_support(uint64_t n, uint64_t m, const uint64_t *row_offsets,
+                          const uint32_t *col_indices, uint32_t flags, const tc_options *opt,
+                          uint64_t *off_plus, uint32_t *col_plus, uint32_t *support,
+                          uint64_t *m_plus, tc_stats *stats) {
+    Call c{n, m, row_offsets, col_indices, flags, resolve(opt)};
+    c.mode = kSupport;
+    c.off_plus = off_plus;
+    c.col_plus = col_plus;
+    c.support = support;
+    c.m_plus = m_plus;
+    c.stats = stats;
+    return guarded(c);
+}
+
+tc_status tc_enumerate(uint64_t n, uint64_t m, const uint64_t *row_offsets,
+                       const uint32_t *col_indices, uint32_t flags, const tc_options *opt,
+                       uint32_t *triangles, uint64_t capacity, uint64_t *total, tc_stats *stats) {
+    Call c{n, m, row_offsets, col_indices, flags, resolve(opt)};
+    c.mode = kEnumerate;
+    c.triangles = triangles;
+    c.capacity = capacity;
+    c.total_host = total;
     c.stats = stats;
     return guarded(c);
 }

@@ -200,7 +200,7 @@ struct Oriented {
 };
 
 // Phase timer: CUDA events on the call's stream, read after the final sync.
-enum Phase { kClean = 0, kOrient, kSort, kBin, kIntersect, kNumPhases };
+enum Phase { kClean = 0, kOrient, kSort, kBin, kIntersect, kPrune, kNumPhases };
 struct Timer {
     cudaEvent_t ev[kNumPhases][2] = {};
     bool used[kNumPhases] = {};
@@ -226,14 +226,37 @@ struct Timer {
     }
 };
 
+// NEXT-2 leaf pruning (prune.cu).  enabled: TC_PRUNE given; rounds: 0 = to the
+// fixed point (2-core).  Filled in: rounds executed, the edge count before pruning.
+struct PruneInfo {
+    bool enabled = false;
+    uint32_t rounds_wanted = 0;
+    uint64_t rounds = 0;
+    const uint64_t *m_before = nullptr;  // device scalar (dirty path)
+    uint64_t m_before_host = 0;          // clean path: arcs / 2
+};
+// Dirty path: E (sorted (min << b | max) keys, *m_dev of them), deg = degrees of E.
+// On return E / m_dev / deg describe the pruned graph (E compacted).
+void prune_pairs(Ctx &ctx, uint64_t n, int b, uint32_t rounds, uint64_t *&E, uint64_t *&m_dev,
+                 uint32_t *&deg, uint64_t m_host_cap, PruneInfo &info);
+// Clean path: deg = row lengths on entry; on return the pruned degrees (0 = deleted
+// vertex); an arc survives iff both endpoint degrees are > 0.
+void prune_csr(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
+               uint32_t rounds, uint32_t *&deg, PruneInfo &info);
+
 // a1 (dirty input) + a2 + a3: raw CSR -> oriented relabelled CSR (+ a4 if need_sorted).
 void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
-                  bool need_sorted, uint32_t segsort_block_max, Oriented &out, Timer *tm);
+                  bool need_sorted, uint32_t segsort_block_max, Oriented &out, Timer *tm,
+                  PruneInfo &prune);
 // a2 + a3 for clean symmetric input (+ a4 if need_sorted).
 void orient_clean(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
-                  bool need_sorted, uint32_t segsort_block_max, Oriented &out, Timer *tm);
+                  bool need_sorted, uint32_t segsort_block_max, Oriented &out, Timer *tm,
+                  PruneInfo &prune);
 // The oriented CSR in INPUT ids with ascending rows (tc_orient output).
-void to_original(Ctx &ctx, const Oriented &g, uint64_t *off_out, uint32_t *col_out);
+// With pay_in (m entries in CSR order, e.g. edge supports) also pay_out[k] = the
+// payload of the edge written to col_out[k].
+void to_original(Ctx &ctx, const Oriented &g, uint64_t *off_out, uint32_t *col_out,
+                 const uint32_t *pay_in = nullptr, uint32_t *pay_out = nullptr);
 // pv_out[v] = pv_new[newid[v]].
 void per_vertex_to_original(Ctx &ctx, const Oriented &g, const uint64_t *pv_new, uint64_t *pv_out);
 
@@ -255,7 +278,8 @@ struct HashParams {
                                        // col+), 0 if not this rank's in-part HASH work
     const uint64_t *ooff = nullptr;    // compacted out-part entries of each owner:
     const uint2 *orange = nullptr;     //   probe ranges [lo, hi) of col+
-    const uint32_t *ovid = nullptr;    //   the edge's target (per-vertex credit)
+    const uint32_t *ovid = nullptr;    //   the edge's target (per-vertex credit), or its CSR
+                                       //   index when binned with edge_ids (edge support)
     const uint64_t *work_prefix = nullptr;  // multi-GPU source split (world > 1)
     uint32_t n = 0, short_max = 0, skew_ratio = 0;
     int force = -1, rank = 0, world = 1;
@@ -314,14 +338,27 @@ struct BinParams {
     int rank, world;
     const uint64_t *work_prefix;  // exclusive prefix of per-source work (world > 1)
     uint64_t work_chunk;          // unused (computed on the device)
+    bool edge_ids = false;        // out-part entries record their edge's CSR index (kCmEdge)
 };
 
 void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins);
 void work_prefix(Ctx &ctx, const Oriented &g, uint64_t *prefix /* n+1 */);
 
-// a6 + a7: all intersection kernels; adds into total_dev (and per_vertex if non-null).
+// What each triangle found in a6 credits besides the total (intersect.cu header).
+enum CreditMode { kCmNone = 0, kCmVertex = 1, kCmEdge = 2, kCmList = 3 };
+struct Credit {
+    int mode = kCmNone;
+    uint64_t *pv = nullptr;           // kCmVertex: t(v), rank ids, n entries
+    uint32_t *sup = nullptr;          // kCmEdge: support per entry of col+ (m entries)
+    uint32_t *tri = nullptr;          // kCmList: cap triples of ascending input ids
+    uint64_t *cursor = nullptr;       // kCmList: triples found so far (device counter)
+    uint64_t cap = 0;
+    const uint32_t *order = nullptr;  // kCmList: rank id -> input id
+};
+
+// a6 + a7: all intersection kernels; adds into total_dev and credits per `cr`.
 void intersect_all(Ctx &ctx, const Oriented &g, const Bins &bins, uint64_t *total_dev,
-                   uint64_t *per_vertex);
+                   const Credit &cr);
 
 // Validation (TC_VALIDATE); returns a TC_EGRAPH message or "".
 std::string validate_graph(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr,

@@ -28,7 +28,8 @@ def declared_functions():
 def test_exports_every_declared_symbol(lib):
     names = declared_functions()
     assert set(names) >= {"tc_count", "tc_count_ex", "tc_count_shard", "tc_orient",
-                          "tc_clustering", "tc_last_error", "tc_default_options", "tc_version"}
+                          "tc_clustering", "tc_edge_support", "tc_enumerate", "tc_last_error",
+                          "tc_default_options", "tc_version"}
     for name in names:
         assert hasattr(lib, name), name
 
@@ -44,7 +45,8 @@ def test_struct_layout(lib):
     assert ctypes.sizeof(tc.Options) == 64
     assert o.short_max == 32 and o.skew_ratio == 0 and o.hub_min_dplus == 64
     assert o.force_variant == -1 and o.segsort_block_max == 8192
-    assert ctypes.sizeof(tc.Stats) == 6 * 8 + 16 * 8
+    assert o.prune_rounds == 0 and not any(o.reserved)
+    assert ctypes.sizeof(tc.Stats) == 7 * 8 + 18 * 8
     assert ctypes.sizeof(tc.ClusteringSummary) == 32
 
 
@@ -56,6 +58,28 @@ def test_clustering_argument_errors(lib):
                              None, None, None, None) == EINVAL
     assert b"implied" in lib.tc_last_error()
     assert lib.tc_clustering(1, 0, None, None, tc.TC_HOST_PTRS, None, None, None, None, None) == EINVAL
+    # leaf pruning would change d(v): rejected
+    assert lib.tc_clustering(1, 0, rp.ctypes.data, None, tc.TC_PRUNE | tc.TC_HOST_PTRS, None,
+                             None, None, None, None) == EINVAL
+    assert b"TC_PRUNE" in lib.tc_last_error()
+
+
+def test_next3_argument_errors(lib):
+    rp = np.zeros(2, np.uint64)
+    EINVAL = 1
+    out = np.zeros(4, np.uint64)
+    # edge support: outputs required, TC_PER_VERTEX rejected
+    assert lib.tc_edge_support(1, 0, rp.ctypes.data, None, tc.TC_HOST_PTRS, None, None, None, None,
+                               None, None) == EINVAL
+    assert lib.tc_edge_support(1, 0, rp.ctypes.data, None, tc.TC_HOST_PTRS | tc.TC_PER_VERTEX, None,
+                               out.ctypes.data, out.ctypes.data, out.ctypes.data, out.ctypes.data,
+                               None) == EINVAL
+    # enumeration: total required; triangles required when capacity > 0
+    assert lib.tc_enumerate(1, 0, rp.ctypes.data, None, tc.TC_HOST_PTRS, None, None, 0, None,
+                            None) == EINVAL
+    assert lib.tc_enumerate(1, 0, rp.ctypes.data, None, tc.TC_HOST_PTRS, None, None, 5,
+                            out.ctypes.data, None) == EINVAL
+    assert b"capacity" in lib.tc_last_error()
 
 
 def test_argument_errors_before_device(lib):
