@@ -62,6 +62,11 @@ def _load():
                                      ctypes.c_void_p]
         lib.oracle_edge_support.restype = None
         lib.oracle_edge_support.argtypes = [ctypes.c_uint64, _u64p, _u32p, _u64p, _u32p, _u32p]
+        lib.oracle_orient_order.restype = ctypes.c_int64
+        lib.oracle_orient_order.argtypes = [ctypes.c_uint64, _u64p, _u32p, ctypes.c_int, _u64p, _u32p]
+        lib.oracle_masked_spgemm.restype = ctypes.c_uint64
+        lib.oracle_masked_spgemm.argtypes = [ctypes.c_uint64, _u64p, _u32p, ctypes.c_int, _u64p, _u32p,
+                                             _u32p]
         lib.oracle_enumerate.restype = ctypes.c_uint64
         lib.oracle_enumerate.argtypes = [ctypes.c_uint64, _u64p, _u32p, ctypes.c_void_p,
                                          ctypes.c_uint64]
@@ -205,6 +210,31 @@ def enumerate_triangles(n: int, clean_rowptr, clean_col):
     T2 = int(lib.oracle_enumerate(n, _p64(clean_rowptr), _p32(clean_col), out.ctypes.data, T))
     assert T2 == T
     return out[:3 * T].reshape(T, 3)
+
+
+def orient_order(n: int, clean_rowptr, clean_col, id_order: bool = False):
+    """oracle.orient with the vertex order of Alg. 3 line 1 (degree, id) or, with id_order,
+    plain ids (Fig. mm): the upper triangle U as a CSR, rows ascending."""
+    lib = _load()
+    clean_rowptr, clean_col = _csr(clean_rowptr, clean_col)
+    off = np.zeros(n + 1, dtype=np.uint64)
+    colp = np.zeros(max(1, int(clean_rowptr[n]) // 2 + 1), dtype=np.uint32)
+    m = lib.oracle_orient_order(n, _p64(clean_rowptr), _p32(clean_col), int(id_order), _p64(off),
+                                _p32(colp))
+    return off, colp[:m].copy()
+
+
+def masked_spgemm(n: int, clean_rowptr, clean_col, id_order: bool = False):
+    """NEXT-4 (Alg. 3, masked per P:723-731): (off_u, col_u, C at U's entries, n=T)."""
+    lib = _load()
+    off, colp = orient_order(n, clean_rowptr, clean_col, id_order)
+    clean_rowptr, clean_col = _csr(clean_rowptr, clean_col)
+    m = int(off[n]) if n else 0
+    c = np.zeros(max(m, 1), dtype=np.uint32)
+    cp = colp if m else np.zeros(1, dtype=np.uint32)
+    T = lib.oracle_masked_spgemm(n, _p64(clean_rowptr), _p32(clean_col), int(id_order), _p64(off),
+                                 _p32(cp), _p32(c))
+    return off, colp, c[:m], int(T)
 
 
 def num_threads() -> int:

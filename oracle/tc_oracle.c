@@ -403,3 +403,57 @@ uint64_t oracle_enumerate(uint64_t n, const uint64_t *crow, const uint32_t *ccol
     }
     return k;
 }
+
+/*
+ * NEXT-4: Alg. 3 "Triangle_Count_Matrix" restricted to
+ * A's nonzeros, its future-work "masking", written out step by step on a
+ * clean symmetric CSR with sorted rows:
+ *   line 1  permute: vertex order pi = increasing number of nonzeros (degree), ties by
+ *           id -- or the identity when id_order != 0 (the order of Fig. mm);
+ *   line 2  L_ij = A_ij if pi(i) > pi(j), U_ij = A_ij if pi(i) < pi(j), A = L + U;
+ *   line 3  B = L U, i.e. B_ij = sum_k L_ik U_kj;
+ *   line 4  C = A o B (Hadamard), evaluated at A's nonzeros only;
+ *   line 5  n = (1/2) sum_ij C_ij (reading R7: the printed A_ij is C_ij).
+ * Output: for every entry e = (i, col_plus[e]) of the upper triangle (off_plus /
+ * col_plus as oracle_orient_order writes it, so pi(i) < pi(j)), c_values[e] = C_ij,
+ * computed as the sum over k in row i of L (neighbours k of i with pi(k) < pi(i)) of
+ * U_kj (A_kj = 1 and pi(k) < pi(j)).  Returns n.
+ */
+static int order_before(const uint64_t *rowptr, int id_order, uint64_t a, uint64_t b) {
+    if (id_order) return a < b;
+    return rank_less(rowptr, a, b);
+}
+
+/* oracle_orient with either order: N+(u) = { v in N(u) : pi(u) < pi(v) }, rows ascending. */
+int64_t oracle_orient_order(uint64_t n, const uint64_t *rowptr, const uint32_t *col, int id_order,
+                            uint64_t *off_plus, uint32_t *col_plus) {
+    uint64_t k = 0;
+    off_plus[0] = 0;
+    for (uint64_t u = 0; u < n; u++) {
+        for (uint64_t e = rowptr[u]; e < rowptr[u + 1]; e++)
+            if (order_before(rowptr, id_order, u, col[e])) col_plus[k++] = col[e];
+        off_plus[u + 1] = k;
+    }
+    return (int64_t)k;
+}
+
+uint64_t oracle_masked_spgemm(uint64_t n, const uint64_t *rowptr, const uint32_t *col, int id_order,
+                              const uint64_t *off_plus, const uint32_t *col_plus,
+                              uint32_t *c_values) {
+    uint64_t sum = 0;
+    for (uint64_t i = 0; i < n; i++) {
+        for (uint64_t e = off_plus[i]; e < off_plus[i + 1]; e++) {
+            uint64_t j = col_plus[e];
+            uint32_t b = 0;                                   /* B_ij at a nonzero A_ij */
+            for (uint64_t p = rowptr[i]; p < rowptr[i + 1]; p++) {
+                uint64_t k = col[p];
+                if (!order_before(rowptr, id_order, k, i)) continue;       /* L_ik = 0 */
+                if (!order_before(rowptr, id_order, k, j)) continue;       /* U_kj = 0 */
+                if (contains(col + rowptr[k], rowptr[k + 1] - rowptr[k], (uint32_t)j)) b++;
+            }
+            c_values[e] = b;                                  /* C_ij = A_ij * B_ij */
+            sum += 2 * (uint64_t)b;                           /* C_ij and C_ji */
+        }
+    }
+    return sum / 2;
+}

@@ -258,3 +258,51 @@ def test_enumerate_wheel_closed_form(n):
     tri = O.enumerate_triangles(n, *clean(G.wheel(n)))
     assert len(tri) == n - 1 and (tri[:, 0] == 0).all()
     assert (tri[:, 0] < tri[:, 1]).all() and (tri[:, 1] < tri[:, 2]).all()
+
+
+# ------------------------------------------------------------------ NEXT-4: masked SpGEMM
+def test_masked_spgemm_fig_mm(golden):
+    """Alg. 3 on the paper's worked example reproduces the printed B and C."""
+    fx = golden("fig_mm.txt")
+    A = np.array(fx["A"], dtype=np.int64)
+    B = np.array(fx["B"], dtype=np.int64)
+    C = np.array(fx["C"], dtype=np.int64)
+    L, U = np.tril(A, -1), np.triu(A, 1)
+    assert (L @ U == B).all() and (A * B == C).all()      # the transcription is consistent
+    assert C.sum() // 2 == fx["T"][0][0] == 3
+    g = G.fig_mm()
+    off, colp, c, T = O.masked_spgemm(7, *clean(g), id_order=True)
+    assert T == 3
+    for i in range(7):
+        for e in range(int(off[i]), int(off[i + 1])):
+            j = int(colp[e])
+            assert j > i and c[e] == C[i, j]
+    assert sum(int(x) for x in c) == C.sum() // 2            # upper triangle only (P:557-559)
+
+
+def perm_order(A, id_order):
+    d = A.sum(1)
+    return np.arange(len(d)) if id_order else np.lexsort((np.arange(len(d)), d))
+
+
+@pytest.mark.parametrize("id_order", [True, False])
+@pytest.mark.parametrize("g", [G.gnp(60, 0.15, 8), G.rmat(8, 8), G.karate(), G.wheel(12),
+                               G.clique_union(500, 300, seed=3), G.road_mesh(12, 12, seed=1)],
+                         ids=lambda g: g.name)
+def test_masked_spgemm_dense_route(g, id_order):
+    """C = A o (L U) by dense numpy matmul on the permuted matrix (Alg. 3 lines 1-4)."""
+    A = np.zeros((g.n, g.n), dtype=np.int64)
+    s, d = g.arc_list()
+    A[s, d] = 1
+    A[d, s] = 1
+    np.fill_diagonal(A, 0)
+    order = perm_order(A, id_order)                         # line 1: rows by nonzeros
+    pos = np.empty(g.n, dtype=np.int64)
+    pos[order] = np.arange(g.n)
+    Ap = A[np.ix_(order, order)].astype(np.float64)
+    Cp = Ap * (np.tril(Ap, -1) @ np.triu(Ap, 1))           # lines 2-4
+    off, colp, c, T = O.masked_spgemm(g.n, *clean(g), id_order=id_order)
+    src = np.repeat(np.arange(g.n), np.diff(off.astype(np.int64)))
+    assert (pos[src] < pos[colp.astype(np.int64)]).all()    # upper triangle in that order
+    assert (c.astype(np.int64) == Cp[pos[src], pos[colp.astype(np.int64)]].astype(np.int64)).all()
+    assert T == int(round(Cp.sum())) // 2 == O.count(g.n, g.rowptr, g.col)
