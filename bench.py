@@ -188,6 +188,15 @@ def next_rows_23(tc, torch, np, graphgen, rp, cl, flush, stream, m, T, count_ms)
         "output_GB_per_s": 12 * T / (ems * 1e-3) / 1e9,
         "call": "tc_enumerate into a preallocated device buffer of T triples (capacity = T)"}
     del tri
+    # NEXT-4 masked SpGEMM (Alg. 3): C = A o (L U) at the upper-triangle nonzeros
+    mms, (_, _, cvals, Tm) = _timed(torch, flush, stream, lambda: tc.masked_spgemm(rp, cl))
+    assert Tm == T and int(cvals.to(torch.int64).sum().item()) == T
+    rows["NEXT-4 masked SpGEMM"] = {
+        "ms_per_call": mms, "edges_per_s": m / (mms * 1e-3), "overhead_vs_count_ms": mms - count_ms,
+        "max_C": int(cvals.max().item()),
+        "call": "tc_masked_spgemm (rank order, Alg. 3 line 1): C at each upper-triangle entry "
+                "mapped back to input ids"}
+    del cvals
     # NEXT-2 leaf pruning where it matters: the road mesh (BASELINE configs[3])
     g = graphgen.road_mesh()
     rrp = torch.from_numpy(g.rowptr.view(np.int64)).to(rp.device)

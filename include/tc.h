@@ -80,7 +80,11 @@ enum {
                                 triangle keeps degree >= 2); ranks use the PRUNED degrees, so
                                 tc_orient returns the oriented pruned graph.  Not allowed with
                                 tc_clustering (c(v) needs the unpruned degrees).             */
-    TC_ALL_FLAGS = 0x3fu
+    TC_ID_ORDER = 1u << 6,   /* orient by vertex id instead of (degree, id): N+(u) = {v in N(u) :
+                                v > u}, the order of the paper's Fig. mm example (Alg. 3 without
+                                its row permutation).  Counts are unchanged; slower
+                                on skewed graphs (d+ is no longer bounded by sqrt(2m)).         */
+    TC_ALL_FLAGS = 0x7fu
 };
 
 typedef enum {
@@ -233,6 +237,25 @@ tc_status tc_edge_support(uint64_t n, uint64_t m, const uint64_t *row_offsets,
 tc_status tc_enumerate(uint64_t n, uint64_t m, const uint64_t *row_offsets,
                        const uint32_t *col_indices, uint32_t flags, const tc_options *opt,
                        uint32_t *triangles, uint64_t capacity, uint64_t *total, tc_stats *stats);
+
+/* NEXT-4: the matrix formulation as a front end on the same
+ * intersection core (Alg. 3 "Triangle_Count_Matrix", and its future-work
+ * "masking" P:723-731: no materialised B, only A's nonzeros, upper triangle only,
+ * P:557-561).  With the vertices in rank order (Alg. 3 line 1: rows "ordered by an
+ * increasing number of nonzeros", ties by id; or id order under TC_ID_ORDER, the
+ * order of Fig. mm), A = L + U and
+ *     C = A o (L U),   C_ij = #{ k : k before i and before j, A_ik = A_kj = 1 }
+ * for every nonzero A_ij -- the number of triangles whose two LATEST vertices are i, j.
+ * Output: the upper triangle (each undirected edge once) in the layout of tc_orient
+ * (input ids, rows ascending; off_plus n+1, col_plus capacity m, *nnz_u used) with
+ * c_values[e] = C at that entry (C is symmetric), and *total = (1/2) sum_ij C_ij = T
+ * (Alg. 3 line 6; R7: the printed "A_ij" there is read as C_ij).  Pointer side per
+ * TC_HOST_PTRS (nnz_u, total: host).  Flags: TC_CLEAN, TC_SORTED, TC_HOST_PTRS,
+ * TC_VALIDATE, TC_PRUNE, TC_ID_ORDER.  Synchronous. */
+tc_status tc_masked_spgemm(uint64_t n, uint64_t m, const uint64_t *row_offsets,
+                           const uint32_t *col_indices, uint32_t flags, const tc_options *opt,
+                           uint64_t *off_plus, uint32_t *col_plus, uint32_t *c_values,
+                           uint64_t *nnz_u, uint64_t *total, tc_stats *stats);
 
 /* Thread-local message describing the last failure on this thread ("" if none). */
 const char *tc_last_error(void);

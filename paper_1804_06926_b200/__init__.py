@@ -20,6 +20,7 @@ import numpy as np
 __all__ = ["count", "count_ex", "count_shard", "orient", "clustering", "edge_support",
            "enumerate_triangles", "stats_dict", "library_path",
            "TC_CLEAN", "TC_SORTED", "TC_PER_VERTEX", "TC_HOST_PTRS", "TC_VALIDATE", "TC_PRUNE",
+           "TC_ID_ORDER", "masked_spgemm",
            "VARIANT_AUTO", "VARIANT_SHORT", "VARIANT_MERGE", "VARIANT_SEARCH", "VARIANT_HASH",
            "TCError"]
 
@@ -27,6 +28,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libtc_b200.so")
 
 TC_CLEAN, TC_SORTED, TC_PER_VERTEX, TC_HOST_PTRS, TC_VALIDATE, TC_PRUNE = 1, 2, 4, 8, 16, 32
+TC_ID_ORDER = 64
 VARIANT_AUTO, VARIANT_SHORT, VARIANT_MERGE, VARIANT_SEARCH, VARIANT_HASH = -1, 0, 1, 2, 3
 _STATUS = {0: "TC_OK", 1: "TC_EINVAL", 2: "TC_EGRAPH", 3: "TC_ENOMEM", 4: "TC_ECUDA"}
 TC_ERROR = (1 << 64) - 1
@@ -101,6 +103,9 @@ def _load():
     lib.tc_enumerate.argtypes = [u64, u64, vp, vp, u32, ctypes.POINTER(Options), vp, u64, vp,
                                  ctypes.POINTER(Stats)]
     lib.tc_enumerate.restype = ctypes.c_int
+    lib.tc_masked_spgemm.argtypes = [u64, u64, vp, vp, u32, ctypes.POINTER(Options), vp, vp, vp, vp,
+                                     vp, ctypes.POINTER(Stats)]
+    lib.tc_masked_spgemm.restype = ctypes.c_int
     lib.tc_last_error.argtypes = []
     lib.tc_last_error.restype = ctypes.c_char_p
     lib.tc_version.argtypes = []
@@ -137,6 +142,14 @@ def _arrays(rowptr, col):
     return n, col.size, rowptr.ctypes.data, (col.ctypes.data if col.size else None), False, (rowptr, col)
 
 
+def _flags(clean=False, sorted_rows=False, per_vertex=False, validate=False, prune=False,
+           id_order=False, on_dev=True):
+    return ((TC_CLEAN if clean else 0) | (TC_SORTED if sorted_rows else 0) |
+            (TC_PER_VERTEX if per_vertex else 0) | (TC_VALIDATE if validate else 0) |
+            (TC_PRUNE if prune else 0) | (TC_ID_ORDER if id_order else 0) |
+            (0 if on_dev else TC_HOST_PTRS))
+
+
 def _options(stream=None, force_variant=None, short_max=None, skew_ratio=None, hub_min_dplus=None,
              segsort_block_max=None, prune_rounds=None, on_device=True):
     o = Options()
@@ -167,7 +180,7 @@ def stats_dict(s: Stats) -> dict:
 
 
 def count_ex(rowptr, col, *, clean=False, sorted_rows=False, per_vertex=False, validate=False,
-             prune=False, stream=None, with_stats=False, **opts):
+             prune=False, id_order=False, stream=None, with_stats=False, **opts):
     """Triangle count of the graph (rowptr, col) [+ per-vertex counts, stats].
 
     torch CUDA tensors -> device pointers on the current stream; numpy arrays or
@@ -177,7 +190,8 @@ def count_ex(rowptr, col, *, clean=False, sorted_rows=False, per_vertex=False, v
     n, M, rp, cp, on_dev, keep = _arrays(rowptr, col)
     flags = (TC_CLEAN if clean else 0) | (TC_SORTED if sorted_rows else 0) | \
             (TC_PER_VERTEX if per_vertex else 0) | (TC_VALIDATE if validate else 0) | \
-            (TC_PRUNE if prune else 0) | (0 if on_dev else TC_HOST_PTRS)
+            (TC_PRUNE if prune else 0) | (TC_ID_ORDER if id_order else 0) | \
+            (0 if on_dev else TC_HOST_PTRS)
     o = _options(stream=stream, on_device=on_dev, **opts)
     total = ctypes.c_uint64(0)
     pv = None
@@ -223,13 +237,13 @@ def count_shard(rowptr, col, rank: int, world: int, partial, *, clean=False, sor
     return stats_dict(st) if with_stats else None
 
 
-def orient(rowptr, col, *, clean=False, sorted_rows=False, prune=False, stream=None, **opts):
+def orient(rowptr, col, *, clean=False, sorted_rows=False, prune=False, id_order=False, stream=None,
+           **opts):
     """Steps a1-a4 only: the oriented compacted CSR (off+, col+) on the input's side
     (with prune=True: of the leaf-pruned graph, NEXT-2)."""
     lib = _load()
     n, M, rp, cp, on_dev, keep = _arrays(rowptr, col)
-    flags = (TC_CLEAN if clean else 0) | (TC_SORTED if sorted_rows else 0) | \
-            (TC_PRUNE if prune else 0) | (0 if on_dev else TC_HOST_PTRS)
+    flags = _flags(clean, sorted_rows, False, False, prune, id_order, on_dev)
     o = _options(stream=stream, on_device=on_dev, **opts)
     mp = ctypes.c_uint64(0)
     if on_dev:
@@ -352,6 +366,36 @@ def enumerate_triangles(rowptr, col, *, capacity=None, out=None, clean=False, so
     _check(lib.tc_enumerate(n, M, rp, cp, flags, ctypes.byref(o), tp, capacity,
                             ctypes.addressof(total), ctypes.byref(st) if with_stats else None))
     out = (int(total.value), tri[:min(total.value, capacity)])
+    return out + (stats_dict(st),) if with_stats else out
+
+
+def masked_spgemm(rowptr, col, *, id_order=False, clean=False, sorted_rows=False, validate=False,
+                  prune=False, stream=None, with_stats=False, **opts):
+    """NEXT-4 (Alg. 3 masked): (off_u, col_u, C, T) -- the upper triangle of A in the vertex
+    order (degree, id) or plain ids (id_order=True, Fig. mm), in input ids with rows ascending,
+    C = A o (L U) at each of its entries, and T = sum(C over both triangles) / 2 [+ stats]."""
+    lib = _load()
+    n, M, rp, cp, on_dev, keep = _arrays(rowptr, col)
+    flags = _flags(clean, sorted_rows, False, validate, prune, id_order, on_dev)
+    o = _options(stream=stream, on_device=on_dev, **opts)
+    nnz = ctypes.c_uint64(0)
+    total = ctypes.c_uint64(0)
+    st = Stats()
+    if on_dev:
+        import torch
+        dev = keep[0].device
+        off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        colp = torch.empty(max(M, 1), dtype=torch.int32, device=dev)
+        c = torch.empty(max(M, 1), dtype=torch.int32, device=dev)
+        ptrs = (off.data_ptr(), colp.data_ptr(), c.data_ptr())
+    else:
+        off = np.zeros(n + 1, dtype=np.uint64)
+        colp = np.zeros(max(M, 1), dtype=np.uint32)
+        c = np.zeros(max(M, 1), dtype=np.uint32)
+        ptrs = (off.ctypes.data, colp.ctypes.data, c.ctypes.data)
+    _check(lib.tc_masked_spgemm(n, M, rp, cp, flags, ctypes.byref(o), *ptrs, ctypes.addressof(nnz),
+                                ctypes.addressof(total), ctypes.byref(st) if with_stats else None))
+    out = (off, colp[:nnz.value], c[:nnz.value], int(total.value))
     return out + (stats_dict(st),) if with_stats else out
 
 

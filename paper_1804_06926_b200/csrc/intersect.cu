@@ -24,7 +24,10 @@
 //   kCmEdge    add 1 to the support of its three edges (u,v), (u,w), (v,w), each an
 //              entry of col+ (NEXT-3 edge support, the k-truss input);
 //   kCmList    write the triangle as three ascending input ids (NEXT-3 enumeration,
-//              "the listings of all the triangles for free").
+//              "the listings of all the triangles for free");
+//   kCmTop     add 1 to its TOP edge only, the edge between its two highest-ranked
+//              vertices: C = A o (L U) at A's nonzeros (NEXT-4, Alg. 3),
+//              since (L U)_ij counts the common neighbours k ranked below i and j.
 // In the HASH kernels the owner-side credit (t(w), or the support of (owner, w)) is
 // counted in shared memory per owner element and flushed once per task.
 #include "block_scan.cuh"
@@ -121,6 +124,7 @@ __global__ void __launch_bounds__(kIxThreads)
                 atomicAdd(&cr.sup[pi], 1u);
                 atomicAdd(&cr.sup[pj], 1u);
             }
+            if (CM == kCmTop) atomicAdd(&cr.sup[pj], 1u);   // (v, w): u < v < w
         });
         credit_edge<CM>(cr, uv.x, uv.y, c);
         if (CM == kCmEdge && c) atomicAdd(&cr.sup[edge_index(off, col, uv.x, uv.y)], c);
@@ -186,6 +190,7 @@ __global__ void __launch_bounds__(kIxThreads)
                 atomicAdd(&cr.sup[ab + i], 1u);
                 atomicAdd(&cr.sup[bb + j], 1u);
             }
+            if (CM == kCmTop) atomicAdd(&cr.sup[bb + j], 1u);   // B = N+(v)
         });
         if (CM == kCmVertex || CM == kCmEdge) {
             uint32_t ce = __reduce_add_sync(0xffffffffu, c);
@@ -218,6 +223,7 @@ __global__ void __launch_bounds__(kIxThreads)
         const uint32_t *B = col + off[uv.y];
         uint32_t na = (uint32_t)(off[uv.x + 1] - off[uv.x]);
         uint32_t nb = (uint32_t)(off[uv.y + 1] - off[uv.y]);
+        const bool swapped = na > nb;   // then A = N+(v)
         if (na > nb) {  // A := the shorter list
             const uint32_t *t = A; A = B; B = t;
             uint32_t tn = na; na = nb; nb = tn;
@@ -243,6 +249,7 @@ __global__ void __launch_bounds__(kIxThreads)
                 atomicAdd(&cr.sup[A - col + k], 1u);
                 atomicAdd(&cr.sup[B - col + l], 1u);
             }
+            if (CM == kCmTop) atomicAdd(&cr.sup[swapped ? A - col + k : B - col + l], 1u);
         });
         if (CM == kCmVertex || CM == kCmEdge) {
             uint32_t ce = __reduce_add_sync(0xffffffffu, c);
@@ -398,7 +405,7 @@ struct HashProbe {  // bucket hash of the owner's N+ (any id range)
     __device__ __forceinline__ void credit(uint32_t w, const Credit &cr) const {
         if (!cnt) {
             if (CM == kCmVertex) atomicAdd((unsigned long long *)&cr.pv[w], 1ull);
-            if (CM == kCmEdge) atomicAdd(&cr.sup[xb + list_pos(xl, xlen, w)], 1u);
+            if (CM == kCmEdge || CM == kCmTop) atomicAdd(&cr.sup[xb + list_pos(xl, xlen, w)], 1u);
             return;
         }
         atomicAdd(&cnt[table_find(tab, bits, w)], 1u);
@@ -441,7 +448,7 @@ struct BitProbe {   // bitmap over the rank-id range [base, base + span) of the 
     __device__ __forceinline__ void credit(uint32_t w, const Credit &cr) const {
         if (!cnt) {
             if (CM == kCmVertex) atomicAdd((unsigned long long *)&cr.pv[w], 1ull);
-            if (CM == kCmEdge) atomicAdd(&cr.sup[xb + list_pos(xl, xlen, w)], 1u);
+            if (CM == kCmEdge || CM == kCmTop) atomicAdd(&cr.sup[xb + list_pos(xl, xlen, w)], 1u);
             return;
         }
         uint32_t o = w - base, word = lds32(bm + 4 * (o >> 5));
@@ -550,6 +557,17 @@ __device__ __forceinline__ uint64_t probe_quads(const Probe &contains,
                     }
                 atomicAdd(&cr.sup[ly[k]], (uint32_t)__popc(hm));
             }
+            if (CM == kCmTop && hm) {
+                // in-part entry (ly = 0): list N+(u) after owner x, triangle u < x < w, top
+                // edge (x, w) = the owner's element; out-part entry (ly = 1): owner u, list
+                // N+(x), top edge (x, w) = the probed slot
+#pragma unroll
+                for (int c = 0; c < kSlot; c++)
+                    if ((hm >> c) & 1u) {
+                        if (ly[k]) atomicAdd(&cr.sup[e0[k] + c], 1u);
+                        else contains.template credit<CM>(e[c], cr);
+                    }
+            }
             if (CM == kCmList) {         // warp-aggregated reservation of the output slots
                 const uint32_t nh = __popc(hm);
                 const uint32_t incl = warp_inclusive_scan<SumOp>(nh);
@@ -581,10 +599,10 @@ __device__ __forceinline__ void hash_desc(const HashParams &hp, uint64_t inb, ui
         lo = hp.ulo[inb + j];
         uint32_t u = hp.in_src[inb + j];
         if (lo) hi = (uint32_t)hp.off[u + 1];
-        y = CM == kCmEdge ? lo - 1 : u;
+        y = CM == kCmEdge ? lo - 1 : (CM == kCmTop ? 0u : u);
     } else if (j - indeg < ocnt) {
         uint2 r = hp.orange[ob + (j - indeg)];
-        y = hp.ovid[ob + (j - indeg)];
+        y = CM == kCmTop ? 1u : hp.ovid[ob + (j - indeg)];
         lo = r.x;
         hi = r.y;
     }
@@ -597,7 +615,7 @@ __global__ void __launch_bounds__(kIxThreads, TC_HASH_WARP_MINBLOCKS)
                 uint64_t *__restrict__ total, Credit cr) {
     constexpr uint32_t L = kWarpTaskLists;
     constexpr bool PV = CM != kCmNone;                        // descriptors carry vid
-    constexpr bool kCnt = CM == kCmVertex || CM == kCmEdge;   // owner-side hit counters
+    constexpr bool kCnt = CM == kCmVertex || CM == kCmEdge || CM == kCmTop;  // owner-side hits
     __shared__ __align__(16) uint32_t s_tab[kHashWarps][kWarpTableSlots];
     __shared__ uint32_t s_qb[kHashWarps][L];
     __shared__ uint2 s_rng[kHashWarps][L];
@@ -653,7 +671,7 @@ __global__ void __launch_bounds__(kIxThreads, TC_HASH_WARP_MINBLOCKS)
                 uint32_t c = s_cnt[wib][s];
                 if (!c) continue;
                 if (CM == kCmVertex) atomicAdd((unsigned long long *)&cr.pv[tab[s]], (unsigned long long)c);
-                if (CM == kCmEdge) atomicAdd(&cr.sup[xb + list_pos(col + xb, dx, tab[s])], c);
+                if (CM == kCmEdge || CM == kCmTop) atomicAdd(&cr.sup[xb + list_pos(col + xb, dx, tab[s])], c);
             }
         }
         if (CM == kCmVertex) {
@@ -687,7 +705,7 @@ __global__ void __launch_bounds__(kIxThreads, CM != kCmNone ? 4 : TC_HASH_CTA_MI
     __shared__ uint64_t s_scan[kHashWarps];
     // per-vertex bitmap owners: hit counters per element of N+(x) (owners with
     // d+ <= kPvCounters; others credit w with global atomics) + word prefix popcounts
-    constexpr bool kCnt = CM == kCmVertex || CM == kCmEdge;  // bitmap: per set bit; hash: per slot
+    constexpr bool kCnt = CM == kCmVertex || CM == kCmEdge || CM == kCmTop;  // per set bit / slot
     static_assert(kPvCounters == kHashSlots, "hash owners count hits per table slot");
     __shared__ uint32_t s_cnt[kCnt ? kPvCounters : 1];
     __shared__ uint16_t s_wpre[kCnt && kBitmap ? kSmemWords + 1 : 1];
@@ -756,7 +774,7 @@ __global__ void __launch_bounds__(kIxThreads, CM != kCmNone ? 4 : TC_HASH_CTA_MI
                     uint32_t c = s_cnt[k];
                     if (!c) continue;
                     if (CM == kCmVertex) atomicAdd((unsigned long long *)&cr.pv[col[xb + k]], (unsigned long long)c);
-                    if (CM == kCmEdge) atomicAdd(&cr.sup[xb + k], c);
+                    if (CM == kCmEdge || CM == kCmTop) atomicAdd(&cr.sup[xb + k], c);
                 }
                 __syncthreads();
             }
@@ -781,7 +799,7 @@ __global__ void __launch_bounds__(kIxThreads, CM != kCmNone ? 4 : TC_HASH_CTA_MI
                         if (!c) continue;
                         if (CM == kCmVertex)
                             atomicAdd((unsigned long long *)&cr.pv[s_tab[s]], (unsigned long long)c);
-                        if (CM == kCmEdge)   // the chunk is col+[xb + c0, + clen), ascending
+                        if (CM == kCmEdge || CM == kCmTop)   // chunk col+[xb + c0, + clen), ascending
                             atomicAdd(&cr.sup[xb + c0 + list_pos(col + xb + c0, clen, s_tab[s])], c);
                     }
                     __syncthreads();
@@ -828,6 +846,7 @@ void intersect_all(Ctx &ctx, const Oriented &g, const Bins &bins, uint64_t *tota
         case kCmVertex: launch_all<kCmVertex>(ctx, g, bins, total_dev, cr); break;
         case kCmEdge: launch_all<kCmEdge>(ctx, g, bins, total_dev, cr); break;
         case kCmList: launch_all<kCmList>(ctx, g, bins, total_dev, cr); break;
+        case kCmTop: launch_all<kCmTop>(ctx, g, bins, total_dev, cr); break;
         default: launch_all<kCmNone>(ctx, g, bins, total_dev, cr); break;
     }
 }

@@ -155,6 +155,23 @@ __global__ void k_newid(const uint32_t *__restrict__ order, uint64_t n, uint32_t
         newid[order[i]] = (uint32_t)i;
 }
 
+// TC_ID_ORDER (Alg. 3 without its row permutation, the order of Fig. mm): the rank
+// key is [d(v) > 0], so every non-isolated vertex ranks by id alone (isolated and
+// pruned-away vertices, key 0, keep failing the rank filter).
+__global__ void k_id_order_key(const uint32_t *__restrict__ deg, uint64_t n, uint32_t *__restrict__ key) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        key[i] = deg[i] ? 1u : 0u;
+}
+
+static const uint32_t *rank_key(Ctx &ctx, uint64_t n, const uint32_t *deg, bool id_order) {
+    if (!id_order) return deg;
+    uint32_t *key = ctx.alloc<uint32_t>(n);
+    k_id_order_key<<<ctx.persistent_grid(8), 256, 0, ctx.stream>>>(deg, n, key);
+    TC_LAUNCHED(ctx);
+    return key;
+}
+
 // order[i] = vertex with the i-th smallest (d, id); newid = inverse.  `deg` is kept.
 static void rank_permutation(Ctx &ctx, uint64_t n, const uint32_t *deg, Oriented &out) {
     int b = id_bits(n);
@@ -235,7 +252,7 @@ static void pairs_to_csr(Ctx &ctx, uint64_t n, uint64_t cap, uint32_t *okey, uin
 
 void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
                   bool need_sorted, uint32_t segsort_block_max, Oriented &out, Timer *tm,
-                  PruneInfo &prune) {
+                  PruneInfo &prune, bool id_order) {
     int b = id_bits(n);
     uint32_t tiles = (uint32_t)((M + kTileItems - 1) / kTileItems);
     if (tm) tm->begin(kClean);
@@ -269,7 +286,7 @@ void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, cons
         prune_pairs(ctx, n, b, prune.rounds_wanted, E, m_dev, deg, M, prune);
         if (tm) tm->end(kPrune);
     }
-    rank_permutation(ctx, n, deg, out);
+    rank_permutation(ctx, n, rank_key(ctx, n, deg, id_order), out);
     uint32_t *okey = ctx.alloc<uint32_t>(M), *oval = ctx.alloc<uint32_t>(M);
     k_orient_pairs<<<grid, 256, 0, ctx.stream>>>(E, m_dev, b, out.newid, okey, oval, dplus);
     TC_LAUNCHED(ctx);
@@ -341,7 +358,7 @@ __global__ void __launch_bounds__(kTileThreads)
 
 void orient_clean(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
                   bool need_sorted, uint32_t segsort_block_max, Oriented &out, Timer *tm,
-                  PruneInfo &prune) {
+                  PruneInfo &prune, bool id_order) {
     uint32_t tiles = (uint32_t)((M + kTileItems - 1) / kTileItems);
     int grid = ctx.persistent_grid(8);
     if (tm) tm->begin(kOrient);
@@ -354,10 +371,11 @@ void orient_clean(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, cons
         prune_csr(ctx, n, M, rowptr, col, prune.rounds_wanted, deg, prune);
         if (tm) tm->end(kPrune);
     }
-    rank_permutation(ctx, n, deg, out);
+    const uint32_t *key = rank_key(ctx, n, deg, id_order);
+    rank_permutation(ctx, n, key, out);
     uint32_t *counts = ctx.alloc<uint32_t>(tiles);
     uint64_t *offs = ctx.alloc<uint64_t>(tiles + 1);
-    k_orient_count<<<tiles, kTileThreads, 0, ctx.stream>>>(rowptr, col, n, M, deg, counts);
+    k_orient_count<<<tiles, kTileThreads, 0, ctx.stream>>>(rowptr, col, n, M, key, counts);
     TC_LAUNCHED(ctx);
     scan_exclusive(ctx, counts, offs, tiles);
     uint64_t cap = M / 2 + 1;
@@ -365,7 +383,7 @@ void orient_clean(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, cons
     uint32_t *dplus = ctx.alloc<uint32_t>(n + 1), *dminus = ctx.alloc<uint32_t>(n + 1);
     TC_CUDA(cudaMemsetAsync(dplus, 0, (n + 1) * sizeof(uint32_t), ctx.stream));
     TC_CUDA(cudaMemsetAsync(dminus, 0, (n + 1) * sizeof(uint32_t), ctx.stream));
-    k_orient_emit<<<tiles, kTileThreads, 0, ctx.stream>>>(rowptr, col, n, M, deg, out.newid, offs,
+    k_orient_emit<<<tiles, kTileThreads, 0, ctx.stream>>>(rowptr, col, n, M, key, out.newid, offs,
                                                           okey, oval, dplus);
     TC_LAUNCHED(ctx);
     k_dminus<<<grid, 256, 0, ctx.stream>>>(deg, out.newid, dplus, n, dminus);

@@ -44,7 +44,7 @@ static uint64_t *pinned_scratch() {
     return p;
 }
 
-enum Mode { kCount, kShard, kOrientOnly, kClustering, kSupport, kEnumerate };
+enum Mode { kCount, kShard, kOrientOnly, kClustering, kSupport, kEnumerate, kMasked };
 
 struct Call {
     uint64_t n, M;
@@ -85,16 +85,20 @@ static tc_status check_args(const Call &c) {
             return set_error("need 0 <= rank < world"), TC_EINVAL;
         if (c.flags & TC_HOST_PTRS) return set_error("tc_count_shard takes device pointers"), TC_EINVAL;
     }
-    if ((c.mode == kOrientOnly || c.mode == kSupport) &&
-        (!c.off_plus || (!c.col_plus && c.M > 0) || !c.m_plus))
-        return set_error("tc_orient / tc_edge_support output pointer is NULL"), TC_EINVAL;
-    if (c.mode == kSupport && !c.support && c.M > 0)
-        return set_error("tc_edge_support: support is NULL"), TC_EINVAL;
+    const bool csr_out = c.mode == kOrientOnly || c.mode == kSupport || c.mode == kMasked;
+    if (csr_out && (!c.off_plus || (!c.col_plus && c.M > 0) || !c.m_plus))
+        return set_error("tc_orient / tc_edge_support / tc_masked_spgemm output pointer is NULL"),
+               TC_EINVAL;
+    if ((c.mode == kSupport || c.mode == kMasked) && !c.support && c.M > 0)
+        return set_error("tc_edge_support / tc_masked_spgemm: value output is NULL"), TC_EINVAL;
+    if (c.mode == kMasked && !c.total_host)
+        return set_error("tc_masked_spgemm: total is NULL"), TC_EINVAL;
     if (c.mode == kEnumerate && (!c.total_host || (c.capacity && !c.triangles)))
         return set_error("tc_enumerate: total is NULL, or triangles is NULL with capacity > 0"),
                TC_EINVAL;
-    if ((c.mode == kSupport || c.mode == kEnumerate) && (c.flags & TC_PER_VERTEX))
-        return set_error("TC_PER_VERTEX is not an option of tc_edge_support / tc_enumerate"),
+    if ((c.mode == kSupport || c.mode == kEnumerate || c.mode == kMasked) && (c.flags & TC_PER_VERTEX))
+        return set_error("TC_PER_VERTEX is not an option of tc_edge_support / tc_enumerate / "
+                         "tc_masked_spgemm"),
                TC_EINVAL;
     if ((c.flags & TC_PER_VERTEX) && c.mode != kOrientOnly && !c.per_vertex)
         return set_error("TC_PER_VERTEX needs per_vertex"), TC_EINVAL;
@@ -194,10 +198,10 @@ static void run(Call &c) {
         Oriented g;
         if (c.flags & TC_CLEAN)
             orient_clean(ctx, c.n, c.M, rowptr, col, need_sorted, c.opt.segsort_block_max, g, tm,
-                         prune);
+                         prune, c.flags & TC_ID_ORDER);
         else
             orient_dirty(ctx, c.n, c.M, rowptr, col, need_sorted, c.opt.segsort_block_max, g, tm,
-                         prune);
+                         prune, c.flags & TC_ID_ORDER);
         if (c.stats && prune.m_before)
             TC_CUDA(cudaMemcpyAsync(pin + 24, prune.m_before, sizeof(uint64_t),
                                     cudaMemcpyDeviceToHost, ctx.stream));
@@ -248,10 +252,10 @@ static void run(Call &c) {
         if (pv) {
             cr.mode = kCmVertex;
             cr.pv = pv_new;
-        } else if (c.mode == kSupport) {
+        } else if (c.mode == kSupport || c.mode == kMasked) {
             sup = ctx.alloc<uint32_t>(g.m_cap);
             TC_CUDA(cudaMemsetAsync(sup, 0, g.m_cap * sizeof(uint32_t), ctx.stream));
-            cr.mode = kCmEdge;
+            cr.mode = c.mode == kSupport ? kCmEdge : kCmTop;
             cr.sup = sup;
         } else if (c.mode == kEnumerate) {
             cr.mode = kCmList;
@@ -264,7 +268,7 @@ static void run(Call &c) {
         if (tm) tm->begin(kIntersect);
         intersect_all(ctx, g, bins, total_dev, cr);
         if (tm) tm->end(kIntersect);
-        if (c.mode == kSupport) {   // N+ in the caller's ids with each edge's support
+        if (c.mode == kSupport || c.mode == kMasked) {   // N+ in the caller's ids + values
             uint64_t *off_o = ctx.alloc<uint64_t>(c.n + 1);
             uint32_t *col_o = ctx.alloc<uint32_t>(g.m_cap), *sup_o = ctx.alloc<uint32_t>(g.m_cap);
             to_original(ctx, g, off_o, col_o, sup, sup_o);
@@ -298,17 +302,19 @@ static void run(Call &c) {
             TC_CUDA(cudaMemcpyAsync(pin + 16, g.m_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost,
                                     ctx.stream));
         }
-    } else if (c.mode == kOrientOnly || c.mode == kSupport) {
+    } else if (c.mode == kOrientOnly || c.mode == kSupport || c.mode == kMasked) {
         cudaMemcpyKind kind = host ? cudaMemcpyHostToHost : cudaMemcpyHostToDevice;
         std::vector<uint64_t> zeros(c.n + 1, 0);
         TC_CUDA(cudaMemcpyAsync(c.off_plus, zeros.data(), (c.n + 1) * sizeof(uint64_t), kind,
                                 ctx.stream));
         TC_CUDA(cudaStreamSynchronize(ctx.stream));
         *c.m_plus = 0;
+        if (c.mode == kMasked) *c.total_host = 0;
         return;
     }
 
-    if (c.mode == kCount || c.mode == kClustering || c.mode == kEnumerate || c.mode == kSupport) {
+    if (c.mode == kCount || c.mode == kClustering || c.mode == kEnumerate || c.mode == kSupport ||
+        c.mode == kMasked) {
         TC_CUDA(cudaMemcpyAsync(pin + 20, total_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost,
                                 ctx.stream));
         st.d2h_bytes += sizeof(uint64_t);
@@ -332,7 +338,7 @@ static void run(Call &c) {
     ctx.release();
     if (c.mode != kShard || c.stats) TC_CUDA(cudaStreamSynchronize(ctx.stream));
     TC_CUDA(cudaGetLastError());
-    if (c.mode == kCount || c.mode == kEnumerate) *c.total_host = pin[20];
+    if (c.mode == kCount || c.mode == kEnumerate || c.mode == kMasked) *c.total_host = pin[20];
     if (c.mode == kClustering && c.csum) {
         tc_clustering_summary &r = *c.csum;
         r.triangles = pin[20];
@@ -503,6 +509,21 @@ tc_status tc_enumerate(uint64_t n, uint64_t m, const uint64_t *row_offsets,
     c.mode = kEnumerate;
     c.triangles = triangles;
     c.capacity = capacity;
+    c.total_host = total;
+    c.stats = stats;
+    return guarded(c);
+}
+
+tc_status tc_masked_spgemm(uint64_t n, uint64_t m, const uint64_t *row_offsets,
+                           const uint32_t *col_indices, uint32_t flags, const tc_options *opt,
+                           uint64_t *off_plus, uint32_t *col_plus, uint32_t *c_values,
+                           uint64_t *nnz_u, uint64_t *total, tc_stats *stats) {
+    Call c{n, m, row_offsets, col_indices, flags, resolve(opt)};
+    c.mode = kMasked;
+    c.off_plus = off_plus;
+    c.col_plus = col_plus;
+    c.support = c_values;
+    c.m_plus = nnz_u;
     c.total_host = total;
     c.stats = stats;
     return guarded(c);

@@ -247,11 +247,11 @@ void prune_csr(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const u
 // a1 (dirty input) + a2 + a3: raw CSR -> oriented relabelled CSR (+ a4 if need_sorted).
 void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
                   bool need_sorted, uint32_t segsort_block_max, Oriented &out, Timer *tm,
-                  PruneInfo &prune);
+                  PruneInfo &prune, bool id_order);
 // a2 + a3 for clean symmetric input (+ a4 if need_sorted).
 void orient_clean(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
                   bool need_sorted, uint32_t segsort_block_max, Oriented &out, Timer *tm,
-                  PruneInfo &prune);
+                  PruneInfo &prune, bool id_order);
 // The oriented CSR in INPUT ids with ascending rows (tc_orient output).
 // With pay_in (m entries in CSR order, e.g. edge supports) also pay_out[k] = the
 // payload of the edge written to col_out[k].
@@ -345,11 +345,11 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins);
 void work_prefix(Ctx &ctx, const Oriented &g, uint64_t *prefix /* n+1 */);
 
 // What each triangle found in a6 credits besides the total (intersect.cu header).
-enum CreditMode { kCmNone = 0, kCmVertex = 1, kCmEdge = 2, kCmList = 3 };
+enum CreditMode { kCmNone = 0, kCmVertex = 1, kCmEdge = 2, kCmList = 3, kCmTop = 4 };
 struct Credit {
     int mode = kCmNone;
     uint64_t *pv = nullptr;           // kCmVertex: t(v), rank ids, n entries
-    uint32_t *sup = nullptr;          // kCmEdge: support per entry of col+ (m entries)
+    uint32_t *sup = nullptr;          // kCmEdge / kCmTop: per entry of col+ (m entries)
     uint32_t *tri = nullptr;          // kCmList: cap triples of ascending input ids
     uint64_t *cursor = nullptr;       // kCmList: triples found so far (device counter)
     uint64_t cap = 0;

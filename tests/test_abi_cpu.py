@@ -28,7 +28,8 @@ def declared_functions():
 def test_exports_every_declared_symbol(lib):
     names = declared_functions()
     assert set(names) >= {"tc_count", "tc_count_ex", "tc_count_shard", "tc_orient",
-                          "tc_clustering", "tc_edge_support", "tc_enumerate", "tc_last_error",
+                          "tc_clustering", "tc_edge_support", "tc_enumerate", "tc_masked_spgemm",
+                          "tc_last_error",
                           "tc_default_options", "tc_version"}
     for name in names:
         assert hasattr(lib, name), name
@@ -80,6 +81,11 @@ def test_next3_argument_errors(lib):
     assert lib.tc_enumerate(1, 0, rp.ctypes.data, None, tc.TC_HOST_PTRS, None, None, 5,
                             out.ctypes.data, None) == EINVAL
     assert b"capacity" in lib.tc_last_error()
+    # masked SpGEMM: total and the value output are required
+    assert lib.tc_masked_spgemm(1, 0, rp.ctypes.data, None, tc.TC_HOST_PTRS | tc.TC_ID_ORDER, None,
+                                out.ctypes.data, out.ctypes.data, out.ctypes.data, out.ctypes.data,
+                                None, None) == EINVAL
+    assert b"total" in lib.tc_last_error()
 
 
 def test_argument_errors_before_device(lib):

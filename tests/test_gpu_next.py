@@ -266,3 +266,60 @@ def test_enumerate_rmat21_full_properties():
             nx = ccol[crow[x]:crow[x + 1]]
             i = np.searchsorted(nx, y)
             assert i < len(nx) and nx[i] == y, (a, b, c)
+
+
+# ------------------------------------------------------------------ NEXT-4: masked SpGEMM
+@pytest.mark.parametrize("name", list(SUPPORT_GRAPHS))
+@pytest.mark.parametrize("id_order", [False, True])
+def test_masked_spgemm_parity(name, id_order):
+    g = SUPPORT_GRAPHS[name]()
+    crow, ccol = O.clean(g.n, g.rowptr, g.col)
+    want_off, want_col, want_c, want_T = O.masked_spgemm(g.n, crow, ccol, id_order=id_order)
+    for v in VARIANTS:
+        rp, cl = on_dev(g.rowptr, g.col)
+        off, colp, c, T = tc.masked_spgemm(rp, cl, id_order=id_order, force_variant=v)
+        assert T == want_T, (name, id_order, v)
+        assert (np_u(off, np.uint64) == want_off).all() and (np_u(colp, np.uint32) == want_col).all()
+        assert (np_u(c, np.uint32) == want_c).all(), (name, id_order, v)
+
+
+def test_masked_spgemm_fig_mm_printed(golden):
+    """The GPU reproduces the paper's printed C in the figure's id order."""
+    fx = golden("fig_mm.txt")
+    C = np.array(fx["C"], dtype=np.int64)
+    g = G.fig_mm()
+    off, colp, c, T = tc.masked_spgemm(g.rowptr, g.col, id_order=True)   # host pointers
+    assert T == 3
+    got = np.zeros((7, 7), dtype=np.int64)
+    src = np.repeat(np.arange(7), np.diff(off.astype(np.int64)))
+    got[src, colp.astype(np.int64)] = c
+    assert (got + got.T == C).all()
+
+
+def test_id_order_counts_and_orientation():
+    g = G.rmat(13, 16, seed=9)
+    T, t = O.count(g.n, g.rowptr, g.col, per_vertex=True)
+    crow, ccol = O.clean(g.n, g.rowptr, g.col)
+    want_off, want_col = O.orient_order(g.n, crow, ccol, id_order=True)
+    for clean in (False, True):
+        rp, cl = on_dev(crow, ccol) if clean else on_dev(g.rowptr, g.col)
+        off, colp = tc.orient(rp, cl, clean=clean, sorted_rows=clean, id_order=True)
+        assert (np_u(off, np.uint64) == want_off).all() and (np_u(colp, np.uint32) == want_col).all()
+        for v in VARIANTS:
+            got, pv = tc.count_ex(rp, cl, clean=clean, sorted_rows=clean, id_order=True,
+                                  per_vertex=True, force_variant=v)
+            assert got == T and (np_u(pv, np.uint64) == t).all(), (clean, v)
+
+
+def test_masked_spgemm_prune_host_and_rmat16():
+    g = G.rmat(16, 16, seed=2)
+    crow, ccol = O.clean(g.n, g.rowptr, g.col)
+    for id_order in (False, True):
+        want = O.masked_spgemm(g.n, crow, ccol, id_order=id_order)
+        off, colp, c, T = tc.masked_spgemm(g.rowptr, g.col, id_order=id_order)
+        assert T == want[3] and (off == want[0]).all() and (colp == want[1]).all() and (c == want[2]).all()
+    prow, pcol, _ = O.prune(g.n, crow, ccol, 0)
+    want = O.masked_spgemm(g.n, prow, pcol, id_order=False)
+    rp, cl = on_dev(crow, ccol)
+    off, colp, c, T = tc.masked_spgemm(rp, cl, clean=True, sorted_rows=True, prune=True)
+    assert T == want[3] and (np_u(colp, np.uint32) == want[1]).all() and (np_u(c, np.uint32) == want[2]).all()
