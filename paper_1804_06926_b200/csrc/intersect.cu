@@ -487,16 +487,43 @@ __device__ __forceinline__ uint32_t quad_count(uint32_t lo, uint32_t hi) {
 // uint4 load and four probes per lane per window.  In each 32-quad window lane t
 // finds its list from a bitmap of the list starts inside the window (reduce-or +
 // popc): no per-item search.  Returns the number of hits.
+// kCmList: the hits are staged per warp in shared memory as (list vertex, w) input-id
+// pairs (kStage of them; the owner is common to the task) and written out as one
+// contiguous run of ascending triples per flush, with ONE global slot reservation.
+constexpr uint32_t kStage = 256;   // >= the hits of one window (32 lanes x kSlot)
+
+__device__ __forceinline__ void flush_stage(const uint2 *stage, uint32_t staged, uint32_t b,
+                                            const Credit &cr) {
+    const uint32_t lane = threadIdx.x & 31;
+    __syncwarp();
+    uint64_t base = 0;
+    if (lane == 0) base = atomicAdd((unsigned long long *)cr.cursor, (unsigned long long)staged);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (uint32_t i = lane; i < staged; i += 32) {
+        if (base + i >= cr.cap) break;
+        const uint2 aw = stage[i];
+        const uint32_t lo3 = min(aw.x, min(b, aw.y)), hi3 = max(aw.x, max(b, aw.y));
+        uint32_t *t = cr.tri + 3 * (base + i);
+        t[0] = lo3;
+        t[1] = aw.x ^ b ^ aw.y ^ lo3 ^ hi3;
+        t[2] = hi3;
+    }
+    __syncwarp();
+}
+
 template <int CM, class Probe>
 __device__ __forceinline__ uint64_t probe_quads(const Probe &contains,
                                                 const QuadDesc &d, uint32_t nl, uint32_t ib,
                                                 uint32_t ie,
                                                 const uint32_t *__restrict__ col,
-                                                uint32_t owner, const Credit &cr) {
+                                                uint32_t owner, const Credit &cr,
+                                                uint2 *stage = nullptr) {
     constexpr bool kVid = CM != kCmNone;
+    uint32_t staged = 0, ord_owner = 0;
+    if (CM == kCmList) ord_owner = cr.order[owner];
     const int lane = threadIdx.x & 31;
     uint32_t hits = 0;
-    if (ib >= ie) return 0;
+    if (ib >= ie) return 0;   // warp-uniform: nothing staged
     uint32_t lo = 0, hi = nl;  // i0 = the list containing quad ib
     while (hi - lo > 1) {
         uint32_t mid = (lo + hi) >> 1;
@@ -568,20 +595,26 @@ __device__ __forceinline__ uint64_t probe_quads(const Probe &contains,
                         else contains.template credit<CM>(e[c], cr);
                     }
             }
-            if (CM == kCmList) {         // warp-aggregated reservation of the output slots
+            if (CM == kCmList) {         // stage as ascending input ids, flush when full
                 const uint32_t nh = __popc(hm);
                 const uint32_t incl = warp_inclusive_scan<SumOp>(nh);
                 const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-                uint64_t sb = 0;
-                if (lane == 0 && tot)
-                    sb = atomicAdd((unsigned long long *)cr.cursor, (unsigned long long)tot);
-                uint64_t slot = __shfl_sync(0xffffffffu, sb, 0) + incl - nh;
+                if (staged + tot > kStage) {
+                    flush_stage(stage, staged, ord_owner, cr);
+                    staged = 0;
+                }
+                if (hm) {
+                    uint32_t pos = staged + incl - nh;
+                    const uint32_t a = cr.order[ly[k]];
 #pragma unroll
-                for (int c = 0; c < kSlot; c++)
-                    if ((hm >> c) & 1u) put_triangle(cr, slot++, ly[k], owner, e[c]);
+                    for (int c = 0; c < kSlot; c++)
+                        if ((hm >> c) & 1u) stage[pos++] = make_uint2(a, cr.order[e[c]]);
+                }
+                staged += tot;
             }
         }
     }
+    if (CM == kCmList && staged) flush_stage(stage, staged, ord_owner, cr);
     return hits;
 }
 
@@ -622,6 +655,7 @@ __global__ void __launch_bounds__(kIxThreads, TC_HASH_WARP_MINBLOCKS)
     __shared__ uint32_t s_pre[kHashWarps][L + 1];
     __shared__ uint32_t s_vid[kHashWarps][PV ? L : 1];
     __shared__ uint32_t s_cnt[kCnt ? kHashWarps : 1][kCnt ? kWarpTableSlots : 1];  // owner hits per slot
+    __shared__ uint2 s_stage[CM == kCmList ? kHashWarps : 1][CM == kCmList ? kStage : 1];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const QuadDesc d{s_pre[wib], s_qb[wib], s_vid[wib], s_rng[wib]};
     uint64_t nt = *ntasks;
@@ -664,7 +698,7 @@ __global__ void __launch_bounds__(kIxThreads, TC_HASH_WARP_MINBLOCKS)
         __syncwarp();
         HashProbe hpb{opaque(smem_addr(tab)), x, bits};
         if (kCnt) hpb.cnt = s_cnt[wib];
-        uint64_t h = probe_quads<CM>(hpb, d, nl, 0, run, col, x, cr);
+        uint64_t h = probe_quads<CM>(hpb, d, nl, 0, run, col, x, cr, s_stage[CM == kCmList ? wib : 0]);
         if (kCnt) {
             __syncwarp();
             for (uint32_t s = lane; s < (1u << bits); s += 32) {
@@ -709,6 +743,8 @@ __global__ void __launch_bounds__(kIxThreads, CM != kCmNone ? 4 : TC_HASH_CTA_MI
     static_assert(kPvCounters == kHashSlots, "hash owners count hits per table slot");
     __shared__ uint32_t s_cnt[kCnt ? kPvCounters : 1];
     __shared__ uint16_t s_wpre[kCnt && kBitmap ? kSmemWords + 1 : 1];
+    __shared__ uint2 s_stage[CM == kCmList ? kHashWarps : 1][CM == kCmList ? kStage : 1];
+    uint2 *stage = s_stage[CM == kCmList ? (threadIdx.x >> 5) : 0];
     const int wib = threadIdx.x >> 5;
     const QuadDesc d{s_pre, s_qb, s_vid, s_rng};
     const uint32_t tab = opaque(smem_addr(s_tab));
@@ -767,7 +803,7 @@ __global__ void __launch_bounds__(kIxThreads, CM != kCmNone ? 4 : TC_HASH_CTA_MI
                 bp.cnt = s_cnt;
                 bp.wpre = s_wpre;
             }
-            h = probe_quads<CM>(bp, d, nl, ib, ie, col, x, cr);
+            h = probe_quads<CM>(bp, d, nl, ib, ie, col, x, cr, stage);
             __syncthreads();
             if (use_cnt) {   // the k-th set bit is the k-th element of the sorted N+(x)
                 for (uint32_t k = threadIdx.x; k < dx; k += blockDim.x) {
@@ -791,7 +827,7 @@ __global__ void __launch_bounds__(kIxThreads, CM != kCmNone ? 4 : TC_HASH_CTA_MI
                 __syncthreads();
                 HashProbe hpb{tab, x, bits};
                 if (kCnt) hpb.cnt = s_cnt;
-                h += probe_quads<CM>(hpb, d, nl, ib, ie, col, x, cr);
+                h += probe_quads<CM>(hpb, d, nl, ib, ie, col, x, cr, stage);
                 __syncthreads();
                 if (kCnt) {
                     for (uint32_t s = threadIdx.x; s < (1u << bits); s += blockDim.x) {
