@@ -71,9 +71,13 @@ __global__ void __launch_bounds__(kTileThreads)
     if (threadIdx.x == 0) counts[blockIdx.x] = (uint32_t)c;
 }
 
+// Also a2 (fused): the degrees of the cleaned graph.  A thread's unique keys are
+// consecutive in (min, max) order, so the min side takes one atomic per run of equal
+// mins, the max side one per key.
 __global__ void __launch_bounds__(kTileThreads)
     k_unique_scatter(const uint64_t *__restrict__ keys, uint64_t M,
-                     const uint64_t *__restrict__ offs, uint64_t *__restrict__ out) {
+                     const uint64_t *__restrict__ offs, uint64_t *__restrict__ out, int b,
+                     uint32_t *__restrict__ deg) {
     __shared__ uint32_t s_scan[kTileThreads / 32];
     uint64_t base = (uint64_t)blockIdx.x * kTileItems + (uint64_t)threadIdx.x * kItemsPerThread;
     uint32_t f[kItemsPerThread];
@@ -86,39 +90,27 @@ __global__ void __launch_bounds__(kTileThreads)
     }
     uint32_t pos = block_exclusive_scan<SumOp>(c, s_scan);
     uint64_t o = offs[blockIdx.x] + pos;
+    const uint64_t mask = (1ull << b) - 1;
+    uint32_t run_a = 0, run_n = 0;
 #pragma unroll
     for (int k = 0; k < kItemsPerThread; k++)
-        if (f[k]) out[o++] = keys[base + k];
-}
-
-// ------------------------------------------------------------------ a2/a3 from pairs
-// E is sorted by (min, max): consecutive keys share their min, so the min side is
-// counted per run of equal mins inside a warp (one atomic per run); the max side
-// (distinct within a run) takes one atomic per key.
-__global__ void k_deg_pairs(const uint64_t *__restrict__ E, const uint64_t *__restrict__ m_dev,
-                            int b, uint32_t *__restrict__ deg) {
-    uint64_t m = *m_dev, mask = (1ull << b) - 1;
-    const uint32_t lane = threadIdx.x & 31;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x; i0 < m; i0 += stride) {
-        uint64_t i = i0 + threadIdx.x;
-        bool ok = i < m;
-        uint64_t k = ok ? E[i] : 0;
-        uint32_t a = (uint32_t)(k >> b);
-        uint32_t prev = __shfl_up_sync(0xffffffffu, a, 1);
-        uint32_t valid = __ballot_sync(0xffffffffu, ok);   // a prefix of the warp
-        uint32_t heads = __ballot_sync(0xffffffffu, ok && (lane == 0 || prev != a));
-        if (ok) {
-            if ((heads >> lane) & 1u) {
-                uint32_t above = heads & ~((2u << lane) - 1u);
-                uint32_t end = above ? (uint32_t)(__ffs(above) - 1) : (uint32_t)__popc(valid);
-                atomicAdd(&deg[a], end - lane);
+        if (f[k]) {
+            const uint64_t key = keys[base + k];
+            out[o++] = key;
+            const uint32_t a = (uint32_t)(key >> b);
+            atomicAdd(&deg[key & mask], 1u);
+            if (run_n && a == run_a) {
+                run_n++;
+            } else {
+                if (run_n) atomicAdd(&deg[run_a], run_n);
+                run_a = a;
+                run_n = 1;
             }
-            atomicAdd(&deg[k & mask], 1u);
         }
-    }
+    if (run_n) atomicAdd(&deg[run_a], run_n);
 }
 
+// ------------------------------------------------------------------ a3 from pairs
 __global__ void k_orient_pairs(const uint64_t *__restrict__ E, const uint64_t *__restrict__ m_dev,
                                int b, const uint32_t *__restrict__ newid, uint32_t *__restrict__ okey,
                                uint32_t *__restrict__ oval, uint32_t *__restrict__ dplus) {
@@ -143,12 +135,6 @@ __global__ void k_orient_pairs(const uint64_t *__restrict__ E, const uint64_t *_
 }
 
 // ------------------------------------------------------------------ rank relabelling
-__global__ void k_iota(uint32_t *__restrict__ a, uint64_t n) {
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x)
-        a[i] = (uint32_t)i;
-}
-
 __global__ void k_newid(const uint32_t *__restrict__ order, uint64_t n, uint32_t *__restrict__ newid) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x)
@@ -176,14 +162,12 @@ static const uint32_t *rank_key(Ctx &ctx, uint64_t n, const uint32_t *deg, bool 
 static void rank_permutation(Ctx &ctx, uint64_t n, const uint32_t *deg, Oriented &out) {
     int b = id_bits(n);
     int grid = ctx.persistent_grid(8);
-    uint32_t *ids = ctx.alloc<uint32_t>(n);
     uint32_t *kA = ctx.alloc<uint32_t>(n), *kB = ctx.alloc<uint32_t>(n);
     uint32_t *vA = ctx.alloc<uint32_t>(n), *vB = ctx.alloc<uint32_t>(n);
-    k_iota<<<grid, 256, 0, ctx.stream>>>(ids, n);
-    TC_LAUNCHED(ctx);
-    // stable sort by degree (< n <= 2^b); ids enter ascending, so ties stay ordered by id
+    // stable sort by degree (< n <= 2^b) of the ids 0..n-1 (generated by the first pass,
+    // ascending), so ties stay ordered by id
     uint32_t *rk, *rv;
-    radix_sort_pairs_from(ctx, deg, ids, kA, kB, vA, vB, n, nullptr, b, &rk, &rv);
+    radix_sort_pairs_from(ctx, deg, nullptr, kA, kB, vA, vB, n, nullptr, b, &rk, &rv);
     out.order = rv;
     out.newid = ctx.alloc<uint32_t>(n);
     k_newid<<<grid, 256, 0, ctx.stream>>>(out.order, n, out.newid);
@@ -202,17 +186,10 @@ __global__ void k_dminus(const uint32_t *__restrict__ deg, const uint32_t *__res
 
 // Oriented pairs (okey = source, oval = target, new ids; m_dev of them) -> CSR with
 // ascending rows (a4) by an LSD radix sort on (source, target): a stable pass set
-// over the target gives the transposed CSR T (in-lists N-(x), sources ascending),
+// over the target gives the transposed CSR T (in-lists N-(x), in edge-list order),
 // then a stable pass set over the source of T's index p.  So pidx[e] = the in-list
 // slot of CSR edge e, col+[e] = T's target at pidx[e], and no edge ever has to be
 // searched for.  dplus / dminus already counted.
-__global__ void k_gather_col(const uint32_t *__restrict__ pidx, const uint32_t *__restrict__ t_tgt,
-                             const uint64_t *__restrict__ m_dev, uint32_t *__restrict__ col) {
-    uint64_t m = *m_dev;
-    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
-         e += (uint64_t)gridDim.x * blockDim.x)
-        col[e] = t_tgt[pidx[e]];
-}
 
 static void pairs_to_csr(Ctx &ctx, uint64_t n, uint64_t cap, uint32_t *okey, uint32_t *oval,
                          uint32_t *dplus, uint32_t *dminus, uint64_t *m_dev, Oriented &out,
@@ -224,16 +201,14 @@ static void pairs_to_csr(Ctx &ctx, uint64_t n, uint64_t cap, uint32_t *okey, uin
     bool a1 = radix_sort_pairs(ctx, oval, oval2, okey, okey2, cap, m_dev, b);
     uint32_t *t_tgt = a1 ? oval2 : oval, *t_src = a1 ? okey2 : okey;
     uint32_t *f_key = a1 ? oval : oval2, *f_val = a1 ? okey : okey2;   // free pair
-    // 2) stable by source of T's index p (values = p), reading T without modifying it
-    uint32_t *iota = ctx.alloc<uint32_t>(cap);
-    k_iota<<<grid, 256, 0, ctx.stream>>>(iota, cap);
-    TC_LAUNCHED(ctx);
+    // 2) stable by source of T's index p (values = p, generated by the first pass),
+    // reading T without modifying it; the last pass also gathers col+[e] = T.target[p]
     uint32_t *g_key = ctx.alloc<uint32_t>(cap), *g_val = ctx.alloc<uint32_t>(cap);
+    uint32_t *col = ctx.alloc<uint32_t>(cap);
     uint32_t *rk, *rv;
-    radix_sort_pairs_from(ctx, t_src, iota, f_key, g_key, f_val, g_val, cap, m_dev, b, &rk, &rv);
-    uint32_t *col = (rk == f_key) ? g_key : f_key;   // a free buffer of cap entries
-    k_gather_col<<<grid, 256, 0, ctx.stream>>>(rv, t_tgt, m_dev, col);
-    TC_LAUNCHED(ctx);
+    radix_sort_pairs_from(ctx, t_src, nullptr, f_key, g_key, f_val, g_val, cap, m_dev, b, &rk, &rv,
+                          t_tgt, col);
+    (void)grid;
     uint64_t *off = ctx.alloc<uint64_t>(n + 1), *in_off = ctx.alloc<uint64_t>(n + 1);
     scan_exclusive(ctx, dplus, off, n);
     scan_exclusive(ctx, dminus, in_off, n);
@@ -264,23 +239,21 @@ void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, cons
     uint64_t *sorted = alt ? keys_alt : keys, *E = alt ? keys : keys_alt;
     uint32_t *counts = ctx.alloc<uint32_t>(tiles);
     uint64_t *offs = ctx.alloc<uint64_t>(tiles + 1);
+    uint32_t *deg = ctx.alloc<uint32_t>(n);
+    TC_CUDA(cudaMemsetAsync(deg, 0, n * sizeof(uint32_t), ctx.stream));
     k_unique_count<<<tiles, kTileThreads, 0, ctx.stream>>>(sorted, M, counts);
     TC_LAUNCHED(ctx);
     scan_exclusive(ctx, counts, offs, tiles);
-    k_unique_scatter<<<tiles, kTileThreads, 0, ctx.stream>>>(sorted, M, offs, E);
+    k_unique_scatter<<<tiles, kTileThreads, 0, ctx.stream>>>(sorted, M, offs, E, b, deg);
     TC_LAUNCHED(ctx);
     uint64_t *m_dev = offs + tiles;
     if (tm) tm->end(kClean);
 
     if (tm) tm->begin(kOrient);
-    uint32_t *deg = ctx.alloc<uint32_t>(n);
     uint32_t *dplus = ctx.alloc<uint32_t>(n + 1), *dminus = ctx.alloc<uint32_t>(n + 1);
-    TC_CUDA(cudaMemsetAsync(deg, 0, n * sizeof(uint32_t), ctx.stream));
     TC_CUDA(cudaMemsetAsync(dplus, 0, (n + 1) * sizeof(uint32_t), ctx.stream));
     TC_CUDA(cudaMemsetAsync(dminus, 0, (n + 1) * sizeof(uint32_t), ctx.stream));
     int grid = ctx.persistent_grid(8);
-    k_deg_pairs<<<grid, 256, 0, ctx.stream>>>(E, m_dev, b, deg);
-    TC_LAUNCHED(ctx);
     if (prune.enabled) {
         if (tm) tm->begin(kPrune);
         prune_pairs(ctx, n, b, prune.rounds_wanted, E, m_dev, deg, M, prune);

@@ -20,6 +20,9 @@ namespace tc {
 #ifndef TC_RS_ROUNDS
 #define TC_RS_ROUNDS 8
 #endif
+#ifndef TC_RS_LB
+#define TC_RS_LB 8   // look-back batch: predecessor status words loaded together
+#endif
 #ifndef TC_RS_MINBLOCKS
 #define TC_RS_MINBLOCKS 2
 #endif
@@ -31,9 +34,15 @@ constexpr int kRsTile = kRsWarps * kRsWarpItems;       // 4096 items per tile
 constexpr int kDigits = 256;
 constexpr int kMaxPasses = 8;
 
-constexpr uint64_t kFlagAgg = 1ull << 62;   // status word: tile aggregate published
-constexpr uint64_t kFlagPre = 2ull << 62;   // status word: inclusive prefix published
-constexpr uint64_t kCountMask = (1ull << 62) - 1;
+// Look-back status words: 2 flag bits (aggregate / inclusive prefix published) over the
+// count.  32-bit words (half the look-back traffic) whenever every prefix fits in 30 bits.
+template <class S>
+struct Status {
+    static constexpr int kBits = 8 * sizeof(S);
+    static constexpr S kFlagAgg = (S)1 << (kBits - 2);
+    static constexpr S kFlagPre = (S)2 << (kBits - 2);
+    static constexpr S kCountMask = ((S)1 << (kBits - 2)) - 1;
+};
 
 __device__ __forceinline__ uint64_t valid_count(uint64_t cap, const uint64_t *count_dev) {
     if (!count_dev) return cap;
@@ -50,6 +59,14 @@ __device__ __forceinline__ void st_relaxed(uint64_t *p, uint64_t v) {
 __device__ __forceinline__ uint64_t ld_relaxed(const uint64_t *p) {
     uint64_t v;
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed(uint32_t *p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 
@@ -114,12 +131,15 @@ struct RsSmem {
     uint32_t tile;
 };
 
-template <class K, bool kVals>
+template <class K, bool kVals, class SW>
 __global__ void __launch_bounds__(kRsThreads, TC_RS_MINBLOCKS)
     k_rs_pass(const K *__restrict__ keys, const uint32_t *__restrict__ vals, K *__restrict__ keys_out,
               uint32_t *__restrict__ vals_out, uint64_t cap, const uint64_t *__restrict__ count_dev,
               int shift, const uint64_t *__restrict__ digit_off, uint32_t *__restrict__ ticket,
-              uint64_t *__restrict__ status) {
+              SW *__restrict__ status, const uint32_t *__restrict__ gather,
+              uint32_t *__restrict__ gather_out) {
+    constexpr SW kFlagAgg = Status<SW>::kFlagAgg, kFlagPre = Status<SW>::kFlagPre;
+    constexpr SW kCountMask = Status<SW>::kCountMask;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     RsSmem<K, kVals> &S = *reinterpret_cast<RsSmem<K, kVals> *>(smem_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -135,7 +155,9 @@ __global__ void __launch_bounds__(kRsThreads, TC_RS_MINBLOCKS)
     // ---- load (warp-blocked, coalesced rounds) and rank stably inside the tile
     const uint32_t wlocal = (uint32_t)warp * kRsWarpItems;
     const K *kp = keys + tile_base + wlocal + lane;
-    const uint32_t *vp = kVals ? vals + tile_base + wlocal + lane : nullptr;
+    // vals == nullptr: the values are the input positions (identity permutation)
+    const uint32_t *vp = kVals && vals ? vals + tile_base + wlocal + lane : nullptr;
+    const uint32_t vid0 = (uint32_t)(tile_base + wlocal + lane);
     K key[kRsRounds];
     uint32_t val[kRsRounds], rank[kRsRounds];
     const uint32_t lt = (1u << lane) - 1u;
@@ -144,7 +166,7 @@ __global__ void __launch_bounds__(kRsThreads, TC_RS_MINBLOCKS)
 #pragma unroll
         for (int j = 0; j < kRsRounds; j++) {
             key[j] = kp[32 * j];
-            if (kVals) val[j] = vp[32 * j];
+            if (kVals) val[j] = vp ? vp[32 * j] : vid0 + 32 * j;
         }
 #pragma unroll
         for (int j = 0; j < kRsRounds; j++) {
@@ -161,7 +183,7 @@ __global__ void __launch_bounds__(kRsThreads, TC_RS_MINBLOCKS)
         for (int j = 0; j < kRsRounds; j++) {
             bool ok = wlocal + 32 * j + lane < tile_n;
             key[j] = ok ? kp[32 * j] : (K)0;
-            if (kVals) val[j] = ok ? vp[32 * j] : 0u;
+            if (kVals) val[j] = ok ? (vp ? vp[32 * j] : vid0 + 32 * j) : 0u;
         }
 #pragma unroll
         for (int j = 0; j < kRsRounds; j++) {
@@ -187,7 +209,7 @@ __global__ void __launch_bounds__(kRsThreads, TC_RS_MINBLOCKS)
     const uint32_t d = threadIdx.x;
     const bool is_digit = d < kDigits;
     uint32_t cnt = 0;
-    uint64_t *my = status + (uint64_t)tile * kDigits + d;
+    SW *my = status + (uint64_t)tile * kDigits + d;
     if (is_digit) {
 #pragma unroll
         for (int w = 0; w < kRsWarps; w++) {
@@ -195,7 +217,7 @@ __global__ void __launch_bounds__(kRsThreads, TC_RS_MINBLOCKS)
             S.wc[w][d] = cnt;
             cnt += c;
         }
-        st_relaxed(my, (tile == 0 ? kFlagPre : kFlagAgg) | cnt);
+        st_relaxed(my, (SW)((tile == 0 ? kFlagPre : kFlagAgg) | (SW)cnt));
     }
     uint32_t dstart = block_exclusive_scan<SumOp>(cnt, S.scan);  // ends with __syncthreads
     if (is_digit) {
@@ -203,9 +225,9 @@ __global__ void __launch_bounds__(kRsThreads, TC_RS_MINBLOCKS)
         if (tile > 0) {
             // look back in batches of kLb predecessors (loads in flight together); a
             // missing tile index (< 0) reads as an inclusive prefix of 0
-            constexpr int kLb = 8;
+            constexpr int kLb = TC_RS_LB;
             for (int64_t t = (int64_t)tile - 1;; t -= kLb) {
-                uint64_t sw[kLb];
+                SW sw[kLb];
 #pragma unroll
                 for (int k = 0; k < kLb; k++)
                     sw[k] = t - k >= 0 ? ld_relaxed(status + (uint64_t)(t - k) * kDigits + d) : kFlagPre;
@@ -220,7 +242,7 @@ __global__ void __launch_bounds__(kRsThreads, TC_RS_MINBLOCKS)
                 }
                 if (done) break;
             }
-            st_relaxed(my, kFlagPre | (excl + cnt));
+            st_relaxed(my, (SW)(kFlagPre | (SW)(excl + cnt)));
         }
         S.dstart[d] = dstart;
         S.gbase[d] = digit_off[d] + excl;
@@ -245,7 +267,11 @@ __global__ void __launch_bounds__(kRsThreads, TC_RS_MINBLOCKS)
         uint32_t dg = (uint32_t)(k >> shift) & 0xffu;
         uint64_t g = S.gbase[dg] + (i - S.dstart[dg]);
         keys_out[g] = k;
-        if (kVals) vals_out[g] = S.vals[i];
+        if (kVals) {
+            const uint32_t v = S.vals[i];
+            vals_out[g] = v;
+            if (gather) gather_out[g] = gather[v];   // fused gather (last pass only)
+        }
     }
 }
 
@@ -254,7 +280,8 @@ __global__ void __launch_bounds__(kRsThreads, TC_RS_MINBLOCKS)
 template <class K, bool kVals>
 static void radix_impl(Ctx &ctx, const K *kin0, const uint32_t *vin0, K *kA, K *kB, uint32_t *vA,
                        uint32_t *vB, uint64_t capacity, const uint64_t *count_dev, int bits,
-                       K **kres, uint32_t **vres) {
+                       K **kres, uint32_t **vres, const uint32_t *gather = nullptr,
+                       uint32_t *gather_out = nullptr) {
     *kres = const_cast<K *>(kin0);
     *vres = const_cast<uint32_t *>(vin0);
     if (capacity == 0 || bits <= 0) return;
@@ -263,7 +290,14 @@ static void radix_impl(Ctx &ctx, const K *kin0, const uint32_t *vin0, K *kA, K *
     uint32_t *hist = ctx.alloc<uint32_t>((uint64_t)passes * kDigits);
     uint64_t *doff = ctx.alloc<uint64_t>((uint64_t)passes * kDigits);
     uint32_t *tickets = ctx.alloc<uint32_t>(passes);
-    uint64_t *status = ctx.alloc<uint64_t>((uint64_t)tiles * kDigits);   // reused per pass
+    // 32-bit status words when every digit prefix (<= capacity) fits in 30 bits
+#ifndef TC_RS_FORCE_WIDE
+    const bool narrow = capacity < (1ull << 30);
+#else
+    const bool narrow = false;
+#endif
+    const size_t sw = narrow ? sizeof(uint32_t) : sizeof(uint64_t);
+    void *status = ctx.alloc<uint64_t>(((uint64_t)tiles * kDigits * sw + 7) / 8);  // reused per pass
     TC_CUDA(cudaMemsetAsync(hist, 0, (size_t)passes * kDigits * sizeof(uint32_t), ctx.stream));
     TC_CUDA(cudaMemsetAsync(tickets, 0, passes * sizeof(uint32_t), ctx.stream));
     k_rs_hist<K><<<ctx.persistent_grid(4), kRsThreads, 0, ctx.stream>>>(kin0, capacity, count_dev,
@@ -272,17 +306,25 @@ static void radix_impl(Ctx &ctx, const K *kin0, const uint32_t *vin0, K *kA, K *
     k_rs_digit_offsets<<<1, 32 * kMaxPasses, 0, ctx.stream>>>(hist, passes, doff);
     TC_LAUNCHED(ctx);
     const size_t smem = sizeof(RsSmem<K, kVals>);
-    TC_CUDA(cudaFuncSetAttribute(k_rs_pass<K, kVals>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
+    TC_CUDA(cudaFuncSetAttribute(k_rs_pass<K, kVals, uint32_t>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    TC_CUDA(cudaFuncSetAttribute(k_rs_pass<K, kVals, uint64_t>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const K *kin = kin0;
     const uint32_t *vin = vin0;
     for (int p = 0; p < passes; p++) {
         K *kout = (p & 1) ? kB : kA;
         uint32_t *vout = (p & 1) ? vB : vA;
-        TC_CUDA(cudaMemsetAsync(status, 0, (size_t)tiles * kDigits * sizeof(uint64_t), ctx.stream));
-        k_rs_pass<K, kVals><<<tiles, kRsThreads, smem, ctx.stream>>>(
-            kin, vin, kout, vout, capacity, count_dev, 8 * p, doff + (uint64_t)p * kDigits,
-            tickets + p, status);
+        TC_CUDA(cudaMemsetAsync(status, 0, (size_t)tiles * kDigits * sw, ctx.stream));
+        const uint32_t *ga = p == passes - 1 ? gather : nullptr;
+        if (narrow)
+            k_rs_pass<K, kVals, uint32_t><<<tiles, kRsThreads, smem, ctx.stream>>>(
+                kin, vin, kout, vout, capacity, count_dev, 8 * p, doff + (uint64_t)p * kDigits,
+                tickets + p, (uint32_t *)status, ga, gather_out);
+        else
+            k_rs_pass<K, kVals, uint64_t><<<tiles, kRsThreads, smem, ctx.stream>>>(
+                kin, vin, kout, vout, capacity, count_dev, 8 * p, doff + (uint64_t)p * kDigits,
+                tickets + p, (uint64_t *)status, ga, gather_out);
         TC_LAUNCHED(ctx);
         kin = kout;
         vin = vout;
@@ -312,9 +354,10 @@ bool radix_sort_pairs(Ctx &ctx, uint32_t *keys, uint32_t *keys_alt, uint32_t *va
 void radix_sort_pairs_from(Ctx &ctx, const uint32_t *keys_in, const uint32_t *vals_in,
                            uint32_t *kA, uint32_t *kB, uint32_t *vA, uint32_t *vB,
                            uint64_t capacity, const uint64_t *count_dev, int bits,
-                           uint32_t **keys_out, uint32_t **vals_out) {
+                           uint32_t **keys_out, uint32_t **vals_out, const uint32_t *gather,
+                           uint32_t *gather_out) {
     radix_impl<uint32_t, true>(ctx, keys_in, vals_in, kA, kB, vA, vB, capacity, count_dev, bits,
-                               keys_out, vals_out);
+                               keys_out, vals_out, gather, gather_out);
 }
 
 }  // namespace tc

@@ -176,10 +176,13 @@ bool radix_sort_pairs(Ctx &ctx, uint32_t *keys, uint32_t *keys_alt, uint32_t *va
                       uint32_t *vals_alt, uint64_t capacity, const uint64_t *count_dev, int bits);
 // Same, reading (keys_in, vals_in) without modifying them; passes ping-pong between
 // A and B; *keys_out / *vals_out receive the buffers holding the result.
+// vals_in == nullptr: the values are the input positions 0, 1, 2, ...  With `gather`, the
+// last pass also writes gather_out[i] = gather[value of sorted item i] (fused gather).
 void radix_sort_pairs_from(Ctx &ctx, const uint32_t *keys_in, const uint32_t *vals_in,
                            uint32_t *kA, uint32_t *kB, uint32_t *vA, uint32_t *vB,
                            uint64_t capacity, const uint64_t *count_dev, int bits,
-                           uint32_t **keys_out, uint32_t **vals_out);
+                           uint32_t **keys_out, uint32_t **vals_out,
+                           const uint32_t *gather = nullptr, uint32_t *gather_out = nullptr);
 
 // ------------------------------------------------------------------ pipeline stages
 // Oriented CSR in RANK-RELABELLED ids: vertex v of the input is newid[v] here,
@@ -189,7 +192,7 @@ struct Oriented {
     uint64_t *off = nullptr;     // off+[n+1]   (indexed by new id)
     uint32_t *col = nullptr;     // col+[m]     (new ids; ascending per row iff rows_sorted)
     uint32_t *dplus = nullptr;   // d+[n]       (indexed by new id)
-    uint64_t *in_off = nullptr;  // transposed CSR: in-lists N-(x), sources ascending
+    uint64_t *in_off = nullptr;  // transposed CSR: in-lists N-(x) (edge-list order)
     uint32_t *in_src = nullptr;
     uint32_t *pidx = nullptr;    // CSR edge e -> its slot in the transposed CSR
     uint32_t *order = nullptr;   // new id -> input id
