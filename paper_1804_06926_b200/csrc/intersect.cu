@@ -278,6 +278,9 @@ __global__ void __launch_bounds__(kIxThreads)
 // starts inside the window (reduce-or + popc): no per-item search.
 constexpr uint32_t kHashSlots = 4096;  // CTA table capacity (power of two), 16 KB
 constexpr uint32_t kHashChunk = 1024;  // owner elements per table build (load factor <= 1/4)
+#ifndef TC_BITMAP_REUSE
+#define TC_BITMAP_REUSE 1
+#endif
 #ifndef TC_HASH_UNROLL
 #define TC_HASH_UNROLL 1
 #endif
@@ -371,6 +374,21 @@ __device__ __forceinline__ uint32_t table_contains(uint32_t tab, int bits, uint3
     return table_contains_slow(tab, (1u << (bits - 2)) - 1u, b, w);
 }
 
+// Probe-list loads (read-only path).  TC_PROBE_NA: hint L1 not to allocate them.
+#ifndef TC_PROBE_NA
+#define TC_PROBE_NA 0
+#endif
+__device__ __forceinline__ uint4 ld_probe(const uint4 *p) {
+#if TC_PROBE_NA
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+
 // Keep a shared-memory base address in a register (stops the compiler from
 // re-deriving it from SR_CgaCtaId at every use).
 __device__ __forceinline__ uint32_t opaque(uint32_t v) {
@@ -429,10 +447,22 @@ struct BitProbe {   // bitmap over the rank-id range [base, base + span) of the 
                                                  uint32_t len) const {
         static_assert(N <= 32, "slot hit vector is one word");
         uint32_t hv = 0;
+#if TC_BITMAP_REUSE
+        // A slot's elements are consecutive entries of a sorted row, so neighbours often
+        // share a bitmap word: load a word only when its index changes (the other lanes
+        // sit the load out, so the shared-memory wavefronts of each probe drop).
+        uint32_t wi_prev = 0xffffffffu, w = 0;
+#endif
 #pragma unroll
         for (int c = 0; c < N; c++) {
             uint32_t o = min(e[c] - base, zero);
+#if TC_BITMAP_REUSE
+            const uint32_t wi = o >> 5;
+            if (wi != wi_prev) w = lds32(bm + 4 * wi);
+            wi_prev = wi;
+#else
             uint32_t w = lds32(bm + 4 * (o >> 5));
+#endif
             // rotate bit (o & 31) of w to position c, collect it in hv
             hv |= __funnelshift_r(w, w, o - c) & (1u << c);
         }
@@ -553,7 +583,7 @@ __device__ __forceinline__ uint64_t probe_quads(const Probe &contains,
             e0[k] = qi << kSlotShift;
             ly[k] = kVid ? d.vid[li] : 0u;
 #pragma unroll
-            for (int v = 0; v < kSlot / 4; v++) q[k][v] = __ldg(col4 + (uint64_t)qi * (kSlot / 4) + v);
+            for (int v = 0; v < kSlot / 4; v++) q[k][v] = ld_probe(col4 + (uint64_t)qi * (kSlot / 4) + v);
             i0 = __shfl_sync(0xffffffffu, li, 31);  // list holding slot wk + 31
         }
 #pragma unroll
