@@ -39,26 +39,31 @@ __device__ __forceinline__ void warp_append(bool take, uint64_t *counter, uint2 
 //   - x owns the edge (suf = |N+(u) after x| <= d+(x)): ulo[p] = e+1 (probe range
 //     [e+1, off[u+1]), the end re-read by the kernel from u = in_src[p]),
 //     an in-part entry of x;
-//   - u owns it (suf > d+(x), ~4% of R-MAT edges): orng[e] = [off[x], off[x] + d+(x)),
-//     an out-part entry of u (compacted in CSR order by k_ocompact);
-// the other slot gets an empty range.  Not-HASH / skipped / other-rank edges: both
-// empty.  SHORT / MERGE / SEARCH edges are appended to their bins.  Also accumulates
+//   - u owns it (suf > d+(x), ~4% of R-MAT edges): bit e of `obits` is set, an
+//     out-part entry of u (probe range N+(x); compacted in CSR order by k_ocompact,
+//     which re-derives the range from x = col+[e]);
+// Not-HASH / skipped / other-rank edges: neither.  One ballot word per warp round
+// (32 consecutive edges) and the tile's out-part count (tcount) replace a per-edge
+// range array.  SHORT / MERGE / SEARCH edges are appended to their bins.  Also accumulates
 // the work statistics.
 __global__ void __launch_bounds__(kTileThreads)
     k_edges(HashParams hp, const uint64_t *__restrict__ m_dev, uint32_t *__restrict__ ulo,
-            uint2 *__restrict__ orng, uint2 *__restrict__ b_short,
-            uint2 *__restrict__ b_merge, uint2 *__restrict__ b_search,
+            uint32_t *__restrict__ obits, uint32_t *__restrict__ tcount,
+            uint2 *__restrict__ b_short, uint2 *__restrict__ b_merge, uint2 *__restrict__ b_search,
             uint64_t *__restrict__ counts) {
     __shared__ uint32_t s_row[kTileItems];
     __shared__ uint32_t s_scan[kTileThreads / 32];
     __shared__ uint64_t s_red[kTileThreads / 32];
     uint64_t m = *m_dev;
     uint64_t t0 = (uint64_t)blockIdx.x * kTileItems;
-    if (t0 >= m) return;
+    if (t0 >= m) {
+        if (threadIdx.x == 0) tcount[blockIdx.x] = 0;
+        return;
+    }
     uint32_t len = (uint32_t)min((uint64_t)kTileItems, m - t0);
     tile_rows(hp.off, hp.n, t0, len, s_row, s_scan);
     const uint64_t chunk = work_chunk(hp);
-    uint64_t W = 0, probe = 0, skipped = 0, hashed = 0;
+    uint64_t W = 0, probe = 0, skipped = 0, hashed = 0, outs = 0;
     // striped: each warp handles 32 consecutive edges per round (warp-aggregated
     // appends); the loads of kBatch rounds are issued before any is used
     constexpr int kRounds = kTileItems / kTileThreads, kBatch = 4;
@@ -84,6 +89,7 @@ __global__ void __launch_bounds__(kTileThreads)
         for (int j = 0; j < kBatch; j++) {
             uint32_t i = (r0 + j) * kTileThreads + threadIdx.x;
             int bin = -1;
+            bool outp = false;
             uint2 item = make_uint2(0, 0);
             if (i < len) {
                 uint64_t e = t0 + i;
@@ -97,18 +103,17 @@ __global__ void __launch_bounds__(kTileThreads)
                 if (bin >= 0 && rank_owner(hp, chunk, u) != hp.rank) bin = -1;
                 item = make_uint2(u, x);
                 uint32_t ri = 0;
-                uint2 ro = make_uint2(0, 0);
                 if (bin == TC_VARIANT_HASH) {
                     hashed++;
-                    if (suf <= dv) {
-                        ri = (uint32_t)(e + 1);
-                    } else {
-                        uint64_t xb = hp.off[x];
-                        ro = make_uint2((uint32_t)xb, (uint32_t)(xb + dv));
-                    }
+                    if (suf <= dv) ri = (uint32_t)(e + 1);
+                    else outp = true;
                 }
                 ulo[ps[j]] = ri;
-                orng[e] = ro;
+            }
+            const uint32_t ob = __ballot_sync(0xffffffffu, outp);
+            if ((threadIdx.x & 31) == 0) {
+                obits[(t0 + (uint64_t)(r0 + j) * kTileThreads + (threadIdx.x & ~31u)) >> 5] = ob;
+                outs += __popc(ob);
             }
             warp_append(bin == TC_VARIANT_SHORT, &counts[0], b_short, item);
             warp_append(bin == TC_VARIANT_MERGE, &counts[1], b_merge, item);
@@ -119,7 +124,9 @@ __global__ void __launch_bounds__(kTileThreads)
     probe = block_sum_u64(probe, s_red);
     skipped = block_sum_u64(skipped, s_red);
     hashed = block_sum_u64(hashed, s_red);
+    outs = block_sum_u64(outs, s_red);
     if (threadIdx.x == 0) {
+        tcount[blockIdx.x] = (uint32_t)outs;
         atomicAdd((unsigned long long *)&counts[3], (unsigned long long)hashed);
         atomicAdd((unsigned long long *)&counts[4], (unsigned long long)W);
         atomicAdd((unsigned long long *)&counts[5], (unsigned long long)probe);
@@ -127,60 +134,56 @@ __global__ void __launch_bounds__(kTileThreads)
     }
 }
 
-// Compaction of the out-part entries (CSR order => grouped by the owning source).
-__global__ void __launch_bounds__(kTileThreads)
-    k_ocount(const uint2 *__restrict__ orng, const uint64_t *__restrict__ m_dev,
-             uint32_t *__restrict__ tcount) {
-    __shared__ uint64_t s_red[kTileThreads / 32];
-    uint64_t m = *m_dev, t0 = (uint64_t)blockIdx.x * kTileItems, c = 0;
-    for (uint32_t i = threadIdx.x; i < kTileItems; i += kTileThreads)
-        if (t0 + i < m) {
-            uint2 r = orng[t0 + i];
-            c += r.y > r.x;
-        }
-    c = block_sum_u64(c, s_red);
-    if (threadIdx.x == 0) tcount[blockIdx.x] = (uint32_t)c;
-}
-
-__global__ void __launch_bounds__(kTileThreads)
-    k_ocompact(const uint2 *__restrict__ orng, const uint32_t *__restrict__ col,
+// Compaction of the out-part entries (CSR order => grouped by the owning source): one
+// 64-thread block per tile, one thread per ballot word.  Entry = probe range N+(x) of
+// the edge's target x and its vid (x, or the edge index for edge support).  Also the
+// in-tile exclusive prefix of each word (wpre) for k_ooff.
+constexpr int kTileWords = kTileItems / 32;
+__global__ void __launch_bounds__(kTileWords)
+    k_ocompact(const uint32_t *__restrict__ obits, const uint32_t *__restrict__ col,
+               const uint64_t *__restrict__ off, const uint32_t *__restrict__ dplus,
                const uint64_t *__restrict__ m_dev, const uint64_t *__restrict__ toff,
-               uint2 *__restrict__ orange, uint32_t *__restrict__ ovid, uint32_t *__restrict__ before,
+               uint2 *__restrict__ orange, uint32_t *__restrict__ ovid, uint16_t *__restrict__ wpre,
                bool edge_ids) {
-    __shared__ uint32_t s_scan[kTileThreads / 32];
-    uint64_t m = *m_dev, t0 = (uint64_t)blockIdx.x * kTileItems;
+    __shared__ uint32_t s_w[kTileWords / 32];
+    const uint64_t m = *m_dev, t0 = (uint64_t)blockIdx.x * kTileItems;
     if (t0 >= m) return;
-    uint32_t len = (uint32_t)min((uint64_t)kTileItems, m - t0);
-    uint32_t i0 = threadIdx.x * kItemsPerThread, c = 0;
-    uint2 r[kItemsPerThread];
-#pragma unroll
-    for (int k = 0; k < kItemsPerThread; k++) {
-        r[k] = i0 + k < len ? orng[t0 + i0 + k] : make_uint2(0, 0);
-        c += r[k].y > r[k].x;
-    }
-    uint32_t pos = block_exclusive_scan<SumOp>(c, s_scan);
-    uint64_t base = toff[blockIdx.x] + pos;
-#pragma unroll
-    for (int k = 0; k < kItemsPerThread; k++) {
-        uint32_t i = i0 + k;
-        if (i < len) before[t0 + i] = (uint32_t)base;
-        if (r[k].y > r[k].x) {
-            orange[base] = r[k];
-            ovid[base] = edge_ids ? (uint32_t)(t0 + i) : col[t0 + i];
-            base++;
-        }
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t gw = (t0 >> 5) + threadIdx.x;
+    const uint64_t e0 = t0 + 32ull * threadIdx.x;
+    uint32_t bits = e0 < m ? obits[gw] : 0u;
+    const uint32_t c = __popc(bits);
+    const uint32_t inc = warp_inclusive_scan<SumOp>(c);
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    uint32_t excl = inc - c;
+    for (uint32_t w = 0; w < warp; w++) excl += s_w[w];
+    if (e0 < m) wpre[gw] = (uint16_t)excl;
+    uint64_t base = toff[blockIdx.x] + excl;
+    while (bits) {
+        const uint32_t b = __ffs(bits) - 1;
+        bits &= bits - 1;
+        const uint64_t e = e0 + b;
+        const uint32_t x = col[e];
+        const uint64_t xb = off[x];
+        orange[base] = make_uint2((uint32_t)xb, (uint32_t)(xb + dplus[x]));
+        ovid[base] = edge_ids ? (uint32_t)e : x;
+        base++;
     }
 }
 
-// ooff[x] = out-part entries before x's row (gather; empty rows are fine).
+// ooff[x] = out-part entries before x's row = tile prefix + word prefix + bits below.
 __global__ void k_ooff(const uint64_t *__restrict__ off, uint64_t n, const uint64_t *__restrict__ m_dev,
-                       const uint32_t *__restrict__ before, const uint64_t *__restrict__ total,
+                       const uint32_t *__restrict__ obits, const uint16_t *__restrict__ wpre,
+                       const uint64_t *__restrict__ toff, const uint64_t *__restrict__ total,
                        uint64_t *__restrict__ ooff) {
     uint64_t m = *m_dev, t = *total;
     for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x <= n;
          x += (uint64_t)gridDim.x * blockDim.x) {
         uint64_t s = off[x];
-        ooff[x] = s < m ? before[s] : t;
+        ooff[x] = s < m ? toff[s / kTileItems] + wpre[s >> 5] +
+                              __popc(obits[s >> 5] & ((1u << (s & 31)) - 1u))
+                        : t;
     }
 }
 
@@ -313,28 +316,27 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
     // HASH: in-part ranges (in-list order), out-part entries (compacted, CSR order),
     // statistics, owners, tasks
     uint32_t *ulo = ctx.alloc<uint32_t>(cap);
-    uint2 *orng = ctx.alloc<uint2>(cap);
+    uint32_t *obits = ctx.alloc<uint32_t>((uint64_t)tiles * kTileWords + 1);
+    uint16_t *wpre = ctx.alloc<uint16_t>((uint64_t)tiles * kTileWords + 1);
     uint2 *orange = ctx.alloc<uint2>(cap);
-    uint32_t *ovid = ctx.alloc<uint32_t>(cap), *before = ctx.alloc<uint32_t>(cap);
+    uint32_t *ovid = ctx.alloc<uint32_t>(cap);
     uint32_t *tcount = ctx.alloc<uint32_t>(tiles + 1);
     uint64_t *toff = ctx.alloc<uint64_t>(tiles + 1), *ooff = ctx.alloc<uint64_t>(n + 1);
     uint32_t *has_in = ctx.alloc<uint32_t>(n + 1);
     if (tiles) {
-        k_edges<<<tiles, kTileThreads, 0, ctx.stream>>>(hp, g.m_dev, ulo, orng,
+        k_edges<<<tiles, kTileThreads, 0, ctx.stream>>>(hp, g.m_dev, ulo, obits, tcount,
                                                         bins.edges[0], bins.edges[1], bins.edges[2],
                                                         bins.count);
-        TC_LAUNCHED(ctx);
-        k_ocount<<<tiles, kTileThreads, 0, ctx.stream>>>(orng, g.m_dev, tcount);
         TC_LAUNCHED(ctx);
     }
     scan_exclusive(ctx, tcount, toff, tiles);
     if (tiles) {
-        k_ocompact<<<tiles, kTileThreads, 0, ctx.stream>>>(orng, g.col, g.m_dev, toff, orange, ovid,
-                                                           before, p.edge_ids);
+        k_ocompact<<<tiles, kTileWords, 0, ctx.stream>>>(obits, g.col, g.off, g.dplus, g.m_dev, toff,
+                                                         orange, ovid, wpre, p.edge_ids);
         TC_LAUNCHED(ctx);
     }
-    k_ooff<<<ctx.persistent_grid(4), 256, 0, ctx.stream>>>(g.off, n, g.m_dev, before, toff + tiles,
-                                                           ooff);
+    k_ooff<<<ctx.persistent_grid(4), 256, 0, ctx.stream>>>(g.off, n, g.m_dev, obits, wpre, toff,
+                                                           toff + tiles, ooff);
     TC_LAUNCHED(ctx);
     hp.ulo = ulo;
     hp.has_in = has_in;

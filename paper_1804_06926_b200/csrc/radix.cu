@@ -281,13 +281,13 @@ template <class K, bool kVals>
 static void radix_impl(Ctx &ctx, const K *kin0, const uint32_t *vin0, K *kA, K *kB, uint32_t *vA,
                        uint32_t *vB, uint64_t capacity, const uint64_t *count_dev, int bits,
                        K **kres, uint32_t **vres, const uint32_t *gather = nullptr,
-                       uint32_t *gather_out = nullptr) {
+                       uint32_t *gather_out = nullptr, const uint32_t *hist_in = nullptr) {
     *kres = const_cast<K *>(kin0);
     *vres = const_cast<uint32_t *>(vin0);
     if (capacity == 0 || bits <= 0) return;
     const int passes = (bits + 7) / 8;
     const uint32_t tiles = (uint32_t)((capacity + kRsTile - 1) / kRsTile);
-    uint32_t *hist = ctx.alloc<uint32_t>((uint64_t)passes * kDigits);
+    const uint32_t *hist = hist_in;   // digit histograms counted by the producer, or here
     uint64_t *doff = ctx.alloc<uint64_t>((uint64_t)passes * kDigits);
     uint32_t *tickets = ctx.alloc<uint32_t>(passes);
     // 32-bit status words when every digit prefix (<= capacity) fits in 30 bits
@@ -298,11 +298,15 @@ static void radix_impl(Ctx &ctx, const K *kin0, const uint32_t *vin0, K *kA, K *
 #endif
     const size_t sw = narrow ? sizeof(uint32_t) : sizeof(uint64_t);
     void *status = ctx.alloc<uint64_t>(((uint64_t)tiles * kDigits * sw + 7) / 8);  // reused per pass
-    TC_CUDA(cudaMemsetAsync(hist, 0, (size_t)passes * kDigits * sizeof(uint32_t), ctx.stream));
     TC_CUDA(cudaMemsetAsync(tickets, 0, passes * sizeof(uint32_t), ctx.stream));
-    k_rs_hist<K><<<ctx.persistent_grid(4), kRsThreads, 0, ctx.stream>>>(kin0, capacity, count_dev,
-                                                                        passes, hist);
-    TC_LAUNCHED(ctx);
+    if (!hist) {
+        uint32_t *h = ctx.alloc<uint32_t>((uint64_t)passes * kDigits);
+        TC_CUDA(cudaMemsetAsync(h, 0, (size_t)passes * kDigits * sizeof(uint32_t), ctx.stream));
+        k_rs_hist<K><<<ctx.persistent_grid(4), kRsThreads, 0, ctx.stream>>>(kin0, capacity, count_dev,
+                                                                            passes, h);
+        TC_LAUNCHED(ctx);
+        hist = h;
+    }
     k_rs_digit_offsets<<<1, 32 * kMaxPasses, 0, ctx.stream>>>(hist, passes, doff);
     TC_LAUNCHED(ctx);
     const size_t smem = sizeof(RsSmem<K, kVals>);
@@ -334,20 +338,21 @@ static void radix_impl(Ctx &ctx, const K *kin0, const uint32_t *vin0, K *kA, K *
 }
 
 bool radix_sort(Ctx &ctx, uint64_t *keys, uint64_t *keys_alt, uint64_t capacity,
-                const uint64_t *count_dev, int bits) {
+                const uint64_t *count_dev, int bits, const uint32_t *hist_in) {
     // (keys -> alt -> keys ...): first pass reads `keys`, then alt/keys alternate
     uint64_t *kr;
     uint32_t *vr;
     radix_impl<uint64_t, false>(ctx, keys, nullptr, keys_alt, keys, nullptr, nullptr, capacity,
-                                count_dev, bits, &kr, &vr);
+                                count_dev, bits, &kr, &vr, nullptr, nullptr, hist_in);
     return kr == keys_alt;
 }
 
 bool radix_sort_pairs(Ctx &ctx, uint32_t *keys, uint32_t *keys_alt, uint32_t *vals,
-                      uint32_t *vals_alt, uint64_t capacity, const uint64_t *count_dev, int bits) {
+                      uint32_t *vals_alt, uint64_t capacity, const uint64_t *count_dev, int bits,
+                      const uint32_t *hist_in) {
     uint32_t *kr, *vr;
     radix_impl<uint32_t, true>(ctx, keys, vals, keys_alt, keys, vals_alt, vals, capacity, count_dev,
-                               bits, &kr, &vr);
+                               bits, &kr, &vr, nullptr, nullptr, hist_in);
     return kr == keys_alt;
 }
 
@@ -355,9 +360,9 @@ void radix_sort_pairs_from(Ctx &ctx, const uint32_t *keys_in, const uint32_t *va
                            uint32_t *kA, uint32_t *kB, uint32_t *vA, uint32_t *vB,
                            uint64_t capacity, const uint64_t *count_dev, int bits,
                            uint32_t **keys_out, uint32_t **vals_out, const uint32_t *gather,
-                           uint32_t *gather_out) {
+                           uint32_t *gather_out, const uint32_t *hist_in) {
     radix_impl<uint32_t, true>(ctx, keys_in, vals_in, kA, kB, vA, vB, capacity, count_dev, bits,
-                               keys_out, vals_out, gather, gather_out);
+                               keys_out, vals_out, gather, gather_out, hist_in);
 }
 
 }  // namespace tc

@@ -162,6 +162,30 @@ __device__ __forceinline__ void tile_rows(const uint64_t *__restrict__ rowptr, u
 }
 
 
+// ------------------------------------------------------------------ fused digit histograms
+// Producers of radix-sort keys count the 8-bit digits of every pass on the fly:
+// shared-memory counters (RsHist) flushed with one global atomic per non-zero digit.
+constexpr int kHistDigits = 256;
+template <int P>
+struct RsHist {
+    uint32_t h[P][kHistDigits];
+    __device__ __forceinline__ void clear() {
+        for (int i = threadIdx.x; i < P * kHistDigits; i += blockDim.x) (&h[0][0])[i] = 0;
+    }
+    template <class K>
+    __device__ __forceinline__ void add(K key, int passes) {
+#pragma unroll
+        for (int p = 0; p < P; p++)
+            if (p < passes) atomicAdd(&h[p][(uint32_t)(key >> (8 * p)) & 0xffu], 1u);
+    }
+    __device__ __forceinline__ void flush(uint32_t *g, int passes) {
+        for (int i = threadIdx.x; i < passes * kHistDigits; i += blockDim.x) {
+            uint32_t v = (&h[0][0])[i];
+            if (v) atomicAdd(&g[i], v);
+        }
+    }
+};
+
 // ------------------------------------------------------------------ host primitives
 // Exclusive scan: out[i] = sum_{j<i} in[j] for i in [0, count], out[count] = total.
 void scan_exclusive(Ctx &ctx, const uint32_t *in, uint64_t *out, uint64_t count);
@@ -170,10 +194,14 @@ void scan_exclusive(Ctx &ctx, const uint64_t *in, uint64_t *out, uint64_t count)
 // Stable LSD radix sort on bits [0, bits) of the keys.  `count_dev`, if non-null,
 // is a device counter that caps the number of valid items (<= capacity).
 // Returns true if the sorted result ended in the *_alt buffers.
+// hist_in (optional): the digit histograms of the keys, hist_in[pass * 256 + digit] for
+// the (bits + 7) / 8 passes, counted by the kernel that produced the keys (skips the
+// histogram pass).
 bool radix_sort(Ctx &ctx, uint64_t *keys, uint64_t *keys_alt, uint64_t capacity,
-                const uint64_t *count_dev, int bits);
+                const uint64_t *count_dev, int bits, const uint32_t *hist_in = nullptr);
 bool radix_sort_pairs(Ctx &ctx, uint32_t *keys, uint32_t *keys_alt, uint32_t *vals,
-                      uint32_t *vals_alt, uint64_t capacity, const uint64_t *count_dev, int bits);
+                      uint32_t *vals_alt, uint64_t capacity, const uint64_t *count_dev, int bits,
+                      const uint32_t *hist_in = nullptr);
 // Same, reading (keys_in, vals_in) without modifying them; passes ping-pong between
 // A and B; *keys_out / *vals_out receive the buffers holding the result.
 // vals_in == nullptr: the values are the input positions 0, 1, 2, ...  With `gather`, the
@@ -182,7 +210,8 @@ void radix_sort_pairs_from(Ctx &ctx, const uint32_t *keys_in, const uint32_t *va
                            uint32_t *kA, uint32_t *kB, uint32_t *vA, uint32_t *vB,
                            uint64_t capacity, const uint64_t *count_dev, int bits,
                            uint32_t **keys_out, uint32_t **vals_out,
-                           const uint32_t *gather = nullptr, uint32_t *gather_out = nullptr);
+                           const uint32_t *gather = nullptr, uint32_t *gather_out = nullptr,
+                           const uint32_t *hist_in = nullptr);
 
 // ------------------------------------------------------------------ pipeline stages
 // Oriented CSR in RANK-RELABELLED ids: vertex v of the input is newid[v] here,
