@@ -54,6 +54,12 @@ __global__ void __launch_bounds__(kTileThreads)
     __shared__ uint32_t s_row[kTileItems];
     __shared__ uint32_t s_scan[kTileThreads / 32];
     __shared__ uint64_t s_red[kTileThreads / 32];
+    // SHORT edges (AUTO sends many) are staged per tile and appended with ONE global
+    // atomic per block: per-warp appends all hit one counter (~1 M atomics per step at s21)
+    __shared__ uint2 s_short[kTileItems];
+    __shared__ uint32_t s_nshort;
+    __shared__ uint64_t s_short_base;
+    if (threadIdx.x == 0) s_nshort = 0;
     uint64_t m = *m_dev;
     uint64_t t0 = (uint64_t)blockIdx.x * kTileItems;
     if (t0 >= m) {
@@ -115,11 +121,27 @@ __global__ void __launch_bounds__(kTileThreads)
                 obits[(t0 + (uint64_t)(r0 + j) * kTileThreads + (threadIdx.x & ~31u)) >> 5] = ob;
                 outs += __popc(ob);
             }
-            warp_append(bin == TC_VARIANT_SHORT, &counts[0], b_short, item);
+            {   // stage SHORT in shared memory (warp-aggregated shared atomic)
+                const bool take = bin == TC_VARIANT_SHORT;
+                const uint32_t mask = __ballot_sync(0xffffffffu, take);
+                if (mask) {
+                    const int lane = threadIdx.x & 31, leader = __ffs(mask) - 1;
+                    uint32_t b0 = 0;
+                    if (lane == leader) b0 = atomicAdd(&s_nshort, (uint32_t)__popc(mask));
+                    b0 = __shfl_sync(0xffffffffu, b0, leader);
+                    if (take) s_short[b0 + __popc(mask & ((1u << lane) - 1u))] = item;
+                }
+            }
             warp_append(bin == TC_VARIANT_MERGE, &counts[1], b_merge, item);
             warp_append(bin == TC_VARIANT_SEARCH, &counts[2], b_search, item);
         }
     }
+    __syncthreads();
+    const uint32_t ns = s_nshort;
+    if (threadIdx.x == 0 && ns)
+        s_short_base = atomicAdd((unsigned long long *)&counts[0], (unsigned long long)ns);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < ns; i += kTileThreads) b_short[s_short_base + i] = s_short[i];
     W = block_sum_u64(W, s_red);
     probe = block_sum_u64(probe, s_red);
     skipped = block_sum_u64(skipped, s_red);

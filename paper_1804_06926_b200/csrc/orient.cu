@@ -120,7 +120,7 @@ __global__ void k_orient_pairs(const uint64_t *__restrict__ E, const uint64_t *_
                                int b, const uint32_t *__restrict__ newid, uint32_t *__restrict__ okey,
                                uint32_t *__restrict__ oval, uint32_t *__restrict__ dplus,
                                uint32_t *__restrict__ hist_key, uint32_t *__restrict__ hist_val,
-                               int passes) {
+                               int passes, int db) {
     __shared__ RsHist<4> s_hk, s_hv;
     s_hk.clear();
     s_hv.clear();
@@ -138,8 +138,8 @@ __global__ void k_orient_pairs(const uint64_t *__restrict__ E, const uint64_t *_
             s = min(a, c);   // low -> high rank
             okey[i] = s;
             oval[i] = max(a, c);
-            s_hk.add(s, passes);
-            s_hv.add(max(a, c), passes);
+            s_hk.add(s, passes, db);
+            s_hv.add(max(a, c), passes, db);
         }
         // runs of one min often keep the same (low-rank) source: aggregate per warp
         uint32_t peers = __match_any_sync(0xffffffffu, s);
@@ -279,11 +279,11 @@ void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, cons
     }
     rank_permutation(ctx, n, rank_key(ctx, n, deg, id_order), out);
     uint32_t *okey = ctx.alloc<uint32_t>(M), *oval = ctx.alloc<uint32_t>(M);
-    const int ppasses = (b + 7) / 8;
+    const int pdb = radix_digit_bits(b), ppasses = (b + pdb - 1) / pdb;
     uint32_t *phist = ctx.alloc<uint32_t>(2 * ppasses * kHistDigits);
     TC_CUDA(cudaMemsetAsync(phist, 0, 2 * ppasses * kHistDigits * sizeof(uint32_t), ctx.stream));
     k_orient_pairs<<<grid, 256, 0, ctx.stream>>>(E, m_dev, b, out.newid, okey, oval, dplus, phist,
-                                                 phist + ppasses * kHistDigits, ppasses);
+                                                 phist + ppasses * kHistDigits, ppasses, pdb);
     TC_LAUNCHED(ctx);
     k_dminus<<<grid, 256, 0, ctx.stream>>>(deg, out.newid, dplus, n, dminus);
     TC_LAUNCHED(ctx);

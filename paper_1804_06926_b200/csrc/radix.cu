@@ -74,15 +74,16 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
 template <class K>
 __global__ void __launch_bounds__(kRsThreads)
     k_rs_hist(const K *__restrict__ keys, uint64_t cap, const uint64_t *__restrict__ count_dev,
-              int passes, uint32_t *__restrict__ hist) {
+              int passes, int db, uint32_t *__restrict__ hist) {
     __shared__ uint32_t h[kMaxPasses][kDigits];
+    const uint32_t dmask = (1u << db) - 1u;
     uint64_t n = valid_count(cap, count_dev);
     for (int i = threadIdx.x; i < kMaxPasses * kDigits; i += kRsThreads) (&h[0][0])[i] = 0;
     __syncthreads();
     for (uint64_t i = (uint64_t)blockIdx.x * kRsThreads + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * kRsThreads) {
         K k = keys[i];
-        for (int p = 0; p < passes; p++) atomicAdd(&h[p][(uint32_t)(k >> (8 * p)) & 0xffu], 1u);
+        for (int p = 0; p < passes; p++) atomicAdd(&h[p][(uint32_t)(k >> (db * p)) & dmask], 1u);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < passes * kDigits; i += kRsThreads) {
@@ -108,12 +109,13 @@ __global__ void k_rs_digit_offsets(const uint32_t *__restrict__ hist, int passes
     }
 }
 
-// Lanes of `active` holding the same 8-bit digit d as this lane: 8 ballots, measured
+// Lanes of `active` holding the same DB-bit digit d as this lane: DB ballots, measured
 // a little faster than __match_any_sync on sm_100a.
+template <int DB>
 __device__ __forceinline__ uint32_t digit_peers(uint32_t active, uint32_t d) {
     uint32_t peers = active;
 #pragma unroll
-    for (int b = 0; b < 8; b++) {
+    for (int b = 0; b < DB; b++) {
         uint32_t m = __ballot_sync(active, (d >> b) & 1u);
         peers &= ((d >> b) & 1u) ? m : ~m;
     }
@@ -131,7 +133,7 @@ struct RsSmem {
     uint32_t tile;
 };
 
-template <class K, bool kVals, class SW>
+template <class K, bool kVals, class SW, int DB>
 __global__ void __launch_bounds__(kRsThreads, TC_RS_MINBLOCKS)
     k_rs_pass(const K *__restrict__ keys, const uint32_t *__restrict__ vals, K *__restrict__ keys_out,
               uint32_t *__restrict__ vals_out, uint64_t cap, const uint64_t *__restrict__ count_dev,
@@ -140,6 +142,7 @@ __global__ void __launch_bounds__(kRsThreads, TC_RS_MINBLOCKS)
               uint32_t *__restrict__ gather_out) {
     constexpr SW kFlagAgg = Status<SW>::kFlagAgg, kFlagPre = Status<SW>::kFlagPre;
     constexpr SW kCountMask = Status<SW>::kCountMask;
+    constexpr uint32_t kD = 1u << DB, kDMask = kD - 1u;   // digits of this pass
     extern __shared__ __align__(16) unsigned char smem_raw[];
     RsSmem<K, kVals> &S = *reinterpret_cast<RsSmem<K, kVals> *>(smem_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -170,8 +173,8 @@ __global__ void __launch_bounds__(kRsThreads, TC_RS_MINBLOCKS)
         }
 #pragma unroll
         for (int j = 0; j < kRsRounds; j++) {
-            uint32_t d = (uint32_t)(key[j] >> shift) & 0xffu;
-            uint32_t peers = digit_peers(0xffffffffu, d);
+            uint32_t d = (uint32_t)(key[j] >> shift) & kDMask;
+            uint32_t peers = digit_peers<DB>(0xffffffffu, d);
             uint32_t old = wc[d];
             __syncwarp();
             if ((peers & lt) == 0) wc[d] = old + __popc(peers);
@@ -188,11 +191,11 @@ __global__ void __launch_bounds__(kRsThreads, TC_RS_MINBLOCKS)
 #pragma unroll
         for (int j = 0; j < kRsRounds; j++) {
             bool ok = wlocal + 32 * j + lane < tile_n;
-            uint32_t d = (uint32_t)(key[j] >> shift) & 0xffu;
+            uint32_t d = (uint32_t)(key[j] >> shift) & kDMask;
             uint32_t active = __ballot_sync(0xffffffffu, ok);
             uint32_t old = 0, peers = 0;
             if (ok) {
-                peers = digit_peers(active, d);
+                peers = digit_peers<DB>(active, d);
                 old = wc[d];
             }
             __syncwarp();
@@ -207,9 +210,9 @@ __global__ void __launch_bounds__(kRsThreads, TC_RS_MINBLOCKS)
     // aggregate, look back
     static_assert(kRsThreads >= kDigits, "one thread per digit");
     const uint32_t d = threadIdx.x;
-    const bool is_digit = d < kDigits;
+    const bool is_digit = d < kD;
     uint32_t cnt = 0;
-    SW *my = status + (uint64_t)tile * kDigits + d;
+    SW *my = status + (uint64_t)tile * kD + d;
     if (is_digit) {
 #pragma unroll
         for (int w = 0; w < kRsWarps; w++) {
@@ -230,13 +233,13 @@ __global__ void __launch_bounds__(kRsThreads, TC_RS_MINBLOCKS)
                 SW sw[kLb];
 #pragma unroll
                 for (int k = 0; k < kLb; k++)
-                    sw[k] = t - k >= 0 ? ld_relaxed(status + (uint64_t)(t - k) * kDigits + d) : kFlagPre;
+                    sw[k] = t - k >= 0 ? ld_relaxed(status + (uint64_t)(t - k) * kD + d) : kFlagPre;
                 bool done = false;
 #pragma unroll
                 for (int k = 0; k < kLb; k++) {
                     if (done) break;
                     while ((sw[k] & ~kCountMask) == 0)
-                        sw[k] = ld_relaxed(status + (uint64_t)(t - k) * kDigits + d);
+                        sw[k] = ld_relaxed(status + (uint64_t)(t - k) * kD + d);
                     excl += sw[k] & kCountMask;
                     done = (sw[k] & kFlagPre) != 0;
                 }
@@ -254,7 +257,7 @@ __global__ void __launch_bounds__(kRsThreads, TC_RS_MINBLOCKS)
     for (int j = 0; j < kRsRounds; j++) {
         uint32_t local = wlocal + 32 * j + lane;
         if (local < tile_n) {
-            uint32_t dg = (uint32_t)(key[j] >> shift) & 0xffu;
+            uint32_t dg = (uint32_t)(key[j] >> shift) & kDMask;
             uint32_t pos = S.dstart[dg] + S.wc[warp][dg] + rank[j];
             S.keys[pos] = key[j];
             if (kVals) S.vals[pos] = val[j];
@@ -264,7 +267,7 @@ __global__ void __launch_bounds__(kRsThreads, TC_RS_MINBLOCKS)
 #pragma unroll 4
     for (uint32_t i = threadIdx.x; i < tile_n; i += kRsThreads) {
         K k = S.keys[i];
-        uint32_t dg = (uint32_t)(k >> shift) & 0xffu;
+        uint32_t dg = (uint32_t)(k >> shift) & kDMask;
         uint64_t g = S.gbase[dg] + (i - S.dstart[dg]);
         keys_out[g] = k;
         if (kVals) {
@@ -285,7 +288,8 @@ static void radix_impl(Ctx &ctx, const K *kin0, const uint32_t *vin0, K *kA, K *
     *kres = const_cast<K *>(kin0);
     *vres = const_cast<uint32_t *>(vin0);
     if (capacity == 0 || bits <= 0) return;
-    const int passes = (bits + 7) / 8;
+    const int db = radix_digit_bits(bits);   // 7-bit digits when they need no extra pass
+    const int passes = (bits + db - 1) / db;
     const uint32_t tiles = (uint32_t)((capacity + kRsTile - 1) / kRsTile);
     const uint32_t *hist = hist_in;   // digit histograms counted by the producer, or here
     uint64_t *doff = ctx.alloc<uint64_t>((uint64_t)passes * kDigits);
@@ -303,17 +307,20 @@ static void radix_impl(Ctx &ctx, const K *kin0, const uint32_t *vin0, K *kA, K *
         uint32_t *h = ctx.alloc<uint32_t>((uint64_t)passes * kDigits);
         TC_CUDA(cudaMemsetAsync(h, 0, (size_t)passes * kDigits * sizeof(uint32_t), ctx.stream));
         k_rs_hist<K><<<ctx.persistent_grid(4), kRsThreads, 0, ctx.stream>>>(kin0, capacity, count_dev,
-                                                                            passes, h);
+                                                                            passes, db, h);
         TC_LAUNCHED(ctx);
         hist = h;
     }
     k_rs_digit_offsets<<<1, 32 * kMaxPasses, 0, ctx.stream>>>(hist, passes, doff);
     TC_LAUNCHED(ctx);
     const size_t smem = sizeof(RsSmem<K, kVals>);
-    TC_CUDA(cudaFuncSetAttribute(k_rs_pass<K, kVals, uint32_t>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    TC_CUDA(cudaFuncSetAttribute(k_rs_pass<K, kVals, uint64_t>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    auto set_smem = [&](auto kern) {
+        TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    };
+    set_smem(k_rs_pass<K, kVals, uint32_t, 7>);
+    set_smem(k_rs_pass<K, kVals, uint32_t, 8>);
+    set_smem(k_rs_pass<K, kVals, uint64_t, 7>);
+    set_smem(k_rs_pass<K, kVals, uint64_t, 8>);
     const K *kin = kin0;
     const uint32_t *vin = vin0;
     for (int p = 0; p < passes; p++) {
@@ -321,14 +328,19 @@ static void radix_impl(Ctx &ctx, const K *kin0, const uint32_t *vin0, K *kA, K *
         uint32_t *vout = (p & 1) ? vB : vA;
         TC_CUDA(cudaMemsetAsync(status, 0, (size_t)tiles * kDigits * sw, ctx.stream));
         const uint32_t *ga = p == passes - 1 ? gather : nullptr;
-        if (narrow)
-            k_rs_pass<K, kVals, uint32_t><<<tiles, kRsThreads, smem, ctx.stream>>>(
-                kin, vin, kout, vout, capacity, count_dev, 8 * p, doff + (uint64_t)p * kDigits,
-                tickets + p, (uint32_t *)status, ga, gather_out);
-        else
-            k_rs_pass<K, kVals, uint64_t><<<tiles, kRsThreads, smem, ctx.stream>>>(
-                kin, vin, kout, vout, capacity, count_dev, 8 * p, doff + (uint64_t)p * kDigits,
-                tickets + p, (uint64_t *)status, ga, gather_out);
+        const uint64_t *dop = doff + (uint64_t)p * kDigits;
+#define TC_RS_LAUNCH(SWT, DBV)                                                                  \
+    k_rs_pass<K, kVals, SWT, DBV><<<tiles, kRsThreads, smem, ctx.stream>>>(                     \
+        kin, vin, kout, vout, capacity, count_dev, db * p, dop, tickets + p, (SWT *)status, ga, \
+        gather_out)
+        if (narrow) {
+            if (db == 7) TC_RS_LAUNCH(uint32_t, 7);
+            else TC_RS_LAUNCH(uint32_t, 8);
+        } else {
+            if (db == 7) TC_RS_LAUNCH(uint64_t, 7);
+            else TC_RS_LAUNCH(uint64_t, 8);
+        }
+#undef TC_RS_LAUNCH
         TC_LAUNCHED(ctx);
         kin = kout;
         vin = vout;

@@ -162,6 +162,17 @@ __device__ __forceinline__ void tile_rows(const uint64_t *__restrict__ rowptr, u
 }
 
 
+// Digit width of an LSD radix sort over `bits` key bits: 7 when 7-bit digits need no
+// more passes than 8-bit ones (fewer ballots per rank, half the look-back digits), else 8.
+inline int radix_digit_bits(int bits) {
+#ifdef TC_RS_FORCE_DB8
+    (void)bits;
+    return 8;
+#else
+    return (bits + 6) / 7 == (bits + 7) / 8 ? 7 : 8;
+#endif
+}
+
 // ------------------------------------------------------------------ fused digit histograms
 // Producers of radix-sort keys count the 8-bit digits of every pass on the fly:
 // shared-memory counters (RsHist) flushed with one global atomic per non-zero digit.
@@ -173,10 +184,11 @@ struct RsHist {
         for (int i = threadIdx.x; i < P * kHistDigits; i += blockDim.x) (&h[0][0])[i] = 0;
     }
     template <class K>
-    __device__ __forceinline__ void add(K key, int passes) {
+    __device__ __forceinline__ void add(K key, int passes, int db) {
+        const uint32_t mask = (1u << db) - 1u;
 #pragma unroll
         for (int p = 0; p < P; p++)
-            if (p < passes) atomicAdd(&h[p][(uint32_t)(key >> (8 * p)) & 0xffu], 1u);
+            if (p < passes) atomicAdd(&h[p][(uint32_t)(key >> (db * p)) & mask], 1u);
     }
     __device__ __forceinline__ void flush(uint32_t *g, int passes) {
         for (int i = threadIdx.x; i < passes * kHistDigits; i += blockDim.x) {
