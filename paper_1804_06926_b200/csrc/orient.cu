@@ -60,28 +60,33 @@ __device__ __forceinline__ bool unique_flag(const uint64_t *__restrict__ keys, u
     return k != ~0ull && (i == 0 || keys[i - 1] != k);
 }
 
-__global__ void __launch_bounds__(kTileThreads)
-    k_unique_count(const uint64_t *__restrict__ keys, uint64_t M, uint32_t *__restrict__ counts) {
-    __shared__ uint64_t s_red[kTileThreads / 32];
-    uint64_t t0 = (uint64_t)blockIdx.x * kTileItems;
-    uint64_t c = 0;
-    for (int k = 0; k < kItemsPerThread; k++) {
-        uint64_t i = t0 + (uint64_t)k * kTileThreads + threadIdx.x;
-        if (i < M) c += unique_flag(keys, i);
-    }
-    c = block_sum_u64(c, s_red);
-    if (threadIdx.x == 0) counts[blockIdx.x] = (uint32_t)c;
-}
-
+// Single pass (no separate count kernel + scan): tiles take a ticket, publish their unique
+// count, and get the exclusive prefix of earlier tiles by decoupled look-back (one
+// warp, 32 predecessors per step).  The last tile writes the total m.
 // Also a2 (fused): the degrees of the cleaned graph.  A thread's unique keys are
 // consecutive in (min, max) order, so the min side takes one atomic per run of equal
 // mins, the max side one per key.
+constexpr uint64_t kUqAgg = 1ull << 62, kUqPre = 2ull << 62, kUqMask = (1ull << 62) - 1;
+__device__ __forceinline__ void uq_st(uint64_t *p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t uq_ld(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __global__ void __launch_bounds__(kTileThreads)
-    k_unique_scatter(const uint64_t *__restrict__ keys, uint64_t M,
-                     const uint64_t *__restrict__ offs, uint64_t *__restrict__ out, int b,
-                     uint32_t *__restrict__ deg) {
+    k_unique_scatter(const uint64_t *__restrict__ keys, uint64_t M, uint32_t *__restrict__ ticket,
+                     uint64_t *__restrict__ status, uint64_t *__restrict__ m_out,
+                     uint64_t *__restrict__ out, int b, uint32_t *__restrict__ deg) {
     __shared__ uint32_t s_scan[kTileThreads / 32];
-    uint64_t base = (uint64_t)blockIdx.x * kTileItems + (uint64_t)threadIdx.x * kItemsPerThread;
+    __shared__ uint32_t s_tile;
+    __shared__ uint64_t s_excl;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint64_t base = (uint64_t)tile * kTileItems + (uint64_t)threadIdx.x * kItemsPerThread;
     uint32_t f[kItemsPerThread];
     uint32_t c = 0;
 #pragma unroll
@@ -90,8 +95,32 @@ __global__ void __launch_bounds__(kTileThreads)
         f[k] = i < M ? unique_flag(keys, i) : 0u;
         c += f[k];
     }
-    uint32_t pos = block_exclusive_scan<SumOp>(c, s_scan);
-    uint64_t o = offs[blockIdx.x] + pos;
+    uint32_t total;
+    uint32_t pos = block_exclusive_scan<SumOp>(c, s_scan, &total);
+    if (threadIdx.x < 32) {   // warp 0: publish, look back, publish the inclusive prefix
+        const uint32_t lane = threadIdx.x;
+        if (lane == 0) uq_st(&status[tile], (tile == 0 ? kUqPre : kUqAgg) | total);
+        uint64_t excl = 0;
+        if (tile > 0) {
+            for (int64_t t = (int64_t)tile - 1;; t -= 32) {
+                const int64_t idx = t - (int64_t)lane;
+                uint64_t sw = idx >= 0 ? uq_ld(&status[idx]) : kUqPre;
+                while (__any_sync(0xffffffffu, (sw & ~kUqMask) == 0))
+                    if ((sw & ~kUqMask) == 0) sw = uq_ld(&status[idx]);
+                const uint32_t pre = __ballot_sync(0xffffffffu, (sw & kUqPre) != 0);
+                const int first = pre ? __ffs(pre) - 1 : 32;
+                excl += warp_sum_u64((int)lane <= first ? (sw & kUqMask) : 0ull);
+                if (pre) break;
+            }
+            if (lane == 0) uq_st(&status[tile], kUqPre | (excl + total));
+        }
+        if (lane == 0) {
+            s_excl = excl;
+            if ((uint64_t)(tile + 1) * kTileItems >= M) *m_out = excl + total;   // last tile
+        }
+    }
+    __syncthreads();
+    uint64_t o = s_excl + pos;
     const uint64_t mask = (1ull << b) - 1;
     uint32_t run_a = 0, run_n = 0;
 #pragma unroll
@@ -255,16 +284,15 @@ void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, cons
     TC_LAUNCHED(ctx);
     bool alt = radix_sort(ctx, keys, keys_alt, M, nullptr, 2 * b);
     uint64_t *sorted = alt ? keys_alt : keys, *E = alt ? keys : keys_alt;
-    uint32_t *counts = ctx.alloc<uint32_t>(tiles);
-    uint64_t *offs = ctx.alloc<uint64_t>(tiles + 1);
+    // status words [0, tiles), the ticket counter, and m (the unique-edge count) at the end
+    uint64_t *uq = ctx.alloc<uint64_t>(tiles + 2);
+    TC_CUDA(cudaMemsetAsync(uq, 0, (tiles + 2) * sizeof(uint64_t), ctx.stream));
     uint32_t *deg = ctx.alloc<uint32_t>(n);
     TC_CUDA(cudaMemsetAsync(deg, 0, n * sizeof(uint32_t), ctx.stream));
-    k_unique_count<<<tiles, kTileThreads, 0, ctx.stream>>>(sorted, M, counts);
+    uint64_t *m_dev = uq + tiles + 1;
+    k_unique_scatter<<<tiles, kTileThreads, 0, ctx.stream>>>(sorted, M, (uint32_t *)(uq + tiles), uq,
+                                                             m_dev, E, b, deg);
     TC_LAUNCHED(ctx);
-    scan_exclusive(ctx, counts, offs, tiles);
-    k_unique_scatter<<<tiles, kTileThreads, 0, ctx.stream>>>(sorted, M, offs, E, b, deg);
-    TC_LAUNCHED(ctx);
-    uint64_t *m_dev = offs + tiles;
     if (tm) tm->end(kClean);
 
     if (tm) tm->begin(kOrient);
