@@ -881,24 +881,30 @@ template <int CM>
 static void launch_all(Ctx &ctx, const Oriented &g, const Bins &bins, uint64_t *total,
                        const Credit &cr) {
     int grid = ctx.persistent_grid(8);
+    // The bitmap hub kernel (most of the work) goes first on the call's stream; the
+    // independent warp-owner / SHORT / MERGE / SEARCH kernels run on a side stream and
+    // fill the SMs the hub kernel's tail leaves idle (all add into the same total).
+#ifndef TC_NO_SIDE_STREAM
+    cudaStream_t s2 = ctx.side();
+#else
+    cudaStream_t s2 = ctx.stream;
+#endif
+    if (s2 != ctx.stream) ctx.fork(s2);   // the side work depends only on binning
     k_hash_cta<CM, true><<<ctx.persistent_grid(8), kIxThreads, 0, ctx.stream>>>(
         bins.tasks_bitmap, bins.ntasks_bitmap, bins.hp, total, cr);
     TC_LAUNCHED(ctx);
     k_hash_cta<CM, false><<<ctx.persistent_grid(8), kIxThreads, 0, ctx.stream>>>(
         bins.tasks_cta, bins.ntasks_cta, bins.hp, total, cr);
     TC_LAUNCHED(ctx);
-    k_hash_warp<CM><<<grid, kIxThreads, 0, ctx.stream>>>(bins.tasks_warp, bins.ntasks_warp, bins.hp,
-                                                          total, cr);
+    k_hash_warp<CM><<<grid, kIxThreads, 0, s2>>>(bins.tasks_warp, bins.ntasks_warp, bins.hp, total, cr);
     TC_LAUNCHED(ctx);
-    k_merge<CM><<<grid, kIxThreads, 0, ctx.stream>>>(bins.edges[1], bins.count + 1, g.off, g.col,
-                                                     total, cr);
+    k_merge<CM><<<grid, kIxThreads, 0, s2>>>(bins.edges[1], bins.count + 1, g.off, g.col, total, cr);
     TC_LAUNCHED(ctx);
-    k_search<CM><<<grid, kIxThreads, 0, ctx.stream>>>(bins.edges[2], bins.count + 2, g.off, g.col,
-                                                      total, cr);
+    k_search<CM><<<grid, kIxThreads, 0, s2>>>(bins.edges[2], bins.count + 2, g.off, g.col, total, cr);
     TC_LAUNCHED(ctx);
-    k_short<CM><<<grid, kIxThreads, 0, ctx.stream>>>(bins.edges[0], bins.count + 0, g.off, g.col,
-                                                     total, cr);
+    k_short<CM><<<grid, kIxThreads, 0, s2>>>(bins.edges[0], bins.count + 0, g.off, g.col, total, cr);
     TC_LAUNCHED(ctx);
+    if (s2 != ctx.stream) ctx.join(s2);
 }
 
 void intersect_all(Ctx &ctx, const Oriented &g, const Bins &bins, uint64_t *total_dev,

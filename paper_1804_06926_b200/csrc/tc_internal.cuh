@@ -70,6 +70,33 @@ struct Ctx {
     ~Ctx() { release(); }
     // Grid for a persistent (grid-stride) kernel: `per_sm` resident CTAs per SM.
     int persistent_grid(int per_sm) const { return num_sms * per_sm; }
+
+    // A second (non-blocking) stream for independent kernels, cached per thread and
+    // device, with fork / join events: work on it starts after everything enqueued on
+    // `stream` so far, and `stream` waits for it at join().
+    cudaStream_t side() {
+        static thread_local cudaStream_t s[64] = {};
+        static thread_local cudaEvent_t e[64][2] = {};
+        int d = device >= 0 && device < 64 ? device : 0;
+        if (!s[d]) {
+            if (cudaStreamCreateWithFlags(&s[d], cudaStreamNonBlocking) != cudaSuccess ||
+                cudaEventCreateWithFlags(&e[d][0], cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&e[d][1], cudaEventDisableTiming) != cudaSuccess)
+                throw Error{TC_ECUDA, "side stream / event creation failed"};
+        }
+        ev_fork = e[d][0];
+        ev_join = e[d][1];
+        return s[d];
+    }
+    void fork(cudaStream_t s2) {
+        if (cudaEventRecord(ev_fork, stream) != cudaSuccess || cudaStreamWaitEvent(s2, ev_fork, 0) != cudaSuccess)
+            throw Error{TC_ECUDA, "fork failed"};
+    }
+    void join(cudaStream_t s2) {
+        if (cudaEventRecord(ev_join, s2) != cudaSuccess || cudaStreamWaitEvent(stream, ev_join, 0) != cudaSuccess)
+            throw Error{TC_ECUDA, "join failed"};
+    }
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 // ------------------------------------------------------------------ device helpers
