@@ -499,7 +499,10 @@ struct QuadDesc {
 };
 
 // Probe slots are aligned groups of kSlot elements of col+ (kSlot / 4 128-bit loads).
-constexpr int kSlotShift = 3;
+#ifndef TC_SLOT_SHIFT
+#define TC_SLOT_SHIFT 3
+#endif
+constexpr int kSlotShift = TC_SLOT_SHIFT;
 constexpr int kSlot = 1 << kSlotShift;
 
 __device__ __forceinline__ void put_desc(const QuadDesc &d, uint32_t i, uint32_t lo, uint32_t hi,
