@@ -164,7 +164,9 @@ tc_status tc_count_ex(uint64_t n, uint64_t m, const uint64_t *row_offsets,
 
 /* Multi-GPU shard: every rank passes the SAME graph; the library
  * runs the (replicated) preprocessing, splits source vertices into `world`
- * contiguous-in-order groups of equal estimated work sum_{v in N+(u)} (1 + min(|N+(u) after v|, d+v))
+ * contiguous-in-order groups of equal estimated work
+ * sum_{v in N+(u)} (c + min(|N+(u) after v|, d+v)), c = 128 (the HASH probes plus a fixed
+ * per-edge cost)
  * (prefix sum over sources, no communication), and counts only triangles whose
  * lowest-rank vertex falls in rank `rank`'s group.  partial_dev (device, 1
  * entry) is OVERWRITTEN with this rank's partial count; per_vertex_partial

@@ -16,7 +16,7 @@
 // order (so grouped by u) by a tile scan.  Owner x's entries = in-list ++ out-part.
 //
 // Multi-GPU: sources are split into `world` groups by an exclusive
-// prefix of per-source work w(u) = sum_{v in N+(u)} (1 + min(|N+(u) after v|, d+v)); a rank keeps
+// prefix of per-source work w(u) = sum_{v in N+(u)} (c + min(|N+(u) after v|, d+v)); a rank keeps
 // only the edges whose source is in its group.  The split needs no communication.
 #include "block_scan.cuh"
 #include "tc_internal.cuh"
@@ -385,8 +385,13 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
                bins.count + 11, bins.tasks_bitmap, bins.ntasks_bitmap);
 }
 
-// Per-source work estimate w(u) = sum_{v in N+(u)} (1 + min(|N+(u) after v|, d+v)) -- the
-// probe work the HASH kernels will do for u's edges -- then its exclusive prefix.
+// Per-source work estimate w(u) = sum_{v in N+(u)} (c + min(|N+(u) after v|, d+v)) -- the
+// probe work the HASH kernels will do for u's edges plus a fixed per-edge cost c -- then
+// its exclusive prefix.
+#ifndef TC_WORK_EDGE_COST
+#define TC_WORK_EDGE_COST 128  // fixed cost of an edge (descriptor, partial slots, table builds), in probes;
+                               // calibrated on per-rank a6 times
+#endif
 __global__ void k_work(const uint64_t *__restrict__ off, const uint32_t *__restrict__ col,
                        const uint32_t *__restrict__ dplus, uint64_t n, uint64_t *__restrict__ work) {
     for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
@@ -396,7 +401,7 @@ __global__ void k_work(const uint64_t *__restrict__ off, const uint32_t *__restr
         uint64_t w = 0;
         (void)du;
         // the HASH cost of edge k: min(|N+(u) after col[k]|, d+(col[k])) probes (+1 per edge)
-        for (uint64_t k = b; k < e; k++) w += 1 + min((uint32_t)(e - k - 1), dplus[col[k]]);
+        for (uint64_t k = b; k < e; k++) w += TC_WORK_EDGE_COST + min((uint32_t)(e - k - 1), dplus[col[k]]);
         work[u] = w;
     }
 }
