@@ -17,7 +17,8 @@ for it in range(6):
     if it >= 1 and (best is None or st["ms_total"] < best["ms_total"]): best = st
 print(f"@NAME@ T={T} total={best['ms_total']:.2f} clean={best['ms_clean']:.2f} orient={best['ms_orient']:.2f} bin={best['ms_bin']:.2f} ix={best['ms_intersect']:.2f}", flush=True)
 '''
-gexpr = {"s21": "G.rmat(21, 16)", "s22": "G.rmat(22, 16)", "cl": "G.chung_lu()", "road": "G.road_mesh()"}[graph]
+gexpr = {"s21": "G.rmat(21, 16)", "s22": "G.rmat(22, 16)", "s23": "G.rmat(23, 16)", "s24": "G.rmat(24, 16)",
+         "cl": "G.chung_lu()", "road": "G.road_mesh()", "clique": "G.clique_union()"}[graph]
 for nm in names:
     lib = os.path.join(ROOT, "paper_1804_06926_b200", "libtc_b200.so") if nm == "base" else \
         os.path.join(ROOT, "variants", nm, "libtc_b200.so")

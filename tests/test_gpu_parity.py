@@ -364,3 +364,22 @@ def test_clustering_rmat21_full():
     """Bench workload (R-MAT s21 ef16, raw arcs): every c(v) bit-exact."""
     g = G.rmat(21, 16)
     check_clustering(g)
+
+
+def test_hash_owners_beyond_bitmap_range():
+    """CTA hash owners whose rank span exceeds the 2^17-bit bitmap (n > 2^17), including
+    an owner with more elements than one hash chunk (TC_ID_ORDER puts a 1500-clique on
+    low ids: owner 0 has d+ = 1499 > kHashChunk)."""
+    n = 300_000
+    e = [(i, j) for i in range(1500) for j in range(i + 1, 1500)]        # K_1500 on 0..1499
+    top = list(range(290_000, 290_100))
+    e += [(10, v) for v in top] + [(a, b) for i, a in enumerate(top) for b in top[i + 1:]]
+    g = G.from_edges(n, e)
+    want = math.comb(1500, 3) + math.comb(101, 3)
+    for kw in (dict(id_order=True), dict(id_order=True, hub_min_dplus=2), dict()):
+        assert gpu_count(g.rowptr, g.col, **kw) == want, kw
+    # R-MAT with many CTA owners below the top window (hub_min_dplus small)
+    r = G.rmat(18, 16, seed=3)
+    T = O.count(r.n, r.rowptr, r.col)
+    for kw in (dict(hub_min_dplus=8), dict(hub_min_dplus=16, id_order=True), dict()):
+        assert gpu_count(r.rowptr, r.col, **kw) == T, kw
