@@ -167,6 +167,30 @@ def _timed(torch, flush, stream, fn, reps=3):
     return tot / reps, out
 
 
+def clean_input_ms(tc, torch, rp, cl, flush, stream, T):
+    """SURVEY §8(d)'s own definition of the headline ms: from a CLEAN symmetric CSR resident on
+    the device (TC_CLEAN | TC_SORTED: a1 skipped) to the count.  The clean CSR is prepared
+    outside the timed region from the library's oriented CSR (torch sort: input plumbing)."""
+    n = rp.numel() - 1
+    off, colp = tc.orient(rp, cl)
+    src = torch.repeat_interleave(torch.arange(n, device=rp.device), off[1:] - off[:-1])
+    dst = colp.to(torch.int64)
+    b = max(1, (n - 1).bit_length())
+    keys = torch.cat([(src << b) | dst, (dst << b) | src])
+    keys, _ = torch.sort(keys)
+    s2, d2 = keys >> b, keys & ((1 << b) - 1)
+    crp = torch.zeros(n + 1, dtype=torch.int64, device=rp.device)
+    crp[1:] = torch.cumsum(torch.bincount(s2, minlength=n), 0)
+    ccl = d2.to(torch.int32).contiguous()
+    del off, colp, src, dst, keys, s2, d2
+    ms, (Tc, st) = _timed(torch, flush, stream,
+                          lambda: tc.count_ex(crp, ccl, clean=True, sorted_rows=True, with_stats=True))
+    assert Tc == T
+    return {"ms_per_call": ms, "edges_per_s": st["m_undirected"] / (ms * 1e-3),
+            "phases_ms": {k: st[k] for k in ("ms_orient", "ms_bin", "ms_intersect")},
+            "call": "tc_count_ex(TC_CLEAN | TC_SORTED) on the symmetric sorted CSR (a2-a7; a1 skipped)"}
+
+
 def next_rows_23(tc, torch, np, graphgen, rp, cl, flush, stream, m, T, count_ms):
     """NEXT-2 / NEXT-3 timed through their C-ABI calls, device pointers."""
     rows = {}
@@ -337,6 +361,10 @@ def main():
                      "survey_B_alg": {"bytes": b_alg, "model": "4W + 16m (SURVEY.md 8(d), merge-based)",
                                       "achieved": achieved_alg, "frac": achieved_alg / peak,
                                       "frac_incl_binning": b_alg / ((ix_ms + bin_ms) * 1e-3) / 1e9 / world / peak},
+                     "survey_B_stage": {"bytes": 4 * (m + st["work_stage"]) + 16 * m,
+                                        "model": "4(m + sum d-(v) d+(v)) + 16m (SURVEY.md 8(d))",
+                                        "frac": (4 * (m + st["work_stage"]) + 16 * m)
+                                                / (ix_ms * 1e-3) / 1e9 / world / peak},
                      "work_W": st["work_W"], "work_probe": st["work_probe"],
                      "table_loads": st["table_loads"]},
         "gpu_launches": launches,
@@ -350,6 +378,9 @@ def main():
             if tr:
                 line["roofline"]["traffic"] = tr["dram_bytes_per_launch"]
                 line["roofline"]["traffic_source"] = tr["source"]
+                for k in ("bitmap_kernel_l2_hit_pct", "bitmap_kernel_dram_throughput_pct"):
+                    if tr.get(k) is not None:
+                        line["roofline"][k] = tr[k]
         except (OSError, ValueError):
             pass
     if world == 1 and not args.no_next:
@@ -371,6 +402,7 @@ def main():
             "transitivity": summ["transitivity"], "avg_clustering": summ["avg_clustering"],
             "wedges": summ["wedges"],
             "call": "tc_clustering (device pointers): count with per-vertex t(v) + local c(v) for all n"}}
+        line["survey_clean_input"] = clean_input_ms(tc, torch, rp, cl, flush, stream, T_total)
         line["next_rows"].update(next_rows_23(tc, torch, np, graphgen, rp, cl, flush, stream, m,
                                               T_total, ms))
     if world == 1 and not args.no_cpu_baseline:

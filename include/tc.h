@@ -146,6 +146,7 @@ typedef struct {
     uint64_t pruned_edges;    /* TC_PRUNE: undirected edges deleted                          */
     uint64_t prune_rounds;    /* TC_PRUNE: rounds executed (fixed-point mode: including the
                                  final round that deleted nothing)                         */
+    uint64_t work_stage;      /* sum_v d-(v) d+(v): SURVEY 8(d)'s B_stage = 4(m + this) + 16m  */
 } tc_stats;
 
 /* Fill *opt with the defaults (auto variant selection, default stream). */

@@ -58,7 +58,8 @@ class Stats(ctypes.Structure):
                 ("kernel_launches", ctypes.c_uint64), ("h2d_bytes", ctypes.c_uint64),
                 ("d2h_bytes", ctypes.c_uint64), ("table_loads", ctypes.c_uint64),
                 ("bytes_hash", ctypes.c_uint64), ("ms_prune", ctypes.c_double),
-                ("pruned_edges", ctypes.c_uint64), ("prune_rounds", ctypes.c_uint64)]
+                ("pruned_edges", ctypes.c_uint64), ("prune_rounds", ctypes.c_uint64),
+                ("work_stage", ctypes.c_uint64)]
 
 
 class ClusteringSummary(ctypes.Structure):

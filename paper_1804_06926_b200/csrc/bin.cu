@@ -46,10 +46,7 @@ __device__ __forceinline__ void warp_append(bool take, uint64_t *counter, uint2 
 // (32 consecutive edges) and the tile's out-part count (tcount) replace a per-edge
 // range array.  SHORT / MERGE / SEARCH edges are appended to their bins.  Also accumulates
 // the work statistics.
-#ifndef TC_EDGES_MINBLOCKS
-#define TC_EDGES_MINBLOCKS 1
-#endif
-__global__ void __launch_bounds__(kTileThreads, TC_EDGES_MINBLOCKS)
+__global__ void __launch_bounds__(kTileThreads)
     k_edges(HashParams hp, const uint64_t *__restrict__ m_dev, uint32_t *__restrict__ ulo,
             uint32_t *__restrict__ obits, uint32_t *__restrict__ tcount,
             uint2 *__restrict__ b_short, uint2 *__restrict__ b_merge, uint2 *__restrict__ b_search,
@@ -311,6 +308,9 @@ static void make_tasks(Ctx &ctx, uint64_t n, uint64_t cap, const uint32_t *owner
     ntasks = toff + n;
 }
 
+__global__ void k_stage_work(const uint64_t *__restrict__ in_off, const uint32_t *__restrict__ dplus,
+                             uint64_t n, uint64_t *__restrict__ out);
+
 void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
     uint64_t cap = g.m_cap, n = g.n;
     bins.cap = cap;
@@ -383,6 +383,22 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
                bins.count + 11, bins.tasks_cta, bins.ntasks_cta);
     make_tasks(ctx, n, cap, bins.owners_bitmap, bins.count + 10, bins.pcnt, g.dplus, kCtaTaskLists,
                bins.count + 11, bins.tasks_bitmap, bins.ntasks_bitmap);
+    if (p.want_stats) {
+        k_stage_work<<<ctx.persistent_grid(2), 256, 0, ctx.stream>>>(g.in_off, g.dplus, n, bins.count + 12);
+        TC_LAUNCHED(ctx);
+    }
+}
+
+// Stats only: sum_v d-(v) d+(v), for SURVEY §8(d)'s B_stage = 4 (m + sum d- d+) + 16 m (the
+// bytes of a method that stages each source list once per in-edge).
+__global__ void k_stage_work(const uint64_t *__restrict__ in_off, const uint32_t *__restrict__ dplus,
+                             uint64_t n, uint64_t *__restrict__ out) {
+    uint64_t acc = 0;
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * blockDim.x)
+        acc += (in_off[v + 1] - in_off[v]) * (uint64_t)dplus[v];
+    acc = warp_sum_u64(acc);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd((unsigned long long *)out, (unsigned long long)acc);
 }
 
 // Per-source work estimate w(u) = sum_{v in N+(u)} (c + min(|N+(u) after v|, d+v)) -- the

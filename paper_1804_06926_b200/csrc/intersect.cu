@@ -374,20 +374,9 @@ __device__ __forceinline__ uint32_t table_contains(uint32_t tab, int bits, uint3
     return table_contains_slow(tab, (1u << (bits - 2)) - 1u, b, w);
 }
 
-// Probe-list loads (read-only path).  TC_PROBE_NA: hint L1 not to allocate them.
-#ifndef TC_PROBE_NA
-#define TC_PROBE_NA 0
-#endif
-__device__ __forceinline__ uint4 ld_probe(const uint4 *p) {
-#if TC_PROBE_NA
-    uint4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-    return v;
-#else
-    return __ldg(p);
-#endif
-}
+// Probe-list loads: read-only path, L1-allocating (48 % L1 hits at s21; the
+// L1::no_allocate hint measured slower).
+__device__ __forceinline__ uint4 ld_probe(const uint4 *p) { return __ldg(p); }
 
 // Keep a shared-memory base address in a register (stops the compiler from
 // re-deriving it from SR_CgaCtaId at every use).
@@ -887,11 +876,7 @@ static void launch_all(Ctx &ctx, const Oriented &g, const Bins &bins, uint64_t *
     // The bitmap hub kernel (most of the work) goes first on the call's stream; the
     // independent warp-owner / SHORT / MERGE / SEARCH kernels run on a side stream and
     // fill the SMs the hub kernel's tail leaves idle (all add into the same total).
-#ifndef TC_NO_SIDE_STREAM
     cudaStream_t s2 = ctx.side();
-#else
-    cudaStream_t s2 = ctx.stream;
-#endif
     if (s2 != ctx.stream) ctx.fork(s2);   // the side work depends only on binning
     k_hash_cta<CM, true><<<ctx.persistent_grid(8), kIxThreads, 0, ctx.stream>>>(
         bins.tasks_bitmap, bins.ntasks_bitmap, bins.hp, total, cr);

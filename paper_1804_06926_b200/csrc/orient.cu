@@ -11,8 +11,8 @@
 // rank(u) < rank(v) <=> newid[u] < newid[v].  The oriented CSR is built in the
 // new id space (sources by a stable radix sort of the oriented pairs), so a
 // hub's N+ lies in the short id range above it (bitmap staging in a6) and the
-// hot lists are contiguous at the end of col+.  Rows are put in ascending order
-// (a4, segmented sort) only when a merge/search variant needs them.
+// hot lists are contiguous at the end of col+.  Every row comes out ascending (a4):
+// the two-key LSD sort (target, then source) that builds the CSR also sorts its rows.
 #include "block_scan.cuh"
 #include "tc_internal.cuh"
 
@@ -268,12 +268,11 @@ static void pairs_to_csr(Ctx &ctx, uint64_t n, uint64_t cap, uint32_t *okey, uin
     out.pidx = rv;
     out.m_dev = m_dev;
     out.m_cap = cap;
-    out.rows_sorted = true;
     if (tm) tm->end(kOrient);
 }
 
 void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
-                  bool need_sorted, uint32_t segsort_block_max, Oriented &out, Timer *tm,
+                  Oriented &out, Timer *tm,
                   PruneInfo &prune, bool id_order) {
     int b = id_bits(n);
     uint32_t tiles = (uint32_t)((M + kTileItems - 1) / kTileItems);
@@ -315,8 +314,6 @@ void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, cons
     TC_LAUNCHED(ctx);
     k_dminus<<<grid, 256, 0, ctx.stream>>>(deg, out.newid, dplus, n, dminus);
     TC_LAUNCHED(ctx);
-    (void)need_sorted;
-    (void)segsort_block_max;
     pairs_to_csr(ctx, n, M, okey, oval, dplus, dminus, m_dev, out, tm, phist,
                  phist + ppasses * kHistDigits);
 }
@@ -381,7 +378,7 @@ __global__ void __launch_bounds__(kTileThreads)
 }
 
 void orient_clean(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
-                  bool need_sorted, uint32_t segsort_block_max, Oriented &out, Timer *tm,
+                  Oriented &out, Timer *tm,
                   PruneInfo &prune, bool id_order) {
     uint32_t tiles = (uint32_t)((M + kTileItems - 1) / kTileItems);
     int grid = ctx.persistent_grid(8);
@@ -412,8 +409,6 @@ void orient_clean(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, cons
     TC_LAUNCHED(ctx);
     k_dminus<<<grid, 256, 0, ctx.stream>>>(deg, out.newid, dplus, n, dminus);
     TC_LAUNCHED(ctx);
-    (void)need_sorted;
-    (void)segsort_block_max;
     pairs_to_csr(ctx, n, cap, okey, oval, dplus, dminus, offs + tiles, out, tm);
 }
 

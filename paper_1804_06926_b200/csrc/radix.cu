@@ -295,11 +295,7 @@ static void radix_impl(Ctx &ctx, const K *kin0, const uint32_t *vin0, K *kA, K *
     uint64_t *doff = ctx.alloc<uint64_t>((uint64_t)passes * kDigits);
     uint32_t *tickets = ctx.alloc<uint32_t>(passes);
     // 32-bit status words when every digit prefix (<= capacity) fits in 30 bits
-#ifndef TC_RS_FORCE_WIDE
     const bool narrow = capacity < (1ull << 30);
-#else
-    const bool narrow = false;
-#endif
     const size_t sw = narrow ? sizeof(uint32_t) : sizeof(uint64_t);
     void *status = ctx.alloc<uint64_t>(((uint64_t)tiles * kDigits * sw + 7) / 8);  // reused per pass
     TC_CUDA(cudaMemsetAsync(tickets, 0, passes * sizeof(uint32_t), ctx.stream));

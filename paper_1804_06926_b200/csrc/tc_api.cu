@@ -187,9 +187,8 @@ static void run(Call &c) {
     uint64_t *pin = pinned_scratch();
     if (c.stats) memset(pin, 0, 32 * sizeof(uint64_t));
 
-    // Rows of N+ are always put in ascending order: the merge / search variants need
+    // Rows of N+ are always put in ascending order (a4): the merge / search variants need
     // it, and the HASH ranges probe only the part of N+(a) after b.
-    const bool need_sorted = true;
 
     PruneInfo prune;
     prune.enabled = c.flags & TC_PRUNE;
@@ -197,10 +196,10 @@ static void run(Call &c) {
     if (c.n > 0 && c.M > 0) {
         Oriented g;
         if (c.flags & TC_CLEAN)
-            orient_clean(ctx, c.n, c.M, rowptr, col, need_sorted, c.opt.segsort_block_max, g, tm,
+            orient_clean(ctx, c.n, c.M, rowptr, col, g, tm,
                          prune, c.flags & TC_ID_ORDER);
         else
-            orient_dirty(ctx, c.n, c.M, rowptr, col, need_sorted, c.opt.segsort_block_max, g, tm,
+            orient_dirty(ctx, c.n, c.M, rowptr, col, g, tm,
                          prune, c.flags & TC_ID_ORDER);
         if (c.stats && prune.m_before)
             TC_CUDA(cudaMemcpyAsync(pin + 24, prune.m_before, sizeof(uint64_t),
@@ -227,6 +226,7 @@ static void run(Call &c) {
         if (tm) tm->begin(kBin);
         BinParams bp;
         bp.edge_ids = c.mode == kSupport;
+        bp.want_stats = c.stats != nullptr;
         bp.short_max = c.opt.short_max;
         bp.skew_ratio = c.opt.skew_ratio;
         bp.hub_min = c.opt.hub_min_dplus;
@@ -234,7 +234,6 @@ static void run(Call &c) {
         bp.rank = c.rank;
         bp.world = c.world;
         bp.work_prefix = nullptr;
-        bp.work_chunk = 0;
         if (c.world > 1) {
             uint64_t *prefix = ctx.alloc<uint64_t>(c.n + 1);
             work_prefix(ctx, g, prefix);
@@ -371,6 +370,7 @@ static void run(Call &c) {
         st.hub_sources = pin[9] + pin[10];
         st.max_dplus = pin[7];
         st.table_loads = pin[11];
+        st.work_stage = pin[12];
         // bytes the HASH method reads in a6: probed elements + one 8-byte range per probe
         // entry (<= 2 per edge, 1 for ~96%) + the owners' lists for the table builds
         st.bytes_hash = 4 * st.work_probe + 8 * st.bin_edges[3] + 4 * st.table_loads;

@@ -191,14 +191,7 @@ __device__ __forceinline__ void tile_rows(const uint64_t *__restrict__ rowptr, u
 
 // Digit width of an LSD radix sort over `bits` key bits: 7 when 7-bit digits need no
 // more passes than 8-bit ones (fewer ballots per rank, half the look-back digits), else 8.
-inline int radix_digit_bits(int bits) {
-#ifdef TC_RS_FORCE_DB8
-    (void)bits;
-    return 8;
-#else
-    return (bits + 6) / 7 == (bits + 7) / 8 ? 7 : 8;
-#endif
-}
+inline int radix_digit_bits(int bits) { return (bits + 6) / 7 == (bits + 7) / 8 ? 7 : 8; }
 
 // ------------------------------------------------------------------ fused digit histograms
 // Producers of radix-sort keys count the 8-bit digits of every pass on the fly:
@@ -258,7 +251,7 @@ void radix_sort_pairs_from(Ctx &ctx, const uint32_t *keys_in, const uint32_t *va
 struct Oriented {
     uint64_t n = 0;
     uint64_t *off = nullptr;     // off+[n+1]   (indexed by new id)
-    uint32_t *col = nullptr;     // col+[m]     (new ids; ascending per row iff rows_sorted)
+    uint32_t *col = nullptr;     // col+[m]     (new ids; every row ascending)
     uint32_t *dplus = nullptr;   // d+[n]       (indexed by new id)
     uint64_t *in_off = nullptr;  // transposed CSR: in-lists N-(x) (edge-list order)
     uint32_t *in_src = nullptr;
@@ -267,7 +260,6 @@ struct Oriented {
     uint32_t *newid = nullptr;   // input id -> new id
     uint64_t *m_dev = nullptr;   // device scalar m
     uint64_t m_cap = 0;          // capacity bound for m (host-known)
-    bool rows_sorted = false;
 };
 
 // Phase timer: CUDA events on the call's stream, read after the final sync.
@@ -315,13 +307,13 @@ void prune_pairs(Ctx &ctx, uint64_t n, int b, uint32_t rounds, uint64_t *&E, uin
 void prune_csr(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
                uint32_t rounds, uint32_t *&deg, PruneInfo &info);
 
-// a1 (dirty input) + a2 + a3: raw CSR -> oriented relabelled CSR (+ a4 if need_sorted).
+// a1 (dirty input) + a2 + a3 + a4: raw CSR -> oriented relabelled CSR, rows ascending.
 void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
-                  bool need_sorted, uint32_t segsort_block_max, Oriented &out, Timer *tm,
+                  Oriented &out, Timer *tm,
                   PruneInfo &prune, bool id_order);
-// a2 + a3 for clean symmetric input (+ a4 if need_sorted).
+// a2 + a3 + a4 for clean symmetric input.
 void orient_clean(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
-                  bool need_sorted, uint32_t segsort_block_max, Oriented &out, Timer *tm,
+                  Oriented &out, Timer *tm,
                   PruneInfo &prune, bool id_order);
 // The oriented CSR in INPUT ids with ascending rows (tc_orient output).
 // With pay_in (m entries in CSR order, e.g. edge supports) also pay_out[k] = the
@@ -385,7 +377,8 @@ struct Bins {
     uint64_t *count = nullptr;  // device: [0..3] SHORT/MERGE/SEARCH/HASH edges, [4] W,
                                 // [5] sum min(|N+(u) after v|, d+(v)), [6] skipped, [7] max d+,
                                 // [8] warp owners, [9] CTA hash owners, [10] CTA bitmap owners,
-                                // [11] table-build loads (sum over tasks of d+(owner))
+                                // [11] table-build loads (sum over tasks of d+(owner)),
+                                // [12] sum_v d-(v) d+(v) (stats only)
     uint32_t *pcnt = nullptr;   // per owner: probe entries
     uint32_t *owners_warp = nullptr;   // owners with d+ < hub_min: tables of one warp
     uint32_t *owners_cta = nullptr;    // larger owners ("hubs"): tables of one CTA
@@ -408,8 +401,8 @@ struct BinParams {
     int force;
     int rank, world;
     const uint64_t *work_prefix;  // exclusive prefix of per-source work (world > 1)
-    uint64_t work_chunk;          // unused (computed on the device)
     bool edge_ids = false;        // out-part entries record their edge's CSR index (kCmEdge)
+    bool want_stats = false;      // also count sum_v d-(v) d+(v) into count[12]
 };
 
 void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins);

@@ -45,9 +45,12 @@ if full:
     drows = list(csv.reader(io.StringIO(det)))
     h = drows[0]
     K, M, V, U = (h.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
+    top = {}   # the dominant (bitmap) kernel's L2 hit rate and DRAM throughput
     for r in drows[1:]:
         if r[M] in keep:
             lines.append(f"{r[K].split('(')[0][:28]:28s} {r[M]:36s} {r[V]:>18s} {r[U]}")
+        if "k_hash_cta<0, 1>" in r[K] and r[M] in ("L2 Hit Rate", "DRAM Throughput") and r[M] not in top:
+            top[r[M]] = float(r[V].replace(",", ""))
     rr = list(csv.reader(io.StringIO(raw)))
     h = rr[0]
     traffic = 0.0
@@ -70,5 +73,7 @@ if full:
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     d = json.load(open(tf)) if os.path.exists(tf) else {}
     d[workload] = {"dram_bytes_per_launch": traffic, "source": f"profiles/{tag}_intersect_full.txt "
-                   "(sum of dram__bytes_read+write over the intersection kernels of one step)"}
+                   "(sum of dram__bytes_read+write over the intersection kernels of one step)",
+                   "bitmap_kernel_l2_hit_pct": top.get("L2 Hit Rate"),
+                   "bitmap_kernel_dram_throughput_pct": top.get("DRAM Throughput")}
     json.dump(d, open(tf, "w"), indent=1)

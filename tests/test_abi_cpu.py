@@ -47,7 +47,7 @@ def test_struct_layout(lib):
     assert o.short_max == 32 and o.skew_ratio == 0 and o.hub_min_dplus == 64
     assert o.force_variant == -1 and o.segsort_block_max == 8192
     assert o.prune_rounds == 0 and not any(o.reserved)
-    assert ctypes.sizeof(tc.Stats) == 7 * 8 + 18 * 8
+    assert ctypes.sizeof(tc.Stats) == 7 * 8 + 19 * 8
     assert ctypes.sizeof(tc.ClusteringSummary) == 32
 
 

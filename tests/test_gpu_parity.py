@@ -175,6 +175,7 @@ def test_stats_consistent():
     assert st["max_dplus"] == st_o["max_dplus"]
     assert st["bytes_alg"] == 4 * st_o["W"] + 16 * st_o["m"]
     assert sum(st["bin_edges"]) + st["skipped_edges"] == st_o["m"]
+    assert st["work_stage"] == st_o["sum_dminus_dplus"]          # SURVEY 8(d) B_stage
     assert st["kernel_launches"] > 0
 
 
