@@ -13,6 +13,8 @@
 // hub's N+ lies in the short id range above it (bitmap staging in a6) and the
 // hot lists are contiguous at the end of col+.  Every row comes out ascending (a4):
 // the two-key LSD sort (target, then source) that builds the CSR also sorts its rows.
+#include <algorithm>
+
 #include "block_scan.cuh"
 #include "tc_internal.cuh"
 
@@ -326,55 +328,95 @@ __global__ void k_deg_rowptr(const uint64_t *__restrict__ rowptr, uint64_t n,
         deg[u] = (uint32_t)(rowptr[u + 1] - rowptr[u]);
 }
 
-__global__ void __launch_bounds__(kTileThreads)
-    k_orient_count(const uint64_t *__restrict__ rowptr, const uint32_t *__restrict__ col,
-                   uint64_t n, uint64_t M, const uint32_t *__restrict__ deg,
-                   uint32_t *__restrict__ counts) {
-    __shared__ uint32_t s_row[kTileItems];
-    __shared__ uint32_t s_scan[kTileThreads / 32];
-    __shared__ uint64_t s_red[kTileThreads / 32];
-    uint64_t t0 = (uint64_t)blockIdx.x * kTileItems;
-    uint32_t len = (uint32_t)min((uint64_t)kTileItems, M - t0);
-    tile_rows(rowptr, n, t0, len, s_row, s_scan);
-    uint64_t c = 0;
-    for (uint32_t i = threadIdx.x; i < len; i += kTileThreads)
-        c += rank_less(deg, s_row[i], col[t0 + i]);
-    c = block_sum_u64(c, s_red);
-    if (threadIdx.x == 0) counts[blockIdx.x] = (uint32_t)c;
-}
-
+// Clean input: one persistent pass (no count kernel + scan).  Tiles of arcs are taken by
+// ticket; each keeps the arcs with rank(u) < rank(v), gets its output offset by decoupled
+// look-back (status words as in k_unique_scatter), writes the oriented pairs in rank ids,
+// counts d+ (one atomic per run of equal sources) and the digit histograms of both radix
+// sorts that follow (flushed once per block).
 __global__ void __launch_bounds__(kTileThreads)
     k_orient_emit(const uint64_t *__restrict__ rowptr, const uint32_t *__restrict__ col,
                   uint64_t n, uint64_t M, const uint32_t *__restrict__ deg,
-                  const uint32_t *__restrict__ newid, const uint64_t *__restrict__ offs,
+                  const uint32_t *__restrict__ newid, uint32_t *__restrict__ ticket,
+                  uint64_t *__restrict__ status, uint64_t *__restrict__ m_out,
                   uint32_t *__restrict__ okey, uint32_t *__restrict__ oval,
-                  uint32_t *__restrict__ dplus) {
+                  uint32_t *__restrict__ dplus, uint32_t *__restrict__ hist_key,
+                  uint32_t *__restrict__ hist_val, int passes, int db) {
     __shared__ uint32_t s_row[kTileItems];
     __shared__ uint32_t s_scan[kTileThreads / 32];
-    uint64_t t0 = (uint64_t)blockIdx.x * kTileItems;
-    uint32_t len = (uint32_t)min((uint64_t)kTileItems, M - t0);
-    tile_rows(rowptr, n, t0, len, s_row, s_scan);
-    uint32_t i0 = threadIdx.x * kItemsPerThread;
-    uint32_t f[kItemsPerThread], v[kItemsPerThread], c = 0;
+    __shared__ uint32_t s_tile;
+    __shared__ uint64_t s_excl;
+    __shared__ RsHist<4> s_hk, s_hv;
+    s_hk.clear();
+    s_hv.clear();
+    const uint64_t tiles = (M + kTileItems - 1) / kTileItems;
+    while (true) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+        __syncthreads();
+        const uint32_t tile = s_tile;
+        if (tile >= tiles) break;
+        const uint64_t t0 = (uint64_t)tile * kTileItems;
+        const uint32_t len = (uint32_t)min((uint64_t)kTileItems, M - t0);
+        tile_rows(rowptr, n, t0, len, s_row, s_scan);
+        const uint32_t i0 = threadIdx.x * kItemsPerThread;
+        uint32_t f[kItemsPerThread], v[kItemsPerThread], c = 0;
 #pragma unroll
-    for (int k = 0; k < kItemsPerThread; k++) {
-        uint32_t i = i0 + k;
-        v[k] = i < len ? col[t0 + i] : 0u;
-        f[k] = i < len ? (uint32_t)rank_less(deg, s_row[i], v[k]) : 0u;
-        c += f[k];
-    }
-    uint32_t pos = block_exclusive_scan<SumOp>(c, s_scan);
-    uint64_t base = offs[blockIdx.x] + pos;
-#pragma unroll
-    for (int k = 0; k < kItemsPerThread; k++) {
-        if (f[k]) {
-            uint32_t s = newid[s_row[i0 + k]], t = newid[v[k]];
-            okey[base] = s;
-            oval[base] = t;
-            atomicAdd(&dplus[s], 1u);
-            base++;
+        for (int k = 0; k < kItemsPerThread; k++) {
+            const uint32_t i = i0 + k;
+            v[k] = i < len ? col[t0 + i] : 0u;
+            f[k] = i < len ? (uint32_t)rank_less(deg, s_row[i], v[k]) : 0u;
+            c += f[k];
         }
+        uint32_t total;
+        const uint32_t pos = block_exclusive_scan<SumOp>(c, s_scan, &total);
+        if (threadIdx.x < 32) {   // warp 0: publish, look back, publish the inclusive prefix
+            const uint32_t lane = threadIdx.x;
+            if (lane == 0) uq_st(&status[tile], (tile == 0 ? kUqPre : kUqAgg) | total);
+            uint64_t excl = 0;
+            if (tile > 0) {
+                for (int64_t t = (int64_t)tile - 1;; t -= 32) {
+                    const int64_t idx = t - (int64_t)lane;
+                    uint64_t sw = idx >= 0 ? uq_ld(&status[idx]) : kUqPre;
+                    while (__any_sync(0xffffffffu, (sw & ~kUqMask) == 0))
+                        if ((sw & ~kUqMask) == 0) sw = uq_ld(&status[idx]);
+                    const uint32_t pre = __ballot_sync(0xffffffffu, (sw & kUqPre) != 0);
+                    const int first = pre ? __ffs(pre) - 1 : 32;
+                    excl += warp_sum_u64((int)lane <= first ? (sw & kUqMask) : 0ull);
+                    if (pre) break;
+                }
+                if (lane == 0) uq_st(&status[tile], kUqPre | (excl + total));
+            }
+            if (lane == 0) {
+                s_excl = excl;
+                if (tile + 1 == tiles) *m_out = excl + total;
+            }
+        }
+        __syncthreads();
+        uint64_t base = s_excl + pos;
+        uint32_t run_s = 0, run_n = 0;
+#pragma unroll
+        for (int k = 0; k < kItemsPerThread; k++) {
+            if (f[k]) {
+                const uint32_t sv = newid[s_row[i0 + k]], tv = newid[v[k]];
+                okey[base] = sv;
+                oval[base] = tv;
+                s_hk.add(sv, passes, db);
+                s_hv.add(tv, passes, db);
+                base++;
+                if (run_n && sv == run_s) {
+                    run_n++;
+                } else {
+                    if (run_n) atomicAdd(&dplus[run_s], run_n);
+                    run_s = sv;
+                    run_n = 1;
+                }
+            }
+        }
+        if (run_n) atomicAdd(&dplus[run_s], run_n);
     }
+    __syncthreads();
+    s_hk.flush(hist_key, passes);
+    s_hv.flush(hist_val, passes);
 }
 
 void orient_clean(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
@@ -394,22 +436,26 @@ void orient_clean(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, cons
     }
     const uint32_t *key = rank_key(ctx, n, deg, id_order);
     rank_permutation(ctx, n, key, out);
-    uint32_t *counts = ctx.alloc<uint32_t>(tiles);
-    uint64_t *offs = ctx.alloc<uint64_t>(tiles + 1);
-    k_orient_count<<<tiles, kTileThreads, 0, ctx.stream>>>(rowptr, col, n, M, key, counts);
-    TC_LAUNCHED(ctx);
-    scan_exclusive(ctx, counts, offs, tiles);
+    // status words [0, tiles), the ticket, m at the end; histograms of both pair sorts
+    uint64_t *st = ctx.alloc<uint64_t>(tiles + 2);
+    TC_CUDA(cudaMemsetAsync(st, 0, (tiles + 2) * sizeof(uint64_t), ctx.stream));
+    const int b = id_bits(n), pdb = radix_digit_bits(b), ppasses = (b + pdb - 1) / pdb;
+    uint32_t *phist = ctx.alloc<uint32_t>(2 * ppasses * kHistDigits);
+    TC_CUDA(cudaMemsetAsync(phist, 0, 2 * ppasses * kHistDigits * sizeof(uint32_t), ctx.stream));
     uint64_t cap = M / 2 + 1;
     uint32_t *okey = ctx.alloc<uint32_t>(cap), *oval = ctx.alloc<uint32_t>(cap);
     uint32_t *dplus = ctx.alloc<uint32_t>(n + 1), *dminus = ctx.alloc<uint32_t>(n + 1);
     TC_CUDA(cudaMemsetAsync(dplus, 0, (n + 1) * sizeof(uint32_t), ctx.stream));
     TC_CUDA(cudaMemsetAsync(dminus, 0, (n + 1) * sizeof(uint32_t), ctx.stream));
-    k_orient_emit<<<tiles, kTileThreads, 0, ctx.stream>>>(rowptr, col, n, M, key, out.newid, offs,
-                                                          okey, oval, dplus);
+    uint32_t egrid = (uint32_t)std::min<uint64_t>(tiles, (uint64_t)ctx.persistent_grid(4));
+    k_orient_emit<<<egrid, kTileThreads, 0, ctx.stream>>>(
+        rowptr, col, n, M, key, out.newid, (uint32_t *)(st + tiles), st, st + tiles + 1, okey, oval,
+        dplus, phist, phist + ppasses * kHistDigits, ppasses, pdb);
     TC_LAUNCHED(ctx);
     k_dminus<<<grid, 256, 0, ctx.stream>>>(deg, out.newid, dplus, n, dminus);
     TC_LAUNCHED(ctx);
-    pairs_to_csr(ctx, n, cap, okey, oval, dplus, dminus, offs + tiles, out, tm);
+    pairs_to_csr(ctx, n, cap, okey, oval, dplus, dminus, st + tiles + 1, out, tm, phist,
+                 phist + ppasses * kHistDigits);
 }
 
 // ------------------------------------------------------------------ back to original ids
