@@ -253,7 +253,9 @@ static void pairs_to_csr(Ctx &ctx, uint64_t n, uint64_t cap, uint32_t *okey, uin
     // 2) stable by source of T's index p (values = p, generated by the first pass),
     // reading T without modifying it; the last pass also gathers col+[e] = T.target[p]
     uint32_t *g_key = ctx.alloc<uint32_t>(cap), *g_val = ctx.alloc<uint32_t>(cap);
-    uint32_t *col = ctx.alloc<uint32_t>(cap);
+    // col+ is read by the a6 probes in aligned 8-element slots (two 16-byte loads): pad the
+    // allocation to whole slots so the last slot never reads past it (compute-sanitizer)
+    uint32_t *col = ctx.alloc<uint32_t>((cap + 7) / 8 * 8);
     uint32_t *rk, *rv;
     radix_sort_pairs_from(ctx, t_src, nullptr, f_key, g_key, f_val, g_val, cap, m_dev, b, &rk, &rv,
                           t_tgt, col, hist_src);
@@ -270,7 +272,7 @@ static void pairs_to_csr(Ctx &ctx, uint64_t n, uint64_t cap, uint32_t *okey, uin
     out.pidx = rv;
     out.m_dev = m_dev;
     out.m_cap = cap;
-    if (tm) tm->end(kOrient);
+    phase_end(tm, kOrient);
 }
 
 void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
@@ -278,7 +280,7 @@ void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, cons
                   PruneInfo &prune, bool id_order) {
     int b = id_bits(n);
     uint32_t tiles = (uint32_t)((M + kTileItems - 1) / kTileItems);
-    if (tm) tm->begin(kClean);
+    phase_begin(tm, kClean);
     uint64_t *keys = ctx.alloc<uint64_t>(M);
     uint64_t *keys_alt = ctx.alloc<uint64_t>(M);
     k_clean_keys<<<tiles, kTileThreads, 0, ctx.stream>>>(rowptr, col, n, M, b, keys);
@@ -294,17 +296,17 @@ void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, cons
     k_unique_scatter<<<tiles, kTileThreads, 0, ctx.stream>>>(sorted, M, (uint32_t *)(uq + tiles), uq,
                                                              m_dev, E, b, deg);
     TC_LAUNCHED(ctx);
-    if (tm) tm->end(kClean);
+    phase_end(tm, kClean);
 
-    if (tm) tm->begin(kOrient);
+    phase_begin(tm, kOrient);
     uint32_t *dplus = ctx.alloc<uint32_t>(n + 1), *dminus = ctx.alloc<uint32_t>(n + 1);
     TC_CUDA(cudaMemsetAsync(dplus, 0, (n + 1) * sizeof(uint32_t), ctx.stream));
     TC_CUDA(cudaMemsetAsync(dminus, 0, (n + 1) * sizeof(uint32_t), ctx.stream));
     int grid = ctx.persistent_grid(8);
     if (prune.enabled) {
-        if (tm) tm->begin(kPrune);
+        phase_begin(tm, kPrune);
         prune_pairs(ctx, n, b, prune.rounds_wanted, E, m_dev, deg, M, prune);
-        if (tm) tm->end(kPrune);
+        phase_end(tm, kPrune);
     }
     rank_permutation(ctx, n, rank_key(ctx, n, deg, id_order), out);
     uint32_t *okey = ctx.alloc<uint32_t>(M), *oval = ctx.alloc<uint32_t>(M);
@@ -424,15 +426,15 @@ void orient_clean(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, cons
                   PruneInfo &prune, bool id_order) {
     uint32_t tiles = (uint32_t)((M + kTileItems - 1) / kTileItems);
     int grid = ctx.persistent_grid(8);
-    if (tm) tm->begin(kOrient);
+    phase_begin(tm, kOrient);
     uint32_t *deg = ctx.alloc<uint32_t>(n);
     k_deg_rowptr<<<grid, 256, 0, ctx.stream>>>(rowptr, n, deg);
     TC_LAUNCHED(ctx);
     if (prune.enabled) {
-        if (tm) tm->begin(kPrune);
+        phase_begin(tm, kPrune);
         prune.m_before_host = M / 2;
         prune_csr(ctx, n, M, rowptr, col, prune.rounds_wanted, deg, prune);
-        if (tm) tm->end(kPrune);
+        phase_end(tm, kPrune);
     }
     const uint32_t *key = rank_key(ctx, n, deg, id_order);
     rank_permutation(ctx, n, key, out);

@@ -223,7 +223,7 @@ static void run(Call &c) {
             return;
         }
 
-        if (tm) tm->begin(kBin);
+        phase_begin(tm, kBin);
         BinParams bp;
         bp.edge_ids = c.mode == kSupport;
         bp.want_stats = c.stats != nullptr;
@@ -244,7 +244,7 @@ static void run(Call &c) {
             bp.force = TC_VARIANT_MERGE;
         Bins bins;
         bin_edges(ctx, g, bp, bins);
-        if (tm) tm->end(kBin);
+        phase_end(tm, kBin);
 
         Credit cr;
         uint32_t *sup = nullptr;
@@ -264,9 +264,9 @@ static void run(Call &c) {
             cr.order = g.order;
             TC_CUDA(cudaMemsetAsync(cr.cursor, 0, sizeof(uint64_t), ctx.stream));
         }
-        if (tm) tm->begin(kIntersect);
+        phase_begin(tm, kIntersect);
         intersect_all(ctx, g, bins, total_dev, cr);
-        if (tm) tm->end(kIntersect);
+        phase_end(tm, kIntersect);
         if (c.mode == kSupport || c.mode == kMasked) {   // N+ in the caller's ids + values
             uint64_t *off_o = ctx.alloc<uint64_t>(c.n + 1);
             uint32_t *col_o = ctx.alloc<uint32_t>(g.m_cap), *sup_o = ctx.alloc<uint32_t>(g.m_cap);

@@ -9,6 +9,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/tc.h"
 #include "block_scan.cuh"
 
@@ -262,6 +264,13 @@ struct Oriented {
     uint64_t m_cap = 0;          // capacity bound for m (host-known)
 };
 
+// NVTX ranges per phase (header-only NVTX v3: free unless a profiler is attached), so
+// Nsight Systems timelines show clean / orient / prune / bin / intersect by name.
+inline const char *phase_name(int p) {
+    static const char *names[] = {"tc.clean (a1)", "tc.orient (a2-a4)", "tc.sort",
+                                  "tc.bin (a5)", "tc.intersect (a6-a7)", "tc.prune (NEXT-2)"};
+    return p >= 0 && p < 6 ? names[p] : "tc.phase";
+}
 // Phase timer: CUDA events on the call's stream, read after the final sync.
 enum Phase { kClean = 0, kOrient, kSort, kBin, kIntersect, kPrune, kNumPhases };
 struct Timer {
@@ -288,6 +297,16 @@ struct Timer {
         return (double)t;
     }
 };
+
+// Phase boundary: NVTX range always, CUDA events when stats were requested (tm != null).
+inline void phase_begin(Timer *tm, Phase p) {
+    nvtxRangePushA(phase_name(p));
+    if (tm) tm->begin(p);
+}
+inline void phase_end(Timer *tm, Phase p) {
+    if (tm) tm->end(p);
+    nvtxRangePop();
+}
 
 // NEXT-2 leaf pruning (prune.cu).  enabled: TC_PRUNE given; rounds: 0 = to the
 // fixed point (2-core).  Filled in: rounds executed, the edge count before pruning.
