@@ -333,10 +333,12 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
     uint32_t tiles = (uint32_t)((cap + kTileItems - 1) / kTileItems);
 
     // edge bins for the merge / search / two-pointer variants (filled by k_edges)
-    const bool edge_bins = p.force == TC_VARIANT_SHORT || p.force == TC_VARIANT_MERGE ||
-                           p.force == TC_VARIANT_SEARCH ||
-                           (p.force < 0 && (p.short_max > 0 || p.skew_ratio > 0));
-    for (int k = 0; k < 3; k++) bins.edges[k] = ctx.alloc<uint2>(edge_bins ? cap : 1);
+    // only the bins that can receive edges get capacity (at s26 each is 8.6 GB): AUTO
+    // routes to SHORT (short_max > 0), SEARCH (skew_ratio > 0) or HASH; MERGE only if forced
+    const bool want[3] = {p.force == TC_VARIANT_SHORT || (p.force < 0 && p.short_max > 0),
+                          p.force == TC_VARIANT_MERGE,
+                          p.force == TC_VARIANT_SEARCH || (p.force < 0 && p.skew_ratio > 0)};
+    for (int k = 0; k < 3; k++) bins.edges[k] = ctx.alloc<uint2>(want[k] ? cap : 1);
 
     // HASH: in-part ranges (in-list order), out-part entries (compacted, CSR order),
     // statistics, owners, tasks

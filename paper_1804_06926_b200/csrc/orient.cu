@@ -318,6 +318,10 @@ void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, cons
     TC_LAUNCHED(ctx);
     k_dminus<<<grid, 256, 0, ctx.stream>>>(deg, out.newid, dplus, n, dminus);
     TC_LAUNCHED(ctx);
+    // the 64-bit keys (E and its sort buffer) are dead: give 16 B per raw arc back to the
+    // pool before the CSR build (peak device memory at s26: -17 GB)
+    ctx.free_now(keys);
+    ctx.free_now(keys_alt);
     pairs_to_csr(ctx, n, M, okey, oval, dplus, dminus, m_dev, out, tm, phist,
                  phist + ppasses * kHistDigits);
 }

@@ -69,6 +69,16 @@ struct Ctx {
         for (void *p : allocs) cudaFreeAsync(p, stream);
         allocs.clear();
     }
+    // Stream-ordered early free (the pool reuses it for later allocations of this call).
+    void free_now(void *p) {
+        for (size_t i = 0; i < allocs.size(); i++)
+            if (allocs[i] == p) {
+                cudaFreeAsync(p, stream);
+                allocs[i] = allocs.back();
+                allocs.pop_back();
+                return;
+            }
+    }
     ~Ctx() { release(); }
     // Grid for a persistent (grid-stride) kernel: `per_sm` resident CTAs per SM.
     int persistent_grid(int per_sm) const { return num_sms * per_sm; }
