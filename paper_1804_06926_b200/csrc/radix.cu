@@ -223,6 +223,25 @@ __global__ void __launch_bounds__(kRsThreads, TC_RS_MINBLOCKS)
         st_relaxed(my, (SW)((tile == 0 ? kFlagPre : kFlagAgg) | (SW)cnt));
     }
     uint32_t dstart = block_exclusive_scan<SumOp>(cnt, S.scan);  // ends with __syncthreads
+    if (is_digit) S.dstart[d] = dstart;
+    __syncthreads();
+    // ---- reorder by digit in shared memory (needs only tile-local offsets) overlapped
+    // with the decoupled look-back: the warps holding no digit reorder first, the digit
+    // warps look back first and reorder after, so the look-back latency hides behind the
+    // other warps' shared-memory traffic
+    auto reorder = [&]() {
+#pragma unroll
+        for (int j = 0; j < kRsRounds; j++) {
+            uint32_t local = wlocal + 32 * j + lane;
+            if (local < tile_n) {
+                uint32_t dg = (uint32_t)(key[j] >> shift) & kDMask;
+                uint32_t pos = S.dstart[dg] + S.wc[warp][dg] + rank[j];
+                S.keys[pos] = key[j];
+                if (kVals) S.vals[pos] = val[j];
+            }
+        }
+    };
+    if (!is_digit) reorder();
     if (is_digit) {
         uint64_t excl = 0;
         if (tile > 0) {
@@ -247,21 +266,8 @@ __global__ void __launch_bounds__(kRsThreads, TC_RS_MINBLOCKS)
             }
             st_relaxed(my, (SW)(kFlagPre | (SW)(excl + cnt)));
         }
-        S.dstart[d] = dstart;
         S.gbase[d] = digit_off[d] + excl;
-    }
-    __syncthreads();
-
-    // ---- reorder by digit in shared memory, then coalesced write-out
-#pragma unroll
-    for (int j = 0; j < kRsRounds; j++) {
-        uint32_t local = wlocal + 32 * j + lane;
-        if (local < tile_n) {
-            uint32_t dg = (uint32_t)(key[j] >> shift) & kDMask;
-            uint32_t pos = S.dstart[dg] + S.wc[warp][dg] + rank[j];
-            S.keys[pos] = key[j];
-            if (kVals) S.vals[pos] = val[j];
-        }
+        reorder();
     }
     __syncthreads();
 #pragma unroll 4
