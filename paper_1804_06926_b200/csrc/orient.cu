@@ -57,11 +57,6 @@ __global__ void __launch_bounds__(kTileThreads)
 }
 
 // ------------------------------------------------------------------ a1: unique
-__device__ __forceinline__ bool unique_flag(const uint64_t *__restrict__ keys, uint64_t i) {
-    uint64_t k = keys[i];
-    return k != ~0ull && (i == 0 || keys[i - 1] != k);
-}
-
 // Single pass (no separate count kernel + scan): tiles take a ticket, publish their unique
 // count, and get the exclusive prefix of earlier tiles by decoupled look-back (one
 // warp, 32 predecessors per step).  The last tile writes the total m.
@@ -90,15 +85,43 @@ __global__ void __launch_bounds__(kTileThreads)
     const uint32_t tile = s_tile;
     const uint64_t base = (uint64_t)tile * kTileItems + (uint64_t)threadIdx.x * kItemsPerThread;
     uint32_t f[kItemsPerThread];
+    uint64_t kk[kItemsPerThread];
     uint32_t c = 0;
 #pragma unroll
     for (int k = 0; k < kItemsPerThread; k++) {
         uint64_t i = base + k;
-        f[k] = i < M ? unique_flag(keys, i) : 0u;
-        c += f[k];
+        kk[k] = i < M ? keys[i] : ~0ull;
+    }
+    {   // flags: the previous key of item 0 comes from global memory, the rest from registers
+        const uint64_t prev0 = base > 0 && base - 1 < M ? keys[base - 1] : ~1ull;
+#pragma unroll
+        for (int k = 0; k < kItemsPerThread; k++) {
+            const uint64_t prev = k ? kk[k - 1] : prev0;
+            f[k] = base + k < M && kk[k] != ~0ull && (base + k == 0 || prev != kk[k]);
+            c += f[k];
+        }
     }
     uint32_t total;
     uint32_t pos = block_exclusive_scan<SumOp>(c, s_scan, &total);
+    // degrees need no output offset: count them while warp 0 looks back
+    if (threadIdx.x >= 32) {
+        const uint64_t mask = (1ull << b) - 1;
+        uint32_t run_a = 0, run_n = 0;
+#pragma unroll
+        for (int k = 0; k < kItemsPerThread; k++)
+            if (f[k]) {
+                const uint32_t a = (uint32_t)(kk[k] >> b);
+                atomicAdd(&deg[kk[k] & mask], 1u);
+                if (run_n && a == run_a) {
+                    run_n++;
+                } else {
+                    if (run_n) atomicAdd(&deg[run_a], run_n);
+                    run_a = a;
+                    run_n = 1;
+                }
+            }
+        if (run_n) atomicAdd(&deg[run_a], run_n);
+    }
     if (threadIdx.x < 32) {   // warp 0: publish, look back, publish the inclusive prefix
         const uint32_t lane = threadIdx.x;
         if (lane == 0) uq_st(&status[tile], (tile == 0 ? kUqPre : kUqAgg) | total);
@@ -120,27 +143,29 @@ __global__ void __launch_bounds__(kTileThreads)
             s_excl = excl;
             if ((uint64_t)(tile + 1) * kTileItems >= M) *m_out = excl + total;   // last tile
         }
+        // warp 0's own degrees, after its look-back
+        const uint64_t mask = (1ull << b) - 1;
+        uint32_t run_a = 0, run_n = 0;
+#pragma unroll
+        for (int k = 0; k < kItemsPerThread; k++)
+            if (f[k]) {
+                const uint32_t a = (uint32_t)(kk[k] >> b);
+                atomicAdd(&deg[kk[k] & mask], 1u);
+                if (run_n && a == run_a) {
+                    run_n++;
+                } else {
+                    if (run_n) atomicAdd(&deg[run_a], run_n);
+                    run_a = a;
+                    run_n = 1;
+                }
+            }
+        if (run_n) atomicAdd(&deg[run_a], run_n);
     }
     __syncthreads();
     uint64_t o = s_excl + pos;
-    const uint64_t mask = (1ull << b) - 1;
-    uint32_t run_a = 0, run_n = 0;
 #pragma unroll
     for (int k = 0; k < kItemsPerThread; k++)
-        if (f[k]) {
-            const uint64_t key = keys[base + k];
-            out[o++] = key;
-            const uint32_t a = (uint32_t)(key >> b);
-            atomicAdd(&deg[key & mask], 1u);
-            if (run_n && a == run_a) {
-                run_n++;
-            } else {
-                if (run_n) atomicAdd(&deg[run_a], run_n);
-                run_a = a;
-                run_n = 1;
-            }
-        }
-    if (run_n) atomicAdd(&deg[run_a], run_n);
+        if (f[k]) out[o++] = kk[k];
 }
 
 // ------------------------------------------------------------------ a3 from pairs
