@@ -20,7 +20,8 @@
  *
  * INPUT LAYOUT (CSR, "Graph" of SPEC.md S:31-41):
  *   n            number of vertices, ids in [0, n), n < 2^32.
- *   m            number of arcs = row_offsets[n].  Each arc is read as an
+ *   m            number of arcs = row_offsets[n], m < 2^32 (TC_EINVAL otherwise:
+ *                edge positions and slots are 32-bit).  Each arc is read as an
  *                undirected edge.
  *   row_offsets  uint64[n+1], row_offsets[0] = 0, non-decreasing,
  *                row_offsets[n] = m.

@@ -72,6 +72,8 @@ struct Call {
 static tc_status check_args(const Call &c) {
     if (c.flags & ~(uint32_t)TC_ALL_FLAGS) return set_error("unknown flag bits"), TC_EINVAL;
     if (c.n >= (1ull << 32)) return set_error("n must be < 2^32"), TC_EINVAL;
+    if (c.M >= (1ull << 32))   // edge positions, in-list slots and probe ranges are 32-bit
+        return set_error("m (arcs) must be < 2^32"), TC_EINVAL;
     if (!c.rowptr) return set_error("row_offsets is NULL"), TC_EINVAL;
     if (c.M > 0 && !c.col) return set_error("col_indices is NULL with m > 0"), TC_EINVAL;
     if (c.mode == kCount && !c.total_host) return set_error("total is NULL"), TC_EINVAL;
@@ -239,9 +241,6 @@ static void run(Call &c) {
             work_prefix(ctx, g, prefix);
             bp.work_prefix = prefix;
         }
-        // The HASH kernels index col+ with 32-bit offsets; beyond that size route to MERGE.
-        if (g.m_cap >= (1ull << 32) && (bp.force < 0 || bp.force == TC_VARIANT_HASH))
-            bp.force = TC_VARIANT_MERGE;
         Bins bins;
         bin_edges(ctx, g, bp, bins);
         phase_end(tm, kBin);

@@ -65,6 +65,15 @@ def test_clustering_argument_errors(lib):
     assert b"TC_PRUNE" in lib.tc_last_error()
 
 
+def test_arc_count_limit(lib):
+    rp = np.zeros(2, np.uint64)
+    total = np.zeros(1, np.uint64)
+    # m >= 2^32 arcs is rejected before any pointer is read
+    assert lib.tc_count_ex(1, 1 << 32, rp.ctypes.data, rp.ctypes.data, tc.TC_HOST_PTRS, None,
+                           total.ctypes.data, None, None) == 1
+    assert b"2^32" in lib.tc_last_error()
+
+
 def test_next3_argument_errors(lib):
     rp = np.zeros(2, np.uint64)
     EINVAL = 1
