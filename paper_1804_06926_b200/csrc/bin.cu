@@ -267,14 +267,12 @@ __global__ void k_task_count(const uint32_t *__restrict__ owners, const uint64_t
                              uint64_t n, uint32_t L, uint32_t *__restrict__ tcnt,
                              uint64_t *__restrict__ tloads) {
     uint64_t no = *ocount, loads = 0;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+    (void)n;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < no;
          i += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t t = 0;
-        if (i < no) {
-            uint32_t x = owners[i];
-            t = (pcnt[x] + L - 1) / L;
-            loads += (uint64_t)t * dplus[x];
-        }
+        uint32_t x = owners[i];
+        uint32_t t = (pcnt[x] + L - 1) / L;
+        loads += (uint64_t)t * dplus[x];
         tcnt[i] = t;
     }
     loads = warp_sum_u64(loads);
@@ -301,15 +299,13 @@ static void make_tasks(Ctx &ctx, uint64_t n, uint64_t cap, const uint32_t *owner
     int grid = ctx.persistent_grid(4);
     k_task_count<<<grid, 256, 0, ctx.stream>>>(owners, ocount, pcnt, dplus, n, L, tcnt, tloads);
     TC_LAUNCHED(ctx);
-    scan_exclusive(ctx, tcnt, toff, n);
+    // the owner list is usually far shorter than n (road mesh: empty): scan only its length
+    scan_exclusive_dc(ctx, tcnt, toff, n, ocount, toff + n);
     tasks = ctx.alloc<uint2>((2 * cap) / L + n + 1);
     k_task_expand<<<grid, 256, 0, ctx.stream>>>(owners, ocount, tcnt, toff, tasks);
     TC_LAUNCHED(ctx);
     ntasks = toff + n;
 }
-
-__global__ void k_stage_work(const uint64_t *__restrict__ in_off, const uint32_t *__restrict__ dplus,
-                             uint64_t n, uint64_t *__restrict__ out);
 
 void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
     uint64_t cap = g.m_cap, n = g.n;
@@ -385,22 +381,6 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
                bins.count + 11, bins.tasks_cta, bins.ntasks_cta);
     make_tasks(ctx, n, cap, bins.owners_bitmap, bins.count + 10, bins.pcnt, g.dplus, kCtaTaskLists,
                bins.count + 11, bins.tasks_bitmap, bins.ntasks_bitmap);
-    if (p.want_stats) {
-        k_stage_work<<<ctx.persistent_grid(2), 256, 0, ctx.stream>>>(g.in_off, g.dplus, n, bins.count + 12);
-        TC_LAUNCHED(ctx);
-    }
-}
-
-// Stats only: sum_v d-(v) d+(v), for SURVEY §8(d)'s B_stage = 4 (m + sum d- d+) + 16 m (the
-// bytes of a method that stages each source list once per in-edge).
-__global__ void k_stage_work(const uint64_t *__restrict__ in_off, const uint32_t *__restrict__ dplus,
-                             uint64_t n, uint64_t *__restrict__ out) {
-    uint64_t acc = 0;
-    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
-         v += (uint64_t)gridDim.x * blockDim.x)
-        acc += (in_off[v + 1] - in_off[v]) * (uint64_t)dplus[v];
-    acc = warp_sum_u64(acc);
-    if ((threadIdx.x & 31) == 0 && acc) atomicAdd((unsigned long long *)out, (unsigned long long)acc);
 }
 
 // Per-source work estimate w(u) = sum_{v in N+(u)} (c + min(|N+(u) after v|, d+v)) -- the

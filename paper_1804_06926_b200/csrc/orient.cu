@@ -247,13 +247,19 @@ static void rank_permutation(Ctx &ctx, uint64_t n, const uint32_t *deg, Oriented
 }
 
 // d-(x) = d(x) - d+(x), in rank ids.
+// Also sum_v d-(v) d+(v) (stats: SURVEY 8(d)'s B_stage) into *stage, one atomic per warp.
 __global__ void k_dminus(const uint32_t *__restrict__ deg, const uint32_t *__restrict__ newid,
-                         const uint32_t *__restrict__ dplus, uint64_t n, uint32_t *__restrict__ dminus) {
+                         const uint32_t *__restrict__ dplus, uint64_t n, uint32_t *__restrict__ dminus,
+                         uint64_t *__restrict__ stage) {
+    uint64_t acc = 0;
     for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
          v += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t x = newid[v];
-        dminus[x] = deg[v] - dplus[x];
+        uint32_t x = newid[v], dp = dplus[x], dm = deg[v] - dp;
+        dminus[x] = dm;
+        acc += (uint64_t)dm * dp;
     }
+    acc = warp_sum_u64(acc);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd((unsigned long long *)stage, (unsigned long long)acc);
 }
 
 // Oriented pairs (okey = source, oval = target, new ids; m_dev of them) -> CSR with
@@ -341,7 +347,9 @@ void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, cons
     k_orient_pairs<<<grid, 256, 0, ctx.stream>>>(E, m_dev, b, out.newid, okey, oval, dplus, phist,
                                                  phist + ppasses * kHistDigits, ppasses, pdb);
     TC_LAUNCHED(ctx);
-    k_dminus<<<grid, 256, 0, ctx.stream>>>(deg, out.newid, dplus, n, dminus);
+    out.stage_work = ctx.alloc<uint64_t>(1);
+    TC_CUDA(cudaMemsetAsync(out.stage_work, 0, sizeof(uint64_t), ctx.stream));
+    k_dminus<<<grid, 256, 0, ctx.stream>>>(deg, out.newid, dplus, n, dminus, out.stage_work);
     TC_LAUNCHED(ctx);
     // the 64-bit keys (E and its sort buffer) are dead: give 16 B per raw arc back to the
     // pool before the CSR build (peak device memory at s26: -17 GB)
@@ -483,7 +491,9 @@ void orient_clean(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, cons
         rowptr, col, n, M, key, out.newid, (uint32_t *)(st + tiles), st, st + tiles + 1, okey, oval,
         dplus, phist, phist + ppasses * kHistDigits, ppasses, pdb);
     TC_LAUNCHED(ctx);
-    k_dminus<<<grid, 256, 0, ctx.stream>>>(deg, out.newid, dplus, n, dminus);
+    out.stage_work = ctx.alloc<uint64_t>(1);
+    TC_CUDA(cudaMemsetAsync(out.stage_work, 0, sizeof(uint64_t), ctx.stream));
+    k_dminus<<<grid, 256, 0, ctx.stream>>>(deg, out.newid, dplus, n, dminus, out.stage_work);
     TC_LAUNCHED(ctx);
     pairs_to_csr(ctx, n, cap, okey, oval, dplus, dminus, st + tiles + 1, out, tm, phist,
                  phist + ppasses * kHistDigits);

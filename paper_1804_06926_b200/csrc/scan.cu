@@ -68,6 +68,73 @@ static void scan_impl(Ctx &ctx, const T *in, uint64_t *out, uint64_t count) {
     TC_LAUNCHED(ctx);
 }
 
+// Device-count variant: only the first *count_dev (<= cap) items are scanned; blocks past
+// them exit at once (no n-sized traffic when few items are live), and the total is also
+// written to *total_out.
+__global__ void __launch_bounds__(kScanThreads) k_scan_reduce_dc(const uint32_t *__restrict__ in,
+                                                                 const uint64_t *__restrict__ count_dev,
+                                                                 uint64_t *__restrict__ partial) {
+    __shared__ uint64_t s_scratch[kScanThreads / 32];
+    const uint64_t count = *count_dev;
+    const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
+    if (base >= count) {
+        if (threadIdx.x == 0) partial[blockIdx.x] = 0;
+        return;
+    }
+    uint64_t sum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; k++) {
+        uint64_t i = base + (uint64_t)k * kScanThreads + threadIdx.x;
+        if (i < count) sum += (uint64_t)in[i];
+    }
+    sum = block_sum_u64(sum, s_scratch);
+    if (threadIdx.x == 0) partial[blockIdx.x] = sum;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_apply_dc(const uint32_t *__restrict__ in,
+                                                                const uint64_t *__restrict__ count_dev,
+                                                                const uint64_t *__restrict__ offsets,
+                                                                uint64_t *__restrict__ out,
+                                                                uint64_t *__restrict__ total_out) {
+    __shared__ uint64_t s_scan[kScanThreads / 32];
+    const uint64_t count = *count_dev;
+    if ((uint64_t)blockIdx.x * kScanTile > count) return;   // block-uniform
+    uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanItems;
+    uint64_t v[kScanItems];
+    uint64_t run = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; k++) {
+        uint64_t i = base + k;
+        uint64_t x = i < count ? (uint64_t)in[i] : 0;
+        v[k] = run;
+        run += x;
+    }
+    uint64_t prefix = block_exclusive_scan<SumOp64>(run, s_scan) + offsets[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < kScanItems; k++) {
+        uint64_t i = base + k;
+        if (i <= count) out[i] = v[k] + prefix;
+        if (i == count) *total_out = v[k] + prefix;
+    }
+}
+
+void scan_exclusive_dc(Ctx &ctx, const uint32_t *in, uint64_t *out, uint64_t cap,
+                       const uint64_t *count_dev, uint64_t *total_out) {
+    uint64_t tiles = (cap + 1 + kScanTile - 1) / kScanTile;
+    uint64_t *partial = ctx.alloc<uint64_t>(tiles);
+    uint64_t *offsets = ctx.alloc<uint64_t>(tiles + 1);
+    k_scan_reduce_dc<<<(unsigned)tiles, kScanThreads, 0, ctx.stream>>>(in, count_dev, partial);
+    TC_LAUNCHED(ctx);
+    if (tiles == 1) {
+        TC_CUDA(cudaMemsetAsync(offsets, 0, sizeof(uint64_t), ctx.stream));
+    } else {
+        scan_impl<uint64_t>(ctx, partial, offsets, tiles);
+    }
+    k_scan_apply_dc<<<(unsigned)tiles, kScanThreads, 0, ctx.stream>>>(in, count_dev, offsets, out,
+                                                                       total_out);
+    TC_LAUNCHED(ctx);
+}
+
 void scan_exclusive(Ctx &ctx, const uint32_t *in, uint64_t *out, uint64_t count) {
     scan_impl<uint32_t>(ctx, in, out, count);
 }

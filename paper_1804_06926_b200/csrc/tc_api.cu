@@ -228,7 +228,6 @@ static void run(Call &c) {
         phase_begin(tm, kBin);
         BinParams bp;
         bp.edge_ids = c.mode == kSupport;
-        bp.want_stats = c.stats != nullptr;
         bp.short_max = c.opt.short_max;
         bp.skew_ratio = c.opt.skew_ratio;
         bp.hub_min = c.opt.hub_min_dplus;
@@ -298,6 +297,8 @@ static void run(Call &c) {
             TC_CUDA(cudaMemcpyAsync(pin, bins.count, 16 * sizeof(uint64_t), cudaMemcpyDeviceToHost,
                                     ctx.stream));
             TC_CUDA(cudaMemcpyAsync(pin + 16, g.m_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                                    ctx.stream));
+            TC_CUDA(cudaMemcpyAsync(pin + 12, g.stage_work, sizeof(uint64_t), cudaMemcpyDeviceToHost,
                                     ctx.stream));
         }
     } else if (c.mode == kOrientOnly || c.mode == kSupport || c.mode == kMasked) {

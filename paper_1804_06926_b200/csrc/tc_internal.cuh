@@ -234,6 +234,9 @@ struct RsHist {
 // Exclusive scan: out[i] = sum_{j<i} in[j] for i in [0, count], out[count] = total.
 void scan_exclusive(Ctx &ctx, const uint32_t *in, uint64_t *out, uint64_t count);
 void scan_exclusive(Ctx &ctx, const uint64_t *in, uint64_t *out, uint64_t count);
+// Same over the first *count_dev (<= cap) items only; the total also goes to *total_out.
+void scan_exclusive_dc(Ctx &ctx, const uint32_t *in, uint64_t *out, uint64_t cap,
+                       const uint64_t *count_dev, uint64_t *total_out);
 
 // Stable LSD radix sort on bits [0, bits) of the keys.  `count_dev`, if non-null,
 // is a device counter that caps the number of valid items (<= capacity).
@@ -271,6 +274,7 @@ struct Oriented {
     uint32_t *order = nullptr;   // new id -> input id
     uint32_t *newid = nullptr;   // input id -> new id
     uint64_t *m_dev = nullptr;   // device scalar m
+    uint64_t *stage_work = nullptr;  // device scalar sum_v d-(v) d+(v) (stats)
     uint64_t m_cap = 0;          // capacity bound for m (host-known)
 };
 
@@ -406,8 +410,7 @@ struct Bins {
     uint64_t *count = nullptr;  // device: [0..3] SHORT/MERGE/SEARCH/HASH edges, [4] W,
                                 // [5] sum min(|N+(u) after v|, d+(v)), [6] skipped, [7] max d+,
                                 // [8] warp owners, [9] CTA hash owners, [10] CTA bitmap owners,
-                                // [11] table-build loads (sum over tasks of d+(owner)),
-                                // [12] sum_v d-(v) d+(v) (stats only)
+                                // [11] table-build loads (sum over tasks of d+(owner))
     uint32_t *pcnt = nullptr;   // per owner: probe entries
     uint32_t *owners_warp = nullptr;   // owners with d+ < hub_min: tables of one warp
     uint32_t *owners_cta = nullptr;    // larger owners ("hubs"): tables of one CTA
@@ -431,7 +434,6 @@ struct BinParams {
     int rank, world;
     const uint64_t *work_prefix;  // exclusive prefix of per-source work (world > 1)
     bool edge_ids = false;        // out-part entries record their edge's CSR index (kCmEdge)
-    bool want_stats = false;      // also count sum_v d-(v) d+(v) into count[12]
 };
 
 void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins);
