@@ -134,7 +134,8 @@ typedef struct {
     uint64_t work_probe;      /* sum over E+ of min(|N+(u) after v|, d+v) (HASH probe work)  */
     uint64_t bytes_alg;       /* 4*W + 16*m: algorithmic bytes of the intersection (B_alg)  */
     uint64_t bin_edges[4];    /* edges routed to SHORT, MERGE, SEARCH, HASH                 */
-    uint64_t skipped_edges;   /* edges that cannot close a triangle (d+(u) < 2 or d+(v) = 0) */
+    uint64_t skipped_edges;   /* edges that cannot close a triangle (|N+(u) after v| = 0 or
+                                 d+(v) = 0)                                                 */
     uint64_t hub_sources;     /* HASH owners handled by a whole CTA (d+ >= hub_min_dplus)   */
     uint64_t max_dplus;       /* max out-degree after orientation                           */
     uint64_t kernel_launches; /* kernels this call launched                                 */
