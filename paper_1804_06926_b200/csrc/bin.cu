@@ -194,35 +194,39 @@ __global__ void __launch_bounds__(kTileWords)
     }
 }
 
-// ooff[x] = out-part entries before x's row = tile prefix + word prefix + bits below.
-__global__ void k_ooff(const uint64_t *__restrict__ off, uint64_t n, const uint64_t *__restrict__ m_dev,
-                       const uint32_t *__restrict__ obits, const uint16_t *__restrict__ wpre,
-                       const uint64_t *__restrict__ toff, const uint64_t *__restrict__ total,
-                       uint64_t *__restrict__ ooff) {
-    uint64_t m = *m_dev, t = *total;
-    for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x <= n;
-         x += (uint64_t)gridDim.x * blockDim.x) {
-        uint64_t s = off[x];
-        ooff[x] = s < m ? toff[s / kTileItems] + wpre[s >> 5] +
-                              __popc(obits[s >> 5] & ((1u << (s & 31)) - 1u))
-                        : t;
+// Out-part entries before CSR position s = tile prefix + in-tile word prefix + bits below.
+struct OutPrefix {
+    const uint32_t *obits;
+    const uint16_t *wpre;
+    const uint64_t *toff;
+    uint64_t m, total;
+    __device__ __forceinline__ uint64_t at(uint64_t s) const {
+        return s < m ? toff[s / kTileItems] + wpre[s >> 5] + __popc(obits[s >> 5] & ((1u << (s & 31)) - 1u))
+                     : total;
     }
-}
+};
 
 // Owner lists and max d+.  pcnt[x] = probe entries of owner x = its in-degree (empty
 // entries included; 0 if none of them is x's) + its compacted out-part entries; warp owners (d+ < cta_min), CTA
 // bitmap owners (rank span n-1-x plus a spare zero word fits kCtaBitmapBits) and CTA
 // hash owners (the rest).
+// Also writes ooff[u] (each owner's first out-part entry; ooff[n] = the total), which the
+// owner counts here need anyway: no separate pass over the vertices.
 __global__ void k_owners(const uint32_t *__restrict__ dplus, const uint64_t *__restrict__ in_off,
                          const uint32_t *__restrict__ ulo, uint32_t *__restrict__ has_in,
-                         const uint64_t *__restrict__ ooff,
+                         uint64_t *__restrict__ ooff, const uint64_t *__restrict__ off,
+                         const uint64_t *__restrict__ m_dev, const uint32_t *__restrict__ obits,
+                         const uint16_t *__restrict__ wpre, const uint64_t *__restrict__ toff,
+                         const uint64_t *__restrict__ ototal,
                          uint64_t n, uint32_t cta_min,
                          uint32_t *__restrict__ pcnt, uint32_t *__restrict__ owners_warp,
                          uint32_t *__restrict__ owners_cta, uint32_t *__restrict__ owners_bitmap,
                          uint64_t *__restrict__ counts) {
     uint32_t local_max = 0;
+    const OutPrefix op{obits, wpre, toff, *m_dev, *ototal};
     uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     uint64_t end = (n + 31) & ~31ull;  // whole warps stay in the loop (warp-aggregated appends)
+    if (blockIdx.x == 0 && threadIdx.x == 0) ooff[n] = op.at(off[n]);
     int lane = threadIdx.x & 31;
     uint32_t lt = (1u << lane) - 1u;
     for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < end; u += stride) {
@@ -230,6 +234,8 @@ __global__ void k_owners(const uint32_t *__restrict__ dplus, const uint64_t *__r
         if (u < n) {
             uint32_t du = dplus[u];
             local_max = max(local_max, du);
+            const uint64_t o0 = op.at(off[u]);
+            ooff[u] = o0;
             uint32_t c = 0, hin = 0;
             if (du) {
                 // does some in-entry of u carry this rank's HASH work?  (first hit exits)
@@ -239,7 +245,7 @@ __global__ void k_owners(const uint32_t *__restrict__ dplus, const uint64_t *__r
                         hin = 1;
                         break;
                     }
-                c = (hin ? (uint32_t)(ie - ib) : 0u) + (uint32_t)(ooff[u + 1] - ooff[u]);
+                c = (hin ? (uint32_t)(ie - ib) : 0u) + (uint32_t)(op.at(off[u + 1]) - o0);
             }
             has_in[u] = hin;
             pcnt[u] = c;
@@ -358,9 +364,6 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
                                                          orange, ovid, wpre, p.edge_ids);
         TC_LAUNCHED(ctx);
     }
-    k_ooff<<<ctx.persistent_grid(4), 256, 0, ctx.stream>>>(g.off, n, g.m_dev, obits, wpre, toff,
-                                                           toff + tiles, ooff);
-    TC_LAUNCHED(ctx);
     hp.ulo = ulo;
     hp.has_in = has_in;
     hp.orange = orange;
@@ -372,8 +375,8 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
     bins.owners_bitmap = ctx.alloc<uint32_t>(n);
     uint32_t cta_min = p.hub_min < kWarpTableSlots / 4 + 1 ? p.hub_min : kWarpTableSlots / 4 + 1;
     k_owners<<<ctx.persistent_grid(4), 256, 0, ctx.stream>>>(
-        g.dplus, g.in_off, ulo, has_in, ooff, n, cta_min, bins.pcnt, bins.owners_warp, bins.owners_cta,
-        bins.owners_bitmap, bins.count);
+        g.dplus, g.in_off, ulo, has_in, ooff, g.off, g.m_dev, obits, wpre, toff, toff + tiles, n,
+        cta_min, bins.pcnt, bins.owners_warp, bins.owners_cta, bins.owners_bitmap, bins.count);
     TC_LAUNCHED(ctx);
     make_tasks(ctx, n, cap, bins.owners_warp, bins.count + 8, bins.pcnt, g.dplus, kWarpTaskLists,
                bins.count + 11, bins.tasks_warp, bins.ntasks_warp);

@@ -207,12 +207,6 @@ __global__ void k_orient_pairs(const uint64_t *__restrict__ E, const uint64_t *_
 }
 
 // ------------------------------------------------------------------ rank relabelling
-__global__ void k_newid(const uint32_t *__restrict__ order, uint64_t n, uint32_t *__restrict__ newid) {
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x)
-        newid[order[i]] = (uint32_t)i;
-}
-
 // TC_ID_ORDER (Alg. 3 without its row permutation, the order of Fig. mm): the rank
 // key is [d(v) > 0], so every non-isolated vertex ranks by id alone (isolated and
 // pruned-away vertices, key 0, keep failing the rank filter).
@@ -239,11 +233,11 @@ static void rank_permutation(Ctx &ctx, uint64_t n, const uint32_t *deg, Oriented
     // stable sort by degree (< n <= 2^b) of the ids 0..n-1 (generated by the first pass,
     // ascending), so ties stay ordered by id
     uint32_t *rk, *rv;
-    radix_sort_pairs_from(ctx, deg, nullptr, kA, kB, vA, vB, n, nullptr, b, &rk, &rv);
+    out.newid = ctx.alloc<uint32_t>(n);   // written by the last pass (fused inverse)
+    radix_sort_pairs_from(ctx, deg, nullptr, kA, kB, vA, vB, n, nullptr, b, &rk, &rv, nullptr,
+                          nullptr, nullptr, out.newid);
     out.order = rv;
-    out.newid = ctx.alloc<uint32_t>(n);
-    k_newid<<<grid, 256, 0, ctx.stream>>>(out.order, n, out.newid);
-    TC_LAUNCHED(ctx);
+    (void)grid;
 }
 
 // d-(x) = d(x) - d+(x), in rank ids.

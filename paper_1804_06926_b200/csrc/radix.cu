@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(kRsThreads, TC_RS_MINBLOCKS)
               uint32_t *__restrict__ vals_out, uint64_t cap, const uint64_t *__restrict__ count_dev,
               int shift, const uint64_t *__restrict__ digit_off, uint32_t *__restrict__ ticket,
               SW *__restrict__ status, const uint32_t *__restrict__ gather,
-              uint32_t *__restrict__ gather_out) {
+              uint32_t *__restrict__ gather_out, uint32_t *__restrict__ inverse) {
     constexpr SW kFlagAgg = Status<SW>::kFlagAgg, kFlagPre = Status<SW>::kFlagPre;
     constexpr SW kCountMask = Status<SW>::kCountMask;
     constexpr uint32_t kD = 1u << DB, kDMask = kD - 1u;   // digits of this pass
@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(kRsThreads, TC_RS_MINBLOCKS)
             const uint32_t v = S.vals[i];
             vals_out[g] = v;
             if (gather) gather_out[g] = gather[v];   // fused gather (last pass only)
+            if (inverse) inverse[v] = (uint32_t)g;   // fused inverse permutation (last pass)
         }
     }
 }
@@ -290,7 +291,8 @@ template <class K, bool kVals>
 static void radix_impl(Ctx &ctx, const K *kin0, const uint32_t *vin0, K *kA, K *kB, uint32_t *vA,
                        uint32_t *vB, uint64_t capacity, const uint64_t *count_dev, int bits,
                        K **kres, uint32_t **vres, const uint32_t *gather = nullptr,
-                       uint32_t *gather_out = nullptr, const uint32_t *hist_in = nullptr) {
+                       uint32_t *gather_out = nullptr, const uint32_t *hist_in = nullptr,
+                       uint32_t *inverse = nullptr) {
     *kres = const_cast<K *>(kin0);
     *vres = const_cast<uint32_t *>(vin0);
     if (capacity == 0 || bits <= 0) return;
@@ -330,11 +332,12 @@ static void radix_impl(Ctx &ctx, const K *kin0, const uint32_t *vin0, K *kA, K *
         uint32_t *vout = (p & 1) ? vB : vA;
         TC_CUDA(cudaMemsetAsync(status, 0, (size_t)tiles * kDigits * sw, ctx.stream));
         const uint32_t *ga = p == passes - 1 ? gather : nullptr;
+        uint32_t *inv = p == passes - 1 ? inverse : nullptr;
         const uint64_t *dop = doff + (uint64_t)p * kDigits;
 #define TC_RS_LAUNCH(SWT, DBV)                                                                  \
     k_rs_pass<K, kVals, SWT, DBV><<<tiles, kRsThreads, smem, ctx.stream>>>(                     \
         kin, vin, kout, vout, capacity, count_dev, db * p, dop, tickets + p, (SWT *)status, ga, \
-        gather_out)
+        gather_out, inv)
         if (narrow) {
             if (db == 7) TC_RS_LAUNCH(uint32_t, 7);
             else TC_RS_LAUNCH(uint32_t, 8);
@@ -374,9 +377,9 @@ void radix_sort_pairs_from(Ctx &ctx, const uint32_t *keys_in, const uint32_t *va
                            uint32_t *kA, uint32_t *kB, uint32_t *vA, uint32_t *vB,
                            uint64_t capacity, const uint64_t *count_dev, int bits,
                            uint32_t **keys_out, uint32_t **vals_out, const uint32_t *gather,
-                           uint32_t *gather_out, const uint32_t *hist_in) {
+                           uint32_t *gather_out, const uint32_t *hist_in, uint32_t *inverse) {
     radix_impl<uint32_t, true>(ctx, keys_in, vals_in, kA, kB, vA, vB, capacity, count_dev, bits,
-                               keys_out, vals_out, gather, gather_out, hist_in);
+                               keys_out, vals_out, gather, gather_out, hist_in, inverse);
 }
 
 }  // namespace tc

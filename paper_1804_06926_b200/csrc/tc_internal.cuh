@@ -252,13 +252,14 @@ bool radix_sort_pairs(Ctx &ctx, uint32_t *keys, uint32_t *keys_alt, uint32_t *va
 // Same, reading (keys_in, vals_in) without modifying them; passes ping-pong between
 // A and B; *keys_out / *vals_out receive the buffers holding the result.
 // vals_in == nullptr: the values are the input positions 0, 1, 2, ...  With `gather`, the
-// last pass also writes gather_out[i] = gather[value of sorted item i] (fused gather).
+// last pass also writes gather_out[i] = gather[value of sorted item i] (fused gather); with
+// `inverse`, inverse[value of sorted item i] = i (fused inverse permutation).
 void radix_sort_pairs_from(Ctx &ctx, const uint32_t *keys_in, const uint32_t *vals_in,
                            uint32_t *kA, uint32_t *kB, uint32_t *vA, uint32_t *vB,
                            uint64_t capacity, const uint64_t *count_dev, int bits,
                            uint32_t **keys_out, uint32_t **vals_out,
                            const uint32_t *gather = nullptr, uint32_t *gather_out = nullptr,
-                           const uint32_t *hist_in = nullptr);
+                           const uint32_t *hist_in = nullptr, uint32_t *inverse = nullptr);
 
 // ------------------------------------------------------------------ pipeline stages
 // Oriented CSR in RANK-RELABELLED ids: vertex v of the input is newid[v] here,
