@@ -422,7 +422,7 @@ void tc_default_options(tc_options *opt) {
     // bin, so those bins are off unless enabled here or forced.
     opt->short_max = 32;
     opt->skew_ratio = 0;
-    opt->hub_min_dplus = 64;
+    opt->hub_min_dplus = 80;
     opt->force_variant = TC_VARIANT_AUTO;
     opt->stream = nullptr;
     opt->segsort_block_max = 8192;
