@@ -420,7 +420,7 @@ void tc_default_options(tc_options *opt) {
     // AUTO defaults, measured on R-MAT s21: the HASH
     // variant (cost min(d+u, d+v) per edge) beats SHORT / SEARCH / MERGE on every
     // bin, so those bins are off unless enabled here or forced.
-    opt->short_max = 32;
+    opt->short_max = 20;
     opt->skew_ratio = 0;
     opt->hub_min_dplus = 80;
     opt->force_variant = TC_VARIANT_AUTO;

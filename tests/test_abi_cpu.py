@@ -44,7 +44,7 @@ def test_struct_layout(lib):
     o = tc.Options()
     lib.tc_default_options(ctypes.byref(o))
     assert ctypes.sizeof(tc.Options) == 64
-    assert o.short_max == 32 and o.skew_ratio == 0 and o.hub_min_dplus == 80
+    assert o.short_max == 20 and o.skew_ratio == 0 and o.hub_min_dplus == 80
     assert o.force_variant == -1 and o.segsort_block_max == 8192
     assert o.prune_rounds == 0 and not any(o.reserved)
     assert ctypes.sizeof(tc.Stats) == 7 * 8 + 19 * 8

@@ -197,7 +197,7 @@ def test_shards_sum_to_total(world):
     assert sum(1 for p in parts if p > 0) >= min(world, 2)      # work really is split
 
 
-@pytest.mark.parametrize("short_max", [0, 8, 32, 128])
+@pytest.mark.parametrize("short_max", [0, 8, 20, 32, 128])
 @pytest.mark.parametrize("world", [1, 3])
 @pytest.mark.parametrize("gname", ["rmat", "chung_lu"])
 def test_shards_with_short_bin(gname, world, short_max):
