@@ -5,7 +5,7 @@ import numpy as np, torch
 import graphgen as G
 import paper_1804_06926_b200 as tc
 mk = {"s21": lambda: G.rmat(21), "chung_lu": G.chung_lu, "road": G.road_mesh, "clique": G.clique_union,
-      "s24": lambda: G.rmat(24)}
+      "s24": lambda: G.rmat(24), "s22": lambda: G.rmat(22), "ef48": lambda: G.rmat(21, 48)}
 cfgs = json.loads(sys.argv[2]) if len(sys.argv) > 2 else [{}]
 for w in sys.argv[1].split(","):
     g = mk[w]()
