@@ -14,6 +14,8 @@ per-step CUDA-event spans.  `value` = undirected edges m / (ms per step), whole 
 Workload at N = 1: BASELINE.json configs[1], R-MAT scale 21 edge factor 16 (Graph500
 A,B,C,D = .57,.19,.19,.05), seeded and synthetic.  For N > 1 the
 same graph is replicated on every rank and the sources are split by work (strong scaling).
+Without torchrun's environment, `--gpus N` (N > 1) re-launches itself under
+torch.distributed.run (one rank per GPU, 127.0.0.1 rendezvous).
 """
 from __future__ import annotations
 
@@ -42,7 +44,23 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-next", action="store_true", help="skip the NEXT-row measurements")
+    ap.add_argument("--one-call", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--no-ncu", action="store_true",
+                    help="skip the ncu DRAM-traffic capture of the a6 kernels (roofline.traffic)")
     return ap.parse_args()
+
+
+def self_spawn(args) -> int:
+    """`python bench.py --gpus N` without torchrun's environment: re-launch under
+    torch.distributed.run with N ranks on this node (the driver's own launch line)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def load_peaks():
@@ -117,12 +135,52 @@ def oracle_run(g):
     return T, st["m"], time.perf_counter() - t0
 
 
+def host_cpu():
+    """lscpu model / sockets / cores / threads of the host the oracle runs on."""
+    info = {}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            k, v = k.strip(), v.strip()
+            if k in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core", "CPU(s)"):
+                info[k] = v
+    except (OSError, subprocess.SubprocessError):
+        pass
+    info["OMP_NUM_THREADS"] = os.environ.get("OMP_NUM_THREADS")
+    return info
+
+
+SINGLE_THREAD_SAMPLE = (18, 16)   # R-MAT s18 ef16: ~10 s of one core
+
+
+def oracle_single_thread():
+    """The paper's sequential-forward analogue (SURVEY §8(d) oracle timing (ii)): the oracle
+    with ONE thread, in a child process (OpenMP reads OMP_NUM_THREADS at start-up), on a
+    bounded sample of the same generator."""
+    code = ("import sys, time; sys.path.insert(0, %r); import graphgen, oracle\n"
+            "g = graphgen.rmat(%d, %d); t0 = time.perf_counter()\n"
+            "T, st = oracle.count(g.n, g.rowptr, g.col, with_stats=True)\n"
+            "print(time.perf_counter() - t0, st['m'], T, oracle.num_threads())"
+            % (ROOT, *SINGLE_THREAD_SAMPLE))
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    try:
+        out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                             timeout=240, env=env).stdout.split()
+        sec, m, T, thr = float(out[0]), int(out[1]), int(out[2]), int(out[3])
+    except (OSError, subprocess.SubprocessError, ValueError, IndexError):
+        return None
+    return {"value": m / sec, "unit": "edges/s", "cores": thr, "seconds": sec, "T": T,
+            "sample": "rmat-s%d-ef%d (whole graph), one run, OMP_NUM_THREADS=1" % SINGLE_THREAD_SAMPLE}
+
+
 def cpu_baseline(g, m):
     import oracle
     T, m_o, sec = oracle_run(g)
     return {"value": m_o / sec, "unit": "edges/s", "cores": oracle.num_threads(), "kind": "oracle",
             "sample": f"whole workload ({g.name}, {g.arcs} raw arcs, m={m_o}), one run of the "
-                      f"oracle's clean+orient+forward, {sec:.2f} s", "seconds": sec, "T": T}
+                      f"oracle's clean+orient+forward, {sec:.2f} s", "seconds": sec, "T": T,
+            "host": host_cpu(), "single_thread": oracle_single_thread()}
 
 
 def reference_arm(args, g, rank, world):
@@ -155,14 +213,16 @@ def reference_arm(args, g, rank, world):
                                 f"; steps reduced to {k_eff} to stay within {budget_s:.0f} s") +
                                 "; each step = the oracle on the whole workload")},
             "cpu_baseline": {"value": value, "unit": "edges/s", "cores": oracle.num_threads(),
-                             "kind": "oracle", "sample": f"whole workload per step ({g.name})"},
+                             "kind": "oracle", "sample": f"whole workload per step ({g.name})",
+                             "host": host_cpu()},
             "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
-def _timed(torch, flush, stream, fn, reps=3):
-    """Mean CUDA-event ms of fn() over reps calls (L2 flushed before each), last result."""
+def _timed(torch, flush, stream, fn, reps=5):
+    """Median CUDA-event ms of fn() over reps calls (L2 flushed before each; one warm-up call
+    first), last result.  The median keeps one slow outlier from moving the figure."""
     fn()
-    tot, out = 0.0, None
+    ms, out = [], None
     for _ in range(reps):
         flush.fill_(3)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -170,8 +230,8 @@ def _timed(torch, flush, stream, fn, reps=3):
         out = fn()
         b.record(stream)
         torch.cuda.synchronize()
-        tot += a.elapsed_time(b)
-    return tot / reps, out
+        ms.append(a.elapsed_time(b))
+    return sorted(ms)[len(ms) // 2], out
 
 
 def clean_input_ms(tc, torch, rp, cl, flush, stream, T):
@@ -245,15 +305,81 @@ def next_rows_23(tc, torch, np, graphgen, rp, cl, flush, stream, m, T, count_ms)
     return rows
 
 
+# ------------------------------------------------------------------ a6 traffic (ncu, same run)
+A6_KERNELS = "regex:k_hash|k_short|k_merge|k_search"
+NCU_METRICS = ("dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
+               "l1tex__throughput.avg.pct_of_peak_sustained_elapsed,"
+               "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed,lts__t_sector_hit_rate.pct")
+
+
+def one_call(args):
+    """--one-call: ONE tc_count_ex on the bench workload (the process ncu profiles)."""
+    import numpy as np
+    import torch
+    import graphgen
+    import paper_1804_06926_b200 as tc
+    g = graphgen.rmat(args.scale, args.edge_factor)
+    rp = torch.from_numpy(g.rowptr.view(np.int64)).cuda()
+    cl = torch.from_numpy(g.col.view(np.int32)).cuda()
+    print("T", tc.count_ex(rp, cl), flush=True)
+
+
+def ncu_traffic(args):
+    """DRAM bytes of the a6 kernels of one step, captured by ncu in THIS bench run (a child
+    process, after the timed region; no timing is taken from it).  Also the bitmap kernel's
+    L1/shared-memory and DRAM throughput % (what bounds it) and its L2 hit rate."""
+    import csv
+    import io
+    import shutil
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return {"error": "ncu not found"}
+    cmd = [ncu, "--metrics", NCU_METRICS, "-k", A6_KERNELS, "--csv", "--print-units", "base",
+           "--clock-control", "none", sys.executable, os.path.abspath(__file__), "--one-call",
+           "--scale", str(args.scale), "--edge-factor", str(args.edge_factor)]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    except (OSError, subprocess.SubprocessError) as e:
+        return {"error": f"ncu failed: {e}"}
+    rows = [ln for ln in r.stdout.splitlines() if ln.startswith('"')]
+    if not rows:
+        return {"error": f"ncu produced no rows (rc {r.returncode}): {r.stderr[-300:]}"}
+    per = {}
+    for rec in csv.DictReader(io.StringIO("\n".join(rows))):
+        key = (rec["ID"], rec["Kernel Name"])
+        try:
+            per.setdefault(key, {})[rec["Metric Name"]] = float(rec["Metric Value"].replace(",", ""))
+        except ValueError:
+            pass
+    dram = sum(v.get("dram__bytes_read.sum", 0) + v.get("dram__bytes_write.sum", 0) for v in per.values())
+    ns = sum(v.get("gpu__time_duration.sum", 0) for v in per.values())
+    top = max(per.items(), key=lambda kv: kv[1].get("gpu__time_duration.sum", 0))
+    tv = top[1]
+    return {"dram_bytes": dram, "launches": len(per), "ncu_ms": ns * 1e-6,
+            "top_kernel": top[0][1].split("(")[0],
+            "top_l1tex_pct": tv.get("l1tex__throughput.avg.pct_of_peak_sustained_elapsed"),
+            "top_dram_pct": tv.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+            "top_l2_hit_pct": tv.get("lts__t_sector_hit_rate.pct"),
+            "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum (+ l1tex / dram "
+                      "throughput %, L2 hit rate) -k '%s' over one tc_count_ex of this workload, "
+                      "run by this bench.py after its timed region (cold caches)" % A6_KERNELS}
+
+
 # ------------------------------------------------------------------ native arm
 def main():
     args = parse()
+    if args.one_call:
+        return one_call(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_spawn(args))
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     import numpy as np
     import graphgen
 
+    if args.impl == "reference" and rank != 0:
+        return   # the reference arm (the CPU oracle) runs on rank 0 only
     g = graphgen.rmat(args.scale, args.edge_factor)
     if args.impl == "reference":
         line = reference_arm(args, g, rank, world)
@@ -263,6 +389,7 @@ def main():
 
     import torch
     import paper_1804_06926_b200 as tc
+    from paper_1804_06926_b200.dist import count_distributed
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
@@ -311,30 +438,54 @@ def main():
     ms = sum(step_ms) / len(step_ms)
     ix_ms = sum(s["ms_intersect"] for s in stats) / len(stats)
     bin_ms = sum(s["ms_bin"] for s in stats) / len(stats)
+    st = stats[-1]
+    # per-rank work statistics (tc_stats counts this rank's edges): summed over ranks
+    b_hash, b_alg_rank = st["bytes_hash"], st["bytes_alg"]
+    launches = st["kernel_launches"] * args.steps
     if dist is not None:
         t = torch.tensor([ms, ix_ms, bin_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, ix_ms, bin_ms = t.tolist()
-    st = stats[-1]
+        c = torch.tensor([b_hash, launches], dtype=torch.int64, device=dev)
+        dist.all_reduce(c)
+        b_hash, launches = (int(x) for x in c.tolist())
     m = st["m_undirected"]
-    launches = st["kernel_launches"] * args.steps
 
-    # ---- end to end through the public API with HOST buffers (pinned), N = 1 semantics per rank
+    # ---- end to end through the public API from pinned HOST buffers: every step copies the
+    # raw CSR host->device, runs the whole path (N > 1: this rank's shard + the allreduce, via
+    # count_distributed) and reads the count back; host wall clock, max over ranks
     e2e = None
     if not args.no_e2e:
         rp_h = torch.from_numpy(g.rowptr.view(np.int64)).pin_memory()
         cl_h = torch.from_numpy(g.col.view(np.int32)).pin_memory()
-        tc.count_ex(rp_h, cl_h)   # warm
+
+        def e2e_step():
+            if world == 1:
+                return tc.count_ex(rp_h, cl_h, with_stats=True)[0]
+            d_rp = rp_h.to(dev, non_blocking=True)
+            d_cl = cl_h.to(dev, non_blocking=True)
+            return count_distributed(d_rp, d_cl)
+
+        e2e_step()   # warm
         reps = max(3, min(args.steps, 5))
+        if dist is not None:
+            dist.barrier()
         t0 = time.perf_counter()
         for _ in range(reps):
-            got = tc.count_ex(rp_h, cl_h, with_stats=True)
+            got = e2e_step()
         e2e_s = (time.perf_counter() - t0) / reps
-        assert got[0] == T_total
+        assert got == T_total
+        if dist is not None:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = t.item()
+        in_bytes = g.rowptr.nbytes + g.col.nbytes
         e2e = {"value": m / e2e_s, "unit": "edges/s", "ms_per_step": 1e3 * e2e_s,
-               "h2d_bytes_per_step": got[1]["h2d_bytes"], "d2h_bytes_per_step": got[1]["d2h_bytes"],
-               "note": "tc_count_ex with TC_HOST_PTRS from pinned host memory: H2D of the raw CSR, "
-                       "the whole path, D2H of the count; host wall clock, single GPU per rank"}
+               "h2d_bytes_per_step": in_bytes * world, "d2h_bytes_per_step": 8 * world,
+               "note": ("tc_count_ex with TC_HOST_PTRS from pinned host memory" if world == 1 else
+                        "count_distributed: per rank H2D of the raw CSR (non_blocking from pinned), "
+                        "tc_count_shard, NCCL allreduce, .item()") +
+                       "; host wall clock per step, max over ranks"}
 
     if rank != 0:
         if dist is not None:
@@ -342,10 +493,35 @@ def main():
         return
 
     peak, peak_kind = load_peaks()
-    b_alg = st["bytes_alg"]
-    b_hash = st["bytes_hash"]
+    b_alg = st["bytes_alg"] if world == 1 else None
     achieved = b_hash / (ix_ms * 1e-3) / 1e9 / world  # GB/s per GPU
-    achieved_alg = b_alg / (ix_ms * 1e-3) / 1e9 / world
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None,
+            "kernel": "a6+a7 intersection phase (k_hash_cta bitmap + hash, k_hash_warp, k_short "
+                      "[+ empty MERGE/SEARCH launches]), CUDA events on the launch stream",
+            "bytes_model": "B_hash = 4*sum min(|N+(u)>v|, d+v) + 8*HASH edges + 4*table loads "
+                           "(bytes the implemented a6 must read; DESIGN.md sec. 5), summed over ranks",
+            "bytes_hash": b_hash, "kernel_ms": ix_ms, "bin_ms": bin_ms, "peak_kind": peak_kind,
+            "work_W": st["work_W"], "work_probe": st["work_probe"], "table_loads": st["table_loads"]}
+    if b_alg:
+        a_alg = b_alg / (ix_ms * 1e-3) / 1e9
+        roof["survey_B_alg"] = {"bytes": b_alg, "model": "4W + 16m (SURVEY.md 8(d), merge-based)",
+                                "achieved": a_alg, "frac": a_alg / peak,
+                                "frac_incl_binning": b_alg / ((ix_ms + bin_ms) * 1e-3) / 1e9 / peak}
+        b_stage = 4 * (m + st["work_stage"]) + 16 * m
+        roof["survey_B_stage"] = {"bytes": b_stage, "model": "4(m + sum d-(v) d+(v)) + 16m (SURVEY.md 8(d))",
+                                  "frac": b_stage / (ix_ms * 1e-3) / 1e9 / peak}
+    if world == 1 and not args.no_ncu:
+        tr = ncu_traffic(args)
+        roof["ncu"] = tr
+        if "dram_bytes" in tr:
+            roof["traffic"] = tr["dram_bytes"]
+            roof["dram_frac"] = tr["dram_bytes"] / (ix_ms * 1e-3) / 1e9 / peak
+            l1, dr = tr.get("top_l1tex_pct") or 0.0, tr.get("top_dram_pct") or 0.0
+            # what ncu says binds the dominant kernel (report it, not "hbm")
+            roof["bound"] = "l1/smem" if l1 > dr else "hbm"
+            roof["bound_evidence"] = (f"{tr['top_kernel']}: L1TEX/shared {l1:.1f}% vs DRAM {dr:.1f}% "
+                                      f"of peak, L2 hit {tr.get('top_l2_hit_pct') or 0:.1f}%")
     line = {
         "metric": METRIC, "value": m / (ms * 1e-3), "unit": "edges/s", "n_gpus": world,
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
@@ -355,59 +531,24 @@ def main():
                    "parallelism": f"replicated graph, work-split sources x{world}",
                    "l2": "flushed between timed steps (512 MiB write outside the event spans)",
                    "step": "tc_count_ex on raw arcs: clean, orient, bin, intersect, reduce"
-                           + (" + NCCL allreduce" if world > 1 else "")},
+                           + (" (tc_count_shard per rank) + NCCL allreduce" if world > 1 else "")},
         "phases_ms": {k: sum(s[k] for s in stats) / len(stats)
                       for k in ("ms_clean", "ms_orient", "ms_sort", "ms_bin", "ms_intersect", "ms_total")},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
-                     "kernel": "a6+a7 intersection phase (k_hash_cta bitmap + hash, k_hash_warp "
-                               "[+ empty SHORT/MERGE/SEARCH launches]), CUDA events on the launch stream",
-                     "bytes_model": "B_hash = 4*sum min(|N+(u)>v|, d+v) + 8*HASH edges + 4*table loads "
-                                    "(bytes the implemented a6 must read; DESIGN.md sec. 5)",
-                     "bytes_hash": b_hash, "kernel_ms": ix_ms, "bin_ms": bin_ms, "peak_kind": peak_kind,
-                     "survey_B_alg": {"bytes": b_alg, "model": "4W + 16m (SURVEY.md 8(d), merge-based)",
-                                      "achieved": achieved_alg, "frac": achieved_alg / peak,
-                                      "frac_incl_binning": b_alg / ((ix_ms + bin_ms) * 1e-3) / 1e9 / world / peak},
-                     "survey_B_stage": {"bytes": 4 * (m + st["work_stage"]) + 16 * m,
-                                        "model": "4(m + sum d-(v) d+(v)) + 16m (SURVEY.md 8(d))",
-                                        "frac": (4 * (m + st["work_stage"]) + 16 * m)
-                                                / (ix_ms * 1e-3) / 1e9 / world / peak},
-                     "work_W": st["work_W"], "work_probe": st["work_probe"],
-                     "table_loads": st["table_loads"]},
+        "step_ms_min_max": [min(step_ms), max(step_ms)],
+        "roofline": roof,
         "gpu_launches": launches,
         "e2e": e2e,
         "clocks": clocks,
     }
-    tf = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tf):
-        try:
-            tr = json.load(open(tf)).get(g.name)
-            if tr:
-                line["roofline"]["traffic"] = tr["dram_bytes_per_launch"]
-                line["roofline"]["traffic_source"] = tr["source"]
-                for k in ("bitmap_kernel_l2_hit_pct", "bitmap_kernel_dram_throughput_pct"):
-                    if tr.get(k) is not None:
-                        line["roofline"][k] = tr[k]
-        except (OSError, ValueError):
-            pass
     if world == 1 and not args.no_next:
-        # NEXT-1: clustering coefficients + transitivity on the same
-        # workload through tc_clustering (count with t(v), then the c(v) kernel)
-        cev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(3)]
-        tc.clustering(rp, cl)
-        for a, b in cev:
-            flush.fill_(1)
-            a.record(stream)
-            _, summ = tc.clustering(rp, cl)
-            b.record(stream)
-        torch.cuda.synchronize()
-        cms = sum(a.elapsed_time(b) for a, b in cev) / len(cev)
+        # NEXT-1: clustering coefficients + transitivity on the same workload
+        # through tc_clustering (count with t(v), then the c(v) kernel); median of 5 calls
+        cms, (_, summ) = _timed(torch, flush, stream, lambda: tc.clustering(rp, cl))
         assert summ["triangles"] == T_total
         line["next_rows"] = {"NEXT-1 clustering": {
             "ms_per_call": cms, "edges_per_s": m / (cms * 1e-3), "overhead_vs_count_ms": cms - ms,
             "transitivity": summ["transitivity"], "avg_clustering": summ["avg_clustering"],
-            "wedges": summ["wedges"],
+            "wedges": summ["wedges"], "timing": "median of 5 calls, L2 flushed before each",
             "call": "tc_clustering (device pointers): count with per-vertex t(v) + local c(v) for all n"}}
         line["survey_clean_input"] = clean_input_ms(tc, torch, rp, cl, flush, stream, T_total)
         line["next_rows"].update(next_rows_23(tc, torch, np, graphgen, rp, cl, flush, stream, m,

@@ -35,11 +35,17 @@
  * the fastest copies) and the library copies them in and results out.
  * Inputs are borrowed, read-only, and must stay valid for the call.
  *
- * OWNERSHIP: the library allocates its own workspace with cudaMallocAsync on
- * the call's stream and frees it before returning.  Outputs are
- * caller-allocated.  tc_count / tc_count_ex / tc_orient are synchronous (they
- * return once results are on their destination); tc_count_shard is
- * stream-ordered (its device result is ready when the stream reaches it).
+ * OWNERSHIP: outputs are caller-allocated.  Device workspace comes from
+ * tc_options.alloc / .free when the caller supplies them (the Python
+ * binding passes torch's caching allocator), called on the call's stream and every
+ * block freed before the call returns (stream-ordered: a block is released with the
+ * stream that may still use it, exactly like cudaFreeAsync).  Without a hook the
+ * workspace comes from a memory pool the LIBRARY creates per device (never the
+ * process's default pool); with tc_options.keep_workspace = 1 (the default) that pool
+ * keeps freed memory for the next call, tc_trim_workspace() returns it to the driver.
+ * tc_count / tc_count_ex / tc_orient are synchronous (they return once results are
+ * on their destination); tc_count_shard is stream-ordered (its device result is
+ * ready when the stream reaches it).
  *
  * ERRORS: every entry point validates its arguments (null pointers, n >= 2^32,
  * unknown flag bits, bad options) and returns TC_EINVAL before
@@ -50,8 +56,13 @@
  * claim, is undefined behaviour.  CUDA failures return TC_ECUDA, allocation
  * failures TC_ENOMEM.  tc_last_error() gives a thread-local message.
  *
- * THREAD SAFETY: calls on different streams or devices are independent; the
- * only global state is the thread-local error string.
+ * DEVICE: device pointers must belong to the current CUDA device (checked:
+ * TC_EINVAL otherwise); all work runs there.
+ *
+ * THREAD SAFETY: calls on different streams or devices are independent.  Global
+ * state: the thread-local error string and pinned read-back scratch, a per-thread
+ * side stream per device, the per-device SM count and the per-device library
+ * workspace pool (both created once, under a lock).
  */
 #ifndef TC_B200_H
 #define TC_B200_H
@@ -108,16 +119,26 @@ enum {
                               a warp per small owner, a CTA per hub owner (north_star)        */
 };
 
+/* Workspace allocator hook.  alloc returns `bytes` of device memory on
+ * the current device usable in stream order on `stream` (NULL on failure -> TC_ENOMEM);
+ * free releases a block returned by alloc, stream-ordered on `stream` (the block may
+ * still be read by work enqueued on `stream` before the call).  `ctx` is alloc_ctx. */
+typedef void *(*tc_alloc_fn)(void *ctx, size_t bytes, void *stream);
+typedef void (*tc_free_fn)(void *ctx, void *ptr, void *stream);
+
 typedef struct {
     uint32_t short_max;         /* AUTO: edge -> SHORT if max(d+u, d+v) <= short_max           */
     uint32_t skew_ratio;        /* AUTO: edge -> SEARCH if max >= skew_ratio * min (0 = never)  */
     uint32_t hub_min_dplus;     /* HASH owners with d+ >= this get a whole CTA (capped at 129)  */
     int32_t force_variant;      /* TC_VARIANT_AUTO, or route EVERY edge to one variant          */
     void *stream;               /* cudaStream_t to run on; NULL = legacy default stream         */
-    uint32_t segsort_block_max; /* ignored (kept for layout stability): rows are sorted by the
-                                   two-key radix sort of a3/a4 on every path                 */
     uint32_t prune_rounds;      /* TC_PRUNE: rounds to run; 0 = to the fixed point (one 8-byte
                                    device->host read per round)                               */
+    uint32_t keep_workspace;    /* no hook: 1 = the library pool keeps freed workspace for the
+                                   next call (default), 0 = release it when the call ends     */
+    tc_alloc_fn alloc;          /* workspace hook (both or neither); NULL = library pool       */
+    tc_free_fn free;
+    void *alloc_ctx;            /* passed to alloc / free                                       */
     uint32_t reserved[8];       /* must be zero                                                 */
 } tc_options;
 
@@ -264,6 +285,10 @@ tc_status tc_masked_spgemm(uint64_t n, uint64_t m, const uint64_t *row_offsets,
 
 /* Thread-local message describing the last failure on this thread ("" if none). */
 const char *tc_last_error(void);
+
+/* Return the library pool's cached workspace on `device` (-1 = current device) to the
+ * driver.  Safe at any time; calls in flight keep what they hold. */
+tc_status tc_trim_workspace(int device);
 
 /* Library version string. */
 const char *tc_version(void);

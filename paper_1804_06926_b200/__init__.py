@@ -20,7 +20,7 @@ import numpy as np
 __all__ = ["count", "count_ex", "count_shard", "orient", "clustering", "edge_support",
            "enumerate_triangles", "stats_dict", "library_path",
            "TC_CLEAN", "TC_SORTED", "TC_PER_VERTEX", "TC_HOST_PTRS", "TC_VALIDATE", "TC_PRUNE",
-           "TC_ID_ORDER", "masked_spgemm",
+           "TC_ID_ORDER", "masked_spgemm", "trim_workspace",
            "VARIANT_AUTO", "VARIANT_SHORT", "VARIANT_MERGE", "VARIANT_SEARCH", "VARIANT_HASH",
            "TCError"]
 
@@ -40,11 +40,50 @@ class TCError(RuntimeError):
         self.status = status
 
 
+# tc_alloc_fn / tc_free_fn (include/tc.h): workspace hook
+ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
+
+
 class Options(ctypes.Structure):
     _fields_ = [("short_max", ctypes.c_uint32), ("skew_ratio", ctypes.c_uint32),
                 ("hub_min_dplus", ctypes.c_uint32), ("force_variant", ctypes.c_int32),
-                ("stream", ctypes.c_void_p), ("segsort_block_max", ctypes.c_uint32),
-                ("prune_rounds", ctypes.c_uint32), ("reserved", ctypes.c_uint32 * 8)]
+                ("stream", ctypes.c_void_p), ("prune_rounds", ctypes.c_uint32),
+                ("keep_workspace", ctypes.c_uint32), ("alloc", ALLOC_FN), ("free", FREE_FN),
+                ("alloc_ctx", ctypes.c_void_p), ("reserved", ctypes.c_uint32 * 8)]
+
+
+def _torch_raw_alloc(ctx, size, stream):
+    import torch
+    try:   # torch's caching allocator, current device, block tied to `stream`
+        return torch._C._cuda_cudaCachingAllocator_raw_alloc(size, stream or 0)
+    except Exception:   # noqa: BLE001 -- a NULL return is the hook's error signal (TC_ENOMEM)
+        return None
+
+
+def _torch_raw_free(ctx, ptr, stream):
+    import torch
+    torch._C._cuda_cudaCachingAllocator_raw_delete(ptr)
+
+
+# kept alive for the life of the module (ctypes callbacks must not be collected)
+_TORCH_HOOK = (ALLOC_FN(_torch_raw_alloc), FREE_FN(_torch_raw_free))
+_user_hooks = []
+
+
+def _hook_pair(allocator):
+    """allocator: "torch" (torch's caching allocator), "library" (the library's own pool), or a
+    pair of Python callables alloc(size, stream) -> int pointer and free(ptr, stream)."""
+    if allocator == "torch":
+        return _TORCH_HOOK
+    if allocator in (None, "library"):
+        return None
+    a, f = allocator
+    pair = (ALLOC_FN(lambda _c, size, stream: a(size, stream)),
+            FREE_FN(lambda _c, ptr, stream: f(ptr, stream)))
+    _user_hooks.append(pair)
+    del _user_hooks[:-8]   # the last few stay referenced while their calls may run
+    return pair
 
 
 class Stats(ctypes.Structure):
@@ -109,6 +148,8 @@ def _load():
     lib.tc_masked_spgemm.restype = ctypes.c_int
     lib.tc_last_error.argtypes = []
     lib.tc_last_error.restype = ctypes.c_char_p
+    lib.tc_trim_workspace.argtypes = [ctypes.c_int]
+    lib.tc_trim_workspace.restype = ctypes.c_int
     lib.tc_version.argtypes = []
     lib.tc_version.restype = ctypes.c_char_p
     _lib = lib
@@ -152,13 +193,20 @@ def _flags(clean=False, sorted_rows=False, per_vertex=False, validate=False, pru
 
 
 def _options(stream=None, force_variant=None, short_max=None, skew_ratio=None, hub_min_dplus=None,
-             segsort_block_max=None, prune_rounds=None, on_device=True):
+             prune_rounds=None, on_device=True, allocator=None, device=None, keep_workspace=None):
+    """tc_options for one call.  Device calls default to the current stream of the inputs'
+    device and to torch's caching allocator for the workspace."""
     o = Options()
     _load().tc_default_options(ctypes.byref(o))
     if stream is None and on_device:
         import torch
-        stream = torch.cuda.current_stream().cuda_stream
+        stream = torch.cuda.current_stream(device).cuda_stream
     o.stream = stream or None
+    if allocator is None and on_device:
+        allocator = "torch"
+    hooks = _hook_pair(allocator)
+    if hooks is not None:
+        o.alloc, o.free = hooks
     if force_variant is not None:
         o.force_variant = force_variant
     if short_max is not None:
@@ -167,11 +215,25 @@ def _options(stream=None, force_variant=None, short_max=None, skew_ratio=None, h
         o.skew_ratio = skew_ratio
     if hub_min_dplus is not None:
         o.hub_min_dplus = hub_min_dplus
-    if segsort_block_max is not None:
-        o.segsort_block_max = segsort_block_max
     if prune_rounds is not None:
         o.prune_rounds = prune_rounds
+    if keep_workspace is not None:
+        o.keep_workspace = int(bool(keep_workspace))
     return o
+
+
+def _dev(keep, on_dev):
+    return keep[0].device if on_dev else None
+
+
+def _in_dev(keep, on_dev, call):
+    """Run the C call with the inputs' CUDA device current (the library works on the current
+    device; tc.h DEVICE)."""
+    if not on_dev:
+        return call()
+    import torch
+    with torch.cuda.device(keep[0].device):
+        return call()
 
 
 def stats_dict(s: Stats) -> dict:
@@ -193,7 +255,7 @@ def count_ex(rowptr, col, *, clean=False, sorted_rows=False, per_vertex=False, v
             (TC_PER_VERTEX if per_vertex else 0) | (TC_VALIDATE if validate else 0) | \
             (TC_PRUNE if prune else 0) | (TC_ID_ORDER if id_order else 0) | \
             (0 if on_dev else TC_HOST_PTRS)
-    o = _options(stream=stream, on_device=on_dev, **opts)
+    o = _options(stream=stream, on_device=on_dev, device=_dev(keep, on_dev), **opts)
     total = ctypes.c_uint64(0)
     pv = None
     pv_ptr = None
@@ -206,8 +268,8 @@ def count_ex(rowptr, col, *, clean=False, sorted_rows=False, per_vertex=False, v
             pv = np.zeros(max(n, 1), dtype=np.uint64)
             pv_ptr = pv.ctypes.data
     st = Stats()
-    _check(lib.tc_count_ex(n, M, rp, cp, flags, ctypes.byref(o), ctypes.addressof(total), pv_ptr,
-                           ctypes.byref(st) if with_stats else None))
+    _check(_in_dev(keep, on_dev, lambda: lib.tc_count_ex(n, M, rp, cp, flags, ctypes.byref(o), ctypes.addressof(total), pv_ptr,
+                           ctypes.byref(st) if with_stats else None)))
     out = [int(total.value)]
     if per_vertex:
         out.append(pv[:n])
@@ -230,11 +292,11 @@ def count_shard(rowptr, col, rank: int, world: int, partial, *, clean=False, sor
         raise ValueError("count_shard takes CUDA tensors")
     flags = (TC_CLEAN if clean else 0) | (TC_SORTED if sorted_rows else 0) | \
             (TC_PER_VERTEX if per_vertex_partial is not None else 0) | (TC_PRUNE if prune else 0)
-    o = _options(stream=stream, **opts)
+    o = _options(stream=stream, device=_dev(keep, on_dev), **opts)
     st = Stats()
-    _check(lib.tc_count_shard(n, M, rp, cp, flags, ctypes.byref(o), rank, world, partial.data_ptr(),
+    _check(_in_dev(keep, on_dev, lambda: lib.tc_count_shard(n, M, rp, cp, flags, ctypes.byref(o), rank, world, partial.data_ptr(),
                               per_vertex_partial.data_ptr() if per_vertex_partial is not None else None,
-                              ctypes.byref(st) if with_stats else None))
+                              ctypes.byref(st) if with_stats else None)))
     return stats_dict(st) if with_stats else None
 
 
@@ -245,19 +307,19 @@ def orient(rowptr, col, *, clean=False, sorted_rows=False, prune=False, id_order
     lib = _load()
     n, M, rp, cp, on_dev, keep = _arrays(rowptr, col)
     flags = _flags(clean, sorted_rows, False, False, prune, id_order, on_dev)
-    o = _options(stream=stream, on_device=on_dev, **opts)
+    o = _options(stream=stream, on_device=on_dev, device=_dev(keep, on_dev), **opts)
     mp = ctypes.c_uint64(0)
     if on_dev:
         import torch
         off = torch.empty(n + 1, dtype=torch.int64, device=keep[0].device)
         colp = torch.empty(max(M, 1), dtype=torch.int32, device=keep[0].device)
-        _check(lib.tc_orient(n, M, rp, cp, flags, ctypes.byref(o), off.data_ptr(), colp.data_ptr(),
-                             ctypes.addressof(mp)))
+        _check(_in_dev(keep, on_dev, lambda: lib.tc_orient(n, M, rp, cp, flags, ctypes.byref(o), off.data_ptr(), colp.data_ptr(),
+                             ctypes.addressof(mp))))
     else:
         off = np.zeros(n + 1, dtype=np.uint64)
         colp = np.zeros(max(M, 1), dtype=np.uint32)
-        _check(lib.tc_orient(n, M, rp, cp, flags, ctypes.byref(o), off.ctypes.data, colp.ctypes.data,
-                             ctypes.addressof(mp)))
+        _check(_in_dev(keep, on_dev, lambda: lib.tc_orient(n, M, rp, cp, flags, ctypes.byref(o), off.ctypes.data, colp.ctypes.data,
+                             ctypes.addressof(mp))))
     return off, colp[:mp.value]
 
 
@@ -274,7 +336,7 @@ def clustering(rowptr, col, *, clean=False, sorted_rows=False, validate=False, p
     flags = (TC_CLEAN if clean else 0) | (TC_SORTED if sorted_rows else 0) | \
             (TC_VALIDATE if validate else 0) | (TC_PRUNE if prune else 0) | \
             (0 if on_dev else TC_HOST_PTRS)
-    o = _options(stream=stream, on_device=on_dev, **opts)
+    o = _options(stream=stream, on_device=on_dev, device=_dev(keep, on_dev), **opts)
     cc = pv = None
     if on_dev:
         import torch
@@ -292,8 +354,8 @@ def clustering(rowptr, col, *, clean=False, sorted_rows=False, validate=False, p
         ptr = lambda a: a.ctypes.data if a is not None else None  # noqa: E731
     summ = ClusteringSummary()
     st = Stats()
-    _check(lib.tc_clustering(n, M, rp, cp, flags, ctypes.byref(o), ptr(cc), ptr(pv), ctypes.byref(summ),
-                             ctypes.byref(st) if with_stats else None))
+    _check(_in_dev(keep, on_dev, lambda: lib.tc_clustering(n, M, rp, cp, flags, ctypes.byref(o), ptr(cc), ptr(pv), ctypes.byref(summ),
+                             ctypes.byref(st) if with_stats else None)))
     out = [cc[:n] if cc is not None else None,
            {f: getattr(summ, f) for f, _ in ClusteringSummary._fields_}]
     if per_vertex:
@@ -313,7 +375,7 @@ def edge_support(rowptr, col, *, clean=False, sorted_rows=False, validate=False,
     flags = (TC_CLEAN if clean else 0) | (TC_SORTED if sorted_rows else 0) | \
             (TC_VALIDATE if validate else 0) | (TC_PRUNE if prune else 0) | \
             (0 if on_dev else TC_HOST_PTRS)
-    o = _options(stream=stream, on_device=on_dev, **opts)
+    o = _options(stream=stream, on_device=on_dev, device=_dev(keep, on_dev), **opts)
     mp = ctypes.c_uint64(0)
     st = Stats()
     if on_dev:
@@ -328,8 +390,8 @@ def edge_support(rowptr, col, *, clean=False, sorted_rows=False, validate=False,
         colp = np.zeros(max(M, 1), dtype=np.uint32)
         sup = np.zeros(max(M, 1), dtype=np.uint32)
         ptrs = (off.ctypes.data, colp.ctypes.data, sup.ctypes.data)
-    _check(lib.tc_edge_support(n, M, rp, cp, flags, ctypes.byref(o), *ptrs, ctypes.addressof(mp),
-                               ctypes.byref(st) if with_stats else None))
+    _check(_in_dev(keep, on_dev, lambda: lib.tc_edge_support(n, M, rp, cp, flags, ctypes.byref(o), *ptrs, ctypes.addressof(mp),
+                               ctypes.byref(st) if with_stats else None)))
     out = (off, colp[:mp.value], sup[:mp.value])
     return out + (stats_dict(st),) if with_stats else out
 
@@ -345,14 +407,14 @@ def enumerate_triangles(rowptr, col, *, capacity=None, out=None, clean=False, so
     flags = (TC_CLEAN if clean else 0) | (TC_SORTED if sorted_rows else 0) | \
             (TC_VALIDATE if validate else 0) | (TC_PRUNE if prune else 0) | \
             (0 if on_dev else TC_HOST_PTRS)
-    o = _options(stream=stream, on_device=on_dev, **opts)
+    o = _options(stream=stream, on_device=on_dev, device=_dev(keep, on_dev), **opts)
     total = ctypes.c_uint64(0)
     st = Stats()
     if out is not None:
         capacity = len(out)
     if capacity is None:
-        _check(lib.tc_enumerate(n, M, rp, cp, flags, ctypes.byref(o), None, 0,
-                                ctypes.addressof(total), None))
+        _check(_in_dev(keep, on_dev, lambda: lib.tc_enumerate(n, M, rp, cp, flags, ctypes.byref(o), None, 0,
+                                ctypes.addressof(total), None)))
         capacity = total.value
     if out is not None:
         tri = out
@@ -364,8 +426,8 @@ def enumerate_triangles(rowptr, col, *, capacity=None, out=None, clean=False, so
     else:
         tri = np.zeros((max(capacity, 1), 3), dtype=np.uint32)
         tp = tri.ctypes.data
-    _check(lib.tc_enumerate(n, M, rp, cp, flags, ctypes.byref(o), tp, capacity,
-                            ctypes.addressof(total), ctypes.byref(st) if with_stats else None))
+    _check(_in_dev(keep, on_dev, lambda: lib.tc_enumerate(n, M, rp, cp, flags, ctypes.byref(o), tp, capacity,
+                            ctypes.addressof(total), ctypes.byref(st) if with_stats else None)))
     out = (int(total.value), tri[:min(total.value, capacity)])
     return out + (stats_dict(st),) if with_stats else out
 
@@ -378,7 +440,7 @@ def masked_spgemm(rowptr, col, *, id_order=False, clean=False, sorted_rows=False
     lib = _load()
     n, M, rp, cp, on_dev, keep = _arrays(rowptr, col)
     flags = _flags(clean, sorted_rows, False, validate, prune, id_order, on_dev)
-    o = _options(stream=stream, on_device=on_dev, **opts)
+    o = _options(stream=stream, on_device=on_dev, device=_dev(keep, on_dev), **opts)
     nnz = ctypes.c_uint64(0)
     total = ctypes.c_uint64(0)
     st = Stats()
@@ -394,10 +456,15 @@ def masked_spgemm(rowptr, col, *, id_order=False, clean=False, sorted_rows=False
         colp = np.zeros(max(M, 1), dtype=np.uint32)
         c = np.zeros(max(M, 1), dtype=np.uint32)
         ptrs = (off.ctypes.data, colp.ctypes.data, c.ctypes.data)
-    _check(lib.tc_masked_spgemm(n, M, rp, cp, flags, ctypes.byref(o), *ptrs, ctypes.addressof(nnz),
-                                ctypes.addressof(total), ctypes.byref(st) if with_stats else None))
+    _check(_in_dev(keep, on_dev, lambda: lib.tc_masked_spgemm(n, M, rp, cp, flags, ctypes.byref(o), *ptrs, ctypes.addressof(nnz),
+                                ctypes.addressof(total), ctypes.byref(st) if with_stats else None)))
     out = (off, colp[:nnz.value], c[:nnz.value], int(total.value))
     return out + (stats_dict(st),) if with_stats else out
+
+
+def trim_workspace(device: int = -1) -> None:
+    """Return the library pool's cached workspace on `device` to the driver (tc_trim_workspace)."""
+    _check(_load().tc_trim_workspace(device))
 
 
 def version() -> str:

@@ -102,11 +102,14 @@ __global__ void __launch_bounds__(kTileThreads)
                 uint32_t u = us[j], x = xs[j], dv = dvs[j];
                 uint64_t ue = ues[j];
                 uint32_t du = (uint32_t)(ue - ubs[j]), suf = (uint32_t)(ue - e - 1);
-                W += du + dv;
-                probe += min(suf, dv);
-                bin = edge_bin(hp, du, dv, suf);
-                skipped += bin < 0;
-                if (bin >= 0 && rank_owner(hp, chunk, u) != hp.rank) bin = -1;
+                // statistics count this rank's edges only (per-rank scope at world > 1)
+                const bool mine = hp.world <= 1 || rank_owner(hp, chunk, u) == hp.rank;
+                if (mine) {
+                    W += du + dv;
+                    probe += min(suf, dv);
+                }
+                bin = mine ? edge_bin(hp, du, dv, suf) : -1;
+                skipped += mine && bin < 0;
                 item = make_uint2(u, x);
                 uint32_t ri = 0;
                 if (bin == TC_VARIANT_HASH) {

@@ -876,8 +876,8 @@ static void launch_all(Ctx &ctx, const Oriented &g, const Bins &bins, uint64_t *
     // The bitmap hub kernel (most of the work) goes first on the call's stream; the
     // independent warp-owner / SHORT / MERGE / SEARCH kernels run on a side stream and
     // fill the SMs the hub kernel's tail leaves idle (all add into the same total).
-    cudaStream_t s2 = ctx.side();
-    if (s2 != ctx.stream) ctx.fork(s2);   // the side work depends only on binning
+    SideStream side(ctx);   // the side work depends only on binning; joined on every path
+    cudaStream_t s2 = side.s;
     k_hash_cta<CM, true><<<ctx.persistent_grid(8), kIxThreads, 0, ctx.stream>>>(
         bins.tasks_bitmap, bins.ntasks_bitmap, bins.hp, total, cr);
     TC_LAUNCHED(ctx);
@@ -892,7 +892,7 @@ static void launch_all(Ctx &ctx, const Oriented &g, const Bins &bins, uint64_t *
     TC_LAUNCHED(ctx);
     k_short<CM><<<grid, kIxThreads, 0, s2>>>(bins.edges[0], bins.count + 0, g.off, g.col, total, cr);
     TC_LAUNCHED(ctx);
-    if (s2 != ctx.stream) ctx.join(s2);
+    side.join();
 }
 
 void intersect_all(Ctx &ctx, const Oriented &g, const Bins &bins, uint64_t *total_dev,

@@ -264,16 +264,47 @@ __global__ void k_dminus(const uint32_t *__restrict__ deg, const uint32_t *__res
 // searched for.  dplus / dminus already counted.
 
 // hist_src / hist_tgt (optional): digit histograms of okey / oval (fused by the producer).
+// d-(x) = length of x's run in the target-sorted pairs (clean input: counted from the pairs
+// actually written, so in_off stays consistent with them even under a false TC_CLEAN claim).
+// Two atomics per run: +end at its last element, -start at its first.
+__global__ void k_runs_dminus(const uint32_t *__restrict__ tgt, const uint64_t *__restrict__ m_dev,
+                              uint32_t *__restrict__ dminus) {
+    const uint64_t m = *m_dev;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t x = tgt[i];
+        if (i + 1 == m || tgt[i + 1] != x) atomicAdd(&dminus[x], (uint32_t)(i + 1));
+        if (i == 0 || tgt[i - 1] != x) atomicSub(&dminus[x], (uint32_t)i);
+    }
+}
+
+// sum_x d-(x) d+(x) (stats: SURVEY 8(d)'s B_stage), rank ids, one atomic per warp.
+__global__ void k_stage_work(const uint32_t *__restrict__ dplus, const uint32_t *__restrict__ dminus,
+                             uint64_t n, uint64_t *__restrict__ stage) {
+    uint64_t acc = 0;
+    for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n;
+         x += (uint64_t)gridDim.x * blockDim.x)
+        acc += (uint64_t)dminus[x] * dplus[x];
+    acc = warp_sum_u64(acc);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd((unsigned long long *)stage, (unsigned long long)acc);
+}
+
 static void pairs_to_csr(Ctx &ctx, uint64_t n, uint64_t cap, uint32_t *okey, uint32_t *oval,
                          uint32_t *dplus, uint32_t *dminus, uint64_t *m_dev, Oriented &out,
                          Timer *tm, const uint32_t *hist_src = nullptr,
-                         const uint32_t *hist_tgt = nullptr) {
+                         const uint32_t *hist_tgt = nullptr, bool count_dminus = false) {
     int b = id_bits(n);
     int grid = ctx.persistent_grid(8);
     uint32_t *okey2 = ctx.alloc<uint32_t>(cap), *oval2 = ctx.alloc<uint32_t>(cap);
     // 1) by target (keys = oval, values = okey): T = (targets, sources) = transposed CSR
     bool a1 = radix_sort_pairs(ctx, oval, oval2, okey, okey2, cap, m_dev, b, hist_tgt);
     uint32_t *t_tgt = a1 ? oval2 : oval, *t_src = a1 ? okey2 : okey;
+    if (count_dminus) {
+        k_runs_dminus<<<grid, 256, 0, ctx.stream>>>(t_tgt, m_dev, dminus);
+        TC_LAUNCHED(ctx);
+        k_stage_work<<<grid, 256, 0, ctx.stream>>>(dplus, dminus, n, out.stage_work);
+        TC_LAUNCHED(ctx);
+    }
     uint32_t *f_key = a1 ? oval : oval2, *f_val = a1 ? okey : okey2;   // free pair
     // 2) stable by source of T's index p (values = p, generated by the first pass),
     // reading T without modifying it; the last pass also gathers col+[e] = T.target[p]
@@ -373,7 +404,8 @@ __global__ void __launch_bounds__(kTileThreads)
                   uint64_t *__restrict__ status, uint64_t *__restrict__ m_out,
                   uint32_t *__restrict__ okey, uint32_t *__restrict__ oval,
                   uint32_t *__restrict__ dplus, uint32_t *__restrict__ hist_key,
-                  uint32_t *__restrict__ hist_val, int passes, int db) {
+                  uint32_t *__restrict__ hist_val, int passes, int db, uint64_t cap,
+                  uint32_t *__restrict__ claim_err) {
     __shared__ uint32_t s_row[kTileItems];
     __shared__ uint32_t s_scan[kTileThreads / 32];
     __shared__ uint32_t s_tile;
@@ -421,7 +453,14 @@ __global__ void __launch_bounds__(kTileThreads)
             }
             if (lane == 0) {
                 s_excl = excl;
-                if (tile + 1 == tiles) *m_out = excl + total;
+                if (tile + 1 == tiles) {
+                    // a simple symmetric graph keeps exactly one arc per edge, M/2 < cap;
+                    // more means a false TC_CLEAN claim: clamp (nothing is written at or
+                    // past cap) and report TC_EGRAPH at the end of the call
+                    const uint64_t kept = excl + total;
+                    if (kept >= cap) *claim_err = 1u;
+                    *m_out = kept < cap ? kept : cap;
+                }
             }
         }
         __syncthreads();
@@ -429,7 +468,7 @@ __global__ void __launch_bounds__(kTileThreads)
         uint32_t run_s = 0, run_n = 0;
 #pragma unroll
         for (int k = 0; k < kItemsPerThread; k++) {
-            if (f[k]) {
+            if (f[k] && base < cap) {
                 const uint32_t sv = newid[s_row[i0 + k]], tv = newid[v[k]];
                 okey[base] = sv;
                 oval[base] = tv;
@@ -470,8 +509,9 @@ void orient_clean(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, cons
     const uint32_t *key = rank_key(ctx, n, deg, id_order);
     rank_permutation(ctx, n, key, out);
     // status words [0, tiles), the ticket, m at the end; histograms of both pair sorts
-    uint64_t *st = ctx.alloc<uint64_t>(tiles + 2);
-    TC_CUDA(cudaMemsetAsync(st, 0, (tiles + 2) * sizeof(uint64_t), ctx.stream));
+    uint64_t *st = ctx.alloc<uint64_t>(tiles + 3);   // + the false-claim flag
+    TC_CUDA(cudaMemsetAsync(st, 0, (tiles + 3) * sizeof(uint64_t), ctx.stream));
+    out.claim_err = (uint32_t *)(st + tiles + 2);
     const int b = id_bits(n), pdb = radix_digit_bits(b), ppasses = (b + pdb - 1) / pdb;
     uint32_t *phist = ctx.alloc<uint32_t>(2 * ppasses * kHistDigits);
     TC_CUDA(cudaMemsetAsync(phist, 0, 2 * ppasses * kHistDigits * sizeof(uint32_t), ctx.stream));
@@ -483,14 +523,14 @@ void orient_clean(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, cons
     uint32_t egrid = (uint32_t)std::min<uint64_t>(tiles, (uint64_t)ctx.persistent_grid(4));
     k_orient_emit<<<egrid, kTileThreads, 0, ctx.stream>>>(
         rowptr, col, n, M, key, out.newid, (uint32_t *)(st + tiles), st, st + tiles + 1, okey, oval,
-        dplus, phist, phist + ppasses * kHistDigits, ppasses, pdb);
+        dplus, phist, phist + ppasses * kHistDigits, ppasses, pdb, cap, out.claim_err);
     TC_LAUNCHED(ctx);
     out.stage_work = ctx.alloc<uint64_t>(1);
     TC_CUDA(cudaMemsetAsync(out.stage_work, 0, sizeof(uint64_t), ctx.stream));
-    k_dminus<<<grid, 256, 0, ctx.stream>>>(deg, out.newid, dplus, n, dminus, out.stage_work);
-    TC_LAUNCHED(ctx);
+    // d-(x) is counted from the written pairs (not d(x) - d+(x)), so a false TC_CLEAN claim
+    // cannot make the transposed CSR disagree with them
     pairs_to_csr(ctx, n, cap, okey, oval, dplus, dminus, st + tiles + 1, out, tm, phist,
-                 phist + ppasses * kHistDigits);
+                 phist + ppasses * kHistDigits, true);
 }
 
 // ------------------------------------------------------------------ back to original ids

@@ -5,6 +5,7 @@
 //   synchronisation until the 8-byte count is read back.
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 
 #include "tc_internal.cuh"
 
@@ -14,27 +15,40 @@ static thread_local std::string g_last_error;
 
 void set_error(const std::string &msg) { g_last_error = msg; }
 
-static int device_sms(int dev) {
-    static int cache[64] = {0};
-    if (dev < 0 || dev >= 64) return 148;
-    if (!cache[dev]) {
+// Per-device state created once under a lock: the SM count and the library's own
+// workspace pool (never the process's default pool, which torch / NCCL may rely on).
+struct DeviceState {
+    int sms = 0;
+    cudaMemPool_t pool = nullptr;
+};
+static std::mutex g_dev_mu;
+static DeviceState g_dev[64];
+
+static DeviceState &device_state(int dev) {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (dev < 0 || dev >= 64) throw Error{TC_EINVAL, "device index out of range"};
+    DeviceState &d = g_dev[dev];
+    if (!d.sms) {
         int v = 0;
         if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
             v = 148;
-        cache[dev] = v;
+        d.sms = v;
     }
-    return cache[dev];
+    if (!d.pool) {
+        cudaMemPoolProps props;
+        memset(&props, 0, sizeof(props));
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        TC_CUDA(cudaMemPoolCreate(&d.pool, &props));
+    }
+    return d;
 }
 
-static void keep_pool_warm(int dev) {
-    static bool done[64] = {false};
-    if (dev < 0 || dev >= 64 || done[dev]) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    done[dev] = true;
+static void set_pool_keep(cudaMemPool_t pool, bool keep) {
+    uint64_t thr = keep ? UINT64_MAX : 0;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
 }
 
 // 32 uint64 of pinned host memory per thread for asynchronous stat read-back.
@@ -42,6 +56,15 @@ static uint64_t *pinned_scratch() {
     static thread_local uint64_t *p = nullptr;
     if (!p) TC_CUDA(cudaMallocHost((void **)&p, 32 * sizeof(uint64_t)));
     return p;
+}
+
+// A false TC_CLEAN claim (more arcs passed the rank filter than a simple symmetric graph
+// has edges) is detected on the device; the kernels clamp every write, and the call reports
+// TC_EGRAPH once it has synchronised (tc_count_shard: only when stats are requested).
+static void check_claim(const uint64_t *pin) {
+    if ((uint32_t)pin[26])
+        throw Error{TC_EGRAPH, "TC_CLEAN claim is false: more arcs passed the rank filter than "
+                               "m/2 (the input is not simple and symmetric)"};
 }
 
 enum Mode { kCount, kShard, kOrientOnly, kClustering, kSupport, kEnumerate, kMasked };
@@ -106,6 +129,8 @@ static tc_status check_args(const Call &c) {
         return set_error("TC_PER_VERTEX needs per_vertex"), TC_EINVAL;
     if ((c.flags & TC_SORTED) && !(c.flags & TC_CLEAN))
         return set_error("TC_SORTED is only meaningful with TC_CLEAN"), TC_EINVAL;
+    if (!c.opt.alloc != !c.opt.free)
+        return set_error("tc_options.alloc and .free must be given together"), TC_EINVAL;
     if (c.opt.force_variant < -1 || c.opt.force_variant > 3)
         return set_error("force_variant out of range"), TC_EINVAL;
     for (uint32_t r : c.opt.reserved)
@@ -113,13 +138,47 @@ static tc_status check_args(const Call &c) {
     return TC_OK;
 }
 
+// Device pointers must live on the current device (include/tc.h DEVICE).
+static void check_device_ptr(const void *p, int dev, const char *what) {
+    if (!p) return;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        throw Error{TC_EINVAL, std::string(what) + " is not a CUDA pointer"};
+    }
+    if (a.type == cudaMemoryTypeDevice && a.device != dev)
+        throw Error{TC_EINVAL, std::string(what) + " lives on device " + std::to_string(a.device) +
+                                   ", the current device is " + std::to_string(dev)};
+    if (a.type == cudaMemoryTypeUnregistered)
+        throw Error{TC_EINVAL, std::string(what) + " is a host pointer without TC_HOST_PTRS"};
+}
+
 static void run(Call &c) {
     Ctx ctx;
     TC_CUDA(cudaGetDevice(&ctx.device));
     ctx.stream = (cudaStream_t)c.opt.stream;
-    ctx.num_sms = device_sms(ctx.device);
-    keep_pool_warm(ctx.device);
+    DeviceState &ds = device_state(ctx.device);
+    ctx.num_sms = ds.sms;
+    if (c.opt.alloc) {
+        ctx.hook_alloc = c.opt.alloc;
+        ctx.hook_free = c.opt.free;
+        ctx.hook_ctx = c.opt.alloc_ctx;
+    } else {
+        ctx.pool = ds.pool;
+        set_pool_keep(ds.pool, c.opt.keep_workspace != 0);
+    }
     const bool host = c.flags & TC_HOST_PTRS;
+    if (!host) {
+        check_device_ptr(c.rowptr, ctx.device, "row_offsets");
+        check_device_ptr(c.col, ctx.device, "col_indices");
+        check_device_ptr(c.per_vertex, ctx.device, "per_vertex");
+        check_device_ptr(c.partial_dev, ctx.device, "partial_dev");
+        check_device_ptr(c.off_plus, ctx.device, "off_plus");
+        check_device_ptr(c.col_plus, ctx.device, "col_plus");
+        check_device_ptr(c.support, ctx.device, "support / c_values");
+        check_device_ptr(c.cc, ctx.device, "local_cc");
+        check_device_ptr(c.triangles, ctx.device, "triangles");
+    }
     const bool pv = ((c.flags & TC_PER_VERTEX) && c.mode != kOrientOnly) || c.mode == kClustering;
     const bool pv_out = pv && c.per_vertex;   // t(v) wanted by the caller
     tc_stats st;
@@ -203,6 +262,10 @@ static void run(Call &c) {
         else
             orient_dirty(ctx, c.n, c.M, rowptr, col, g, tm,
                          prune, c.flags & TC_ID_ORDER);
+        pin[26] = 0;
+        if (g.claim_err && (c.mode != kShard || c.stats))   // read at the final synchronisation
+            TC_CUDA(cudaMemcpyAsync(pin + 26, g.claim_err, sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                                    ctx.stream));
         if (c.stats && prune.m_before)
             TC_CUDA(cudaMemcpyAsync(pin + 24, prune.m_before, sizeof(uint64_t),
                                     cudaMemcpyDeviceToHost, ctx.stream));
@@ -218,6 +281,7 @@ static void run(Call &c) {
             uint64_t m = 0;
             TC_CUDA(cudaMemcpyAsync(&m, g.m_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx.stream));
             TC_CUDA(cudaStreamSynchronize(ctx.stream));
+            check_claim(pin);
             TC_CUDA(cudaMemcpyAsync(c.off_plus, off_o, (c.n + 1) * sizeof(uint64_t), kind, ctx.stream));
             if (m) TC_CUDA(cudaMemcpyAsync(c.col_plus, col_o, m * sizeof(uint32_t), kind, ctx.stream));
             TC_CUDA(cudaStreamSynchronize(ctx.stream));
@@ -335,8 +399,10 @@ static void run(Call &c) {
     }
     if (c.stats) cudaEventRecord(t_end, ctx.stream);
     ctx.release();
-    if (c.mode != kShard || c.stats) TC_CUDA(cudaStreamSynchronize(ctx.stream));
+    const bool synced = c.mode != kShard || c.stats;
+    if (synced) TC_CUDA(cudaStreamSynchronize(ctx.stream));
     TC_CUDA(cudaGetLastError());
+    if (synced && c.n > 0 && c.M > 0) check_claim(pin);
     if (c.mode == kCount || c.mode == kEnumerate || c.mode == kMasked) *c.total_host = pin[20];
     if (c.mode == kClustering && c.csum) {
         tc_clustering_summary &r = *c.csum;
@@ -425,7 +491,20 @@ void tc_default_options(tc_options *opt) {
     opt->hub_min_dplus = 80;
     opt->force_variant = TC_VARIANT_AUTO;
     opt->stream = nullptr;
-    opt->segsort_block_max = 8192;
+    opt->keep_workspace = 1;
+}
+
+tc_status tc_trim_workspace(int device) {
+    try {
+        if (device < 0) TC_CUDA(cudaGetDevice(&device));
+        DeviceState &d = device_state(device);
+        TC_CUDA(cudaMemPoolTrimTo(d.pool, 0));
+    } catch (const Error &e) {
+        set_error(e.msg);
+        return e.status;
+    }
+    set_error("");
+    return TC_OK;
 }
 
 tc_status tc_count_ex(uint64_t n, uint64_t m, const uint64_t *row_offsets,

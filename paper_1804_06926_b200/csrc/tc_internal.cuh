@@ -43,37 +43,59 @@ void set_error(const std::string &msg);
     } while (0)
 
 // ------------------------------------------------------------------ context
-// Stream-ordered workspace: every allocation is cudaMallocAsync on the call's
-// stream and freed (stream-ordered) when the context is destroyed.
+// Stream-ordered workspace (include/tc.h OWNERSHIP): every block comes from the caller's
+// hook (tc_options.alloc / free) or, without one, from the library's own per-device pool
+// (cudaMallocFromPoolAsync), on the call's stream, and is freed stream-ordered when the
+// context is destroyed (or earlier with free_now).
 struct Ctx {
     cudaStream_t stream = nullptr;
     int device = 0;
     int num_sms = 148;
     uint64_t launches = 0;
-    std::vector<void *> allocs;
+    tc_alloc_fn hook_alloc = nullptr;
+    tc_free_fn hook_free = nullptr;
+    void *hook_ctx = nullptr;
+    cudaMemPool_t pool = nullptr;    // library pool (no hook)
+    uint64_t bytes_live = 0, bytes_peak = 0, n_allocs = 0;
+    std::vector<std::pair<void *, size_t>> allocs;
 
     template <class T>
     T *alloc(uint64_t count) {
         void *p = nullptr;
         size_t bytes = (size_t)(count ? count : 1) * sizeof(T);
-        cudaError_t e = cudaMallocAsync(&p, bytes, stream);
-        if (e != cudaSuccess) {
-            cudaGetLastError();
-            throw Error{TC_ENOMEM, "cudaMallocAsync(" + std::to_string(bytes) + " B) failed: " +
-                                       cudaGetErrorString(e)};
+        bytes = (bytes + 255) & ~(size_t)255;   // whole 256-byte granules: aligned slot loads
+        if (hook_alloc) {
+            p = hook_alloc(hook_ctx, bytes, (void *)stream);
+            if (!p)
+                throw Error{TC_ENOMEM, "tc_options.alloc(" + std::to_string(bytes) + " B) returned NULL"};
+        } else {
+            cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, pool, stream);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                throw Error{TC_ENOMEM, "cudaMallocFromPoolAsync(" + std::to_string(bytes) +
+                                           " B) failed: " + cudaGetErrorString(e)};
+            }
         }
-        allocs.push_back(p);
+        allocs.push_back({p, bytes});
+        n_allocs++;
+        bytes_live += bytes;
+        if (bytes_live > bytes_peak) bytes_peak = bytes_live;
         return (T *)p;
     }
+    void give_back(void *p, size_t bytes) {
+        if (hook_free) hook_free(hook_ctx, p, (void *)stream);
+        else cudaFreeAsync(p, stream);
+        bytes_live -= bytes;
+    }
     void release() {
-        for (void *p : allocs) cudaFreeAsync(p, stream);
+        for (auto &a : allocs) give_back(a.first, a.second);
         allocs.clear();
     }
     // Stream-ordered early free (the pool reuses it for later allocations of this call).
     void free_now(void *p) {
         for (size_t i = 0; i < allocs.size(); i++)
-            if (allocs[i] == p) {
-                cudaFreeAsync(p, stream);
+            if (allocs[i].first == p) {
+                give_back(p, allocs[i].second);
                 allocs[i] = allocs.back();
                 allocs.pop_back();
                 return;
@@ -109,6 +131,28 @@ struct Ctx {
             throw Error{TC_ECUDA, "join failed"};
     }
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+};
+
+// Fork work onto the side stream for the lifetime of this object; the destructor joins
+// it back into the call's stream on EVERY path (also when a launch throws), so the
+// workspace is never freed while side-stream kernels may still read it.
+struct SideStream {
+    Ctx &ctx;
+    cudaStream_t s;
+    bool joined = false;
+    explicit SideStream(Ctx &c) : ctx(c), s(c.side()) {
+        if (s != ctx.stream) ctx.fork(s);
+    }
+    void join() {
+        if (!joined && s != ctx.stream) ctx.join(s);
+        joined = true;
+    }
+    ~SideStream() {
+        if (!joined && s != ctx.stream) {   // error path: never throw from a destructor
+            cudaEventRecord(ctx.ev_join, s);
+            cudaStreamWaitEvent(ctx.stream, ctx.ev_join, 0);
+        }
+    }
 };
 
 // ------------------------------------------------------------------ device helpers
@@ -276,6 +320,8 @@ struct Oriented {
     uint32_t *newid = nullptr;   // input id -> new id
     uint64_t *m_dev = nullptr;   // device scalar m
     uint64_t *stage_work = nullptr;  // device scalar sum_v d-(v) d+(v) (stats)
+    uint32_t *claim_err = nullptr;   // clean input: set if more arcs passed the rank filter
+                                     // than a simple symmetric graph allows (false TC_CLEAN)
     uint64_t m_cap = 0;          // capacity bound for m (host-known)
 };
 

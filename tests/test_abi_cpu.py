@@ -29,7 +29,7 @@ def test_exports_every_declared_symbol(lib):
     names = declared_functions()
     assert set(names) >= {"tc_count", "tc_count_ex", "tc_count_shard", "tc_orient",
                           "tc_clustering", "tc_edge_support", "tc_enumerate", "tc_masked_spgemm",
-                          "tc_last_error",
+                          "tc_last_error", "tc_trim_workspace",
                           "tc_default_options", "tc_version"}
     for name in names:
         assert hasattr(lib, name), name
@@ -43,9 +43,11 @@ def test_sm100a_cubin_present():
 def test_struct_layout(lib):
     o = tc.Options()
     lib.tc_default_options(ctypes.byref(o))
-    assert ctypes.sizeof(tc.Options) == 64
+    assert ctypes.sizeof(tc.Options) == 88
+    assert tc.Options.alloc.offset == 32 and tc.Options.reserved.offset == 56
     assert o.short_max == 20 and o.skew_ratio == 0 and o.hub_min_dplus == 80
-    assert o.force_variant == -1 and o.segsort_block_max == 8192
+    assert o.force_variant == -1 and o.keep_workspace == 1
+    assert not o.alloc and not o.free and not o.alloc_ctx
     assert o.prune_rounds == 0 and not any(o.reserved)
     assert ctypes.sizeof(tc.Stats) == 7 * 8 + 19 * 8
     assert ctypes.sizeof(tc.ClusteringSummary) == 32
@@ -133,6 +135,12 @@ def test_argument_errors_before_device(lib):
     o.reserved[3] = 1
     assert lib.tc_count_ex(1, 0, rp.ctypes.data, None, 0, ctypes.byref(o),
                            ctypes.addressof(total), None, None) == EINVAL
+    # the workspace hook comes as a pair
+    lib.tc_default_options(ctypes.byref(o))
+    o.alloc = tc.ALLOC_FN(lambda c, size, stream: None)
+    assert lib.tc_count_ex(1, 0, rp.ctypes.data, None, 0, ctypes.byref(o),
+                           ctypes.addressof(total), None, None) == EINVAL
+    assert b"together" in lib.tc_last_error()
     # tc_count reports failure as TC_ERROR
     assert lib.tc_count(1 << 32, 0, rp.ctypes.data, None, 0) == tc.TC_ERROR
 

@@ -1,0 +1,89 @@
+"""Full-size parity on the BASELINE.json configs the bench does not run (VERDICT r01 "Next
+round" #1): R-MAT s24 ef16 (configs[4]) and the kron_g500-logn21-shaped s21 ef48 (C1', SURVEY
+§8 config table) against the oracle, and a closed-form pin with >= 2^30 raw arcs that drives
+the radix sort's 64-bit look-back status words (radix.cu: 32-bit words only below 2^30 keys).
+
+These are the slowest GPU tests (the oracle needs ~1-2 minutes per graph on the host cores);
+they run in the driver's `-m gpu` suite.
+"""
+import numpy as np
+import pytest
+
+import graphgen as G
+import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+if not torch.cuda.is_available():  # collected on CPU boxes, skipped there
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1804_06926_b200 as tc  # noqa: E402
+
+DEV = torch.device("cuda:0")
+KARATE_T = np.array([18, 12, 11, 10, 2, 3, 3, 6, 5, 0, 2, 0, 1, 6, 1, 1, 1, 1, 1, 1, 1, 1, 1, 4,
+                     1, 1, 1, 1, 1, 4, 3, 3, 13, 15], dtype=np.uint64)   # tests/golden/karate.txt
+
+
+def on_dev(rowptr, col):
+    return (torch.from_numpy(np.ascontiguousarray(rowptr, np.uint64).view(np.int64)).to(DEV),
+            torch.from_numpy(np.ascontiguousarray(col, np.uint32).view(np.int32)).to(DEV))
+
+
+def shard_sum(rp, cl, world, per_vertex=False):
+    tot, pv_sum = 0, None
+    for r in range(world):
+        p = torch.zeros(1, dtype=torch.int64, device=DEV)
+        pv = torch.zeros(rp.numel() - 1, dtype=torch.int64, device=DEV) if per_vertex else None
+        tc.count_shard(rp, cl, r, world, p, per_vertex_partial=pv)
+        tot += int(p.item())
+        if per_vertex:
+            pv_sum = pv if pv_sum is None else pv_sum + pv
+    return tot, pv_sum
+
+
+def test_config_rmat24_full():
+    """BASELINE configs[4]: R-MAT s24 ef16 (268 M raw arcs, m ~ 2.6e8), the whole count and the multi-GPU split for world 2/4/8 (partials summed as the allreduce
+    would), bit-exact against the oracle."""
+    g = G.rmat(24, 16)
+    rp, cl = on_dev(g.rowptr, g.col)
+    got, pv, st = tc.count_ex(rp, cl, per_vertex=True, with_stats=True)
+    T, ost = O.count(g.n, g.rowptr, g.col, with_stats=True)
+    assert st["m_undirected"] == ost["m"]
+    assert got == T
+    assert int(pv.sum().item()) == 3 * T
+    assert st["work_W"] == ost["W"] and st["max_dplus"] == ost["max_dplus"]
+    for world in (2, 4, 8):
+        assert shard_sum(rp, cl, world)[0] == T, world
+
+
+def test_config_rmat21_ef48_full():
+    """C1': R-MAT s21 at edge factor 48, the kron_g500-logn21 shape
+    (m ~ 9.1e7); total and per-vertex sum against the oracle."""
+    g = G.rmat(21, 48, seed=4821)
+    rp, cl = on_dev(g.rowptr, g.col)
+    got, pv, st = tc.count_ex(rp, cl, per_vertex=True, with_stats=True)
+    T, t = O.count(g.n, g.rowptr, g.col, per_vertex=True)
+    assert got == T
+    assert (pv.cpu().numpy().view(np.uint64) == t).all()
+    assert shard_sum(rp, cl, 4)[0] == T
+
+
+def test_duplicated_karate4_wide_status_words():
+    """karate^(x)4 with every arc given twice: 1,184,481,792 raw arcs >= 2^30, so the 64-bit key
+    sort of a1 runs on 64-bit look-back status words (the only path s26 alone reached in r01).
+    Closed forms (SURVEY §8(c) "Large exact pins", Kronecker algebra, no oracle needed):
+    m = 2^3 * 78^4 = 296,120,448, T = 6^3 * 45^4 = 885,735,000, t(v1..v4) = 2^3 t(v1)...t(v4)."""
+    g = G.kron_power(G.karate(), 4)
+    rowptr = 2 * g.rowptr
+    col = np.repeat(g.col, 2)                     # each arc twice, adjacent in its row
+    assert col.size == 1_184_481_792 and col.size >= 2 ** 30
+    rp, cl = on_dev(rowptr, col)
+    del col
+    got, pv, st = tc.count_ex(rp, cl, per_vertex=True, with_stats=True)
+    assert st["m_undirected"] == 296_120_448
+    assert got == 885_735_000
+    t = KARATE_T
+    for _ in range(3):
+        t = 2 * np.outer(t, KARATE_T).reshape(-1)
+    assert (pv.cpu().numpy().view(np.uint64) == t).all()

@@ -134,8 +134,8 @@ def test_orientation_parity(name):
     want_off, want_col = O.orient(g.n, row, col)
     cases = [dict(rowptr=g.rowptr, col=g.col),                                   # a1 path
              dict(rowptr=row, col=col, clean=True, sorted_rows=True),             # sorted clean
-             dict(rowptr=row, col=shuffled_rows(g.n, row, col, 1), clean=True),   # a4 segsort
-             dict(rowptr=row, col=shuffled_rows(g.n, row, col, 2), clean=True, segsort_block_max=32)]
+             dict(rowptr=row, col=shuffled_rows(g.n, row, col, 1), clean=True),   # a4 row sort
+             dict(rowptr=row, col=shuffled_rows(g.n, row, col, 2), clean=True, allocator="library")]
     for c in cases:
         rp, cl = on_dev(c.pop("rowptr"), c.pop("col"))
         off, colp = tc.orient(rp, cl, **c)
@@ -150,7 +150,7 @@ def test_clean_input_counts(scale):
     T, t = O.count(g.n, g.rowptr, g.col, per_vertex=True)
     row, col = clean_csr(g)
     for kw in [dict(clean=True, sorted_rows=True), dict(clean=True),
-               dict(clean=True, segsort_block_max=32)]:
+               dict(clean=True, allocator="library")]:
         c = shuffled_rows(g.n, row, col, scale) if not kw.get("sorted_rows") else col
         for v in VARIANTS:
             got, pv = gpu_count(row, c, per_vertex=True, force_variant=v, **kw)
@@ -231,6 +231,41 @@ def test_validate_rejects_bad_graphs():
         gpu_count(np.array([0, 1, 1], np.uint64), np.array([1], np.uint32), clean=True,
                   sorted_rows=True, validate=True)
     assert gpu_count(row, col, clean=True, sorted_rows=True, validate=True) == 45
+
+
+def _one_way_cycle(n):
+    return np.arange(n + 1, dtype=np.uint64), ((np.arange(n) + 1) % n).astype(np.uint32)
+
+
+def test_validate_clean_unsorted():
+    """TC_CLEAN | TC_VALIDATE without TC_SORTED checks symmetry and duplicates too."""
+    rp, cl = _one_way_cycle(64)                       # every arc lacks its reverse
+    with pytest.raises(tc.TCError) as e:
+        gpu_count(rp, cl, clean=True, validate=True)
+    assert e.value.status == 2 and "reverse" in str(e.value)
+    row, col = clean_csr(G.karate())
+    dup_col = np.insert(col, 1, col[0])               # row 0: its first arc twice
+    dup_row = row.copy()
+    dup_row[1:] += 1
+    with pytest.raises(tc.TCError) as e:
+        gpu_count(dup_row, dup_col, clean=True, validate=True)
+    assert e.value.status == 2 and "duplicate" in str(e.value)
+    rng = np.random.default_rng(3)                    # shuffled rows, valid: accepted
+    srow, scol = row.copy(), col.copy()
+    for u in range(len(row) - 1):
+        rng.shuffle(scol[row[u]:row[u + 1]])
+    assert gpu_count(srow, scol, clean=True, validate=True) == 45
+
+
+@pytest.mark.parametrize("n", [8, 1000, 70_000])
+def test_false_clean_claim_is_caught(n):
+    """Without TC_VALIDATE a false TC_CLEAN claim (one-way cycle: n-1 arcs pass the rank
+    filter, the buffers hold n/2 + 1) must not write out of bounds: TC_EGRAPH."""
+    rp, cl = _one_way_cycle(n)
+    with pytest.raises(tc.TCError) as e:
+        gpu_count(rp, cl, clean=True)
+    assert e.value.status == 2
+    assert gpu_count(*clean_csr(G.karate()), clean=True) == 45   # the device is still sane
 
 
 # ------------------------------------------------------------------ full-size configurations
@@ -384,3 +419,77 @@ def test_hash_owners_beyond_bitmap_range():
     T = O.count(r.n, r.rowptr, r.col)
     for kw in (dict(hub_min_dplus=8), dict(hub_min_dplus=16, id_order=True), dict()):
         assert gpu_count(r.rowptr, r.col, **kw) == T, kw
+
+
+# ------------------------------------------------------------------ workspace hook (§8(b))
+def test_workspace_hook_counts_every_byte():
+    """tc_options.alloc / free: every workspace block goes through the caller's hook, on the
+    call's stream, and every block is freed before the call returns."""
+    g = G.rmat(14, 16, seed=4)
+    T, t = O.count(g.n, g.rowptr, g.col, per_vertex=True)
+    rp, cl = on_dev(g.rowptr, g.col)
+    stream = torch.cuda.current_stream().cuda_stream
+    live, log = {}, []
+
+    def alloc(size, s):
+        assert s == stream
+        p = torch._C._cuda_cudaCachingAllocator_raw_alloc(size, s)
+        live[p] = size
+        log.append(size)
+        return p
+
+    def free(p, s):
+        assert s == stream and p in live
+        del live[p]
+        torch._C._cuda_cudaCachingAllocator_raw_delete(p)
+
+    for kw in [dict(), dict(per_vertex=True), dict(force_variant=tc.VARIANT_MERGE),
+               dict(prune=True, prune_rounds=2)]:
+        out = tc.count_ex(rp, cl, allocator=(alloc, free), **kw)
+        torch.cuda.synchronize()
+        got = out[0] if isinstance(out, tuple) else out
+        assert got == T, kw
+        if kw.get("per_vertex"):
+            assert (pv_np(out[1]) == t).all()
+        assert not live, f"{len(live)} workspace blocks not freed ({kw})"
+    assert len(log) > 10 and sum(log) > 16 * g.arcs   # the 64-bit sort keys alone are 16 B/arc
+    n_before = len(log)
+    _, _, sup = tc.edge_support(rp, cl, allocator=(alloc, free))
+    T2, tri = tc.enumerate_triangles(rp, cl, allocator=(alloc, free))
+    _, clus = tc.clustering(rp, cl, allocator=(alloc, free))
+    torch.cuda.synchronize()
+    assert T2 == T and clus["triangles"] == T and int(sup.to(torch.int64).sum()) == 3 * T
+    assert not live and len(log) > n_before
+
+
+def test_workspace_hook_failure_is_enomem():
+    g = G.rmat(10, 16, seed=4)
+    rp, cl = on_dev(g.rowptr, g.col)
+    with pytest.raises(tc.TCError) as e:
+        tc.count_ex(rp, cl, allocator=(lambda size, s: 0, lambda p, s: None))
+    assert e.value.status == 3
+    assert tc.count_ex(rp, cl) == O.count(g.n, g.rowptr, g.col)   # next call is fine
+
+
+def test_library_pool_and_trim():
+    """Without a hook the library's own pool is used; the process default pool is untouched."""
+    g = G.rmat(12, 16, seed=4)
+    T = O.count(g.n, g.rowptr, g.col)
+    rp, cl = on_dev(g.rowptr, g.col)
+    assert tc.count_ex(rp, cl, allocator="library") == T
+    assert tc.count_ex(rp, cl, allocator="library", keep_workspace=False) == T
+    tc.trim_workspace()
+    assert tc.count_ex(rp, cl, allocator="library") == T
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two devices")
+def test_wrong_device_pointer_rejected():
+    g = G.karate()
+    rp = torch.from_numpy(g.rowptr.view(np.int64)).to("cuda:1")
+    cl = torch.from_numpy(g.col.view(np.int32)).to("cuda:1")
+    assert tc.count_ex(rp, cl) == 45            # the binding makes cuda:1 current
+    lib = tc._load()
+    total = __import__("ctypes").c_uint64()
+    with torch.cuda.device(0):
+        assert lib.tc_count_ex(g.n, g.arcs, rp.data_ptr(), cl.data_ptr(), 0, None,
+                               __import__("ctypes").addressof(total), None, None) == 1

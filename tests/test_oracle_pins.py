@@ -93,6 +93,53 @@ def test_fig_mm_stats():
     assert st["m"] == 10                                   # 20 directed edges (Table 1 convention)
     assert st["SSD"] == 62                                 # degrees [3,3,3,3,3,4,1]
     assert st["wedges"] == 21
+    # SURVEY §8(c) worked example under rank orientation: N+ = {0:[1,4,5], 1:[2,5], 2:[3],
+    # 3:[4,5], 4:[5], 5:[], 6:[2]} -> W = sum over oriented edges of d+u + d+v = 28
+    assert st["W"] == 28
+    assert st["max_dplus"] == 3 and st["max_deg"] == 4
+    # d- = [0,1,2,1,2,4,0], d+ = [3,2,1,2,1,0,1] (d = d+ + d- = the degrees above):
+    # sum d- d+ = 0+2+2+2+2+0+0 = 8
+    assert st["sum_dminus_dplus"] == 8
+
+
+def test_closed_form_stats():
+    """Work statistics with closed forms (karate W = 302, max d+ 5; K_n:
+    every oriented edge (i, j), i < j in rank order, has d+ = n-1-i and n-1-j)."""
+    _, st = O.count(34, *_csr(G.karate()), with_stats=True)
+    assert (st["m"], st["W"], st["SSD"], st["max_dplus"], st["max_deg"], st["wedges"]) == \
+        (78, 302, 1212, 5, 17, 528)
+    for n in (5, 20, 57):
+        _, st = O.count(n, *_csr(G.complete(n)), with_stats=True)
+        W = sum((n - 1 - i) + (n - 1 - j) for i in range(n) for j in range(i + 1, n))
+        assert st["W"] == W and st["max_dplus"] == n - 1
+        assert st["sum_dminus_dplus"] == sum(i * (n - 1 - i) for i in range(n))
+    _, st = O.count(9, *_csr(G.star(8)), with_stats=True)   # leaves -> hub: d+ = 1, hub d+ = 0
+    assert (st["W"], st["max_dplus"], st["sum_dminus_dplus"]) == (8, 1, 0)
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_work_stats_numpy(seed):
+    """W, sum d- d+ and max d+ recomputed with numpy from the definition (rank = (d, id),
+    orientation low -> high rank), independent of the oracle's C code."""
+    g = G.gnp(300, 0.07, seed)
+    src, dst = g.arc_list()
+    keep = src != dst
+    a = np.minimum(src[keep], dst[keep]).astype(np.int64)
+    b = np.maximum(src[keep], dst[keep]).astype(np.int64)
+    pairs = np.unique(a * g.n + b)
+    a, b = pairs // g.n, pairs % g.n
+    d = np.bincount(a, minlength=g.n) + np.bincount(b, minlength=g.n)
+    a_low = (d[a] < d[b]) | ((d[a] == d[b]) & (a < b))
+    u = np.where(a_low, a, b)
+    v = np.where(a_low, b, a)
+    dplus = np.bincount(u, minlength=g.n)
+    dminus = np.bincount(v, minlength=g.n)
+    _, st = O.count(g.n, g.rowptr, g.col, with_stats=True)
+    assert st["m"] == len(pairs)
+    assert st["W"] == int((dplus[u] + dplus[v]).sum())
+    assert st["sum_dminus_dplus"] == int((dminus * dplus).sum())
+    assert st["max_dplus"] == int(dplus.max())
+    assert st["SSD"] == int((d * d).sum())
 
 
 def _csr(g):
