@@ -361,8 +361,8 @@ def ncu_traffic(args):
             "top_dram_pct": tv.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
             "top_l2_hit_pct": tv.get("lts__t_sector_hit_rate.pct"),
             "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum (+ l1tex / dram "
-                      "throughput %, L2 hit rate) -k '%s' over one tc_count_ex of this workload, "
-                      "run by this bench.py after its timed region (cold caches)" % A6_KERNELS}
+                      f"throughput %, L2 hit rate) -k '{A6_KERNELS}' over one tc_count_ex of this "
+                      "workload, run by this bench.py after its timed region (cold caches)"}
 
 
 # ------------------------------------------------------------------ native arm

@@ -215,7 +215,8 @@ struct OutPrefix {
 // hash owners (the rest).
 // Also writes ooff[u] (each owner's first out-part entry; ooff[n] = the total), which the
 // owner counts here need anyway: no separate pass over the vertices.
-__global__ void k_owners(const uint32_t *__restrict__ dplus, const uint64_t *__restrict__ in_off,
+__global__ void k_owners(const uint32_t *__restrict__ dplus, const uint32_t *__restrict__ col,
+                         const uint64_t *__restrict__ in_off,
                          const uint32_t *__restrict__ ulo, uint32_t *__restrict__ has_in,
                          uint64_t *__restrict__ ooff, const uint64_t *__restrict__ off,
                          const uint64_t *__restrict__ m_dev, const uint32_t *__restrict__ obits,
@@ -252,7 +253,10 @@ __global__ void k_owners(const uint32_t *__restrict__ dplus, const uint64_t *__r
             }
             has_in[u] = hin;
             pcnt[u] = c;
-            if (c) kind = du < cta_min ? 0 : (n - 1 - u + 32 <= kCtaBitmapBits ? 2 : 1);
+            // bitmap owners: N+(u) spans [first, last] element (rows ascending) + a spare word
+            if (c)
+                kind = du < cta_min ? 0
+                       : ((uint64_t)col[off[u + 1] - 1] - col[off[u]] + 1 + 32 <= kCtaBitmapBits ? 2 : 1);
         }
         uint32_t *dst[3] = {owners_warp, owners_cta, owners_bitmap};
 #pragma unroll
@@ -378,14 +382,14 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
     bins.owners_bitmap = ctx.alloc<uint32_t>(n);
     uint32_t cta_min = p.hub_min < kWarpTableSlots / 4 + 1 ? p.hub_min : kWarpTableSlots / 4 + 1;
     k_owners<<<ctx.persistent_grid(4), 256, 0, ctx.stream>>>(
-        g.dplus, g.in_off, ulo, has_in, ooff, g.off, g.m_dev, obits, wpre, toff, toff + tiles, n,
+        g.dplus, g.col, g.in_off, ulo, has_in, ooff, g.off, g.m_dev, obits, wpre, toff, toff + tiles, n,
         cta_min, bins.pcnt, bins.owners_warp, bins.owners_cta, bins.owners_bitmap, bins.count);
     TC_LAUNCHED(ctx);
     make_tasks(ctx, n, cap, bins.owners_warp, bins.count + 8, bins.pcnt, g.dplus, kWarpTaskLists,
                bins.count + 11, bins.tasks_warp, bins.ntasks_warp);
     make_tasks(ctx, n, cap, bins.owners_cta, bins.count + 9, bins.pcnt, g.dplus, kCtaTaskLists,
                bins.count + 11, bins.tasks_cta, bins.ntasks_cta);
-    make_tasks(ctx, n, cap, bins.owners_bitmap, bins.count + 10, bins.pcnt, g.dplus, kCtaTaskLists,
+    make_tasks(ctx, n, cap, bins.owners_bitmap, bins.count + 10, bins.pcnt, g.dplus, kBitmapTaskLists,
                bins.count + 11, bins.tasks_bitmap, bins.ntasks_bitmap);
 }
 

@@ -741,6 +741,7 @@ __global__ void __launch_bounds__(kIxThreads, TC_HASH_WARP_MINBLOCKS)
 // kBitmap: the owner's N+ (rank ids in (x, n)) is a bitmap over [x+1, n) -- one
 // 32-bit shared load per probe; otherwise the bucket hash (chunked if d+ > 2048).
 constexpr uint32_t kSmemWords = kHashSlots;            // 16 KB of table / bitmap per CTA
+static_assert(kCtaTaskLists * kBitmapBatches == kBitmapTaskLists, "bitmap task size (bin.cu)");
 constexpr uint32_t kPvCounters = 4096;                 // per-vertex: smem hit counters (16 KB)
 static_assert(kCtaBitmapBits == kSmemWords * 32, "bitmap owners are classified in bin.cu");
 template <int CM, bool kBitmap>
@@ -777,34 +778,42 @@ __global__ void __launch_bounds__(kIxThreads, CM != kCmNone ? 4 : TC_HASH_CTA_MI
         uint64_t inb = hp.in_off[x], ob = hp.ooff[x];
         uint32_t indeg = hp.has_in[x] ? (uint32_t)(hp.in_off[x + 1] - inb) : 0u;
         uint32_t ocnt = (uint32_t)(hp.ooff[x + 1] - ob);
-        uint32_t lo, hi, y;
-        hash_desc<CM>(hp, inb, indeg, ob, ocnt, task.y * L + threadIdx.x, lo, hi, y);
-        uint32_t nq = quad_count(lo, hi);
-        // one 64-bit scan: high word = compacted index of non-empty entries, low = quads
-        uint64_t tot;
-        uint64_t pre = block_exclusive_scan<SumOp64>(((uint64_t)(nq != 0) << 32) | nq, s_scan, &tot);
-        const uint32_t items = (uint32_t)tot, nl = (uint32_t)(tot >> 32);
-        if (nq) put_desc(d, (uint32_t)(pre >> 32), lo, hi, (uint32_t)pre, y, PV);
-        if (threadIdx.x == 0) d.pre[nl] = items;
-        uint32_t ib = (uint32_t)(((uint64_t)items * wib) / kHashWarps);
-        uint32_t ie = (uint32_t)(((uint64_t)items * (wib + 1)) / kHashWarps);
         uint64_t h = 0;
+        // descriptors of the probe entries j0 + threadIdx.x (one per thread), compacted, and
+        // this warp's equal share [ib, ie) of their quads
+        uint32_t nl = 0, ib = 0, ie = 0;
+        auto batch = [&](uint32_t j0) {
+            uint32_t lo, hi, y;
+            hash_desc<CM>(hp, inb, indeg, ob, ocnt, j0 + threadIdx.x, lo, hi, y);
+            uint32_t nq = quad_count(lo, hi);
+            // one 64-bit scan: high word = compacted index of non-empty entries, low = quads
+            uint64_t tot;
+            uint64_t pre = block_exclusive_scan<SumOp64>(((uint64_t)(nq != 0) << 32) | nq, s_scan, &tot);
+            const uint32_t items = (uint32_t)tot;
+            nl = (uint32_t)(tot >> 32);
+            if (nq) put_desc(d, (uint32_t)(pre >> 32), lo, hi, (uint32_t)pre, y, PV);
+            if (threadIdx.x == 0) d.pre[nl] = items;
+            ib = (uint32_t)(((uint64_t)items * wib) / kHashWarps);
+            ie = (uint32_t)(((uint64_t)items * (wib + 1)) / kHashWarps);
+        };
         if (kBitmap) {
-            // N+(x) lies in (x, n): bits [0, span) for ids x+1 .. n-1, then one zero word
-            const uint32_t base = x + 1, span = n - 1 - x, words = span / 32 + 1;
+            // N+(x) lies in [lo_x, hi_x] (its first and last element, rows ascending): bits
+            // [0, span) for ids lo_x .. hi_x, then one spare zero word; every other id maps to it
+            const uint32_t base = col[xb], span = col[xb + dx - 1] - base + 1, words = span / 32 + 1;
             for (uint32_t w = threadIdx.x; w < words; w += blockDim.x) s_tab[w] = 0u;
             __syncthreads();
             for (uint32_t k = threadIdx.x; k < dx; k += blockDim.x) {
                 uint32_t o = col[xb + k] - base;
                 atomicOr(&s_tab[o >> 5], 1u << (o & 31));
             }
-            __syncthreads();
+            // (the first batch's block scan below orders these writes before any probe)
             BitProbe bp{tab, base, (words - 1) * 32 + 31};
             bp.xl = col + xb;
             bp.xlen = dx;
             bp.xb = xb;
             const bool use_cnt = kCnt && kBitmap && dx <= kPvCounters;
             if (use_cnt) {
+                __syncthreads();   // the bitmap is complete before its words are counted
                 // exclusive prefix popcount per bitmap word (blocked: thread t owns a run)
                 const uint32_t per = (words + kIxThreads - 1) / kIxThreads;
                 const uint32_t w0 = min(words, threadIdx.x * per), w1 = min(words, w0 + per);
@@ -820,8 +829,15 @@ __global__ void __launch_bounds__(kIxThreads, CM != kCmNone ? 4 : TC_HASH_CTA_MI
                 bp.cnt = s_cnt;
                 bp.wpre = s_wpre;
             }
-            h = probe_quads<CM>(bp, d, nl, ib, ie, col, x, cr, stage);
-            __syncthreads();
+            // one bitmap serves up to kBitmapBatches batches of kCtaTaskLists probe entries
+            const uint32_t npe = indeg + ocnt;
+            for (uint32_t bt = 0; bt < kBitmapBatches; bt++) {
+                const uint32_t j0 = (task.y * kBitmapBatches + bt) * L;
+                if (j0 >= npe) break;   // block-uniform
+                batch(j0);
+                h += probe_quads<CM>(bp, d, nl, ib, ie, col, x, cr, stage);
+                __syncthreads();   // descriptors are rewritten by the next batch
+            }
             if (use_cnt) {   // the k-th set bit is the k-th element of the sorted N+(x)
                 for (uint32_t k = threadIdx.x; k < dx; k += blockDim.x) {
                     uint32_t c = s_cnt[k];
@@ -832,6 +848,7 @@ __global__ void __launch_bounds__(kIxThreads, CM != kCmNone ? 4 : TC_HASH_CTA_MI
                 __syncthreads();
             }
         } else {
+            batch(task.y * L);
             for (uint32_t c0 = 0; c0 < dx; c0 += kHashChunk) {
                 uint32_t clen = min(kHashChunk, dx - c0);
                 int bits = table_bits(clen);

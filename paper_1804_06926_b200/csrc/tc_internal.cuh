@@ -472,7 +472,12 @@ struct Bins {
 
 constexpr uint32_t kWarpTableSlots = 512;   // per-warp hash table (owner d+ <= 128, load <= 1/4)
 constexpr uint32_t kWarpTaskLists = 64;     // probe entries per warp task
-constexpr uint32_t kCtaTaskLists = 256;     // probe entries per CTA task
+constexpr uint32_t kCtaTaskLists = 256;     // probe entries per CTA task (one descriptor batch)
+#ifndef TC_BITMAP_BATCHES
+#define TC_BITMAP_BATCHES 4
+#endif
+constexpr uint32_t kBitmapBatches = TC_BITMAP_BATCHES;   // bitmap tasks: batches per bitmap build
+constexpr uint32_t kBitmapTaskLists = kCtaTaskLists * kBitmapBatches;
 constexpr uint32_t kCtaBitmapBits = 4096 * 32;  // rank span of a CTA bitmap (16 KB)
 
 struct BinParams {

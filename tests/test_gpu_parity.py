@@ -432,14 +432,14 @@ def test_workspace_hook_counts_every_byte():
     live, log = {}, []
 
     def alloc(size, s):
-        assert s == stream
+        assert (s or 0) == stream          # ctypes passes the NULL (legacy) stream as None
         p = torch._C._cuda_cudaCachingAllocator_raw_alloc(size, s)
         live[p] = size
         log.append(size)
         return p
 
     def free(p, s):
-        assert s == stream and p in live
+        assert (s or 0) == stream and p in live
         del live[p]
         torch._C._cuda_cudaCachingAllocator_raw_delete(p)
 
