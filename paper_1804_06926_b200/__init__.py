@@ -79,8 +79,20 @@ def _hook_pair(allocator):
     if allocator in (None, "library"):
         return None
     a, f = allocator
-    pair = (ALLOC_FN(lambda _c, size, stream: a(size, stream)),
-            FREE_FN(lambda _c, ptr, stream: f(ptr, stream)))
+
+    def _a(_c, size, stream):
+        try:
+            return a(size, stream or 0)
+        except Exception:   # noqa: BLE001 -- NULL is the hook's error signal (TC_ENOMEM)
+            return None
+
+    def _f(_c, ptr, stream):
+        try:
+            f(ptr, stream or 0)
+        except Exception:   # noqa: BLE001 -- nothing can be reported from a free
+            pass
+
+    pair = (ALLOC_FN(_a), FREE_FN(_f))
     _user_hooks.append(pair)
     del _user_hooks[:-8]   # the last few stay referenced while their calls may run
     return pair

@@ -254,9 +254,13 @@ __global__ void k_owners(const uint32_t *__restrict__ dplus, const uint32_t *__r
             has_in[u] = hin;
             pcnt[u] = c;
             // bitmap owners: N+(u) spans [first, last] element (rows ascending) + a spare word
+#if TC_BITMAP_EFFSPAN
             if (c)
                 kind = du < cta_min ? 0
                        : ((uint64_t)col[off[u + 1] - 1] - col[off[u]] + 1 + 32 <= kCtaBitmapBits ? 2 : 1);
+#else
+            if (c) kind = du < cta_min ? 0 : (n - 1 - u + 32 <= kCtaBitmapBits ? 2 : 1);
+#endif
         }
         uint32_t *dst[3] = {owners_warp, owners_cta, owners_bitmap};
 #pragma unroll

@@ -795,11 +795,16 @@ __global__ void __launch_bounds__(kIxThreads, CM != kCmNone ? 4 : TC_HASH_CTA_MI
             if (threadIdx.x == 0) d.pre[nl] = items;
             ib = (uint32_t)(((uint64_t)items * wib) / kHashWarps);
             ie = (uint32_t)(((uint64_t)items * (wib + 1)) / kHashWarps);
+            __syncthreads();   // every descriptor is written before any warp probes
         };
         if (kBitmap) {
             // N+(x) lies in [lo_x, hi_x] (its first and last element, rows ascending): bits
             // [0, span) for ids lo_x .. hi_x, then one spare zero word; every other id maps to it
+#if TC_BITMAP_EFFSPAN
             const uint32_t base = col[xb], span = col[xb + dx - 1] - base + 1, words = span / 32 + 1;
+#else
+            const uint32_t base = x + 1, span = n - 1 - x, words = span / 32 + 1;
+#endif
             for (uint32_t w = threadIdx.x; w < words; w += blockDim.x) s_tab[w] = 0u;
             __syncthreads();
             for (uint32_t k = threadIdx.x; k < dx; k += blockDim.x) {

@@ -473,8 +473,11 @@ struct Bins {
 constexpr uint32_t kWarpTableSlots = 512;   // per-warp hash table (owner d+ <= 128, load <= 1/4)
 constexpr uint32_t kWarpTaskLists = 64;     // probe entries per warp task
 constexpr uint32_t kCtaTaskLists = 256;     // probe entries per CTA task (one descriptor batch)
+#ifndef TC_BITMAP_EFFSPAN
+#define TC_BITMAP_EFFSPAN 1   // bitmap over [min, max] of N+(x) (1) or over (x, n) (0)
+#endif
 #ifndef TC_BITMAP_BATCHES
-#define TC_BITMAP_BATCHES 4
+#define TC_BITMAP_BATCHES 1
 #endif
 constexpr uint32_t kBitmapBatches = TC_BITMAP_BATCHES;   // bitmap tasks: batches per bitmap build
 constexpr uint32_t kBitmapTaskLists = kCtaTaskLists * kBitmapBatches;

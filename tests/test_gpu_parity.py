@@ -433,7 +433,7 @@ def test_workspace_hook_counts_every_byte():
 
     def alloc(size, s):
         assert (s or 0) == stream          # ctypes passes the NULL (legacy) stream as None
-        p = torch._C._cuda_cudaCachingAllocator_raw_alloc(size, s)
+        p = torch._C._cuda_cudaCachingAllocator_raw_alloc(size, s or 0)
         live[p] = size
         log.append(size)
         return p
