@@ -163,13 +163,17 @@ typedef struct {
     uint64_t h2d_bytes;       /* bytes copied host->device (TC_HOST_PTRS)                   */
     uint64_t d2h_bytes;       /* bytes copied device->host                                   */
     uint64_t table_loads;     /* HASH: sum over owner tasks of d+(owner) (table builds)      */
-    uint64_t bytes_hash;      /* HASH algorithmic bytes: 4*work_probe + 8*HASH edges +
-                                 4*table_loads (the method's own a6 byte model)           */
+    uint64_t bytes_hash;      /* HASH algorithmic bytes: 4*(probes of the HASH / SHORT edges)
+                                 + 8*HASH edges + 4*table_loads (the a6 byte model)       */
     double ms_prune;          /* TC_PRUNE: the pruning rounds (inside ms_orient)             */
     uint64_t pruned_edges;    /* TC_PRUNE: undirected edges deleted                          */
     uint64_t prune_rounds;    /* TC_PRUNE: rounds executed (fixed-point mode: including the
                                  final round that deleted nothing)                         */
     uint64_t work_stage;      /* sum_v d-(v) d+(v): SURVEY 8(d)'s B_stage = 4(m + this) + 16m  */
+    uint64_t core_edges;      /* edges counted by the dense-core bitmap path (plain counts)    */
+    uint64_t core_words;      /* 32-bit word ANDs they took (work_probe still counts their
+                                 HASH-equivalent probes)                                     */
+    uint64_t bytes_core;      /* 8 * core_words: the core path's algorithmic bytes           */
 } tc_stats;
 
 /* Fill *opt with the defaults (auto variant selection, default stream). */
@@ -186,13 +190,13 @@ tc_status tc_count_ex(uint64_t n, uint64_t m, const uint64_t *row_offsets,
                       const uint32_t *col_indices, uint32_t flags, const tc_options *opt,
                       uint64_t *total, uint64_t *per_vertex, tc_stats *stats);
 
-/* Multi-GPU shard: every rank passes the SAME graph; the library
- * runs the (replicated) preprocessing, splits source vertices into `world`
- * contiguous-in-order groups of equal estimated work
- * sum_{v in N+(u)} (c + min(|N+(u) after v|, d+v)), c = 128 (the HASH probes plus a fixed
- * per-edge cost)
- * (prefix sum over sources, no communication), and counts only triangles whose
- * lowest-rank vertex falls in rank `rank`'s group.  partial_dev (device, 1
+/* Multi-GPU shard: every rank passes the SAME graph; the library runs the
+ * (replicated) preprocessing and binning, then splits the intersection work: HASH work by
+ * OWNER (the vertex whose N+ is staged as the table; owners are cut into `world` contiguous
+ * groups of equal estimated work -- probe lengths + 64 per probe entry + the table builds --
+ * by a prefix sum, so every table is built on exactly one rank) and the SHORT / MERGE /
+ * SEARCH edges by CSR edge range.  No communication is needed for the split; every
+ * triangle is counted on exactly one rank.  partial_dev (device, 1
  * entry) is OVERWRITTEN with this rank's partial count; per_vertex_partial
  * (device, n entries, nullable unless TC_PER_VERTEX) is overwritten with this
  * rank's per-vertex contributions.  Summing over ranks (one allreduce) gives

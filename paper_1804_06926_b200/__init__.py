@@ -110,7 +110,8 @@ class Stats(ctypes.Structure):
                 ("d2h_bytes", ctypes.c_uint64), ("table_loads", ctypes.c_uint64),
                 ("bytes_hash", ctypes.c_uint64), ("ms_prune", ctypes.c_double),
                 ("pruned_edges", ctypes.c_uint64), ("prune_rounds", ctypes.c_uint64),
-                ("work_stage", ctypes.c_uint64)]
+                ("work_stage", ctypes.c_uint64), ("core_edges", ctypes.c_uint64),
+                ("core_words", ctypes.c_uint64), ("bytes_core", ctypes.c_uint64)]
 
 
 class ClusteringSummary(ctypes.Structure):

@@ -15,15 +15,18 @@
 // probes N+(v) into a table of N+(u): such out-part entries are compacted in CSR
 // order (so grouped by u) by a tile scan.  Owner x's entries = in-list ++ out-part.
 //
-// Multi-GPU: sources are split into `world` groups by an exclusive
-// prefix of per-source work w(u) = sum_{v in N+(u)} (c + min(|N+(u) after v|, d+v)); a rank keeps
-// only the edges whose source is in its group.  The split needs no communication.
+// Multi-GPU: every rank bins every edge identically; then the HASH work is
+// split by OWNER -- owners are cut into `world` contiguous groups by an exclusive prefix of
+// their work w(x) (k_owner_work: probe lengths + a fixed cost per entry + the table builds),
+// so each owner's table is built on exactly one rank -- and the SHORT / MERGE / SEARCH
+// edges by CSR edge range.  No communication: every rank computes the same prefix.
 #include "block_scan.cuh"
 #include "tc_internal.cuh"
 
 namespace tc {
 
-__device__ __forceinline__ void warp_append(bool take, uint64_t *counter, uint2 *out, uint2 item) {
+template <class Item>
+__device__ __forceinline__ void warp_append(bool take, uint64_t *counter, Item *out, Item item) {
     uint32_t mask = __ballot_sync(0xffffffffu, take);
     if (!mask) return;
     int lane = threadIdx.x & 31;
@@ -50,6 +53,7 @@ __global__ void __launch_bounds__(kTileThreads)
     k_edges(HashParams hp, const uint64_t *__restrict__ m_dev, uint32_t *__restrict__ ulo,
             uint32_t *__restrict__ obits, uint32_t *__restrict__ tcount,
             uint2 *__restrict__ b_short, uint2 *__restrict__ b_merge, uint2 *__restrict__ b_search,
+            uint4 *__restrict__ b_core,
             uint64_t *__restrict__ counts) {
     __shared__ uint32_t s_row[kTileItems];
     __shared__ uint32_t s_scan[kTileThreads / 32];
@@ -68,8 +72,7 @@ __global__ void __launch_bounds__(kTileThreads)
     }
     uint32_t len = (uint32_t)min((uint64_t)kTileItems, m - t0);
     tile_rows(hp.off, hp.n, t0, len, s_row, s_scan);
-    const uint64_t chunk = work_chunk(hp);
-    uint64_t W = 0, probe = 0, skipped = 0, hashed = 0, outs = 0;
+    uint64_t W = 0, probe = 0, skipped = 0, hashed = 0, outs = 0, cedges = 0, cwords = 0, cprobe = 0;
     // striped: each warp handles 32 consecutive edges per round (warp-aggregated
     // appends); the loads of kBatch rounds are issued before any is used
     constexpr int kRounds = kTileItems / kTileThreads, kBatch = 4;
@@ -97,23 +100,38 @@ __global__ void __launch_bounds__(kTileThreads)
             int bin = -1;
             bool outp = false;
             uint2 item = make_uint2(0, 0);
+            uint32_t cw0 = 0, cw1 = 0;
             if (i < len) {
                 uint64_t e = t0 + i;
                 uint32_t u = us[j], x = xs[j], dv = dvs[j];
                 uint64_t ue = ues[j];
                 uint32_t du = (uint32_t)(ue - ubs[j]), suf = (uint32_t)(ue - e - 1);
-                // statistics count this rank's edges only (per-rank scope at world > 1)
-                const bool mine = hp.world <= 1 || rank_owner(hp, chunk, u) == hp.rank;
-                if (mine) {
+                bin = edge_bin(hp, du, dv, suf);
+                uint32_t w0 = 0, w1 = 0;
+                if (bin == TC_VARIANT_HASH && hp.core && u >= hp.core_lo &&
+                    core_edge(hp, u, x, min(suf, dv), hp.col[ue - 1], hp.col[hp.off[x + 1] - 1], w0, w1))
+                    bin = kBinCore;
+                cw0 = w0;
+                cw1 = w1;
+                // world > 1: HASH edges are binned on every rank (split later by owner, whose
+                // statistics k_owners counts); the other bins keep this rank's edge range
+                const bool mine = hp.world <= 1 || bin == TC_VARIANT_HASH ||
+                                  split_rank(e, m, hp.world) == hp.rank;
+                if (!mine) bin = -1;
+                if (mine && (hp.world <= 1 || bin != TC_VARIANT_HASH)) {
                     W += du + dv;
                     probe += min(suf, dv);
+                    skipped += bin < 0;
+                    if (bin == kBinCore) {
+                        cedges++;
+                        cwords += w1 - w0 + 1;
+                        cprobe += min(suf, dv);
+                    }
                 }
-                bin = mine ? edge_bin(hp, du, dv, suf) : -1;
-                skipped += mine && bin < 0;
                 item = make_uint2(u, x);
                 uint32_t ri = 0;
                 if (bin == TC_VARIANT_HASH) {
-                    hashed++;
+                    hashed += hp.world <= 1;
                     if (suf <= dv) ri = (uint32_t)(e + 1);
                     else outp = true;
                 }
@@ -137,6 +155,9 @@ __global__ void __launch_bounds__(kTileThreads)
             }
             warp_append(bin == TC_VARIANT_MERGE, &counts[1], b_merge, item);
             warp_append(bin == TC_VARIANT_SEARCH, &counts[2], b_search, item);
+            if (hp.core)   // dense-core edges: (u, x, w0 | w1 << 16) for core.cu (warp-uniform test)
+                warp_append(bin == kBinCore, &counts[12], b_core,
+                            make_uint4(item.x, item.y, cw0 | (cw1 << 16), 0u));
         }
     }
     __syncthreads();
@@ -150,8 +171,16 @@ __global__ void __launch_bounds__(kTileThreads)
     skipped = block_sum_u64(skipped, s_red);
     hashed = block_sum_u64(hashed, s_red);
     outs = block_sum_u64(outs, s_red);
+    cedges = block_sum_u64(cedges, s_red);
+    cwords = block_sum_u64(cwords, s_red);
+    cprobe = block_sum_u64(cprobe, s_red);
     if (threadIdx.x == 0) {
         tcount[blockIdx.x] = (uint32_t)outs;
+        if (cedges) {
+            atomicAdd((unsigned long long *)&counts[13], (unsigned long long)cedges);
+            atomicAdd((unsigned long long *)&counts[14], (unsigned long long)cwords);
+            atomicAdd((unsigned long long *)&counts[15], (unsigned long long)cprobe);
+        }
         atomicAdd((unsigned long long *)&counts[3], (unsigned long long)hashed);
         atomicAdd((unsigned long long *)&counts[4], (unsigned long long)W);
         atomicAdd((unsigned long long *)&counts[5], (unsigned long long)probe);
@@ -215,8 +244,11 @@ struct OutPrefix {
 // hash owners (the rest).
 // Also writes ooff[u] (each owner's first out-part entry; ooff[n] = the total), which the
 // owner counts here need anyway: no separate pass over the vertices.
+template <bool shard>
 __global__ void k_owners(const uint32_t *__restrict__ dplus, const uint32_t *__restrict__ col,
-                         const uint64_t *__restrict__ in_off,
+                         const uint64_t *__restrict__ in_off, const uint32_t *__restrict__ in_src,
+                         const uint2 *__restrict__ orange, const uint64_t *__restrict__ owner_prefix,
+                         int rank, int world,
                          const uint32_t *__restrict__ ulo, uint32_t *__restrict__ has_in,
                          uint64_t *__restrict__ ooff, const uint64_t *__restrict__ off,
                          const uint64_t *__restrict__ m_dev, const uint32_t *__restrict__ obits,
@@ -233,26 +265,51 @@ __global__ void k_owners(const uint32_t *__restrict__ dplus, const uint32_t *__r
     if (blockIdx.x == 0 && threadIdx.x == 0) ooff[n] = op.at(off[n]);
     int lane = threadIdx.x & 31;
     uint32_t lt = (1u << lane) - 1u;
+    uint64_t s_hashed = 0, s_probe = 0, s_W = 0;   // shard statistics (this rank's owners)
     for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < end; u += stride) {
         int kind = -1;
         if (u < n) {
             uint32_t du = dplus[u];
             local_max = max(local_max, du);
-            const uint64_t o0 = op.at(off[u]);
-            ooff[u] = o0;
             uint32_t c = 0, hin = 0;
-            if (du) {
-                // does some in-entry of u carry this rank's HASH work?  (first hit exits)
-                uint64_t ib = in_off[u], ie = in_off[u + 1];
-                for (uint64_t p = ib; p < ie; p++)
-                    if (ulo[p]) {
-                        hin = 1;
-                        break;
+            if (shard) {   // k_owner_work wrote has_in, pcnt and the owner work prefix
+                c = pcnt[u];
+                if (c && split_rank(owner_prefix[u], owner_prefix[n], world) != rank) c = 0;
+                if (c) {   // this rank's owner: its HASH statistics
+                    hin = has_in[u];
+                    const uint64_t ib = in_off[u], ie = hin ? in_off[u + 1] : ib;
+                    for (uint64_t p = ib; p < ie; p++) {
+                        const uint32_t lo = ulo[p];
+                        if (!lo) continue;
+                        const uint32_t src = in_src[p];
+                        const uint64_t sb = off[src], se = off[src + 1];
+                        s_hashed++;
+                        s_probe += se - lo;
+                        s_W += (se - sb) + du;
                     }
-                c = (hin ? (uint32_t)(ie - ib) : 0u) + (uint32_t)(op.at(off[u + 1]) - o0);
+                    for (uint64_t k = ooff[u], ke = ooff[u + 1]; k < ke; k++) {
+                        const uint2 r = orange[k];
+                        s_hashed++;
+                        s_probe += r.y - r.x;
+                        s_W += du + (r.y - r.x);
+                    }
+                }
+            } else {
+                const uint64_t o0 = op.at(off[u]);
+                ooff[u] = o0;
+                if (du) {
+                    // does some in-entry of u carry HASH work?  (first hit exits)
+                    uint64_t ib = in_off[u], ie = in_off[u + 1];
+                    for (uint64_t p = ib; p < ie; p++)
+                        if (ulo[p]) {
+                            hin = 1;
+                            break;
+                        }
+                    c = (hin ? (uint32_t)(ie - ib) : 0u) + (uint32_t)(op.at(off[u + 1]) - o0);
+                }
+                has_in[u] = hin;
+                pcnt[u] = c;
             }
-            has_in[u] = hin;
-            pcnt[u] = c;
             // bitmap owners: N+(u) spans [first, last] element (rows ascending) + a spare word
 #if TC_BITMAP_EFFSPAN
             if (c)
@@ -275,6 +332,67 @@ __global__ void k_owners(const uint32_t *__restrict__ dplus, const uint32_t *__r
     }
     local_max = __reduce_max_sync(0xffffffffu, local_max);
     if (lane == 0) atomicMax((unsigned long long *)&counts[7], (unsigned long long)local_max);
+    if (shard) {
+        s_hashed = warp_sum_u64(s_hashed);
+        s_probe = warp_sum_u64(s_probe);
+        s_W = warp_sum_u64(s_W);
+        if (lane == 0 && s_hashed) {
+            atomicAdd((unsigned long long *)&counts[3], (unsigned long long)s_hashed);
+            atomicAdd((unsigned long long *)&counts[4], (unsigned long long)s_W);
+            atomicAdd((unsigned long long *)&counts[5], (unsigned long long)s_probe);
+        }
+    }
+}
+
+// world > 1, before k_owners: for every owner x, has_in / pcnt as k_owners computes them, the
+// first out-part entry ooff[x], and its work w(x) = sum over its probe entries of
+// (kEntryCost + probe length) + (table builds: d+(x) + bitmap words, per CTA task).
+#ifndef TC_SHARD_ENTRY_COST
+#define TC_SHARD_ENTRY_COST 64   // fixed cost of a probe entry (descriptor, partial slots), in probes
+#endif
+__global__ void k_owner_work(const uint32_t *__restrict__ dplus, const uint32_t *__restrict__ col,
+                             const uint64_t *__restrict__ off, const uint64_t *__restrict__ in_off,
+                             const uint32_t *__restrict__ in_src, const uint32_t *__restrict__ ulo,
+                             const uint64_t *__restrict__ m_dev, const uint32_t *__restrict__ obits,
+                             const uint16_t *__restrict__ wpre, const uint64_t *__restrict__ toff,
+                             const uint64_t *__restrict__ ototal, const uint2 *__restrict__ orange,
+                             uint64_t n, uint32_t *__restrict__ has_in, uint32_t *__restrict__ pcnt,
+                             uint64_t *__restrict__ ooff, uint64_t *__restrict__ work) {
+    const OutPrefix op{obits, wpre, toff, *m_dev, *ototal};
+    if (blockIdx.x == 0 && threadIdx.x == 0) ooff[n] = op.at(off[n]);
+    for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
+         u += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t du = dplus[u];
+        const uint64_t o0 = op.at(off[u]), o1 = op.at(off[u + 1]);
+        ooff[u] = o0;
+        uint64_t w = 0;
+        uint32_t hin = 0, entries = 0;
+        if (du) {
+            const uint64_t ib = in_off[u], ie = in_off[u + 1];
+            for (uint64_t p = ib; p < ie; p++) {
+                const uint32_t lo = ulo[p];
+                if (!lo) continue;
+                hin = 1;
+                entries++;
+                w += TC_SHARD_ENTRY_COST + (off[in_src[p] + 1] - lo);
+            }
+            for (uint64_t k = o0; k < o1; k++) {
+                const uint2 r = orange[k];
+                entries++;
+                w += TC_SHARD_ENTRY_COST + (r.y - r.x);
+            }
+            const uint32_t c = (hin ? (uint32_t)(ie - ib) : 0u) + (uint32_t)(o1 - o0);
+            pcnt[u] = c;
+            if (c) {
+                const uint64_t span = (uint64_t)col[off[u + 1] - 1] - col[off[u]] + 1;
+                w += (uint64_t)((c + kCtaTaskLists - 1) / kCtaTaskLists) * (du + span / 32);
+            }
+        } else {
+            pcnt[u] = 0;
+        }
+        has_in[u] = hin;
+        work[u] = w;
+    }
 }
 
 // Tasks: owner i of `owners` (i < *ocount) gets ceil(pcnt / L) tasks.
@@ -342,8 +460,9 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
     hp.force = p.force;
     hp.rank = p.rank;
     hp.world = p.world;
-    hp.work_prefix = p.work_prefix;
     uint32_t tiles = (uint32_t)((cap + kTileItems - 1) / kTileItems);
+    // dense core (core.cu): plain counts under the AUTO policy only
+    if (p.core && p.force < 0) core_build(ctx, g, hp);
 
     // edge bins for the merge / search / two-pointer variants (filled by k_edges)
     // only the bins that can receive edges get capacity (at s26 each is 8.6 GB): AUTO
@@ -352,6 +471,9 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
                           p.force == TC_VARIANT_MERGE,
                           p.force == TC_VARIANT_SEARCH || (p.force < 0 && p.skew_ratio > 0)};
     for (int k = 0; k < 3; k++) bins.edges[k] = ctx.alloc<uint2>(want[k] ? cap : 1);
+    // dense-core edges: only the core sources' rows can hold them
+    bins.core_edges = ctx.alloc<uint4>(hp.core ? std::min<uint64_t>(cap, (uint64_t)hp.core_words * 32 *
+                                                                     hp.core_words * 16) : 1);
 
     // HASH: in-part ranges (in-list order), out-part entries (compacted, CSR order),
     // statistics, owners, tasks
@@ -366,6 +488,7 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
     if (tiles) {
         k_edges<<<tiles, kTileThreads, 0, ctx.stream>>>(hp, g.m_dev, ulo, obits, tcount,
                                                         bins.edges[0], bins.edges[1], bins.edges[2],
+                                                        bins.core_edges,
                                                         bins.count);
         TC_LAUNCHED(ctx);
     }
@@ -385,9 +508,23 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
     bins.owners_cta = ctx.alloc<uint32_t>(n);
     bins.owners_bitmap = ctx.alloc<uint32_t>(n);
     uint32_t cta_min = p.hub_min < kWarpTableSlots / 4 + 1 ? p.hub_min : kWarpTableSlots / 4 + 1;
-    k_owners<<<ctx.persistent_grid(4), 256, 0, ctx.stream>>>(
-        g.dplus, g.col, g.in_off, ulo, has_in, ooff, g.off, g.m_dev, obits, wpre, toff, toff + tiles, n,
-        cta_min, bins.pcnt, bins.owners_warp, bins.owners_cta, bins.owners_bitmap, bins.count);
+    if (p.world > 1) {   // owner split: work per owner, its exclusive prefix, then this rank's owners
+        uint64_t *work = ctx.alloc<uint64_t>(n), *wprefix = ctx.alloc<uint64_t>(n + 1);
+        k_owner_work<<<ctx.persistent_grid(8), 256, 0, ctx.stream>>>(
+            g.dplus, g.col, g.off, g.in_off, g.in_src, ulo, g.m_dev, obits, wpre, toff, toff + tiles,
+            orange, n, has_in, bins.pcnt, ooff, work);
+        TC_LAUNCHED(ctx);
+        scan_exclusive(ctx, work, wprefix, n);
+        k_owners<true><<<ctx.persistent_grid(4), 256, 0, ctx.stream>>>(
+            g.dplus, g.col, g.in_off, g.in_src, orange, wprefix, p.rank, p.world, ulo, has_in, ooff,
+            g.off, g.m_dev, obits, wpre, toff, toff + tiles, n, cta_min, bins.pcnt, bins.owners_warp,
+            bins.owners_cta, bins.owners_bitmap, bins.count);
+    } else {
+        k_owners<false><<<ctx.persistent_grid(4), 256, 0, ctx.stream>>>(
+            g.dplus, g.col, g.in_off, g.in_src, orange, nullptr, 0, 1, ulo, has_in, ooff, g.off,
+            g.m_dev, obits, wpre, toff, toff + tiles, n, cta_min, bins.pcnt, bins.owners_warp,
+            bins.owners_cta, bins.owners_bitmap, bins.count);
+    }
     TC_LAUNCHED(ctx);
     make_tasks(ctx, n, cap, bins.owners_warp, bins.count + 8, bins.pcnt, g.dplus, kWarpTaskLists,
                bins.count + 11, bins.tasks_warp, bins.ntasks_warp);
@@ -395,34 +532,6 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
                bins.count + 11, bins.tasks_cta, bins.ntasks_cta);
     make_tasks(ctx, n, cap, bins.owners_bitmap, bins.count + 10, bins.pcnt, g.dplus, kBitmapTaskLists,
                bins.count + 11, bins.tasks_bitmap, bins.ntasks_bitmap);
-}
-
-// Per-source work estimate w(u) = sum_{v in N+(u)} (c + min(|N+(u) after v|, d+v)) -- the
-// probe work the HASH kernels will do for u's edges plus a fixed per-edge cost c -- then
-// its exclusive prefix.
-#ifndef TC_WORK_EDGE_COST
-#define TC_WORK_EDGE_COST 128  // fixed cost of an edge (descriptor, partial slots, table builds), in probes;
-                               // calibrated on per-rank a6 times
-#endif
-__global__ void k_work(const uint64_t *__restrict__ off, const uint32_t *__restrict__ col,
-                       const uint32_t *__restrict__ dplus, uint64_t n, uint64_t *__restrict__ work) {
-    for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
-         u += (uint64_t)gridDim.x * blockDim.x) {
-        uint64_t b = off[u], e = off[u + 1];
-        uint32_t du = (uint32_t)(e - b);
-        uint64_t w = 0;
-        (void)du;
-        // the HASH cost of edge k: min(|N+(u) after col[k]|, d+(col[k])) probes (+1 per edge)
-        for (uint64_t k = b; k < e; k++) w += TC_WORK_EDGE_COST + min((uint32_t)(e - k - 1), dplus[col[k]]);
-        work[u] = w;
-    }
-}
-
-void work_prefix(Ctx &ctx, const Oriented &g, uint64_t *prefix) {
-    uint64_t *work = ctx.alloc<uint64_t>(g.n);
-    k_work<<<ctx.persistent_grid(8), 256, 0, ctx.stream>>>(g.off, g.col, g.dplus, g.n, work);
-    TC_LAUNCHED(ctx);
-    scan_exclusive(ctx, work, prefix, g.n);
 }
 
 }  // namespace tc

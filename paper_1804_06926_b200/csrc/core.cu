@@ -1,0 +1,118 @@
+// core.cu -- a6 + a7 for the DENSE CORE: word-parallel intersection of adjacency bitmaps.
+//
+// After the rank relabelling (orient.cu) the highest-ranked vertices -- the highest
+// degrees -- are the last ids, and their mutual adjacency is dense (R-MAT / power-law hubs
+// form a dense core).  For an oriented edge (u, x), u < x, the triangles it closes are
+// w in N+(u) with w > x and w in N+(x) (the forward algorithm, Alg. 2 Compute_Intersection
+// P:345-352, "the number of triangles formed with e is N"); if u lies in the core
+// [core_lo, n) then so do x and every w.  So with one bitmap per core vertex y -- bit
+// (z - core_lo) set iff z in N+(y) -- the count is
+//
+//     c(u, x) = sum over words k in [w0, w1] of popc(B_u[k] & B_x[k])
+//
+// over the words covering (x, min(last N+(u), last N+(x))] (B_x has no bit <= x, so the
+// AND needs no mask).  That costs w1 - w0 + 1 word operations instead of min(suf, d+x)
+// shared-memory probes (intersect.cu HASH); binning (bin.cu) sends an edge here when its
+// word count is at most its probe count (core_edge, tc_internal.cuh).  Only the plain
+// count uses it (per-vertex / edge / list credits need the individual matches).
+//
+// Layout: K = core_words * 32 core ids (the top min(TC_CORE_MAX, n) ranks, rounded up to
+// 128), row r = vertex core_lo + r, words [0, core_words) each (K^2 / 8 bytes: 32 MB at
+// K = 16384, L2-resident); only the words a row can ever be read at -- from the 16-byte
+// group holding its own vertex's word on -- are written (about half).  The paper has no such path (its kernels merge or
+// binary-search); this is the B200-first replacement of its "TwoLarge"
+// kernel for the densest lists.
+#include "tc_internal.cuh"
+
+namespace tc {
+
+#ifndef TC_CORE_MAX
+#define TC_CORE_MAX 16384
+#endif
+constexpr uint32_t kCoreMax = TC_CORE_MAX;          // core ids (multiple of 128)
+constexpr uint32_t kCoreMaxWords = kCoreMax / 32;
+static_assert(kCoreMax % 128 == 0, "rows are read as 16-byte groups");
+constexpr int kCoreBuildWarps = 8;
+
+// One warp per core vertex y: its row is assembled in shared memory (zero, set the bits of
+// N+(y) with shared atomics) and stored from y's own word on, 16 bytes per lane.
+__global__ void __launch_bounds__(kCoreBuildWarps * 32)
+    k_core_build(const uint64_t *__restrict__ off, const uint32_t *__restrict__ col, uint32_t n,
+                 uint32_t core_lo, uint32_t words, uint32_t *__restrict__ bm) {
+    __shared__ __align__(16) uint32_t s_row[kCoreBuildWarps][kCoreMaxWords];
+    const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    uint32_t *row = s_row[wib];
+    for (uint32_t y = core_lo + blockIdx.x * kCoreBuildWarps + wib; y < n;
+         y += gridDim.x * kCoreBuildWarps) {
+        const uint32_t w_first = ((y - core_lo) >> 5) & ~3u;   // 16-byte aligned start
+        for (uint32_t k = w_first + lane; k < words; k += 32) row[k] = 0u;
+        __syncwarp();
+        const uint64_t b = off[y], e = off[y + 1];
+        for (uint64_t k = b + lane; k < e; k += 32) {
+            const uint32_t o = col[k] - core_lo;
+            atomicOr(&row[o >> 5], 1u << (o & 31));
+        }
+        __syncwarp();
+        uint4 *dst = reinterpret_cast<uint4 *>(bm + (uint64_t)(y - core_lo) * words);
+        const uint4 *src = reinterpret_cast<const uint4 *>(row);
+        for (uint32_t q = (w_first >> 2) + lane; q < (words >> 2); q += 32) dst[q] = src[q];
+        __syncwarp();
+    }
+}
+
+// The core edges binned by k_edges (bin.cu) as (u, x, w0 | w1 << 16), in about CSR order
+// (consecutive edges share u: its row stays in L1).  Groups of 8 lanes share an edge: 32
+// words (8 x 16 bytes of each row) per step; persistent, grid-strided over the list.
+constexpr int kCoreGroup = 8;
+__global__ void __launch_bounds__(256)
+    k_core_count(const uint32_t *__restrict__ core, uint32_t core_lo, uint32_t core_words,
+                 const uint4 *__restrict__ edges, const uint64_t *__restrict__ count,
+                 uint64_t *__restrict__ total) {
+    __shared__ uint64_t s_red[32];
+    const uint64_t ne = *count;
+    const uint32_t gl = threadIdx.x % kCoreGroup;
+    const uint64_t g0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / kCoreGroup;
+    const uint64_t ng = ((uint64_t)gridDim.x * blockDim.x) / kCoreGroup;
+    uint64_t acc = 0;
+    for (uint64_t i = g0; i < ne; i += ng) {
+        const uint4 it = edges[i];
+        const uint32_t w0 = it.z & 0xffffu, w1 = it.z >> 16;
+        const uint4 *bu = reinterpret_cast<const uint4 *>(core + (uint64_t)(it.x - core_lo) * core_words);
+        const uint4 *bx = reinterpret_cast<const uint4 *>(core + (uint64_t)(it.y - core_lo) * core_words);
+        // 16-byte groups from w0 & ~3: row x is written from its 16-byte group holding x's
+        // own word on (k_core_build), and its words below w0 cover ids <= x, so they are 0
+        for (uint32_t q = (w0 >> 2) + gl; q <= (w1 >> 2); q += kCoreGroup) {
+            const uint4 a = __ldg(bu + q), b = __ldg(bx + q);
+            acc += __popc(a.x & b.x) + __popc(a.y & b.y) + __popc(a.z & b.z) + __popc(a.w & b.w);
+        }
+    }
+    const uint64_t t = block_sum_u64(acc, s_red);
+    if (threadIdx.x == 0 && t) atomicAdd((unsigned long long *)total, (unsigned long long)t);
+}
+
+void core_build(Ctx &ctx, const Oriented &g, HashParams &hp) {
+    hp.core = nullptr;
+    const uint32_t n = (uint32_t)g.n;
+    if (n == 0) return;
+    const uint32_t K = std::min<uint64_t>(kCoreMax, ((uint64_t)n + 127) / 128 * 128);
+    hp.core_lo = n > K ? n - K : 0u;
+    hp.core_words = K / 32;
+    uint32_t *bm = ctx.alloc<uint32_t>((uint64_t)K * hp.core_words);
+    const uint32_t rows = n - hp.core_lo;
+    const uint32_t grid = std::min<uint32_t>((rows + kCoreBuildWarps - 1) / kCoreBuildWarps,
+                                             (uint32_t)ctx.persistent_grid(4));
+    k_core_build<<<grid, kCoreBuildWarps * 32, 0, ctx.stream>>>(g.off, g.col, n, hp.core_lo,
+                                                                 hp.core_words, bm);
+    TC_LAUNCHED(ctx);
+    hp.core = bm;
+}
+
+void core_count(Ctx &ctx, const HashParams &hp, const uint4 *edges, const uint64_t *count,
+                uint64_t *total_dev, cudaStream_t stream) {
+    if (!hp.core) return;
+    k_core_count<<<ctx.persistent_grid(8), 256, 0, stream>>>(hp.core, hp.core_lo, hp.core_words,
+                                                              edges, count, total_dev);
+    TC_LAUNCHED(ctx);
+}
+
+}  // namespace tc

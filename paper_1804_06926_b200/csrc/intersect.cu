@@ -290,6 +290,9 @@ constexpr uint32_t kHashChunk = 1024;  // owner elements per table build (load f
 #ifndef TC_HASH_CTA_MINBLOCKS
 #define TC_HASH_CTA_MINBLOCKS 8
 #endif
+#ifndef TC_HASH_PREFETCH
+#define TC_HASH_PREFETCH 0
+#endif
 constexpr int kUnroll = TC_HASH_UNROLL;  // independent 32-slot windows per probe step
 constexpr int kHashWarps = kIxThreads / 32;
 
@@ -576,6 +579,19 @@ __device__ __forceinline__ uint64_t probe_quads(const Probe &contains,
 #pragma unroll
             for (int v = 0; v < kSlot / 4; v++) q[k][v] = ld_probe(col4 + (uint64_t)qi * (kSlot / 4) + v);
             i0 = __shfl_sync(0xffffffffu, li, 31);  // list holding slot wk + 31
+#if TC_HASH_PREFETCH
+            {   // this lane's slot of the NEXT window, found the same way, prefetched into L1 so
+                // its loads hit while this window is probed (no registers held across)
+                const uint32_t wn = wk + 32 * kUnroll, jn = i0 + 1 + lane;
+                const uint32_t sn = (jn < nl ? d.pre[jn] : 0xffffffffu) - wn;
+                const uint32_t stn = __reduce_or_sync(0xffffffffu, sn < 32 ? (1u << sn) : 0u);
+                const uint32_t tn = wn + lane;
+                if (tn < ie) {
+                    const uint32_t qn = d.pk[i0 + __popc(stn & le_mask)].x + tn;
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(col4 + (uint64_t)qn * (kSlot / 4)));
+                }
+            }
+#endif
         }
 #pragma unroll
         for (int k = 0; k < kUnroll; k++) {
@@ -914,6 +930,8 @@ static void launch_all(Ctx &ctx, const Oriented &g, const Bins &bins, uint64_t *
     TC_LAUNCHED(ctx);
     k_short<CM><<<grid, kIxThreads, 0, s2>>>(bins.edges[0], bins.count + 0, g.off, g.col, total, cr);
     TC_LAUNCHED(ctx);
+    if (CM == kCmNone)   // dense-core edges (core.cu)
+        core_count(ctx, bins.hp, bins.core_edges, bins.count + 12, total, s2);
     side.join();
 }
 

@@ -298,12 +298,7 @@ static void run(Call &c) {
         bp.force = c.opt.force_variant;
         bp.rank = c.rank;
         bp.world = c.world;
-        bp.work_prefix = nullptr;
-        if (c.world > 1) {
-            uint64_t *prefix = ctx.alloc<uint64_t>(c.n + 1);
-            work_prefix(ctx, g, prefix);
-            bp.work_prefix = prefix;
-        }
+        bp.core = (c.mode == kCount || c.mode == kShard) && !pv;   // plain count only
         Bins bins;
         bin_edges(ctx, g, bp, bins);
         phase_end(tm, kBin);
@@ -437,9 +432,13 @@ static void run(Call &c) {
         st.max_dplus = pin[7];
         st.table_loads = pin[11];
         st.work_stage = pin[12];
+        st.core_edges = pin[13];
+        st.core_words = pin[14];
         // bytes the HASH method reads in a6: probed elements + one 8-byte range per probe
         // entry (<= 2 per edge, 1 for ~96%) + the owners' lists for the table builds
-        st.bytes_hash = 4 * st.work_probe + 8 * st.bin_edges[3] + 4 * st.table_loads;
+        // (core edges are binned before HASH; their probes pin[15] are not HASH bytes)
+        st.bytes_hash = 4 * (st.work_probe - pin[15]) + 8 * st.bin_edges[3] + 4 * st.table_loads;
+        st.bytes_core = 8 * st.core_words;
         st.kernel_launches = ctx.launches;
         if (prune.enabled && c.n > 0 && c.M > 0) {
             st.ms_prune = tm->ms(kPrune);

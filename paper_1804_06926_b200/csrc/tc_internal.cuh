@@ -423,20 +423,41 @@ struct HashParams {
     const uint2 *orange = nullptr;     //   probe ranges [lo, hi) of col+
     const uint32_t *ovid = nullptr;    //   the edge's target (per-vertex credit), or its CSR
                                        //   index when binned with edge_ids (edge support)
-    const uint64_t *work_prefix = nullptr;  // multi-GPU source split (world > 1)
     uint32_t n = 0, short_max = 0, skew_ratio = 0;
     int force = -1, rank = 0, world = 1;
+    // dense core (core.cu): rank ids [core_lo, n) have adjacency bitmaps of core_words words
+    // each; nullptr = no core path (per-vertex / edge / list modes, forced variants)
+    const uint32_t *core = nullptr;
+    uint32_t core_lo = 0, core_words = 0;
 };
 
-// ceil(total work / world) for the multi-GPU source split (0 when world == 1).
-__device__ __forceinline__ uint64_t work_chunk(const HashParams &hp) {
-    return hp.world > 1 ? (hp.work_prefix[hp.n] + hp.world - 1) / hp.world : 0;
+constexpr int kBinCore = 4;   // internal bin of k_edges: dense-core edge (core.cu)
+
+// Dense-core decision (core.cu header), shared by binning and the core kernel so both take
+// it identically: an edge (u, x) whose source u is in the core intersects inside the core
+// id range (x, min(last(u), last(x))]; words [w0, w1] of the core bitmaps cover it.  It goes
+// to the core path when its word count is at most its HASH probe count.
+#ifndef TC_CORE_WORDS_PER_PROBE
+#define TC_CORE_WORDS_PER_PROBE 1   // a core edge takes <= this many words per probe it saves
+#endif
+__device__ __forceinline__ bool core_edge(const HashParams &hp, uint32_t u, uint32_t x, uint32_t probe,
+                                          uint32_t last_u, uint32_t last_x, uint32_t &w0, uint32_t &w1) {
+    if (!hp.core || u < hp.core_lo || probe == 0) return false;
+    const uint32_t hi = min(last_u, last_x);
+    if (hi <= x) return false;
+    w0 = (x + 1 - hp.core_lo) >> 5;
+    w1 = (hi - hp.core_lo) >> 5;
+    return (uint64_t)(w1 - w0 + 1) <= (uint64_t)probe * TC_CORE_WORDS_PER_PROBE;
 }
-// Rank owning source u: floor(prefix[u] / chunk), clamped.
-__device__ __forceinline__ int rank_owner(const HashParams &hp, uint64_t chunk, uint32_t u) {
-    if (hp.world <= 1 || chunk == 0) return 0;
-    uint64_t r = hp.work_prefix[u] / chunk;
-    return r >= (uint64_t)hp.world ? hp.world - 1 : (int)r;
+
+// Multi-GPU split (world > 1): the rank of a unit whose exclusive work prefix is
+// `pre`, out of `total`: floor(pre / ceil(total / world)), clamped.  Deterministic on every
+// rank, no communication.
+__device__ __forceinline__ int split_rank(uint64_t pre, uint64_t total, int world) {
+    if (world <= 1) return 0;
+    const uint64_t chunk = (total + world - 1) / world;
+    const uint64_t r = chunk ? pre / chunk : 0;
+    return r >= (uint64_t)world ? world - 1 : (int)r;
 }
 // Variant of oriented edge (u,v): -1 = cannot close a triangle (suf = |N+(u) after
 // v| = 0, or d+(v) = 0); else the forced variant, or the AUTO policy.
@@ -454,6 +475,7 @@ __device__ __forceinline__ int edge_bin(const HashParams &hp, uint32_t du, uint3
 // followed, if it owns out-part edges, by its own row.
 struct Bins {
     uint2 *edges[3] = {nullptr, nullptr, nullptr};  // SHORT, MERGE, SEARCH: (u, v) pairs
+    uint4 *core_edges = nullptr;  // dense-core edges (u, x, w0 | w1 << 16); count at count[12]
     uint64_t *count = nullptr;  // device: [0..3] SHORT/MERGE/SEARCH/HASH edges, [4] W,
                                 // [5] sum min(|N+(u) after v|, d+(v)), [6] skipped, [7] max d+,
                                 // [8] warp owners, [9] CTA hash owners, [10] CTA bitmap owners,
@@ -487,12 +509,18 @@ struct BinParams {
     uint32_t short_max, skew_ratio, hub_min;
     int force;
     int rank, world;
-    const uint64_t *work_prefix;  // exclusive prefix of per-source work (world > 1)
     bool edge_ids = false;        // out-part entries record their edge's CSR index (kCmEdge)
+    bool core = false;            // route dense-core edges to the core path (count mode, AUTO)
 };
 
 void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins);
-void work_prefix(Ctx &ctx, const Oriented &g, uint64_t *prefix /* n+1 */);
+
+// Dense core (core.cu): builds the adjacency bitmaps of the top-ranked vertices into
+// hp.core / core_lo / core_words (count mode only; a no-op when the graph is empty).
+void core_build(Ctx &ctx, const Oriented &g, HashParams &hp);
+// a6 + a7 for the core edges (plain count): popc of bitmap ANDs, added into total_dev.
+void core_count(Ctx &ctx, const HashParams &hp, const uint4 *edges, const uint64_t *count,
+                uint64_t *total_dev, cudaStream_t stream);
 
 // What each triangle found in a6 credits besides the total (intersect.cu header).
 enum CreditMode { kCmNone = 0, kCmVertex = 1, kCmEdge = 2, kCmList = 3, kCmTop = 4 };

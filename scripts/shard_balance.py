@@ -12,6 +12,9 @@ import torch
 import graphgen as G
 import paper_1804_06926_b200 as tc
 
+if os.environ.get("TC_LIB"):   # a variants/<name>/libtc_b200.so build
+    tc._LIB_PATH = os.environ["TC_LIB"]
+
 out = {}
 for scale in [int(a) for a in sys.argv[1:]] or [21, 24]:
     g = G.rmat(scale, 16)
@@ -32,7 +35,8 @@ for scale in [int(a) for a in sys.argv[1:]] or [21, 24]:
         assert sum(parts) == T1
         res[f"world{world}"] = {"ix_ms": ix, "ix_max_over_mean": max(ix) / (sum(ix) / world),
                                 "ix_speedup": st1["ms_intersect"] / max(ix),
-                                "total_ms_per_rank": tot}
+                                "ix_sum_over_world1": sum(ix) / st1["ms_intersect"],
+                                "total_ms_per_rank": tot, "projected_step_ms": max(tot)}
     out[g.name] = res
     print(json.dumps({g.name: res}), flush=True)
     del rp, cl

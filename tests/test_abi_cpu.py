@@ -49,7 +49,7 @@ def test_struct_layout(lib):
     assert o.force_variant == -1 and o.keep_workspace == 1
     assert not o.alloc and not o.free and not o.alloc_ctx
     assert o.prune_rounds == 0 and not any(o.reserved)
-    assert ctypes.sizeof(tc.Stats) == 7 * 8 + 19 * 8
+    assert ctypes.sizeof(tc.Stats) == 7 * 8 + 22 * 8
     assert ctypes.sizeof(tc.ClusteringSummary) == 32
 
 

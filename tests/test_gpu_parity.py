@@ -174,7 +174,8 @@ def test_stats_consistent():
     assert st["m_undirected"] == st_o["m"] and st["work_W"] == st_o["W"]
     assert st["max_dplus"] == st_o["max_dplus"]
     assert st["bytes_alg"] == 4 * st_o["W"] + 16 * st_o["m"]
-    assert sum(st["bin_edges"]) + st["skipped_edges"] == st_o["m"]
+    # the bins, the dense-core edges and the skipped edges partition the edge set
+    assert sum(st["bin_edges"]) + st["core_edges"] + st["skipped_edges"] == st_o["m"]
     assert st["work_stage"] == st_o["sum_dminus_dplus"]          # SURVEY 8(d) B_stage
     assert st["kernel_launches"] > 0
 
@@ -493,3 +494,42 @@ def test_wrong_device_pointer_rejected():
     with torch.cuda.device(0):
         assert lib.tc_count_ex(g.n, g.arcs, rp.data_ptr(), cl.data_ptr(), 0, None,
                                __import__("ctypes").addressof(total), None, None) == 1
+
+
+# ------------------------------------------------------------------ dense core (core.cu)
+CORE_GRAPHS = {
+    "karate": G.karate,                                   # n < 128: the whole graph is the core
+    "K700": lambda: G.complete(700),
+    "rmat14": lambda: G.rmat(14, 16, seed=21),
+    "rmat17": lambda: G.rmat(17, 16, seed=22),             # n > the 16384-id core
+    "clique": lambda: G.clique_union(60_000, 90_000),
+    "gnp": lambda: G.gnp(3000, 0.05, 7),
+    "kron2": lambda: G.kron_power(G.karate(), 2),
+}
+
+
+@pytest.mark.parametrize("name", sorted(CORE_GRAPHS))
+def test_core_path_counts(name):
+    """Plain counts under AUTO route dense-core edges to the bitmap-AND path (core.cu); the
+    total must equal the oracle, and the core path must have run where the graph has a core."""
+    g = CORE_GRAPHS[name]()
+    T = O.count(g.n, g.rowptr, g.col)
+    got, st = gpu_count(g.rowptr, g.col, with_stats=True)
+    assert got == T
+    if name != "karate":
+        assert st["core_edges"] > 0 and st["core_words"] > 0, st
+    # the per-vertex call does not use the core path: same total, zero core edges
+    got2, _, st2 = gpu_count(g.rowptr, g.col, per_vertex=True, with_stats=True)
+    assert got2 == T and st2["core_edges"] == 0
+    # a forced variant disables it too
+    got3, st3 = gpu_count(g.rowptr, g.col, force_variant=tc.VARIANT_HASH, with_stats=True)
+    assert got3 == T and st3["core_edges"] == 0
+    # shards: core edges split by edge range, HASH by owner
+    rp, cl = on_dev(g.rowptr, g.col)
+    for world in (2, 3, 8):
+        tot = 0
+        for r in range(world):
+            p = torch.zeros(1, dtype=torch.int64, device=DEV)
+            tc.count_shard(rp, cl, r, world, p)
+            tot += int(p.item())
+        assert tot == T, world
