@@ -305,6 +305,28 @@ def next_rows_23(tc, torch, np, graphgen, rp, cl, flush, stream, m, T, count_ms)
     return rows
 
 
+def small_graph_latency(tc, torch, graphgen, dev, reps=50):
+    """Launch-bound regime: one synchronous tc_count_ex on Zachary's karate club
+    (BASELINE configs[0]) from device pointers, host wall clock per call (median of `reps`),
+    through the one-kernel small-graph path and through the general pipeline."""
+    import numpy as np
+    g = graphgen.karate()
+    rp = torch.from_numpy(g.rowptr.view(np.int64)).to(dev)
+    cl = torch.from_numpy(g.col.view(np.int32)).to(dev)
+    out = {"workload": "karate (n=34, 78 edges)"}
+    for name, kw in (("one_kernel", {}), ("pipeline", {"tiny_max_n": 0})):
+        for _ in range(5):
+            T, st = tc.count_ex(rp, cl, with_stats=True, **kw)
+        us = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            T = tc.count_ex(rp, cl, **kw)
+            us.append(1e6 * (time.perf_counter() - t0))
+        assert T == 45
+        out[name] = {"us_per_call": sorted(us)[len(us) // 2], "launches": st["kernel_launches"]}
+    return out
+
+
 # ------------------------------------------------------------------ a6 traffic (ncu, same run)
 A6_KERNELS = "regex:k_hash|k_short|k_merge|k_search"
 NCU_METRICS = ("dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
@@ -551,6 +573,7 @@ def main():
             "wedges": summ["wedges"], "timing": "median of 5 calls, L2 flushed before each",
             "call": "tc_clustering (device pointers): count with per-vertex t(v) + local c(v) for all n"}}
         line["survey_clean_input"] = clean_input_ms(tc, torch, rp, cl, flush, stream, T_total)
+        line["small_graph"] = small_graph_latency(tc, torch, graphgen, dev)
         line["next_rows"].update(next_rows_23(tc, torch, np, graphgen, rp, cl, flush, stream, m,
                                               T_total, ms))
     if world == 1 and not args.no_cpu_baseline:

@@ -139,6 +139,11 @@ typedef struct {
     tc_alloc_fn alloc;          /* workspace hook (both or neither); NULL = library pool       */
     tc_free_fn free;
     void *alloc_ctx;            /* passed to alloc / free                                       */
+    uint32_t tiny_max_n;        /* tc_count / tc_count_ex / tc_count_shard on graphs with
+                                   n <= min(tiny_max_n, 1024) (AUTO, no TC_PRUNE / TC_ID_ORDER):
+                                   the whole method in ONE kernel on a shared-memory adjacency
+                                   bitmap (small graphs are launch-bound); 0 = off.
+                                   Default 1024.  Stats then carry m_undirected and times only */
     uint32_t reserved[8];       /* must be zero                                                 */
 } tc_options;
 

@@ -50,7 +50,8 @@ class Options(ctypes.Structure):
                 ("hub_min_dplus", ctypes.c_uint32), ("force_variant", ctypes.c_int32),
                 ("stream", ctypes.c_void_p), ("prune_rounds", ctypes.c_uint32),
                 ("keep_workspace", ctypes.c_uint32), ("alloc", ALLOC_FN), ("free", FREE_FN),
-                ("alloc_ctx", ctypes.c_void_p), ("reserved", ctypes.c_uint32 * 8)]
+                ("alloc_ctx", ctypes.c_void_p), ("tiny_max_n", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint32 * 8)]
 
 
 def _torch_raw_alloc(ctx, size, stream):
@@ -206,7 +207,8 @@ def _flags(clean=False, sorted_rows=False, per_vertex=False, validate=False, pru
 
 
 def _options(stream=None, force_variant=None, short_max=None, skew_ratio=None, hub_min_dplus=None,
-             prune_rounds=None, on_device=True, allocator=None, device=None, keep_workspace=None):
+             prune_rounds=None, on_device=True, allocator=None, device=None, keep_workspace=None,
+             tiny_max_n=None):
     """tc_options for one call.  Device calls default to the current stream of the inputs'
     device and to torch's caching allocator for the workspace."""
     o = Options()
@@ -232,6 +234,8 @@ def _options(stream=None, force_variant=None, short_max=None, skew_ratio=None, h
         o.prune_rounds = prune_rounds
     if keep_workspace is not None:
         o.keep_workspace = int(bool(keep_workspace))
+    if tiny_max_n is not None:
+        o.tiny_max_n = tiny_max_n
     return o
 
 

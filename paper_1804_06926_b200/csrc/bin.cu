@@ -49,7 +49,13 @@ __device__ __forceinline__ void warp_append(bool take, uint64_t *counter, Item *
 // (32 consecutive edges) and the tile's out-part count (tcount) replace a per-edge
 // range array.  SHORT / MERGE / SEARCH edges are appended to their bins.  Also accumulates
 // the work statistics.
-__global__ void __launch_bounds__(kTileThreads)
+#ifndef TC_EDGES_MINBLOCKS
+#define TC_EDGES_MINBLOCKS 4   // 64 registers: measured s21 bin -0.09 ms, road -0.19 ms
+#endif
+#ifndef TC_EDGES_BATCH
+#define TC_EDGES_BATCH 4
+#endif
+__global__ void __launch_bounds__(kTileThreads, TC_EDGES_MINBLOCKS)
     k_edges(HashParams hp, const uint64_t *__restrict__ m_dev, uint32_t *__restrict__ ulo,
             uint32_t *__restrict__ obits, uint32_t *__restrict__ tcount,
             uint2 *__restrict__ b_short, uint2 *__restrict__ b_merge, uint2 *__restrict__ b_search,
@@ -75,7 +81,7 @@ __global__ void __launch_bounds__(kTileThreads)
     uint64_t W = 0, probe = 0, skipped = 0, hashed = 0, outs = 0, cedges = 0, cwords = 0, cprobe = 0;
     // striped: each warp handles 32 consecutive edges per round (warp-aggregated
     // appends); the loads of kBatch rounds are issued before any is used
-    constexpr int kRounds = kTileItems / kTileThreads, kBatch = 4;
+    constexpr int kRounds = kTileItems / kTileThreads, kBatch = TC_EDGES_BATCH;
 #pragma unroll 1
     for (int r0 = 0; r0 < kRounds; r0 += kBatch) {
         uint32_t us[kBatch], xs[kBatch], ps[kBatch], dvs[kBatch];
@@ -107,12 +113,11 @@ __global__ void __launch_bounds__(kTileThreads)
                 uint64_t ue = ues[j];
                 uint32_t du = (uint32_t)(ue - ubs[j]), suf = (uint32_t)(ue - e - 1);
                 bin = edge_bin(hp, du, dv, suf);
-                uint32_t w0 = 0, w1 = 0;
-                if (bin == TC_VARIANT_HASH && hp.core && u >= hp.core_lo &&
-                    core_edge(hp, u, x, min(suf, dv), hp.col[ue - 1], hp.col[hp.off[x + 1] - 1], w0, w1))
-                    bin = kBinCore;
-                cw0 = w0;
-                cw1 = w1;
+                if (bin == TC_VARIANT_HASH && hp.core && u >= hp.core_lo) {
+                    // (suf > 0 here: the element after x in N+(u) is col+[e + 1])
+                    const int ce = core_edge(hp, u, x, hp.col[e + 1], min(suf, dv), cw0, cw1);
+                    bin = ce == 1 ? kBinCore : (ce == 2 ? -1 : bin);
+                }
                 // world > 1: HASH edges are binned on every rank (split later by owner, whose
                 // statistics k_owners counts); the other bins keep this rank's edge range
                 const bool mine = hp.world <= 1 || bin == TC_VARIANT_HASH ||
@@ -124,7 +129,7 @@ __global__ void __launch_bounds__(kTileThreads)
                     skipped += bin < 0;
                     if (bin == kBinCore) {
                         cedges++;
-                        cwords += w1 - w0 + 1;
+                        cwords += cw1 - cw0 + 1;
                         cprobe += min(suf, dv);
                     }
                 }
@@ -249,7 +254,7 @@ __global__ void k_owners(const uint32_t *__restrict__ dplus, const uint32_t *__r
                          const uint64_t *__restrict__ in_off, const uint32_t *__restrict__ in_src,
                          const uint2 *__restrict__ orange, const uint64_t *__restrict__ owner_prefix,
                          int rank, int world,
-                         const uint32_t *__restrict__ ulo, uint32_t *__restrict__ has_in,
+                         const uint32_t *__restrict__ ulo, uint32_t *__restrict__ in_cnt,
                          uint64_t *__restrict__ ooff, const uint64_t *__restrict__ off,
                          const uint64_t *__restrict__ m_dev, const uint32_t *__restrict__ obits,
                          const uint16_t *__restrict__ wpre, const uint64_t *__restrict__ toff,
@@ -272,12 +277,12 @@ __global__ void k_owners(const uint32_t *__restrict__ dplus, const uint32_t *__r
             uint32_t du = dplus[u];
             local_max = max(local_max, du);
             uint32_t c = 0, hin = 0;
-            if (shard) {   // k_owner_work wrote has_in, pcnt and the owner work prefix
+            (void)hin;
+            if (shard) {   // k_owner_work wrote in_cnt, pcnt and the owner work prefix
                 c = pcnt[u];
                 if (c && split_rank(owner_prefix[u], owner_prefix[n], world) != rank) c = 0;
                 if (c) {   // this rank's owner: its HASH statistics
-                    hin = has_in[u];
-                    const uint64_t ib = in_off[u], ie = hin ? in_off[u + 1] : ib;
+                    const uint64_t ib = in_off[u], ie = ib + in_cnt[u];
                     for (uint64_t p = ib; p < ie; p++) {
                         const uint32_t lo = ulo[p];
                         if (!lo) continue;
@@ -302,12 +307,12 @@ __global__ void k_owners(const uint32_t *__restrict__ dplus, const uint32_t *__r
                     uint64_t ib = in_off[u], ie = in_off[u + 1];
                     for (uint64_t p = ib; p < ie; p++)
                         if (ulo[p]) {
-                            hin = 1;
+                            hin = (uint32_t)(ie - ib);
                             break;
                         }
-                    c = (hin ? (uint32_t)(ie - ib) : 0u) + (uint32_t)(op.at(off[u + 1]) - o0);
+                    c = hin + (uint32_t)(op.at(off[u + 1]) - o0);
                 }
-                has_in[u] = hin;
+                in_cnt[u] = hin;
                 pcnt[u] = c;
             }
             // bitmap owners: N+(u) spans [first, last] element (rows ascending) + a spare word
@@ -356,8 +361,9 @@ __global__ void k_owner_work(const uint32_t *__restrict__ dplus, const uint32_t 
                              const uint64_t *__restrict__ m_dev, const uint32_t *__restrict__ obits,
                              const uint16_t *__restrict__ wpre, const uint64_t *__restrict__ toff,
                              const uint64_t *__restrict__ ototal, const uint2 *__restrict__ orange,
-                             uint64_t n, uint32_t *__restrict__ has_in, uint32_t *__restrict__ pcnt,
-                             uint64_t *__restrict__ ooff, uint64_t *__restrict__ work) {
+                             uint64_t n, uint32_t *__restrict__ in_cnt,
+                             uint32_t *__restrict__ pcnt, uint64_t *__restrict__ ooff,
+                             uint64_t *__restrict__ work) {
     const OutPrefix op{obits, wpre, toff, *m_dev, *ototal};
     if (blockIdx.x == 0 && threadIdx.x == 0) ooff[n] = op.at(off[n]);
     for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
@@ -382,6 +388,7 @@ __global__ void k_owner_work(const uint32_t *__restrict__ dplus, const uint32_t 
                 w += TC_SHARD_ENTRY_COST + (r.y - r.x);
             }
             const uint32_t c = (hin ? (uint32_t)(ie - ib) : 0u) + (uint32_t)(o1 - o0);
+            in_cnt[u] = hin ? (uint32_t)(ie - ib) : 0u;
             pcnt[u] = c;
             if (c) {
                 const uint64_t span = (uint64_t)col[off[u + 1] - 1] - col[off[u]] + 1;
@@ -389,8 +396,8 @@ __global__ void k_owner_work(const uint32_t *__restrict__ dplus, const uint32_t 
             }
         } else {
             pcnt[u] = 0;
+            in_cnt[u] = 0;
         }
-        has_in[u] = hin;
         work[u] = w;
     }
 }
@@ -484,7 +491,7 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
     uint32_t *ovid = ctx.alloc<uint32_t>(cap);
     uint32_t *tcount = ctx.alloc<uint32_t>(tiles + 1);
     uint64_t *toff = ctx.alloc<uint64_t>(tiles + 1), *ooff = ctx.alloc<uint64_t>(n + 1);
-    uint32_t *has_in = ctx.alloc<uint32_t>(n + 1);
+    uint32_t *in_cnt = ctx.alloc<uint32_t>(n + 1);
     if (tiles) {
         k_edges<<<tiles, kTileThreads, 0, ctx.stream>>>(hp, g.m_dev, ulo, obits, tcount,
                                                         bins.edges[0], bins.edges[1], bins.edges[2],
@@ -499,7 +506,7 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
         TC_LAUNCHED(ctx);
     }
     hp.ulo = ulo;
-    hp.has_in = has_in;
+    hp.in_cnt = in_cnt;
     hp.orange = orange;
     hp.ovid = ovid;
     hp.ooff = ooff;
@@ -508,20 +515,23 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
     bins.owners_cta = ctx.alloc<uint32_t>(n);
     bins.owners_bitmap = ctx.alloc<uint32_t>(n);
     uint32_t cta_min = p.hub_min < kWarpTableSlots / 4 + 1 ? p.hub_min : kWarpTableSlots / 4 + 1;
+    // (core owners keep the now-empty entries of their core edges in their in-lists:
+    // compacting them in place, one CTA per core owner, measured +0.43 ms in binning for
+    // -0.13 ms in a6 at s21)
     if (p.world > 1) {   // owner split: work per owner, its exclusive prefix, then this rank's owners
         uint64_t *work = ctx.alloc<uint64_t>(n), *wprefix = ctx.alloc<uint64_t>(n + 1);
         k_owner_work<<<ctx.persistent_grid(8), 256, 0, ctx.stream>>>(
             g.dplus, g.col, g.off, g.in_off, g.in_src, ulo, g.m_dev, obits, wpre, toff, toff + tiles,
-            orange, n, has_in, bins.pcnt, ooff, work);
+            orange, n, in_cnt, bins.pcnt, ooff, work);
         TC_LAUNCHED(ctx);
         scan_exclusive(ctx, work, wprefix, n);
         k_owners<true><<<ctx.persistent_grid(4), 256, 0, ctx.stream>>>(
-            g.dplus, g.col, g.in_off, g.in_src, orange, wprefix, p.rank, p.world, ulo, has_in, ooff,
+            g.dplus, g.col, g.in_off, g.in_src, orange, wprefix, p.rank, p.world, ulo, in_cnt, ooff,
             g.off, g.m_dev, obits, wpre, toff, toff + tiles, n, cta_min, bins.pcnt, bins.owners_warp,
             bins.owners_cta, bins.owners_bitmap, bins.count);
     } else {
         k_owners<false><<<ctx.persistent_grid(4), 256, 0, ctx.stream>>>(
-            g.dplus, g.col, g.in_off, g.in_src, orange, nullptr, 0, 1, ulo, has_in, ooff, g.off,
+            g.dplus, g.col, g.in_off, g.in_src, orange, nullptr, 0, 1, ulo, in_cnt, ooff, g.off,
             g.m_dev, obits, wpre, toff, toff + tiles, n, cta_min, bins.pcnt, bins.owners_warp,
             bins.owners_cta, bins.owners_bitmap, bins.count);
     }

@@ -16,10 +16,12 @@
 // word count is at most its probe count (core_edge, tc_internal.cuh).  Only the plain
 // count uses it (per-vertex / edge / list credits need the individual matches).
 //
-// Layout: K = core_words * 32 core ids (the top min(TC_CORE_MAX, n) ranks, rounded up to
-// 128), row r = vertex core_lo + r, words [0, core_words) each (K^2 / 8 bytes: 32 MB at
-// K = 16384, L2-resident); only the words a row can ever be read at -- from the 16-byte
-// group holding its own vertex's word on -- are written (about half).  The paper has no such path (its kernels merge or
+// Layout: K = core_words * 32 core ids (the top K ranks, K = 16384 or 32768 below / from 2^23
+// vertices, at most n rounded up to 128), row r = vertex core_lo + r, words [0, core_words)
+// each (K^2 / 8 bytes: 32 MB at K = 16384, L2-resident); only the words a row can ever be
+// read at -- from the 16-byte group holding its own vertex's word on -- are written (about
+// half).  core_range[r] = (first, last) element of N+(core_lo + r) bounds the word range of
+// every core edge (core_edge, tc_internal.cuh).  The paper has no such path (its kernels merge or
 // binary-search); this is the B200-first replacement of its "TwoLarge"
 // kernel for the densest lists.
 #include "tc_internal.cuh"
@@ -27,18 +29,26 @@
 namespace tc {
 
 #ifndef TC_CORE_MAX
-#define TC_CORE_MAX 16384
+#define TC_CORE_MAX 32768
 #endif
-constexpr uint32_t kCoreMax = TC_CORE_MAX;          // core ids (multiple of 128)
+#ifndef TC_CORE_SMALL
+#define TC_CORE_SMALL 16384
+#endif
+// core ids K (multiple of 128): TC_CORE_SMALL below 2^23 vertices (the core bitmaps stay
+// L2-resident next to the rest of the a6 working set), TC_CORE_MAX from there on (measured:
+// s21 16384 vs 32768 equal, s24 32768 -1.4 ms)
+constexpr uint32_t kCoreMax = TC_CORE_MAX;
 constexpr uint32_t kCoreMaxWords = kCoreMax / 32;
-static_assert(kCoreMax % 128 == 0, "rows are read as 16-byte groups");
+static_assert(kCoreMax % 128 == 0 && TC_CORE_SMALL % 128 == 0 && TC_CORE_SMALL <= kCoreMax,
+              "rows are read as 16-byte groups");
 constexpr int kCoreBuildWarps = 8;
 
 // One warp per core vertex y: its row is assembled in shared memory (zero, set the bits of
 // N+(y) with shared atomics) and stored from y's own word on, 16 bytes per lane.
 __global__ void __launch_bounds__(kCoreBuildWarps * 32)
     k_core_build(const uint64_t *__restrict__ off, const uint32_t *__restrict__ col, uint32_t n,
-                 uint32_t core_lo, uint32_t words, uint32_t *__restrict__ bm) {
+                 uint32_t core_lo, uint32_t words, uint32_t *__restrict__ bm,
+                 uint2 *__restrict__ range) {
     __shared__ __align__(16) uint32_t s_row[kCoreBuildWarps][kCoreMaxWords];
     const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     uint32_t *row = s_row[wib];
@@ -48,6 +58,7 @@ __global__ void __launch_bounds__(kCoreBuildWarps * 32)
         for (uint32_t k = w_first + lane; k < words; k += 32) row[k] = 0u;
         __syncwarp();
         const uint64_t b = off[y], e = off[y + 1];
+        if (lane == 0) range[y - core_lo] = e > b ? make_uint2(col[b], col[e - 1]) : make_uint2(~0u, 0u);
         for (uint64_t k = b + lane; k < e; k += 32) {
             const uint32_t o = col[k] - core_lo;
             atomicOr(&row[o >> 5], 1u << (o & 31));
@@ -94,17 +105,20 @@ void core_build(Ctx &ctx, const Oriented &g, HashParams &hp) {
     hp.core = nullptr;
     const uint32_t n = (uint32_t)g.n;
     if (n == 0) return;
-    const uint32_t K = std::min<uint64_t>(kCoreMax, ((uint64_t)n + 127) / 128 * 128);
+    const uint32_t cap = n < (1u << 23) ? TC_CORE_SMALL : kCoreMax;
+    const uint32_t K = std::min<uint64_t>(cap, ((uint64_t)n + 127) / 128 * 128);
     hp.core_lo = n > K ? n - K : 0u;
     hp.core_words = K / 32;
     uint32_t *bm = ctx.alloc<uint32_t>((uint64_t)K * hp.core_words);
+    uint2 *range = ctx.alloc<uint2>(K);
     const uint32_t rows = n - hp.core_lo;
     const uint32_t grid = std::min<uint32_t>((rows + kCoreBuildWarps - 1) / kCoreBuildWarps,
                                              (uint32_t)ctx.persistent_grid(4));
     k_core_build<<<grid, kCoreBuildWarps * 32, 0, ctx.stream>>>(g.off, g.col, n, hp.core_lo,
-                                                                 hp.core_words, bm);
+                                                                 hp.core_words, bm, range);
     TC_LAUNCHED(ctx);
     hp.core = bm;
+    hp.core_range = range;
 }
 
 void core_count(Ctx &ctx, const HashParams &hp, const uint4 *edges, const uint64_t *count,

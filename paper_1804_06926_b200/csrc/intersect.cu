@@ -705,7 +705,7 @@ __global__ void __launch_bounds__(kIxThreads, TC_HASH_WARP_MINBLOCKS)
         uint64_t xb = hp.off[x];
         uint32_t dx = (uint32_t)(hp.off[x + 1] - xb);
         uint64_t inb = hp.in_off[x], ob = hp.ooff[x];
-        uint32_t indeg = hp.has_in[x] ? (uint32_t)(hp.in_off[x + 1] - inb) : 0u;
+        uint32_t indeg = hp.in_cnt[x];
         uint32_t ocnt = (uint32_t)(hp.ooff[x + 1] - ob);
         uint32_t j0 = task.y * L;
         // descriptors of entries j0 + lane, j0 + 32 + lane; non-empty ones compacted in
@@ -792,7 +792,7 @@ __global__ void __launch_bounds__(kIxThreads, CM != kCmNone ? 4 : TC_HASH_CTA_MI
         uint64_t xb = hp.off[x];
         uint32_t dx = (uint32_t)(hp.off[x + 1] - xb);
         uint64_t inb = hp.in_off[x], ob = hp.ooff[x];
-        uint32_t indeg = hp.has_in[x] ? (uint32_t)(hp.in_off[x + 1] - inb) : 0u;
+        uint32_t indeg = hp.in_cnt[x];
         uint32_t ocnt = (uint32_t)(hp.ooff[x + 1] - ob);
         uint64_t h = 0;
         // descriptors of the probe entries j0 + threadIdx.x (one per thread), compacted, and

@@ -254,7 +254,21 @@ static void run(Call &c) {
     PruneInfo prune;
     prune.enabled = c.flags & TC_PRUNE;
     prune.rounds_wanted = c.opt.prune_rounds;
-    if (c.n > 0 && c.M > 0) {
+    const bool tiny = (c.mode == kCount || c.mode == kShard) && c.n > 0 && c.M > 0 &&
+                      c.n <= c.opt.tiny_max_n && c.n <= kTinyMaxN && c.opt.force_variant < 0 &&
+                      !(c.flags & (TC_PRUNE | TC_ID_ORDER));
+    if (tiny) {   // one kernel (tiny.cu); a shard other than rank 0 contributes nothing
+        pin[16] = 0;
+        uint64_t *m_dev = ctx.alloc<uint64_t>(1);
+        TC_CUDA(cudaMemsetAsync(m_dev, 0, sizeof(uint64_t), ctx.stream));
+        phase_begin(tm, kIntersect);
+        if (c.mode != kShard || c.rank == 0)
+            tiny_count(ctx, c.n, rowptr, col, total_dev, pv_out ? pv_dev : nullptr, m_dev);
+        phase_end(tm, kIntersect);
+        if (c.stats)
+            TC_CUDA(cudaMemcpyAsync(pin + 16, m_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                                    ctx.stream));
+    } else if (c.n > 0 && c.M > 0) {
         Oriented g;
         if (c.flags & TC_CLEAN)
             orient_clean(ctx, c.n, c.M, rowptr, col, g, tm,
@@ -491,6 +505,7 @@ void tc_default_options(tc_options *opt) {
     opt->force_variant = TC_VARIANT_AUTO;
     opt->stream = nullptr;
     opt->keep_workspace = 1;
+    opt->tiny_max_n = (uint32_t)kTinyMaxN;
 }
 
 tc_status tc_trim_workspace(int device) {

@@ -415,8 +415,8 @@ struct HashParams {
     const uint64_t *in_off = nullptr;  // transposed CSR: in-lists
     const uint32_t *in_src = nullptr;
     const uint32_t *pidx = nullptr;    // CSR edge e -> its in-list slot
-    const uint32_t *has_in = nullptr;  // x: 1 if some in-part entry of x is this rank's HASH
-                                       // work (else x's probe entries skip its in-list)
+    const uint32_t *in_cnt = nullptr;  // x: entries of its in-list its tasks take (0 = none: no
+                                       // in-part entry of x is this rank's HASH work)
     const uint32_t *ulo = nullptr;     // in-edge p = (u,x): e+1 (probe range [e+1, off[u+1]) of
                                        // col+), 0 if not this rank's in-part HASH work
     const uint64_t *ooff = nullptr;    // compacted out-part entries of each owner:
@@ -428,26 +428,30 @@ struct HashParams {
     // dense core (core.cu): rank ids [core_lo, n) have adjacency bitmaps of core_words words
     // each; nullptr = no core path (per-vertex / edge / list modes, forced variants)
     const uint32_t *core = nullptr;
+    const uint2 *core_range = nullptr;   // (first, last) element of N+(y), y in the core
     uint32_t core_lo = 0, core_words = 0;
 };
 
 constexpr int kBinCore = 4;   // internal bin of k_edges: dense-core edge (core.cu)
 
-// Dense-core decision (core.cu header), shared by binning and the core kernel so both take
-// it identically: an edge (u, x) whose source u is in the core intersects inside the core
-// id range (x, min(last(u), last(x))]; words [w0, w1] of the core bitmaps cover it.  It goes
-// to the core path when its word count is at most its HASH probe count.
+// Dense-core decision (core.cu header) for an edge (u, x) whose source u is in the core (so
+// x and every common element are too): the common elements of N+(u) after x and N+(x) lie
+// in [max(next, first(x)), min(last(u), last(x))] (next = the element after x in N+(u));
+// words [w0, w1] of the core bitmaps cover it.  An empty range means no triangle (the edge
+// is skipped); otherwise the edge goes to the core path when its word count is at most
+// TC_CORE_WORDS_PER_PROBE times its HASH probe count.  Returns 0 (not core), 1 (core) or
+// 2 (empty range: no triangle).
 #ifndef TC_CORE_WORDS_PER_PROBE
-#define TC_CORE_WORDS_PER_PROBE 1   // a core edge takes <= this many words per probe it saves
+#define TC_CORE_WORDS_PER_PROBE 1
 #endif
-__device__ __forceinline__ bool core_edge(const HashParams &hp, uint32_t u, uint32_t x, uint32_t probe,
-                                          uint32_t last_u, uint32_t last_x, uint32_t &w0, uint32_t &w1) {
-    if (!hp.core || u < hp.core_lo || probe == 0) return false;
-    const uint32_t hi = min(last_u, last_x);
-    if (hi <= x) return false;
-    w0 = (x + 1 - hp.core_lo) >> 5;
+__device__ __forceinline__ int core_edge(const HashParams &hp, uint32_t u, uint32_t x, uint32_t next,
+                                         uint32_t probe, uint32_t &w0, uint32_t &w1) {
+    const uint2 ru = hp.core_range[u - hp.core_lo], rx = hp.core_range[x - hp.core_lo];
+    const uint32_t lo = max(next, rx.x), hi = min(ru.y, rx.y);
+    if (hi < lo) return 2;
+    w0 = (lo - hp.core_lo) >> 5;
     w1 = (hi - hp.core_lo) >> 5;
-    return (uint64_t)(w1 - w0 + 1) <= (uint64_t)probe * TC_CORE_WORDS_PER_PROBE;
+    return (uint64_t)(w1 - w0 + 1) <= (uint64_t)probe * TC_CORE_WORDS_PER_PROBE ? 1 : 0;
 }
 
 // Multi-GPU split (world > 1): the rank of a unit whose exclusive work prefix is
@@ -537,6 +541,12 @@ struct Credit {
 // a6 + a7: all intersection kernels; adds into total_dev and credits per `cr`.
 void intersect_all(Ctx &ctx, const Oriented &g, const Bins &bins, uint64_t *total_dev,
                    const Credit &cr);
+
+// tiny.cu: the whole count in one CTA for n <= kTinyMaxN (total, per-vertex t(v) in input
+// ids if pv_dev, and the undirected edge count m into m_dev).
+constexpr uint64_t kTinyMaxN = 1024;
+void tiny_count(Ctx &ctx, uint64_t n, const uint64_t *rowptr, const uint32_t *col,
+                uint64_t *total_dev, uint64_t *pv_dev, uint64_t *m_dev);
 
 // Validation (TC_VALIDATE); returns a TC_EGRAPH message or "".
 std::string validate_graph(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr,

@@ -533,3 +533,38 @@ def test_core_path_counts(name):
             tc.count_shard(rp, cl, r, world, p)
             tot += int(p.item())
         assert tot == T, world
+
+
+# ------------------------------------------------------------------ tiny graphs (tiny.cu)
+TINY_GRAPHS = {
+    "fig_mm": G.fig_mm, "karate": G.karate, "K20": lambda: G.complete(20),
+    "K1024": lambda: G.complete(1024),                               # the size limit
+    "gnp1000": lambda: G.dirty(G.gnp(1000, 0.1, 3), seed=4),          # duplicates, loops, reversed
+    "rmat10": lambda: G.rmat(10, 16, seed=5),
+    "wheel": lambda: G.wheel(600), "star": lambda: G.star(900), "path": lambda: G.path(1000),
+    "single": lambda: G.from_edges(2, [(0, 1)]),
+}
+
+
+@pytest.mark.parametrize("name", sorted(TINY_GRAPHS))
+def test_tiny_path(name):
+    """n <= 1024: the one-kernel path (tiny.cu) against the oracle, total and every t(v), and
+    against the general pipeline (tiny_max_n = 0) on the same input."""
+    g = TINY_GRAPHS[name]()
+    T, t = O.count(g.n, g.rowptr, g.col, per_vertex=True)
+    got, pv, st = gpu_count(g.rowptr, g.col, per_vertex=True, with_stats=True)
+    assert got == T and (pv_np(pv) == t).all()
+    assert st["kernel_launches"] == 1
+    assert st["m_undirected"] == O.count(g.n, g.rowptr, g.col, with_stats=True)[1]["m"]
+    assert gpu_count(g.rowptr, g.col) == T
+    got2, pv2 = gpu_count(g.rowptr, g.col, per_vertex=True, tiny_max_n=0)
+    assert got2 == T and (pv_np(pv2) == t).all()
+    rp, cl = on_dev(g.rowptr, g.col)
+    tot = 0
+    for r in range(3):            # shards: rank 0 takes the whole tiny graph
+        p = torch.zeros(1, dtype=torch.int64, device=DEV)
+        tc.count_shard(rp, cl, r, 3, p)
+        tot += int(p.item())
+    assert tot == T
+    h = tc.count_ex(g.rowptr, g.col, per_vertex=True)               # host pointers
+    assert h[0] == T and (h[1] == t).all()
