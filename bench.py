@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-next", action="store_true", help="skip the NEXT-row measurements")
     ap.add_argument("--one-call", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--clean-input", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--no-ncu", action="store_true",
                     help="skip the ncu DRAM-traffic capture of the a6 kernels (roofline.traffic)")
     return ap.parse_args()
@@ -238,18 +239,7 @@ def clean_input_ms(tc, torch, rp, cl, flush, stream, T):
     """SURVEY §8(d)'s own definition of the headline ms: from a CLEAN symmetric CSR resident on
     the device (TC_CLEAN | TC_SORTED: a1 skipped) to the count.  The clean CSR is prepared
     outside the timed region from the library's oriented CSR (torch sort: input plumbing)."""
-    n = rp.numel() - 1
-    off, colp = tc.orient(rp, cl)
-    src = torch.repeat_interleave(torch.arange(n, device=rp.device), off[1:] - off[:-1])
-    dst = colp.to(torch.int64)
-    b = max(1, (n - 1).bit_length())
-    keys = torch.cat([(src << b) | dst, (dst << b) | src])
-    keys, _ = torch.sort(keys)
-    s2, d2 = keys >> b, keys & ((1 << b) - 1)
-    crp = torch.zeros(n + 1, dtype=torch.int64, device=rp.device)
-    crp[1:] = torch.cumsum(torch.bincount(s2, minlength=n), 0)
-    ccl = d2.to(torch.int32).contiguous()
-    del off, colp, src, dst, keys, s2, d2
+    crp, ccl = clean_csr_of(tc, torch, rp, cl)
     ms, (Tc, st) = _timed(torch, flush, stream,
                           lambda: tc.count_ex(crp, ccl, clean=True, sorted_rows=True, with_stats=True))
     assert Tc == T
@@ -334,8 +324,24 @@ NCU_METRICS = ("dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.su
                "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed,lts__t_sector_hit_rate.pct")
 
 
+def clean_csr_of(tc, torch, rp, cl):
+    """The symmetric, sorted, simple CSR of the graph (input plumbing for SURVEY §8(d)'s clean-
+    input measurement, built outside any timed region from the library's oriented CSR)."""
+    n = rp.numel() - 1
+    off, colp = tc.orient(rp, cl)
+    src = torch.repeat_interleave(torch.arange(n, device=rp.device), off[1:] - off[:-1])
+    dst = colp.to(torch.int64)
+    b = max(1, (n - 1).bit_length())
+    keys, _ = torch.sort(torch.cat([(src << b) | dst, (dst << b) | src]))
+    s2, d2 = keys >> b, keys & ((1 << b) - 1)
+    crp = torch.zeros(n + 1, dtype=torch.int64, device=rp.device)
+    crp[1:] = torch.cumsum(torch.bincount(s2, minlength=n), 0)
+    return crp, d2.to(torch.int32).contiguous()
+
+
 def one_call(args):
-    """--one-call: ONE tc_count_ex on the bench workload (the process ncu profiles)."""
+    """--one-call: ONE tc_count_ex on the bench workload (the process ncu profiles);
+    --clean-input: on its clean sorted CSR (TC_CLEAN | TC_SORTED)."""
     import numpy as np
     import torch
     import graphgen
@@ -343,6 +349,10 @@ def one_call(args):
     g = graphgen.rmat(args.scale, args.edge_factor)
     rp = torch.from_numpy(g.rowptr.view(np.int64)).cuda()
     cl = torch.from_numpy(g.col.view(np.int32)).cuda()
+    if args.clean_input:
+        rp, cl = clean_csr_of(tc, torch, rp, cl)
+        print("T", tc.count_ex(rp, cl, clean=True, sorted_rows=True), flush=True)
+        return
     print("T", tc.count_ex(rp, cl), flush=True)
 
 
@@ -462,7 +472,9 @@ def main():
     bin_ms = sum(s["ms_bin"] for s in stats) / len(stats)
     st = stats[-1]
     # per-rank work statistics (tc_stats counts this rank's edges): summed over ranks
-    b_hash, b_alg_rank = st["bytes_hash"], st["bytes_alg"]
+    # a6 algorithmic bytes of the implemented method: HASH probes + ranges + table loads, plus
+    # the dense-core path's word ANDs (8 bytes per word pair)
+    b_hash, b_alg_rank = st["bytes_hash"] + st["bytes_core"], st["bytes_alg"]
     launches = st["kernel_launches"] * args.steps
     if dist is not None:
         t = torch.tensor([ms, ix_ms, bin_ms], dtype=torch.float64, device=dev)
@@ -521,9 +533,11 @@ def main():
             "frac": achieved / peak, "traffic": None,
             "kernel": "a6+a7 intersection phase (k_hash_cta bitmap + hash, k_hash_warp, k_short "
                       "[+ empty MERGE/SEARCH launches]), CUDA events on the launch stream",
-            "bytes_model": "B_hash = 4*sum min(|N+(u)>v|, d+v) + 8*HASH edges + 4*table loads "
-                           "(bytes the implemented a6 must read; DESIGN.md sec. 5), summed over ranks",
-            "bytes_hash": b_hash, "kernel_ms": ix_ms, "bin_ms": bin_ms, "peak_kind": peak_kind,
+            "bytes_model": "B_a6 = 4*(probes of HASH/SHORT edges) + 8*HASH edges + 4*table loads "
+                           "+ 8*core words (bytes the implemented a6 must read; DESIGN.md sec. 5), "
+                           "summed over ranks",
+            "bytes_a6": b_hash, "bytes_core": st["bytes_core"], "core_edges": st["core_edges"],
+            "kernel_ms": ix_ms, "bin_ms": bin_ms, "peak_kind": peak_kind,
             "work_W": st["work_W"], "work_probe": st["work_probe"], "table_loads": st["table_loads"]}
     if b_alg:
         a_alg = b_alg / (ix_ms * 1e-3) / 1e9

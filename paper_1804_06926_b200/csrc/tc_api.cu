@@ -247,6 +247,7 @@ static void run(Call &c) {
     TC_CUDA(cudaMemsetAsync(total_dev, 0, sizeof(uint64_t), ctx.stream));
     uint64_t *pin = pinned_scratch();
     if (c.stats) memset(pin, 0, 32 * sizeof(uint64_t));
+    pin[26] = 0;   // the false-TC_CLEAN flag of THIS call (check_claim)
 
     // Rows of N+ are always put in ascending order (a4): the merge / search variants need
     // it, and the HASH ranges probe only the part of N+(a) after b.
@@ -276,7 +277,6 @@ static void run(Call &c) {
         else
             orient_dirty(ctx, c.n, c.M, rowptr, col, g, tm,
                          prune, c.flags & TC_ID_ORDER);
-        pin[26] = 0;
         if (g.claim_err && (c.mode != kShard || c.stats))   // read at the final synchronisation
             TC_CUDA(cudaMemcpyAsync(pin + 26, g.claim_err, sizeof(uint32_t), cudaMemcpyDeviceToHost,
                                     ctx.stream));
