@@ -18,8 +18,10 @@
 // Multi-GPU: every rank bins every edge identically; then the HASH work is
 // split by OWNER -- owners are cut into `world` contiguous groups by an exclusive prefix of
 // their work w(x) (k_owner_work: probe lengths + a fixed cost per entry + the table builds),
-// so each owner's table is built on exactly one rank -- and the SHORT / MERGE / SEARCH
-// edges by CSR edge range.  No communication: every rank computes the same prefix.
+// so each owner's table is built on exactly one rank -- and the SHORT / MERGE / SEARCH / core
+// edges by interleaved 2048-edge blocks of CSR order (edge_rank; contiguous ranges would hand
+// the whole dense core, the last rows, to the last rank).  No communication: every rank
+// computes the same prefix.
 #include "block_scan.cuh"
 #include "tc_internal.cuh"
 
@@ -120,8 +122,7 @@ __global__ void __launch_bounds__(kTileThreads, TC_EDGES_MINBLOCKS)
                 }
                 // world > 1: HASH edges are binned on every rank (split later by owner, whose
                 // statistics k_owners counts); the other bins keep this rank's edge range
-                const bool mine = hp.world <= 1 || bin == TC_VARIANT_HASH ||
-                                  split_rank(e, m, hp.world) == hp.rank;
+                const bool mine = hp.world <= 1 || bin == TC_VARIANT_HASH || edge_rank(e, hp.world) == hp.rank;
                 if (!mine) bin = -1;
                 if (mine && (hp.world <= 1 || bin != TC_VARIANT_HASH)) {
                     W += du + dv;
@@ -251,7 +252,8 @@ struct OutPrefix {
 // owner counts here need anyway: no separate pass over the vertices.
 template <bool shard>
 __global__ void k_owners(const uint32_t *__restrict__ dplus, const uint32_t *__restrict__ col,
-                         const uint64_t *__restrict__ in_off, const uint32_t *__restrict__ in_src,
+                         const uint64_t *__restrict__ in_off, const uint64_t *__restrict__ pre_cnt,
+                         const uint64_t *__restrict__ pre_len,
                          const uint2 *__restrict__ orange, const uint64_t *__restrict__ owner_prefix,
                          int rank, int world,
                          const uint32_t *__restrict__ ulo, uint32_t *__restrict__ in_cnt,
@@ -281,17 +283,10 @@ __global__ void k_owners(const uint32_t *__restrict__ dplus, const uint32_t *__r
             if (shard) {   // k_owner_work wrote in_cnt, pcnt and the owner work prefix
                 c = pcnt[u];
                 if (c && split_rank(owner_prefix[u], owner_prefix[n], world) != rank) c = 0;
-                if (c) {   // this rank's owner: its HASH statistics
-                    const uint64_t ib = in_off[u], ie = ib + in_cnt[u];
-                    for (uint64_t p = ib; p < ie; p++) {
-                        const uint32_t lo = ulo[p];
-                        if (!lo) continue;
-                        const uint32_t src = in_src[p];
-                        const uint64_t sb = off[src], se = off[src + 1];
-                        s_hashed++;
-                        s_probe += se - lo;
-                        s_W += (se - sb) + du;
-                    }
+                if (c) {   // this rank's owner: its HASH statistics (W: out-part entries only)
+                    const uint64_t ib = in_off[u], ie = in_off[u + 1];
+                    s_hashed += pre_cnt[ie] - pre_cnt[ib];
+                    s_probe += pre_len[ie] - pre_len[ib];
                     for (uint64_t k = ooff[u], ke = ooff[u + 1]; k < ke; k++) {
                         const uint2 r = orange[k];
                         s_hashed++;
@@ -349,19 +344,35 @@ __global__ void k_owners(const uint32_t *__restrict__ dplus, const uint32_t *__r
     }
 }
 
-// world > 1, before k_owners: for every owner x, has_in / pcnt as k_owners computes them, the
+// world > 1: per in-list entry p (owner = its in-list's vertex), 1 and its probe length if it is
+// HASH work (ulo[p] != 0), else 0 / 0 -- prefix-scanned so every owner's sums are two
+// lookups (a thread per owner would walk a hub's 10^5-entry in-list alone).
+__global__ void k_entry_vals(const uint64_t *__restrict__ off, const uint32_t *__restrict__ in_src,
+                             const uint32_t *__restrict__ ulo, const uint64_t *__restrict__ m_dev,
+                             uint32_t *__restrict__ cnt, uint32_t *__restrict__ len) {
+    const uint64_t m = *m_dev;
+    for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
+         p += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t lo = ulo[p];
+        cnt[p] = lo ? 1u : 0u;
+        len[p] = lo ? (uint32_t)(off[in_src[p] + 1] - lo) : 0u;
+    }
+}
+
+// world > 1, before k_owners: for every owner x, in_cnt / pcnt as k_owners computes them, the
 // first out-part entry ooff[x], and its work w(x) = sum over its probe entries of
-// (kEntryCost + probe length) + (table builds: d+(x) + bitmap words, per CTA task).
+// (kEntryCost + probe length) + the table builds per CTA task (d+(x), plus the bitmap words
+// for a bitmap owner).
 #ifndef TC_SHARD_ENTRY_COST
 #define TC_SHARD_ENTRY_COST 64   // fixed cost of a probe entry (descriptor, partial slots), in probes
 #endif
 __global__ void k_owner_work(const uint32_t *__restrict__ dplus, const uint32_t *__restrict__ col,
                              const uint64_t *__restrict__ off, const uint64_t *__restrict__ in_off,
-                             const uint32_t *__restrict__ in_src, const uint32_t *__restrict__ ulo,
+                             const uint64_t *__restrict__ pre_cnt, const uint64_t *__restrict__ pre_len,
                              const uint64_t *__restrict__ m_dev, const uint32_t *__restrict__ obits,
                              const uint16_t *__restrict__ wpre, const uint64_t *__restrict__ toff,
                              const uint64_t *__restrict__ ototal, const uint2 *__restrict__ orange,
-                             uint64_t n, uint32_t *__restrict__ in_cnt,
+                             uint64_t n, uint32_t cta_min, uint32_t *__restrict__ in_cnt,
                              uint32_t *__restrict__ pcnt, uint64_t *__restrict__ ooff,
                              uint64_t *__restrict__ work) {
     const OutPrefix op{obits, wpre, toff, *m_dev, *ototal};
@@ -372,32 +383,27 @@ __global__ void k_owner_work(const uint32_t *__restrict__ dplus, const uint32_t 
         const uint64_t o0 = op.at(off[u]), o1 = op.at(off[u + 1]);
         ooff[u] = o0;
         uint64_t w = 0;
-        uint32_t hin = 0, entries = 0;
+        uint32_t c = 0, ic = 0;
         if (du) {
             const uint64_t ib = in_off[u], ie = in_off[u + 1];
-            for (uint64_t p = ib; p < ie; p++) {
-                const uint32_t lo = ulo[p];
-                if (!lo) continue;
-                hin = 1;
-                entries++;
-                w += TC_SHARD_ENTRY_COST + (off[in_src[p] + 1] - lo);
-            }
-            for (uint64_t k = o0; k < o1; k++) {
+            const uint64_t entries = pre_cnt[ie] - pre_cnt[ib];
+            w = entries * TC_SHARD_ENTRY_COST + (pre_len[ie] - pre_len[ib]);
+            for (uint64_t k = o0; k < o1; k++) {   // out-part: at most d+(u) entries
                 const uint2 r = orange[k];
-                entries++;
                 w += TC_SHARD_ENTRY_COST + (r.y - r.x);
             }
-            const uint32_t c = (hin ? (uint32_t)(ie - ib) : 0u) + (uint32_t)(o1 - o0);
-            in_cnt[u] = hin ? (uint32_t)(ie - ib) : 0u;
-            pcnt[u] = c;
-            if (c) {
+            ic = entries ? (uint32_t)(ie - ib) : 0u;
+            c = ic + (uint32_t)(o1 - o0);
+            if (c && du < cta_min) {          // warp owner: a warp table per 64 entries
+                w += (uint64_t)((c + kWarpTaskLists - 1) / kWarpTaskLists) * du;
+            } else if (c) {                   // CTA owner: bitmap (zeroed span) or hash table
                 const uint64_t span = (uint64_t)col[off[u + 1] - 1] - col[off[u]] + 1;
-                w += (uint64_t)((c + kCtaTaskLists - 1) / kCtaTaskLists) * (du + span / 32);
+                const bool bitmap = span + 32 <= kCtaBitmapBits;
+                w += (uint64_t)((c + kCtaTaskLists - 1) / kCtaTaskLists) * (du + (bitmap ? span / 32 : 0));
             }
-        } else {
-            pcnt[u] = 0;
-            in_cnt[u] = 0;
         }
+        in_cnt[u] = ic;
+        pcnt[u] = c;
         work[u] = w;
     }
 }
@@ -519,19 +525,26 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
     // compacting them in place, one CTA per core owner, measured +0.43 ms in binning for
     // -0.13 ms in a6 at s21)
     if (p.world > 1) {   // owner split: work per owner, its exclusive prefix, then this rank's owners
+        uint32_t *ecnt = ctx.alloc<uint32_t>(cap), *elen = ctx.alloc<uint32_t>(cap);
+        uint64_t *pre_cnt = ctx.alloc<uint64_t>(cap + 1), *pre_len = ctx.alloc<uint64_t>(cap + 1);
+        k_entry_vals<<<ctx.persistent_grid(8), 256, 0, ctx.stream>>>(g.off, g.in_src, ulo, g.m_dev,
+                                                                     ecnt, elen);
+        TC_LAUNCHED(ctx);
+        scan_exclusive_dc(ctx, ecnt, pre_cnt, cap, g.m_dev, pre_cnt + cap);
+        scan_exclusive_dc(ctx, elen, pre_len, cap, g.m_dev, pre_len + cap);
         uint64_t *work = ctx.alloc<uint64_t>(n), *wprefix = ctx.alloc<uint64_t>(n + 1);
         k_owner_work<<<ctx.persistent_grid(8), 256, 0, ctx.stream>>>(
-            g.dplus, g.col, g.off, g.in_off, g.in_src, ulo, g.m_dev, obits, wpre, toff, toff + tiles,
-            orange, n, in_cnt, bins.pcnt, ooff, work);
+            g.dplus, g.col, g.off, g.in_off, pre_cnt, pre_len, g.m_dev, obits, wpre, toff,
+            toff + tiles, orange, n, cta_min, in_cnt, bins.pcnt, ooff, work);
         TC_LAUNCHED(ctx);
         scan_exclusive(ctx, work, wprefix, n);
         k_owners<true><<<ctx.persistent_grid(4), 256, 0, ctx.stream>>>(
-            g.dplus, g.col, g.in_off, g.in_src, orange, wprefix, p.rank, p.world, ulo, in_cnt, ooff,
+            g.dplus, g.col, g.in_off, pre_cnt, pre_len, orange, wprefix, p.rank, p.world, ulo, in_cnt, ooff,
             g.off, g.m_dev, obits, wpre, toff, toff + tiles, n, cta_min, bins.pcnt, bins.owners_warp,
             bins.owners_cta, bins.owners_bitmap, bins.count);
     } else {
         k_owners<false><<<ctx.persistent_grid(4), 256, 0, ctx.stream>>>(
-            g.dplus, g.col, g.in_off, g.in_src, orange, nullptr, 0, 1, ulo, in_cnt, ooff, g.off,
+            g.dplus, g.col, g.in_off, nullptr, nullptr, orange, nullptr, 0, 1, ulo, in_cnt, ooff, g.off,
             g.m_dev, obits, wpre, toff, toff + tiles, n, cta_min, bins.pcnt, bins.owners_warp,
             bins.owners_cta, bins.owners_bitmap, bins.count);
     }

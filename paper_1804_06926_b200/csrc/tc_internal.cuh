@@ -454,6 +454,11 @@ __device__ __forceinline__ int core_edge(const HashParams &hp, uint32_t u, uint3
     return (uint64_t)(w1 - w0 + 1) <= (uint64_t)probe * TC_CORE_WORDS_PER_PROBE ? 1 : 0;
 }
 
+// Multi-GPU split of the per-edge bins (SHORT / MERGE / SEARCH / dense core): interleaved
+// blocks of 2048 CSR edges.
+__device__ __forceinline__ int edge_rank(uint64_t e, int world) {
+    return world <= 1 ? 0 : (int)((e >> 11) % (uint64_t)world);
+}
 // Multi-GPU split (world > 1): the rank of a unit whose exclusive work prefix is
 // `pre`, out of `total`: floor(pre / ceil(total / world)), clamped.  Deterministic on every
 // rank, no communication.
