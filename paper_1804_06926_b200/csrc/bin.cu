@@ -366,6 +366,12 @@ __global__ void k_entry_vals(const uint64_t *__restrict__ off, const uint32_t *_
 #ifndef TC_SHARD_ENTRY_COST
 #define TC_SHARD_ENTRY_COST 64   // fixed cost of a probe entry (descriptor, partial slots), in probes
 #endif
+#ifndef TC_SHARD_HASH_WEIGHT
+#define TC_SHARD_HASH_WEIGHT 3   // bucket-hash owner probes relative to bitmap probes
+#endif
+#ifndef TC_SHARD_WARP_WEIGHT
+#define TC_SHARD_WARP_WEIGHT 2   // warp-table owner probes relative to bitmap probes (measured: s21 w8 max/mean 1.50 -> 1.31)
+#endif
 __global__ void k_owner_work(const uint32_t *__restrict__ dplus, const uint32_t *__restrict__ col,
                              const uint64_t *__restrict__ off, const uint64_t *__restrict__ in_off,
                              const uint64_t *__restrict__ pre_cnt, const uint64_t *__restrict__ pre_len,
@@ -395,10 +401,11 @@ __global__ void k_owner_work(const uint32_t *__restrict__ dplus, const uint32_t 
             ic = entries ? (uint32_t)(ie - ib) : 0u;
             c = ic + (uint32_t)(o1 - o0);
             if (c && du < cta_min) {          // warp owner: a warp table per 64 entries
-                w += (uint64_t)((c + kWarpTaskLists - 1) / kWarpTaskLists) * du;
+                w = w * TC_SHARD_WARP_WEIGHT + (uint64_t)((c + kWarpTaskLists - 1) / kWarpTaskLists) * du;
             } else if (c) {                   // CTA owner: bitmap (zeroed span) or hash table
                 const uint64_t span = (uint64_t)col[off[u + 1] - 1] - col[off[u]] + 1;
                 const bool bitmap = span + 32 <= kCtaBitmapBits;
+                if (!bitmap) w *= TC_SHARD_HASH_WEIGHT;   // bucket-hash probes cost more
                 w += (uint64_t)((c + kCtaTaskLists - 1) / kCtaTaskLists) * (du + (bitmap ? span / 32 : 0));
             }
         }
