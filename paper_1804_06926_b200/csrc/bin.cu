@@ -61,7 +61,6 @@ __global__ void __launch_bounds__(kTileThreads, TC_EDGES_MINBLOCKS)
     k_edges(HashParams hp, const uint64_t *__restrict__ m_dev, uint32_t *__restrict__ ulo,
             uint32_t *__restrict__ obits, uint32_t *__restrict__ tcount,
             uint2 *__restrict__ b_short, uint2 *__restrict__ b_merge, uint2 *__restrict__ b_search,
-            uint4 *__restrict__ b_core,
             uint64_t *__restrict__ counts) {
     __shared__ uint32_t s_row[kTileItems];
     __shared__ uint32_t s_scan[kTileThreads / 32];
@@ -80,7 +79,7 @@ __global__ void __launch_bounds__(kTileThreads, TC_EDGES_MINBLOCKS)
     }
     uint32_t len = (uint32_t)min((uint64_t)kTileItems, m - t0);
     tile_rows(hp.off, hp.n, t0, len, s_row, s_scan);
-    uint64_t W = 0, probe = 0, skipped = 0, hashed = 0, outs = 0, cedges = 0, cwords = 0, cprobe = 0;
+    uint64_t W = 0, probe = 0, skipped = 0, hashed = 0, outs = 0, cedges = 0, cprobe = 0;
     // striped: each warp handles 32 consecutive edges per round (warp-aggregated
     // appends); the loads of kBatch rounds are issued before any is used
     constexpr int kRounds = kTileItems / kTileThreads, kBatch = TC_EDGES_BATCH;
@@ -108,18 +107,14 @@ __global__ void __launch_bounds__(kTileThreads, TC_EDGES_MINBLOCKS)
             int bin = -1;
             bool outp = false;
             uint2 item = make_uint2(0, 0);
-            uint32_t cw0 = 0, cw1 = 0;
             if (i < len) {
                 uint64_t e = t0 + i;
                 uint32_t u = us[j], x = xs[j], dv = dvs[j];
                 uint64_t ue = ues[j];
                 uint32_t du = (uint32_t)(ue - ubs[j]), suf = (uint32_t)(ue - e - 1);
                 bin = edge_bin(hp, du, dv, suf);
-                if (bin == TC_VARIANT_HASH && hp.core && u >= hp.core_lo) {
-                    // (suf > 0 here: the element after x in N+(u) is col+[e + 1])
-                    const int ce = core_edge(hp, u, x, hp.col[e + 1], min(suf, dv), cw0, cw1);
-                    bin = ce == 1 ? kBinCore : (ce == 2 ? -1 : bin);
-                }
+                // a HASH edge of a core source is counted by the dense-core path (core.cu)
+                if (bin == TC_VARIANT_HASH && hp.core && u >= hp.core_lo) bin = kBinCore;
                 // world > 1: HASH edges are binned on every rank (split later by owner, whose
                 // statistics k_owners counts); the other bins keep this rank's edge range
                 const bool mine = hp.world <= 1 || bin == TC_VARIANT_HASH || edge_rank(e, hp.world) == hp.rank;
@@ -130,7 +125,6 @@ __global__ void __launch_bounds__(kTileThreads, TC_EDGES_MINBLOCKS)
                     skipped += bin < 0;
                     if (bin == kBinCore) {
                         cedges++;
-                        cwords += cw1 - cw0 + 1;
                         cprobe += min(suf, dv);
                     }
                 }
@@ -161,9 +155,6 @@ __global__ void __launch_bounds__(kTileThreads, TC_EDGES_MINBLOCKS)
             }
             warp_append(bin == TC_VARIANT_MERGE, &counts[1], b_merge, item);
             warp_append(bin == TC_VARIANT_SEARCH, &counts[2], b_search, item);
-            if (hp.core)   // dense-core edges: (u, x, w0 | w1 << 16) for core.cu (warp-uniform test)
-                warp_append(bin == kBinCore, &counts[12], b_core,
-                            make_uint4(item.x, item.y, cw0 | (cw1 << 16), 0u));
         }
     }
     __syncthreads();
@@ -178,13 +169,11 @@ __global__ void __launch_bounds__(kTileThreads, TC_EDGES_MINBLOCKS)
     hashed = block_sum_u64(hashed, s_red);
     outs = block_sum_u64(outs, s_red);
     cedges = block_sum_u64(cedges, s_red);
-    cwords = block_sum_u64(cwords, s_red);
     cprobe = block_sum_u64(cprobe, s_red);
     if (threadIdx.x == 0) {
         tcount[blockIdx.x] = (uint32_t)outs;
         if (cedges) {
             atomicAdd((unsigned long long *)&counts[13], (unsigned long long)cedges);
-            atomicAdd((unsigned long long *)&counts[14], (unsigned long long)cwords);
             atomicAdd((unsigned long long *)&counts[15], (unsigned long long)cprobe);
         }
         atomicAdd((unsigned long long *)&counts[3], (unsigned long long)hashed);
@@ -491,9 +480,6 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
                           p.force == TC_VARIANT_MERGE,
                           p.force == TC_VARIANT_SEARCH || (p.force < 0 && p.skew_ratio > 0)};
     for (int k = 0; k < 3; k++) bins.edges[k] = ctx.alloc<uint2>(want[k] ? cap : 1);
-    // dense-core edges: only the core sources' rows can hold them
-    bins.core_edges = ctx.alloc<uint4>(hp.core ? std::min<uint64_t>(cap, (uint64_t)hp.core_words * 32 *
-                                                                     hp.core_words * 16) : 1);
 
     // HASH: in-part ranges (in-list order), out-part entries (compacted, CSR order),
     // statistics, owners, tasks
@@ -508,7 +494,6 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
     if (tiles) {
         k_edges<<<tiles, kTileThreads, 0, ctx.stream>>>(hp, g.m_dev, ulo, obits, tcount,
                                                         bins.edges[0], bins.edges[1], bins.edges[2],
-                                                        bins.core_edges,
                                                         bins.count);
         TC_LAUNCHED(ctx);
     }

@@ -71,34 +71,54 @@ __global__ void __launch_bounds__(kCoreBuildWarps * 32)
     }
 }
 
-// The core edges binned by k_edges (bin.cu) as (u, x, w0 | w1 << 16), in about CSR order
-// (consecutive edges share u: its row stays in L1).  Groups of 8 lanes share an edge: 32
-// words (8 x 16 bytes of each row) per step; persistent, grid-strided over the list.
+// One CTA per core source u (grid-strided; the longest rows, just above core_lo, come first,
+// so every CTA starts with one of them): B_u is staged in shared memory once, then groups of
+// 8 lanes take the edges (u, x) of its row that binning sent here -- the HASH-bin edges of a
+// core source (bin.cu) -- and AND B_u with B_x (from L2) over the words covering the common
+// range [max(next, first(x)), min(last(u), last(x))]; an empty range closes no triangle.
 constexpr int kCoreGroup = 8;
 __global__ void __launch_bounds__(256)
-    k_core_count(const uint32_t *__restrict__ core, uint32_t core_lo, uint32_t core_words,
-                 const uint4 *__restrict__ edges, const uint64_t *__restrict__ count,
-                 uint64_t *__restrict__ total) {
+    k_core_count(HashParams hp, const uint64_t *__restrict__ m_dev, uint64_t *__restrict__ total,
+                 uint64_t *__restrict__ words_out) {
+    __shared__ __align__(16) uint32_t s_bu[kCoreMaxWords];
     __shared__ uint64_t s_red[32];
-    const uint64_t ne = *count;
-    const uint32_t gl = threadIdx.x % kCoreGroup;
-    const uint64_t g0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / kCoreGroup;
-    const uint64_t ng = ((uint64_t)gridDim.x * blockDim.x) / kCoreGroup;
-    uint64_t acc = 0;
-    for (uint64_t i = g0; i < ne; i += ng) {
-        const uint4 it = edges[i];
-        const uint32_t w0 = it.z & 0xffffu, w1 = it.z >> 16;
-        const uint4 *bu = reinterpret_cast<const uint4 *>(core + (uint64_t)(it.x - core_lo) * core_words);
-        const uint4 *bx = reinterpret_cast<const uint4 *>(core + (uint64_t)(it.y - core_lo) * core_words);
-        // 16-byte groups from w0 & ~3: row x is written from its 16-byte group holding x's
-        // own word on (k_core_build), and its words below w0 cover ids <= x, so they are 0
-        for (uint32_t q = (w0 >> 2) + gl; q <= (w1 >> 2); q += kCoreGroup) {
-            const uint4 a = __ldg(bu + q), b = __ldg(bx + q);
-            acc += __popc(a.x & b.x) + __popc(a.y & b.y) + __popc(a.z & b.z) + __popc(a.w & b.w);
+    const uint64_t m = *m_dev;
+    const uint32_t gl = threadIdx.x % kCoreGroup, grp = threadIdx.x / kCoreGroup;
+    constexpr uint32_t kGroups = 256 / kCoreGroup;
+    uint64_t acc = 0, words = 0;
+    for (uint32_t u = hp.core_lo + blockIdx.x; u < hp.n; u += gridDim.x) {
+        const uint64_t ub = hp.off[u], ue = hp.off[u + 1];
+        if (ue - ub < 2) continue;   // block-uniform: a single edge has no suffix
+        __syncthreads();             // the previous row's B_u is no longer read
+        const uint4 *src = reinterpret_cast<const uint4 *>(hp.core + (uint64_t)(u - hp.core_lo) * hp.core_words);
+        uint4 *dst = reinterpret_cast<uint4 *>(s_bu);
+        for (uint32_t q = ((u - hp.core_lo) >> 7) + threadIdx.x; q < (hp.core_words >> 2); q += 256)
+            dst[q] = __ldg(src + q);
+        __syncthreads();
+        const uint32_t du = (uint32_t)(ue - ub), last_u = hp.core_range[u - hp.core_lo].y;
+        for (uint64_t e = ub + grp; e + 1 < ue; e += kGroups) {
+            if (hp.world > 1 && edge_rank(e, hp.world) != hp.rank) continue;
+            const uint32_t x = hp.col[e], dv = hp.dplus[x], suf = (uint32_t)(ue - e - 1);
+            if (edge_bin(hp, du, dv, suf) != TC_VARIANT_HASH) continue;
+            const uint2 rx = hp.core_range[x - hp.core_lo];
+            const uint32_t lo = max(hp.col[e + 1], rx.x), hi = min(last_u, rx.y);
+            if (hi < lo) continue;
+            const uint32_t w0 = (lo - hp.core_lo) >> 5, w1 = (hi - hp.core_lo) >> 5;
+            if (gl == 0) words += w1 - w0 + 1;
+            // 16-byte groups from w0 & ~3: row x is written from its 16-byte group holding x's
+            // own word on (k_core_build), and its words below w0 cover ids <= x, so they are 0
+            const uint4 *bx = reinterpret_cast<const uint4 *>(hp.core + (uint64_t)(x - hp.core_lo) * hp.core_words);
+            for (uint32_t q = (w0 >> 2) + gl; q <= (w1 >> 2); q += kCoreGroup) {
+                const uint4 a = dst[q], b = __ldg(bx + q);
+                acc += __popc(a.x & b.x) + __popc(a.y & b.y) + __popc(a.z & b.z) + __popc(a.w & b.w);
+            }
         }
     }
     const uint64_t t = block_sum_u64(acc, s_red);
+    const uint64_t wsum = block_sum_u64(words, s_red);
     if (threadIdx.x == 0 && t) atomicAdd((unsigned long long *)total, (unsigned long long)t);
+    if (threadIdx.x == 0 && wsum) atomicAdd((unsigned long long *)words_out, (unsigned long long)wsum);
+    (void)m;
 }
 
 void core_build(Ctx &ctx, const Oriented &g, HashParams &hp) {
@@ -121,11 +141,12 @@ void core_build(Ctx &ctx, const Oriented &g, HashParams &hp) {
     hp.core_range = range;
 }
 
-void core_count(Ctx &ctx, const HashParams &hp, const uint4 *edges, const uint64_t *count,
-                uint64_t *total_dev, cudaStream_t stream) {
+void core_count(Ctx &ctx, const Oriented &g, const HashParams &hp, uint64_t *total_dev,
+                uint64_t *words_dev, cudaStream_t stream) {
     if (!hp.core) return;
-    k_core_count<<<ctx.persistent_grid(8), 256, 0, stream>>>(hp.core, hp.core_lo, hp.core_words,
-                                                              edges, count, total_dev);
+    const uint32_t rows = (uint32_t)g.n - hp.core_lo;
+    const uint32_t grid = std::min<uint32_t>(rows, (uint32_t)ctx.persistent_grid(8));
+    k_core_count<<<grid, 256, 0, stream>>>(hp, g.m_dev, total_dev, words_dev);
     TC_LAUNCHED(ctx);
 }
 

@@ -930,8 +930,8 @@ static void launch_all(Ctx &ctx, const Oriented &g, const Bins &bins, uint64_t *
     TC_LAUNCHED(ctx);
     k_short<CM><<<grid, kIxThreads, 0, s2>>>(bins.edges[0], bins.count + 0, g.off, g.col, total, cr);
     TC_LAUNCHED(ctx);
-    if (CM == kCmNone)   // dense-core edges (core.cu)
-        core_count(ctx, bins.hp, bins.core_edges, bins.count + 12, total, s2);
+    if (CM == kCmNone)   // dense-core edges (core.cu); their word count -> stats
+        core_count(ctx, g, bins.hp, total, bins.count + 14, s2);
     side.join();
 }
 

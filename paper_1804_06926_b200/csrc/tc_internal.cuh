@@ -434,25 +434,6 @@ struct HashParams {
 
 constexpr int kBinCore = 4;   // internal bin of k_edges: dense-core edge (core.cu)
 
-// Dense-core decision (core.cu header) for an edge (u, x) whose source u is in the core (so
-// x and every common element are too): the common elements of N+(u) after x and N+(x) lie
-// in [max(next, first(x)), min(last(u), last(x))] (next = the element after x in N+(u));
-// words [w0, w1] of the core bitmaps cover it.  An empty range means no triangle (the edge
-// is skipped); otherwise the edge goes to the core path when its word count is at most
-// TC_CORE_WORDS_PER_PROBE times its HASH probe count.  Returns 0 (not core), 1 (core) or
-// 2 (empty range: no triangle).
-#ifndef TC_CORE_WORDS_PER_PROBE
-#define TC_CORE_WORDS_PER_PROBE 1
-#endif
-__device__ __forceinline__ int core_edge(const HashParams &hp, uint32_t u, uint32_t x, uint32_t next,
-                                         uint32_t probe, uint32_t &w0, uint32_t &w1) {
-    const uint2 ru = hp.core_range[u - hp.core_lo], rx = hp.core_range[x - hp.core_lo];
-    const uint32_t lo = max(next, rx.x), hi = min(ru.y, rx.y);
-    if (hi < lo) return 2;
-    w0 = (lo - hp.core_lo) >> 5;
-    w1 = (hi - hp.core_lo) >> 5;
-    return (uint64_t)(w1 - w0 + 1) <= (uint64_t)probe * TC_CORE_WORDS_PER_PROBE ? 1 : 0;
-}
 
 // Multi-GPU split of the per-edge bins (SHORT / MERGE / SEARCH / dense core): interleaved
 // blocks of 2048 CSR edges.
@@ -484,7 +465,6 @@ __device__ __forceinline__ int edge_bin(const HashParams &hp, uint32_t du, uint3
 // followed, if it owns out-part edges, by its own row.
 struct Bins {
     uint2 *edges[3] = {nullptr, nullptr, nullptr};  // SHORT, MERGE, SEARCH: (u, v) pairs
-    uint4 *core_edges = nullptr;  // dense-core edges (u, x, w0 | w1 << 16); count at count[12]
     uint64_t *count = nullptr;  // device: [0..3] SHORT/MERGE/SEARCH/HASH edges, [4] W,
                                 // [5] sum min(|N+(u) after v|, d+(v)), [6] skipped, [7] max d+,
                                 // [8] warp owners, [9] CTA hash owners, [10] CTA bitmap owners,
@@ -528,8 +508,8 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins);
 // hp.core / core_lo / core_words (count mode only; a no-op when the graph is empty).
 void core_build(Ctx &ctx, const Oriented &g, HashParams &hp);
 // a6 + a7 for the core edges (plain count): popc of bitmap ANDs, added into total_dev.
-void core_count(Ctx &ctx, const HashParams &hp, const uint4 *edges, const uint64_t *count,
-                uint64_t *total_dev, cudaStream_t stream);
+void core_count(Ctx &ctx, const Oriented &g, const HashParams &hp, uint64_t *total_dev,
+                uint64_t *words_dev, cudaStream_t stream);
 
 // What each triangle found in a6 credits besides the total (intersect.cu header).
 enum CreditMode { kCmNone = 0, kCmVertex = 1, kCmEdge = 2, kCmList = 3, kCmTop = 4 };
