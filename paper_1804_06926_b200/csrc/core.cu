@@ -76,7 +76,10 @@ __global__ void __launch_bounds__(kCoreBuildWarps * 32)
 // 8 lanes take the edges (u, x) of its row that binning sent here -- the HASH-bin edges of a
 // core source (bin.cu) -- and AND B_u with B_x (from L2) over the words covering the common
 // range [max(next, first(x)), min(last(u), last(x))]; an empty range closes no triangle.
-constexpr int kCoreGroup = 8;
+#ifndef TC_CORE_GROUP
+#define TC_CORE_GROUP 4   // measured s21 ix: 2 2.35, 4 2.29, 8 2.41, 16 2.68 ms
+#endif
+constexpr int kCoreGroup = TC_CORE_GROUP;   // lanes per core edge
 __global__ void __launch_bounds__(256)
     k_core_count(HashParams hp, const uint64_t *__restrict__ m_dev, uint64_t *__restrict__ total,
                  uint64_t *__restrict__ words_out) {
