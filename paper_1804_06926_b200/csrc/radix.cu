@@ -14,8 +14,11 @@
 
 namespace tc {
 
+// Tile geometry, re-swept after the 4-op ballot form (s21 / road / s24 total ms): 512x8, 2 CTAs/SM
+// 6.96 / 3.52 / 78.98; 384x8, 3/SM 6.85 / 3.53 / 78.44; 256x16, 4/SM 6.93 / 3.48 / 77.87;
+// 512x6, 3/SM 7.02 / 3.59 / 80.18.
 #ifndef TC_RS_THREADS
-#define TC_RS_THREADS 512
+#define TC_RS_THREADS 384
 #endif
 #ifndef TC_RS_ROUNDS
 #define TC_RS_ROUNDS 8
@@ -24,7 +27,7 @@ namespace tc {
 #define TC_RS_LB 8   // look-back batch: predecessor status words loaded together
 #endif
 #ifndef TC_RS_MINBLOCKS
-#define TC_RS_MINBLOCKS 2
+#define TC_RS_MINBLOCKS 3
 #endif
 constexpr int kRsThreads = TC_RS_THREADS;
 constexpr int kRsWarps = kRsThreads / 32;
