@@ -420,12 +420,16 @@ __global__ void __launch_bounds__(kTileThreads)
         const uint32_t len = (uint32_t)min((uint64_t)kTileItems, M - t0);
         tile_rows(rowptr, n, t0, len, s_row, s_scan);
         const uint32_t i0 = threadIdx.x * kItemsPerThread;
-        uint32_t f[kItemsPerThread], v[kItemsPerThread], c = 0;
+        // rank(u) < rank(v) <=> newid[u] < newid[v] (the rank sort's order), so one gather per
+        // arc serves both the filter and the output ids; deg[u] = 0 marks a pruned vertex
+        uint32_t f[kItemsPerThread], nu[kItemsPerThread], nv[kItemsPerThread], c = 0;
 #pragma unroll
         for (int k = 0; k < kItemsPerThread; k++) {
             const uint32_t i = i0 + k;
-            v[k] = i < len ? col[t0 + i] : 0u;
-            f[k] = i < len ? (uint32_t)rank_less(deg, s_row[i], v[k]) : 0u;
+            const uint32_t u = i < len ? s_row[i] : 0u;
+            nv[k] = i < len ? newid[col[t0 + i]] : 0u;
+            nu[k] = newid[u];
+            f[k] = i < len && deg[u] != 0 && nu[k] < nv[k];
             c += f[k];
         }
         uint32_t total;
@@ -437,7 +441,7 @@ __global__ void __launch_bounds__(kTileThreads)
 #pragma unroll
         for (int k = 0; k < kItemsPerThread; k++) {
             if (f[k] && base < cap) {
-                const uint32_t sv = newid[s_row[i0 + k]], tv = newid[v[k]];
+                const uint32_t sv = nu[k], tv = nv[k];
                 okey[base] = sv;
                 oval[base] = tv;
                 s_hk.add(sv, passes, db);

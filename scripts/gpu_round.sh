@@ -15,6 +15,8 @@ if [ "$2" = "ncu" ]; then
       -o gpurun_out/ix_full -f python bench.py --one-call > gpurun_out/ncu_ix.log 2>&1
   ncu --set full --import-source on --clock-control none -k regex:k_rs_pass -s 2 -c 1 \
       -o gpurun_out/rs_full -f python bench.py --one-call > gpurun_out/ncu_rs.log 2>&1
+  ncu --set full --import-source on --clock-control none -k regex:"k_core_count|k_edges|k_hash_warp" -c 3 \
+      -o gpurun_out/misc_full -f python bench.py --one-call > gpurun_out/ncu_misc.log 2>&1
   ncu --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file gpurun_out/launches.csv python bench.py --one-call > gpurun_out/ncu_launch.log 2>&1
   ls -la gpurun_out
