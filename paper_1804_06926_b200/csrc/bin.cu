@@ -423,30 +423,42 @@ __global__ void k_task_count(const uint32_t *__restrict__ owners, const uint64_t
     if ((threadIdx.x & 31) == 0 && loads) atomicAdd((unsigned long long *)tloads, (unsigned long long)loads);
 }
 
+// Task records: task k of owner x = {x, first entry k*L, d+(x), in_cnt(x)} and {off+[x],
+// in_off[x], ooff[x], out-part entries of x} (all offsets < 2^32: m < 2^32), so a6 reads
+// its task header with two 16-byte loads instead of a task -> owner -> offsets chain.
 __global__ void k_task_expand(const uint32_t *__restrict__ owners, const uint64_t *__restrict__ ocount,
                               const uint32_t *__restrict__ tcnt, const uint64_t *__restrict__ toff,
-                              uint2 *__restrict__ tasks) {
+                              uint32_t L, const uint64_t *__restrict__ off,
+                              const uint64_t *__restrict__ in_off, const uint32_t *__restrict__ in_cnt,
+                              const uint64_t *__restrict__ ooff, uint4 *__restrict__ tasks) {
     uint64_t no = *ocount;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < no;
          i += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t x = owners[i], c = tcnt[i];
-        uint64_t o = toff[i];
-        for (uint32_t k = 0; k < c; k++) tasks[o + k] = make_uint2(x, k);
+        const uint32_t x = owners[i], c = tcnt[i];
+        const uint64_t o = toff[i], xb = off[x], ob = ooff[x];
+        const uint4 r1 = make_uint4((uint32_t)xb, (uint32_t)in_off[x], (uint32_t)ob,
+                                    (uint32_t)(ooff[x + 1] - ob));
+        const uint32_t dx = (uint32_t)(off[x + 1] - xb), ic = in_cnt[x];
+        for (uint32_t k = 0; k < c; k++) {
+            tasks[2 * (o + k)] = make_uint4(x, k * L, dx, ic);
+            tasks[2 * (o + k) + 1] = r1;
+        }
     }
 }
 
 static void make_tasks(Ctx &ctx, uint64_t n, uint64_t cap, const uint32_t *owners,
-                       const uint64_t *ocount, const uint32_t *pcnt, const uint32_t *dplus,
-                       uint32_t L, uint64_t *tloads, uint2 *&tasks, uint64_t *&ntasks) {
+                       const uint64_t *ocount, const uint32_t *pcnt, const HashParams &hp,
+                       uint32_t L, uint64_t *tloads, uint4 *&tasks, uint64_t *&ntasks) {
     uint32_t *tcnt = ctx.alloc<uint32_t>(n);
     uint64_t *toff = ctx.alloc<uint64_t>(n + 1);
     int grid = ctx.persistent_grid(4);
-    k_task_count<<<grid, 256, 0, ctx.stream>>>(owners, ocount, pcnt, dplus, n, L, tcnt, tloads);
+    k_task_count<<<grid, 256, 0, ctx.stream>>>(owners, ocount, pcnt, hp.dplus, n, L, tcnt, tloads);
     TC_LAUNCHED(ctx);
     // the owner list is usually far shorter than n (road mesh: empty): scan only its length
     scan_exclusive_dc(ctx, tcnt, toff, n, ocount, toff + n);
-    tasks = ctx.alloc<uint2>((2 * cap) / L + n + 1);
-    k_task_expand<<<grid, 256, 0, ctx.stream>>>(owners, ocount, tcnt, toff, tasks);
+    tasks = ctx.alloc<uint4>(2 * ((2 * cap) / L + n + 1));
+    k_task_expand<<<grid, 256, 0, ctx.stream>>>(owners, ocount, tcnt, toff, L, hp.off, hp.in_off,
+                                                hp.in_cnt, hp.ooff, tasks);
     TC_LAUNCHED(ctx);
     ntasks = toff + n;
 }
@@ -541,11 +553,11 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
             bins.owners_cta, bins.owners_bitmap, bins.count);
     }
     TC_LAUNCHED(ctx);
-    make_tasks(ctx, n, cap, bins.owners_warp, bins.count + 8, bins.pcnt, g.dplus, kWarpTaskLists,
+    make_tasks(ctx, n, cap, bins.owners_warp, bins.count + 8, bins.pcnt, hp, kWarpTaskLists,
                bins.count + 11, bins.tasks_warp, bins.ntasks_warp);
-    make_tasks(ctx, n, cap, bins.owners_cta, bins.count + 9, bins.pcnt, g.dplus, kCtaTaskLists,
+    make_tasks(ctx, n, cap, bins.owners_cta, bins.count + 9, bins.pcnt, hp, kCtaTaskLists,
                bins.count + 11, bins.tasks_cta, bins.ntasks_cta);
-    make_tasks(ctx, n, cap, bins.owners_bitmap, bins.count + 10, bins.pcnt, g.dplus, kBitmapTaskLists,
+    make_tasks(ctx, n, cap, bins.owners_bitmap, bins.count + 10, bins.pcnt, hp, kBitmapTaskLists,
                bins.count + 11, bins.tasks_bitmap, bins.ntasks_bitmap);
 }
 

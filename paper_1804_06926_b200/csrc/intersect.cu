@@ -293,7 +293,11 @@ constexpr uint32_t kHashChunk = 1024;  // owner elements per table build (load f
 #ifndef TC_HASH_PREFETCH
 #define TC_HASH_PREFETCH 0
 #endif
+#ifndef TC_HASH_RR
+#define TC_HASH_RR 1
+#endif
 constexpr int kUnroll = TC_HASH_UNROLL;  // independent 32-slot windows per probe step
+constexpr uint32_t kCtaStride = TC_HASH_RR ? 32u * (kIxThreads / 32) : 32u;   // window stride of a CTA task's warps
 constexpr int kHashWarps = kIxThreads / 32;
 
 // Explicit shared-memory accesses on 32-bit shared addresses (keeps the hot
@@ -541,7 +545,8 @@ __device__ __forceinline__ uint64_t probe_quads(const Probe &contains,
                                                 uint32_t ie,
                                                 const uint32_t *__restrict__ col,
                                                 uint32_t owner, const Credit &cr,
-                                                uint2 *stage = nullptr) {
+                                                uint2 *stage = nullptr,
+                                                uint32_t stride = 32 * kUnroll) {
     uint32_t staged = 0, ord_owner = 0;
     if (CM == kCmList) ord_owner = cr.order[owner];
     const int lane = threadIdx.x & 31;
@@ -555,7 +560,15 @@ __device__ __forceinline__ uint64_t probe_quads(const Probe &contains,
     uint32_t i0 = lo;
     const uint32_t le_mask = (2u << lane) - 1u;
     const uint4 *col4 = reinterpret_cast<const uint4 *>(col);
-    for (uint32_t wb = ib; wb < ie; wb += 32 * kUnroll) {
+    for (uint32_t wb = ib; wb < ie; wb += stride) {
+        if (stride > 32 * kUnroll && wb != ib) {   // strided windows: the list holding quad wb,
+            uint32_t lo2 = i0, hi2 = nl;          // searched from the previous window's last
+            while (hi2 - lo2 > 1) {
+                const uint32_t mid = (lo2 + hi2) >> 1;
+                if (d.pre[mid] <= wb) lo2 = mid; else hi2 = mid;
+            }
+            i0 = lo2;
+        }
         uint4 q[kUnroll][kSlot / 4];
         uint2 r[kUnroll];
         uint32_t e0[kUnroll], ly[kUnroll];
@@ -681,7 +694,7 @@ __device__ __forceinline__ void hash_desc(const HashParams &hp, uint64_t inb, ui
 // Warp tasks: owners with d+(x) <= kWarpTableSlots/4 (table in the warp's smem slice).
 template <int CM>
 __global__ void __launch_bounds__(kIxThreads, TC_HASH_WARP_MINBLOCKS)
-    k_hash_warp(const uint2 *__restrict__ tasks, const uint64_t *__restrict__ ntasks, HashParams hp,
+    k_hash_warp(const uint4 *__restrict__ tasks, const uint64_t *__restrict__ ntasks, HashParams hp,
                 uint64_t *__restrict__ total, Credit cr) {
     constexpr uint32_t L = kWarpTaskLists;
     constexpr bool PV = CM != kCmNone;                        // descriptors carry vid
@@ -700,14 +713,9 @@ __global__ void __launch_bounds__(kIxThreads, TC_HASH_WARP_MINBLOCKS)
     const uint32_t *col = hp.col;
     uint64_t acc = 0;
     for (uint64_t i = gw; i < nt; i += nw) {
-        uint2 task = tasks[i];
-        uint32_t x = task.x;
-        uint64_t xb = hp.off[x];
-        uint32_t dx = (uint32_t)(hp.off[x + 1] - xb);
-        uint64_t inb = hp.in_off[x], ob = hp.ooff[x];
-        uint32_t indeg = hp.in_cnt[x];
-        uint32_t ocnt = (uint32_t)(hp.ooff[x + 1] - ob);
-        uint32_t j0 = task.y * L;
+        const uint4 t0 = tasks[2 * i], t1 = tasks[2 * i + 1];   // bin.cu k_task_expand
+        const uint32_t x = t0.x, j0 = t0.y, dx = t0.z, indeg = t0.w, ocnt = t1.w;
+        const uint64_t xb = t1.x, inb = t1.y, ob = t1.z;
         // descriptors of entries j0 + lane, j0 + 32 + lane; non-empty ones compacted in
         // order (the list-start bitmap of probe_quads needs distinct starts)
         uint32_t run = 0, nl = 0;
@@ -762,7 +770,7 @@ constexpr uint32_t kPvCounters = 4096;                 // per-vertex: smem hit c
 static_assert(kCtaBitmapBits == kSmemWords * 32, "bitmap owners are classified in bin.cu");
 template <int CM, bool kBitmap>
 __global__ void __launch_bounds__(kIxThreads, CM != kCmNone ? 4 : TC_HASH_CTA_MINBLOCKS)
-    k_hash_cta(const uint2 *__restrict__ tasks, const uint64_t *__restrict__ ntasks, HashParams hp,
+    k_hash_cta(const uint4 *__restrict__ tasks, const uint64_t *__restrict__ ntasks, HashParams hp,
                uint64_t *__restrict__ total, Credit cr) {
     constexpr uint32_t L = kCtaTaskLists;
     constexpr bool PV = CM != kCmNone;   // descriptors carry vid
@@ -787,13 +795,9 @@ __global__ void __launch_bounds__(kIxThreads, CM != kCmNone ? 4 : TC_HASH_CTA_MI
     uint64_t nt = *ntasks;
     uint64_t acc = 0;
     for (uint64_t i = blockIdx.x; i < nt; i += gridDim.x) {
-        uint2 task = tasks[i];
-        uint32_t x = task.x;
-        uint64_t xb = hp.off[x];
-        uint32_t dx = (uint32_t)(hp.off[x + 1] - xb);
-        uint64_t inb = hp.in_off[x], ob = hp.ooff[x];
-        uint32_t indeg = hp.in_cnt[x];
-        uint32_t ocnt = (uint32_t)(hp.ooff[x + 1] - ob);
+        const uint4 t0 = tasks[2 * i], t1 = tasks[2 * i + 1];   // bin.cu k_task_expand
+        const uint32_t x = t0.x, j_task = t0.y, dx = t0.z, indeg = t0.w, ocnt = t1.w;
+        const uint64_t xb = t1.x, inb = t1.y, ob = t1.z;
         uint64_t h = 0;
         // descriptors of the probe entries j0 + threadIdx.x (one per thread), compacted, and
         // this warp's equal share [ib, ie) of their quads
@@ -809,8 +813,15 @@ __global__ void __launch_bounds__(kIxThreads, CM != kCmNone ? 4 : TC_HASH_CTA_MI
             nl = (uint32_t)(tot >> 32);
             if (nq) put_desc(d, (uint32_t)(pre >> 32), lo, hi, (uint32_t)pre, y, PV);
             if (threadIdx.x == 0) d.pre[nl] = items;
+#if TC_HASH_RR
+            // windows of 32 slots dealt round-robin to the warps (full windows even for small
+            // tasks; contiguous per-warp shares left most lanes of a small task's windows idle)
+            ib = 32u * wib;
+            ie = items;
+#else
             ib = (uint32_t)(((uint64_t)items * wib) / kHashWarps);
             ie = (uint32_t)(((uint64_t)items * (wib + 1)) / kHashWarps);
+#endif
             __syncthreads();   // every descriptor is written before any warp probes
         };
         if (kBitmap) {
@@ -853,10 +864,10 @@ __global__ void __launch_bounds__(kIxThreads, CM != kCmNone ? 4 : TC_HASH_CTA_MI
             // one bitmap serves up to kBitmapBatches batches of kCtaTaskLists probe entries
             const uint32_t npe = indeg + ocnt;
             for (uint32_t bt = 0; bt < kBitmapBatches; bt++) {
-                const uint32_t j0 = (task.y * kBitmapBatches + bt) * L;
+                const uint32_t j0 = j_task + bt * L;
                 if (j0 >= npe) break;   // block-uniform
                 batch(j0);
-                h += probe_quads<CM>(bp, d, nl, ib, ie, col, x, cr, stage);
+                h += probe_quads<CM>(bp, d, nl, ib, ie, col, x, cr, stage, kCtaStride);
                 __syncthreads();   // descriptors are rewritten by the next batch
             }
             if (use_cnt) {   // the k-th set bit is the k-th element of the sorted N+(x)
@@ -869,7 +880,7 @@ __global__ void __launch_bounds__(kIxThreads, CM != kCmNone ? 4 : TC_HASH_CTA_MI
                 __syncthreads();
             }
         } else {
-            batch(task.y * L);
+            batch(j_task);
             for (uint32_t c0 = 0; c0 < dx; c0 += kHashChunk) {
                 uint32_t clen = min(kHashChunk, dx - c0);
                 int bits = table_bits(clen);
@@ -882,7 +893,7 @@ __global__ void __launch_bounds__(kIxThreads, CM != kCmNone ? 4 : TC_HASH_CTA_MI
                 __syncthreads();
                 HashProbe hpb{tab, x, bits};
                 if (kCnt) hpb.cnt = s_cnt;
-                h += probe_quads<CM>(hpb, d, nl, ib, ie, col, x, cr, stage);
+                h += probe_quads<CM>(hpb, d, nl, ib, ie, col, x, cr, stage, kCtaStride);
                 __syncthreads();
                 if (kCnt) {
                     for (uint32_t s = threadIdx.x; s < (1u << bits); s += blockDim.x) {

@@ -475,7 +475,7 @@ struct Bins {
     uint32_t *owners_bitmap = nullptr; // hubs whose rank span (x, n) fits a smem bitmap
     // Tasks = (owner, k): the k-th block of kWarpTaskLists / kCtaTaskLists probe
     // entries of an owner, so no warp / CTA is stuck with a hub's whole group.
-    uint2 *tasks_warp = nullptr, *tasks_cta = nullptr, *tasks_bitmap = nullptr;
+    uint4 *tasks_warp = nullptr, *tasks_cta = nullptr, *tasks_bitmap = nullptr;   // 2 per task
     uint64_t *ntasks_warp = nullptr, *ntasks_cta = nullptr, *ntasks_bitmap = nullptr;  // device
     HashParams hp;
     uint64_t cap = 0;
