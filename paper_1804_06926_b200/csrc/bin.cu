@@ -491,7 +491,10 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
     const bool want[3] = {p.force == TC_VARIANT_SHORT || (p.force < 0 && p.short_max > 0),
                           p.force == TC_VARIANT_MERGE,
                           p.force == TC_VARIANT_SEARCH || (p.force < 0 && p.skew_ratio > 0)};
-    for (int k = 0; k < 3; k++) bins.edges[k] = ctx.alloc<uint2>(want[k] ? cap : 1);
+    for (int k = 0; k < 3; k++) {
+        bins.edges[k] = ctx.alloc<uint2>(want[k] ? cap : 1);
+        bins.has[k] = want[k];
+    }
 
     // HASH: in-part ranges (in-list order), out-part entries (compacted, CSR order),
     // statistics, owners, tasks

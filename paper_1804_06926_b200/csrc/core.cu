@@ -20,8 +20,8 @@
 // vertices, at most n rounded up to 128), row r = vertex core_lo + r, words [0, core_words)
 // each (K^2 / 8 bytes: 32 MB at K = 16384, L2-resident); only the words a row can ever be
 // read at -- from the 16-byte group holding its own vertex's word on -- are written (about
-// half).  core_range[r] = (first, last) element of N+(core_lo + r) bounds the word range of
-// every core edge (core_edge, tc_internal.cuh).  The paper has no such path (its kernels merge or
+// half).  core_info[r] = (first, last element, d+) of N+(core_lo + r) bounds the word range
+// of every core edge.  The paper has no such path (its kernels merge or
 // binary-search); this is the B200-first replacement of its "TwoLarge"
 // kernel for the densest lists.
 #include "tc_internal.cuh"
@@ -48,7 +48,7 @@ constexpr int kCoreBuildWarps = 8;
 __global__ void __launch_bounds__(kCoreBuildWarps * 32)
     k_core_build(const uint64_t *__restrict__ off, const uint32_t *__restrict__ col, uint32_t n,
                  uint32_t core_lo, uint32_t words, uint32_t *__restrict__ bm,
-                 uint2 *__restrict__ range) {
+                 uint4 *__restrict__ info) {
     __shared__ __align__(16) uint32_t s_row[kCoreBuildWarps][kCoreMaxWords];
     const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     uint32_t *row = s_row[wib];
@@ -58,7 +58,9 @@ __global__ void __launch_bounds__(kCoreBuildWarps * 32)
         for (uint32_t k = w_first + lane; k < words; k += 32) row[k] = 0u;
         __syncwarp();
         const uint64_t b = off[y], e = off[y + 1];
-        if (lane == 0) range[y - core_lo] = e > b ? make_uint2(col[b], col[e - 1]) : make_uint2(~0u, 0u);
+        if (lane == 0)
+            info[y - core_lo] = e > b ? make_uint4(col[b], col[e - 1], (uint32_t)(e - b), 0u)
+                                      : make_uint4(~0u, 0u, 0u, 0u);
         for (uint64_t k = b + lane; k < e; k += 32) {
             const uint32_t o = col[k] - core_lo;
             atomicOr(&row[o >> 5], 1u << (o & 31));
@@ -98,13 +100,19 @@ __global__ void __launch_bounds__(256)
         for (uint32_t q = ((u - hp.core_lo) >> 7) + threadIdx.x; q < (hp.core_words >> 2); q += 256)
             dst[q] = __ldg(src + q);
         __syncthreads();
-        const uint32_t du = (uint32_t)(ue - ub), last_u = hp.core_range[u - hp.core_lo].y;
-        for (uint64_t e = ub + grp; e + 1 < ue; e += kGroups) {
+        const uint32_t du = (uint32_t)(ue - ub), last_u = hp.core_info[u - hp.core_lo].y;
+        // the next edge's target is loaded one iteration ahead (the chain per edge is then
+        // core_info[x] -> B_x words)
+        uint64_t e = ub + grp;
+        uint32_t x_next = e + 1 < ue ? hp.col[e] : 0u;
+        for (; e + 1 < ue; e += kGroups) {
+            const uint32_t x = x_next, nxt = hp.col[e + 1];
+            x_next = e + kGroups + 1 < ue ? hp.col[e + kGroups] : 0u;
             if (hp.world > 1 && edge_rank(e, hp.world) != hp.rank) continue;
-            const uint32_t x = hp.col[e], dv = hp.dplus[x], suf = (uint32_t)(ue - e - 1);
-            if (edge_bin(hp, du, dv, suf) != TC_VARIANT_HASH) continue;
-            const uint2 rx = hp.core_range[x - hp.core_lo];
-            const uint32_t lo = max(hp.col[e + 1], rx.x), hi = min(last_u, rx.y);
+            const uint4 rx = hp.core_info[x - hp.core_lo];   // first, last, d+ of x
+            const uint32_t suf = (uint32_t)(ue - e - 1);
+            if (edge_bin(hp, du, rx.z, suf) != TC_VARIANT_HASH) continue;
+            const uint32_t lo = max(nxt, rx.x), hi = min(last_u, rx.y);
             if (hi < lo) continue;
             const uint32_t w0 = (lo - hp.core_lo) >> 5, w1 = (hi - hp.core_lo) >> 5;
             if (gl == 0) words += w1 - w0 + 1;
@@ -133,15 +141,15 @@ void core_build(Ctx &ctx, const Oriented &g, HashParams &hp) {
     hp.core_lo = n > K ? n - K : 0u;
     hp.core_words = K / 32;
     uint32_t *bm = ctx.alloc<uint32_t>((uint64_t)K * hp.core_words);
-    uint2 *range = ctx.alloc<uint2>(K);
+    uint4 *info = ctx.alloc<uint4>(K);
     const uint32_t rows = n - hp.core_lo;
     const uint32_t grid = std::min<uint32_t>((rows + kCoreBuildWarps - 1) / kCoreBuildWarps,
                                              (uint32_t)ctx.persistent_grid(4));
     k_core_build<<<grid, kCoreBuildWarps * 32, 0, ctx.stream>>>(g.off, g.col, n, hp.core_lo,
-                                                                 hp.core_words, bm, range);
+                                                                 hp.core_words, bm, info);
     TC_LAUNCHED(ctx);
     hp.core = bm;
-    hp.core_range = range;
+    hp.core_info = info;
 }
 
 void core_count(Ctx &ctx, const Oriented &g, const HashParams &hp, uint64_t *total_dev,

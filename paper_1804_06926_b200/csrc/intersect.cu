@@ -935,12 +935,19 @@ static void launch_all(Ctx &ctx, const Oriented &g, const Bins &bins, uint64_t *
     TC_LAUNCHED(ctx);
     k_hash_warp<CM><<<grid, kIxThreads, 0, s2>>>(bins.tasks_warp, bins.ntasks_warp, bins.hp, total, cr);
     TC_LAUNCHED(ctx);
-    k_merge<CM><<<grid, kIxThreads, 0, s2>>>(bins.edges[1], bins.count + 1, g.off, g.col, total, cr);
-    TC_LAUNCHED(ctx);
-    k_search<CM><<<grid, kIxThreads, 0, s2>>>(bins.edges[2], bins.count + 2, g.off, g.col, total, cr);
-    TC_LAUNCHED(ctx);
-    k_short<CM><<<grid, kIxThreads, 0, s2>>>(bins.edges[0], bins.count + 0, g.off, g.col, total, cr);
-    TC_LAUNCHED(ctx);
+    // bins the policy cannot fill (bin.cu gives them no capacity) are not launched
+    if (bins.has[1]) {
+        k_merge<CM><<<grid, kIxThreads, 0, s2>>>(bins.edges[1], bins.count + 1, g.off, g.col, total, cr);
+        TC_LAUNCHED(ctx);
+    }
+    if (bins.has[2]) {
+        k_search<CM><<<grid, kIxThreads, 0, s2>>>(bins.edges[2], bins.count + 2, g.off, g.col, total, cr);
+        TC_LAUNCHED(ctx);
+    }
+    if (bins.has[0]) {
+        k_short<CM><<<grid, kIxThreads, 0, s2>>>(bins.edges[0], bins.count + 0, g.off, g.col, total, cr);
+        TC_LAUNCHED(ctx);
+    }
     if (CM == kCmNone)   // dense-core edges (core.cu); their word count -> stats
         core_count(ctx, g, bins.hp, total, bins.count + 14, s2);
     side.join();

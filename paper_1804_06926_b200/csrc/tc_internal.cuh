@@ -428,7 +428,7 @@ struct HashParams {
     // dense core (core.cu): rank ids [core_lo, n) have adjacency bitmaps of core_words words
     // each; nullptr = no core path (per-vertex / edge / list modes, forced variants)
     const uint32_t *core = nullptr;
-    const uint2 *core_range = nullptr;   // (first, last) element of N+(y), y in the core
+    const uint4 *core_info = nullptr;    // (first, last element, d+) of N+(y), y in the core
     uint32_t core_lo = 0, core_words = 0;
 };
 
@@ -465,6 +465,7 @@ __device__ __forceinline__ int edge_bin(const HashParams &hp, uint32_t du, uint3
 // followed, if it owns out-part edges, by its own row.
 struct Bins {
     uint2 *edges[3] = {nullptr, nullptr, nullptr};  // SHORT, MERGE, SEARCH: (u, v) pairs
+    bool has[3] = {false, false, false};            // the policy can route edges there
     uint64_t *count = nullptr;  // device: [0..3] SHORT/MERGE/SEARCH/HASH edges, [4] W,
                                 // [5] sum min(|N+(u) after v|, d+(v)), [6] skipped, [7] max d+,
                                 // [8] warp owners, [9] CTA hash owners, [10] CTA bitmap owners,
