@@ -31,11 +31,22 @@ _u64p = ctypes.POINTER(ctypes.c_uint64)
 _u32p = ctypes.POINTER(ctypes.c_uint32)
 
 
+# TC_ORACLE_SANITIZE=1: build and load an AddressSanitizer + UBSan build instead (run the
+# Python process with LD_PRELOAD=$(gcc -print-file-name=libasan.so), see
+# scripts/oracle_sanitize.sh); any report aborts the process.
+_SANITIZE = os.environ.get("TC_ORACLE_SANITIZE") == "1"
+if _SANITIZE:
+    _LIB = os.path.join(_HERE, "liboracle_asan.so")
+
+
 def build(force: bool = False) -> str:
     """Compile tc_oracle.c into liboracle.so (gcc, -O2, OpenMP)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         cmd = ["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-std=c11", "-Wall",
                "-o", _LIB, _SRC]
+        if _SANITIZE:
+            cmd[1:1] = ["-g", "-fsanitize=address,undefined", "-fno-omit-frame-pointer",
+                        "-fno-sanitize-recover=undefined"]
         subprocess.run(cmd, check=True)
     return _LIB
 

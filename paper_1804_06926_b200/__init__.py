@@ -218,7 +218,9 @@ def _options(stream=None, force_variant=None, short_max=None, skew_ratio=None, h
         stream = torch.cuda.current_stream(device).cuda_stream
     o.stream = stream or None
     if allocator is None and on_device:
-        allocator = "torch"
+        # TC_ALLOCATOR=library: the library's own pool (compute-sanitizer sees each block;
+        # torch's caching allocator sub-allocates large segments)
+        allocator = os.environ.get("TC_ALLOCATOR", "torch")
     hooks = _hook_pair(allocator)
     if hooks is not None:
         o.alloc, o.free = hooks

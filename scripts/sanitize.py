@@ -12,7 +12,7 @@ import oracle as O
 import paper_1804_06926_b200 as tc
 
 graphs = [G.karate(), G.rmat(10, 16, seed=3), G.road_mesh(40, 30, seed=2),
-          G.kron(G.karate(), G.fig_mm())]
+          G.kron(G.karate(), G.fig_mm()), G.rmat(12, 16, seed=5)]   # s12: dense-core path
 for g in graphs:
     T, t = O.count(g.n, g.rowptr, g.col, per_vertex=True)
     rp = torch.from_numpy(g.rowptr.view(np.int64)).cuda()
@@ -20,6 +20,9 @@ for g in graphs:
     for v in (None, tc.VARIANT_SHORT, tc.VARIANT_MERGE, tc.VARIANT_SEARCH, tc.VARIANT_HASH):
         got, pv = tc.count_ex(rp, cl, per_vertex=True, force_variant=v)
         assert got == T and (pv.cpu().numpy().view(np.uint64) == t).all(), (g.name, v)
+    # the plain count through the pipeline (dense core) and through the one-kernel path
+    assert tc.count_ex(rp, cl, tiny_max_n=0) == T and tc.count_ex(rp, cl) == T
+    assert tc.count_ex(rp, cl, allocator="library") == T
     assert tc.count_ex(rp, cl, prune=True, hub_min_dplus=2) == T
     assert tc.count_ex(rp, cl, id_order=True) == T
     assert tc.clustering(rp, cl)[1]["triangles"] == T

@@ -1,6 +1,6 @@
 """compute-sanitizer memcheck over every entry point on small graphs (scripts/sanitize.py):
 no out-of-bounds or misaligned device access, no CUDA API error.  (racecheck and
-synccheck of the same script are recorded in profiles/r01_sanitizers.txt.)"""
+synccheck of the same script are recorded in profiles/r02_sanitizers.txt.)"""
 import os
 import shutil
 import subprocess
@@ -19,8 +19,9 @@ def test_memcheck_all_entry_points():
     cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
     if not os.path.exists(cs):
         pytest.skip("compute-sanitizer not installed")
+    env = dict(os.environ, TC_ALLOCATOR="library")   # per-block tracking (binding note)
     r = subprocess.run([cs, "--tool", "memcheck", "--error-exitcode", "9", sys.executable,
                         os.path.join(ROOT, "scripts", "sanitize.py")],
-                       capture_output=True, text=True, timeout=900)
+                       capture_output=True, text=True, timeout=900, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert "ERROR SUMMARY: 0 errors" in r.stdout + r.stderr
