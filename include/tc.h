@@ -212,6 +212,30 @@ tc_status tc_count_shard(uint64_t n, uint64_t m, const uint64_t *row_offsets,
                          int rank, int world, uint64_t *partial_dev,
                          uint64_t *per_vertex_partial, tc_stats *stats);
 
+/* Sharded a1 for multi-GPU runs (the cleaning step, Table 1 caption P:604-606,
+ * split over the ranks instead of repeated on each).  Every rank passes the SAME raw CSR
+ * (device pointers; n, m as in tc_count) and cleans only the arcs of ITS undirected edges:
+ * those whose smaller endpoint v has v % world == rank (every copy of an edge lands on one
+ * rank).  Output: edges[0 .. *m_edges) (device, capacity m) = this rank's unique undirected
+ * edges as sorted keys (min << b) | max with b = the bit width of n - 1 (at least 1);
+ * degrees (device, n entries, overwritten) = the degrees those edges give their endpoints;
+ * *m_edges (host).  The caller all-reduces (sums) the degrees and concatenates the ranks'
+ * edges (any order), then calls tc_count_edges_shard.  No flags.  Synchronous. */
+tc_status tc_clean_shard(uint64_t n, uint64_t m, const uint64_t *row_offsets,
+                         const uint32_t *col_indices, uint32_t flags, const tc_options *opt,
+                         int rank, int world, uint64_t *edges, uint32_t *degrees,
+                         uint64_t *m_edges);
+
+/* tc_count_shard's work from a cleaned edge list: edges (device, m_edges keys as
+ * tc_clean_shard writes them, every rank's, any order, each undirected edge once) and
+ * degrees (device, n: the full degrees, e.g. the all-reduced tc_clean_shard outputs);
+ * partial_dev / per_vertex_partial as tc_count_shard (summing over ranks gives tc_count's
+ * results).  Flags: TC_PER_VERTEX, TC_ID_ORDER.  Stream-ordered like tc_count_shard. */
+tc_status tc_count_edges_shard(uint64_t n, uint64_t m_edges, const uint64_t *edges,
+                               const uint32_t *degrees, uint32_t flags, const tc_options *opt,
+                               int rank, int world, uint64_t *partial_dev,
+                               uint64_t *per_vertex_partial, tc_stats *stats);
+
 /* Steps a1-a4 only ("Form_Filtered_Edge_List", Alg. 2): writes the
  * oriented, compacted CSR N+ (off_plus: n+1 entries; col_plus: capacity m
  * entries, first m_plus used; each row ascending) and *m_plus (host).

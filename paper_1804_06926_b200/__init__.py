@@ -20,7 +20,7 @@ import numpy as np
 __all__ = ["count", "count_ex", "count_shard", "orient", "clustering", "edge_support",
            "enumerate_triangles", "stats_dict", "library_path",
            "TC_CLEAN", "TC_SORTED", "TC_PER_VERTEX", "TC_HOST_PTRS", "TC_VALIDATE", "TC_PRUNE",
-           "TC_ID_ORDER", "masked_spgemm", "trim_workspace",
+           "TC_ID_ORDER", "masked_spgemm", "trim_workspace", "clean_shard", "count_edges_shard",
            "VARIANT_AUTO", "VARIANT_SHORT", "VARIANT_MERGE", "VARIANT_SEARCH", "VARIANT_HASH",
            "TCError"]
 
@@ -146,6 +146,12 @@ def _load():
     lib.tc_count_shard.argtypes = [u64, u64, vp, vp, u32, ctypes.POINTER(Options), ctypes.c_int,
                                    ctypes.c_int, vp, vp, ctypes.POINTER(Stats)]
     lib.tc_count_shard.restype = ctypes.c_int
+    lib.tc_clean_shard.argtypes = [u64, u64, vp, vp, u32, ctypes.POINTER(Options), ctypes.c_int,
+                                   ctypes.c_int, vp, vp, vp]
+    lib.tc_clean_shard.restype = ctypes.c_int
+    lib.tc_count_edges_shard.argtypes = [u64, u64, vp, vp, u32, ctypes.POINTER(Options), ctypes.c_int,
+                                         ctypes.c_int, vp, vp, ctypes.POINTER(Stats)]
+    lib.tc_count_edges_shard.restype = ctypes.c_int
     lib.tc_orient.argtypes = [u64, u64, vp, vp, u32, ctypes.POINTER(Options), vp, vp, vp]
     lib.tc_orient.restype = ctypes.c_int
     lib.tc_clustering.argtypes = [u64, u64, vp, vp, u32, ctypes.POINTER(Options), vp, vp,
@@ -316,6 +322,46 @@ def count_shard(rowptr, col, rank: int, world: int, partial, *, clean=False, sor
     _check(_in_dev(keep, on_dev, lambda: lib.tc_count_shard(n, M, rp, cp, flags, ctypes.byref(o), rank, world, partial.data_ptr(),
                               per_vertex_partial.data_ptr() if per_vertex_partial is not None else None,
                               ctypes.byref(st) if with_stats else None)))
+    return stats_dict(st) if with_stats else None
+
+
+def clean_shard(rowptr, col, rank: int, world: int, *, stream=None, **opts):
+    """Sharded a1 (tc_clean_shard): this rank's unique undirected edges as sorted int64 keys
+    (min << b) | max (a CUDA tensor view of length m_r) and the degrees they contribute
+    (int32[n]); sum the degrees and concatenate the edges over ranks, then count_edges_shard."""
+    import torch
+    lib = _load()
+    n, M, rp, cp, on_dev, keep = _arrays(rowptr, col)
+    if not on_dev:
+        raise ValueError("clean_shard takes CUDA tensors")
+    dev = keep[0].device
+    edges = torch.empty(max(M, 1), dtype=torch.int64, device=dev)
+    deg = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    o = _options(stream=stream, device=dev, **opts)
+    m = ctypes.c_uint64(0)
+    _check(_in_dev(keep, on_dev, lambda: lib.tc_clean_shard(
+        n, M, rp, cp, 0, ctypes.byref(o), rank, world, edges.data_ptr(), deg.data_ptr(),
+        ctypes.addressof(m))))
+    return edges[:m.value], deg[:n]
+
+
+def count_edges_shard(n: int, edges, degrees, rank: int, world: int, partial, *,
+                      per_vertex_partial=None, id_order=False, stream=None, with_stats=False, **opts):
+    """tc_count_edges_shard: this rank's share of the count from the cleaned edge list of every
+    rank (int64 CUDA tensor, any order) and the summed degrees; `partial` (int64[1]) is
+    overwritten."""
+    lib = _load()
+    edges = edges.contiguous()
+    degrees = degrees.contiguous()
+    keep = (edges, degrees)
+    flags = (TC_PER_VERTEX if per_vertex_partial is not None else 0) | (TC_ID_ORDER if id_order else 0)
+    o = _options(stream=stream, device=edges.device, **opts)
+    st = Stats()
+    _check(_in_dev(keep, True, lambda: lib.tc_count_edges_shard(
+        n, edges.numel(), edges.data_ptr() if edges.numel() else degrees.data_ptr(),
+        degrees.data_ptr(), flags, ctypes.byref(o), rank, world, partial.data_ptr(),
+        per_vertex_partial.data_ptr() if per_vertex_partial is not None else None,
+        ctypes.byref(st) if with_stats else None)))
     return stats_dict(st) if with_stats else None
 
 

@@ -56,6 +56,45 @@ __global__ void __launch_bounds__(kTileThreads)
     }
 }
 
+// tc_clean_shard: only the arcs whose undirected edge belongs to this rank (min endpoint
+// mod world == rank: every copy of an edge lands on one rank, and the ranks get about equal
+// shares), compacted -- one atomic per tile, order free (the keys are sorted next).
+__global__ void __launch_bounds__(kTileThreads)
+    k_clean_keys_shard(const uint64_t *__restrict__ rowptr, const uint32_t *__restrict__ col,
+                       uint64_t n, uint64_t M, int b, uint32_t rank, uint32_t world,
+                       uint64_t *__restrict__ keys, uint64_t *__restrict__ count) {
+    __shared__ uint32_t s_row[kTileItems];
+    __shared__ uint32_t s_scan[kTileThreads / 32];
+    __shared__ uint64_t s_base;
+    const uint64_t t0 = (uint64_t)blockIdx.x * kTileItems;
+    const uint32_t len = (uint32_t)min((uint64_t)kTileItems, M - t0);
+    tile_rows(rowptr, n, t0, len, s_row, s_scan);
+    const uint32_t i0 = threadIdx.x * kItemsPerThread;
+    uint64_t kk[kItemsPerThread];
+    uint32_t c = 0;
+#pragma unroll
+    for (int k = 0; k < kItemsPerThread; k++) {
+        const uint32_t i = i0 + k;
+        kk[k] = ~0ull;
+        if (i < len) {
+            const uint64_t u = s_row[i], v = col[t0 + i];
+            const uint64_t a = u < v ? u : v, d = u < v ? v : u;
+            if (u != v && a % world == rank) {
+                kk[k] = (a << b) | d;
+                c++;
+            }
+        }
+    }
+    uint32_t total;
+    const uint32_t pos = block_exclusive_scan<SumOp>(c, s_scan, &total);
+    if (threadIdx.x == 0) s_base = atomicAdd((unsigned long long *)count, (unsigned long long)total);
+    __syncthreads();
+    uint64_t o = s_base + pos;
+#pragma unroll
+    for (int k = 0; k < kItemsPerThread; k++)
+        if (kk[k] != ~0ull) keys[o++] = kk[k];
+}
+
 // ------------------------------------------------------------------ a1: unique
 // Single pass (no separate count kernel + scan): tiles take a ticket, publish their unique
 // count, and get the exclusive prefix of earlier tiles by decoupled look-back (one
@@ -74,15 +113,25 @@ __device__ __forceinline__ uint64_t uq_ld(const uint64_t *p) {
 }
 
 __global__ void __launch_bounds__(kTileThreads)
-    k_unique_scatter(const uint64_t *__restrict__ keys, uint64_t M, uint32_t *__restrict__ ticket,
-                     uint64_t *__restrict__ status, uint64_t *__restrict__ m_out,
-                     uint64_t *__restrict__ out, int b, uint32_t *__restrict__ deg) {
+    k_unique_scatter(const uint64_t *__restrict__ keys, uint64_t M, const uint64_t *__restrict__ count_dev,
+                     uint32_t *__restrict__ ticket, uint64_t *__restrict__ status,
+                     uint64_t *__restrict__ m_out, uint64_t *__restrict__ out, int b,
+                     uint32_t *__restrict__ deg) {
     __shared__ uint32_t s_scan[kTileThreads / 32];
     __shared__ uint32_t s_tile;
     __shared__ uint64_t s_excl;
+    if (count_dev) {   // the keys are a compacted prefix (tc_clean_shard): tiles past it exit
+        const uint64_t c = *count_dev;
+        M = c < M ? c : M;
+        if (M == 0) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) *m_out = 0;
+            return;
+        }
+    }
     if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
     __syncthreads();
     const uint32_t tile = s_tile;
+    if ((uint64_t)tile * kTileItems >= M) return;   // nobody waits on a tile past the keys
     const uint64_t base = (uint64_t)tile * kTileItems + (uint64_t)threadIdx.x * kItemsPerThread;
     uint32_t f[kItemsPerThread];
     uint64_t kk[kItemsPerThread];
@@ -331,29 +380,70 @@ static void pairs_to_csr(Ctx &ctx, uint64_t n, uint64_t cap, uint32_t *okey, uin
     phase_end(tm, kOrient);
 }
 
+// a1 on all arcs, or (world > 1, tc_clean_shard) on this rank's share: the unique undirected
+// edges as sorted keys (min << b) | max in E (m_dev of them; E = one of keys / keys_alt),
+// and the degrees they give both endpoints added into deg (zeroed by the caller).
+static void clean_arcs(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
+                       int rank, int world, uint64_t *keys, uint64_t *keys_alt, uint64_t *&E,
+                       uint64_t *&m_dev, uint32_t *deg) {
+    const int b = id_bits(n);
+    const uint32_t tiles = (uint32_t)((M + kTileItems - 1) / kTileItems);
+    // status words [0, tiles), the ticket counter, m (the unique-edge count), the key count
+    uint64_t *uq = ctx.alloc<uint64_t>(tiles + 3);
+    TC_CUDA(cudaMemsetAsync(uq, 0, (tiles + 3) * sizeof(uint64_t), ctx.stream));
+    m_dev = uq + tiles + 1;
+    const uint64_t *count = nullptr;
+    if (world > 1) {
+        k_clean_keys_shard<<<tiles, kTileThreads, 0, ctx.stream>>>(rowptr, col, n, M, b, (uint32_t)rank,
+                                                                   (uint32_t)world, keys, uq + tiles + 2);
+        count = uq + tiles + 2;
+    } else {
+        k_clean_keys<<<tiles, kTileThreads, 0, ctx.stream>>>(rowptr, col, n, M, b, keys);
+    }
+    TC_LAUNCHED(ctx);
+    bool alt = radix_sort(ctx, keys, keys_alt, M, count, 2 * b);
+    uint64_t *sorted = alt ? keys_alt : keys;
+    E = alt ? keys : keys_alt;
+    k_unique_scatter<<<tiles, kTileThreads, 0, ctx.stream>>>(sorted, M, count, (uint32_t *)(uq + tiles),
+                                                             uq, m_dev, E, b, deg);
+    TC_LAUNCHED(ctx);
+}
+
+void clean_shard(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
+                 int rank, int world, uint64_t *edges, uint32_t *deg, uint64_t *m_dev_out) {
+    uint64_t *alt = ctx.alloc<uint64_t>(M), *E = nullptr, *m_dev = nullptr;
+    // keys are sorted in `edges` / `alt`; the unique edges end up in the other one
+    clean_arcs(ctx, n, M, rowptr, col, rank, world, edges, alt, E, m_dev, deg);
+    if (E != edges) {
+        uint64_t m = 0;
+        TC_CUDA(cudaMemcpyAsync(&m, m_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx.stream));
+        TC_CUDA(cudaStreamSynchronize(ctx.stream));
+        if (m) TC_CUDA(cudaMemcpyAsync(edges, E, m * sizeof(uint64_t), cudaMemcpyDeviceToDevice, ctx.stream));
+    }
+    TC_CUDA(cudaMemcpyAsync(m_dev_out, m_dev, sizeof(uint64_t), cudaMemcpyDeviceToDevice, ctx.stream));
+}
+
 void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
                   Oriented &out, Timer *tm,
                   PruneInfo &prune, bool id_order) {
-    int b = id_bits(n);
-    uint32_t tiles = (uint32_t)((M + kTileItems - 1) / kTileItems);
     phase_begin(tm, kClean);
     uint64_t *keys = ctx.alloc<uint64_t>(M);
     uint64_t *keys_alt = ctx.alloc<uint64_t>(M);
-    k_clean_keys<<<tiles, kTileThreads, 0, ctx.stream>>>(rowptr, col, n, M, b, keys);
-    TC_LAUNCHED(ctx);
-    bool alt = radix_sort(ctx, keys, keys_alt, M, nullptr, 2 * b);
-    uint64_t *sorted = alt ? keys_alt : keys, *E = alt ? keys : keys_alt;
-    // status words [0, tiles), the ticket counter, and m (the unique-edge count) at the end
-    uint64_t *uq = ctx.alloc<uint64_t>(tiles + 2);
-    TC_CUDA(cudaMemsetAsync(uq, 0, (tiles + 2) * sizeof(uint64_t), ctx.stream));
     uint32_t *deg = ctx.alloc<uint32_t>(n);
     TC_CUDA(cudaMemsetAsync(deg, 0, n * sizeof(uint32_t), ctx.stream));
-    uint64_t *m_dev = uq + tiles + 1;
-    k_unique_scatter<<<tiles, kTileThreads, 0, ctx.stream>>>(sorted, M, (uint32_t *)(uq + tiles), uq,
-                                                             m_dev, E, b, deg);
-    TC_LAUNCHED(ctx);
+    uint64_t *E = nullptr, *m_dev = nullptr;
+    clean_arcs(ctx, n, M, rowptr, col, 0, 1, keys, keys_alt, E, m_dev, deg);
     phase_end(tm, kClean);
+    orient_edges(ctx, n, M, E, m_dev, deg, out, tm, prune, id_order, keys, keys_alt);
+}
 
+// a2-a4 from the unique undirected edges E (keys (min << b) | max; any order) and the degrees
+// of the graph they form.  free0 / free1: workspace blocks that are dead once the oriented
+// pairs exist (the a1 key buffers), given back to the pool before the CSR build.
+void orient_edges(Ctx &ctx, uint64_t n, uint64_t M, uint64_t *E, uint64_t *m_dev, uint32_t *deg,
+                  Oriented &out, Timer *tm, PruneInfo &prune, bool id_order, void *free0,
+                  void *free1) {
+    const int b = id_bits(n);
     phase_begin(tm, kOrient);
     uint32_t *dplus = ctx.alloc<uint32_t>(n + 1), *dminus = ctx.alloc<uint32_t>(n + 1);
     TC_CUDA(cudaMemsetAsync(dplus, 0, (n + 1) * sizeof(uint32_t), ctx.stream));
@@ -378,8 +468,8 @@ void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, cons
     TC_LAUNCHED(ctx);
     // the 64-bit keys (E and its sort buffer) are dead: give 16 B per raw arc back to the
     // pool before the CSR build (peak device memory at s26: -17 GB)
-    ctx.free_now(keys);
-    ctx.free_now(keys_alt);
+    if (free0) ctx.free_now(free0);
+    if (free1) ctx.free_now(free1);
     pairs_to_csr(ctx, n, M, okey, oval, dplus, dminus, m_dev, out, tm, phist,
                  phist + ppasses * kHistDigits);
 }

@@ -67,7 +67,7 @@ static void check_claim(const uint64_t *pin) {
                                "m/2 (the input is not simple and symmetric)"};
 }
 
-enum Mode { kCount, kShard, kOrientOnly, kClustering, kSupport, kEnumerate, kMasked };
+enum Mode { kCount, kShard, kOrientOnly, kClustering, kSupport, kEnumerate, kMasked, kCleanShard };
 
 struct Call {
     uint64_t n, M;
@@ -90,10 +90,35 @@ struct Call {
     uint32_t *support = nullptr;      // kSupport (with off_plus / col_plus / m_plus)
     uint32_t *triangles = nullptr;    // kEnumerate: capacity triples
     uint64_t capacity = 0;
+    // kShard from a sharded a1 (tc_count_edges_shard): the unique edges and their degrees
+    const uint64_t *edges_in = nullptr;
+    const uint32_t *deg_in = nullptr;
+    // kCleanShard (tc_clean_shard): this rank's unique edges, degree partials, edge count
+    uint64_t *edges_out = nullptr;
+    uint32_t *deg_out = nullptr;
+    uint64_t *m_edges_out = nullptr;
 };
 
 static tc_status check_args(const Call &c) {
     if (c.flags & ~(uint32_t)TC_ALL_FLAGS) return set_error("unknown flag bits"), TC_EINVAL;
+    if (c.mode == kCleanShard || c.edges_in) {   // the sharded-a1 pair (tc.h)
+        if (c.world < 1 || c.rank < 0 || c.rank >= c.world)
+            return set_error("need 0 <= rank < world"), TC_EINVAL;
+        if (c.n >= (1ull << 32) || c.M >= (1ull << 32))
+            return set_error("n and m must be < 2^32"), TC_EINVAL;
+        const uint32_t allowed = c.mode == kCleanShard ? 0u : (uint32_t)(TC_PER_VERTEX | TC_ID_ORDER);
+        if (c.flags & ~allowed) return set_error("flag not supported by this entry point"), TC_EINVAL;
+        if (c.mode == kCleanShard && (!c.rowptr || (c.M && !c.col) || !c.edges_out || !c.deg_out ||
+                                      !c.m_edges_out))
+            return set_error("tc_clean_shard: NULL argument"), TC_EINVAL;
+        if (c.edges_in && (!c.deg_in || !c.partial_dev || ((c.flags & TC_PER_VERTEX) && !c.per_vertex)))
+            return set_error("tc_count_edges_shard: NULL argument"), TC_EINVAL;
+        if (c.opt.force_variant < -1 || c.opt.force_variant > 3)
+            return set_error("force_variant out of range"), TC_EINVAL;
+        if (!c.opt.alloc != !c.opt.free)
+            return set_error("tc_options.alloc and .free must be given together"), TC_EINVAL;
+        return TC_OK;
+    }
     if (c.n >= (1ull << 32)) return set_error("n must be < 2^32"), TC_EINVAL;
     if (c.M >= (1ull << 32))   // edge positions, in-list slots and probe ranges are 32-bit
         return set_error("m (arcs) must be < 2^32"), TC_EINVAL;
@@ -167,10 +192,31 @@ static void run(Call &c) {
         ctx.pool = ds.pool;
         set_pool_keep(ds.pool, c.opt.keep_workspace != 0);
     }
-    const bool host = c.flags & TC_HOST_PTRS;
-    if (!host) {
+    if (c.mode == kCleanShard) {
         check_device_ptr(c.rowptr, ctx.device, "row_offsets");
         check_device_ptr(c.col, ctx.device, "col_indices");
+        check_device_ptr(c.edges_out, ctx.device, "edges");
+        check_device_ptr(c.deg_out, ctx.device, "degrees");
+        if (c.n) TC_CUDA(cudaMemsetAsync(c.deg_out, 0, c.n * sizeof(uint32_t), ctx.stream));
+        uint64_t *m_dev = ctx.alloc<uint64_t>(1);
+        TC_CUDA(cudaMemsetAsync(m_dev, 0, sizeof(uint64_t), ctx.stream));
+        if (c.n && c.M) clean_shard(ctx, c.n, c.M, c.rowptr, c.col, c.rank, c.world, c.edges_out,
+                                    c.deg_out, m_dev);
+        uint64_t *pin = pinned_scratch();
+        TC_CUDA(cudaMemcpyAsync(pin + 27, m_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx.stream));
+        ctx.release();
+        TC_CUDA(cudaStreamSynchronize(ctx.stream));
+        *c.m_edges_out = pin[27];
+        return;
+    }
+    const bool host = c.flags & TC_HOST_PTRS;
+    if (!host) {
+        if (!c.edges_in) {
+            check_device_ptr(c.rowptr, ctx.device, "row_offsets");
+            check_device_ptr(c.col, ctx.device, "col_indices");
+        }
+        check_device_ptr(c.edges_in, ctx.device, "edges");
+        check_device_ptr(c.deg_in, ctx.device, "degrees");
         check_device_ptr(c.per_vertex, ctx.device, "per_vertex");
         check_device_ptr(c.partial_dev, ctx.device, "partial_dev");
         check_device_ptr(c.off_plus, ctx.device, "off_plus");
@@ -255,7 +301,7 @@ static void run(Call &c) {
     PruneInfo prune;
     prune.enabled = c.flags & TC_PRUNE;
     prune.rounds_wanted = c.opt.prune_rounds;
-    const bool tiny = (c.mode == kCount || c.mode == kShard) && c.n > 0 && c.M > 0 &&
+    const bool tiny = (c.mode == kCount || c.mode == kShard) && !c.edges_in && c.n > 0 && c.M > 0 &&
                       c.n <= c.opt.tiny_max_n && c.n <= kTinyMaxN && c.opt.force_variant < 0 &&
                       !(c.flags & (TC_PRUNE | TC_ID_ORDER));
     if (tiny) {   // one kernel (tiny.cu); a shard other than rank 0 contributes nothing
@@ -271,7 +317,12 @@ static void run(Call &c) {
                                     ctx.stream));
     } else if (c.n > 0 && c.M > 0) {
         Oriented g;
-        if (c.flags & TC_CLEAN)
+        if (c.edges_in) {   // after a sharded a1: the unique edges of every rank, all degrees
+            uint64_t *m_dev = ctx.alloc<uint64_t>(1);
+            TC_CUDA(cudaMemcpyAsync(m_dev, &c.M, sizeof(uint64_t), cudaMemcpyHostToDevice, ctx.stream));
+            orient_edges(ctx, c.n, c.M, const_cast<uint64_t *>(c.edges_in), m_dev,
+                         const_cast<uint32_t *>(c.deg_in), g, tm, prune, c.flags & TC_ID_ORDER);
+        } else if (c.flags & TC_CLEAN)
             orient_clean(ctx, c.n, c.M, rowptr, col, g, tm,
                          prune, c.flags & TC_ID_ORDER);
         else
@@ -551,6 +602,36 @@ tc_status tc_count_shard(uint64_t n, uint64_t m, const uint64_t *row_offsets,
     c.mode = kShard;
     c.rank = rank;
     c.world = world;
+    c.partial_dev = partial_dev;
+    c.per_vertex = per_vertex_partial;
+    c.stats = stats;
+    return guarded(c);
+}
+
+tc_status tc_clean_shard(uint64_t n, uint64_t m, const uint64_t *row_offsets,
+                         const uint32_t *col_indices, uint32_t flags, const tc_options *opt,
+                         int rank, int world, uint64_t *edges, uint32_t *degrees, uint64_t *m_edges) {
+    Call c{n, m, row_offsets, col_indices, flags, resolve(opt)};
+    c.mode = kCleanShard;
+    c.rank = rank;
+    c.world = world;
+    c.edges_out = edges;
+    c.deg_out = degrees;
+    c.m_edges_out = m_edges;
+    return guarded(c);
+}
+
+tc_status tc_count_edges_shard(uint64_t n, uint64_t m_edges, const uint64_t *edges,
+                               const uint32_t *degrees, uint32_t flags, const tc_options *opt,
+                               int rank, int world, uint64_t *partial_dev,
+                               uint64_t *per_vertex_partial, tc_stats *stats) {
+    static const uint64_t kNoRows = 0;   // the CSR is not read on this path
+    Call c{n, m_edges, &kNoRows, nullptr, flags, resolve(opt)};
+    c.mode = kShard;
+    c.rank = rank;
+    c.world = world;
+    c.edges_in = edges;
+    c.deg_in = degrees;
     c.partial_dev = partial_dev;
     c.per_vertex = per_vertex_partial;
     c.stats = stats;

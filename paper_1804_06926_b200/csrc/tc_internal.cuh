@@ -391,6 +391,15 @@ void prune_csr(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const u
 void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
                   Oriented &out, Timer *tm,
                   PruneInfo &prune, bool id_order);
+// a2 + a3 + a4 from unique undirected edges E (keys (min << b) | max, b = id bits of n, any
+// order; m_dev of them, at most M) and their graph's degrees deg (both kept by the caller).
+void orient_edges(Ctx &ctx, uint64_t n, uint64_t M, uint64_t *E, uint64_t *m_dev, uint32_t *deg,
+                  Oriented &out, Timer *tm, PruneInfo &prune, bool id_order,
+                  void *free0 = nullptr, void *free1 = nullptr);
+// tc_clean_shard: a1 on the arcs of this rank's edges (min endpoint mod world == rank): the
+// unique edges, sorted, into edges[0, *m_dev_out) and their degrees added into deg.
+void clean_shard(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
+                 int rank, int world, uint64_t *edges, uint32_t *deg, uint64_t *m_dev_out);
 // a2 + a3 + a4 for clean symmetric input.
 void orient_clean(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
                   Oriented &out, Timer *tm,

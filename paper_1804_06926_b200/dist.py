@@ -13,7 +13,49 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-from . import count_shard
+from . import clean_shard, count_edges_shard, count_shard
+
+
+def exchange_clean_shards(rowptr: torch.Tensor, col: torch.Tensor, group=None, *, clean_fn=None):
+    """Sharded a1 (tc_clean_shard on every rank) + its exchange: ONE all-reduce of the n int32
+    degree partials and ONE all-gather of the ranks' cleaned edge lists (padded to the longest,
+    the valid prefixes concatenated).  Returns (edges of every rank, summed degrees)."""
+    world = dist.get_world_size(group)
+    fn = clean_fn or clean_shard
+    edges, deg = fn(rowptr, col, dist.get_rank(group), world)
+    dist.all_reduce(deg, op=dist.ReduceOp.SUM, group=group)
+    dev = deg.device
+    m = torch.tensor([edges.numel()], dtype=torch.int64, device=dev)
+    sizes = [torch.zeros_like(m) for _ in range(world)]
+    dist.all_gather(sizes, m, group=group)
+    sizes = [int(x.item()) for x in sizes]
+    pad = max(sizes) if sizes else 0
+    buf = torch.zeros(pad, dtype=torch.int64, device=dev)
+    buf[:edges.numel()] = edges
+    out = [torch.empty(pad, dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(out, buf, group=group)
+    return torch.cat([o[:s] for o, s in zip(out, sizes)]), deg
+
+
+def count_distributed_sharded_a1(rowptr: torch.Tensor, col: torch.Tensor, group=None, *,
+                                 per_vertex: bool = False, clean_fn=None, count_fn=None):
+    """count_distributed with the cleaning step (a1) split over the ranks instead of repeated:
+    exchange_clean_shards, then tc_count_edges_shard on the gathered edges and one all-reduce
+    of the partial count (and of the per-vertex partials)."""
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    n = rowptr.numel() - 1
+    edges, deg = exchange_clean_shards(rowptr, col, group, clean_fn=clean_fn)
+    dev = rowptr.device
+    partial = torch.zeros(1, dtype=torch.int64, device=dev)
+    pv = torch.zeros(n, dtype=torch.int64, device=dev) if per_vertex else None
+    (count_fn or count_edges_shard)(n, edges, deg, rank, world, partial, per_vertex_partial=pv)
+    if per_vertex:
+        both = torch.cat([partial, pv])
+        dist.all_reduce(both, op=dist.ReduceOp.SUM, group=group)
+        return int(both[0].item()), both[1:]
+    dist.all_reduce(partial, op=dist.ReduceOp.SUM, group=group)
+    return int(partial.item())
 
 
 def count_distributed(rowptr: torch.Tensor, col: torch.Tensor, group=None, *, shard_fn=None,

@@ -35,4 +35,14 @@ for g in graphs:
         tc.count_shard(rp, cl, r, 3, p)
         parts.append(int(p.item()))
     assert sum(parts) == T
+    # the sharded cleaning step (tc_clean_shard + tc_count_edges_shard), 2 ranks in turn
+    cs = [tc.clean_shard(rp, cl, r, 2) for r in range(2)]
+    edges = torch.cat([e for e, _ in cs])
+    deg = (cs[0][1].to(torch.int64) + cs[1][1].to(torch.int64)).to(torch.int32)
+    tot = 0
+    for r in range(2):
+        p = torch.zeros(1, dtype=torch.int64, device="cuda")
+        tc.count_edges_shard(g.n, edges, deg, r, 2, p)
+        tot += int(p.item())
+    assert tot == T
     print(g.name, "ok", T, flush=True)

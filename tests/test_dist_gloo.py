@@ -75,3 +75,58 @@ def test_allreduce_wiring_world2():
     for rank, T1, T2, pv in res:
         assert T1 == T and T2 == T
         assert (pv.astype(np.uint64) == t).all()
+
+
+def _clean_worker(rank, world, port, q):
+    """exchange_clean_shards' wiring (degree all-reduce, variable-size edge all-gather) with a
+    CPU stand-in for tc_clean_shard: this rank's edges = the clean edges whose smaller endpoint
+    is = rank (mod world), as (min << b) | max keys, and the degrees they contribute."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import graphgen as G
+        import oracle as O
+        from paper_1804_06926_b200.dist import exchange_clean_shards
+
+        g = G.dirty(G.gnp(400, 0.05, 2), seed=3)
+        b = max(1, (g.n - 1).bit_length())
+
+        def clean_fn(rowptr, col, r, w):
+            crow, ccol = O.clean(g.n, g.rowptr, g.col)
+            src = np.repeat(np.arange(g.n, dtype=np.int64), np.diff(crow).astype(np.int64))
+            dst = ccol.astype(np.int64)
+            keep = (src < dst) & (src % w == r)
+            keys = (src[keep] << b) | dst[keep]
+            deg = np.bincount(src[keep], minlength=g.n) + np.bincount(dst[keep], minlength=g.n)
+            return torch.from_numpy(keys), torch.from_numpy(deg.astype(np.int32))
+
+        rp = torch.from_numpy(g.rowptr.view(np.int64))
+        cl = torch.from_numpy(g.col.view(np.int32))
+        edges, deg = exchange_clean_shards(rp, cl, clean_fn=clean_fn)
+        q.put((rank, np.sort(edges.numpy()), deg.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_clean_shard_exchange_world2():
+    import graphgen as G
+    import oracle as O
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_clean_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = G.dirty(G.gnp(400, 0.05, 2), seed=3)
+    crow, ccol = O.clean(g.n, g.rowptr, g.col)
+    b = max(1, (g.n - 1).bit_length())
+    src = np.repeat(np.arange(g.n, dtype=np.int64), np.diff(crow).astype(np.int64))
+    dst = ccol.astype(np.int64)
+    want = np.sort(((src << b) | dst)[src < dst])
+    for rank, keys, deg in res:
+        assert (keys == want).all(), rank
+        assert (deg == np.diff(crow)).all(), rank

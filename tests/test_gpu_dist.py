@@ -34,13 +34,17 @@ def _worker(rank, world, port, name, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_1804_06926_b200.dist import count_distributed
+        from paper_1804_06926_b200.dist import count_distributed, count_distributed_sharded_a1
         g = _graph(name)
         dev = torch.device("cuda:0")
         rp = torch.from_numpy(g.rowptr.view(np.int64)).to(dev)
         cl = torch.from_numpy(g.col.view(np.int32)).to(dev)
         T = count_distributed(rp, cl)
         T2, pv = count_distributed(rp, cl, per_vertex=True)
+        # the cleaning step split over the ranks: one degree all-reduce + one edge all-gather
+        T3 = count_distributed_sharded_a1(rp, cl)
+        T4, pv4 = count_distributed_sharded_a1(rp, cl, per_vertex=True)
+        assert T3 == T and T4 == T and (pv4 == pv).all()
         q.put((rank, T, T2, pv.cpu().numpy().copy()))
     finally:
         dist.destroy_process_group()

@@ -568,3 +568,37 @@ def test_tiny_path(name):
     assert tot == T
     h = tc.count_ex(g.rowptr, g.col, per_vertex=True)               # host pointers
     assert h[0] == T and (h[1] == t).all()
+
+
+# ------------------------------------------------------------------ sharded a1 (multi-GPU)
+@pytest.mark.parametrize("name", ["rmat14", "dirty_gnp", "clique", "road"])
+def test_sharded_clean_then_count(name):
+    """tc_clean_shard on every rank + the exchange (degree sum, edge concatenation), emulated
+    on one GPU, then tc_count_edges_shard per rank: the gathered edges are exactly the
+    oracle's clean edge set, the summed degrees its degrees, and the partial counts (and
+    per-vertex partials) sum to the oracle's."""
+    g = {"rmat14": lambda: G.rmat(14, 16, seed=12), "dirty_gnp": lambda: G.dirty(G.gnp(3000, 0.01, 5), seed=6),
+         "clique": lambda: G.clique_union(30_000, 40_000), "road": lambda: G.road_mesh(300, 200, seed=3)}[name]()
+    T, t = O.count(g.n, g.rowptr, g.col, per_vertex=True)
+    crow, ccol = O.clean(g.n, g.rowptr, g.col)
+    b = max(1, (g.n - 1).bit_length())
+    src = np.repeat(np.arange(g.n, dtype=np.uint64), np.diff(crow).astype(np.int64))
+    want_keys = np.sort(((src << np.uint64(b)) | ccol.astype(np.uint64))[src < ccol.astype(np.uint64)])
+    want_deg = np.diff(crow).astype(np.int64)
+    rp, cl = on_dev(g.rowptr, g.col)
+    for world in (1, 2, 3, 8):
+        parts = [tc.clean_shard(rp, cl, r, world) for r in range(world)]
+        edges = torch.cat([e for e, _ in parts])
+        deg = sum(d.to(torch.int64) for _, d in parts).to(torch.int32)
+        got_keys = np.sort(edges.cpu().numpy().view(np.uint64))
+        assert (got_keys == want_keys).all(), world
+        assert (deg.cpu().numpy() == want_deg).all(), world
+        tot, pv_sum = 0, torch.zeros(g.n, dtype=torch.int64, device=DEV)
+        for r in range(world):
+            p = torch.zeros(1, dtype=torch.int64, device=DEV)
+            pv = torch.zeros(g.n, dtype=torch.int64, device=DEV)
+            tc.count_edges_shard(g.n, edges, deg, r, world, p, per_vertex_partial=pv)
+            tot += int(p.item())
+            pv_sum += pv
+        torch.cuda.synchronize()
+        assert tot == T and (pv_np(pv_sum) == t).all(), world
