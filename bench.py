@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-next", action="store_true", help="skip the NEXT-row measurements")
+    ap.add_argument("--replicated-a1", action="store_true",
+                    help="N > 1: every rank cleans all arcs (default: the cleaning step is split "
+                         "over the ranks, tc_clean_shard + one all-reduce + one all-gather)")
     ap.add_argument("--one-call", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--clean-input", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--no-ncu", action="store_true",
@@ -421,7 +424,8 @@ def main():
 
     import torch
     import paper_1804_06926_b200 as tc
-    from paper_1804_06926_b200.dist import count_distributed
+    from paper_1804_06926_b200.dist import (count_distributed, count_distributed_sharded_a1,
+                                            exchange_clean_shards)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
@@ -437,7 +441,11 @@ def main():
     def step(with_stats=False):
         if world == 1:
             return tc.count_ex(rp, cl, with_stats=with_stats)
-        st = tc.count_shard(rp, cl, rank, world, partial, with_stats=with_stats)
+        if args.replicated_a1:   # every rank cleans all arcs (SURVEY §8(e) as written)
+            st = tc.count_shard(rp, cl, rank, world, partial, with_stats=with_stats)
+        else:                    # the cleaning step split over the ranks (dist.py)
+            edges, deg = exchange_clean_shards(rp, cl)
+            st = tc.count_edges_shard(g.n, edges, deg, rank, world, partial, with_stats=with_stats)
         dist.all_reduce(partial)
         return (int(partial.item()), st) if with_stats else int(partial.item())
 
@@ -498,7 +506,9 @@ def main():
                 return tc.count_ex(rp_h, cl_h, with_stats=True)[0]
             d_rp = rp_h.to(dev, non_blocking=True)
             d_cl = cl_h.to(dev, non_blocking=True)
-            return count_distributed(d_rp, d_cl)
+            if args.replicated_a1:
+                return count_distributed(d_rp, d_cl)
+            return count_distributed_sharded_a1(d_rp, d_cl)
 
         e2e_step()   # warm
         reps = max(3, min(args.steps, 5))
@@ -517,8 +527,8 @@ def main():
         e2e = {"value": m / e2e_s, "unit": "edges/s", "ms_per_step": 1e3 * e2e_s,
                "h2d_bytes_per_step": in_bytes * world, "d2h_bytes_per_step": 8 * world,
                "note": ("tc_count_ex with TC_HOST_PTRS from pinned host memory" if world == 1 else
-                        "count_distributed: per rank H2D of the raw CSR (non_blocking from pinned), "
-                        "tc_count_shard, NCCL allreduce, .item()") +
+                        "count_distributed[_sharded_a1]: per rank H2D of the raw CSR (non_blocking "
+                        "from pinned), the same path as the step, .item()") +
                        "; host wall clock per step, max over ranks"}
 
     if rank != 0:
@@ -564,10 +574,13 @@ def main():
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (seeded R-MAT, Graph500 A,B,C,D=.57,.19,.19,.05; raw arcs)",
         "config": {"workload": g.name, "n": g.n, "m": m, "raw_arcs": g.arcs, "T": T_total,
-                   "parallelism": f"replicated graph, work-split sources x{world}",
+                   "parallelism": (f"dp{world}: replicated input, owner-split intersection"
+                                   + ("" if world == 1 or args.replicated_a1 else ", sharded cleaning")),
                    "l2": "flushed between timed steps (512 MiB write outside the event spans)",
                    "step": "tc_count_ex on raw arcs: clean, orient, bin, intersect, reduce"
-                           + (" (tc_count_shard per rank) + NCCL allreduce" if world > 1 else "")},
+                           + ((" (tc_count_shard per rank) + NCCL allreduce" if args.replicated_a1 else
+                               " (tc_clean_shard per rank, NCCL all-reduce of degrees + all-gather of "
+                               "edges, tc_count_edges_shard, NCCL allreduce)") if world > 1 else "")},
         "phases_ms": {k: sum(s[k] for s in stats) / len(stats)
                       for k in ("ms_clean", "ms_orient", "ms_sort", "ms_bin", "ms_intersect", "ms_total")},
         "step_ms_min_max": [min(step_ms), max(step_ms)],
