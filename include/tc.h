@@ -144,7 +144,13 @@ typedef struct {
                                    the whole method in ONE kernel on a shared-memory adjacency
                                    bitmap (small graphs are launch-bound); 0 = off.
                                    Default 1024.  Stats then carry m_undirected and times only */
-    uint32_t reserved[8];       /* must be zero                                                 */
+    uint32_t clean_method;      /* a1 on dirty input (no TC_CLEAN) and tc_clean_shard: the arcs
+                                   become 64-bit (min, max) keys, radix-sorted, then unique.
+                                   0 (default) = sorted by a hash of the key in its low 24/32
+                                   bits only (3-4 passes; duplicates share a run of equal
+                                   hash), 1 = sorted in full (min, max) order (6-8 passes).
+                                   Same results                                                */
+    uint32_t reserved[7];       /* must be zero                                                 */
 } tc_options;
 
 typedef struct {
@@ -217,7 +223,8 @@ tc_status tc_count_shard(uint64_t n, uint64_t m, const uint64_t *row_offsets,
  * (device pointers; n, m as in tc_count) and cleans only the arcs of ITS undirected edges:
  * those whose smaller endpoint v has v % world == rank (every copy of an edge lands on one
  * rank).  Output: edges[0 .. *m_edges) (device, capacity m) = this rank's unique undirected
- * edges as sorted keys (min << b) | max with b = the bit width of n - 1 (at least 1);
+ * edges as keys (min << b) | max with b = the bit width of n - 1 (at least 1), in an
+ * unspecified order (ascending with tc_options.clean_method = 1);
  * degrees (device, n entries, overwritten) = the degrees those edges give their endpoints;
  * *m_edges (host).  The caller all-reduces (sums) the degrees and concatenates the ranks'
  * edges (any order), then calls tc_count_edges_shard.  No flags.  Synchronous. */

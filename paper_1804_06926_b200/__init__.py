@@ -51,7 +51,7 @@ class Options(ctypes.Structure):
                 ("stream", ctypes.c_void_p), ("prune_rounds", ctypes.c_uint32),
                 ("keep_workspace", ctypes.c_uint32), ("alloc", ALLOC_FN), ("free", FREE_FN),
                 ("alloc_ctx", ctypes.c_void_p), ("tiny_max_n", ctypes.c_uint32),
-                ("reserved", ctypes.c_uint32 * 8)]
+                ("clean_method", ctypes.c_uint32), ("reserved", ctypes.c_uint32 * 7)]
 
 
 def _torch_raw_alloc(ctx, size, stream):
@@ -214,7 +214,7 @@ def _flags(clean=False, sorted_rows=False, per_vertex=False, validate=False, pru
 
 def _options(stream=None, force_variant=None, short_max=None, skew_ratio=None, hub_min_dplus=None,
              prune_rounds=None, on_device=True, allocator=None, device=None, keep_workspace=None,
-             tiny_max_n=None):
+             tiny_max_n=None, clean_method=None):
     """tc_options for one call.  Device calls default to the current stream of the inputs'
     device and to torch's caching allocator for the workspace."""
     o = Options()
@@ -244,6 +244,8 @@ def _options(stream=None, force_variant=None, short_max=None, skew_ratio=None, h
         o.keep_workspace = int(bool(keep_workspace))
     if tiny_max_n is not None:
         o.tiny_max_n = tiny_max_n
+    if clean_method is not None:
+        o.clean_method = clean_method
     return o
 
 

@@ -35,11 +35,56 @@ static int id_bits(uint64_t n) {
 }
 
 // ------------------------------------------------------------------ a1: keys
+// Round 2: the a1 radix sort orders the keys by (min, h-bit hash of max) only, not by the
+// full (min, max): the key (min << b) | max is re-laid out BIJECTIVELY as
+//     [ high b - h bits of mix(max) | min (b bits) | low h bits of mix(max) ]
+// (mix = an invertible xorshift-multiply-xorshift on b bits) and the sort takes its low
+// b + h bits.  Equal edges stay equal and land in one RUN of equal (min, hash) -- the unique
+// step compares each key with the earlier keys of its run (runs of one min group of D arcs
+// average D / 2^h keys) -- and the output stays grouped by min (the degree atomics of the
+// min side aggregate per run, k_orient_pairs keeps its locality).  b + h is a multiple of 8
+// with h >= 11: 4 passes instead of 6 at s21 (b = 21), 5 instead of 6 at s24 and on the road
+// mesh.  h = 0: plain (min, max) order (tc_options.clean_method = 1, the round-1 sort).
+constexpr uint64_t kMixOdd = 0x9E3779B97F4A7C15ull;
+__device__ __forceinline__ uint64_t mix_inv_odd() {   // kMixOdd^-1 mod 2^64 (Newton)
+    uint64_t x = kMixOdd;
+#pragma unroll
+    for (int i = 0; i < 5; i++) x *= 2 - kMixOdd * x;
+    return x;
+}
+__device__ __forceinline__ uint64_t key_enc(uint64_t key, int b, int h) {
+    if (h == 0) return key;
+    const uint64_t mb = (1ull << b) - 1, s = (uint64_t)(b + 1) / 2;
+    uint64_t x = key & mb;
+    x ^= x >> s;
+    x = (x * kMixOdd) & mb;
+    x ^= x >> s;
+    const uint64_t mn = key >> b;
+    return ((x >> h) << (b + h)) | (mn << h) | (x & ((1ull << h) - 1));
+}
+__device__ __forceinline__ uint64_t key_dec(uint64_t k, int b, int h) {
+    if (h == 0) return k;
+    const uint64_t mb = (1ull << b) - 1, s = (uint64_t)(b + 1) / 2, mh = (1ull << h) - 1;
+    uint64_t x = ((k >> (b + h)) << h) | (k & mh);
+    x ^= x >> s;
+    x = (x * mix_inv_odd()) & mb;
+    x ^= x >> s;
+    return (((k >> h) & mb) << b) | x;
+}
+
+// Hash bits h of the a1 sort (0 = full order); the sort then takes b + h bits.
+static int clean_hash_bits(int b, uint32_t method) {
+    if (method != 0) return 0;
+    const int S = (b + 11 + 7) / 8 * 8, full = 2 * b;
+    const int dbf = radix_digit_bits(full), pf = (full + dbf - 1) / dbf;
+    return S < full && S / 8 < pf ? S - b : 0;
+}
+
 // (Fusing the radix digit histograms in here was measured slower than the separate
 // histogram pass: +0.13 ms against -0.09 ms at s21.)
 __global__ void __launch_bounds__(kTileThreads)
     k_clean_keys(const uint64_t *__restrict__ rowptr, const uint32_t *__restrict__ col, uint64_t n,
-                 uint64_t M, int b, uint64_t *__restrict__ keys) {
+                 uint64_t M, int b, int hb, uint64_t *__restrict__ keys) {
     __shared__ uint32_t s_row[kTileItems];
     __shared__ uint32_t s_scan[kTileThreads / 32];
     uint64_t t0 = (uint64_t)blockIdx.x * kTileItems;
@@ -50,7 +95,7 @@ __global__ void __launch_bounds__(kTileThreads)
         uint64_t key = ~0ull;  // self-loop: invalid, sorts last on the low 2b bits
         if (u != v) {
             uint64_t a = u < v ? u : v, c = u < v ? v : u;
-            key = (a << b) | c;
+            key = key_enc((a << b) | c, b, hb);
         }
         keys[t0 + i] = key;
     }
@@ -61,7 +106,7 @@ __global__ void __launch_bounds__(kTileThreads)
 // shares), compacted -- one atomic per tile, order free (the keys are sorted next).
 __global__ void __launch_bounds__(kTileThreads)
     k_clean_keys_shard(const uint64_t *__restrict__ rowptr, const uint32_t *__restrict__ col,
-                       uint64_t n, uint64_t M, int b, uint32_t rank, uint32_t world,
+                       uint64_t n, uint64_t M, int b, int hb, uint32_t rank, uint32_t world,
                        uint64_t *__restrict__ keys, uint64_t *__restrict__ count) {
     __shared__ uint32_t s_row[kTileItems];
     __shared__ uint32_t s_scan[kTileThreads / 32];
@@ -80,7 +125,7 @@ __global__ void __launch_bounds__(kTileThreads)
             const uint64_t u = s_row[i], v = col[t0 + i];
             const uint64_t a = u < v ? u : v, d = u < v ? v : u;
             if (u != v && a % world == rank) {
-                kk[k] = (a << b) | d;
+                kk[k] = key_enc((a << b) | d, b, hb);
                 c++;
             }
         }
@@ -96,122 +141,79 @@ __global__ void __launch_bounds__(kTileThreads)
 }
 
 // ------------------------------------------------------------------ a1: unique
-// Single pass (no separate count kernel + scan): tiles take a ticket, publish their unique
-// count, and get the exclusive prefix of earlier tiles by decoupled look-back (one
-// warp, 32 predecessors per step).  The last tile writes the total m.
-// Also a2 (fused): the degrees of the cleaned graph.  A thread's unique keys are
-// consecutive in (min, max) order, so the min side takes one atomic per run of equal
-// mins, the max side one per key.
-constexpr uint64_t kUqAgg = 1ull << 62, kUqPre = 2ull << 62, kUqMask = (1ull << 62) - 1;
-__device__ __forceinline__ void uq_st(uint64_t *p, uint64_t v) {
-    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t uq_ld(const uint64_t *p) {
-    uint64_t v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
+// One pass: a key is unique iff no EARLIER key of its run (equal sort bits, i.e. equal
+// (min, hash) -- or equal keys in the full order) is equal to it.  The output order is free
+// (every consumer of E -- orientation, pruning, tc_clean_shard -- takes any order), so each
+// tile takes its output offset with ONE atomic (round 2; round 1 kept the sorted order with a
+// decoupled look-back, whose chain made every tile wait for the slowest predecessor).
+// Also a2 (fused): the degrees of the cleaned graph.  A thread's unique keys are grouped by
+// min (the sort order), so the min side takes one atomic per run of equal mins, the max side
+// one per key.
 __global__ void __launch_bounds__(kTileThreads)
     k_unique_scatter(const uint64_t *__restrict__ keys, uint64_t M, const uint64_t *__restrict__ count_dev,
-                     uint32_t *__restrict__ ticket, uint64_t *__restrict__ status,
-                     uint64_t *__restrict__ m_out, uint64_t *__restrict__ out, int b,
+                     uint64_t *__restrict__ m_out, uint64_t *__restrict__ out, int b, int hb,
                      uint32_t *__restrict__ deg) {
     __shared__ uint32_t s_scan[kTileThreads / 32];
-    __shared__ uint32_t s_tile;
-    __shared__ uint64_t s_excl;
+    __shared__ uint64_t s_base;
     if (count_dev) {   // the keys are a compacted prefix (tc_clean_shard): tiles past it exit
         const uint64_t c = *count_dev;
         M = c < M ? c : M;
-        if (M == 0) {
-            if (blockIdx.x == 0 && threadIdx.x == 0) *m_out = 0;
-            return;
-        }
     }
-    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    if ((uint64_t)tile * kTileItems >= M) return;   // nobody waits on a tile past the keys
-    const uint64_t base = (uint64_t)tile * kTileItems + (uint64_t)threadIdx.x * kItemsPerThread;
-    uint32_t f[kItemsPerThread];
+    if ((uint64_t)blockIdx.x * kTileItems >= M) return;
+    const uint64_t base = (uint64_t)blockIdx.x * kTileItems + (uint64_t)threadIdx.x * kItemsPerThread;
     uint64_t kk[kItemsPerThread];
-    uint32_t c = 0;
+    bool dup[kItemsPerThread];
 #pragma unroll
     for (int k = 0; k < kItemsPerThread; k++) {
-        uint64_t i = base + k;
+        const uint64_t i = base + k;
         kk[k] = i < M ? keys[i] : ~0ull;
     }
-    {   // flags: the previous key of item 0 comes from global memory, the rest from registers
-        const uint64_t prev0 = base > 0 && base - 1 < M ? keys[base - 1] : ~1ull;
+    const uint64_t lowm = hb == 0 ? ~0ull : (1ull << (b + hb)) - 1;
+    // earlier keys of the same run among the thread's own items ...
 #pragma unroll
-        for (int k = 0; k < kItemsPerThread; k++) {
-            const uint64_t prev = k ? kk[k - 1] : prev0;
-            f[k] = base + k < M && kk[k] != ~0ull && (base + k == 0 || prev != kk[k]);
-            c += f[k];
+    for (int k = 0; k < kItemsPerThread; k++) {
+        dup[k] = false;
+#pragma unroll
+        for (int q = 0; q < k; q++) dup[k] |= kk[q] == kk[k];
+    }
+    // ... and before them: ONE backward walk over the run of item 0 (if it began earlier),
+    // compared with every item of that run
+    if (base > 0 && base < M && ((keys[base - 1] ^ kk[0]) & lowm) == 0) {
+        for (uint64_t j = base; j-- > 0;) {
+            const uint64_t pk = keys[j];
+            if (((pk ^ kk[0]) & lowm) != 0) break;
+#pragma unroll
+            for (int k = 0; k < kItemsPerThread; k++) dup[k] |= pk == kk[k];
         }
+    }
+    uint32_t f[kItemsPerThread], c = 0;
+#pragma unroll
+    for (int k = 0; k < kItemsPerThread; k++) {
+        f[k] = base + k < M && kk[k] != ~0ull && !dup[k];
+        c += f[k];
+        kk[k] = key_dec(kk[k], b, hb);   // (min << b) | max
     }
     uint32_t total;
-    uint32_t pos = block_exclusive_scan<SumOp>(c, s_scan, &total);
-    // degrees need no output offset: count them while warp 0 looks back
-    if (threadIdx.x >= 32) {
-        const uint64_t mask = (1ull << b) - 1;
-        uint32_t run_a = 0, run_n = 0;
+    const uint32_t pos = block_exclusive_scan<SumOp>(c, s_scan, &total);
+    if (threadIdx.x == 0) s_base = atomicAdd((unsigned long long *)m_out, (unsigned long long)total);
+    const uint64_t mask = (1ull << b) - 1;
+    uint32_t run_a = 0, run_n = 0;
 #pragma unroll
-        for (int k = 0; k < kItemsPerThread; k++)
-            if (f[k]) {
-                const uint32_t a = (uint32_t)(kk[k] >> b);
-                atomicAdd(&deg[kk[k] & mask], 1u);
-                if (run_n && a == run_a) {
-                    run_n++;
-                } else {
-                    if (run_n) atomicAdd(&deg[run_a], run_n);
-                    run_a = a;
-                    run_n = 1;
-                }
+    for (int k = 0; k < kItemsPerThread; k++)
+        if (f[k]) {
+            const uint32_t a = (uint32_t)(kk[k] >> b);
+            atomicAdd(&deg[kk[k] & mask], 1u);
+            if (run_n && a == run_a) {
+                run_n++;
+            } else {
+                if (run_n) atomicAdd(&deg[run_a], run_n);
+                run_a = a;
+                run_n = 1;
             }
-        if (run_n) atomicAdd(&deg[run_a], run_n);
-    }
-    if (threadIdx.x < 32) {   // warp 0: publish, look back, publish the inclusive prefix
-        const uint32_t lane = threadIdx.x;
-        if (lane == 0) uq_st(&status[tile], (tile == 0 ? kUqPre : kUqAgg) | total);
-        uint64_t excl = 0;
-        if (tile > 0) {
-            for (int64_t t = (int64_t)tile - 1;; t -= 32) {
-                const int64_t idx = t - (int64_t)lane;
-                uint64_t sw = idx >= 0 ? uq_ld(&status[idx]) : kUqPre;
-                while (__any_sync(0xffffffffu, (sw & ~kUqMask) == 0))
-                    if ((sw & ~kUqMask) == 0) sw = uq_ld(&status[idx]);
-                const uint32_t pre = __ballot_sync(0xffffffffu, (sw & kUqPre) != 0);
-                const int first = pre ? __ffs(pre) - 1 : 32;
-                excl += warp_sum_u64((int)lane <= first ? (sw & kUqMask) : 0ull);
-                if (pre) break;
-            }
-            if (lane == 0) uq_st(&status[tile], kUqPre | (excl + total));
         }
-        if (lane == 0) {
-            s_excl = excl;
-            if ((uint64_t)(tile + 1) * kTileItems >= M) *m_out = excl + total;   // last tile
-        }
-        // warp 0's own degrees, after its look-back
-        const uint64_t mask = (1ull << b) - 1;
-        uint32_t run_a = 0, run_n = 0;
-#pragma unroll
-        for (int k = 0; k < kItemsPerThread; k++)
-            if (f[k]) {
-                const uint32_t a = (uint32_t)(kk[k] >> b);
-                atomicAdd(&deg[kk[k] & mask], 1u);
-                if (run_n && a == run_a) {
-                    run_n++;
-                } else {
-                    if (run_n) atomicAdd(&deg[run_a], run_n);
-                    run_a = a;
-                    run_n = 1;
-                }
-            }
-        if (run_n) atomicAdd(&deg[run_a], run_n);
-    }
+    if (run_n) atomicAdd(&deg[run_a], run_n);
     __syncthreads();
-    uint64_t o = s_excl + pos;
+    uint64_t o = s_base + pos;
 #pragma unroll
     for (int k = 0; k < kItemsPerThread; k++)
         if (f[k]) out[o++] = kk[k];
@@ -385,35 +387,36 @@ static void pairs_to_csr(Ctx &ctx, uint64_t n, uint64_t cap, uint32_t *okey, uin
 // and the degrees they give both endpoints added into deg (zeroed by the caller).
 static void clean_arcs(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
                        int rank, int world, uint64_t *keys, uint64_t *keys_alt, uint64_t *&E,
-                       uint64_t *&m_dev, uint32_t *deg) {
+                       uint64_t *&m_dev, uint32_t *deg, uint32_t method) {
     const int b = id_bits(n);
+    const int hb = clean_hash_bits(b, method), sb = hb ? b + hb : 2 * b;
     const uint32_t tiles = (uint32_t)((M + kTileItems - 1) / kTileItems);
-    // status words [0, tiles), the ticket counter, m (the unique-edge count), the key count
-    uint64_t *uq = ctx.alloc<uint64_t>(tiles + 3);
-    TC_CUDA(cudaMemsetAsync(uq, 0, (tiles + 3) * sizeof(uint64_t), ctx.stream));
-    m_dev = uq + tiles + 1;
+    // m (the unique-edge count), the key count (sharded)
+    uint64_t *uq = ctx.alloc<uint64_t>(2);
+    TC_CUDA(cudaMemsetAsync(uq, 0, 2 * sizeof(uint64_t), ctx.stream));
+    m_dev = uq;
     const uint64_t *count = nullptr;
     if (world > 1) {
-        k_clean_keys_shard<<<tiles, kTileThreads, 0, ctx.stream>>>(rowptr, col, n, M, b, (uint32_t)rank,
-                                                                   (uint32_t)world, keys, uq + tiles + 2);
-        count = uq + tiles + 2;
+        k_clean_keys_shard<<<tiles, kTileThreads, 0, ctx.stream>>>(rowptr, col, n, M, b, hb, (uint32_t)rank,
+                                                                   (uint32_t)world, keys, uq + 1);
+        count = uq + 1;
     } else {
-        k_clean_keys<<<tiles, kTileThreads, 0, ctx.stream>>>(rowptr, col, n, M, b, keys);
+        k_clean_keys<<<tiles, kTileThreads, 0, ctx.stream>>>(rowptr, col, n, M, b, hb, keys);
     }
     TC_LAUNCHED(ctx);
-    bool alt = radix_sort(ctx, keys, keys_alt, M, count, 2 * b);
+    bool alt = radix_sort(ctx, keys, keys_alt, M, count, sb);
     uint64_t *sorted = alt ? keys_alt : keys;
     E = alt ? keys : keys_alt;
-    k_unique_scatter<<<tiles, kTileThreads, 0, ctx.stream>>>(sorted, M, count, (uint32_t *)(uq + tiles),
-                                                             uq, m_dev, E, b, deg);
+    k_unique_scatter<<<tiles, kTileThreads, 0, ctx.stream>>>(sorted, M, count, m_dev, E, b, hb, deg);
     TC_LAUNCHED(ctx);
 }
 
 void clean_shard(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
-                 int rank, int world, uint64_t *edges, uint32_t *deg, uint64_t *m_dev_out) {
+                 int rank, int world, uint64_t *edges, uint32_t *deg, uint64_t *m_dev_out,
+                 uint32_t method) {
     uint64_t *alt = ctx.alloc<uint64_t>(M), *E = nullptr, *m_dev = nullptr;
     // keys are sorted in `edges` / `alt`; the unique edges end up in the other one
-    clean_arcs(ctx, n, M, rowptr, col, rank, world, edges, alt, E, m_dev, deg);
+    clean_arcs(ctx, n, M, rowptr, col, rank, world, edges, alt, E, m_dev, deg, method);
     if (E != edges) {
         uint64_t m = 0;
         TC_CUDA(cudaMemcpyAsync(&m, m_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx.stream));
@@ -425,14 +428,14 @@ void clean_shard(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const
 
 void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
                   Oriented &out, Timer *tm,
-                  PruneInfo &prune, bool id_order) {
+                  PruneInfo &prune, bool id_order, uint32_t method) {
     phase_begin(tm, kClean);
     uint64_t *keys = ctx.alloc<uint64_t>(M);
     uint64_t *keys_alt = ctx.alloc<uint64_t>(M);
     uint32_t *deg = ctx.alloc<uint32_t>(n);
     TC_CUDA(cudaMemsetAsync(deg, 0, n * sizeof(uint32_t), ctx.stream));
     uint64_t *E = nullptr, *m_dev = nullptr;
-    clean_arcs(ctx, n, M, rowptr, col, 0, 1, keys, keys_alt, E, m_dev, deg);
+    clean_arcs(ctx, n, M, rowptr, col, 0, 1, keys, keys_alt, E, m_dev, deg, method);
     phase_end(tm, kClean);
     orient_edges(ctx, n, M, E, m_dev, deg, out, tm, prune, id_order, keys, keys_alt);
 }

@@ -201,7 +201,7 @@ static void run(Call &c) {
         uint64_t *m_dev = ctx.alloc<uint64_t>(1);
         TC_CUDA(cudaMemsetAsync(m_dev, 0, sizeof(uint64_t), ctx.stream));
         if (c.n && c.M) clean_shard(ctx, c.n, c.M, c.rowptr, c.col, c.rank, c.world, c.edges_out,
-                                    c.deg_out, m_dev);
+                                    c.deg_out, m_dev, c.opt.clean_method);
         uint64_t *pin = pinned_scratch();
         TC_CUDA(cudaMemcpyAsync(pin + 27, m_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx.stream));
         ctx.release();
@@ -327,7 +327,7 @@ static void run(Call &c) {
                          prune, c.flags & TC_ID_ORDER);
         else
             orient_dirty(ctx, c.n, c.M, rowptr, col, g, tm,
-                         prune, c.flags & TC_ID_ORDER);
+                         prune, c.flags & TC_ID_ORDER, c.opt.clean_method);
         if (g.claim_err && (c.mode != kShard || c.stats))   // read at the final synchronisation
             TC_CUDA(cudaMemcpyAsync(pin + 26, g.claim_err, sizeof(uint32_t), cudaMemcpyDeviceToHost,
                                     ctx.stream));

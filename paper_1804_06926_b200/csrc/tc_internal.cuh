@@ -378,7 +378,7 @@ struct PruneInfo {
     const uint64_t *m_before = nullptr;  // device scalar (dirty path)
     uint64_t m_before_host = 0;          // clean path: arcs / 2
 };
-// Dirty path: E (sorted (min << b | max) keys, *m_dev of them), deg = degrees of E.
+// Dirty path: E (unique (min << b | max) keys, any order, *m_dev of them), deg = degrees of E.
 // On return E / m_dev / deg describe the pruned graph (E compacted).
 void prune_pairs(Ctx &ctx, uint64_t n, int b, uint32_t rounds, uint64_t *&E, uint64_t *&m_dev,
                  uint32_t *&deg, uint64_t m_host_cap, PruneInfo &info);
@@ -388,18 +388,20 @@ void prune_csr(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const u
                uint32_t rounds, uint32_t *&deg, PruneInfo &info);
 
 // a1 (dirty input) + a2 + a3 + a4: raw CSR -> oriented relabelled CSR, rows ascending.
+// method: tc_options.clean_method (0 = hashed sort order, 1 = full (min, max) order).
 void orient_dirty(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
                   Oriented &out, Timer *tm,
-                  PruneInfo &prune, bool id_order);
+                  PruneInfo &prune, bool id_order, uint32_t method);
 // a2 + a3 + a4 from unique undirected edges E (keys (min << b) | max, b = id bits of n, any
 // order; m_dev of them, at most M) and their graph's degrees deg (both kept by the caller).
 void orient_edges(Ctx &ctx, uint64_t n, uint64_t M, uint64_t *E, uint64_t *m_dev, uint32_t *deg,
                   Oriented &out, Timer *tm, PruneInfo &prune, bool id_order,
                   void *free0 = nullptr, void *free1 = nullptr);
 // tc_clean_shard: a1 on the arcs of this rank's edges (min endpoint mod world == rank): the
-// unique edges, sorted, into edges[0, *m_dev_out) and their degrees added into deg.
+// unique edges (any order) into edges[0, *m_dev_out) and their degrees added into deg.
 void clean_shard(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
-                 int rank, int world, uint64_t *edges, uint32_t *deg, uint64_t *m_dev_out);
+                 int rank, int world, uint64_t *edges, uint32_t *deg, uint64_t *m_dev_out,
+                 uint32_t method);
 // a2 + a3 + a4 for clean symmetric input.
 void orient_clean(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,
                   Oriented &out, Timer *tm,
