@@ -243,6 +243,66 @@ tc_status tc_count_edges_shard(uint64_t n, uint64_t m_edges, const uint64_t *edg
                                int rank, int world, uint64_t *partial_dev,
                                uint64_t *per_vertex_partial, tc_stats *stats);
 
+/* ---- Sharded pipeline (round 2): a2-a5 split over the ranks as well (north_star
+ * "the edge range is split by a prefix sum over estimated intersection work, followed by one
+ * NCCL allreduce of the 64-bit count").  After tc_clean_shard + the degree all-reduce, each
+ * rank runs the six phases below; between them the CALLER runs the collective named in
+ * brackets (paper_1804_06926_b200/dist.py: NCCL; shard.py: a one-GPU emulation).  All
+ * pointers are device pointers on the current device unless marked host; outputs are
+ * caller-owned and overwritten; every phase is synchronous.  world <= 64; n < 2^32 and fewer
+ * than 2^31 oriented edges; force_variant must be AUTO.  Summing the ranks' partials gives
+ * tc_count's total (and, with TC_PER_VERTEX, its t(v)) exactly.
+ *
+ * tc_shard_orient: newid (n) = the rank relabelling of Alg. 2 (rank = (d, id)) from
+ *   the summed degrees; the rank's own unique edges (tc_clean_shard's) oriented low -> high
+ *   rank as (src[i], dst[i]) rank ids; dplus (n) = the d+ they contribute.  Flags: TC_ID_ORDER.
+ *   [all-reduce dplus] */
+tc_status tc_shard_orient(uint64_t n, uint64_t m_local, const uint64_t *edges, const uint32_t *degrees,
+                          uint32_t flags, const tc_options *opt, uint32_t *newid, uint32_t *src,
+                          uint32_t *dst, uint32_t *dplus);
+/* tc_shard_partition: off_plus (n+1) = the exclusive scan of the summed dplus (the oriented
+ *   CSR's row offsets, identical on every rank); row range q = rank ids [row_bounds[q],
+ *   row_bounds[q+1]) holding about m/world edges, col+ positions [col_bounds[q], col_bounds[q+1])
+ *   (host arrays, world+1 entries); pairs_out (m_local, int64 src | dst << 32) = the rank's pairs
+ *   grouped by the range of their source, send_counts (host, world) per range.
+ *   [all-to-all of the pairs by send_counts] */
+tc_status tc_shard_partition(uint64_t n, uint64_t m_local, const uint32_t *src, const uint32_t *dst,
+                             const uint32_t *dplus, const tc_options *opt, int rank, int world,
+                             uint64_t *off_plus, uint64_t *pairs_out, uint64_t *send_counts,
+                             uint64_t *row_bounds, uint64_t *col_bounds);
+/* tc_shard_rows: the m_recv received pairs (exactly the rows of this rank's range) sorted by
+ *   (source, target) into col_plus[col_begin, col_begin + m_recv): rows ascending (a3 + a4).
+ *   [all-gather: each rank's col+ range to every rank] */
+tc_status tc_shard_rows(uint64_t n, uint64_t m_recv, const uint64_t *pairs, const tc_options *opt,
+                        uint64_t col_begin, uint32_t *col_plus);
+/* tc_shard_work: a5 on the oriented edges [e_begin, e_end) (this rank's rows of the full
+ *   off_plus / col_plus): ent_cnt (n) / ent_len (n, uint64) = per HASH owner the probe entries
+ *   and probe lengths these edges give it (bin.cu's rule: owner = target if |N+(u) after x| <=
+ *   d+(x), else source).  Flags: TC_PER_VERTEX (then the dense core is off).
+ *   [all-reduce ent_cnt and ent_len] */
+tc_status tc_shard_work(uint64_t n, const uint64_t *off_plus, const uint32_t *col_plus, const uint32_t *dplus,
+                        uint32_t flags, const tc_options *opt, uint64_t e_begin, uint64_t e_end,
+                        uint32_t *ent_cnt, uint64_t *ent_len);
+/* tc_shard_route: owner work w(x) from the summed entries / lengths (the single-GPU owner
+ *   split's model), its exclusive prefix, owner x -> rank split_rank(prefix(x)); entries_out =
+ *   the HASH probe entries of edges [e_begin, e_end) grouped by their owner's rank, three
+ *   uint32 each (owner, other endpoint, CSR index | out-part flag << 31), send_counts (host,
+ *   world) entries per rank.  Same flags as tc_shard_work.  [all-to-all of the entries] */
+tc_status tc_shard_route(uint64_t n, const uint64_t *off_plus, const uint32_t *col_plus, const uint32_t *dplus,
+                         const uint32_t *ent_cnt, const uint64_t *ent_len, uint32_t flags,
+                         const tc_options *opt, int rank, int world, uint64_t e_begin, uint64_t e_end,
+                         uint32_t *entries_out, uint64_t *send_counts);
+/* tc_shard_count: a6 + a7 of this rank: its HASH owners' tables probed with the n_entries
+ *   received entries, the SHORT / SEARCH edges of [e_begin, e_end), the dense-core edges of its
+ *   interleaved 2048-edge blocks (count mode).  *partial_dev (uint64) = its share; with
+ *   TC_PER_VERTEX (needs newid) per_vertex_partial (n, input ids) = its t(v) shares.  m = the
+ *   oriented edge count (off_plus[n]).  [all-reduce partial_dev (and per_vertex_partial)] */
+tc_status tc_shard_count(uint64_t n, uint64_t m, const uint64_t *off_plus, const uint32_t *col_plus,
+                         const uint32_t *dplus, const uint32_t *newid, uint64_t n_entries,
+                         const uint32_t *entries, uint32_t flags, const tc_options *opt, int rank,
+                         int world, uint64_t e_begin, uint64_t e_end, uint64_t *partial_dev,
+                         uint64_t *per_vertex_partial);
+
 /* Steps a1-a4 only ("Form_Filtered_Edge_List", Alg. 2): writes the
  * oriented, compacted CSR N+ (off_plus: n+1 entries; col_plus: capacity m
  * entries, first m_plus used; each row ascending) and *m_plus (host).

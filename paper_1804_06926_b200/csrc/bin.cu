@@ -446,7 +446,7 @@ __global__ void k_task_expand(const uint32_t *__restrict__ owners, const uint64_
     }
 }
 
-static void make_tasks(Ctx &ctx, uint64_t n, uint64_t cap, const uint32_t *owners,
+void make_tasks(Ctx &ctx, uint64_t n, uint64_t cap, const uint32_t *owners,
                        const uint64_t *ocount, const uint32_t *pcnt, const HashParams &hp,
                        uint32_t L, uint64_t *tloads, uint4 *&tasks, uint64_t *&ntasks) {
     uint32_t *tcnt = ctx.alloc<uint32_t>(n);

@@ -132,13 +132,23 @@ __global__ void __launch_bounds__(256)
     (void)m;
 }
 
+// Core size K and first core rank id: the top K = 16384 ranks below 2^23 vertices, 32768
+// from there on (rounded to whole 128-id groups for small n).
+static uint32_t core_size(uint32_t n) {
+    const uint32_t cap = n < (1u << 23) ? TC_CORE_SMALL : kCoreMax;
+    return (uint32_t)std::min<uint64_t>(cap, ((uint64_t)n + 127) / 128 * 128);
+}
+uint32_t core_first(uint64_t n) {
+    const uint32_t K = core_size((uint32_t)n);
+    return n > K ? (uint32_t)n - K : 0u;
+}
+
 void core_build(Ctx &ctx, const Oriented &g, HashParams &hp) {
     hp.core = nullptr;
     const uint32_t n = (uint32_t)g.n;
     if (n == 0) return;
-    const uint32_t cap = n < (1u << 23) ? TC_CORE_SMALL : kCoreMax;
-    const uint32_t K = std::min<uint64_t>(cap, ((uint64_t)n + 127) / 128 * 128);
-    hp.core_lo = n > K ? n - K : 0u;
+    const uint32_t K = core_size(n);
+    hp.core_lo = core_first(n);
     hp.core_words = K / 32;
     uint32_t *bm = ctx.alloc<uint32_t>((uint64_t)K * hp.core_words);
     uint4 *info = ctx.alloc<uint4>(K);

@@ -291,6 +291,12 @@ static void rank_permutation(Ctx &ctx, uint64_t n, const uint32_t *deg, Oriented
     (void)grid;
 }
 
+void rank_relabel(Ctx &ctx, uint64_t n, const uint32_t *deg, bool id_order, uint32_t *newid_out) {
+    Oriented o;
+    rank_permutation(ctx, n, rank_key(ctx, n, deg, id_order), o);
+    TC_CUDA(cudaMemcpyAsync(newid_out, o.newid, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, ctx.stream));
+}
+
 // d-(x) = d(x) - d+(x), in rank ids.
 // Also sum_v d-(v) d+(v) (stats: SURVEY 8(d)'s B_stage) into *stage, one atomic per warp.
 __global__ void k_dminus(const uint32_t *__restrict__ deg, const uint32_t *__restrict__ newid,

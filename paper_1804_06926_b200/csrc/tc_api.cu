@@ -538,6 +538,45 @@ static tc_options resolve(const tc_options *opt) {
     return o;
 }
 
+// The phase entry points of shard.cu: options resolved and checked, workspace (hook or the
+// library pool) and stream set up, fn run, every exception mapped to a tc_status.  fn ends
+// with whatever synchronisation its outputs need.
+tc_status run_phase(const tc_options *opt_in, const std::function<void(Ctx &, const tc_options &)> &fn) {
+    const tc_options opt = resolve(opt_in);
+    for (uint32_t r : opt.reserved)
+        if (r) return set_error("tc_options.reserved must be zero"), TC_EINVAL;
+    if (!opt.alloc != !opt.free)
+        return set_error("tc_options.alloc and .free must be given together"), TC_EINVAL;
+    try {
+        Ctx ctx;
+        TC_CUDA(cudaGetDevice(&ctx.device));
+        ctx.stream = (cudaStream_t)opt.stream;
+        DeviceState &ds = device_state(ctx.device);
+        ctx.num_sms = ds.sms;
+        if (opt.alloc) {
+            ctx.hook_alloc = opt.alloc;
+            ctx.hook_free = opt.free;
+            ctx.hook_ctx = opt.alloc_ctx;
+        } else {
+            ctx.pool = ds.pool;
+            set_pool_keep(ds.pool, opt.keep_workspace != 0);
+        }
+        fn(ctx, opt);
+        ctx.release();
+        TC_CUDA(cudaStreamSynchronize(ctx.stream));
+    } catch (const Error &e) {
+        set_error(e.msg);
+        return e.status;
+    } catch (const std::bad_alloc &) {
+        set_error("host allocation failed");
+        return TC_ENOMEM;
+    }
+    set_error("");
+    return TC_OK;
+}
+
+void check_device(const void *p, int dev, const char *what) { check_device_ptr(p, dev, what); }
+
 }  // namespace tc
 
 using namespace tc;

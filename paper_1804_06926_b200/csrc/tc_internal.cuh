@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -519,6 +520,8 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins);
 // Dense core (core.cu): builds the adjacency bitmaps of the top-ranked vertices into
 // hp.core / core_lo / core_words (count mode only; a no-op when the graph is empty).
 void core_build(Ctx &ctx, const Oriented &g, HashParams &hp);
+// First rank id of the dense core (the same rule as core_build).
+uint32_t core_first(uint64_t n);
 // a6 + a7 for the core edges (plain count): popc of bitmap ANDs, added into total_dev.
 void core_count(Ctx &ctx, const Oriented &g, const HashParams &hp, uint64_t *total_dev,
                 uint64_t *words_dev, cudaStream_t stream);
@@ -544,6 +547,16 @@ void intersect_all(Ctx &ctx, const Oriented &g, const Bins &bins, uint64_t *tota
 constexpr uint64_t kTinyMaxN = 1024;
 void tiny_count(Ctx &ctx, uint64_t n, const uint64_t *rowptr, const uint32_t *col,
                 uint64_t *total_dev, uint64_t *pv_dev, uint64_t *m_dev);
+
+// Multi-GPU phases (shard.cu): tc_api.cu's option / workspace / error wrapper.
+tc_status run_phase(const tc_options *opt, const std::function<void(Ctx &, const tc_options &)> &fn);
+void check_device(const void *p, int dev, const char *what);   // TC_EINVAL unless on `dev`
+// rank relabelling (a2): newid_out[v] = rank position of v (orient.cu)
+void rank_relabel(Ctx &ctx, uint64_t n, const uint32_t *deg, bool id_order, uint32_t *newid_out);
+// Tasks of an owner list (bin.cu): ceil(pcnt / L) per owner, their records, *ntasks.
+void make_tasks(Ctx &ctx, uint64_t n, uint64_t cap, const uint32_t *owners, const uint64_t *ocount,
+                const uint32_t *pcnt, const HashParams &hp, uint32_t L, uint64_t *tloads,
+                uint4 *&tasks, uint64_t *&ntasks);
 
 // Validation (TC_VALIDATE); returns a TC_EGRAPH message or "".
 std::string validate_graph(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr,
