@@ -45,8 +45,11 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-next", action="store_true", help="skip the NEXT-row measurements")
     ap.add_argument("--replicated-a1", action="store_true",
-                    help="N > 1: every rank cleans all arcs (default: the cleaning step is split "
-                         "over the ranks, tc_clean_shard + one all-reduce + one all-gather)")
+                    help="N > 1: every rank runs a1-a5 on the whole graph, tc_count_shard (round 1)")
+    ap.add_argument("--sharded-a1-only", action="store_true",
+                    help="N > 1: only the cleaning step split over the ranks (tc_clean_shard, "
+                         "all-gather of the edges, tc_count_edges_shard); default: a1-a5 all "
+                         "sharded (shard.py / csrc/shard.cu)")
     ap.add_argument("--one-call", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--clean-input", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--no-ncu", action="store_true",
@@ -424,8 +427,9 @@ def main():
 
     import torch
     import paper_1804_06926_b200 as tc
-    from paper_1804_06926_b200.dist import (count_distributed, count_distributed_sharded_a1,
-                                            exchange_clean_shards)
+    from paper_1804_06926_b200.dist import (Comm, count_distributed, count_distributed_sharded,
+                                            count_distributed_sharded_a1, exchange_clean_shards)
+    from paper_1804_06926_b200.shard import run_rank
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
@@ -437,10 +441,30 @@ def main():
     cl = torch.from_numpy(g.col.view(np.int32)).to(dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     partial = torch.zeros(1, dtype=torch.int64, device=dev)
+    mode = "single" if world == 1 else ("replicated" if args.replicated_a1 else
+                                        ("sharded-a1" if args.sharded_a1_only else "sharded"))
+    comm = Comm() if world > 1 else None
+    base_st = None
+    if mode == "sharded":
+        # the graph's byte model and sizes (B_a6, m, W: properties of the whole graph, the same
+        # on every rank) from one single-GPU call outside the timed region
+        base_st = tc.count_ex(rp, cl, with_stats=True)[1]
 
     def step(with_stats=False):
         if world == 1:
             return tc.count_ex(rp, cl, with_stats=with_stats)
+        if mode == "sharded":   # a1-a5 split over the ranks too (shard.py run_rank)
+            times = {} if with_stats else None
+            part, _ = run_rank(rp, cl, rank, world, comm, times=times)
+            comm.all_reduce(part)
+            T = int(part.item())
+            if not with_stats:
+                return T
+            st = dict(base_st)
+            st.update(ms_clean=times["clean"], ms_orient=times["orient"] + times["partition"] + times["rows"],
+                      ms_sort=0.0, ms_bin=times["work"] + times["route"], ms_intersect=times["count"],
+                      ms_total=sum(times.values()), ms_collectives=times["comm"])
+            return T, st
         if args.replicated_a1:   # every rank cleans all arcs (SURVEY §8(e) as written)
             st = tc.count_shard(rp, cl, rank, world, partial, with_stats=with_stats)
         else:                    # the cleaning step split over the ranks (dist.py)
@@ -463,6 +487,7 @@ def main():
     torch.cuda.synchronize()
     sampler.start()
     T_total = None
+    launches0 = tc.launches_issued()
     for k in range(args.steps):
         flush.fill_(k & 0xff)
         ev[k][0].record(stream)
@@ -471,6 +496,7 @@ def main():
         T_total, st = out
         stats.append(st)
     torch.cuda.synchronize()
+    launches = tc.launches_issued() - launches0   # this rank's kernels in the timed region
     if dist is not None:
         dist.barrier()
     clocks = sampler.stop()
@@ -483,14 +509,16 @@ def main():
     # a6 algorithmic bytes of the implemented method: HASH probes + ranges + table loads, plus
     # the dense-core path's word ANDs (8 bytes per word pair)
     b_hash, b_alg_rank = st["bytes_hash"] + st["bytes_core"], st["bytes_alg"]
-    launches = st["kernel_launches"] * args.steps
     if dist is not None:
         t = torch.tensor([ms, ix_ms, bin_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, ix_ms, bin_ms = t.tolist()
-        c = torch.tensor([b_hash, launches], dtype=torch.int64, device=dev)
+        # per-rank byte counts sum to the graph's; the sharded mode already has the whole graph's
+        c = torch.tensor([b_hash if mode != "sharded" else 0, launches], dtype=torch.int64, device=dev)
         dist.all_reduce(c)
-        b_hash, launches = (int(x) for x in c.tolist())
+        if mode != "sharded":
+            b_hash = int(c[0].item())
+        launches = int(c[1].item())
     m = st["m_undirected"]
 
     # ---- end to end through the public API from pinned HOST buffers: every step copies the
@@ -506,9 +534,11 @@ def main():
                 return tc.count_ex(rp_h, cl_h, with_stats=True)[0]
             d_rp = rp_h.to(dev, non_blocking=True)
             d_cl = cl_h.to(dev, non_blocking=True)
-            if args.replicated_a1:
+            if mode == "replicated":
                 return count_distributed(d_rp, d_cl)
-            return count_distributed_sharded_a1(d_rp, d_cl)
+            if mode == "sharded-a1":
+                return count_distributed_sharded_a1(d_rp, d_cl)
+            return count_distributed_sharded(d_rp, d_cl)
 
         e2e_step()   # warm
         reps = max(3, min(args.steps, 5))
@@ -527,7 +557,7 @@ def main():
         e2e = {"value": m / e2e_s, "unit": "edges/s", "ms_per_step": 1e3 * e2e_s,
                "h2d_bytes_per_step": in_bytes * world, "d2h_bytes_per_step": 8 * world,
                "note": ("tc_count_ex with TC_HOST_PTRS from pinned host memory" if world == 1 else
-                        "count_distributed[_sharded_a1]: per rank H2D of the raw CSR (non_blocking "
+                        "count_distributed[_sharded[_a1]]: per rank H2D of the raw CSR (non_blocking "
                         "from pinned), the same path as the step, .item()") +
                        "; host wall clock per step, max over ranks"}
 
@@ -574,13 +604,21 @@ def main():
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (seeded R-MAT, Graph500 A,B,C,D=.57,.19,.19,.05; raw arcs)",
         "config": {"workload": g.name, "n": g.n, "m": m, "raw_arcs": g.arcs, "T": T_total,
-                   "parallelism": (f"dp{world}: replicated input, owner-split intersection"
-                                   + ("" if world == 1 or args.replicated_a1 else ", sharded cleaning")),
+                   "parallelism": (f"dp{world}: replicated input, owner-split intersection" +
+                                   {"single": "", "replicated": ", a1-a5 replicated",
+                                    "sharded-a1": ", sharded cleaning, a2-a5 replicated",
+                                    "sharded": ", a1-a5 sharded (row-range CSR slices, all-gathered; "
+                                               "HASH entries routed to their owner's rank)"}[mode]),
                    "l2": "flushed between timed steps (512 MiB write outside the event spans)",
                    "step": "tc_count_ex on raw arcs: clean, orient, bin, intersect, reduce"
-                           + ((" (tc_count_shard per rank) + NCCL allreduce" if args.replicated_a1 else
-                               " (tc_clean_shard per rank, NCCL all-reduce of degrees + all-gather of "
-                               "edges, tc_count_edges_shard, NCCL allreduce)") if world > 1 else "")},
+                           + ({"single": "",
+                               "replicated": " (tc_count_shard per rank) + NCCL allreduce",
+                               "sharded-a1": " (tc_clean_shard per rank, NCCL all-reduce of degrees + "
+                                             "all-gather of edges, tc_count_edges_shard, NCCL allreduce)",
+                               "sharded": " (shard.py run_rank: tc_clean_shard / tc_shard_orient / "
+                                          "partition / rows / work / route / count per rank between "
+                                          "NCCL all-reduce, all-to-all and broadcast collectives, then "
+                                          "the count all-reduce)"}[mode])},
         "phases_ms": {k: sum(s[k] for s in stats) / len(stats)
                       for k in ("ms_clean", "ms_orient", "ms_sort", "ms_bin", "ms_intersect", "ms_total")},
         "step_ms_min_max": [min(step_ms), max(step_ms)],

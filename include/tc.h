@@ -275,26 +275,30 @@ tc_status tc_shard_partition(uint64_t n, uint64_t m_local, const uint32_t *src, 
  *   [all-gather: each rank's col+ range to every rank] */
 tc_status tc_shard_rows(uint64_t n, uint64_t m_recv, const uint64_t *pairs, const tc_options *opt,
                         uint64_t col_begin, uint32_t *col_plus);
-/* tc_shard_work: a5 on the oriented edges [e_begin, e_end) (this rank's rows of the full
- *   off_plus / col_plus): ent_cnt (n) / ent_len (n, uint64) = per HASH owner the probe entries
- *   and probe lengths these edges give it (bin.cu's rule: owner = target if |N+(u) after x| <=
- *   d+(x), else source).  Flags: TC_PER_VERTEX (then the dense core is off).
- *   [all-reduce ent_cnt and ent_len] */
+/* tc_shard_work: a5 on this rank's rows [row_begin, row_end) = oriented edges [e_begin, e_end)
+ *   (only this rank's slice of col_plus is read, so the col+ all-gather may still be in
+ *   flight): ent_cnt (n) / ent_len (n, uint64) = per HASH owner the probe entries and probe
+ *   lengths these edges give it (bin.cu's rule: owner = target if |N+(u) after x| <= d+(x),
+ *   else source); spans (n) = last - first + 1 of N+(x) for its rows, 0 elsewhere.  Flags:
+ *   TC_PER_VERTEX (then the dense core is off).  [all-reduce ent_cnt, ent_len, spans] */
 tc_status tc_shard_work(uint64_t n, const uint64_t *off_plus, const uint32_t *col_plus, const uint32_t *dplus,
-                        uint32_t flags, const tc_options *opt, uint64_t e_begin, uint64_t e_end,
-                        uint32_t *ent_cnt, uint64_t *ent_len);
-/* tc_shard_route: owner work w(x) from the summed entries / lengths (the single-GPU owner
- *   split's model), its exclusive prefix, owner x -> rank split_rank(prefix(x)); entries_out =
- *   the HASH probe entries of edges [e_begin, e_end) grouped by their owner's rank, three
- *   uint32 each (owner, other endpoint, CSR index | out-part flag << 31), send_counts (host,
- *   world) entries per rank.  Same flags as tc_shard_work.  [all-to-all of the entries] */
+                        uint32_t flags, const tc_options *opt, uint64_t row_begin, uint64_t row_end,
+                        uint64_t e_begin, uint64_t e_end, uint32_t *ent_cnt, uint64_t *ent_len,
+                        uint32_t *spans);
+/* tc_shard_route: owner work w(x) from the summed entries / lengths / spans (the single-GPU
+ *   owner split's model), its exclusive prefix, owner x -> rank split_rank(prefix(x));
+ *   entries_out = the HASH probe entries of edges [e_begin, e_end) grouped by their owner's rank,
+ *   three uint32 each (owner, other endpoint, CSR index | out-part flag << 31), with this rank's
+ *   SHORT / SEARCH edges routed to itself (owner field = source | 1 << 31, then the target, the
+ *   CSR index | SEARCH flag << 31); send_counts (host, world) entries per rank.  Reads only this
+ *   rank's slice of col_plus.  Same flags as tc_shard_work.  [all-to-all of the entries] */
 tc_status tc_shard_route(uint64_t n, const uint64_t *off_plus, const uint32_t *col_plus, const uint32_t *dplus,
-                         const uint32_t *ent_cnt, const uint64_t *ent_len, uint32_t flags,
+                         const uint32_t *ent_cnt, const uint64_t *ent_len, const uint32_t *spans, uint32_t flags,
                          const tc_options *opt, int rank, int world, uint64_t e_begin, uint64_t e_end,
                          uint32_t *entries_out, uint64_t *send_counts);
-/* tc_shard_count: a6 + a7 of this rank: its HASH owners' tables probed with the n_entries
- *   received entries, the SHORT / SEARCH edges of [e_begin, e_end), the dense-core edges of its
- *   interleaved 2048-edge blocks (count mode).  *partial_dev (uint64) = its share; with
+/* tc_shard_count: a6 + a7 of this rank (needs the whole col_plus): its HASH owners' tables
+ *   probed with the n_entries received entries, its SHORT / SEARCH edges (received from itself),
+ *   the dense-core edges of its interleaved 2048-edge blocks (count mode); n < 2^30.  *partial_dev (uint64) = its share; with
  *   TC_PER_VERTEX (needs newid) per_vertex_partial (n, input ids) = its t(v) shares.  m = the
  *   oriented edge count (off_plus[n]).  [all-reduce partial_dev (and per_vertex_partial)] */
 tc_status tc_shard_count(uint64_t n, uint64_t m, const uint64_t *off_plus, const uint32_t *col_plus,
@@ -384,6 +388,10 @@ tc_status tc_masked_spgemm(uint64_t n, uint64_t m, const uint64_t *row_offsets,
                            uint64_t *nnz_u, uint64_t *total, tc_stats *stats);
 
 /* Thread-local message describing the last failure on this thread ("" if none). */
+/* Kernels launched so far by the calls made from this thread (all entry points; a
+ * monotone counter for launch accounting, e.g. bench.py's gpu_launches). */
+uint64_t tc_launches_issued(void);
+
 const char *tc_last_error(void);
 
 /* Return the library pool's cached workspace on `device` (-1 = current device) to the

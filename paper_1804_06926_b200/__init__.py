@@ -168,6 +168,8 @@ def _load():
     lib.tc_masked_spgemm.restype = ctypes.c_int
     lib.tc_last_error.argtypes = []
     lib.tc_last_error.restype = ctypes.c_char_p
+    lib.tc_launches_issued.argtypes = []
+    lib.tc_launches_issued.restype = ctypes.c_uint64
     lib.tc_trim_workspace.argtypes = [ctypes.c_int]
     lib.tc_trim_workspace.restype = ctypes.c_int
     lib.tc_version.argtypes = []
@@ -536,3 +538,8 @@ def trim_workspace(device: int = -1) -> None:
 
 def version() -> str:
     return _load().tc_version().decode()
+
+
+def launches_issued() -> int:
+    """tc_launches_issued: kernels launched so far by this thread's library calls."""
+    return int(_load().tc_launches_issued())

@@ -401,20 +401,28 @@ static void clean_arcs(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr,
     uint64_t *uq = ctx.alloc<uint64_t>(2);
     TC_CUDA(cudaMemsetAsync(uq, 0, 2 * sizeof(uint64_t), ctx.stream));
     m_dev = uq;
-    const uint64_t *count = nullptr;
+    uint64_t mk = M;   // keys to sort
     if (world > 1) {
         k_clean_keys_shard<<<tiles, kTileThreads, 0, ctx.stream>>>(rowptr, col, n, M, b, hb, (uint32_t)rank,
                                                                    (uint32_t)world, keys, uq + 1);
-        count = uq + 1;
+        TC_LAUNCHED(ctx);
+        // this rank's share of the keys, read back so the sort and the unique step launch exactly
+        // its tiles (a capacity-M launch spent ~0.4 ms per radix pass at s24, world 8, on tail
+        // tiles that only exit); tc_clean_shard is synchronous anyway
+        TC_CUDA(cudaMemcpyAsync(&mk, uq + 1, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx.stream));
+        TC_CUDA(cudaStreamSynchronize(ctx.stream));
     } else {
         k_clean_keys<<<tiles, kTileThreads, 0, ctx.stream>>>(rowptr, col, n, M, b, hb, keys);
+        TC_LAUNCHED(ctx);
     }
-    TC_LAUNCHED(ctx);
-    bool alt = radix_sort(ctx, keys, keys_alt, M, count, sb);
+    bool alt = radix_sort(ctx, keys, keys_alt, mk, nullptr, sb);
     uint64_t *sorted = alt ? keys_alt : keys;
     E = alt ? keys : keys_alt;
-    k_unique_scatter<<<tiles, kTileThreads, 0, ctx.stream>>>(sorted, M, count, m_dev, E, b, hb, deg);
-    TC_LAUNCHED(ctx);
+    const uint32_t utiles = (uint32_t)((mk + kTileItems - 1) / kTileItems);
+    if (utiles) {
+        k_unique_scatter<<<utiles, kTileThreads, 0, ctx.stream>>>(sorted, mk, nullptr, m_dev, E, b, hb, deg);
+        TC_LAUNCHED(ctx);
+    }
 }
 
 void clean_shard(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, const uint32_t *col,

@@ -184,7 +184,7 @@ __device__ __forceinline__ int slice_kind(const SliceParams &sp, uint32_t u, uin
 template <int kMode>
 __global__ void __launch_bounds__(kTileThreads)
     k_slice(SliceParams sp, uint64_t e0, uint64_t e1, uint32_t *__restrict__ cnt,
-            unsigned long long *__restrict__ len, const uint64_t *__restrict__ wprefix, int G,
+            unsigned long long *__restrict__ len, const uint64_t *__restrict__ wprefix, int G, int self_rank,
             unsigned long long *__restrict__ dcnt, unsigned long long *__restrict__ dcur,
             const uint64_t *__restrict__ dbase, uint32_t *__restrict__ ent, uint2 *__restrict__ b_short,
             uint2 *__restrict__ b_search, uint64_t *__restrict__ counts) {
@@ -230,6 +230,12 @@ __global__ void __launch_bounds__(kTileThreads)
                 ee[k] = (uint32_t)e | (kind == kHashOut ? 0x80000000u : 0u);
                 dq[k] = split_rank(wprefix[o], wtot, G);
                 slot[k] = atomicAdd(&s_c[dq[k]], 1u);
+            } else if (kind == kShort || kind == kSearch) {   // per-edge bins stay on this rank
+                own[k] = u | 0x80000000u;
+                oth[k] = x;
+                ee[k] = (uint32_t)e | (kind == kSearch ? 0x80000000u : 0u);
+                dq[k] = self_rank;
+                slot[k] = atomicAdd(&s_c[dq[k]], 1u);
             }
         } else {
             if (kind == kShort) {
@@ -262,6 +268,17 @@ __global__ void __launch_bounds__(kTileThreads)
     }
 }
 
+// Rank span last - first + 1 of N+(x) for the rows x in [r0, r1) (0 elsewhere: all-reduced by
+// summation), so the owner work needs no remote rows of col+.
+__global__ void k_row_spans(const uint64_t *__restrict__ off, const uint32_t *__restrict__ col, uint64_t r0,
+                            uint64_t r1, uint32_t *__restrict__ spans) {
+    for (uint64_t x = r0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < r1;
+         x += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t a = off[x], b = off[x + 1];
+        spans[x] = b > a ? col[b - 1] - col[a] + 1 : 0u;
+    }
+}
+
 // Owner work w(x) from its HASH entries c and their probe lengths l: the single-GPU owner
 // split's model (bin.cu k_owner_work: a fixed cost per entry, class weights, table builds).
 #ifndef TC_SHARD_ENTRY_COST
@@ -274,9 +291,8 @@ __global__ void __launch_bounds__(kTileThreads)
 #define TC_SHARD_WARP_WEIGHT 2
 #endif
 __global__ void k_shard_owner_work(const uint32_t *__restrict__ cnt, const unsigned long long *__restrict__ len,
-                                   const uint64_t *__restrict__ off, const uint32_t *__restrict__ col,
-                                   const uint32_t *__restrict__ dplus, uint64_t n, uint32_t cta_min,
-                                   uint64_t *__restrict__ work) {
+                                   const uint32_t *__restrict__ spans, const uint32_t *__restrict__ dplus,
+                                   uint64_t n, uint32_t cta_min, uint64_t *__restrict__ work) {
     for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n;
          x += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t c = cnt[x], du = dplus[x];
@@ -286,7 +302,7 @@ __global__ void k_shard_owner_work(const uint32_t *__restrict__ cnt, const unsig
             if (du < cta_min) {
                 w = w * TC_SHARD_WARP_WEIGHT + (uint64_t)((c + kWarpTaskLists - 1) / kWarpTaskLists) * du;
             } else {
-                const uint64_t span = (uint64_t)col[off[x + 1] - 1] - col[off[x]] + 1;
+                const uint64_t span = spans[x];
                 const bool bitmap = span + 32 <= kCtaBitmapBits;
                 if (!bitmap) w *= TC_SHARD_HASH_WEIGHT;
                 w += (uint64_t)((c + kCtaTaskLists - 1) / kCtaTaskLists) * (du + (bitmap ? span / 32 : 0));
@@ -297,33 +313,82 @@ __global__ void k_shard_owner_work(const uint32_t *__restrict__ cnt, const unsig
 }
 
 // ------------------------------------------------------------------ P6: owner structures
-__global__ void k_ent_count(const uint32_t *__restrict__ ent, uint64_t k, uint32_t *__restrict__ icnt,
-                            uint32_t *__restrict__ ocnt) {
+// Received entries grouped by a stable radix sort of key = out-part flag << b | owner (no
+// per-owner atomics: a hub owner receives up to 10^6 entries): in-part entries first, by
+// owner, then the out-part entries, by owner.
+// Classes: 0 HASH in-part, 1 HASH out-part (flag in bit 31 of the CSR index), 2 SHORT edge,
+// 3 SEARCH edge (bit 31 of the owner field marks the per-edge bins; owner = u, other = x).
+__global__ void k_ent_keys(const uint32_t *__restrict__ ent, uint64_t k, int b, uint32_t *__restrict__ key) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k;
          i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t o = ent[3 * i], ef = ent[3 * i + 2];
-        atomicAdd(ef & 0x80000000u ? &ocnt[o] : &icnt[o], 1u);
+        const uint32_t o = ent[3 * i], cls = (o >> 31) * 2 + (ent[3 * i + 2] >> 31);
+        key[i] = (o & 0x7fffffffu) | (cls << b);
     }
 }
 
-// in-part entry (x, u, e): in_src = u, ulo = e + 1 (probe [e + 1, off[u + 1]));
-// out-part entry (u, x, e): orange = N+(x), ovid = x.  Cursors: icur / ocur (zeroed).
-__global__ void k_ent_place(const uint32_t *__restrict__ ent, uint64_t k, const uint64_t *__restrict__ in_off,
-                            const uint64_t *__restrict__ ooff, const uint64_t *__restrict__ off,
-                            uint32_t *__restrict__ icur, uint32_t *__restrict__ ocur,
-                            uint32_t *__restrict__ in_src, uint32_t *__restrict__ ulo,
-                            uint2 *__restrict__ orange, uint32_t *__restrict__ ovid) {
+// Entries per owner (icnt: class 0, ocnt: class 1) from the runs of the sorted keys (two
+// atomics per run, each on its own owner's counter).
+__global__ void k_ent_runs(const uint32_t *__restrict__ key, uint64_t k, int b, uint32_t *__restrict__ icnt,
+                           uint32_t *__restrict__ ocnt) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k;
          i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t o = ent[3 * i], y = ent[3 * i + 1], ef = ent[3 * i + 2];
-        if (ef & 0x80000000u) {
-            const uint64_t q = ooff[o] + atomicAdd(&ocur[o], 1u);
-            orange[q] = make_uint2((uint32_t)off[y], (uint32_t)off[y + 1]);
-            ovid[q] = y;
+        const uint32_t x = key[i], cls = x >> b;
+        if (cls >= 2) continue;
+        const uint32_t o = x & ((1u << b) - 1u);
+        uint32_t *c = cls ? ocnt : icnt;
+        if (i + 1 == k || key[i + 1] != x) atomicAdd(&c[o], (uint32_t)(i + 1));
+        if (i == 0 || key[i - 1] != x) atomicSub(&c[o], (uint32_t)i);
+    }
+}
+
+// Entries per class: the sorted keys hold the class in their top bits, so its boundaries are
+// found by binary search (a per-run atomic on 4 counters serialised for ms at s24).
+__global__ void k_ent_classes(const uint32_t *__restrict__ key, uint64_t k, int b,
+                              unsigned long long *__restrict__ tot) {
+    __shared__ uint64_t s_at[5];
+    const int c = threadIdx.x;
+    if (c <= 4) {
+        uint64_t lo = 0, hi = k;   // first i with key[i] >= c << b
+        const uint64_t want = (uint64_t)c << b;
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if ((uint64_t)key[mid] < want) lo = mid + 1;
+            else hi = mid;
+        }
+        s_at[c] = c == 4 ? k : lo;
+    }
+    __syncthreads();
+    if (c < 4) tot[c] = s_at[c + 1] - s_at[c];
+}
+
+// Sorted position i (entry perm[i]): i < k_in -> in-list slot i: in_src = u, ulo = e + 1
+// (probe [e + 1, off[u + 1])); else out-part slot i - k_in: orange = N+(x), ovid = x.
+// ... and the SHORT / SEARCH edges into their bins (whose counts come from tot).
+__global__ void k_ent_place(const uint32_t *__restrict__ ent, const uint32_t *__restrict__ perm, uint64_t k,
+                            const unsigned long long *__restrict__ tot, const uint64_t *__restrict__ off,
+                            uint32_t *__restrict__ in_src, uint32_t *__restrict__ ulo,
+                            uint2 *__restrict__ orange, uint32_t *__restrict__ ovid,
+                            uint2 *__restrict__ b_short, uint2 *__restrict__ b_search,
+                            uint64_t *__restrict__ counts) {
+    const uint64_t k_in = tot[0], k_o = k_in + tot[1], k_s = k_o + tot[2];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        counts[0] = tot[2];
+        counts[2] = tot[3];
+    }
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t e = perm[i];
+        const uint32_t y = ent[3 * e + 1], ef = ent[3 * e + 2];
+        if (i < k_in) {
+            in_src[i] = y;
+            ulo[i] = ef + 1;
+        } else if (i < k_o) {
+            orange[i - k_in] = make_uint2((uint32_t)off[y], (uint32_t)off[y + 1]);
+            ovid[i - k_in] = y;
         } else {
-            const uint64_t p = in_off[o] + atomicAdd(&icur[o], 1u);
-            in_src[p] = y;
-            ulo[p] = ef + 1;
+            const uint2 uv = make_uint2(ent[3 * e] & 0x7fffffffu, y);
+            if (i < k_s) b_short[i - k_o] = uv;
+            else b_search[i - k_s] = uv;
         }
     }
 }
@@ -512,19 +577,26 @@ tc_status tc_shard_rows(uint64_t n, uint64_t m_recv, const uint64_t *pairs, cons
 }
 
 tc_status tc_shard_work(uint64_t n, const uint64_t *off_plus, const uint32_t *col_plus, const uint32_t *dplus,
-                        uint32_t flags, const tc_options *opt, uint64_t e_begin, uint64_t e_end,
-                        uint32_t *ent_cnt, uint64_t *ent_len) {
+                        uint32_t flags, const tc_options *opt, uint64_t row_begin, uint64_t row_end,
+                        uint64_t e_begin, uint64_t e_end, uint32_t *ent_cnt, uint64_t *ent_len,
+                        uint32_t *spans) {
     return run_phase(opt, [&](Ctx &ctx, const tc_options &o) {
         check_opts(o);
         check_device(ent_cnt, ctx.device, "ent_cnt");
         check_device(ent_len, ctx.device, "ent_len");
+        check_device(spans, ctx.device, "spans");
         TC_CUDA(cudaMemsetAsync(ent_cnt, 0, n * sizeof(uint32_t), ctx.stream));
         TC_CUDA(cudaMemsetAsync(ent_len, 0, n * sizeof(uint64_t), ctx.stream));
+        TC_CUDA(cudaMemsetAsync(spans, 0, n * sizeof(uint32_t), ctx.stream));
+        if (row_end > row_begin) {
+            k_row_spans<<<ctx.persistent_grid(8), 256, 0, ctx.stream>>>(off_plus, col_plus, row_begin, row_end, spans);
+            TC_LAUNCHED(ctx);
+        }
         if (e_end <= e_begin) return;
         const SliceParams sp = slice_params(ctx, n, off_plus, col_plus, dplus, o, !(flags & TC_PER_VERTEX));
         const uint32_t tiles = (uint32_t)((e_end - e_begin + kTileItems - 1) / kTileItems);
         k_slice<0><<<tiles, kTileThreads, 0, ctx.stream>>>(sp, e_begin, e_end, ent_cnt,
-                                                            (unsigned long long *)ent_len, nullptr, 1,
+                                                            (unsigned long long *)ent_len, nullptr, 1, 0,
                                                             nullptr, nullptr, nullptr, nullptr, nullptr,
                                                             nullptr, nullptr);
         TC_LAUNCHED(ctx);
@@ -532,7 +604,7 @@ tc_status tc_shard_work(uint64_t n, const uint64_t *off_plus, const uint32_t *co
 }
 
 tc_status tc_shard_route(uint64_t n, const uint64_t *off_plus, const uint32_t *col_plus, const uint32_t *dplus,
-                         const uint32_t *ent_cnt, const uint64_t *ent_len, uint32_t flags,
+                         const uint32_t *ent_cnt, const uint64_t *ent_len, const uint32_t *spans, uint32_t flags,
                          const tc_options *opt, int rank, int world, uint64_t e_begin, uint64_t e_end,
                          uint32_t *entries_out, uint64_t *send_counts) {
     return run_phase(opt, [&](Ctx &ctx, const tc_options &o) {
@@ -542,7 +614,7 @@ tc_status tc_shard_route(uint64_t n, const uint64_t *off_plus, const uint32_t *c
         const int G = world;
         uint64_t *work = ctx.alloc<uint64_t>(n), *wprefix = ctx.alloc<uint64_t>(n + 1);
         k_shard_owner_work<<<ctx.persistent_grid(8), 256, 0, ctx.stream>>>(
-            ent_cnt, (const unsigned long long *)ent_len, off_plus, col_plus, dplus, n, cta_min_of(o), work);
+            ent_cnt, (const unsigned long long *)ent_len, spans, dplus, n, cta_min_of(o), work);
         TC_LAUNCHED(ctx);
         scan_exclusive(ctx, work, wprefix, n);
         unsigned long long *cnt = ctx.alloc<unsigned long long>(2 * G);
@@ -552,14 +624,14 @@ tc_status tc_shard_route(uint64_t n, const uint64_t *off_plus, const uint32_t *c
         const uint32_t tiles = e_end > e_begin ? (uint32_t)((e_end - e_begin + kTileItems - 1) / kTileItems) : 0;
         if (tiles) {
             k_slice<1><<<tiles, kTileThreads, 0, ctx.stream>>>(sp, e_begin, e_end, nullptr, nullptr, wprefix, G,
-                                                                cnt, nullptr, nullptr, nullptr, nullptr,
+                                                                rank, cnt, nullptr, nullptr, nullptr, nullptr,
                                                                 nullptr, nullptr);
             TC_LAUNCHED(ctx);
         }
         dest_offsets(ctx, cnt, G, base, send_counts);
         if (tiles) {
             k_slice<1><<<tiles, kTileThreads, 0, ctx.stream>>>(sp, e_begin, e_end, nullptr, nullptr, wprefix, G,
-                                                                nullptr, cnt + G, base, entries_out, nullptr,
+                                                                rank, nullptr, cnt + G, base, entries_out, nullptr,
                                                                 nullptr, nullptr);
             TC_LAUNCHED(ctx);
         }
@@ -577,6 +649,7 @@ tc_status tc_shard_count(uint64_t n, uint64_t m, const uint64_t *off_plus, const
         if (flags & ~(uint32_t)TC_PER_VERTEX) throw Error{TC_EINVAL, "tc_shard_count: flags: TC_PER_VERTEX only"};
         const bool pv = flags & TC_PER_VERTEX;
         if (pv && (!per_vertex_partial || !newid)) throw Error{TC_EINVAL, "TC_PER_VERTEX needs newid and per_vertex_partial"};
+        if (n >= (1ull << 30) || m >= (1ull << 31)) throw Error{TC_EINVAL, "the sharded pipeline needs n < 2^30, m < 2^31"};
         check_device(partial_dev, ctx.device, "partial_dev");
         check_device(per_vertex_partial, ctx.device, "per_vertex_partial");
         TC_CUDA(cudaMemsetAsync(partial_dev, 0, sizeof(uint64_t), ctx.stream));
@@ -593,13 +666,26 @@ tc_status tc_shard_count(uint64_t n, uint64_t m, const uint64_t *off_plus, const
         g.m_cap = m;
         // ---- HASH owners of this rank: in-lists and out-part lists from the received entries
         const uint64_t k = n_entries;
+        const int b = sh_id_bits(n);
         uint32_t *icnt = ctx.alloc<uint32_t>(n + 1), *ocnt = ctx.alloc<uint32_t>(n + 1);
         TC_CUDA(cudaMemsetAsync(icnt, 0, (n + 1) * sizeof(uint32_t), ctx.stream));
         TC_CUDA(cudaMemsetAsync(ocnt, 0, (n + 1) * sizeof(uint32_t), ctx.stream));
         const int grid = ctx.persistent_grid(8);
+        uint32_t *perm = nullptr;
+        unsigned long long *tot = ctx.alloc<unsigned long long>(4);
+        TC_CUDA(cudaMemsetAsync(tot, 0, 4 * sizeof(unsigned long long), ctx.stream));
         if (k) {
             check_device(entries, ctx.device, "entries");
-            k_ent_count<<<grid, 256, 0, ctx.stream>>>(entries, k, icnt, ocnt);
+            uint32_t *key = ctx.alloc<uint32_t>(k);
+            k_ent_keys<<<grid, 256, 0, ctx.stream>>>(entries, k, b, key);
+            TC_LAUNCHED(ctx);
+            uint32_t *kA = ctx.alloc<uint32_t>(k), *kB = ctx.alloc<uint32_t>(k);
+            uint32_t *vA = ctx.alloc<uint32_t>(k), *vB = ctx.alloc<uint32_t>(k);
+            uint32_t *sk;
+            radix_sort_pairs_from(ctx, key, nullptr, kA, kB, vA, vB, k, nullptr, b + 2, &sk, &perm);
+            k_ent_runs<<<grid, 256, 0, ctx.stream>>>(sk, k, b, icnt, ocnt);
+            TC_LAUNCHED(ctx);
+            k_ent_classes<<<1, 32, 0, ctx.stream>>>(sk, k, b, tot);
             TC_LAUNCHED(ctx);
         }
         uint64_t *in_off = ctx.alloc<uint64_t>(n + 1), *ooff = ctx.alloc<uint64_t>(n + 1);
@@ -619,13 +705,19 @@ tc_status tc_shard_count(uint64_t n, uint64_t m, const uint64_t *off_plus, const
                                                                        bins.owners_warp, bins.owners_cta,
                                                                        bins.owners_bitmap, bins.count);
         TC_LAUNCHED(ctx);
-        TC_CUDA(cudaMemsetAsync(icnt, 0, (n + 1) * sizeof(uint32_t), ctx.stream));   // now cursors
-        TC_CUDA(cudaMemsetAsync(ocnt, 0, (n + 1) * sizeof(uint32_t), ctx.stream));
         uint32_t *in_src = ctx.alloc<uint32_t>(k), *ulo = ctx.alloc<uint32_t>(k), *ovid = ctx.alloc<uint32_t>(k);
         uint2 *orange = ctx.alloc<uint2>(k);
+        // per-edge bins of this rank's rows (routed to itself by tc_shard_route)
+        const bool want_short = o.short_max > 0, want_search = o.skew_ratio > 0;
+        bins.edges[0] = ctx.alloc<uint2>(want_short ? std::max<uint64_t>(k, 1) : 1);
+        bins.edges[1] = ctx.alloc<uint2>(1);
+        bins.edges[2] = ctx.alloc<uint2>(want_search ? std::max<uint64_t>(k, 1) : 1);
+        bins.has[0] = want_short;
+        bins.has[1] = false;
+        bins.has[2] = want_search;
         if (k) {
-            k_ent_place<<<grid, 256, 0, ctx.stream>>>(entries, k, in_off, ooff, off_plus, icnt, ocnt, in_src, ulo,
-                                                     orange, ovid);
+            k_ent_place<<<grid, 256, 0, ctx.stream>>>(entries, perm, k, tot, off_plus, in_src, ulo, orange, ovid,
+                                                     bins.edges[0], bins.edges[2], bins.count);
             TC_LAUNCHED(ctx);
         }
         g.in_off = in_off;
@@ -647,22 +739,7 @@ tc_status tc_shard_count(uint64_t n, uint64_t m, const uint64_t *off_plus, const
         hp.force = -1;
         hp.rank = rank;
         hp.world = world;
-        // ---- per-edge bins of this rank's slice; the dense core by interleaved edge blocks
-        const bool want_short = o.short_max > 0, want_search = o.skew_ratio > 0;
-        bins.edges[0] = ctx.alloc<uint2>(want_short ? std::max<uint64_t>(e_end - e_begin, 1) : 1);
-        bins.edges[1] = ctx.alloc<uint2>(1);
-        bins.edges[2] = ctx.alloc<uint2>(want_search ? std::max<uint64_t>(e_end - e_begin, 1) : 1);
-        bins.has[0] = want_short;
-        bins.has[1] = false;
-        bins.has[2] = want_search;
-        const SliceParams sp = slice_params(ctx, n, off_plus, col_plus, dplus, o, !pv);
-        if (e_end > e_begin) {
-            const uint32_t tiles = (uint32_t)((e_end - e_begin + kTileItems - 1) / kTileItems);
-            k_slice<2><<<tiles, kTileThreads, 0, ctx.stream>>>(sp, e_begin, e_end, nullptr, nullptr, nullptr, 1,
-                                                                nullptr, nullptr, nullptr, nullptr, bins.edges[0],
-                                                                bins.edges[2], bins.count);
-            TC_LAUNCHED(ctx);
-        }
+        // the dense core by interleaved 2048-edge blocks (core.cu, every rank holds the CSR)
         if (!pv) core_build(ctx, g, hp);
         make_tasks(ctx, n, m, bins.owners_warp, bins.count + 8, bins.pcnt, hp, kWarpTaskLists, bins.count + 11,
                    bins.tasks_warp, bins.ntasks_warp);

@@ -15,6 +15,11 @@ static thread_local std::string g_last_error;
 
 void set_error(const std::string &msg) { g_last_error = msg; }
 
+uint64_t &thread_launches() {
+    static thread_local uint64_t n = 0;
+    return n;
+}
+
 // Per-device state created once under a lock: the SM count and the library's own
 // workspace pool (never the process's default pool, which torch / NCCL may rely on).
 struct DeviceState {
@@ -743,6 +748,8 @@ tc_status tc_masked_spgemm(uint64_t n, uint64_t m, const uint64_t *row_offsets,
 }
 
 const char *tc_last_error(void) { return g_last_error.c_str(); }
+
+uint64_t tc_launches_issued(void) { return thread_launches(); }
 
 const char *tc_version(void) { return "tc_b200 0.1 (sm_100a)"; }
 

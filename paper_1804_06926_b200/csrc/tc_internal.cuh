@@ -48,6 +48,8 @@ void set_error(const std::string &msg);
 // hook (tc_options.alloc / free) or, without one, from the library's own per-device pool
 // (cudaMallocFromPoolAsync), on the call's stream, and is freed stream-ordered when the
 // context is destroyed (or earlier with free_now).
+uint64_t &thread_launches();   // kernels launched by this thread's calls (tc_launches_issued)
+
 struct Ctx {
     cudaStream_t stream = nullptr;
     int device = 0;
@@ -102,7 +104,10 @@ struct Ctx {
                 return;
             }
     }
-    ~Ctx() { release(); }
+    ~Ctx() {
+        release();
+        thread_launches() += launches;
+    }
     // Grid for a persistent (grid-stride) kernel: `per_sm` resident CTAs per SM.
     int persistent_grid(int per_sm) const { return num_sms * per_sm; }
 

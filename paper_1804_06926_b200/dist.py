@@ -16,6 +16,81 @@ import torch.distributed as dist
 from . import clean_shard, count_edges_shard, count_shard
 
 
+class Comm:
+    """The collectives of the sharded pipeline (shard.py) over a torch.distributed group:
+    NCCL on GPUs (gloo on CPU tensors for the host-logic tests)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        # gloo (CPU tests; two ranks sharing one GPU in the GPU tests) stages CUDA tensors
+        # through host memory; NCCL works on them directly
+        self.stage = dist.get_backend(group) == "gloo"
+
+    def _src(self, q):
+        return dist.get_global_rank(self.group, q) if self.group is not None else q
+
+    def all_reduce(self, t):
+        if self.stage and t.is_cuda:
+            h = t.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=self.group)
+            t.copy_(h)
+            return
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+
+    def all_to_all(self, send, counts, width):
+        """send holds `width` elements per item, grouped by destination (counts[q] items for
+        rank q); returns the items every rank sent here, grouped by source rank."""
+        dev = send.device
+        cdev = torch.device("cpu") if self.stage else dev
+        sc = torch.tensor(counts, dtype=torch.int64, device=cdev)
+        rc = torch.empty_like(sc)
+        dist.all_to_all_single(rc, sc, group=self.group)
+        rcount = [int(x) for x in rc.tolist()]
+        recv = torch.empty(width * sum(rcount), dtype=send.dtype, device=cdev)
+        dist.all_to_all_single(recv, send[:width * sum(counts)].to(cdev),
+                               output_split_sizes=[width * c for c in rcount],
+                               input_split_sizes=[width * c for c in counts], group=self.group)
+        return recv.to(dev)
+
+    def broadcast_slices(self, buf, bounds, async_op=False):
+        """All-gather of contiguous slices: rank q owns buf[bounds[q]:bounds[q+1]] (in place).
+        async_op: NCCL broadcasts left in flight, returned for wait()."""
+        works = []
+        for q in range(self.world):
+            if bounds[q + 1] > bounds[q]:
+                sl = buf[bounds[q]:bounds[q + 1]]
+                if self.stage and sl.is_cuda:
+                    h = sl.cpu()
+                    dist.broadcast(h, src=self._src(q), group=self.group)
+                    sl.copy_(h)
+                else:
+                    w = dist.broadcast(sl, src=self._src(q), group=self.group, async_op=async_op)
+                    if async_op:
+                        works.append(w)
+        return works
+
+    def wait(self, works):
+        for w in works or []:
+            w.wait()
+
+
+def count_distributed_sharded(rowptr: torch.Tensor, col: torch.Tensor, group=None, *,
+                              per_vertex: bool = False, **opts):
+    """Exact triangle count with a1-a5 sharded too (shard.py run_rank: six phases between the
+    collectives of Comm) and one all-reduce of the partial count [and per-vertex partials]."""
+    from .shard import run_rank
+    comm = Comm(group)
+    partial, pv = run_rank(rowptr, col, comm.rank, comm.world, comm, per_vertex=per_vertex, **opts)
+    if per_vertex:
+        both = torch.cat([partial, pv])
+        comm.all_reduce(both)
+        return int(both[0].item()), both[1:]
+    comm.all_reduce(partial)
+    return int(partial.item())
+
+
 def exchange_clean_shards(rowptr: torch.Tensor, col: torch.Tensor, group=None, *, clean_fn=None):
     """Sharded a1 (tc_clean_shard on every rank) + its exchange: ONE all-reduce of the n int32
     degree partials and ONE all-gather of the ranks' cleaned edge lists (padded to the longest,

@@ -18,6 +18,7 @@ parity tests of the sharded path (a GPU cannot run ranks that wait on each other
 from __future__ import annotations
 
 import ctypes
+import os
 
 from . import (TC_ID_ORDER, TC_PER_VERTEX, _check, _load, _options, clean_shard)
 
@@ -34,8 +35,8 @@ def _lib():
         lib.tc_shard_orient.argtypes = [u64, u64, vp, vp, u32, po, vp, vp, vp, vp]
         lib.tc_shard_partition.argtypes = [u64, u64, vp, vp, vp, po, i, i, vp, vp, vp, vp, vp]
         lib.tc_shard_rows.argtypes = [u64, u64, vp, po, u64, vp]
-        lib.tc_shard_work.argtypes = [u64, vp, vp, vp, u32, po, u64, u64, vp, vp]
-        lib.tc_shard_route.argtypes = [u64, vp, vp, vp, vp, vp, u32, po, i, i, u64, u64, vp, vp]
+        lib.tc_shard_work.argtypes = [u64, vp, vp, vp, u32, po, u64, u64, u64, u64, vp, vp, vp]
+        lib.tc_shard_route.argtypes = [u64, vp, vp, vp, vp, vp, vp, u32, po, i, i, u64, u64, vp, vp]
         lib.tc_shard_count.argtypes = [u64, u64, vp, vp, vp, vp, u64, vp, u32, po, i, i, u64, u64,
                                        vp, vp]
         for f in ("tc_shard_orient", "tc_shard_partition", "tc_shard_rows", "tc_shard_work",
@@ -90,21 +91,24 @@ def shard_rows(n, pairs, col_plus, col_begin, *, stream=None, **opts):
                                 col_plus.data_ptr()))
 
 
-def shard_work(n, off, col_plus, dplus, e_begin, e_end, *, per_vertex=False, stream=None, **opts):
+def shard_work(n, off, col_plus, dplus, row_begin, row_end, e_begin, e_end, *, per_vertex=False,
+               stream=None, **opts):
     """P4: per-owner HASH entries (int32[n]) and probe lengths (int64[n]) of edges
-    [e_begin, e_end) (partials: all-reduce them)."""
+    [e_begin, e_end), and the rank spans of rows [row_begin, row_end) (int32[n]) -- partials:
+    all-reduce them."""
     import torch
     dev = off.device
     cnt = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
     ln = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    sp = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
     o = _options(stream=stream, device=dev, **opts)
     _check(_lib().tc_shard_work(n, off.data_ptr(), col_plus.data_ptr(), dplus.data_ptr(),
-                                TC_PER_VERTEX if per_vertex else 0, ctypes.byref(o), e_begin, e_end,
-                                cnt.data_ptr(), ln.data_ptr()))
-    return cnt[:n], ln[:n]
+                                TC_PER_VERTEX if per_vertex else 0, ctypes.byref(o), row_begin, row_end,
+                                e_begin, e_end, cnt.data_ptr(), ln.data_ptr(), sp.data_ptr()))
+    return cnt[:n], ln[:n], sp[:n]
 
 
-def shard_route(n, off, col_plus, dplus, cnt, ln, rank, world, e_begin, e_end, *, per_vertex=False,
+def shard_route(n, off, col_plus, dplus, cnt, ln, spans, rank, world, e_begin, e_end, *, per_vertex=False,
                 stream=None, **opts):
     """P5: the HASH probe entries of edges [e_begin, e_end) grouped by their owner's rank
     (int32 triples: owner, other endpoint, CSR index | out-part flag << 31) and their counts."""
@@ -114,7 +118,7 @@ def shard_route(n, off, col_plus, dplus, cnt, ln, rank, world, e_begin, e_end, *
     sc = _u64s(world)
     o = _options(stream=stream, device=dev, **opts)
     _check(_lib().tc_shard_route(n, off.data_ptr(), col_plus.data_ptr(), dplus.data_ptr(), cnt.data_ptr(),
-                                 ln.data_ptr(), TC_PER_VERTEX if per_vertex else 0, ctypes.byref(o), rank,
+                                 ln.data_ptr(), spans.data_ptr(), TC_PER_VERTEX if per_vertex else 0, ctypes.byref(o), rank,
                                  world, e_begin, e_end, ent.data_ptr(), sc))
     counts = list(sc)
     return ent[:3 * sum(counts)], counts
@@ -134,33 +138,65 @@ def shard_count(n, off, col_plus, dplus, newid, entries, rank, world, e_begin, e
 
 
 # ---------------------------------------------------------------- one rank against a Comm
-def run_rank(rowptr, col, rank, world, comm, *, per_vertex=False, **opts):
+def run_rank(rowptr, col, rank, world, comm, *, per_vertex=False, times=None, **opts):
     """The whole sharded count on one rank; `comm` provides all_reduce(t), all_to_all(send,
     counts, width) -> recv, broadcast_slices(col_plus, bounds).  Returns the partial count
-    (int64[1]) [and the per-vertex partials] BEFORE the final all-reduce."""
+    (int64[1]) [and the per-vertex partials] BEFORE the final all-reduce.  With a `times` dict,
+    each phase's CUDA-event ms (on the current stream; the phases are synchronous) is added
+    under its name, the collectives' under "comm"."""
     import torch
     n = rowptr.numel() - 1
     dev = rowptr.device
+    marks = []
+
+    def mark(name):
+        if times is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            marks.append((name, e))
+
+    mark("start")
     edges, deg = clean_shard(rowptr, col, rank, world, **opts)
+    mark("clean")
     comm.all_reduce(deg)
+    mark("comm")
     newid, src, dst, dplus = shard_orient(n, edges, deg, **opts)
+    mark("orient")
     comm.all_reduce(dplus)
+    mark("comm")
     off, pairs, cnt, rb, cb = shard_partition(n, src, dst, dplus, rank, world, **opts)
+    mark("partition")
     recv = comm.all_to_all(pairs, cnt, 1)
+    mark("comm")
     col_plus = torch.empty(max(cb[world], 1), dtype=torch.int32, device=dev)
     shard_rows(n, recv, col_plus, cb[rank], **opts)
-    comm.broadcast_slices(col_plus, cb)
+    mark("rows")
+    # the col+ all-gather runs while this rank bins its own rows (work / route read only them)
+    pending = comm.broadcast_slices(col_plus, cb, async_op=True)
+    mark("comm")
     e0, e1 = cb[rank], cb[rank + 1]
-    ecnt, elen = shard_work(n, off, col_plus, dplus, e0, e1, per_vertex=per_vertex, **opts)
+    ecnt, elen, spans = shard_work(n, off, col_plus, dplus, rb[rank], rb[rank + 1], e0, e1,
+                                   per_vertex=per_vertex, **opts)
+    mark("work")
     comm.all_reduce(ecnt)
     comm.all_reduce(elen)
-    ent, sc = shard_route(n, off, col_plus, dplus, ecnt, elen, rank, world, e0, e1,
+    comm.all_reduce(spans)
+    mark("comm")
+    ent, sc = shard_route(n, off, col_plus, dplus, ecnt, elen, spans, rank, world, e0, e1,
                           per_vertex=per_vertex, **opts)
+    mark("route")
     rent = comm.all_to_all(ent, sc, 3)
+    comm.wait(pending)
+    mark("comm")
     partial = torch.zeros(1, dtype=torch.int64, device=dev)
     pv = torch.zeros(n, dtype=torch.int64, device=dev) if per_vertex else None
     shard_count(n, off, col_plus[:cb[world]], dplus, newid, rent, rank, world, e0, e1, partial,
                 per_vertex_partial=pv, **opts)
+    mark("count")
+    if times is not None:
+        torch.cuda.synchronize()
+        for (_, a), (name, b) in zip(marks, marks[1:]):
+            times[name] = times.get(name, 0.0) + a.elapsed_time(b)
     return partial, pv
 
 
@@ -206,7 +242,7 @@ def emulate(rowptr, col, world, *, per_vertex=False, timed=False, **opts):
     newid = p1[0][0]
     p2 = [run("partition", lambda r=r: shard_partition(n, p1[r][1], p1[r][2], dplus, r, G, **opts), r)
           for r in range(G)]
-    off, cb = p2[0][0], p2[0][4]
+    off, rows, cb = p2[0][0], p2[0][3], p2[0][4]
     recv = []
     for q in range(G):   # destination q gets every rank's chunk q
         parts = []
@@ -222,14 +258,15 @@ def emulate(rowptr, col, world, *, per_vertex=False, timed=False, **opts):
         run("rows", lambda r=r: shard_rows(n, recv[r], col_plus, cb[r], **opts), r)
     coll("all-gather col+", 4.0 * cb[G] * (G - 1) / G / NVLINK_GATHER * 1e3)
     del recv
-    w = [run("work", lambda r=r: shard_work(n, off, col_plus, dplus, cb[r], cb[r + 1],
+    w = [run("work", lambda r=r: shard_work(n, off, col_plus, dplus, rows[r], rows[r + 1], cb[r], cb[r + 1],
                                              per_vertex=per_vertex, **opts), r) for r in range(G)]
     ecnt = sum(x[0].to(torch.int64) for x in w).to(torch.int32)
     elen = sum(x[1] for x in w)
+    spans = sum(x[2].to(torch.int64) for x in w).to(torch.int32)
     del w
-    coll("all-reduce owner work", 12.0 * n * 2 * (G - 1) / G / NVLINK_REDUCE * 1e3)
-    rt = [run("route", lambda r=r: shard_route(n, off, col_plus, dplus, ecnt, elen, r, G, cb[r], cb[r + 1],
-                                                per_vertex=per_vertex, **opts), r) for r in range(G)]
+    coll("all-reduce owner work", 16.0 * n * 2 * (G - 1) / G / NVLINK_REDUCE * 1e3)
+    rt = [run("route", lambda r=r: shard_route(n, off, col_plus, dplus, ecnt, elen, spans, r, G, cb[r],
+                                                cb[r + 1], per_vertex=per_vertex, **opts), r) for r in range(G)]
     rent = []
     for q in range(G):
         parts = []
@@ -241,16 +278,26 @@ def emulate(rowptr, col, world, *, per_vertex=False, timed=False, **opts):
     coll("all-to-all entries", max(4.0 * x[0].numel() * (G - 1) / G for x in rt) / NVLINK_GATHER * 1e3)
     del rt
     total, pv_sum = 0, torch.zeros(n, dtype=torch.int64, device=dev) if per_vertex else None
+    prof = int(os.environ.get("TC_PROFILE_COUNT_RANK", "-1"))   # ncu --profile-from-start off
     for r in range(G):
         partial = torch.zeros(1, dtype=torch.int64, device=dev)
         pv = torch.zeros(n, dtype=torch.int64, device=dev) if per_vertex else None
+        if r == prof:
+            torch.cuda.profiler.start()
         run("count", lambda r=r: shard_count(n, off, col_plus[:cb[G]], dplus, newid, rent[r], r, G, cb[r],
                                              cb[r + 1], partial, per_vertex_partial=pv, **opts), r)
+        if r == prof:
+            torch.cuda.profiler.stop()
         total += int(partial.item())
         if per_vertex:
             pv_sum += pv
     coll("all-reduce count", 8.0 * (n + 1 if per_vertex else 1) * 2 * (G - 1) / G / NVLINK_REDUCE * 1e3)
     if timed:
         rep["step_ms"] = sum(max(v) for v in rep["phases"].values()) + sum(rep["collectives"].values())
+        # the col+ all-gather overlaps work + route + their collectives (run_rank issues it async)
+        hidden = min(rep["collectives"]["all-gather col+"],
+                     max(rep["phases"]["work"]) + max(rep["phases"]["route"]) +
+                     rep["collectives"]["all-reduce owner work"] + rep["collectives"]["all-to-all entries"])
+        rep["step_ms_overlapped"] = rep["step_ms"] - hidden
         rep["slowest_rank_ms"] = max(sum(v[r] for v in rep["phases"].values()) for r in range(G))
     return total, pv_sum, rep

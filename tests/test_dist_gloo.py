@@ -130,3 +130,50 @@ def test_clean_shard_exchange_world2():
     for rank, keys, deg in res:
         assert (keys == want).all(), rank
         assert (deg == np.diff(crow)).all(), rank
+
+
+# ------------------------------------------------------------------ sharded pipeline collectives
+def _comm_worker(rank, world, port, q):
+    """dist.Comm (the sharded pipeline's collectives, shard.py run_rank) under gloo: all-to-all
+    of width-3 items with uneven counts, slice all-gather by broadcasts, all-reduce."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1804_06926_b200.dist import Comm
+        comm = Comm()
+        counts = [rank + 1 + 2 * d for d in range(world)]          # items for destination d
+        send = torch.cat([torch.arange(3 * c, dtype=torch.int32) + 1000 * rank + 100 * d
+                          for d, c in enumerate(counts)])
+        recv = comm.all_to_all(send, counts, 3)
+        bounds = [0, 3, 10][:world + 1]
+        buf = torch.full((bounds[world],), -1, dtype=torch.int32)
+        buf[bounds[rank]:bounds[rank + 1]] = rank + 7
+        comm.broadcast_slices(buf, bounds)
+        t = torch.tensor([rank + 1, 10 * rank], dtype=torch.int64)
+        comm.all_reduce(t)
+        q.put((rank, recv.numpy().copy(), buf.numpy().copy(), t.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_comm_world2():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_comm_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, recv, buf, t = q.get(timeout=120)
+        res[r] = (recv, buf, t)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        # what shard.emulate builds locally: every source's chunk for r, in source order
+        want = np.concatenate([np.arange(3 * (s + 1 + 2 * r), dtype=np.int32) + 1000 * s + 100 * r
+                               for s in range(world)])
+        assert (res[r][0] == want).all()
+        assert (res[r][1] == np.array([7, 7, 7] + [8] * 7, np.int32)).all()
+        assert (res[r][2] == np.array([3, 10])).all()

@@ -1,4 +1,4 @@
-"""The multi-GPU path end to end through the REAL library (the gloo test used an
+"""The multi-GPU paths end to end through the REAL library (the gloo test used an
 oracle stand-in shard): world-2 process group, both ranks on cuda:0 (the round's boxes have
 one GPU; NCCL refuses two ranks on one device, so the group is gloo over CUDA tensors), each
 rank running paper_1804_06926_b200.dist.count_distributed -> tc_count_shard + allreduce.
@@ -34,7 +34,8 @@ def _worker(rank, world, port, name, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_1804_06926_b200.dist import count_distributed, count_distributed_sharded_a1
+        from paper_1804_06926_b200.dist import (count_distributed, count_distributed_sharded,
+                                                count_distributed_sharded_a1)
         g = _graph(name)
         dev = torch.device("cuda:0")
         rp = torch.from_numpy(g.rowptr.view(np.int64)).to(dev)
@@ -45,6 +46,10 @@ def _worker(rank, world, port, name, q):
         T3 = count_distributed_sharded_a1(rp, cl)
         T4, pv4 = count_distributed_sharded_a1(rp, cl, per_vertex=True)
         assert T3 == T and T4 == T and (pv4 == pv).all()
+        # a1-a5 sharded (shard.py run_rank through dist.Comm: all-reduce, all-to-all, broadcasts)
+        T5 = count_distributed_sharded(rp, cl)
+        T6, pv6 = count_distributed_sharded(rp, cl, per_vertex=True)
+        assert T5 == T and T6 == T and (pv6 == pv).all()
         q.put((rank, T, T2, pv.cpu().numpy().copy()))
     finally:
         dist.destroy_process_group()
