@@ -430,12 +430,20 @@ def main():
     from paper_1804_06926_b200.dist import (Comm, count_distributed, count_distributed_sharded,
                                             count_distributed_sharded_a1, exchange_clean_shards)
     from paper_1804_06926_b200.shard import run_rank
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # TC_BENCH_SHARED_GPU=1 (tests only): every rank on cuda:0 over gloo -- the boxes of this
+    # round have one GPU and NCCL refuses two ranks on one device; the numbers are then
+    # meaningless, the point is exercising the N > 1 code path end to end
+    shared = os.environ.get("TC_BENCH_SHARED_GPU") == "1"
+    gpu = 0 if shared else local
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.current_stream()
     rp = torch.from_numpy(g.rowptr.view(np.int64)).to(dev)
     cl = torch.from_numpy(g.col.view(np.int32)).to(dev)
@@ -478,7 +486,7 @@ def main():
     torch.cuda.synchronize()
 
     # ---- timed region: K steps, per-step CUDA events, L2 flushed between steps
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(gpu)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     stats = []
