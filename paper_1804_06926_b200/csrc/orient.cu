@@ -499,21 +499,24 @@ __global__ void k_deg_rowptr(const uint64_t *__restrict__ rowptr, uint64_t n,
         deg[u] = (uint32_t)(rowptr[u + 1] - rowptr[u]);
 }
 
-// Clean input: one persistent pass.  Tiles of arcs keep the arcs with rank(u) < rank(v) and
-// write them as oriented pairs in rank ids at a tile offset taken by ONE atomic per tile (the
+// Clean input: one persistent pass.  Tiles of arcs keep the arcs with u < v (ids; each edge of
+// a simple symmetric CSR once) and write them as oriented pairs (lower rank, higher rank) in rank ids at a tile offset taken by ONE atomic per tile (the
 // pair order is free: the two-key sort that follows fixes the CSR order), count d+ (one atomic
 // per run of equal sources) and the digit histograms of both radix sorts that follow (flushed
 // once per block).  (A decoupled look-back for an order-preserving offset measured 1.07 ms at
 // s21 against this.)  Writes stop at cap: a false TC_CLEAN claim is reported, never written
 // out of bounds.
-__global__ void __launch_bounds__(kTileThreads)
+#ifndef TC_EMIT_MINB
+#define TC_EMIT_MINB 1
+#endif
+__global__ void __launch_bounds__(kTileThreads, TC_EMIT_MINB)
     k_orient_emit(const uint64_t *__restrict__ rowptr, const uint32_t *__restrict__ col,
                   uint64_t n, uint64_t M, const uint32_t *__restrict__ deg,
                   const uint32_t *__restrict__ newid, uint64_t *__restrict__ m_out,
                   uint32_t *__restrict__ okey, uint32_t *__restrict__ oval,
                   uint32_t *__restrict__ dplus, uint32_t *__restrict__ hist_key,
                   uint32_t *__restrict__ hist_val, int passes, int db, uint64_t cap,
-                  uint32_t *__restrict__ claim_err) {
+                  uint32_t *__restrict__ claim_err, const uint2 *__restrict__ tb, bool pruned) {
     __shared__ uint32_t s_row[kTileItems];
     __shared__ uint32_t s_scan[kTileThreads / 32];
     __shared__ uint64_t s_base;
@@ -525,18 +528,21 @@ __global__ void __launch_bounds__(kTileThreads)
         __syncthreads();   // s_row / s_base of the previous tile are no longer read
         const uint64_t t0 = tile * kTileItems;
         const uint32_t len = (uint32_t)min((uint64_t)kTileItems, M - t0);
-        tile_rows(rowptr, n, t0, len, s_row, s_scan);
+        tile_rows_b(rowptr, t0, len, tb[tile], s_row, s_scan);
         const uint32_t i0 = threadIdx.x * kItemsPerThread;
-        // rank(u) < rank(v) <=> newid[u] < newid[v] (the rank sort's order), so one gather per
-        // arc serves both the filter and the output ids; deg[u] = 0 marks a pruned vertex
+        // a symmetric input holds every edge twice: keep the arc with u < v (ids, no gather
+        // needed to decide) and orient it by rank, rank(u) < rank(v) <=> newid[u] < newid[v]
+        // (round 2: half the random newid gathers of filtering every arc by rank); deg = 0
+        // marks a pruned vertex (TC_PRUNE only)
         uint32_t f[kItemsPerThread], nu[kItemsPerThread], nv[kItemsPerThread], c = 0;
 #pragma unroll
         for (int k = 0; k < kItemsPerThread; k++) {
             const uint32_t i = i0 + k;
-            const uint32_t u = i < len ? s_row[i] : 0u;
-            nv[k] = i < len ? newid[col[t0 + i]] : 0u;
-            nu[k] = newid[u];
-            f[k] = i < len && deg[u] != 0 && nu[k] < nv[k];
+            const uint32_t u = i < len ? s_row[i] : 0u, v = i < len ? col[t0 + i] : 0u;
+            f[k] = i < len && u < v && (!pruned || (deg[u] != 0 && deg[v] != 0));
+            const uint32_t a = newid[u], b = f[k] ? newid[v] : 0u;
+            nu[k] = min(a, b);
+            nv[k] = max(a, b);
             c += f[k];
         }
         uint32_t total;
@@ -613,10 +619,12 @@ void orient_clean(Ctx &ctx, uint64_t n, uint64_t M, const uint64_t *rowptr, cons
 #define TC_EMIT_PER_SM 4   // swept 4 / 6 / 8: clean-input orient 2.53 / 2.77 / 2.65 ms (s21)
 #endif
     uint32_t egrid = (uint32_t)std::min<uint64_t>(tiles, (uint64_t)ctx.persistent_grid(TC_EMIT_PER_SM));
+    uint2 *tb = ctx.alloc<uint2>(tiles + 1);
+    tile_bounds(ctx, rowptr, n, M, nullptr, tb);
     k_orient_emit<<<egrid, kTileThreads, 0, ctx.stream>>>(rowptr, col, n, M, key, out.newid, m_dev,
                                                           okey, oval, dplus, phist,
                                                           phist + ppasses * kHistDigits, ppasses,
-                                                          pdb, cap, out.claim_err);
+                                                          pdb, cap, out.claim_err, tb, prune.enabled);
     TC_LAUNCHED(ctx);
     k_emit_clamp<<<1, 1, 0, ctx.stream>>>(m_dev, cap, out.claim_err);
     TC_LAUNCHED(ctx);

@@ -1,5 +1,7 @@
 // scan.cu -- device-wide exclusive scan (reduce-then-scan) and the block-level
 // scan / tile row-search helpers every tile kernel uses.
+#include <algorithm>
+
 #include "tc_internal.cuh"
 #include "block_scan.cuh"
 
@@ -140,6 +142,37 @@ void scan_exclusive(Ctx &ctx, const uint32_t *in, uint64_t *out, uint64_t count)
 }
 void scan_exclusive(Ctx &ctx, const uint64_t *in, uint64_t *out, uint64_t count) {
     scan_impl<uint64_t>(ctx, in, out, count);
+}
+
+// ------------------------------------------------------------------ tile row bounds
+__device__ __forceinline__ uint64_t lower_bound_u64(const uint64_t *__restrict__ a, uint64_t len, uint64_t x) {
+    uint64_t lo = 0, hi = len;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (a[mid] < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+__global__ void k_tile_bounds(const uint64_t *__restrict__ rowptr, uint64_t n, uint64_t items,
+                              const uint64_t *__restrict__ items_dev, uint2 *__restrict__ bounds) {
+    const uint64_t m = items_dev ? min(*items_dev, items) : items;
+    const uint64_t tiles = (m + kTileItems - 1) / kTileItems;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tiles;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t t0 = t * kTileItems, len = min((uint64_t)kTileItems, m - t0);
+        bounds[t] = make_uint2((uint32_t)lower_bound_u64(rowptr, n + 1, t0 + 1),
+                               (uint32_t)lower_bound_u64(rowptr, n + 1, t0 + len));
+    }
+}
+
+void tile_bounds(Ctx &ctx, const uint64_t *rowptr, uint64_t n, uint64_t items, const uint64_t *items_dev,
+                 uint2 *bounds) {
+    const uint64_t tiles = (items + kTileItems - 1) / kTileItems;
+    if (!tiles) return;
+    const uint32_t grid = (uint32_t)std::min<uint64_t>((tiles + 255) / 256, (uint64_t)ctx.persistent_grid(8));
+    k_tile_bounds<<<grid, 256, 0, ctx.stream>>>(rowptr, n, items, items_dev, bounds);
+    TC_LAUNCHED(ctx);
 }
 
 }  // namespace tc

@@ -250,6 +250,34 @@ __device__ __forceinline__ void tile_rows(const uint64_t *__restrict__ rowptr, u
     __syncthreads();
 }
 
+// Same, with the row bounds of the tile precomputed by tile_bounds (round 2): the two warp
+// searches above are a chain of dependent L2 round trips per tile, which a persistent loop
+// pays once per tile in series.  b = (first row starting after tile_start, first row starting
+// at or after the tile's last item).
+__device__ __forceinline__ void tile_rows_b(const uint64_t *__restrict__ rowptr, uint64_t tile_start,
+                                            uint32_t len, uint2 b, uint32_t *s_row, uint32_t *s_scan) {
+    for (int i = threadIdx.x; i < kTileItems; i += blockDim.x) s_row[i] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(&s_row[0], b.x - 1u);
+    for (uint64_t u = b.x + threadIdx.x; u < b.y; u += blockDim.x)
+        atomicMax(&s_row[rowptr[u] - tile_start], (uint32_t)u);
+    __syncthreads();
+    uint32_t v[kItemsPerThread];
+    uint32_t run = 0;
+#pragma unroll
+    for (int k = 0; k < kItemsPerThread; k++) {
+        run = max(run, s_row[threadIdx.x * kItemsPerThread + k]);
+        v[k] = run;
+    }
+    uint32_t prefix = block_exclusive_scan<MaxOp>(run, s_scan);
+#pragma unroll
+    for (int k = 0; k < kItemsPerThread; k++)
+        s_row[threadIdx.x * kItemsPerThread + k] = max(v[k], prefix);
+    __syncthreads();
+}
+// bounds[t] for the tiles of `items` (host count, or *items_dev when given) CSR items.
+void tile_bounds(Ctx &ctx, const uint64_t *rowptr, uint64_t n, uint64_t items, const uint64_t *items_dev,
+                 uint2 *bounds);
 
 // Digit width of an LSD radix sort over `bits` key bits: 7 when 7-bit digits need no
 // more passes than 8-bit ones (fewer ballots per rank, half the look-back digits), else 8.
