@@ -1,8 +1,8 @@
 // radix.cu -- hand-written stable LSD radix sort (8-bit digits), onesweep style:
 //   1. one histogram kernel reads the keys once and counts the digits of EVERY
 //      pass (shared-memory histograms, one global atomic per digit per block);
-//   2. a tiny kernel turns them into per-pass exclusive digit offsets;
-//   3. per pass ONE kernel: each CTA takes the next tile (atomic ticket, so a
+//   2. per pass ONE kernel (the pass's digit offsets are the exclusive prefix of its histogram,
+//      scanned by every tile together with its own digit counts): each CTA takes the next tile (atomic ticket, so a
 //      tile only ever waits on tiles that already started), ranks its keys
 //      stably inside the tile (ballot-built digit peer masks per warp round), publishes its
 //      per-digit counts, and obtains the exclusive prefix of earlier tiles by
@@ -95,23 +95,6 @@ __global__ void __launch_bounds__(kRsThreads)
     }
 }
 
-// Exclusive scan of each pass's 256 digit counts (one warp per pass).
-__global__ void k_rs_digit_offsets(const uint32_t *__restrict__ hist, int passes,
-                                   uint64_t *__restrict__ offs) {
-    int p = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (p >= passes) return;
-    uint64_t run = 0;
-    for (int c = 0; c < kDigits; c += 32) {
-        uint64_t v = hist[p * kDigits + c + lane], inc = v;
-        for (int o = 1; o < 32; o <<= 1) {
-            uint64_t y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += y;
-        }
-        offs[p * kDigits + c + lane] = run + inc - v;
-        run += __shfl_sync(0xffffffffu, inc, 31);
-    }
-}
-
 // Lanes of `active` holding the same DB-bit digit d as this lane: DB ballots, measured
 // a little faster than __match_any_sync on sm_100a.
 // Per bit: one predicate test, the ballot, one select and one 3-input LOP
@@ -140,7 +123,7 @@ struct RsSmem {
     uint32_t wc[kRsWarps][kDigits];   // per-warp digit counters -> per-warp exclusive offsets
     uint32_t dstart[kDigits];         // tile-local digit start
     uint64_t gbase[kDigits];          // global start of this tile's run of each digit
-    uint32_t scan[kRsWarps];
+    uint64_t scan[kRsWarps];
     uint32_t tile;
 };
 
@@ -148,7 +131,7 @@ template <class K, bool kVals, class SW, int DB>
 __global__ void __launch_bounds__(kRsThreads, TC_RS_MINBLOCKS)
     k_rs_pass(const K *__restrict__ keys, const uint32_t *__restrict__ vals, K *__restrict__ keys_out,
               uint32_t *__restrict__ vals_out, uint64_t cap, const uint64_t *__restrict__ count_dev,
-              int shift, const uint64_t *__restrict__ digit_off, uint32_t *__restrict__ ticket,
+              int shift, const uint32_t *__restrict__ hist_p, uint32_t *__restrict__ ticket,
               SW *__restrict__ status, const uint32_t *__restrict__ gather,
               uint32_t *__restrict__ gather_out, uint32_t *__restrict__ inverse) {
     constexpr SW kFlagAgg = Status<SW>::kFlagAgg, kFlagPre = Status<SW>::kFlagPre;
@@ -222,7 +205,7 @@ __global__ void __launch_bounds__(kRsThreads, TC_RS_MINBLOCKS)
     static_assert(kRsThreads >= kDigits, "one thread per digit");
     const uint32_t d = threadIdx.x;
     const bool is_digit = d < kD;
-    uint32_t cnt = 0;
+    uint32_t cnt = 0, hd = 0;
     SW *my = status + (uint64_t)tile * kD + d;
     if (is_digit) {
 #pragma unroll
@@ -232,8 +215,12 @@ __global__ void __launch_bounds__(kRsThreads, TC_RS_MINBLOCKS)
             cnt += c;
         }
         st_relaxed(my, (SW)((tile == 0 ? kFlagPre : kFlagAgg) | (SW)cnt));
+        hd = hist_p[d];   // this pass's global count of digit d
     }
-    uint32_t dstart = block_exclusive_scan<SumOp>(cnt, S.scan);  // ends with __syncthreads
+    // one 64-bit scan gives both the tile-local digit starts (low word) and the pass's global
+    // digit offsets (high word: exclusive prefix of the histogram; no separate offsets kernel)
+    const uint64_t both = block_exclusive_scan<SumOp64>(((uint64_t)hd << 32) | cnt, S.scan);
+    const uint32_t dstart = (uint32_t)both;
     if (is_digit) S.dstart[d] = dstart;
     __syncthreads();
     // ---- reorder by digit in shared memory (needs only tile-local offsets) overlapped
@@ -277,7 +264,7 @@ __global__ void __launch_bounds__(kRsThreads, TC_RS_MINBLOCKS)
             }
             st_relaxed(my, (SW)(kFlagPre | (SW)(excl + cnt)));
         }
-        S.gbase[d] = digit_off[d] + excl;
+        S.gbase[d] = (both >> 32) + excl;
         reorder();
     }
     __syncthreads();
@@ -311,7 +298,6 @@ static void radix_impl(Ctx &ctx, const K *kin0, const uint32_t *vin0, K *kA, K *
     const int passes = (bits + db - 1) / db;
     const uint32_t tiles = (uint32_t)((capacity + kRsTile - 1) / kRsTile);
     const uint32_t *hist = hist_in;   // digit histograms counted by the producer, or here
-    uint64_t *doff = ctx.alloc<uint64_t>((uint64_t)passes * kDigits);
     uint32_t *tickets = ctx.alloc<uint32_t>(passes);
     // 32-bit status words when every digit prefix (<= capacity) fits in 30 bits
     const bool narrow = capacity < (1ull << 30);
@@ -326,8 +312,6 @@ static void radix_impl(Ctx &ctx, const K *kin0, const uint32_t *vin0, K *kA, K *
         TC_LAUNCHED(ctx);
         hist = h;
     }
-    k_rs_digit_offsets<<<1, 32 * kMaxPasses, 0, ctx.stream>>>(hist, passes, doff);
-    TC_LAUNCHED(ctx);
     const size_t smem = sizeof(RsSmem<K, kVals>);
     auto set_smem = [&](auto kern) {
         TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -344,7 +328,7 @@ static void radix_impl(Ctx &ctx, const K *kin0, const uint32_t *vin0, K *kA, K *
         TC_CUDA(cudaMemsetAsync(status, 0, (size_t)tiles * kDigits * sw, ctx.stream));
         const uint32_t *ga = p == passes - 1 ? gather : nullptr;
         uint32_t *inv = p == passes - 1 ? inverse : nullptr;
-        const uint64_t *dop = doff + (uint64_t)p * kDigits;
+        const uint32_t *dop = hist + (uint64_t)p * kDigits;
 #define TC_RS_LAUNCH(SWT, DBV)                                                                  \
     k_rs_pass<K, kVals, SWT, DBV><<<tiles, kRsThreads, smem, ctx.stream>>>(                     \
         kin, vin, kout, vout, capacity, count_dev, db * p, dop, tickets + p, (SWT *)status, ga, \

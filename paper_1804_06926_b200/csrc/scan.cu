@@ -1,4 +1,4 @@
-// scan.cu -- device-wide exclusive scan (reduce-then-scan) and the block-level
+// scan.cu -- device-wide exclusive scan (single pass, decoupled look-back) and the block-level
 // scan / tile row-search helpers every tile kernel uses.
 #include <algorithm>
 
@@ -12,136 +12,93 @@ constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
+// Single pass (round 2): tiles take a ticket, publish their aggregate, and get the exclusive
+// prefix of earlier tiles by decoupled look-back (one warp, 32 predecessors per step): one
+// launch and one read of the input instead of reduce + (recursive scan) + apply.  With
+// count_dev only the first *count_dev (<= cap) items are scanned; out[count] = the total,
+// also written to *total_out when given.
+constexpr uint64_t kScAgg = 1ull << 62, kScPre = 2ull << 62, kScMask = (1ull << 62) - 1;
 template <class T>
-__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const T *__restrict__ in,
-                                                              uint64_t count,
-                                                              uint64_t *__restrict__ partial) {
-    __shared__ uint64_t s_scratch[kScanThreads / 32];
-    uint64_t base = (uint64_t)blockIdx.x * kScanTile;
-    uint64_t sum = 0;
-#pragma unroll
-    for (int k = 0; k < kScanItems; k++) {
-        uint64_t i = base + (uint64_t)k * kScanThreads + threadIdx.x;
-        if (i < count) sum += (uint64_t)in[i];
-    }
-    sum = block_sum_u64(sum, s_scratch);
-    if (threadIdx.x == 0) partial[blockIdx.x] = sum;
-}
-
-template <class T>
-__global__ void __launch_bounds__(kScanThreads) k_scan_apply(const T *__restrict__ in,
-                                                             uint64_t count,
-                                                             const uint64_t *__restrict__ offsets,
-                                                             uint64_t *__restrict__ out) {
+__global__ void __launch_bounds__(kScanThreads)
+    k_scan_1p(const T *__restrict__ in, uint64_t cap, const uint64_t *__restrict__ count_dev,
+              uint64_t *__restrict__ out, uint64_t *__restrict__ total_out, uint32_t *__restrict__ ticket,
+              uint64_t *__restrict__ status) {
     __shared__ uint64_t s_scan[kScanThreads / 32];
-    uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanItems;
+    __shared__ uint32_t s_tile;
+    __shared__ uint64_t s_excl;
+    const uint64_t count = count_dev ? min(*count_dev, cap) : cap;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    if ((uint64_t)tile * kScanTile > count) return;   // tiles cover [0, count]; nobody waits here
+    const uint64_t base = (uint64_t)tile * kScanTile + (uint64_t)threadIdx.x * kScanItems;
     uint64_t v[kScanItems];
     uint64_t run = 0;
 #pragma unroll
     for (int k = 0; k < kScanItems; k++) {
-        uint64_t i = base + k;
-        uint64_t x = i < count ? (uint64_t)in[i] : 0;
+        const uint64_t i = base + k;
+        const uint64_t x = i < count ? (uint64_t)in[i] : 0;
         v[k] = run;
         run += x;
     }
-    uint64_t prefix = block_exclusive_scan<SumOp64>(run, s_scan) + offsets[blockIdx.x];
+    uint64_t total;
+    const uint64_t pre = block_exclusive_scan<SumOp64>(run, s_scan, &total);
+    if (threadIdx.x < 32) {
+        const uint32_t lane = threadIdx.x;
+        uint64_t excl = 0;
+        if (lane == 0)
+            asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(status + tile),
+                         "l"((tile == 0 ? kScPre : kScAgg) | total) : "memory");
+        if (tile > 0) {
+            for (int64_t t = (int64_t)tile - 1;; t -= 32) {
+                const int64_t idx = t - (int64_t)lane;
+                uint64_t sw = kScPre;
+                if (idx >= 0) asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(sw) : "l"(status + idx) : "memory");
+                while (__any_sync(0xffffffffu, (sw & ~kScMask) == 0))
+                    if ((sw & ~kScMask) == 0)
+                        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(sw) : "l"(status + idx) : "memory");
+                const uint32_t pm = __ballot_sync(0xffffffffu, (sw & kScPre) != 0);
+                const int first = pm ? __ffs(pm) - 1 : 32;
+                excl += warp_sum_u64((int)lane <= first ? (sw & kScMask) : 0ull);
+                if (pm) break;
+            }
+            if (lane == 0)
+                asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(status + tile),
+                             "l"(kScPre | (excl + total)) : "memory");
+        }
+        if (lane == 0) s_excl = excl;
+    }
+    __syncthreads();
+    const uint64_t prefix = pre + s_excl;
 #pragma unroll
     for (int k = 0; k < kScanItems; k++) {
-        uint64_t i = base + k;
-        if (i <= count) out[i] = v[k] + prefix;   // out[count] = total
-    }
-}
-
-template <class T>
-static void scan_impl(Ctx &ctx, const T *in, uint64_t *out, uint64_t count) {
-    // tiles cover [0, count] inclusive so the total lands in out[count]
-    uint64_t items = count + 1;
-    uint64_t tiles = (items + kScanTile - 1) / kScanTile;
-    uint64_t *partial = ctx.alloc<uint64_t>(tiles);
-    uint64_t *offsets = ctx.alloc<uint64_t>(tiles + 1);
-    k_scan_reduce<T><<<(unsigned)tiles, kScanThreads, 0, ctx.stream>>>(in, count, partial);
-    TC_LAUNCHED(ctx);
-    if (tiles == 1) {
-        TC_CUDA(cudaMemsetAsync(offsets, 0, sizeof(uint64_t), ctx.stream));
-    } else {
-        scan_impl<uint64_t>(ctx, partial, offsets, tiles);
-    }
-    k_scan_apply<T><<<(unsigned)tiles, kScanThreads, 0, ctx.stream>>>(in, count, offsets, out);
-    TC_LAUNCHED(ctx);
-}
-
-// Device-count variant: only the first *count_dev (<= cap) items are scanned; blocks past
-// them exit at once (no n-sized traffic when few items are live), and the total is also
-// written to *total_out.
-__global__ void __launch_bounds__(kScanThreads) k_scan_reduce_dc(const uint32_t *__restrict__ in,
-                                                                 const uint64_t *__restrict__ count_dev,
-                                                                 uint64_t *__restrict__ partial) {
-    __shared__ uint64_t s_scratch[kScanThreads / 32];
-    const uint64_t count = *count_dev;
-    const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
-    if (base >= count) {
-        if (threadIdx.x == 0) partial[blockIdx.x] = 0;
-        return;
-    }
-    uint64_t sum = 0;
-#pragma unroll
-    for (int k = 0; k < kScanItems; k++) {
-        uint64_t i = base + (uint64_t)k * kScanThreads + threadIdx.x;
-        if (i < count) sum += (uint64_t)in[i];
-    }
-    sum = block_sum_u64(sum, s_scratch);
-    if (threadIdx.x == 0) partial[blockIdx.x] = sum;
-}
-
-__global__ void __launch_bounds__(kScanThreads) k_scan_apply_dc(const uint32_t *__restrict__ in,
-                                                                const uint64_t *__restrict__ count_dev,
-                                                                const uint64_t *__restrict__ offsets,
-                                                                uint64_t *__restrict__ out,
-                                                                uint64_t *__restrict__ total_out) {
-    __shared__ uint64_t s_scan[kScanThreads / 32];
-    const uint64_t count = *count_dev;
-    if ((uint64_t)blockIdx.x * kScanTile > count) return;   // block-uniform
-    uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanItems;
-    uint64_t v[kScanItems];
-    uint64_t run = 0;
-#pragma unroll
-    for (int k = 0; k < kScanItems; k++) {
-        uint64_t i = base + k;
-        uint64_t x = i < count ? (uint64_t)in[i] : 0;
-        v[k] = run;
-        run += x;
-    }
-    uint64_t prefix = block_exclusive_scan<SumOp64>(run, s_scan) + offsets[blockIdx.x];
-#pragma unroll
-    for (int k = 0; k < kScanItems; k++) {
-        uint64_t i = base + k;
+        const uint64_t i = base + k;
         if (i <= count) out[i] = v[k] + prefix;
-        if (i == count) *total_out = v[k] + prefix;
+        if (i == count && total_out) *total_out = v[k] + prefix;
     }
+}
+
+template <class T>
+static void scan_1p(Ctx &ctx, const T *in, uint64_t *out, uint64_t cap, const uint64_t *count_dev,
+                    uint64_t *total_out) {
+    const uint64_t tiles = (cap + 1 + kScanTile - 1) / kScanTile;
+    uint64_t *st = ctx.alloc<uint64_t>(tiles + 1);   // status words, then the ticket
+    TC_CUDA(cudaMemsetAsync(st, 0, (tiles + 1) * sizeof(uint64_t), ctx.stream));
+    k_scan_1p<T><<<(unsigned)tiles, kScanThreads, 0, ctx.stream>>>(in, cap, count_dev, out, total_out,
+                                                                   (uint32_t *)(st + tiles), st);
+    TC_LAUNCHED(ctx);
 }
 
 void scan_exclusive_dc(Ctx &ctx, const uint32_t *in, uint64_t *out, uint64_t cap,
                        const uint64_t *count_dev, uint64_t *total_out) {
-    uint64_t tiles = (cap + 1 + kScanTile - 1) / kScanTile;
-    uint64_t *partial = ctx.alloc<uint64_t>(tiles);
-    uint64_t *offsets = ctx.alloc<uint64_t>(tiles + 1);
-    k_scan_reduce_dc<<<(unsigned)tiles, kScanThreads, 0, ctx.stream>>>(in, count_dev, partial);
-    TC_LAUNCHED(ctx);
-    if (tiles == 1) {
-        TC_CUDA(cudaMemsetAsync(offsets, 0, sizeof(uint64_t), ctx.stream));
-    } else {
-        scan_impl<uint64_t>(ctx, partial, offsets, tiles);
-    }
-    k_scan_apply_dc<<<(unsigned)tiles, kScanThreads, 0, ctx.stream>>>(in, count_dev, offsets, out,
-                                                                       total_out);
-    TC_LAUNCHED(ctx);
+    scan_1p<uint32_t>(ctx, in, out, cap, count_dev, total_out);
 }
 
 void scan_exclusive(Ctx &ctx, const uint32_t *in, uint64_t *out, uint64_t count) {
-    scan_impl<uint32_t>(ctx, in, out, count);
+    scan_1p<uint32_t>(ctx, in, out, count, nullptr, nullptr);
 }
 void scan_exclusive(Ctx &ctx, const uint64_t *in, uint64_t *out, uint64_t count) {
-    scan_impl<uint64_t>(ctx, in, out, count);
+    scan_1p<uint64_t>(ctx, in, out, count, nullptr, nullptr);
 }
 
 // ------------------------------------------------------------------ tile row bounds
