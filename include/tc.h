@@ -300,12 +300,13 @@ tc_status tc_shard_route(uint64_t n, const uint64_t *off_plus, const uint32_t *c
  *   probed with the n_entries received entries, its SHORT / SEARCH edges (received from itself),
  *   the dense-core edges of its interleaved 2048-edge blocks (count mode); n < 2^30.  *partial_dev (uint64) = its share; with
  *   TC_PER_VERTEX (needs newid) per_vertex_partial (n, input ids) = its t(v) shares.  m = the
- *   oriented edge count (off_plus[n]).  [all-reduce partial_dev (and per_vertex_partial)] */
+ *   oriented edge count (off_plus[n]).  ms_a6 (host, nullable): the a6 + a7 kernels' CUDA-event
+ *   span (the owner-structure build excluded).  [all-reduce partial_dev (and per_vertex_partial)] */
 tc_status tc_shard_count(uint64_t n, uint64_t m, const uint64_t *off_plus, const uint32_t *col_plus,
                          const uint32_t *dplus, const uint32_t *newid, uint64_t n_entries,
                          const uint32_t *entries, uint32_t flags, const tc_options *opt, int rank,
                          int world, uint64_t e_begin, uint64_t e_end, uint64_t *partial_dev,
-                         uint64_t *per_vertex_partial);
+                         uint64_t *per_vertex_partial, double *ms_a6);
 
 /* Steps a1-a4 only ("Form_Filtered_Edge_List", Alg. 2): writes the
  * oriented, compacted CSR N+ (off_plus: n+1 entries; col_plus: capacity m

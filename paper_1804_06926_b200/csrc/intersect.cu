@@ -927,7 +927,10 @@ static void launch_all(Ctx &ctx, const Oriented &g, const Bins &bins, uint64_t *
     // fill the SMs the hub kernel's tail leaves idle (all add into the same total).
     SideStream side(ctx);   // the side work depends only on binning; joined on every path
     cudaStream_t s2 = side.s;
-    k_hash_cta<CM, true><<<ctx.persistent_grid(8), kIxThreads, 0, ctx.stream>>>(
+#ifndef TC_HASH_CTA_GRID
+#define TC_HASH_CTA_GRID 8   // CTAs per SM of the persistent bitmap-owner kernel
+#endif
+    k_hash_cta<CM, true><<<ctx.persistent_grid(TC_HASH_CTA_GRID), kIxThreads, 0, ctx.stream>>>(
         bins.tasks_bitmap, bins.ntasks_bitmap, bins.hp, total, cr);
     TC_LAUNCHED(ctx);
     k_hash_cta<CM, false><<<ctx.persistent_grid(8), kIxThreads, 0, ctx.stream>>>(

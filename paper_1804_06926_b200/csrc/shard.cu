@@ -642,8 +642,9 @@ tc_status tc_shard_count(uint64_t n, uint64_t m, const uint64_t *off_plus, const
                          const uint32_t *dplus, const uint32_t *newid, uint64_t n_entries,
                          const uint32_t *entries, uint32_t flags, const tc_options *opt, int rank,
                          int world, uint64_t e_begin, uint64_t e_end, uint64_t *partial_dev,
-                         uint64_t *per_vertex_partial) {
+                         uint64_t *per_vertex_partial, double *ms_a6) {
     return run_phase(opt, [&](Ctx &ctx, const tc_options &o) {
+        if (ms_a6) *ms_a6 = 0.0;
         check_opts(o);
         check_world(rank, world);
         if (flags & ~(uint32_t)TC_PER_VERTEX) throw Error{TC_EINVAL, "tc_shard_count: flags: TC_PER_VERTEX only"};
@@ -755,8 +756,19 @@ tc_status tc_shard_count(uint64_t n, uint64_t m, const uint64_t *off_plus, const
             cr.mode = kCmVertex;
             cr.pv = pv_new;
         }
+        Timer *tm = ms_a6 ? new Timer(ctx.stream) : nullptr;
+        struct Del {
+            Timer *t;
+            ~Del() { delete t; }
+        } del{tm};
+        if (tm) tm->begin(kIntersect);
         intersect_all(ctx, g, bins, partial_dev, cr);
+        if (tm) tm->end(kIntersect);
         if (pv) per_vertex_to_original(ctx, g, pv_new, per_vertex_partial);
+        if (tm) {
+            TC_CUDA(cudaStreamSynchronize(ctx.stream));
+            *ms_a6 = tm->ms(kIntersect);
+        }
     });
 }
 

@@ -38,7 +38,7 @@ def _lib():
         lib.tc_shard_work.argtypes = [u64, vp, vp, vp, u32, po, u64, u64, u64, u64, vp, vp, vp]
         lib.tc_shard_route.argtypes = [u64, vp, vp, vp, vp, vp, vp, u32, po, i, i, u64, u64, vp, vp]
         lib.tc_shard_count.argtypes = [u64, u64, vp, vp, vp, vp, u64, vp, u32, po, i, i, u64, u64,
-                                       vp, vp]
+                                       vp, vp, ctypes.POINTER(ctypes.c_double)]
         for f in ("tc_shard_orient", "tc_shard_partition", "tc_shard_rows", "tc_shard_work",
                   "tc_shard_route", "tc_shard_count"):
             getattr(lib, f).restype = ctypes.c_int
@@ -125,16 +125,20 @@ def shard_route(n, off, col_plus, dplus, cnt, ln, spans, rank, world, e_begin, e
 
 
 def shard_count(n, off, col_plus, dplus, newid, entries, rank, world, e_begin, e_end, partial, *,
-                per_vertex_partial=None, stream=None, **opts):
+                per_vertex_partial=None, stream=None, a6_ms=None, **opts):
     """P6: this rank's share of the count into partial (int64[1], overwritten) [and t(v)
-    partials in input ids into per_vertex_partial (int64[n], overwritten)]."""
+    partials in input ids into per_vertex_partial (int64[n], overwritten)].  a6_ms: a list that
+    receives the a6 kernels' CUDA-event span."""
     m = col_plus.numel()
+    ms = ctypes.c_double(0.0)
     o = _options(stream=stream, device=off.device, **opts)
     flags = TC_PER_VERTEX if per_vertex_partial is not None else 0
     _check(_lib().tc_shard_count(n, m, off.data_ptr(), col_plus.data_ptr(), dplus.data_ptr(),
                                  _ptr(newid), entries.numel() // 3, _ptr(entries), flags, ctypes.byref(o),
                                  rank, world, e_begin, e_end, partial.data_ptr(),
-                                 _ptr(per_vertex_partial)))
+                                 _ptr(per_vertex_partial), ctypes.byref(ms) if a6_ms is not None else None))
+    if a6_ms is not None:
+        a6_ms.append(ms.value)
 
 
 # ---------------------------------------------------------------- one rank against a Comm
@@ -284,8 +288,11 @@ def emulate(rowptr, col, world, *, per_vertex=False, timed=False, **opts):
         pv = torch.zeros(n, dtype=torch.int64, device=dev) if per_vertex else None
         if r == prof:
             torch.cuda.profiler.start()
+        a6 = [] if timed else None
         run("count", lambda r=r: shard_count(n, off, col_plus[:cb[G]], dplus, newid, rent[r], r, G, cb[r],
-                                             cb[r + 1], partial, per_vertex_partial=pv, **opts), r)
+                                             cb[r + 1], partial, per_vertex_partial=pv, a6_ms=a6, **opts), r)
+        if timed:
+            rep.setdefault("a6_ms", [0.0] * G)[r] = a6[0]
         if r == prof:
             torch.cuda.profiler.stop()
         total += int(partial.item())

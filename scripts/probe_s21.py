@@ -4,6 +4,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import graphgen as G
 import paper_1804_06926_b200 as tc
+if os.environ.get("TC_LIB"):
+    tc._LIB_PATH = os.environ["TC_LIB"]
 scale = int(sys.argv[1]) if len(sys.argv) > 1 else 21
 t = time.time(); g = G.rmat(scale, 16); print("gen", round(time.time() - t, 2), "s arcs", g.arcs, flush=True)
 rp = torch.from_numpy(g.rowptr.view(np.int64)).cuda(); cl = torch.from_numpy(g.col.view(np.int32)).cuda()
