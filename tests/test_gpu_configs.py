@@ -87,3 +87,22 @@ def test_duplicated_karate4_wide_status_words():
     for _ in range(3):
         t = 2 * np.outer(t, KARATE_T).reshape(-1)
     assert (pv.cpu().numpy().view(np.uint64) == t).all()
+
+
+def test_config_rmat26_against_recorded_oracle():
+    """R-MAT s26 ef16 (the top of BASELINE configs[4]: 1.07e9 raw arcs) against the oracle
+    total recorded by scripts/check_s24.py 26 (which calls only oracle/; 525 s on 16 cores,
+    too slow to repeat here): both a1 sort orders and the sharded pipeline emulated at world 8."""
+    import json
+    import os
+    from paper_1804_06926_b200 import shard
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    rec = json.loads(open(os.path.join(root, "profiles", "r02_s26_parity.json")).read().strip().splitlines()[-1])
+    g = G.rmat(26, 16)
+    assert g.arcs == rec["raw_arcs"]
+    rp, cl = on_dev(g.rowptr, g.col)
+    del g
+    for method in (0, 1):
+        assert tc.count_ex(rp, cl, clean_method=method) == rec["T_oracle"]
+    torch.cuda.synchronize()
+    assert shard.emulate(rp, cl, 8)[0] == rec["T_oracle"]
