@@ -52,6 +52,8 @@ def parse():
                          "sharded (shard.py / csrc/shard.cu)")
     ap.add_argument("--one-call", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--clean-input", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--no-projection", action="store_true",
+                    help="skip the one-GPU multi-GPU projection (shard.emulate) of the N = 1 line")
     ap.add_argument("--no-ncu", action="store_true",
                     help="skip the ncu DRAM-traffic capture of the a6 kernels (roofline.traffic)")
     return ap.parse_args()
@@ -328,6 +330,46 @@ A6_KERNELS = "regex:k_hash|k_short|k_merge|k_search"
 NCU_METRICS = ("dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
                "l1tex__throughput.avg.pct_of_peak_sustained_elapsed,"
                "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed,lts__t_sector_hit_rate.pct")
+
+
+def multi_gpu_projection(tc, torch, graphgen, np, rp, cl, one_gpu_ms, peak_gbs):
+    """The sharded multi-GPU pipeline projected from ONE GPU (shard.emulate, timed: every rank's
+    phases in turn with CUDA events, the collectives charged at the measured NVLink rates); the
+    bench workload at worlds 2 / 4 / 8 and R-MAT s24 (BASELINE configs[4]) at world 8.  Context
+    for the N > 1 runs, never a measured multi-GPU number."""
+    from paper_1804_06926_b200 import shard
+
+    def one(rp_, cl_, worlds, base_ms, b_a6):
+        out = {}
+        for w in worlds:
+            shard.emulate(rp_, cl_, w)   # warm
+            total, _, rep = shard.emulate(rp_, cl_, w, timed=True)
+            out[f"world{w}"] = {
+                "T": total, "projected_step_ms": rep["step_ms_overlapped"],
+                "speedup_vs_one_gpu": base_ms / rep["step_ms_overlapped"],
+                "slowest_a6_ms": max(rep["a6_ms"]),
+                "a6_aggregate_hbm_frac": b_a6 / (w * max(rep["a6_ms"]) * 1e-3) / (peak_gbs * 1e9),
+                "phases_ms_slowest_rank": {k: max(v) for k, v in rep["phases"].items()},
+                "collectives_ms": rep["collectives"]}
+        return out
+
+    _, st = tc.count_ex(rp, cl, with_stats=True)
+    res = {"method": "one-GPU emulation (shard.emulate): each rank's phases timed in turn with CUDA "
+                     "events; collectives charged at 770 GB/s (all-gather / all-to-all) and 725 GB/s "
+                     "(all-reduce); the col+ all-gather overlapped with binning as run_rank does.  "
+                     "NCCL was not run (one GPU per box this round)",
+           "bench_workload": one(rp, cl, (2, 4, 8), one_gpu_ms, st["bytes_hash"] + st["bytes_core"])}
+    g24 = graphgen.rmat(24, 16)
+    rp24 = torch.from_numpy(g24.rowptr.view(np.int64)).to(rp.device)
+    cl24 = torch.from_numpy(g24.col.view(np.int32)).to(rp.device)
+    del g24
+    for _ in range(2):
+        _, st24 = tc.count_ex(rp24, cl24, with_stats=True)
+    res["rmat-s24-ef16"] = {"one_gpu_ms": st24["ms_total"], **one(rp24, cl24, (8,), st24["ms_total"],
+                                                                  st24["bytes_hash"] + st24["bytes_core"])}
+    del rp24, cl24
+    torch.cuda.empty_cache()
+    return res
 
 
 def clean_csr_of(tc, torch, rp, cl):
@@ -649,6 +691,8 @@ def main():
         line["small_graph"] = small_graph_latency(tc, torch, graphgen, dev)
         line["next_rows"].update(next_rows_23(tc, torch, np, graphgen, rp, cl, flush, stream, m,
                                               T_total, ms))
+    if world == 1 and not args.no_projection:
+        line["multi_gpu_projection"] = multi_gpu_projection(tc, torch, graphgen, np, rp, cl, ms, peak)
     if world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline(g, m)
         assert cb.pop("T") == T_total, "oracle and CUDA path disagree"

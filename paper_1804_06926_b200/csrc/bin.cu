@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(kTileThreads, TC_EDGES_MINBLOCKS)
     k_edges(HashParams hp, const uint64_t *__restrict__ m_dev, uint32_t *__restrict__ ulo,
             uint32_t *__restrict__ obits, uint32_t *__restrict__ tcount,
             uint2 *__restrict__ b_short, uint2 *__restrict__ b_merge, uint2 *__restrict__ b_search,
-            uint64_t *__restrict__ counts) {
+            uint64_t *__restrict__ counts, const uint2 *__restrict__ tb) {
     __shared__ uint32_t s_row[kTileItems];
     __shared__ uint32_t s_scan[kTileThreads / 32];
     __shared__ uint64_t s_red[kTileThreads / 32];
@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(kTileThreads, TC_EDGES_MINBLOCKS)
         return;
     }
     uint32_t len = (uint32_t)min((uint64_t)kTileItems, m - t0);
-    tile_rows(hp.off, hp.n, t0, len, s_row, s_scan);
+    tile_rows_tb(hp.off, hp.n, blockIdx.x, t0, len, tb, s_row, s_scan);
     uint64_t W = 0, probe = 0, skipped = 0, hashed = 0, outs = 0, cedges = 0, cprobe = 0;
     // striped: each warp handles 32 consecutive edges per round (warp-aggregated
     // appends); the loads of kBatch rounds are issued before any is used
@@ -507,9 +507,14 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
     uint64_t *toff = ctx.alloc<uint64_t>(tiles + 1), *ooff = ctx.alloc<uint64_t>(n + 1);
     uint32_t *in_cnt = ctx.alloc<uint32_t>(n + 1);
     if (tiles) {
+        uint2 *tb = nullptr;
+        if (TC_TILE_BOUNDS) {
+            tb = ctx.alloc<uint2>(tiles + 1);
+            tile_bounds(ctx, g.off, n, cap, g.m_dev, tb);
+        }
         k_edges<<<tiles, kTileThreads, 0, ctx.stream>>>(hp, g.m_dev, ulo, obits, tcount,
                                                         bins.edges[0], bins.edges[1], bins.edges[2],
-                                                        bins.count);
+                                                        bins.count, tb);
         TC_LAUNCHED(ctx);
     }
     scan_exclusive(ctx, tcount, toff, tiles);

@@ -275,6 +275,16 @@ __device__ __forceinline__ void tile_rows_b(const uint64_t *__restrict__ rowptr,
         s_row[threadIdx.x * kItemsPerThread + k] = max(v[k], prefix);
     __syncthreads();
 }
+#ifndef TC_TILE_BOUNDS
+#define TC_TILE_BOUNDS 0   // k_edges / k_clean_keys on precomputed row bounds: measured no change (s21 6.57 vs 6.57 ms)
+#endif
+// tile_rows with the bounds precomputed when tb != nullptr (TC_TILE_BOUNDS), else searched.
+__device__ __forceinline__ void tile_rows_tb(const uint64_t *__restrict__ rowptr, uint64_t n, uint64_t tile,
+                                             uint64_t tile_start, uint32_t len, const uint2 *__restrict__ tb,
+                                             uint32_t *s_row, uint32_t *s_scan) {
+    if (tb) tile_rows_b(rowptr, tile_start, len, tb[tile], s_row, s_scan);
+    else tile_rows(rowptr, n, tile_start, len, s_row, s_scan);
+}
 // bounds[t] for the tiles of `items` (host count, or *items_dev when given) CSR items.
 void tile_bounds(Ctx &ctx, const uint64_t *rowptr, uint64_t n, uint64_t items, const uint64_t *items_dev,
                  uint2 *bounds);
