@@ -262,6 +262,9 @@ __global__ void k_owners(const uint32_t *__restrict__ dplus, const uint32_t *__r
     int lane = threadIdx.x & 31;
     uint32_t lt = (1u << lane) - 1u;
     uint64_t s_hashed = 0, s_probe = 0, s_W = 0;   // shard statistics (this rank's owners)
+    // world 1: k_edges counted the HASH edges (counts[3]); none -> every owner is empty (the
+    // in-list scans below would read every ulo entry for nothing: road mesh 0.23 ms)
+    const bool any_hash = shard || counts[3] != 0;
     for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < end; u += stride) {
         int kind = -1;
         if (u < n) {
@@ -283,6 +286,10 @@ __global__ void k_owners(const uint32_t *__restrict__ dplus, const uint32_t *__r
                         s_W += du + (r.y - r.x);
                     }
                 }
+            } else if (!any_hash) {   // no HASH edge at all (road-like graphs): nothing to own
+                ooff[u] = 0;
+                in_cnt[u] = 0;
+                pcnt[u] = 0;
             } else {
                 const uint64_t o0 = op.at(off[u]);
                 ooff[u] = o0;
