@@ -150,7 +150,15 @@ typedef struct {
                                    bits only (3-4 passes; duplicates share a run of equal
                                    hash), 1 = sorted in full (min, max) order (6-8 passes).
                                    Same results                                                */
-    uint32_t reserved[7];       /* must be zero                                                 */
+    uint32_t graph_cache;       /* 1 = tc_count / tc_count_ex on device pointers (no stats,
+                                   TC_PRUNE, TC_VALIDATE or allocator hook) is captured into a
+                                   CUDA graph on first use and REPLAYED by later calls with the
+                                   same arguments (sizes, pointers, flags, options; per thread,
+                                   up to 4 graphs): one graph launch instead of ~36 kernels and
+                                   ~60 workspace allocations -- for launch-bound small and
+                                   mid-size graphs.  The graph keeps its workspace reserved
+                                   between calls.  0 (default) = off                           */
+    uint32_t reserved[6];       /* must be zero                                                 */
 } tc_options;
 
 typedef struct {

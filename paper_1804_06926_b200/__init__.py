@@ -51,7 +51,8 @@ class Options(ctypes.Structure):
                 ("stream", ctypes.c_void_p), ("prune_rounds", ctypes.c_uint32),
                 ("keep_workspace", ctypes.c_uint32), ("alloc", ALLOC_FN), ("free", FREE_FN),
                 ("alloc_ctx", ctypes.c_void_p), ("tiny_max_n", ctypes.c_uint32),
-                ("clean_method", ctypes.c_uint32), ("reserved", ctypes.c_uint32 * 7)]
+                ("clean_method", ctypes.c_uint32), ("graph_cache", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint32 * 6)]
 
 
 def _torch_raw_alloc(ctx, size, stream):
@@ -216,7 +217,7 @@ def _flags(clean=False, sorted_rows=False, per_vertex=False, validate=False, pru
 
 def _options(stream=None, force_variant=None, short_max=None, skew_ratio=None, hub_min_dplus=None,
              prune_rounds=None, on_device=True, allocator=None, device=None, keep_workspace=None,
-             tiny_max_n=None, clean_method=None):
+             tiny_max_n=None, clean_method=None, graph_cache=None):
     """tc_options for one call.  Device calls default to the current stream of the inputs'
     device and to torch's caching allocator for the workspace."""
     o = Options()
@@ -227,8 +228,9 @@ def _options(stream=None, force_variant=None, short_max=None, skew_ratio=None, h
     o.stream = stream or None
     if allocator is None and on_device:
         # TC_ALLOCATOR=library: the library's own pool (compute-sanitizer sees each block;
-        # torch's caching allocator sub-allocates large segments)
-        allocator = os.environ.get("TC_ALLOCATOR", "torch")
+        # torch's caching allocator sub-allocates large segments); graph replay owns its
+        # workspace (graph memory), so it takes no hook
+        allocator = "library" if graph_cache else os.environ.get("TC_ALLOCATOR", "torch")
     hooks = _hook_pair(allocator)
     if hooks is not None:
         o.alloc, o.free = hooks
@@ -248,6 +250,8 @@ def _options(stream=None, force_variant=None, short_max=None, skew_ratio=None, h
         o.tiny_max_n = tiny_max_n
     if clean_method is not None:
         o.clean_method = clean_method
+    if graph_cache is not None:
+        o.graph_cache = int(bool(graph_cache))
     return o
 
 

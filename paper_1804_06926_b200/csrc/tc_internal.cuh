@@ -59,6 +59,7 @@ struct Ctx {
     tc_free_fn hook_free = nullptr;
     void *hook_ctx = nullptr;
     cudaMemPool_t pool = nullptr;    // library pool (no hook)
+    bool graph_alloc = false;        // under CUDA graph capture: graph memory nodes
     uint64_t bytes_live = 0, bytes_peak = 0, n_allocs = 0;
     std::vector<std::pair<void *, size_t>> allocs;
 
@@ -71,6 +72,12 @@ struct Ctx {
             p = hook_alloc(hook_ctx, bytes, (void *)stream);
             if (!p)
                 throw Error{TC_ENOMEM, "tc_options.alloc(" + std::to_string(bytes) + " B) returned NULL"};
+        } else if (graph_alloc) {
+            cudaError_t e = cudaMallocAsync(&p, bytes, stream);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                throw Error{TC_ECUDA, std::string("cudaMallocAsync under capture: ") + cudaGetErrorString(e)};
+            }
         } else {
             cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, pool, stream);
             if (e != cudaSuccess) {
