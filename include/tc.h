@@ -404,7 +404,8 @@ uint64_t tc_launches_issued(void);
 const char *tc_last_error(void);
 
 /* Return the library pool's cached workspace on `device` (-1 = current device) to the
- * driver.  Safe at any time; calls in flight keep what they hold. */
+ * driver, and drop the calling thread's replay graphs of that device (graph_cache) with the
+ * graph memory they reserved (synchronises the device).  Calls in flight keep what they hold. */
 tc_status tc_trim_workspace(int device);
 
 /* Library version string. */

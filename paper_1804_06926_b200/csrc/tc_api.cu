@@ -741,6 +741,17 @@ tc_status tc_trim_workspace(int device) {
         if (device < 0) TC_CUDA(cudaGetDevice(&device));
         DeviceState &d = device_state(device);
         TC_CUDA(cudaMemPoolTrimTo(d.pool, 0));
+        // this thread's replay graphs (graph_cache) of the device, and the graph memory they held
+        auto &cache = graph_cache();
+        for (size_t i = 0; i < cache.size();)
+            if (cache[i].key.device == device) {
+                cudaGraphExecDestroy(cache[i].exec);
+                cache.erase(cache.begin() + i);
+            } else {
+                i++;
+            }
+        TC_CUDA(cudaDeviceSynchronize());
+        TC_CUDA(cudaDeviceGraphMemTrim(device));
     } catch (const Error &e) {
         set_error(e.msg);
         return e.status;

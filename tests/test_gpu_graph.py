@@ -63,3 +63,14 @@ def test_graph_replay_clean_input_and_tiny():
     kr, kc = on_dev(k.rowptr, k.col)
     for _ in range(3):   # the one-kernel path captured too
         assert tc.count_ex(kr, kc, graph_cache=1) == 45
+
+
+def test_trim_drops_replay_graphs():
+    g = G.rmat(11, 16, seed=3)
+    T = O.count(g.n, g.rowptr, g.col)
+    rp, cl = on_dev(g.rowptr, g.col)
+    for _ in range(2):
+        assert tc.count_ex(rp, cl, graph_cache=1, tiny_max_n=0) == T
+    tc.trim_workspace()
+    for _ in range(2):   # captured again after the trim
+        assert tc.count_ex(rp, cl, graph_cache=1, tiny_max_n=0) == T
