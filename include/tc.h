@@ -257,8 +257,10 @@ tc_status tc_count_edges_shard(uint64_t n, uint64_t m_edges, const uint64_t *edg
  * rank runs the six phases below; between them the CALLER runs the collective named in
  * brackets (paper_1804_06926_b200/dist.py: NCCL; shard.py: a one-GPU emulation).  All
  * pointers are device pointers on the current device unless marked host; outputs are
- * caller-owned and overwritten; every phase is synchronous.  world <= 64; n < 2^32 and fewer
- * than 2^31 oriented edges; force_variant must be AUTO.  Summing the ranks' partials gives
+ * caller-owned and overwritten; every phase is synchronous.  world <= 64; n < 2^30 and fewer
+ * than 2^31 oriented edges; force_variant must be AUTO.  The buffers passed from one phase to
+ * the next are trusted (produced by the previous phase and the collective); sizes named by the
+ * caller (m_recv, col_begin, n_entries) must be the ones those produced.  Summing the ranks' partials gives
  * tc_count's total (and, with TC_PER_VERTEX, its t(v)) exactly.
  *
  * tc_shard_orient: newid (n) = the rank relabelling of Alg. 2 (rank = (d, id)) from
