@@ -490,7 +490,7 @@ tc_status tc_shard_orient(uint64_t n, uint64_t m_local, const uint64_t *edges, c
                           uint32_t *dst, uint32_t *dplus) {
     return run_phase(opt, [&](Ctx &ctx, const tc_options &o) {
         if (flags & ~(uint32_t)TC_ID_ORDER) throw Error{TC_EINVAL, "tc_shard_orient: flags: TC_ID_ORDER only"};
-        if (n >= (1ull << 32) || m_local >= (1ull << 31)) throw Error{TC_EINVAL, "n < 2^32, m < 2^31"};
+        if (n >= (1ull << 30) || m_local >= (1ull << 31)) throw Error{TC_EINVAL, "the sharded pipeline needs n < 2^30, m < 2^31"};
         check_device(edges, ctx.device, "edges");
         check_device(degrees, ctx.device, "degrees");
         check_device(newid, ctx.device, "newid");
