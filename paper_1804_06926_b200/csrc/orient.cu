@@ -149,25 +149,54 @@ __global__ void __launch_bounds__(kTileThreads)
 // Also a2 (fused): the degrees of the cleaned graph.  A thread's unique keys are grouped by
 // min (the sort order), so the min side takes one atomic per run of equal mins, the max side
 // one per key.
+// TC_UNIQUE_SMEM: the tile's keys are read with coalesced (striped) loads into shared memory
+// and each thread takes its kItemsPerThread consecutive keys from there (padded rows: no bank
+// conflicts), and the unique keys are staged in shared memory and written out coalesced --
+// instead of per-thread runs of 64 bytes at a 64-byte lane stride on both sides.
+#ifndef TC_UNIQUE_SMEM
+#define TC_UNIQUE_SMEM 1
+#endif
+constexpr int kUqPad = kItemsPerThread + 1;   // shared row of a thread's keys, padded
 __global__ void __launch_bounds__(kTileThreads)
     k_unique_scatter(const uint64_t *__restrict__ keys, uint64_t M, const uint64_t *__restrict__ count_dev,
                      uint64_t *__restrict__ m_out, uint64_t *__restrict__ out, int b, int hb,
                      uint32_t *__restrict__ deg) {
     __shared__ uint32_t s_scan[kTileThreads / 32];
     __shared__ uint64_t s_base;
+#if TC_UNIQUE_SMEM
+    __shared__ uint64_t s_k[kTileThreads * kUqPad];
+#endif
     if (count_dev) {   // the keys are a compacted prefix (tc_clean_shard): tiles past it exit
         const uint64_t c = *count_dev;
         M = c < M ? c : M;
     }
-    if ((uint64_t)blockIdx.x * kTileItems >= M) return;
-    const uint64_t base = (uint64_t)blockIdx.x * kTileItems + (uint64_t)threadIdx.x * kItemsPerThread;
+    const uint64_t t0 = (uint64_t)blockIdx.x * kTileItems;
+    if (t0 >= M) return;
+    const uint64_t base = t0 + (uint64_t)threadIdx.x * kItemsPerThread;
     uint64_t kk[kItemsPerThread];
     bool dup[kItemsPerThread];
+#if TC_UNIQUE_SMEM
+    const uint32_t len = (uint32_t)min((uint64_t)kTileItems, M - t0);
+#pragma unroll
+    for (int k = 0; k < kItemsPerThread; k++) {   // striped global -> padded rows
+        const uint32_t i = k * kTileThreads + threadIdx.x;
+        s_k[(i / kItemsPerThread) * kUqPad + i % kItemsPerThread] = i < len ? keys[t0 + i] : ~0ull;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kItemsPerThread; k++) kk[k] = s_k[threadIdx.x * kUqPad + k];
+    // the key before this thread's first one: the previous row's last (the previous tile's
+    // last key for thread 0)
+    const uint64_t before = threadIdx.x ? s_k[(threadIdx.x - 1) * kUqPad + kItemsPerThread - 1]
+                                        : (t0 ? keys[t0 - 1] : ~0ull);
+#else
 #pragma unroll
     for (int k = 0; k < kItemsPerThread; k++) {
         const uint64_t i = base + k;
         kk[k] = i < M ? keys[i] : ~0ull;
     }
+    const uint64_t before = base > 0 && base < M ? keys[base - 1] : ~0ull;
+#endif
     const uint64_t lowm = hb == 0 ? ~0ull : (1ull << (b + hb)) - 1;
     // earlier keys of the same run among the thread's own items ...
 #pragma unroll
@@ -178,9 +207,9 @@ __global__ void __launch_bounds__(kTileThreads)
     }
     // ... and before them: ONE backward walk over the run of item 0 (if it began earlier),
     // compared with every item of that run
-    if (base > 0 && base < M && ((keys[base - 1] ^ kk[0]) & lowm) == 0) {
+    if (base > 0 && base < M && ((before ^ kk[0]) & lowm) == 0) {
         for (uint64_t j = base; j-- > 0;) {
-            const uint64_t pk = keys[j];
+            const uint64_t pk = j + 1 == base ? before : keys[j];
             if (((pk ^ kk[0]) & lowm) != 0) break;
 #pragma unroll
             for (int k = 0; k < kItemsPerThread; k++) dup[k] |= pk == kk[k];
@@ -194,7 +223,7 @@ __global__ void __launch_bounds__(kTileThreads)
         kk[k] = key_dec(kk[k], b, hb);   // (min << b) | max
     }
     uint32_t total;
-    const uint32_t pos = block_exclusive_scan<SumOp>(c, s_scan, &total);
+    const uint32_t pos = block_exclusive_scan<SumOp>(c, s_scan, &total);   // ends with a barrier
     if (threadIdx.x == 0) s_base = atomicAdd((unsigned long long *)m_out, (unsigned long long)total);
     const uint64_t mask = (1ull << b) - 1;
     uint32_t run_a = 0, run_n = 0;
@@ -212,11 +241,23 @@ __global__ void __launch_bounds__(kTileThreads)
             }
         }
     if (run_n) atomicAdd(&deg[run_a], run_n);
+#if TC_UNIQUE_SMEM
+    {   // stage the unique keys (the scan's barrier ordered every read of s_k before this)
+        uint32_t o = pos;
+#pragma unroll
+        for (int k = 0; k < kItemsPerThread; k++)
+            if (f[k]) s_k[o++] = kk[k];
+    }
+    __syncthreads();
+    const uint64_t ob = s_base;
+    for (uint32_t i = threadIdx.x; i < total; i += kTileThreads) out[ob + i] = s_k[i];
+#else
     __syncthreads();
     uint64_t o = s_base + pos;
 #pragma unroll
     for (int k = 0; k < kItemsPerThread; k++)
         if (f[k]) out[o++] = kk[k];
+#endif
 }
 
 // ------------------------------------------------------------------ a3 from pairs
