@@ -158,7 +158,19 @@ typedef struct {
                                    ~60 workspace allocations -- for launch-bound small and
                                    mid-size graphs.  The graph keeps its workspace reserved
                                    between calls.  0 (default) = off                           */
-    uint32_t reserved[6];       /* must be zero                                                 */
+    uint32_t lowdeg_max;        /* tc_count / tc_count_ex (plain or per-vertex counts, AUTO, no
+                                   TC_PRUNE / TC_ID_ORDER / graph_cache, m <= 8n arcs) on graphs
+                                   whose every vertex has at most min(lowdeg_max, 32) arc
+                                   incidences (road networks, meshes: P:700-702's filter-bound
+                                   regime): the bounded-degree path (lowdeg.cu), a thread per
+                                   vertex cleans, orients and intersects its lists in local
+                                   memory -- 5-6 kernels instead of ~40.  Eligibility is tested
+                                   on the device and read back once (one extra synchronisation;
+                                   a graph that fails takes the general pipeline).  Stats then
+                                   carry m_undirected, work_W, work_probe, max_dplus,
+                                   work_stage, skipped_edges, bin_edges[SHORT] (the rest of the
+                                   edges) and times.  Default 32; 0 = off                      */
+    uint32_t reserved[5];       /* must be zero                                                 */
 } tc_options;
 
 typedef struct {

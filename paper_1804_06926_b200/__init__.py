@@ -52,7 +52,7 @@ class Options(ctypes.Structure):
                 ("keep_workspace", ctypes.c_uint32), ("alloc", ALLOC_FN), ("free", FREE_FN),
                 ("alloc_ctx", ctypes.c_void_p), ("tiny_max_n", ctypes.c_uint32),
                 ("clean_method", ctypes.c_uint32), ("graph_cache", ctypes.c_uint32),
-                ("reserved", ctypes.c_uint32 * 6)]
+                ("lowdeg_max", ctypes.c_uint32), ("reserved", ctypes.c_uint32 * 5)]
 
 
 def _torch_raw_alloc(ctx, size, stream):
@@ -217,7 +217,7 @@ def _flags(clean=False, sorted_rows=False, per_vertex=False, validate=False, pru
 
 def _options(stream=None, force_variant=None, short_max=None, skew_ratio=None, hub_min_dplus=None,
              prune_rounds=None, on_device=True, allocator=None, device=None, keep_workspace=None,
-             tiny_max_n=None, clean_method=None, graph_cache=None):
+             tiny_max_n=None, clean_method=None, graph_cache=None, lowdeg_max=None):
     """tc_options for one call.  Device calls default to the current stream of the inputs'
     device and to torch's caching allocator for the workspace."""
     o = Options()
@@ -252,6 +252,8 @@ def _options(stream=None, force_variant=None, short_max=None, skew_ratio=None, h
         o.clean_method = clean_method
     if graph_cache is not None:
         o.graph_cache = int(bool(graph_cache))
+    if lowdeg_max is not None:
+        o.lowdeg_max = lowdeg_max
     return o
 
 

@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libtc_b200.so")
-SOURCES = ["scan.cu", "radix.cu", "orient.cu", "prune.cu", "bin.cu", "intersect.cu", "core.cu", "tiny.cu", "shard.cu",
+SOURCES = ["scan.cu", "radix.cu", "orient.cu", "prune.cu", "bin.cu", "intersect.cu", "core.cu", "tiny.cu", "lowdeg.cu", "shard.cu",
            "validate.cu", "clustering.cu", "tc_api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -1,0 +1,314 @@
+// lowdeg.cu -- the bounded-degree path (round 2): graphs on which every vertex has at most
+// L <= 32 arc incidences (road networks, meshes: BASELINE configs[3]).
+//
+// The paper flags this regime: on road networks the filtering step's "overhead causes a
+// slowdown" because there is little intersection work to amortise it.  The general
+// pipeline spends 3.3 ms on the 14 M-vertex road mesh, 97 % of it in a1-a5 (rank sort, two-key
+// pair sort, in-lists, binning) for 0.09 ms of intersection.  When no vertex has more than L
+// incidences, every list fits in one thread's registers / local memory and none of that
+// machinery is needed -- the method is unchanged, only its data layout is:
+//   a1 clean      (Table 1 caption; DESIGN R1)  each vertex gathers its incidences
+//                 (its out-arcs plus its in-arcs, scattered by one counting pass), drops
+//                 self-loops, sorts and de-duplicates them in a thread: N(v) ascending, d(v);
+//   a2 degree     (R3)  d(v) = |N(v)| after cleaning;
+//   a3 filter     (Alg. 2, R2)  N+(u) = {x in N(u) : (d(u), u) < (d(x), x)} is taken
+//                 on the fly from N(u) and d(.), in the thread that owns u (no relabelling: the
+//                 rank test is a comparison, as in tiny.cu);
+//   a4 sort       rows are ascending by id (the cleaning sorted them), so N+(u) is too;
+//   a6 intersect  (Alg. 2, "TwoSmall" P:533)  for each x in N+(u) a two-pointer merge
+//                 of N+(u) with N(x), counting common w with rank(w) > rank(x), i.e. w in
+//                 N+(x): |N+(u) & N+(x)| exactly as P:315-321 (each triangle once, at its
+//                 lowest-ranked vertex u and middle vertex x);
+//   a7 reduce  per-thread u64 -> warp shuffle -> shared memory -> one atomicAdd.
+// Per-vertex counts credit u, x and w.  Eligibility is decided on the device (a row longer than
+// L, or a vertex with more than L incidences, sets a flag) and read once by the host; a graph
+// that fails takes the general pipeline (tc_api.cu).
+#include "tc_internal.cuh"
+
+namespace tc {
+
+constexpr uint32_t kLdThreads = 256;
+
+__device__ __forceinline__ bool ld_rank_less(uint32_t du, uint32_t u, uint32_t dv, uint32_t v) {
+    return du < dv || (du == dv && u < v);
+}
+
+__device__ __forceinline__ uint64_t ld_block_sum(uint64_t x, uint64_t *s_red) {
+    x = __reduce_add_sync(0xffffffffu, (uint32_t)x) + ((uint64_t)__reduce_add_sync(0xffffffffu, (uint32_t)(x >> 32)) << 32);
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) s_red[warp] = x;
+    __syncthreads();
+    uint64_t s = 0;
+    if (threadIdx.x == 0)
+        for (uint32_t w = 0; w < kLdThreads / 32; w++) s += s_red[w];
+    return s;   // valid in thread 0
+}
+
+#define LD_FOR_VERTICES(v, n)                                                                  \
+    for (uint64_t v = (uint64_t)blockIdx.x * kLdThreads + threadIdx.x; v < (n);               \
+         v += (uint64_t)gridDim.x * kLdThreads)
+
+// Dirty input, pass 1: in-arc counts cin[v]; flag a row longer than L or a count above L.
+__global__ void __launch_bounds__(kLdThreads)
+    k_ld_in(const uint64_t *__restrict__ rowptr, const uint32_t *__restrict__ col, uint64_t n,
+            uint32_t L, uint32_t *__restrict__ cin, uint32_t *__restrict__ flag) {
+    LD_FOR_VERTICES(u, n) {
+        const uint64_t b = rowptr[u], e = rowptr[u + 1];
+        if (e - b > L) {
+            *flag = 1u;
+            continue;
+        }
+        for (uint64_t k = b; k < e; k++) {
+            const uint32_t v = col[k];
+            if (v != (uint32_t)u && atomicAdd(&cin[v], 1u) == L) *flag = 1u;
+        }
+    }
+}
+
+// Pass 2: inc[v] = out-arcs + in-arcs (the slots v's incidences take); flag inc > L.
+__global__ void __launch_bounds__(kLdThreads)
+    k_ld_inc(const uint64_t *__restrict__ rowptr, uint64_t n, uint32_t L, uint32_t *__restrict__ inc,
+             uint32_t *__restrict__ flag) {
+    LD_FOR_VERTICES(v, n) {
+        const uint64_t x = (rowptr[v + 1] - rowptr[v]) + inc[v];
+        if (x > L) *flag = 1u;
+        inc[v] = (uint32_t)min(x, (uint64_t)0xffffffffu);
+    }
+}
+
+// Pass 3: every incidence into its vertex's slots: row u's out-arcs at [aoff[u], aoff[u] + od),
+// the in-arc u of v at aoff[v] + (a slot in [od(v), inc(v)) taken by atomicSub on inc[v]).
+__global__ void __launch_bounds__(kLdThreads)
+    k_ld_scatter(const uint64_t *__restrict__ rowptr, const uint32_t *__restrict__ col, uint64_t n,
+                 const uint64_t *__restrict__ aoff, uint32_t *__restrict__ inc, uint32_t *__restrict__ adj,
+                 const uint32_t *__restrict__ flag) {
+    if (*flag) return;   // not eligible: the call is re-run on the general pipeline
+    LD_FOR_VERTICES(u, n) {
+        const uint64_t b = rowptr[u], e = rowptr[u + 1], s = aoff[u];
+        for (uint64_t k = b; k < e; k++) {
+            const uint32_t v = col[k];
+            adj[s + (k - b)] = v;
+            if (v != (uint32_t)u) {
+                const uint32_t slot = atomicSub(&inc[v], 1u) - 1u;
+                adj[aoff[v] + slot] = (uint32_t)u;
+            }
+        }
+    }
+}
+
+// Pass 4 (a1 + a2): each vertex sorts its incidences, drops self-loops and duplicates, and
+// writes N(v) ascending back to the front of its slots; d(v); Sum d(v) = 2m into *m2.
+__global__ void __launch_bounds__(kLdThreads)
+    k_ld_clean(const uint64_t *__restrict__ aoff, uint64_t n, uint32_t *__restrict__ adj,
+               uint32_t *__restrict__ deg, unsigned long long *__restrict__ m2,
+               const uint32_t *__restrict__ flag) {
+    __shared__ uint64_t s_red[kLdThreads / 32];
+    if (*flag) return;   // (uniform: the flag is final before this kernel starts)
+    uint64_t sum = 0;
+    LD_FOR_VERTICES(v, n) {
+        const uint64_t s = aoff[v];
+        const uint32_t c = (uint32_t)(aoff[v + 1] - s);
+        uint32_t a[32];
+        uint32_t k = 0;
+        for (uint32_t i = 0; i < c && i < 32; i++) {   // insertion sort, self-loops dropped
+            const uint32_t x = adj[s + i];
+            if (x == (uint32_t)v) continue;
+            uint32_t j = k++;
+            while (j > 0 && a[j - 1] > x) {
+                a[j] = a[j - 1];
+                j--;
+            }
+            a[j] = x;
+        }
+        uint32_t d = 0;
+        for (uint32_t i = 0; i < k; i++)
+            if (i == 0 || a[i] != a[i - 1]) adj[s + d++] = a[i];
+        deg[v] = d;
+        sum += d;
+    }
+    sum = ld_block_sum(sum, s_red);
+    if (threadIdx.x == 0 && sum) atomicAdd(m2, (unsigned long long)sum);
+}
+
+// Clean input (TC_CLEAN): d(v) = row length; flag a row longer than L; rows not promised
+// sorted are sorted into adj (same offsets).
+__global__ void __launch_bounds__(kLdThreads)
+    k_ld_clean_rows(const uint64_t *__restrict__ rowptr, const uint32_t *__restrict__ col, uint64_t n,
+                    uint32_t L, bool sort, uint32_t *__restrict__ adj, uint32_t *__restrict__ deg,
+                    uint32_t *__restrict__ flag) {
+    LD_FOR_VERTICES(v, n) {
+        const uint64_t b = rowptr[v], c = rowptr[v + 1] - b;
+        if (c > L) {
+            *flag = 1u;
+            deg[v] = 0;
+            continue;
+        }
+        deg[v] = (uint32_t)c;
+        if (!sort) continue;
+        uint32_t a[32];
+        for (uint32_t i = 0; i < (uint32_t)c; i++) {
+            const uint32_t x = col[b + i];
+            uint32_t j = i;
+            while (j > 0 && a[j - 1] > x) {
+                a[j] = a[j - 1];
+                j--;
+            }
+            a[j] = x;
+        }
+        for (uint32_t i = 0; i < (uint32_t)c; i++) adj[b + i] = a[i];
+    }
+}
+
+// a3 + a6 + a7: one thread per vertex u.  out[]: 0 = W, 1 = probe work, 2 = max d+,
+// 3 = Sum d-(v) d+(v), 4 = skipped edges, 5 = Sum d+ (arcs passing the rank filter).
+template <bool STATS>
+__global__ void __launch_bounds__(kLdThreads)
+    k_ld_count(const uint64_t *__restrict__ aoff, const uint32_t *__restrict__ adj,
+               const uint32_t *__restrict__ deg, uint64_t n, unsigned long long *__restrict__ total,
+               unsigned long long *__restrict__ pv, unsigned long long *__restrict__ out,
+               const uint32_t *__restrict__ flag) {
+    __shared__ uint64_t s_red[kLdThreads / 32];
+    if (*flag) return;   // not eligible: nothing is counted, the call is re-run
+    uint64_t tri = 0, npsum = 0, W = 0, probe = 0, stage = 0, skipped = 0, maxdp = 0;
+    LD_FOR_VERTICES(u, n) {
+        const uint32_t du = deg[u];
+        const uint64_t s = aoff[u];
+        uint32_t pid[32], pdeg[32];
+        uint32_t np = 0;
+        for (uint32_t i = 0; i < du; i++) {   // N+(u), ascending by id
+            const uint32_t x = adj[s + i];
+            const uint32_t dx = deg[x];
+            if (ld_rank_less(du, (uint32_t)u, dx, x)) {
+                pid[np] = x;
+                pdeg[np] = dx;
+                np++;
+            }
+        }
+        npsum += np;
+        uint64_t tu = 0;
+        for (uint32_t j = 0; j < np; j++) {
+            const uint32_t x = pid[j], dx = pdeg[j];
+            const uint64_t sx = aoff[x];
+            uint32_t i = 0, k = 0;
+            while (i < dx && k < np) {   // N(x) merged with N+(u): common w with rank(w) > rank(x)
+                const uint32_t w = adj[sx + i], y = pid[k];
+                if (w < y) i++;
+                else if (y < w) k++;
+                else {
+                    if (ld_rank_less(dx, x, pdeg[k], w)) {
+                        tu++;
+                        if (pv) {
+                            atomicAdd(&pv[x], 1ull);
+                            atomicAdd(&pv[w], 1ull);
+                        }
+                    }
+                    i++;
+                    k++;
+                }
+            }
+            if (STATS) {   // d+(x), |N+(u) after x| (rank order): W, probe work, skipped edges
+                uint32_t dpx = 0;
+                for (uint32_t t = 0; t < dx; t++) {
+                    const uint32_t w = adj[sx + t];
+                    dpx += ld_rank_less(dx, x, deg[w], w);
+                }
+                uint32_t after = 0;
+                for (uint32_t t = 0; t < np; t++) after += ld_rank_less(dx, x, pdeg[t], pid[t]);
+                W += np + dpx;
+                probe += min(after, dpx);
+                skipped += (after == 0 || dpx == 0);
+            }
+        }
+        if (pv && tu) atomicAdd(&pv[u], (unsigned long long)tu);
+        tri += tu;
+        if (STATS) {
+            stage += (uint64_t)(du - np) * np;
+            maxdp = max(maxdp, (uint64_t)np);
+        }
+    }
+    tri = ld_block_sum(tri, s_red);
+    if (threadIdx.x == 0 && tri) atomicAdd(total, (unsigned long long)tri);
+    npsum = ld_block_sum(npsum, s_red);
+    if (threadIdx.x == 0 && npsum) atomicAdd(&out[5], (unsigned long long)npsum);
+    if (STATS) {
+        W = ld_block_sum(W, s_red);
+        probe = ld_block_sum(probe, s_red);
+        stage = ld_block_sum(stage, s_red);
+        skipped = ld_block_sum(skipped, s_red);
+        if (threadIdx.x == 0) {
+            atomicAdd(&out[0], (unsigned long long)W);
+            atomicAdd(&out[1], (unsigned long long)probe);
+            atomicAdd(&out[3], (unsigned long long)stage);
+            atomicAdd(&out[4], (unsigned long long)skipped);
+        }
+        if (maxdp) atomicMax(&out[2], (unsigned long long)maxdp);
+    }
+}
+
+static uint32_t ld_grid(const Ctx &ctx, uint64_t n) {
+    return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((n + kLdThreads - 1) / kLdThreads,
+                                                              (uint64_t)ctx.persistent_grid(8)));
+}
+
+void lowdeg_prepare(Ctx &ctx, LowDeg &ld, uint64_t n, uint64_t M, const uint64_t *rowptr,
+                    const uint32_t *col, bool clean, bool sorted, uint32_t L, uint32_t *flag_dev) {
+    L = std::min<uint32_t>(L, kLowDegMax);
+    const uint32_t grid = ld_grid(ctx, n);
+    ld.n = n;
+    ld.flag = flag_dev;
+    ld.deg = ctx.alloc<uint32_t>(n);
+    if (clean) {
+        ld.aoff = rowptr;
+        ld.adj = sorted ? col : ctx.alloc<uint32_t>(M);
+        k_ld_clean_rows<<<grid, kLdThreads, 0, ctx.stream>>>(rowptr, col, n, L, !sorted,
+                                                            const_cast<uint32_t *>(ld.adj), ld.deg, flag_dev);
+        TC_LAUNCHED(ctx);
+        ld.m2_host = M;
+        return;
+    }
+    // dirty: in-counts, slot counts, offsets, scatter (k_ld_clean runs after the host's check)
+    ld.m2 = ctx.alloc<uint64_t>(1);
+    TC_CUDA(cudaMemsetAsync(ld.m2, 0, sizeof(uint64_t), ctx.stream));
+    uint32_t *inc = ctx.alloc<uint32_t>(n);
+    TC_CUDA(cudaMemsetAsync(inc, 0, n * sizeof(uint32_t), ctx.stream));
+    k_ld_in<<<grid, kLdThreads, 0, ctx.stream>>>(rowptr, col, n, L, inc, flag_dev);
+    TC_LAUNCHED(ctx);
+    k_ld_inc<<<grid, kLdThreads, 0, ctx.stream>>>(rowptr, n, L, inc, flag_dev);
+    TC_LAUNCHED(ctx);
+    ld.inc = inc;
+    ld.rowptr = rowptr;
+    ld.col = col;
+}
+
+void lowdeg_count(Ctx &ctx, LowDeg &ld, uint64_t M, Timer *tm, uint64_t *total_dev, uint64_t *pv_dev,
+                  uint64_t *out_dev, bool stats) {
+    const uint64_t n = ld.n;
+    const uint32_t grid = ld_grid(ctx, n);
+    if (ld.inc) {   // dirty input: finish a1 + a2
+        uint64_t *aoff = ctx.alloc<uint64_t>(n + 1);
+        scan_exclusive(ctx, ld.inc, aoff, n);
+        uint32_t *adj = ctx.alloc<uint32_t>(2 * M);
+        k_ld_scatter<<<grid, kLdThreads, 0, ctx.stream>>>(ld.rowptr, ld.col, n, aoff, ld.inc, adj, ld.flag);
+        TC_LAUNCHED(ctx);
+        k_ld_clean<<<grid, kLdThreads, 0, ctx.stream>>>(aoff, n, adj, ld.deg,
+                                                       (unsigned long long *)ld.m2, ld.flag);
+        TC_LAUNCHED(ctx);
+        ld.aoff = aoff;
+        ld.adj = adj;
+    }
+    phase_end(tm, kClean);
+    phase_begin(tm, kIntersect);
+    if (stats)
+        k_ld_count<true><<<grid, kLdThreads, 0, ctx.stream>>>(
+            ld.aoff, ld.adj, ld.deg, n, (unsigned long long *)total_dev, (unsigned long long *)pv_dev,
+            (unsigned long long *)out_dev, ld.flag);
+    else
+        k_ld_count<false><<<grid, kLdThreads, 0, ctx.stream>>>(
+            ld.aoff, ld.adj, ld.deg, n, (unsigned long long *)total_dev, (unsigned long long *)pv_dev,
+            (unsigned long long *)out_dev, ld.flag);
+    TC_LAUNCHED(ctx);
+    phase_end(tm, kIntersect);
+}
+
+}  // namespace tc

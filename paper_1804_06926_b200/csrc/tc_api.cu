@@ -59,7 +59,7 @@ static void set_pool_keep(cudaMemPool_t pool, bool keep) {
 // 32 uint64 of pinned host memory per thread for asynchronous stat read-back.
 static uint64_t *pinned_scratch() {
     static thread_local uint64_t *p = nullptr;
-    if (!p) TC_CUDA(cudaMallocHost((void **)&p, 32 * sizeof(uint64_t)));
+    if (!p) TC_CUDA(cudaMallocHost((void **)&p, 64 * sizeof(uint64_t)));   // [32, 40): lowdeg
     return p;
 }
 
@@ -235,9 +235,18 @@ static GraphKey graph_key(const Call &c, int dev) {
 }
 
 static void run_impl(Call &c, bool capture);
+struct LowDegRetry {};   // thrown by run_impl when the bounded-degree path was not eligible
 
 static void run(Call &c) {
-    if (!graph_eligible(c)) return run_impl(c, false);
+    if (!graph_eligible(c)) {
+        try {
+            return run_impl(c, false);
+        } catch (const LowDegRetry &) {   // more than lowdeg_max incidences somewhere
+            Call c2 = c;
+            c2.opt.lowdeg_max = 0;
+            return run_impl(c2, false);
+        }
+    }
     int dev = 0;
     TC_CUDA(cudaGetDevice(&dev));
     const GraphKey key = graph_key(c, dev);
@@ -268,6 +277,44 @@ static void run(Call &c) {
         Call plain = c;
         plain.opt.graph_cache = 0;
         run_impl(plain, false);
+    }
+}
+
+// The bounded-degree path (lowdeg.cu): the eligibility passes and the count, enqueued without
+// a synchronisation; their flag (some vertex has more than lowdeg_max incidences: nothing was
+// counted) is read with the count, and run() then re-runs the call on the general pipeline
+// (LowDegRetry).  Fills pin[] as the general path does for the stats it has.
+static bool run_lowdeg(Ctx &ctx, const Call &c, const uint64_t *rowptr, const uint32_t *col, Timer *tm,
+                       uint64_t *total_dev, uint64_t *pv_dev, uint64_t *pin) {
+    const bool clean = c.flags & TC_CLEAN;
+    uint64_t *out = ctx.alloc<uint64_t>(8);     // [0..5] lowdeg_count's sums, [6] the flag
+    TC_CUDA(cudaMemsetAsync(out, 0, 8 * sizeof(uint64_t), ctx.stream));
+    uint32_t *flag = (uint32_t *)(out + 6);
+    LowDeg ld;
+    phase_begin(tm, kClean);
+    lowdeg_prepare(ctx, ld, c.n, c.M, rowptr, col, clean, c.flags & TC_SORTED, c.opt.lowdeg_max, flag);
+    lowdeg_count(ctx, ld, c.M, tm, total_dev, pv_dev, out, c.stats != nullptr);
+    // pin[32 + i] = out[i] (one copy): the flag, Sum d+ (a false TC_CLEAN claim has more than
+    // m/2 arcs passing the rank filter) and the stats sums; pin[39] = Sum d(v) = 2m
+    TC_CUDA(cudaMemcpyAsync(pin + 32, out, 7 * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx.stream));
+    if (c.stats) {
+        if (ld.m2) TC_CUDA(cudaMemcpyAsync(pin + 39, ld.m2, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx.stream));
+        else pin[39] = ld.m2_host;
+    }
+    return true;
+}
+// After the final synchronisation: the claim flag and the stats slots of the general path.
+static void finish_lowdeg(const Call &c, uint64_t *pin) {
+    const uint64_t *o = pin + 32;
+    if ((c.flags & TC_CLEAN) && o[5] > c.M / 2) pin[26] = 1;
+    if (c.stats) {
+        pin[4] = o[0];                    // W
+        pin[5] = o[1];                    // probe work
+        pin[7] = o[2];                    // max d+
+        pin[12] = o[3];                   // Sum d- d+
+        pin[6] = o[4];                    // skipped edges
+        pin[16] = pin[39] / 2;            // m
+        pin[0] = pin[16] - pin[6];        // SHORT-like: every edge that can close a triangle
     }
 }
 
@@ -426,6 +473,12 @@ static void run_impl(Call &c, bool capture) {
     const bool tiny = (c.mode == kCount || c.mode == kShard) && !c.edges_in && c.n > 0 && c.M > 0 &&
                       c.n <= c.opt.tiny_max_n && c.n <= kTinyMaxN && c.opt.force_variant < 0 &&
                       !(c.flags & (TC_PRUNE | TC_ID_ORDER));
+    // the bounded-degree path: few incidences per vertex (m <= 8n arcs as a host-side gate,
+    // then a device test); never under capture (its decision is a host read of the data)
+    const bool lowdeg = c.mode == kCount && !tiny && !capture && !c.edges_in && c.n > 0 && c.M > 0 &&
+                        c.opt.lowdeg_max > 0 && c.M <= 8 * c.n && c.opt.force_variant < 0 &&
+                        !(c.flags & (TC_PRUNE | TC_ID_ORDER));
+    bool ld_ran = false;
     if (tiny) {   // one kernel (tiny.cu); a shard other than rank 0 contributes nothing
         pin[16] = 0;
         uint64_t *m_dev = ctx.alloc<uint64_t>(1);
@@ -437,6 +490,9 @@ static void run_impl(Call &c, bool capture) {
         if (c.stats)
             TC_CUDA(cudaMemcpyAsync(pin + 16, m_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost,
                                     ctx.stream));
+    } else if (lowdeg && (ld_ran = run_lowdeg(ctx, c, rowptr, col, tm, total_dev, pv_out ? pv_dev : nullptr,
+                                              pin))) {
+        // counted by the bounded-degree path (lowdeg.cu); stats are in pin[]
     } else if (c.n > 0 && c.M > 0) {
         Oriented g;
         if (c.edges_in) {   // after a sharded a1: the unique edges of every rank, all degrees
@@ -600,6 +656,8 @@ static void run_impl(Call &c, bool capture) {
     const bool synced = c.mode != kShard || c.stats;
     if (synced) TC_CUDA(cudaStreamSynchronize(ctx.stream));
     TC_CUDA(cudaGetLastError());
+    if (ld_ran && pin[38]) throw LowDegRetry{};   // not eligible: run() re-runs on the pipeline
+    if (ld_ran) finish_lowdeg(c, pin);
     if (synced && c.n > 0 && c.M > 0) check_claim(pin);
     if (c.mode == kCount || c.mode == kEnumerate || c.mode == kMasked) *c.total_host = pin[20];
     if (c.mode == kClustering && c.csum) {
@@ -734,6 +792,7 @@ void tc_default_options(tc_options *opt) {
     opt->stream = nullptr;
     opt->keep_workspace = 1;
     opt->tiny_max_n = (uint32_t)kTinyMaxN;
+    opt->lowdeg_max = kLowDegMax;
 }
 
 tc_status tc_trim_workspace(int device) {

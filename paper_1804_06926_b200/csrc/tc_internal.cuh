@@ -598,6 +598,27 @@ constexpr uint64_t kTinyMaxN = 1024;
 void tiny_count(Ctx &ctx, uint64_t n, const uint64_t *rowptr, const uint32_t *col,
                 uint64_t *total_dev, uint64_t *pv_dev, uint64_t *m_dev);
 
+// lowdeg.cu: the bounded-degree path (every vertex has <= L <= kLowDegMax incidences).
+// lowdeg_prepare enqueues the eligibility passes (they set *flag_dev when some vertex has
+// more); lowdeg_count finishes a1-a2 and counts -- its kernels do nothing when the flag is
+// set, and the host, reading the flag with the count, re-runs the call on the pipeline --
+// (total, per-vertex t(v) in input ids, and into out_dev[6]: W, probe work, max d+,
+// Sum d- d+, skipped edges (these with stats), Sum d+).
+constexpr uint32_t kLowDegMax = 32;
+struct LowDeg {
+    uint64_t n = 0;
+    const uint64_t *rowptr = nullptr, *aoff = nullptr;
+    const uint32_t *col = nullptr, *adj = nullptr;
+    uint32_t *inc = nullptr, *deg = nullptr;
+    const uint32_t *flag = nullptr;   // device: set when some vertex has more than L incidences
+    uint64_t *m2 = nullptr;     // device: Sum d(v) (dirty input)
+    uint64_t m2_host = 0;       // clean input: M
+};
+void lowdeg_prepare(Ctx &ctx, LowDeg &ld, uint64_t n, uint64_t M, const uint64_t *rowptr,
+                    const uint32_t *col, bool clean, bool sorted, uint32_t L, uint32_t *flag_dev);
+void lowdeg_count(Ctx &ctx, LowDeg &ld, uint64_t M, Timer *tm, uint64_t *total_dev, uint64_t *pv_dev,
+                  uint64_t *out_dev, bool stats);
+
 // Multi-GPU phases (shard.cu): tc_api.cu's option / workspace / error wrapper.
 tc_status run_phase(const tc_options *opt, const std::function<void(Ctx &, const tc_options &)> &fn);
 void check_device(const void *p, int dev, const char *what);   // TC_EINVAL unless on `dev`

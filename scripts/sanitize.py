@@ -21,7 +21,7 @@ for g in graphs:
         got, pv = tc.count_ex(rp, cl, per_vertex=True, force_variant=v)
         assert got == T and (pv.cpu().numpy().view(np.uint64) == t).all(), (g.name, v)
     # the plain count through the pipeline (dense core) and through the one-kernel path
-    assert tc.count_ex(rp, cl, tiny_max_n=0) == T and tc.count_ex(rp, cl) == T
+    assert tc.count_ex(rp, cl, tiny_max_n=0, lowdeg_max=0) == T and tc.count_ex(rp, cl) == T
     assert tc.count_ex(rp, cl, allocator="library") == T
     assert tc.count_ex(rp, cl, prune=True, hub_min_dplus=2) == T
     assert tc.count_ex(rp, cl, id_order=True) == T

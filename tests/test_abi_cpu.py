@@ -45,9 +45,10 @@ def test_struct_layout(lib):
     lib.tc_default_options(ctypes.byref(o))
     assert ctypes.sizeof(tc.Options) == 96
     assert tc.Options.alloc.offset == 32 and tc.Options.clean_method.offset == 60
-    assert tc.Options.graph_cache.offset == 64 and tc.Options.reserved.offset == 68
+    assert tc.Options.graph_cache.offset == 64 and tc.Options.lowdeg_max.offset == 68
+    assert tc.Options.reserved.offset == 72
     assert o.graph_cache == 0
-    assert o.tiny_max_n == 1024 and o.clean_method == 0
+    assert o.tiny_max_n == 1024 and o.clean_method == 0 and o.lowdeg_max == 32
     assert o.short_max == 20 and o.skew_ratio == 0 and o.hub_min_dplus == 80
     assert o.force_variant == -1 and o.keep_workspace == 1
     assert not o.alloc and not o.free and not o.alloc_ctx

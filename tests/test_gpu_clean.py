@@ -91,13 +91,13 @@ def test_clean_vs_oracle(name, method):
     g = CASES[name]()
     T, t = O.count(g.n, g.rowptr, g.col, per_vertex=True)
     rp, cl = on_dev(g.rowptr, g.col)
-    got, pv = tc.count_ex(rp, cl, per_vertex=True, tiny_max_n=0, clean_method=method)
+    got, pv = tc.count_ex(rp, cl, per_vertex=True, tiny_max_n=0, lowdeg_max=0, clean_method=method)
     torch.cuda.synchronize()
     assert got == T, (name, method, got, T)
     assert (pv.cpu().numpy().view(np.uint64) == t).all(), (name, method)
     row, col = O.clean(g.n, g.rowptr, g.col)
     want_off, want_col = O.orient(g.n, row, col)
-    off, colp = tc.orient(rp, cl, tiny_max_n=0, clean_method=method)
+    off, colp = tc.orient(rp, cl, tiny_max_n=0, lowdeg_max=0, clean_method=method)
     torch.cuda.synchronize()
     assert (off.cpu().numpy().view(np.uint64) == want_off).all(), (name, method)
     assert (colp.cpu().numpy().view(np.uint32) == want_col).all(), (name, method)

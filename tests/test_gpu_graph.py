@@ -35,19 +35,19 @@ def test_graph_replay_matches_oracle(scale):
     rp, cl = on_dev(g1.rowptr, g1.col)
     pv = torch.zeros(g1.n, dtype=torch.int64, device=DEV)
     for _ in range(3):   # capture, then replays
-        assert tc.count_ex(rp, cl, graph_cache=1, tiny_max_n=0) == T1
+        assert tc.count_ex(rp, cl, graph_cache=1, tiny_max_n=0, lowdeg_max=0) == T1
     l0 = tc.launches_issued()
-    assert tc.count_ex(rp, cl, graph_cache=1, tiny_max_n=0) == T1
+    assert tc.count_ex(rp, cl, graph_cache=1, tiny_max_n=0, lowdeg_max=0) == T1
     assert tc.launches_issued() - l0 > 10          # the replayed graph's kernels are counted
     # same buffers, new content: the replay recomputes everything
     r2, c2 = on_dev(g2.rowptr, g2.col)
     rp.copy_(r2)
     cl.copy_(c2)
     torch.cuda.synchronize()
-    assert tc.count_ex(rp, cl, graph_cache=1, tiny_max_n=0) == T2
-    assert tc.count_ex(rp, cl, tiny_max_n=0) == T2                 # and without the graph
-    got, pvo = tc.count_ex(rp, cl, per_vertex=True, graph_cache=1, tiny_max_n=0)
-    got, pvo = tc.count_ex(rp, cl, per_vertex=True, graph_cache=1, tiny_max_n=0)
+    assert tc.count_ex(rp, cl, graph_cache=1, tiny_max_n=0, lowdeg_max=0) == T2
+    assert tc.count_ex(rp, cl, tiny_max_n=0, lowdeg_max=0) == T2                 # and without the graph
+    got, pvo = tc.count_ex(rp, cl, per_vertex=True, graph_cache=1, tiny_max_n=0, lowdeg_max=0)
+    got, pvo = tc.count_ex(rp, cl, per_vertex=True, graph_cache=1, tiny_max_n=0, lowdeg_max=0)
     torch.cuda.synchronize()
     assert got == T2 and (pvo.cpu().numpy().view(np.uint64) == t2).all()
 
@@ -70,7 +70,7 @@ def test_trim_drops_replay_graphs():
     T = O.count(g.n, g.rowptr, g.col)
     rp, cl = on_dev(g.rowptr, g.col)
     for _ in range(2):
-        assert tc.count_ex(rp, cl, graph_cache=1, tiny_max_n=0) == T
+        assert tc.count_ex(rp, cl, graph_cache=1, tiny_max_n=0, lowdeg_max=0) == T
     tc.trim_workspace()
     for _ in range(2):   # captured again after the trim
-        assert tc.count_ex(rp, cl, graph_cache=1, tiny_max_n=0) == T
+        assert tc.count_ex(rp, cl, graph_cache=1, tiny_max_n=0, lowdeg_max=0) == T

@@ -264,7 +264,7 @@ def test_false_clean_claim_is_caught(n):
     filter, the buffers hold n/2 + 1) must not write out of bounds: TC_EGRAPH."""
     rp, cl = _one_way_cycle(n)
     with pytest.raises(tc.TCError) as e:
-        gpu_count(rp, cl, clean=True, tiny_max_n=0)   # (the one-kernel path symmetrises anyway)
+        gpu_count(rp, cl, clean=True, tiny_max_n=0, lowdeg_max=0)   # (the one-kernel path symmetrises anyway)
     assert e.value.status == 2
     assert gpu_count(*clean_csr(G.karate()), clean=True) == 45   # the device is still sane
 
@@ -514,12 +514,12 @@ def test_core_path_counts(name):
     total must equal the oracle, and the core path must have run where the graph has a core."""
     g = CORE_GRAPHS[name]()
     T = O.count(g.n, g.rowptr, g.col)
-    got, st = gpu_count(g.rowptr, g.col, with_stats=True, tiny_max_n=0)
+    got, st = gpu_count(g.rowptr, g.col, with_stats=True, tiny_max_n=0, lowdeg_max=0)
     assert got == T
     if name != "karate":
         assert st["core_edges"] > 0 and st["core_words"] > 0, st
     # the per-vertex call does not use the core path: same total, zero core edges
-    got2, _, st2 = gpu_count(g.rowptr, g.col, per_vertex=True, with_stats=True, tiny_max_n=0)
+    got2, _, st2 = gpu_count(g.rowptr, g.col, per_vertex=True, with_stats=True, tiny_max_n=0, lowdeg_max=0)
     assert got2 == T and st2["core_edges"] == 0
     # a forced variant disables it too
     got3, st3 = gpu_count(g.rowptr, g.col, force_variant=tc.VARIANT_HASH, with_stats=True)
@@ -557,7 +557,7 @@ def test_tiny_path(name):
     assert st["kernel_launches"] == 1
     assert st["m_undirected"] == O.count(g.n, g.rowptr, g.col, with_stats=True)[1]["m"]
     assert gpu_count(g.rowptr, g.col) == T
-    got2, pv2 = gpu_count(g.rowptr, g.col, per_vertex=True, tiny_max_n=0)
+    got2, pv2 = gpu_count(g.rowptr, g.col, per_vertex=True, tiny_max_n=0, lowdeg_max=0)
     assert got2 == T and (pv_np(pv2) == t).all()
     rp, cl = on_dev(g.rowptr, g.col)
     tot = 0
