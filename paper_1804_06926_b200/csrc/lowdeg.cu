@@ -24,6 +24,7 @@
 // L, or a vertex with more than L incidences, sets a flag) and read once by the host; a graph
 // that fails takes the general pipeline (tc_api.cu).
 #include "tc_internal.cuh"
+#include "block_scan.cuh"
 
 namespace tc {
 
@@ -49,10 +50,33 @@ __device__ __forceinline__ uint64_t ld_block_sum(uint64_t x, uint64_t *s_red) {
     for (uint64_t v = (uint64_t)blockIdx.x * kLdThreads + threadIdx.x; v < (n);               \
          v += (uint64_t)gridDim.x * kLdThreads)
 
-// Dirty input, pass 1: in-arc counts cin[v]; flag a row longer than L or a count above L.
+// Rows of at most kLdReg entries (all of them on road meshes) are held in registers: static
+// indices only (a sorting network, membership masks); longer rows use local-memory arrays.
+constexpr uint32_t kLdReg = 8;
+constexpr uint32_t kLdNone = 0xffffffffu;   // padding: above every vertex id
+// pk[v] = d(v) << 40 | offset of v's row in adj (offsets < 2^33: 2M < 2^33 arcs): the count
+// kernel's gather of a neighbour x yields its degree AND its row in one 8-byte load.
+__device__ __forceinline__ uint64_t ld_pack(uint32_t d, uint64_t off) { return ((uint64_t)d << 40) | off; }
+__device__ __forceinline__ uint32_t ld_pk_deg(uint64_t p) { return (uint32_t)(p >> 40); }
+__device__ __forceinline__ uint64_t ld_pk_off(uint64_t p) { return p & ((1ull << 40) - 1); }
+__device__ __forceinline__ void ld_cswap(uint32_t &a, uint32_t &b) {
+    const uint32_t lo = min(a, b), hi = max(a, b);
+    a = lo;
+    b = hi;
+}
+__device__ __forceinline__ void ld_sort8(uint32_t (&a)[8]) {   // Batcher's 19-comparator network
+    ld_cswap(a[0], a[1]); ld_cswap(a[2], a[3]); ld_cswap(a[4], a[5]); ld_cswap(a[6], a[7]);
+    ld_cswap(a[0], a[2]); ld_cswap(a[1], a[3]); ld_cswap(a[4], a[6]); ld_cswap(a[5], a[7]);
+    ld_cswap(a[1], a[2]); ld_cswap(a[5], a[6]); ld_cswap(a[0], a[4]); ld_cswap(a[3], a[7]);
+    ld_cswap(a[1], a[5]); ld_cswap(a[2], a[6]); ld_cswap(a[1], a[4]); ld_cswap(a[3], a[6]);
+    ld_cswap(a[2], a[4]); ld_cswap(a[3], a[5]); ld_cswap(a[3], a[4]);
+}
+
+// Dirty input, pass 1: in-arc counts cin[v]; each arc keeps the slot its atomic returned
+// (slot8[k], one byte: slots < L <= 32); flag a row longer than L or a count above L.
 __global__ void __launch_bounds__(kLdThreads)
     k_ld_in(const uint64_t *__restrict__ rowptr, const uint32_t *__restrict__ col, uint64_t n,
-            uint32_t L, uint32_t *__restrict__ cin, uint32_t *__restrict__ flag) {
+            uint32_t L, uint32_t *__restrict__ cin, uint8_t *__restrict__ slot8, uint32_t *__restrict__ flag) {
     LD_FOR_VERTICES(u, n) {
         const uint64_t b = rowptr[u], e = rowptr[u + 1];
         if (e - b > L) {
@@ -61,70 +85,100 @@ __global__ void __launch_bounds__(kLdThreads)
         }
         for (uint64_t k = b; k < e; k++) {
             const uint32_t v = col[k];
-            if (v != (uint32_t)u && atomicAdd(&cin[v], 1u) == L) *flag = 1u;
+            if (v == (uint32_t)u) continue;
+            const uint32_t old = atomicAdd(&cin[v], 1u);
+            slot8[k] = (uint8_t)min(old, 255u);
+            if (old == L) *flag = 1u;
         }
     }
 }
 
-// Pass 2: inc[v] = out-arcs + in-arcs (the slots v's incidences take); flag inc > L.
+// Pass 2: inc[v] = in-arcs + out-arcs (flag inc > L) and the row offsets aoff[v]: a block scan
+// of inc plus ONE atomic per block on *next (rows are contiguous per block of vertices, blocks
+// in any order: no device-wide scan).  inc overwrites cin.
 __global__ void __launch_bounds__(kLdThreads)
-    k_ld_inc(const uint64_t *__restrict__ rowptr, uint64_t n, uint32_t L, uint32_t *__restrict__ inc,
-             uint32_t *__restrict__ flag) {
-    LD_FOR_VERTICES(v, n) {
-        const uint64_t x = (rowptr[v + 1] - rowptr[v]) + inc[v];
-        if (x > L) *flag = 1u;
-        inc[v] = (uint32_t)min(x, (uint64_t)0xffffffffu);
+    k_ld_offsets(const uint64_t *__restrict__ rowptr, uint64_t n, uint32_t L, uint32_t *__restrict__ inc,
+                 uint64_t *__restrict__ aoff, unsigned long long *__restrict__ next, uint32_t *__restrict__ flag) {
+    __shared__ uint32_t s_scan[kLdThreads / 32];
+    __shared__ uint64_t s_base;
+    for (uint64_t v0 = (uint64_t)blockIdx.x * kLdThreads; v0 < n; v0 += (uint64_t)gridDim.x * kLdThreads) {
+        const uint64_t v = v0 + threadIdx.x;
+        uint32_t x = 0;
+        if (v < n) {
+            const uint64_t c = (rowptr[v + 1] - rowptr[v]) + inc[v];
+            if (c > L) *flag = 1u;
+            x = (uint32_t)min(c, (uint64_t)kLowDegMax + 1);   // (rows of a flagged graph are never read)
+            inc[v] = x;
+        }
+        uint32_t total;
+        const uint32_t pre = block_exclusive_scan<SumOp>(x, s_scan, &total);
+        if (threadIdx.x == 0) s_base = atomicAdd(next, (unsigned long long)total);
+        __syncthreads();
+        if (v < n) aoff[v] = s_base + pre;
+        __syncthreads();
     }
 }
 
-// Pass 3: every incidence into its vertex's slots: row u's out-arcs at [aoff[u], aoff[u] + od),
-// the in-arc u of v at aoff[v] + (a slot in [od(v), inc(v)) taken by atomicSub on inc[v]).
+// Pass 3: every incidence into its vertex's row: the in-arc u of v at aoff[v] + slot8, row u's
+// out-arcs after its in-arcs at aoff[u] + cin(u).
 __global__ void __launch_bounds__(kLdThreads)
     k_ld_scatter(const uint64_t *__restrict__ rowptr, const uint32_t *__restrict__ col, uint64_t n,
-                 const uint64_t *__restrict__ aoff, uint32_t *__restrict__ inc, uint32_t *__restrict__ adj,
-                 const uint32_t *__restrict__ flag) {
+                 const uint64_t *__restrict__ aoff, const uint32_t *__restrict__ inc,
+                 const uint8_t *__restrict__ slot8, uint32_t *__restrict__ adj, const uint32_t *__restrict__ flag) {
     if (*flag) return;   // not eligible: the call is re-run on the general pipeline
     LD_FOR_VERTICES(u, n) {
-        const uint64_t b = rowptr[u], e = rowptr[u + 1], s = aoff[u];
+        const uint64_t b = rowptr[u], e = rowptr[u + 1];
+        if (b == e) continue;
+        const uint64_t s = aoff[u] + (inc[u] - (uint32_t)(e - b));
         for (uint64_t k = b; k < e; k++) {
             const uint32_t v = col[k];
             adj[s + (k - b)] = v;
-            if (v != (uint32_t)u) {
-                const uint32_t slot = atomicSub(&inc[v], 1u) - 1u;
-                adj[aoff[v] + slot] = (uint32_t)u;
-            }
+            if (v != (uint32_t)u) adj[aoff[v] + slot8[k]] = (uint32_t)u;
         }
     }
 }
 
 // Pass 4 (a1 + a2): each vertex sorts its incidences, drops self-loops and duplicates, and
-// writes N(v) ascending back to the front of its slots; d(v); Sum d(v) = 2m into *m2.
+// writes N(v) ascending back to the front of its row; d(v); Sum d(v) = 2m into *m2.
 __global__ void __launch_bounds__(kLdThreads)
-    k_ld_clean(const uint64_t *__restrict__ aoff, uint64_t n, uint32_t *__restrict__ adj,
-               uint32_t *__restrict__ deg, unsigned long long *__restrict__ m2,
+    k_ld_clean(const uint64_t *__restrict__ aoff, const uint32_t *__restrict__ inc, uint64_t n,
+               uint32_t *__restrict__ adj, uint64_t *__restrict__ pk, unsigned long long *__restrict__ m2,
                const uint32_t *__restrict__ flag) {
     __shared__ uint64_t s_red[kLdThreads / 32];
     if (*flag) return;   // (uniform: the flag is final before this kernel starts)
     uint64_t sum = 0;
     LD_FOR_VERTICES(v, n) {
         const uint64_t s = aoff[v];
-        const uint32_t c = (uint32_t)(aoff[v + 1] - s);
-        uint32_t a[32];
-        uint32_t k = 0;
-        for (uint32_t i = 0; i < c && i < 32; i++) {   // insertion sort, self-loops dropped
-            const uint32_t x = adj[s + i];
-            if (x == (uint32_t)v) continue;
-            uint32_t j = k++;
-            while (j > 0 && a[j - 1] > x) {
-                a[j] = a[j - 1];
-                j--;
-            }
-            a[j] = x;
-        }
+        const uint32_t c = inc[v];
         uint32_t d = 0;
-        for (uint32_t i = 0; i < k; i++)
-            if (i == 0 || a[i] != a[i - 1]) adj[s + d++] = a[i];
-        deg[v] = d;
+        if (c <= kLdReg) {   // registers: pad, sort (network), unique
+            uint32_t r[8];
+#pragma unroll
+            for (uint32_t i = 0; i < 8; i++) {
+                const uint32_t x = i < c ? adj[s + i] : kLdNone;
+                r[i] = x == (uint32_t)v ? kLdNone : x;
+            }
+            ld_sort8(r);
+#pragma unroll
+            for (uint32_t i = 0; i < 8; i++)
+                if (r[i] != kLdNone && (i == 0 || r[i] != r[i - 1])) adj[s + d++] = r[i];
+        } else {
+            uint32_t a[32];
+            uint32_t k = 0;
+            for (uint32_t i = 0; i < c && i < 32; i++) {   // insertion sort, self-loops dropped
+                const uint32_t x = adj[s + i];
+                if (x == (uint32_t)v) continue;
+                uint32_t j = k++;
+                while (j > 0 && a[j - 1] > x) {
+                    a[j] = a[j - 1];
+                    j--;
+                }
+                a[j] = x;
+            }
+            for (uint32_t i = 0; i < k; i++)
+                if (i == 0 || a[i] != a[i - 1]) adj[s + d++] = a[i];
+        }
+        pk[v] = ld_pack(d, s);
         sum += d;
     }
     sum = ld_block_sum(sum, s_red);
@@ -135,16 +189,15 @@ __global__ void __launch_bounds__(kLdThreads)
 // sorted are sorted into adj (same offsets).
 __global__ void __launch_bounds__(kLdThreads)
     k_ld_clean_rows(const uint64_t *__restrict__ rowptr, const uint32_t *__restrict__ col, uint64_t n,
-                    uint32_t L, bool sort, uint32_t *__restrict__ adj, uint32_t *__restrict__ deg,
+                    uint32_t L, bool sort, uint32_t *__restrict__ adj, uint64_t *__restrict__ pk,
                     uint32_t *__restrict__ flag) {
     LD_FOR_VERTICES(v, n) {
         const uint64_t b = rowptr[v], c = rowptr[v + 1] - b;
         if (c > L) {
             *flag = 1u;
-            deg[v] = 0;
             continue;
         }
-        deg[v] = (uint32_t)c;
+        pk[v] = ld_pack((uint32_t)c, b);
         if (!sort) continue;
         uint32_t a[32];
         for (uint32_t i = 0; i < (uint32_t)c; i++) {
@@ -163,40 +216,41 @@ __global__ void __launch_bounds__(kLdThreads)
 // a3 + a6 + a7: one thread per vertex u.  out[]: 0 = W, 1 = probe work, 2 = max d+,
 // 3 = Sum d-(v) d+(v), 4 = skipped edges, 5 = Sum d+ (arcs passing the rank filter).
 template <bool STATS>
-__global__ void __launch_bounds__(kLdThreads)
-    k_ld_count(const uint64_t *__restrict__ aoff, const uint32_t *__restrict__ adj,
-               const uint32_t *__restrict__ deg, uint64_t n, unsigned long long *__restrict__ total,
-               unsigned long long *__restrict__ pv, unsigned long long *__restrict__ out,
-               const uint32_t *__restrict__ flag) {
+__global__ void __launch_bounds__(kLdThreads, 8)   // 8 CTAs / SM: occupancy hides the gathers
+    k_ld_count(const uint32_t *__restrict__ adj, const uint64_t *__restrict__ pk, uint64_t n,
+               unsigned long long *__restrict__ total, unsigned long long *__restrict__ pv,
+               unsigned long long *__restrict__ out, const uint32_t *__restrict__ flag) {
     __shared__ uint64_t s_red[kLdThreads / 32];
     if (*flag) return;   // not eligible: nothing is counted, the call is re-run
     uint64_t tri = 0, npsum = 0, W = 0, probe = 0, stage = 0, skipped = 0, maxdp = 0;
     LD_FOR_VERTICES(u, n) {
-        const uint32_t du = deg[u];
-        const uint64_t s = aoff[u];
-        uint32_t pid[32], pdeg[32];
+        const uint64_t pu = pk[u];   // one 8-byte load: d(u) and the row's offset
+        const uint32_t du = ld_pk_deg(pu);
+        const uint64_t s = ld_pk_off(pu);
+        uint32_t pid[32];
+        uint64_t ppk[32];
         uint32_t np = 0;
         for (uint32_t i = 0; i < du; i++) {   // N+(u), ascending by id
             const uint32_t x = adj[s + i];
-            const uint32_t dx = deg[x];
-            if (ld_rank_less(du, (uint32_t)u, dx, x)) {
+            const uint64_t px = pk[x];
+            if (ld_rank_less(du, (uint32_t)u, ld_pk_deg(px), x)) {
                 pid[np] = x;
-                pdeg[np] = dx;
+                ppk[np] = px;
                 np++;
             }
         }
         npsum += np;
         uint64_t tu = 0;
         for (uint32_t j = 0; j < np; j++) {
-            const uint32_t x = pid[j], dx = pdeg[j];
-            const uint64_t sx = aoff[x];
+            const uint32_t x = pid[j], dx = ld_pk_deg(ppk[j]);
+            const uint64_t sx = ld_pk_off(ppk[j]);
             uint32_t i = 0, k = 0;
             while (i < dx && k < np) {   // N(x) merged with N+(u): common w with rank(w) > rank(x)
                 const uint32_t w = adj[sx + i], y = pid[k];
                 if (w < y) i++;
                 else if (y < w) k++;
                 else {
-                    if (ld_rank_less(dx, x, pdeg[k], w)) {
+                    if (ld_rank_less(dx, x, ld_pk_deg(ppk[k]), w)) {
                         tu++;
                         if (pv) {
                             atomicAdd(&pv[x], 1ull);
@@ -211,10 +265,10 @@ __global__ void __launch_bounds__(kLdThreads)
                 uint32_t dpx = 0;
                 for (uint32_t t = 0; t < dx; t++) {
                     const uint32_t w = adj[sx + t];
-                    dpx += ld_rank_less(dx, x, deg[w], w);
+                    dpx += ld_rank_less(dx, x, ld_pk_deg(pk[w]), w);
                 }
                 uint32_t after = 0;
-                for (uint32_t t = 0; t < np; t++) after += ld_rank_less(dx, x, pdeg[t], pid[t]);
+                for (uint32_t t = 0; t < np; t++) after += ld_rank_less(dx, x, ld_pk_deg(ppk[t]), pid[t]);
                 W += np + dpx;
                 probe += min(after, dpx);
                 skipped += (after == 0 || dpx == 0);
@@ -257,26 +311,31 @@ void lowdeg_prepare(Ctx &ctx, LowDeg &ld, uint64_t n, uint64_t M, const uint64_t
     const uint32_t grid = ld_grid(ctx, n);
     ld.n = n;
     ld.flag = flag_dev;
-    ld.deg = ctx.alloc<uint32_t>(n);
+    ld.pk = ctx.alloc<uint64_t>(n);
     if (clean) {
         ld.aoff = rowptr;
         ld.adj = sorted ? col : ctx.alloc<uint32_t>(M);
         k_ld_clean_rows<<<grid, kLdThreads, 0, ctx.stream>>>(rowptr, col, n, L, !sorted,
-                                                            const_cast<uint32_t *>(ld.adj), ld.deg, flag_dev);
+                                                            const_cast<uint32_t *>(ld.adj), ld.pk, flag_dev);
         TC_LAUNCHED(ctx);
         ld.m2_host = M;
         return;
     }
-    // dirty: in-counts, slot counts, offsets, scatter (k_ld_clean runs after the host's check)
-    ld.m2 = ctx.alloc<uint64_t>(1);
-    TC_CUDA(cudaMemsetAsync(ld.m2, 0, sizeof(uint64_t), ctx.stream));
+    // dirty: in-counts (+ each arc's slot), slot counts and row offsets; the scatter and
+    // k_ld_clean run in lowdeg_count
+    ld.m2 = ctx.alloc<uint64_t>(2);
+    TC_CUDA(cudaMemsetAsync(ld.m2, 0, 2 * sizeof(uint64_t), ctx.stream));   // [0] Sum d, [1] next row
     uint32_t *inc = ctx.alloc<uint32_t>(n);
     TC_CUDA(cudaMemsetAsync(inc, 0, n * sizeof(uint32_t), ctx.stream));
-    k_ld_in<<<grid, kLdThreads, 0, ctx.stream>>>(rowptr, col, n, L, inc, flag_dev);
+    ld.slot8 = ctx.alloc<uint8_t>(M);
+    k_ld_in<<<grid, kLdThreads, 0, ctx.stream>>>(rowptr, col, n, L, inc, ld.slot8, flag_dev);
     TC_LAUNCHED(ctx);
-    k_ld_inc<<<grid, kLdThreads, 0, ctx.stream>>>(rowptr, n, L, inc, flag_dev);
+    uint64_t *aoff = ctx.alloc<uint64_t>(n);
+    k_ld_offsets<<<grid, kLdThreads, 0, ctx.stream>>>(rowptr, n, L, inc, aoff,
+                                                     (unsigned long long *)(ld.m2 + 1), flag_dev);
     TC_LAUNCHED(ctx);
     ld.inc = inc;
+    ld.aoff = aoff;
     ld.rowptr = rowptr;
     ld.col = col;
 }
@@ -286,26 +345,24 @@ void lowdeg_count(Ctx &ctx, LowDeg &ld, uint64_t M, Timer *tm, uint64_t *total_d
     const uint64_t n = ld.n;
     const uint32_t grid = ld_grid(ctx, n);
     if (ld.inc) {   // dirty input: finish a1 + a2
-        uint64_t *aoff = ctx.alloc<uint64_t>(n + 1);
-        scan_exclusive(ctx, ld.inc, aoff, n);
         uint32_t *adj = ctx.alloc<uint32_t>(2 * M);
-        k_ld_scatter<<<grid, kLdThreads, 0, ctx.stream>>>(ld.rowptr, ld.col, n, aoff, ld.inc, adj, ld.flag);
+        k_ld_scatter<<<grid, kLdThreads, 0, ctx.stream>>>(ld.rowptr, ld.col, n, ld.aoff, ld.inc, ld.slot8,
+                                                         adj, ld.flag);
         TC_LAUNCHED(ctx);
-        k_ld_clean<<<grid, kLdThreads, 0, ctx.stream>>>(aoff, n, adj, ld.deg,
+        k_ld_clean<<<grid, kLdThreads, 0, ctx.stream>>>(ld.aoff, ld.inc, n, adj, ld.pk,
                                                        (unsigned long long *)ld.m2, ld.flag);
         TC_LAUNCHED(ctx);
-        ld.aoff = aoff;
         ld.adj = adj;
     }
     phase_end(tm, kClean);
     phase_begin(tm, kIntersect);
     if (stats)
         k_ld_count<true><<<grid, kLdThreads, 0, ctx.stream>>>(
-            ld.aoff, ld.adj, ld.deg, n, (unsigned long long *)total_dev, (unsigned long long *)pv_dev,
+            ld.adj, ld.pk, n, (unsigned long long *)total_dev, (unsigned long long *)pv_dev,
             (unsigned long long *)out_dev, ld.flag);
     else
         k_ld_count<false><<<grid, kLdThreads, 0, ctx.stream>>>(
-            ld.aoff, ld.adj, ld.deg, n, (unsigned long long *)total_dev, (unsigned long long *)pv_dev,
+            ld.adj, ld.pk, n, (unsigned long long *)total_dev, (unsigned long long *)pv_dev,
             (unsigned long long *)out_dev, ld.flag);
     TC_LAUNCHED(ctx);
     phase_end(tm, kIntersect);

@@ -609,7 +609,9 @@ struct LowDeg {
     uint64_t n = 0;
     const uint64_t *rowptr = nullptr, *aoff = nullptr;
     const uint32_t *col = nullptr, *adj = nullptr;
-    uint32_t *inc = nullptr, *deg = nullptr;
+    uint32_t *inc = nullptr;
+    uint64_t *pk = nullptr;           // d(v) << 40 | offset of v's row in adj
+    uint8_t *slot8 = nullptr;         // dirty input: each arc's slot in its target's row
     const uint32_t *flag = nullptr;   // device: set when some vertex has more than L incidences
     uint64_t *m2 = nullptr;     // device: Sum d(v) (dirty input)
     uint64_t m2_host = 0;       // clean input: M

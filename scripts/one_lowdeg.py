@@ -5,6 +5,8 @@ import numpy as np, torch
 import graphgen as G
 import oracle as O
 import paper_1804_06926_b200 as tc
+if os.environ.get("TC_LIB"):
+    tc._LIB_PATH = os.environ["TC_LIB"]
 g = G.road_mesh()
 rp = torch.from_numpy(g.rowptr.view(np.int64)).cuda()
 cl = torch.from_numpy(g.col.view(np.int32)).cuda()

@@ -7,6 +7,8 @@ import numpy as np, torch
 import graphgen as G
 import oracle as O
 import paper_1804_06926_b200 as tc
+if os.environ.get("TC_LIB"):
+    tc._LIB_PATH = os.environ["TC_LIB"]
 
 
 def timed(rp, cl, **kw):
@@ -37,7 +39,7 @@ for w in which:
                               ("clean lowdeg", (rpc, clc), {"clean": True, "sorted_rows": True}),
                               ("clean pipeline", (rpc, clc), {"clean": True, "sorted_rows": True, "lowdeg_max": 0})]:
         T, ms, st = timed(a, b, **kw)
-        print(f"{w} {label}: T={T} m={st['m_undirected']} call {ms:.3f} ms (stats call: total "
+        print(f"{os.environ.get('TC_LIB', '')} {w} {label}: T={T} m={st['m_undirected']} call {ms:.3f} ms (stats call: total "
               f"{st['ms_total']:.3f} clean {st['ms_clean']:.3f} orient {st['ms_orient']:.3f} bin "
               f"{st['ms_bin']:.3f} ix {st['ms_intersect']:.3f}) launches {st['kernel_launches']} "
               f"edges/s {st['m_undirected'] / ms * 1e3:.3e}", flush=True)
