@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-next", action="store_true", help="skip the NEXT-row measurements")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the road mesh / Chung-Lu / clique-union rows (other_configs)")
     ap.add_argument("--replicated-a1", action="store_true",
                     help="N > 1: every rank runs a1-a5 on the whole graph, tc_count_shard (round 1)")
     ap.add_argument("--sharded-a1-only", action="store_true",
@@ -303,16 +305,51 @@ def next_rows_23(tc, torch, np, graphgen, rp, cl, flush, stream, m, T, count_ms)
     return rows
 
 
+def other_configs(tc, torch, np, graphgen, dev, flush, stream):
+    """BASELINE configs[2] and [3] beside the headline (configs[1]): each graph's raw arcs
+    resident on the device, one tc_count_ex per call (median of 5, L2 flushed), through the
+    default path (the road mesh takes the bounded-degree path, DESIGN §4 step 8) and, for the
+    road mesh, the general pipeline (lowdeg_max = 0) and the clean sorted CSR; plus the
+    clique union (co-author-like).  Counts agree across paths (asserted); the parity tests hold
+    them against the oracle."""
+    rows = {}
+    for name, make in (("road mesh (configs[3])", graphgen.road_mesh),
+                       ("Chung-Lu LiveJournal-like (configs[2])", graphgen.chung_lu),
+                       ("clique union (co-author-like)", graphgen.clique_union)):
+        g = make()
+        rp = torch.from_numpy(g.rowptr.view(np.int64)).to(dev)
+        cl = torch.from_numpy(g.col.view(np.int32)).to(dev)
+        ms, (T, st) = _timed(torch, flush, stream, lambda: tc.count_ex(rp, cl, with_stats=True))
+        m = st["m_undirected"]
+        row = {"workload": g.name, "n": g.n, "raw_arcs": g.arcs, "m": m, "T": T, "ms_per_call": ms,
+               "edges_per_s": m / (ms * 1e-3), "launches": st["kernel_launches"]}
+        if "road" in name:
+            pms, (Tp, sp) = _timed(torch, flush, stream,
+                                   lambda: tc.count_ex(rp, cl, lowdeg_max=0, with_stats=True))
+            assert Tp == T
+            row["pipeline (lowdeg_max=0)"] = {"ms_per_call": pms, "launches": sp["kernel_launches"]}
+            crp, ccl = clean_csr_of(tc, torch, rp, cl)
+            cms, Tc = _timed(torch, flush, stream, lambda: tc.count_ex(crp, ccl, clean=True, sorted_rows=True))
+            assert Tc == T
+            row["clean sorted CSR"] = {"ms_per_call": cms, "edges_per_s": m / (cms * 1e-3)}
+            del crp, ccl
+        rows[name] = row
+        del rp, cl
+        torch.cuda.empty_cache()
+    return rows
+
+
 def small_graph_latency(tc, torch, graphgen, dev, reps=50):
     """Launch-bound regime: one synchronous tc_count_ex on Zachary's karate club
     (BASELINE configs[0]) from device pointers, host wall clock per call (median of `reps`),
-    through the one-kernel small-graph path and through the general pipeline."""
+    through the one-kernel small-graph path, the bounded-degree path and the general pipeline."""
     import numpy as np
     g = graphgen.karate()
     rp = torch.from_numpy(g.rowptr.view(np.int64)).to(dev)
     cl = torch.from_numpy(g.col.view(np.int32)).to(dev)
     out = {"workload": "karate (n=34, 78 edges)"}
-    for name, kw in (("one_kernel", {}), ("pipeline", {"tiny_max_n": 0})):
+    for name, kw in (("one_kernel", {}), ("bounded_degree", {"tiny_max_n": 0}),
+                     ("pipeline", {"tiny_max_n": 0, "lowdeg_max": 0})):
         for _ in range(5):
             T, st = tc.count_ex(rp, cl, with_stats=True, **kw)
         us = []
@@ -689,6 +726,8 @@ def main():
             "call": "tc_clustering (device pointers): count with per-vertex t(v) + local c(v) for all n"}}
         line["survey_clean_input"] = clean_input_ms(tc, torch, rp, cl, flush, stream, T_total)
         line["small_graph"] = small_graph_latency(tc, torch, graphgen, dev)
+        if not args.no_configs:
+            line["other_configs"] = other_configs(tc, torch, np, graphgen, dev, flush, stream)
         line["next_rows"].update(next_rows_23(tc, torch, np, graphgen, rp, cl, flush, stream, m,
                                               T_total, ms))
     if world == 1 and not args.no_projection:
