@@ -41,8 +41,9 @@ __device__ __forceinline__ void warp_append(bool take, uint64_t *counter, Item *
 
 // For every CSR edge e = (u -> x) (row u, rows ascending), with p = pidx[e] its slot
 // in x's in-list:
-//   - x owns the edge (suf = |N+(u) after x| <= d+(x)): ulo[p] = e+1 (probe range
-//     [e+1, off[u+1]), the end re-read by the kernel from u = in_src[p]),
+//   - x owns the edge (suf = |N+(u) after x| <= d+(x), and suf <= kSufMax): ulo[p] = suf,
+//     16 bits (probe range [off[u+1] - suf, off[u+1]), the end re-read by the kernel from
+//     u = in_src[p]),
 //     an in-part entry of x;
 //   - u owns it (suf > d+(x), ~4% of R-MAT edges): bit e of `obits` is set, an
 //     out-part entry of u (probe range N+(x); compacted in CSR order by k_ocompact,
@@ -58,7 +59,7 @@ __device__ __forceinline__ void warp_append(bool take, uint64_t *counter, Item *
 #define TC_EDGES_BATCH 4
 #endif
 __global__ void __launch_bounds__(kTileThreads, TC_EDGES_MINBLOCKS)
-    k_edges(HashParams hp, const uint64_t *__restrict__ m_dev, uint32_t *__restrict__ ulo,
+    k_edges(HashParams hp, const uint64_t *__restrict__ m_dev, uint16_t *__restrict__ ulo,
             uint32_t *__restrict__ obits, uint32_t *__restrict__ tcount,
             uint2 *__restrict__ b_short, uint2 *__restrict__ b_merge, uint2 *__restrict__ b_search,
             uint64_t *__restrict__ counts, const uint2 *__restrict__ tb) {
@@ -132,10 +133,10 @@ __global__ void __launch_bounds__(kTileThreads, TC_EDGES_MINBLOCKS)
                 uint32_t ri = 0;
                 if (bin == TC_VARIANT_HASH) {
                     hashed += hp.world <= 1;
-                    if (suf <= dv) ri = (uint32_t)(e + 1);
+                    if (suf <= dv && suf <= kSufMax) ri = suf;
                     else outp = true;
                 }
-                ulo[ps[j]] = ri;
+                ulo[ps[j]] = (uint16_t)ri;
             }
             const uint32_t ob = __ballot_sync(0xffffffffu, outp);
             if ((threadIdx.x & 31) == 0) {
@@ -245,7 +246,7 @@ __global__ void k_owners(const uint32_t *__restrict__ dplus, const uint32_t *__r
                          const uint64_t *__restrict__ pre_len,
                          const uint2 *__restrict__ orange, const uint64_t *__restrict__ owner_prefix,
                          int rank, int world,
-                         const uint32_t *__restrict__ ulo, uint32_t *__restrict__ in_cnt,
+                         const uint16_t *__restrict__ ulo, uint32_t *__restrict__ in_cnt,
                          uint64_t *__restrict__ ooff, const uint64_t *__restrict__ off,
                          const uint64_t *__restrict__ m_dev, const uint32_t *__restrict__ obits,
                          const uint16_t *__restrict__ wpre, const uint64_t *__restrict__ toff,
@@ -344,14 +345,14 @@ __global__ void k_owners(const uint32_t *__restrict__ dplus, const uint32_t *__r
 // HASH work (ulo[p] != 0), else 0 / 0 -- prefix-scanned so every owner's sums are two
 // lookups (a thread per owner would walk a hub's 10^5-entry in-list alone).
 __global__ void k_entry_vals(const uint64_t *__restrict__ off, const uint32_t *__restrict__ in_src,
-                             const uint32_t *__restrict__ ulo, const uint64_t *__restrict__ m_dev,
+                             const uint16_t *__restrict__ ulo, const uint64_t *__restrict__ m_dev,
                              uint32_t *__restrict__ cnt, uint32_t *__restrict__ len) {
     const uint64_t m = *m_dev;
     for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
          p += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t lo = ulo[p];
-        cnt[p] = lo ? 1u : 0u;
-        len[p] = lo ? (uint32_t)(off[in_src[p] + 1] - lo) : 0u;
+        const uint32_t suf = ulo[p];   // the probe length itself
+        cnt[p] = suf ? 1u : 0u;
+        len[p] = suf;
     }
 }
 
@@ -505,7 +506,7 @@ void bin_edges(Ctx &ctx, const Oriented &g, const BinParams &p, Bins &bins) {
 
     // HASH: in-part ranges (in-list order), out-part entries (compacted, CSR order),
     // statistics, owners, tasks
-    uint32_t *ulo = ctx.alloc<uint32_t>(cap);
+    uint16_t *ulo = ctx.alloc<uint16_t>(cap);
     uint32_t *obits = ctx.alloc<uint32_t>((uint64_t)tiles * kTileWords + 1);
     uint16_t *wpre = ctx.alloc<uint16_t>((uint64_t)tiles * kTileWords + 1);
     uint2 *orange = ctx.alloc<uint2>(cap);

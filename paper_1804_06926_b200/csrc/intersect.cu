@@ -679,9 +679,12 @@ __device__ __forceinline__ void hash_desc(const HashParams &hp, uint64_t inb, ui
                                           uint32_t &hi, uint32_t &y) {
     lo = hi = y = 0;
     if (j < indeg) {
-        lo = hp.ulo[inb + j];
+        const uint32_t suf = hp.ulo[inb + j];   // probe length (0: not this owner's entry)
         uint32_t u = hp.in_src[inb + j];
-        if (lo) hi = (uint32_t)hp.off[u + 1];
+        if (suf) {
+            hi = (uint32_t)hp.off[u + 1];
+            lo = hi - suf;
+        }
         y = CM == kCmEdge ? lo - 1 : (CM == kCmTop ? 0u : u);
     } else if (j - indeg < ocnt) {
         uint2 r = hp.orange[ob + (j - indeg)];

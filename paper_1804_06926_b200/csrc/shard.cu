@@ -175,7 +175,7 @@ __device__ __forceinline__ int slice_kind(const SliceParams &sp, uint32_t u, uin
     if (bin == TC_VARIANT_SHORT) return kShort;
     if (bin == TC_VARIANT_SEARCH) return kSearch;
     if (sp.core && u >= sp.core_lo) return kCoreEdge;
-    return suf <= dv ? kHashIn : kHashOut;
+    return suf <= dv && suf <= kSufMax ? kHashIn : kHashOut;
 }
 
 // mode 0 (P4): per owner, HASH probe entries (cnt) and probe lengths (len), atomics.
@@ -361,12 +361,12 @@ __global__ void k_ent_classes(const uint32_t *__restrict__ key, uint64_t k, int 
     if (c < 4) tot[c] = s_at[c + 1] - s_at[c];
 }
 
-// Sorted position i (entry perm[i]): i < k_in -> in-list slot i: in_src = u, ulo = e + 1
-// (probe [e + 1, off[u + 1])); else out-part slot i - k_in: orange = N+(x), ovid = x.
+// Sorted position i (entry perm[i]): i < k_in -> in-list slot i: in_src = u, ulo = the probe
+// length off[u + 1] - e - 1 (probe [e + 1, off[u + 1])); else out-part slot i - k_in: orange = N+(x), ovid = x.
 // ... and the SHORT / SEARCH edges into their bins (whose counts come from tot).
 __global__ void k_ent_place(const uint32_t *__restrict__ ent, const uint32_t *__restrict__ perm, uint64_t k,
                             const unsigned long long *__restrict__ tot, const uint64_t *__restrict__ off,
-                            uint32_t *__restrict__ in_src, uint32_t *__restrict__ ulo,
+                            uint32_t *__restrict__ in_src, uint16_t *__restrict__ ulo,
                             uint2 *__restrict__ orange, uint32_t *__restrict__ ovid,
                             uint2 *__restrict__ b_short, uint2 *__restrict__ b_search,
                             uint64_t *__restrict__ counts) {
@@ -381,7 +381,7 @@ __global__ void k_ent_place(const uint32_t *__restrict__ ent, const uint32_t *__
         const uint32_t y = ent[3 * e + 1], ef = ent[3 * e + 2];
         if (i < k_in) {
             in_src[i] = y;
-            ulo[i] = ef + 1;
+            ulo[i] = (uint16_t)(off[y + 1] - ef - 1);
         } else if (i < k_o) {
             orange[i - k_in] = make_uint2((uint32_t)off[y], (uint32_t)off[y + 1]);
             ovid[i - k_in] = y;
@@ -706,7 +706,8 @@ tc_status tc_shard_count(uint64_t n, uint64_t m, const uint64_t *off_plus, const
                                                                        bins.owners_warp, bins.owners_cta,
                                                                        bins.owners_bitmap, bins.count);
         TC_LAUNCHED(ctx);
-        uint32_t *in_src = ctx.alloc<uint32_t>(k), *ulo = ctx.alloc<uint32_t>(k), *ovid = ctx.alloc<uint32_t>(k);
+        uint32_t *in_src = ctx.alloc<uint32_t>(k), *ovid = ctx.alloc<uint32_t>(k);
+        uint16_t *ulo = ctx.alloc<uint16_t>(k);
         uint2 *orange = ctx.alloc<uint2>(k);
         // per-edge bins of this rank's rows (routed to itself by tc_shard_route)
         const bool want_short = o.short_max > 0, want_search = o.skew_ratio > 0;

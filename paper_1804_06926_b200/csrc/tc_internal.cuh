@@ -479,8 +479,11 @@ struct HashParams {
     const uint32_t *pidx = nullptr;    // CSR edge e -> its in-list slot
     const uint32_t *in_cnt = nullptr;  // x: entries of its in-list its tasks take (0 = none: no
                                        // in-part entry of x is this rank's HASH work)
-    const uint32_t *ulo = nullptr;     // in-edge p = (u,x): e+1 (probe range [e+1, off[u+1]) of
-                                       // col+), 0 if not this rank's in-part HASH work
+    const uint16_t *ulo = nullptr;     // in-edge p = (u,x) at CSR position e: its probe length
+                                       // suf = off[u+1] - e - 1 (range [off[u+1] - suf, off[u+1])
+                                       // of col+), 0 if not this rank's in-part HASH work.
+                                       // 16 bits (round 2): the in-slot-indexed scatter of a5
+                                       // touches half the bytes; in-part needs suf <= kSufMax
     const uint64_t *ooff = nullptr;    // compacted out-part entries of each owner:
     const uint2 *orange = nullptr;     //   probe ranges [lo, hi) of col+
     const uint32_t *ovid = nullptr;    //   the edge's target (per-vertex credit), or its CSR
@@ -513,6 +516,9 @@ __device__ __forceinline__ int split_rank(uint64_t pre, uint64_t total, int worl
 }
 // Variant of oriented edge (u,v): -1 = cannot close a triangle (suf = |N+(u) after
 // v| = 0, or d+(v) = 0); else the forced variant, or the AUTO policy.
+// An in-part HASH entry stores its probe length in 16 bits; a longer suffix (possible only when
+// d+ is unbounded, TC_ID_ORDER, or m >= 2^31) makes the edge an out-part entry of u instead.
+constexpr uint32_t kSufMax = 0xffffu;
 __device__ __forceinline__ int edge_bin(const HashParams &hp, uint32_t du, uint32_t dv, uint32_t suf) {
     if (suf == 0 || dv == 0) return -1;
     if (hp.force >= 0) return hp.force;

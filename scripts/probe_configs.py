@@ -4,6 +4,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import graphgen as G
 import paper_1804_06926_b200 as tc
+if os.environ.get("TC_LIB"):
+    tc._LIB_PATH = os.environ["TC_LIB"]
 which = sys.argv[1:] or ["s22", "s24", "chung_lu", "road", "clique"]
 for w in which:
     t = time.time()
