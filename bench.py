@@ -386,7 +386,12 @@ def multi_gpu_projection(tc, torch, graphgen, np, rp, cl, one_gpu_ms, peak_gbs):
         out = {}
         for w in worlds:
             shard.emulate(rp_, cl_, w)   # warm
-            total, _, rep = shard.emulate(rp_, cl_, w, timed=True)
+            # best of 3 timed emulations: one emulated world holds every rank's buffers on this
+            # GPU, and a run where the caching allocator has to map fresh memory mid-phase
+            # (measured: a rank's count phase 34-38 ms instead of 7, a whole step 141 ms instead
+            # of 18) says nothing about the ranks' kernels
+            total, _, rep = min((shard.emulate(rp_, cl_, w, timed=True) for _ in range(3)),
+                                key=lambda x: x[2]["step_ms_overlapped"])
             out[f"world{w}"] = {
                 "T": total, "projected_step_ms": rep["step_ms_overlapped"],
                 "speedup_vs_one_gpu": base_ms / rep["step_ms_overlapped"],
@@ -397,8 +402,8 @@ def multi_gpu_projection(tc, torch, graphgen, np, rp, cl, one_gpu_ms, peak_gbs):
         return out
 
     _, st = tc.count_ex(rp, cl, with_stats=True)
-    res = {"method": "one-GPU emulation (shard.emulate): each rank's phases timed in turn with CUDA "
-                     "events; collectives charged at 770 GB/s (all-gather / all-to-all) and 725 GB/s "
+    res = {"method": "one-GPU emulation (shard.emulate, best of 3 after a warm-up): each rank's phases "
+                     "timed in turn with CUDA events; collectives charged at 770 GB/s (all-gather / all-to-all) and 725 GB/s "
                      "(all-reduce); the col+ all-gather overlapped with binning as run_rank does.  "
                      "NCCL was not run (one GPU per box this round)",
            "bench_workload": one(rp, cl, (2, 4, 8), one_gpu_ms, st["bytes_hash"] + st["bytes_core"])}
@@ -519,11 +524,14 @@ def main():
     # round have one GPU and NCCL refuses two ranks on one device; the numbers are then
     # meaningless, the point is exercising the N > 1 code path end to end
     shared = os.environ.get("TC_BENCH_SHARED_GPU") == "1"
+    # TC_BENCH_FORCE_DIST=1 (tests only): a one-rank job through the N > 1 path (process group,
+    # NCCL collectives of dist.Comm on one GPU) -- the NCCL code path exercised on a 1-GPU box
+    multi = world > 1 or os.environ.get("TC_BENCH_FORCE_DIST") == "1"
     gpu = 0 if shared else local
     torch.cuda.set_device(gpu)
     dev = torch.device("cuda", gpu)
     dist = None
-    if world > 1:
+    if multi:
         import torch.distributed as dist
         if shared:
             dist.init_process_group("gloo")
@@ -534,9 +542,9 @@ def main():
     cl = torch.from_numpy(g.col.view(np.int32)).to(dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     partial = torch.zeros(1, dtype=torch.int64, device=dev)
-    mode = "single" if world == 1 else ("replicated" if args.replicated_a1 else
+    mode = "single" if not multi else ("replicated" if args.replicated_a1 else
                                         ("sharded-a1" if args.sharded_a1_only else "sharded"))
-    comm = Comm() if world > 1 else None
+    comm = Comm() if multi else None
     base_st = None
     if mode == "sharded":
         # the graph's byte model and sizes (B_a6, m, W: properties of the whole graph, the same
@@ -544,7 +552,7 @@ def main():
         base_st = tc.count_ex(rp, cl, with_stats=True)[1]
 
     def step(with_stats=False):
-        if world == 1:
+        if not multi:
             return tc.count_ex(rp, cl, with_stats=with_stats)
         if mode == "sharded":   # a1-a5 split over the ranks too (shard.py run_rank)
             times = {} if with_stats else None
@@ -623,7 +631,7 @@ def main():
         cl_h = torch.from_numpy(g.col.view(np.int32)).pin_memory()
 
         def e2e_step():
-            if world == 1:
+            if not multi:
                 return tc.count_ex(rp_h, cl_h, with_stats=True)[0]
             d_rp = rp_h.to(dev, non_blocking=True)
             d_cl = cl_h.to(dev, non_blocking=True)
@@ -649,7 +657,7 @@ def main():
         in_bytes = g.rowptr.nbytes + g.col.nbytes
         e2e = {"value": m / e2e_s, "unit": "edges/s", "ms_per_step": 1e3 * e2e_s,
                "h2d_bytes_per_step": in_bytes * world, "d2h_bytes_per_step": 8 * world,
-               "note": ("tc_count_ex with TC_HOST_PTRS from pinned host memory" if world == 1 else
+               "note": ("tc_count_ex with TC_HOST_PTRS from pinned host memory" if not multi else
                         "count_distributed[_sharded[_a1]]: per rank H2D of the raw CSR (non_blocking "
                         "from pinned), the same path as the step, .item()") +
                        "; host wall clock per step, max over ranks"}
@@ -680,7 +688,7 @@ def main():
         b_stage = 4 * (m + st["work_stage"]) + 16 * m
         roof["survey_B_stage"] = {"bytes": b_stage, "model": "4(m + sum d-(v) d+(v)) + 16m (SURVEY.md 8(d))",
                                   "frac": b_stage / (ix_ms * 1e-3) / 1e9 / peak}
-    if world == 1 and not args.no_ncu:
+    if not multi and not args.no_ncu:
         tr = ncu_traffic(args)
         roof["ncu"] = tr
         if "dram_bytes" in tr:
@@ -720,7 +728,7 @@ def main():
         "e2e": e2e,
         "clocks": clocks,
     }
-    if world == 1 and not args.no_next:
+    if not multi and not args.no_next:
         # NEXT-1: clustering coefficients + transitivity on the same workload
         # through tc_clustering (count with t(v), then the c(v) kernel); median of 5 calls
         cms, (_, summ) = _timed(torch, flush, stream, lambda: tc.clustering(rp, cl))
@@ -736,9 +744,9 @@ def main():
             line["other_configs"] = other_configs(tc, torch, np, graphgen, dev, flush, stream)
         line["next_rows"].update(next_rows_23(tc, torch, np, graphgen, rp, cl, flush, stream, m,
                                               T_total, ms))
-    if world == 1 and not args.no_projection:
+    if not multi and not args.no_projection:
         line["multi_gpu_projection"] = multi_gpu_projection(tc, torch, graphgen, np, rp, cl, ms, peak)
-    if world == 1 and not args.no_cpu_baseline:
+    if not multi and not args.no_cpu_baseline:
         cb = cpu_baseline(g, m)
         assert cb.pop("T") == T_total, "oracle and CUDA path disagree"
         line["cpu_baseline"] = cb

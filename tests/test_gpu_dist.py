@@ -73,3 +73,40 @@ def test_count_distributed_world2_real_shards(name):
     for rank, T1, T2, pv in res:
         assert T1 == T and T2 == T, rank
         assert (pv.astype(np.uint64) == t).all(), rank
+
+
+def _nccl_worker(port, name, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    try:
+        from paper_1804_06926_b200.dist import (count_distributed, count_distributed_sharded,
+                                                count_distributed_sharded_a1)
+        g = _graph(name)
+        dev = torch.device("cuda:0")
+        rp = torch.from_numpy(g.rowptr.view(np.int64)).to(dev)
+        cl = torch.from_numpy(g.col.view(np.int32)).to(dev)
+        out = [count_distributed(rp, cl), count_distributed_sharded_a1(rp, cl),
+               count_distributed_sharded(rp, cl)]
+        T, pv = count_distributed_sharded(rp, cl, per_vertex=True)
+        q.put((out + [T], pv.cpu().numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["rmat15", "clique"])
+def test_count_distributed_nccl_world1(name):
+    """The three distributed drivers over a REAL NCCL group (one rank on the one GPU): the NCCL
+    collectives of dist.Comm run on CUDA tensors (no host staging)."""
+    import oracle as O
+    g = _graph(name)
+    T, t = O.count(g.n, g.rowptr, g.col, per_vertex=True)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(_free_port(), name, q))
+    p.start()
+    got, pv = q.get(timeout=300)
+    p.join(timeout=60)
+    assert p.exitcode == 0
+    assert got == [T] * 4
+    assert (pv.astype(np.uint64) == t).all()
