@@ -29,6 +29,15 @@
 namespace tc {
 
 constexpr uint32_t kLdThreads = 256;
+// TC_BOUNDS_CHECK=1 (scripts/build_variant.py; the pool's compute-sanitizer is closed): every
+// index into the rows, the slot bytes and the per-thread lists is asserted (trap on violation)
+#ifndef TC_BOUNDS_CHECK
+#define TC_BOUNDS_CHECK 0
+#endif
+#define LD_CHECK(c)                          \
+    do {                                     \
+        if (TC_BOUNDS_CHECK && !(c)) __trap(); \
+    } while (0)
 
 __device__ __forceinline__ bool ld_rank_less(uint32_t du, uint32_t u, uint32_t dv, uint32_t v) {
     return du < dv || (du == dv && u < v);
@@ -124,7 +133,8 @@ __global__ void __launch_bounds__(kLdThreads)
 __global__ void __launch_bounds__(kLdThreads)
     k_ld_scatter(const uint64_t *__restrict__ rowptr, const uint32_t *__restrict__ col, uint64_t n,
                  const uint64_t *__restrict__ aoff, const uint32_t *__restrict__ inc,
-                 const uint8_t *__restrict__ slot8, uint32_t *__restrict__ adj, const uint32_t *__restrict__ flag) {
+                 const uint8_t *__restrict__ slot8, uint32_t *__restrict__ adj, uint64_t cap,
+                 const uint32_t *__restrict__ flag) {
     if (*flag) return;   // not eligible: the call is re-run on the general pipeline
     LD_FOR_VERTICES(u, n) {
         const uint64_t b = rowptr[u], e = rowptr[u + 1];
@@ -132,8 +142,12 @@ __global__ void __launch_bounds__(kLdThreads)
         const uint64_t s = aoff[u] + (inc[u] - (uint32_t)(e - b));
         for (uint64_t k = b; k < e; k++) {
             const uint32_t v = col[k];
+            LD_CHECK(v < n && s + (k - b) < cap && (k - b) < inc[u]);
             adj[s + (k - b)] = v;
-            if (v != (uint32_t)u) adj[aoff[v] + slot8[k]] = (uint32_t)u;
+            if (v != (uint32_t)u) {
+                LD_CHECK(slot8[k] < inc[v] && aoff[v] + slot8[k] < cap);
+                adj[aoff[v] + slot8[k]] = (uint32_t)u;
+            }
         }
     }
 }
@@ -150,6 +164,7 @@ __global__ void __launch_bounds__(kLdThreads)
     LD_FOR_VERTICES(v, n) {
         const uint64_t s = aoff[v];
         const uint32_t c = inc[v];
+        LD_CHECK(c <= kLowDegMax);
         uint32_t d = 0;
         if (c <= kLdReg) {   // registers: pad, sort (network), unique
             uint32_t r[8];
@@ -217,7 +232,7 @@ __global__ void __launch_bounds__(kLdThreads)
 // 3 = Sum d-(v) d+(v), 4 = skipped edges, 5 = Sum d+ (arcs passing the rank filter).
 template <bool STATS>
 __global__ void __launch_bounds__(kLdThreads, 8)   // 8 CTAs / SM: occupancy hides the gathers
-    k_ld_count(const uint32_t *__restrict__ adj, const uint64_t *__restrict__ pk, uint64_t n,
+    k_ld_count(const uint32_t *__restrict__ adj, uint64_t cap, const uint64_t *__restrict__ pk, uint64_t n,
                unsigned long long *__restrict__ total, unsigned long long *__restrict__ pv,
                unsigned long long *__restrict__ out, const uint32_t *__restrict__ flag) {
     __shared__ uint64_t s_red[kLdThreads / 32];
@@ -230,8 +245,10 @@ __global__ void __launch_bounds__(kLdThreads, 8)   // 8 CTAs / SM: occupancy hid
         uint32_t pid[32];
         uint64_t ppk[32];
         uint32_t np = 0;
+        LD_CHECK(du <= kLowDegMax && s + du <= cap);
         for (uint32_t i = 0; i < du; i++) {   // N+(u), ascending by id
             const uint32_t x = adj[s + i];
+            LD_CHECK(x < n && (i == 0 || adj[s + i - 1] < x));
             const uint64_t px = pk[x];
             if (ld_rank_less(du, (uint32_t)u, ld_pk_deg(px), x)) {
                 pid[np] = x;
@@ -244,6 +261,7 @@ __global__ void __launch_bounds__(kLdThreads, 8)   // 8 CTAs / SM: occupancy hid
         for (uint32_t j = 0; j < np; j++) {
             const uint32_t x = pid[j], dx = ld_pk_deg(ppk[j]);
             const uint64_t sx = ld_pk_off(ppk[j]);
+            LD_CHECK(dx <= kLowDegMax && sx + dx <= cap);
             uint32_t i = 0, k = 0;
             while (i < dx && k < np) {   // N(x) merged with N+(u): common w with rank(w) > rank(x)
                 const uint32_t w = adj[sx + i], y = pid[k];
@@ -319,6 +337,7 @@ void lowdeg_prepare(Ctx &ctx, LowDeg &ld, uint64_t n, uint64_t M, const uint64_t
                                                             const_cast<uint32_t *>(ld.adj), ld.pk, flag_dev);
         TC_LAUNCHED(ctx);
         ld.m2_host = M;
+        ld.adj_cap = M;
         return;
     }
     // dirty: in-counts (+ each arc's slot), slot counts and row offsets; the scatter and
@@ -347,22 +366,23 @@ void lowdeg_count(Ctx &ctx, LowDeg &ld, uint64_t M, Timer *tm, uint64_t *total_d
     if (ld.inc) {   // dirty input: finish a1 + a2
         uint32_t *adj = ctx.alloc<uint32_t>(2 * M);
         k_ld_scatter<<<grid, kLdThreads, 0, ctx.stream>>>(ld.rowptr, ld.col, n, ld.aoff, ld.inc, ld.slot8,
-                                                         adj, ld.flag);
+                                                         adj, 2 * M, ld.flag);
         TC_LAUNCHED(ctx);
         k_ld_clean<<<grid, kLdThreads, 0, ctx.stream>>>(ld.aoff, ld.inc, n, adj, ld.pk,
                                                        (unsigned long long *)ld.m2, ld.flag);
         TC_LAUNCHED(ctx);
         ld.adj = adj;
+        ld.adj_cap = 2 * M;
     }
     phase_end(tm, kClean);
     phase_begin(tm, kIntersect);
     if (stats)
         k_ld_count<true><<<grid, kLdThreads, 0, ctx.stream>>>(
-            ld.adj, ld.pk, n, (unsigned long long *)total_dev, (unsigned long long *)pv_dev,
+            ld.adj, ld.adj_cap, ld.pk, n, (unsigned long long *)total_dev, (unsigned long long *)pv_dev,
             (unsigned long long *)out_dev, ld.flag);
     else
         k_ld_count<false><<<grid, kLdThreads, 0, ctx.stream>>>(
-            ld.adj, ld.pk, n, (unsigned long long *)total_dev, (unsigned long long *)pv_dev,
+            ld.adj, ld.adj_cap, ld.pk, n, (unsigned long long *)total_dev, (unsigned long long *)pv_dev,
             (unsigned long long *)out_dev, ld.flag);
     TC_LAUNCHED(ctx);
     phase_end(tm, kIntersect);

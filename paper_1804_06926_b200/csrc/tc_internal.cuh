@@ -621,6 +621,7 @@ struct LowDeg {
     const uint32_t *flag = nullptr;   // device: set when some vertex has more than L incidences
     uint64_t *m2 = nullptr;     // device: Sum d(v) (dirty input)
     uint64_t m2_host = 0;       // clean input: M
+    uint64_t adj_cap = 0;             // entries of adj
 };
 void lowdeg_prepare(Ctx &ctx, LowDeg &ld, uint64_t n, uint64_t M, const uint64_t *rowptr,
                     const uint32_t *col, bool clean, bool sorted, uint32_t L, uint32_t *flag_dev);
